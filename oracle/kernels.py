@@ -1,0 +1,608 @@
+"""Oracle for the three EncFormer CKKS kernels + the GPU half of the complex C2M export.
+
+TEST INFRASTRUCTURE ONLY (see oracle/ckks.py header).
+
+The kernels are written as schedules over an evaluator `ev` so the same code runs
+  * on real ciphertexts (Ev: oracle/ckks.py arithmetic, bit-exact reference for the GPU), and
+  * in count-only mode (CountEv) at the paper's own shapes (n = 16384) to pin the key-switch counts
+    of Table 2.
+Every step cites the passage it follows; the schedule choices where the paper is silent or wrong are
+SURVEY.md §8c C6-C9 / G1-G29 and are restated in DESIGN.md "Readings".
+"""
+from collections import Counter
+
+import numpy as np
+
+from . import ckks as O
+
+
+# ====================================================================================== packing (slot level)
+def mat(x, m):
+    """(mat x)_{r,s} = x_{s m + r}."""
+    return np.asarray(x).reshape(-1, m).T
+
+
+def vec(X):
+    return np.asarray(X).T.reshape(-1)
+
+
+def seg_column_pack(X, m, C, g, n):
+    """Segment-column packing: segment c < C holds column X[:, gC + c] (zero past d_in)."""
+    d = X.shape[1]
+    z = np.zeros(n, dtype=np.complex128)
+    for c in range(C):
+        col = g * C + c
+        if col < d:
+            z[c * m:(c + 1) * m] = X[:, col]
+    return z
+
+
+def seg_column_unpack(z, m, C, d, b):
+    """Inverse for output block b: columns bC .. bC+C-1 (clipped to d)."""
+    cols = [z[c * m:(c + 1) * m] for c in range(C) if b * C + c < d]
+    return np.stack(cols, axis=1) if cols else np.zeros((m, 0))
+
+
+def pi_S(H, d_h):
+    """Score-friendly column order: pi_S(h,u) = uH + h; returns perm with
+    Wpi[:, pi_S(h,u)] = W[:, k(h,u)], k(h,u) = h d_h + u."""
+    perm = np.empty(H * d_h, dtype=np.int64)
+    for h in range(H):
+        for u in range(d_h):
+            perm[u * H + h] = h * d_h + u
+    return perm
+
+
+def apply_col_perm(W, perm):
+    return W[:, perm]
+
+
+def k_min(n_entries, n):
+    """K_min(x) = ceil(N(x) / 2n)."""
+    return -(-int(n_entries) // (2 * int(n)))
+
+
+# ====================================================================================== masks
+def mask_slots(desc, m, n):
+    """Mask descriptor (r0, r1, s0, sstride, scount): ones on rows [r0, r1) of segments
+    s0 + k*sstride (k < scount), zero elsewhere.  Covers H/U of Alg A.2, e_s / m_c /
+    n_u of App. A.3 and the export range masks."""
+    r0, r1, s0, ss, sc = desc
+    z = np.zeros(n)
+    for k in range(sc):
+        s = s0 + k * ss
+        z[s * m + r0: s * m + r1] = 1.0
+    return z
+
+
+def psi_masks(t, m, N_seg, seg0=0, nseg=None):
+    """H and U of Alg A.2 for shift t (already reduced mod m), optionally restricted to
+    segments [seg0, seg0+nseg)."""
+    nseg = N_seg if nseg is None else nseg
+    return (0, m - t, seg0, 1, nseg), (m - t, m, seg0, 1, nseg)
+
+
+# ====================================================================================== evaluators
+class Ev:
+    """Real evaluator over the oracle's CKKS (bit-exact reference)."""
+
+    def __init__(self, P, keys, m=None):
+        self.P, self.keys = P, keys
+        self.ledger = Counter()
+        self.masks = {}          # (desc, level, m) -> Pt   (what the schedule used)
+        self.m = m
+
+    # -- plaintexts
+    def mask(self, desc, L, m=None):
+        m = m or self.m
+        key = (tuple(desc), L, m)
+        if key not in self.masks:
+            z = mask_slots(desc, m, self.P.n)
+            self.masks[key] = O.encode(self.P, z, float(self.P.q[L - 1]), L)
+        return self.masks[key]
+
+    # -- ciphertext ops
+    def rot(self, ct, r):
+        if int(r) % self.P.n:
+            self.ledger["rot"] += 1
+        return O.rotate(self.P, self.keys, ct, r)
+
+    def rot_hoisted(self, ct, rs):
+        self.ledger["rot"] += sum(1 for r in rs if int(r) % self.P.n)
+        self.ledger["modup_hoisted"] += 1
+        return O.rotate_hoisted(self.P, self.keys, ct, rs)
+
+    def conj(self, ct):
+        self.ledger["conj"] += 1
+        return O.conjugate(self.P, self.keys, ct)
+
+    def tensor(self, a, b):
+        self.ledger["ctmul"] += 1
+        return O.tensor(self.P, a, b)
+
+    def relin(self, ct):
+        self.ledger["relin"] += 1
+        return O.relinearize(self.P, self.keys, ct)
+
+    def ptmul(self, ct, pt):
+        self.ledger["ptmul"] += 1
+        return O.ptmul(self.P, ct, pt)
+
+    def add(self, a, b):
+        return O.add(self.P, a, b)
+
+    def sub(self, a, b):
+        return O.sub(self.P, a, b)
+
+    def mul_i(self, ct):
+        return O.mul_i(self.P, ct)
+
+    def rescale(self, ct):
+        self.ledger["rescale"] += 1
+        return O.rescale(self.P, ct)
+
+    def mod_drop(self, ct, L):
+        return O.mod_drop(self.P, ct, L)
+
+    def scale_mul(self, ct, f):
+        """Scale bookkeeping only (the 1/2 of decomplexification, G3): no arithmetic."""
+        return O.Ct(ct.c, ct.scale * f)
+
+    def mac_ptmul(self, cts, pts):
+        """sum_i cts[i] (.) pts[i]  (exact modular sum of ring products; evaluated in the oracle's NTT
+        domain -- the sum of ring products is unique)."""
+        self.ledger["ptmul"] += len(cts)
+        P, N = self.P, self.P.N
+        L = cts[0].L
+        mods = P.q[:L]
+        acc = [np.zeros((L, N), np.uint64) for _ in range(2)]
+        cache = self.__dict__.setdefault("_ntt_cache", {})
+        for ct, pt in zip(cts, pts):
+            if ct.L != L or pt.L != L:
+                raise O.OracleError("LEVEL_MISMATCH")
+            key = id(ct)
+            if key not in cache or cache[key][0] is not ct:
+                cache[key] = (ct, [O.ntt(ct.c[c], mods, N) for c in range(2)])
+            ctn = cache[key][1]
+            ptn = O.ntt(pt.m, mods, N)
+            for c in range(2):
+                acc[c] = O.padd(acc[c], O.pmul_pointwise(ctn[c], ptn, mods, N), mods, N)
+        scale = cts[0].scale * pts[0].scale
+        for ct, pt in zip(cts, pts):
+            if ct.scale * pt.scale != scale:
+                raise O.OracleError("SCALE_MISMATCH")
+        return O.Ct(np.stack([O.intt(a, mods, N) for a in acc]), scale)
+
+    def tensor_sum(self, pairs):
+        """sum_t a_t (x) b_t without relinearisation (lazy sum; exact)."""
+        out = None
+        for a, b in pairs:
+            t = self.tensor(a, b)
+            out = t if out is None else O.add(self.P, out, t)
+        return out
+
+
+class FakeCt:
+    def __init__(self, L, scale=1.0, ncomp=2):
+        self.L, self.scale, self.ncomp = L, scale, ncomp
+
+
+class CountEv:
+    """Count-only evaluator: same schedule, no arithmetic (for the paper's n=16384 count pins)."""
+
+    def __init__(self, n, q_of_level=None, m=None):
+        self.n = n
+        self.ledger = Counter()
+        self.m = m
+
+    def mask(self, desc, L, m=None):
+        return FakeCt(L, 1.0, 1)
+
+    def rot(self, ct, r):
+        if int(r) % self.n:
+            self.ledger["rot"] += 1
+        return FakeCt(ct.L, ct.scale)
+
+    def rot_hoisted(self, ct, rs):
+        self.ledger["rot"] += sum(1 for r in rs if int(r) % self.n)
+        self.ledger["modup_hoisted"] += 1
+        return [FakeCt(ct.L, ct.scale) for _ in rs]
+
+    def conj(self, ct):
+        self.ledger["conj"] += 1
+        return FakeCt(ct.L, ct.scale)
+
+    def tensor(self, a, b):
+        self.ledger["ctmul"] += 1
+        return FakeCt(a.L, 1.0, 3)
+
+    def relin(self, ct):
+        self.ledger["relin"] += 1
+        return FakeCt(ct.L, ct.scale)
+
+    def ptmul(self, ct, pt):
+        self.ledger["ptmul"] += 1
+        return FakeCt(ct.L, ct.scale, ct.ncomp)
+
+    def add(self, a, b):
+        return FakeCt(a.L, a.scale, max(a.ncomp, b.ncomp))
+
+    sub = add
+
+    def mul_i(self, ct):
+        return ct
+
+    def rescale(self, ct):
+        self.ledger["rescale"] += 1
+        return FakeCt(ct.L - 1, ct.scale, ct.ncomp)
+
+    def mod_drop(self, ct, L):
+        return FakeCt(L, ct.scale, ct.ncomp)
+
+    def scale_mul(self, ct, f):
+        return ct
+
+    def mac_ptmul(self, cts, pts):
+        self.ledger["ptmul"] += len(cts)
+        return FakeCt(cts[0].L, 1.0)
+
+    def tensor_sum(self, pairs):
+        for _ in pairs:
+            self.ledger["ctmul"] += 1
+        return FakeCt(pairs[0][0].L, 1.0, 3)
+
+
+# ====================================================================================== shifts (App. A.1)
+def Phi(ev, x, delta, m):
+    """Phi^Delta = rot(x; Delta m)  (Alg A.1)."""
+    return ev.rot(x, delta * m)
+
+
+def Psi_hoisted(ev, x, ts, m, N_seg, seg0=0, nseg=None):
+    """Psi^t for every t in ts from ONE hoisted ModUp of x (Alg A.2):
+       Psi^t(x) = rot(x; t)(.)h_t + rot(x; (t-m) mod n)(.)u_t, then rescale.
+    t = 0 (mod m) is realised as x(.)h_0 then rescale (no rotation), so every bank entry sits at the
+    same level and scale (reading R-PSI0).  Optional segment restriction merges a trailing
+    segment mask (used by the score align step)."""
+    L = x.L
+    tt = [int(t) % m for t in ts]
+    steps = []
+    for t in tt:
+        if t:
+            steps += [t, t - m]
+    rots = ev.rot_hoisted(x, steps) if steps else []
+    out, i = [], 0
+    for t in tt:
+        hd, ud = psi_masks(t, m, N_seg, seg0, nseg)
+        if t == 0:
+            y = ev.ptmul(x, ev.mask(hd, L, m))
+        else:
+            a = ev.ptmul(rots[i], ev.mask(hd, L, m))
+            b = ev.ptmul(rots[i + 1], ev.mask(ud, L, m))
+            y = ev.add(a, b)
+            i += 2
+        out.append(ev.rescale(y))
+    return out
+
+
+# ====================================================================================== projection (§3.2, App. A.2)
+class ProjPlan:
+    """Plan of the shared pt-ct projection Y = X W.
+    C = active segments (default N_seg, G4), N1 | C (G5), N2 = C/N1, G = ceil(d_in/C),
+    U = ceil(G/2) complexified inputs, B_out = ceil(d_out/C)."""
+
+    def __init__(self, n, m, d_in, d_out, C=None, N1=None):
+        self.n, self.m, self.d_in, self.d_out = n, m, d_in, d_out
+        self.N_seg = n // m
+        self.C = C or self.N_seg
+        self.G = -(-d_in // self.C)
+        self.U = -(-self.G // 2)
+        self.B_out = -(-d_out // self.C)
+        if N1 is None:
+            N1 = default_n1(self.C, self.B_out, self.U)
+        assert self.C % N1 == 0
+        self.N1, self.N2 = N1, self.C // N1
+
+
+def default_n1(C, B_out, U):
+    """Power of two dividing C nearest sqrt(B_out*C/U) (minimises key switches)."""
+    import math
+    target = math.sqrt(B_out * C / U)
+    best = 1
+    p = 1
+    while p <= C:
+        if C % p == 0 and abs(math.log2(p) - math.log2(target)) < abs(math.log2(best) - math.log2(target)) - 1e-12:
+            best = p
+        p *= 2
+    return best
+
+
+def proj_inputs(X, plan):
+    """Complexified inputs x~_u = x^(2u) + i x^(2u+1) as slot vectors."""
+    return [seg_column_pack(X, plan.m, plan.C, 2 * u, plan.n) + 1j * seg_column_pack(X, plan.m, plan.C, 2 * u + 1, plan.n)
+            for u in range(plan.U)]
+
+
+def proj_weight_slots(Wbar, plan, b, p, u, q):
+    """w~^(b)_{u,p,q}(c) = Wbar[(2u)C + alpha, bC + beta] - i Wbar[(2u+1)C + alpha, bC + beta],
+    alpha = (c+q) mod C, beta = (c - p N1) mod C; constant over the m rows of segment c; zero for
+    c >= C and outside d_in x d_out."""
+    C, m = plan.C, plan.m
+    d_in, d_out = Wbar.shape
+    z = np.zeros(plan.n, dtype=np.complex128)
+    for c in range(C):
+        a = (c + q) % C
+        be = (c - p * plan.N1) % C
+        col = b * C + be
+        if col >= d_out:
+            continue
+        r0, r1 = (2 * u) * C + a, (2 * u + 1) * C + a
+        w = (Wbar[r0, col] if r0 < d_in else 0.0) - 1j * (Wbar[r1, col] if r1 < d_in else 0.0)
+        z[c * m:(c + 1) * m] = w
+    return z
+
+
+def proj_weight_index(plan, b, p, u, q):
+    """Flat index of plaintext (b,p,u,q) in the [b][p][u][q] weight stream (the ABI layout)."""
+    return ((b * plan.N2 + p) * plan.U + u) * plan.N1 + q
+
+
+def projection(ev, plan, xt, w, decomplexify=True):
+    """C6 (G2/G3):
+      1. bank[u][0] = x~_u ; bank[u][q] = HOISTED rot(x~_u, q m), q = 1..N1-1
+      2. c~_{b,p} = sum_{u,q} bank[u][q] (.) w~_{b,p,u,q}          (exact modular sum)
+      3. acc_b = c~_{b,0} + sum_{p>=1} rot(c~_{b,p}, p N1 m)       (single rotations)
+      4. z_b = acc_b + conj(acc_b), scale x2  (decomplexify AFTER the fold, G2; the 1/2 is bookkeeping, G3)
+      5. y_b = rescale(z_b)
+    w(b, p, u, q) -> plaintext.  Returns the B_out outputs y_b."""
+    m, N1 = plan.m, plan.N1
+    bank = []
+    for u in range(plan.U):
+        rots = ev.rot_hoisted(xt[u], [q * m for q in range(1, N1)]) if N1 > 1 else []
+        bank.append([xt[u]] + list(rots))
+    ys = []
+    for b in range(plan.B_out):
+        acc = None
+        for p in range(plan.N2):
+            cts = [bank[u][q] for u in range(plan.U) for q in range(N1)]
+            pts = [w(b, p, u, q) for u in range(plan.U) for q in range(N1)]
+            c = ev.mac_ptmul(cts, pts)
+            if p:
+                c = ev.rot(c, p * N1 * m)
+            acc = c if acc is None else ev.add(acc, c)
+        if decomplexify:
+            acc = ev.scale_mul(ev.add(acc, ev.conj(acc)), 2.0)
+        ys.append(ev.rescale(acc))
+    return ys
+
+
+# ====================================================================================== score kernel (§3.3.1, App. A.3)
+class ScorePlan:
+    """Score kernel plan.  C_qk used segments per block (multiple of H with
+    C_qk/H a power of two -> routing tree; G8 padding), beta | m, g = m/beta even."""
+
+    def __init__(self, n, m, H, d_h, C_qk=None, beta=None):
+        if m % 2:
+            raise O.OracleError("ODD_SEQ")
+        self.n, self.m, self.H, self.d_h = n, m, H, d_h
+        self.N_seg = n // m
+        if C_qk is None:
+            C_qk = H
+            while C_qk * 2 <= self.N_seg and C_qk < H * d_h:
+                C_qk *= 2
+        self.C = C_qk
+        assert C_qk % H == 0 and C_qk <= self.N_seg, "C_qk must be a multiple of H (phases r_l = 0, G8)"
+        self.B = -(-(H * d_h) // C_qk)
+        self.beta = beta or default_beta(m)
+        self.g = m // self.beta
+        assert m % self.beta == 0 and self.g % 2 == 0
+        self.n_out = k_min(H * m * m, n)
+
+
+def default_beta(m):
+    b = 1
+    while b * b < m:
+        b *= 2
+    return b
+
+
+def score_qk_slots(Qp, plan, l):
+    """Block l of Q^{pi_S} (or K^{pi_S}) in segment-column packing: segment c holds column l C_qk + c."""
+    return seg_column_pack(Qp, plan.m, plan.C, l, plan.n)
+
+
+def score(ev, plan, qs, ks):
+    """C7.  Per block l: Q bank Psi^{-s} (s < beta), K bank Psi^{j beta}, Psi^{m/2 + j beta} (j < g/2),
+    all hoisted from one ModUp each.  Per t = j beta + s < m/2:
+      T_t = sum_l q_{-s} (x) (k_{j beta} + i k_{m/2 + j beta})   lazy tensor sum, ONE relin, rescale (G6)
+      route: x <- x + Phi^{stride}(x) for stride = C/2, C/4, ..., H segments  (Phi^{c - (c mod H)}, G7)
+      S_t = Psi^{s}(route) restricted to segments [0, H)  (align + e_[0,H) mask merged, one rescale)
+    Returns [S_0 .. S_{m/2-1}]."""
+    m, H, beta, g, N_seg = plan.m, plan.H, plan.beta, plan.g, plan.N_seg
+    qb, kb = [], []
+    for l in range(plan.B):
+        qb.append(Psi_hoisted(ev, qs[l], [-s for s in range(beta)], m, N_seg))
+        kt = [j * beta for j in range(g // 2)] + [m // 2 + j * beta for j in range(g // 2)]
+        kk = Psi_hoisted(ev, ks[l], kt, m, N_seg)
+        kb.append({t: c for t, c in zip(kt, kk)})
+    S = []
+    for t in range(m // 2):
+        j, s = t // beta, t % beta
+        pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in range(plan.B)]
+        T = ev.rescale(ev.relin(ev.tensor_sum(pairs)))
+        T = route(ev, T, plan.C // H, H, m)
+        S.append(Psi_hoisted(ev, T, [s], m, N_seg, 0, H)[0])
+    return S
+
+
+def route(ev, x, k, H, m):
+    """Fold segment c onto c mod H: out[h] = sum_{j<k} x[h + jH] (the paper's sum_c Phi^{c - (c mod H)}
+    (x (.) m_c) with the sign of P:397 corrected, G7), as a binary rotate-add: O(log k) single rotations
+    (the m log C term of #rot_S).  Segments >= H hold garbage and are masked by the caller."""
+    result, offset, cnt, pw = None, 0, 1, x
+    kk = k
+    while kk:
+        if kk & 1:
+            y = Phi(ev, pw, offset * H, m) if offset else pw
+            result = y if result is None else ev.add(result, y)
+            offset += cnt
+        kk >>= 1
+        if kk:
+            pw = ev.add(pw, Phi(ev, pw, cnt * H, m))
+            cnt *= 2
+    return result
+
+
+def score_export(ev, plan, S):
+    """Minimal export stream (A20; t-major order S:181): stream slot (t H + h) m + j
+    -> ciphertext floor(./n), slot (. mod n).  S_t is rotated right by its offset o (single KS) and
+    masked by the slot range(s) it covers in each ciphertext (straddling pieces split by masks; the
+    tail is zero).  One rescale per output ciphertext.  Returns K_min(S) ciphertexts."""
+    m, H, n = plan.m, plan.H, plan.n
+    seg = H * m
+    outs = [None] * plan.n_out
+    for t, st in enumerate(S):
+        start = t * seg
+        o = start % n
+        r = ev.rot(st, -o) if o else st
+        k = start // n
+        first = min(seg, n - o)
+        pieces = [(k, o, o + first)]
+        if first < seg:
+            pieces.append((k + 1, 0, seg - first))
+        for (ci, a, b) in pieces:
+            desc = (0, m, a // m, 1, (b - a) // m)
+            y = ev.ptmul(r, ev.mask(desc, r.L, m))
+            outs[ci] = y if outs[ci] is None else ev.add(outs[ci], y)
+    return [ev.rescale(y) for y in outs]
+
+
+def score_reference(Qh, Kh):
+    """Brute force: S^h = Q^h (K^h)^T; Re S_t[h m + j] = S^h[j, (j+t) mod m], Im = S^h[j, (j+t+m/2) mod m]."""
+    H, m, _ = Qh.shape
+    S = np.einsum("hid,hjd->hij", Qh, Kh)
+    out = []
+    for t in range(m // 2):
+        v = np.zeros(H * m, dtype=np.complex128)
+        for h in range(H):
+            for jj in range(m):
+                v[h * m + jj] = S[h, jj, (jj + t) % m] + 1j * S[h, jj, (jj + t + m // 2) % m]
+        out.append(v)
+    return out
+
+
+# ====================================================================================== value kernel (§3.3.2, App. A.3)
+class ValuePlan:
+    """Value kernel plan: head-major V, folded-diagonal P_fd; needs d_h = m/2
+    for the folded stream to reshape directly; otherwise H_blk = 1 (G10)."""
+
+    def __init__(self, n, m, H, d_h, H_blk=None):
+        if m % 2:
+            raise O.OracleError("ODD_SEQ")
+        self.n, self.m, self.H, self.d_h = n, m, H, d_h
+        self.N_seg = n // m
+        if H_blk is None:
+            H_blk = self.N_seg // d_h if d_h == m // 2 else 1
+        assert H_blk * max(d_h, m // 2) <= self.N_seg
+        self.H_blk = H_blk
+        self.B_V = -(-H // H_blk)
+        self.seg_stride = max(d_h, m // 2)   # segments per local head
+
+
+def value_v_slots(Vh, plan, l):
+    """Head-major V block l: segment h~ d_h + u holds V^(l H_blk + h~)[:, u]."""
+    n, m = plan.n, plan.m
+    z = np.zeros(n, dtype=np.complex128)
+    for hh in range(plan.H_blk):
+        h = l * plan.H_blk + hh
+        if h >= plan.H:
+            continue
+        for u in range(plan.d_h):
+            s = hh * plan.seg_stride + u
+            z[s * m:(s + 1) * m] = Vh[h][:, u]
+    return z
+
+
+def value_p_slots(Ph, plan, l):
+    """Folded-diagonal P_fd block l: segment h~ (m/2) + t holds p_t + i p_{t+m/2} of local head h~,
+    p_t[j] = P[j, (j+t) mod m]."""
+    n, m = plan.n, plan.m
+    z = np.zeros(n, dtype=np.complex128)
+    jj = np.arange(m)
+    for hh in range(plan.H_blk):
+        h = l * plan.H_blk + hh
+        if h >= plan.H:
+            continue
+        for t in range(m // 2):
+            s = hh * plan.seg_stride + t
+            z[s * m:(s + 1) * m] = Ph[h][jj, (jj + t) % m] + 1j * Ph[h][jj, (jj + t + m // 2) % m]
+    return z
+
+
+def value(ev, plan, ps, vs):
+    """C8 (P:425-455 with G9: u_t = Psi^{+t} u):
+      1. uu = v (.) e_all - i (rot(v, m/2)(.)h_{m/2} + rot(v, -m/2)(.)u_{m/2}), ONE rescale
+      2. U bank: u_t = Psi^{t}(uu), t = 0..m/2-1 (hoisted)
+      3. Phi bank of p_fd: delta in [-(d_h-1), m/2-1] (hoisted single rotations by delta m)
+      4. b_t = sum_u Phi^{t-u}(p_fd) (.) n_u, rescale
+      5. o = sum_t u_t (x) b_t (u_t mod-dropped to b_t's level), ONE relin, rescale."""
+    m, N_seg = plan.m, plan.N_seg
+    half = m // 2
+    outs = []
+    for l in range(plan.B_V):
+        v, p = vs[l], ps[l]
+        Lv = v.L
+        rv = ev.rot_hoisted(v, [half, half - m])
+        hd, ud = psi_masks(half, m, N_seg)
+        sh = ev.add(ev.ptmul(rv[0], ev.mask(hd, Lv, m)), ev.ptmul(rv[1], ev.mask(ud, Lv, m)))
+        uu = ev.rescale(ev.sub(ev.ptmul(v, ev.mask((0, m, 0, 1, N_seg), Lv, m)), ev.mul_i(sh)))
+        ub = Psi_hoisted(ev, uu, list(range(half)), m, N_seg)
+        deltas = [d for d in range(-(plan.d_h - 1), half) if d != 0]
+        pb = dict(zip(deltas, ev.rot_hoisted(p, [d * m for d in deltas])))
+        pb[0] = p
+        Lp = p.L
+        bt = []
+        for t in range(half):
+            acc = None
+            for u in range(plan.d_h):
+                desc = (0, m, u, plan.seg_stride, plan.H_blk)
+                y = ev.ptmul(pb[t - u], ev.mask(desc, Lp, m))
+                acc = y if acc is None else ev.add(acc, y)
+            bt.append(ev.rescale(acc))
+        Lb = bt[0].L
+        pairs = [(ev.mod_drop(ub[t], Lb) if ub[t].L > Lb else ub[t], bt[t]) for t in range(half)]
+        outs.append(ev.rescale(ev.relin(ev.tensor_sum(pairs))))
+    return outs
+
+
+def value_reference(Ph, Vh):
+    return np.einsum("hij,hjd->hid", Ph, Vh)
+
+
+# ====================================================================================== export (Alg 3, GPU half)
+def l_conv(P, ell=43, sigma=40, scale=None, B_max=1.0):
+    """Modulus trimming: smallest L with log2 Q_L >= ell + sigma + 1 and Q_L/2 > Delta B_max.
+    ell = 43, sigma = 40 (G19).  Returns None if no level satisfies it (ENCF_ERR_CONFIG)."""
+    import math
+    scale = scale if scale is not None else 2.0 ** P.log2_scale
+    Q = 1
+    for L in range(1, P.L_max + 1):
+        Q *= P.q[L - 1]
+        if math.log2(Q) >= ell + sigma + 1 and Q / 2 > scale * B_max:
+            return L
+    return None
+
+
+def export_c2m(P, ct, L_conv, mask_seed, stream_id):
+    """Alg 3 steps 1 (P1 side) with trimming (C9):
+      mod-drop to L_conv; r^ uniform mod q_i per limb (coefficient domain, G18) from
+      stream mask(stream_id); d = (c0 + r^, c1) goes to P0; the server share is -r^ mod q_i.
+    Returns (masked ciphertext, server share [L_conv][N])."""
+    if ct.ncomp != 2:
+        raise O.OracleError("FORMAT")
+    d = O.mod_drop(P, ct, L_conv)
+    mods = P.q[:L_conv]
+    r = O.sample_uniform(mask_seed, O.stream_mask(stream_id), mods, list(range(L_conv)), P.N)
+    c0 = O.padd(d.c[0], r, mods, P.N)
+    share = O.pneg(r, mods, P.N)
+    return O.Ct(np.stack([c0, d.c[1]]), ct.scale), share
