@@ -1,0 +1,216 @@
+// ctx.cu -- context creation: modulus constants, NTT twiddles, base-conversion and rescale tables.
+// All constants are computed on the host with exact 128-bit modular arithmetic (no big integers
+// are needed: every CRT factor is a product of primes reduced modulo a single prime).
+#include <cstring>
+#include "ctx.cuh"
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& s) { g_last_error = s; }
+const char* encf_last_error_impl() { return g_last_error.c_str(); }
+
+void* encf_ctx::dev_alloc(size_t bytes) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes ? bytes : 8);
+    if (e != cudaSuccess) throw EncfError(ENCF_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    allocations.push_back(p);
+    return p;
+}
+
+static u64* upload(encf_ctx& c, const std::vector<u64>& v) {
+    u64* d = (u64*)c.dev_alloc(v.size() * sizeof(u64));
+    CUDA_TRY(cudaMemcpy(d, v.data(), v.size() * sizeof(u64), cudaMemcpyHostToDevice));
+    return d;
+}
+
+static int bitrev(int x, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
+    return r;
+}
+
+static bool is_prime_u64(u64 n) {   // deterministic Miller-Rabin for 64-bit
+    if (n < 2) return false;
+    for (u64 p : {2ull, 3ull, 5ull, 7ull, 11ull, 13ull, 17ull, 19ull, 23ull, 29ull, 31ull, 37ull}) {
+        if (n % p == 0) return n == p;
+    }
+    u64 d = n - 1; int r = 0;
+    while ((d & 1) == 0) { d >>= 1; r++; }
+    for (u64 a : {2ull, 325ull, 9375ull, 28178ull, 450775ull, 9780504ull, 1795265022ull}) {
+        u64 x = h_powmod(a % n, d, n);
+        if (a % n == 0 || x == 1 || x == n - 1) continue;
+        bool comp = true;
+        for (int i = 1; i < r; i++) { x = h_mulmod(x, x, n); if (x == n - 1) { comp = false; break; } }
+        if (comp) return false;
+    }
+    return true;
+}
+
+// A primitive 2N-th root of unity: g^((q-1)/2N) for the first g with psi^N = -1.
+static u64 find_psi(u64 q, int N) {
+    for (u64 g = 2; g < 100000; g++) {
+        u64 r = h_powmod(g, (q - 1) / (2 * (u64)N), q);
+        if (h_powmod(r, (u64)N, q) == q - 1) return r;
+    }
+    throw EncfError(ENCF_ERR_ARG, "no primitive 2N-th root");
+}
+
+static void build(encf_ctx& c, const encf_params* p) {
+    c.N = p->N;
+    c.logN = 0;
+    while ((1 << c.logN) < c.N) c.logN++;
+    if ((1 << c.logN) != c.N || c.logN < 4 || c.logN > 16) throw EncfError(ENCF_ERR_ARG, "N must be a power of two in [2^4, 2^16]");
+    c.L = p->L; c.K = p->K; c.alpha = p->alpha;
+    if (c.L < 1 || c.K < 1 || c.alpha < 1 || c.L + c.K > MAX_MODS || c.alpha > 16)
+        throw EncfError(ENCF_ERR_ARG, "bad L/K/alpha");
+    c.s1 = c.logN / 2;
+    c.s2 = c.logN - c.s1;
+    c.mods.assign(p->q, p->q + c.L);
+    c.mods.insert(c.mods.end(), p->p, p->p + c.K);
+    for (u64 q : c.mods) {
+        if (q >= (1ull << 61) || (q - 1) % (2 * (u64)c.N) != 0 || !is_prime_u64(q))
+            throw EncfError(ENCF_ERR_ARG, "every modulus must be a prime < 2^61 with q = 1 mod 2N");
+    }
+    const int M = (int)c.mods.size(), N = c.N;
+    std::vector<ModConst> mc(M);
+    std::vector<u64> psi(M * (size_t)N), psi_sh(M * (size_t)N), ipsi(M * (size_t)N), ipsi_sh(M * (size_t)N);
+    std::vector<u64> ninv(M), ninv_sh(M), im(M), im_sh(M);
+    c.psi.resize(M);
+    for (int i = 0; i < M; i++) {
+        u64 q = c.mods[i];
+        mc[i].q = q;
+        mc[i].two_q = 2 * q;
+        h_ratio128(q, mc[i].rhi, mc[i].rlo);
+        u64 ps = find_psi(q, N), ips = h_invmod(ps, q);
+        c.psi[i] = ps;
+        // powers psi^k, psi^-k for k < N, then scatter to bit-reversed positions
+        std::vector<u64> pw(N), ipw(N);
+        pw[0] = 1; ipw[0] = 1;
+        for (int k = 1; k < N; k++) { pw[k] = h_mulmod(pw[k - 1], ps, q); ipw[k] = h_mulmod(ipw[k - 1], ips, q); }
+        for (int k = 0; k < N; k++) {
+            int br = bitrev(k, c.logN);
+            size_t o = (size_t)i * N + k;
+            psi[o] = pw[br];
+            psi_sh[o] = shoup_pre(pw[br], q);
+            ipsi[o] = ipw[br];
+            ipsi_sh[o] = shoup_pre(ipw[br], q);
+        }
+        ninv[i] = h_invmod((u64)N % q, q);
+        ninv_sh[i] = shoup_pre(ninv[i], q);
+        im[i] = h_powmod(ps, (u64)N / 2, q);   // psi^{N/2}: X^{N/2} evaluates to +-im at every NTT point
+        im_sh[i] = shoup_pre(im[i], q);
+    }
+    c.d_mod = (ModConst*)c.dev_alloc(M * sizeof(ModConst));
+    CUDA_TRY(cudaMemcpy(c.d_mod, mc.data(), M * sizeof(ModConst), cudaMemcpyHostToDevice));
+    c.d_psi = upload(c, psi); c.d_psi_sh = upload(c, psi_sh);
+    c.d_ipsi = upload(c, ipsi); c.d_ipsi_sh = upload(c, ipsi_sh);
+    c.d_ninv = upload(c, ninv); c.d_ninv_sh = upload(c, ninv_sh);
+    c.d_imag = upload(c, im); c.d_imag_sh = upload(c, im_sh);
+
+    // ModUp tables per (level, digit) -- SURVEY §8c C4: d~_{j,t} = sum_{i in j} [d_i (Q_j/q_i)^{-1}]_{q_i} (Q_j/q_i) mod t
+    c.modup.assign(c.L + 1, {});
+    c.moddown.assign(c.L + 1, {});
+    c.rescale.assign(c.L + 1, {});
+    for (int lev = 1; lev <= c.L; lev++) {
+        LimbMap ext = c.extmap(lev);
+        for (int j = 0; j < c.dnum(lev); j++) {
+            ModUpTab t;
+            t.lo = j * c.alpha;
+            t.hi = std::min((j + 1) * c.alpha, lev);
+            t.tgt.n = 0;
+            for (int e = 0; e < ext.n; e++) {
+                if (e >= t.lo && e < t.hi) continue;
+                t.tgt.mod[t.tgt.n++] = ext.mod[e];
+                t.tgt_pos.push_back(e);
+            }
+            int na = t.hi - t.lo;
+            std::vector<u64> vf(na), vfs(na), wf((size_t)na * t.tgt.n);
+            for (int a = 0; a < na; a++) {
+                u64 qi = c.mods[t.lo + a];
+                u64 prod = 1;   // Q_j / q_i mod q_i
+                for (int b = 0; b < na; b++) if (b != a) prod = h_mulmod(prod, c.mods[t.lo + b] % qi, qi);
+                vf[a] = h_invmod(prod, qi);
+                vfs[a] = shoup_pre(vf[a], qi);
+                for (int k = 0; k < t.tgt.n; k++) {
+                    u64 tq = c.mods[t.tgt.mod[k]];
+                    u64 pr = 1;
+                    for (int b = 0; b < na; b++) if (b != a) pr = h_mulmod(pr, c.mods[t.lo + b] % tq, tq);
+                    wf[(size_t)a * t.tgt.n + k] = pr;
+                }
+            }
+            t.d_vfac = upload(c, vf); t.d_vfac_sh = upload(c, vfs); t.d_wfac = upload(c, wf);
+            c.modup[lev].push_back(t);
+        }
+        // ModDown: y = fastBConv_{P->Q}([b]_P); out_i = (b_i - y_i) P^{-1} mod q_i
+        ModDownTab md;
+        std::vector<u64> vf(c.K), vfs(c.K), wf((size_t)c.K * lev), pinv(lev), pinvs(lev);
+        for (int k = 0; k < c.K; k++) {
+            u64 pk = c.mods[c.L + k];
+            u64 prod = 1;
+            for (int b = 0; b < c.K; b++) if (b != k) prod = h_mulmod(prod, c.mods[c.L + b] % pk, pk);
+            vf[k] = h_invmod(prod, pk);
+            vfs[k] = shoup_pre(vf[k], pk);
+            for (int i = 0; i < lev; i++) {
+                u64 qi = c.mods[i];
+                u64 pr = 1;
+                for (int b = 0; b < c.K; b++) if (b != k) pr = h_mulmod(pr, c.mods[c.L + b] % qi, qi);
+                wf[(size_t)k * lev + i] = pr;
+            }
+        }
+        for (int i = 0; i < lev; i++) {
+            u64 qi = c.mods[i], P = 1;
+            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            pinv[i] = h_invmod(P, qi);
+            pinvs[i] = shoup_pre(pinv[i], qi);
+        }
+        md.d_vfac = upload(c, vf); md.d_vfac_sh = upload(c, vfs); md.d_wfac = upload(c, wf);
+        md.d_pinv = upload(c, pinv); md.d_pinv_sh = upload(c, pinvs);
+        c.moddown[lev] = md;
+        // Rescale (C5) dropping q_{lev-1}
+        if (lev >= 2) {
+            RescaleTab rt;
+            u64 qL = c.mods[lev - 1], h = qL / 2;
+            std::vector<u64> inv(lev - 1), invs(lev - 1), hm(lev - 1);
+            for (int i = 0; i < lev - 1; i++) {
+                u64 qi = c.mods[i];
+                inv[i] = h_invmod(qL % qi, qi);
+                invs[i] = shoup_pre(inv[i], qi);
+                hm[i] = h % qi;
+            }
+            rt.d_inv = upload(c, inv); rt.d_inv_sh = upload(c, invs); rt.d_hmod = upload(c, hm);
+            c.rescale[lev] = rt;
+        }
+    }
+    // rotation group 5^j mod 2N (encode / decode)
+    c.rot_group.resize(N / 2);
+    u64 x = 1;
+    for (int j = 0; j < N / 2; j++) { c.rot_group[j] = (int)x; x = x * 5 % (2 * (u64)N); }
+    c.d_rot_group = (int*)c.dev_alloc(sizeof(int) * (N / 2));
+    CUDA_TRY(cudaMemcpy(c.d_rot_group, c.rot_group.data(), sizeof(int) * (N / 2), cudaMemcpyHostToDevice));
+}
+
+encf_status ctx_create_impl(const encf_params* params, int device, encf_ctx** out) {
+    if (!params || !out || !params->q || !params->p) return ENCF_ERR_ARG;
+    encf_ctx* c = new encf_ctx();
+    try {
+        c->device = device;
+        CUDA_TRY(cudaSetDevice(device));
+        build(*c, params);
+        *out = c;
+        return ENCF_OK;
+    } catch (const EncfError& e) {
+        set_last_error(e.msg);
+        for (void* p : c->allocations) cudaFree(p);
+        delete c;
+        return e.code;
+    }
+}
+
+encf_status ctx_destroy_impl(encf_ctx* c) {
+    if (!c) return ENCF_ERR_ARG;
+    cudaSetDevice(c->device);
+    cudaDeviceSynchronize();
+    for (auto& kv : c->masks) cudaFree(kv.second);
+    for (void* p : c->allocations) cudaFree(p);
+    delete c;
+    return ENCF_OK;
+}

@@ -1,0 +1,181 @@
+// ctx.cuh -- library context (tables built once per parameter set) and internal launcher API.
+#pragma once
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "../../include/encf.h"
+
+struct Status {
+    encf_status code;
+    std::string msg;
+};
+
+void set_last_error(const std::string& s);
+
+#define CUDA_TRY(x)                                                                        \
+    do {                                                                                   \
+        cudaError_t _e = (x);                                                              \
+        if (_e != cudaSuccess) {                                                           \
+            set_last_error(std::string(#x) + ": " + cudaGetErrorString(_e));               \
+            throw EncfError(ENCF_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(_e)); \
+        }                                                                                  \
+    } while (0)
+
+struct EncfError {
+    encf_status code;
+    std::string msg;
+    EncfError(encf_status c, const std::string& m) : code(c), msg(m) {}
+};
+
+// A batch of limb polynomials: limb l of poly p lives at base + p*poly_stride + l*N, mod map.mod[l].
+struct PolyBatch {
+    u64* base;
+    i64 poly_stride;
+    int npolys;
+    LimbMap map;
+};
+
+struct ModUpTab {         // fast BConv of digit j at level L: digit limbs [lo,hi) -> targets
+    int lo, hi;
+    LimbMap tgt;          // target modulus ids
+    std::vector<int> tgt_pos;   // position of each target inside the extended [Q_L | P] layout
+    u64* d_vfac;          // [alpha]      (Q_j/q_i)^{-1} mod q_i
+    u64* d_vfac_sh;
+    u64* d_wfac;          // [alpha][ntgt] (Q_j/q_i) mod t
+};
+
+struct ModDownTab {       // P -> Q_L
+    u64* d_vfac;          // [K]   (P/p_k)^{-1} mod p_k
+    u64* d_vfac_sh;
+    u64* d_wfac;          // [K][L] (P/p_k) mod q_i
+    u64* d_pinv;          // [L]   P^{-1} mod q_i
+    u64* d_pinv_sh;
+};
+
+struct RescaleTab {       // drop q_{L-1}
+    u64* d_inv;           // [L-1] q_{L-1}^{-1} mod q_i
+    u64* d_inv_sh;
+    u64* d_hmod;          // [L-1] floor(q_{L-1}/2) mod q_i
+};
+
+struct MaskKey {
+    int m, r0, r1, s0, ss, sc, level;
+    bool operator<(const MaskKey& o) const {
+        return std::tie(m, r0, r1, s0, ss, sc, level) < std::tie(o.m, o.r0, o.r1, o.s0, o.ss, o.sc, o.level);
+    }
+};
+
+struct encf_ctx {
+    int device = 0;
+    int N = 0, logN = 0, L = 0, K = 0, alpha = 0;
+    int s1 = 0, s2 = 0;                 // NTT phase split: N = 2^s1 (rows) x 2^s2 (columns)
+    std::vector<u64> mods;              // q_0..q_{L-1}, p_0..p_{K-1}
+    std::vector<u64> psi;               // chosen primitive 2N-th roots
+    ModConst* d_mod = nullptr;          // [L+K]
+    u64 *d_psi = nullptr, *d_psi_sh = nullptr, *d_ipsi = nullptr, *d_ipsi_sh = nullptr;   // [L+K][N]
+    u64 *d_ninv = nullptr, *d_ninv_sh = nullptr;    // [L+K]
+    u64 *d_imag = nullptr, *d_imag_sh = nullptr;    // [L+K]  psi^{N/2} (a 4th root of unity)
+    std::vector<std::vector<ModUpTab>> modup;       // [level][digit]
+    std::vector<ModDownTab> moddown;                // [level]
+    std::vector<RescaleTab> rescale;                // [level]
+    std::vector<void*> allocations;
+    std::mutex mu;
+    std::map<MaskKey, u64*> masks;      // NTT-form mask plaintexts [level][N]
+    std::vector<int> rot_group;         // 5^j mod 2N (host, for encode)
+    int* d_rot_group = nullptr;
+    // statistics
+    std::atomic<uint64_t> st_ks{0}, st_modup{0}, st_ntt{0}, st_ptmul{0}, st_ctmul{0}, st_launch{0}, st_bytes{0};
+
+    int dnum(int level) const { return (level + alpha - 1) / alpha; }
+    LimbMap qmap(int level) const {
+        LimbMap m; m.n = level;
+        for (int i = 0; i < level; i++) m.mod[i] = (unsigned char)i;
+        return m;
+    }
+    LimbMap extmap(int level) const {   // [q_0..q_{level-1}, p_0..p_{K-1}]
+        LimbMap m; m.n = level + K;
+        for (int i = 0; i < level; i++) m.mod[i] = (unsigned char)i;
+        for (int k = 0; k < K; k++) m.mod[level + k] = (unsigned char)(L + k);
+        return m;
+    }
+    size_t limb_words() const { return (size_t)N; }
+    void* dev_alloc(size_t bytes);
+};
+
+// key material (device, NTT form)
+struct encf_keys {
+    int max_level = 0;
+    int dnum = 0;
+    u64* sk = nullptr;                  // [max_level + K][N]
+    std::map<uint32_t, u64*> ksk;       // galois (0 = relin) -> [dnum][2][max_level + K][N]
+    std::vector<void*> allocations;
+    int device = 0;
+};
+
+// ------------------------------------------------------------------------------------ scratch
+struct Scratch {   // stream-ordered device scratch, freed in the destructor (cudaFreeAsync)
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t st) : s(st) {}
+    u64* get(size_t words) {
+        void* p = nullptr;
+        cudaError_t e = cudaMallocAsync(&p, words * sizeof(u64), s);
+        if (e != cudaSuccess) throw EncfError(ENCF_ERR_OOM, std::string("cudaMallocAsync: ") + cudaGetErrorString(e));
+        ptrs.push_back(p);
+        return (u64*)p;
+    }
+    ~Scratch() { for (void* p : ptrs) cudaFreeAsync(p, s); }
+};
+
+// ------------------------------------------------------------------------------------ launchers (ntt.cu)
+void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
+void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------ launchers (poly.cu)
+void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s);
+void k_mul(encf_ctx& c, const u64* a, i64 a_stride, const u64* b, i64 b_stride, u64* out, i64 o_stride,
+           int npolys, const LimbMap& m, cudaStream_t s);
+void k_mul_i(encf_ctx& c, const u64* a, u64* out, int npolys, const LimbMap& m, cudaStream_t s);
+void k_automorph(encf_ctx& c, const u64* in, i64 in_stride, u64* out, i64 out_stride, int npolys, int nlimbs,
+                 uint32_t g, cudaStream_t s);
+void k_copy(const u64* in, u64* out, size_t words, cudaStream_t s);
+void k_sample_uniform(encf_ctx& c, u64 seed, u64 stream, u64* out, const LimbMap& m, const int* gids, cudaStream_t s);
+void k_sample_small(encf_ctx& c, u64 seed, u64 stream, int kind /*0 ternary, 1 cbd21*/, u64* out, const LimbMap& m,
+                    cudaStream_t s);
+void k_scalar_mul(encf_ctx& c, u64* data, int npolys, const LimbMap& m, const u64* d_scal, const u64* d_scal_sh,
+                  cudaStream_t s);
+void k_mod_reduce(encf_ctx& c, u64* data, int npolys, const LimbMap& m, cudaStream_t s);
+void k_rescale_prep(encf_ctx& c, const u64* last_coeff, u64* corr, int level, int ncomp, i64 last_stride,
+                    cudaStream_t s);
+void k_rescale_finish(encf_ctx& c, const u64* in, i64 in_stride, const u64* corr, u64* out, i64 out_stride,
+                      int ncomp, int level, cudaStream_t s);
+void k_bconv(encf_ctx& c, const u64* in, const LimbMap& in_map, const u64* d_vfac, const u64* d_vfac_sh,
+             const u64* d_wfac, const LimbMap& out_map, u64* out, const int* out_pos, cudaStream_t s);
+void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const u64* key, int key_nl,
+                const LimbMap& key_limb_of, u64* acc, cudaStream_t s);
+void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level,
+                      const ModDownTab& t, cudaStream_t s);
+void k_tensor_acc(encf_ctx& c, const u64* const* a, const u64* const* b, int nterms, u64* out3, int level,
+                  cudaStream_t s);
+void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units, i64 w_unit_stride,
+                u64* acc, i64 acc_stride, int level, cudaStream_t s);
+void k_masked_sum(encf_ctx& c, const u64* const* cts, const u64* const* masks, int nterms, u64* out, int level,
+                  cudaStream_t s);
+void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s);
+void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_slots, double scale, int level,
+                    u64* out, cudaStream_t s);
+void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);
+
+// ------------------------------------------------------------------------------------ ciphertext-level ops (ks.cu)
+struct CtView {
+    u64* d;
+    int ncomp, L;
+    double scale;
+    u64* comp(int c) const;
+};
+struct Eval;   // defined in ks.cu

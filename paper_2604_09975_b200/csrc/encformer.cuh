@@ -1,0 +1,31 @@
+// encformer.cuh -- plans and schedule entry points of the EncFormer kernels.
+#pragma once
+#include <algorithm>
+#include <vector>
+#include "eval.cuh"
+
+struct encf_proj_plan {
+    int n, m, d_in, d_out, N_seg, C, G, U, B_out, N1, N2;
+    uint32_t flags;
+};
+
+struct encf_attn_plan {
+    int n, m, H, d_h, N_seg, C, B, beta, g, n_out, H_blk, B_V, seg_stride;
+};
+
+void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C, int N1, uint32_t flags);
+std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p);
+void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
+                 int u1, std::vector<DCt>& accs);
+void proj_finalize(Ev& ev, const encf_proj_plan& p, const DCt& acc, DCt& y);
+
+void attn_plan_init(encf_attn_plan& a, int n, int m, int H, int d_h, int C_qk, int beta, int H_blk);
+std::vector<uint32_t> attn_galois(Ev& ev, const encf_attn_plan& a);
+void psi_hoisted(Ev& ev, const DCt& x, const std::vector<int>& ts, int m, int N_seg, int seg0, int nseg,
+                 std::vector<DCt>& outs);
+void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, const std::vector<DCt>& ks, int t0, int t1,
+               std::vector<DCt>& S);
+void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S, std::vector<DCt>& outs);
+void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs,
+               std::vector<DCt>& outs);
+int l_conv_rule(const encf_ctx& c, int ell, int sigma, double scale, double B_max);

@@ -1,0 +1,601 @@
+// poly.cu -- sm_100a kernels for everything that is not an NTT:
+//   pointwise add/sub/ptmul, x i (= X^{N/2}), Galois automorphism as an NTT-domain gather,
+//   counter-PRNG sampling, fast base conversion (ModUp / ModDown), the key-switching inner
+//   product (hoisted: the automorphism is fused into the digit loads), ModDown epilogue, rescale,
+//   the lazy ct x ct tensor sum, the fused plaintext-diagonal multiply-accumulate of the
+//   projection, masked sums (Psi shifts, broadcasts), export masking, and float64 encode/decode.
+// Integer work runs on the IMAD pipe with 64x64->128 products; every kernel is HBM- or IMAD-bound
+// (no dense contraction here: DESIGN.md "Why no tensor cores").
+#include "ctx.cuh"
+
+namespace {
+
+constexpr int TB = 256;
+
+inline int nblocks(size_t work, int per_block = TB, int cap = 148 * 32) {
+    size_t b = (work + per_block - 1) / per_block;
+    return (int)(b < (size_t)cap ? b : (size_t)cap);
+}
+
+__device__ __forceinline__ int brv(int x, int logN) { return (int)(__brev((unsigned)x) >> (32 - logN)); }
+
+// ------------------------------------------------------------------------------------ pointwise
+__global__ void add_kernel(const u64* __restrict__ a, const u64* __restrict__ b, u64* __restrict__ out,
+                           size_t total, int N, LimbMap m, const ModConst* mod, int sub) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)((i / N) % m.n);
+        u64 q = mod[m.mod[limb]].q;
+        u64 x = a[i], y = b[i];
+        out[i] = sub ? sub_mod(x, y, q) : add_mod(x, y, q);
+    }
+}
+
+__global__ void mul_kernel(const u64* __restrict__ a, i64 as, const u64* __restrict__ b, i64 bs, u64* __restrict__ out,
+                           i64 os, int npolys, int N, LimbMap m, const ModConst* mod) {
+    size_t per = (size_t)m.n * N, total = per * npolys;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        size_t p = i / per, r = i % per;
+        int limb = (int)(r / N);
+        ModConst mc = mod[m.mod[limb]];
+        out[p * os + r] = mulmod_barrett(a[p * as + r], b[p * bs + r], mc.q, mc.rhi, mc.rlo);
+    }
+}
+
+// x i: X^{N/2}(psi^{e}) = psi^{e N/2} = im^{e mod 4}; in bit-reversed order e_i = 2 brv(i) + 1 is
+// 1 mod 4 exactly for i < N/2, so the first half is multiplied by im and the second by -im.
+__global__ void mul_i_kernel(const u64* __restrict__ a, u64* __restrict__ out, size_t total, int N, LimbMap m,
+                             const ModConst* mod, const u64* im, const u64* im_sh) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)((i / N) % m.n), k = (int)(i % N);
+        int mi = m.mod[limb];
+        u64 q = mod[mi].q;
+        u64 r = mul_shoup(a[i], im[mi], im_sh[mi], q);
+        if (k >= N / 2) r = r ? q - r : 0;
+        out[i] = r;
+    }
+}
+
+// sigma_g in the NTT domain: out[i] = in[brv(((e_i g mod 2N) - 1) / 2)], e_i = 2 brv(i) + 1.
+// Within an aligned block of 2^k indices the sources are a permutation of an aligned block, so warp
+// accesses stay inside one 256-byte segment (coalesced gather).
+__global__ void automorph_kernel(const u64* __restrict__ in, i64 is, u64* __restrict__ out, i64 os,
+                                 int npolys, int nlimbs, int N, int logN, uint32_t g) {
+    size_t per = (size_t)nlimbs * N, total = per * npolys;
+    const uint32_t mask2n = 2 * N - 1;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        size_t p = i / per, r = i % per;
+        size_t limb = r / N;
+        int k = (int)(r % N);
+        uint32_t e = 2u * (uint32_t)brv(k, logN) + 1u;
+        uint32_t e2 = (uint32_t)(((uint64_t)e * g) & mask2n);
+        int src = brv((int)((e2 - 1) >> 1), logN);
+        out[p * os + limb * N + k] = in[p * is + limb * N + src];
+    }
+}
+
+// ------------------------------------------------------------------------------------ PRNG
+__device__ __forceinline__ u64 prng_draw(u64 seed, u64 stream, u64 index) {
+    u64 z = (seed ^ (stream * 0xD1B54A32D192ED03ULL)) + (index + 1) * 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+struct Gids { int g[MAX_LIMBS]; };
+
+__global__ void sample_uniform_kernel(u64 seed, u64 stream, u64* out, int N, LimbMap m, Gids gids, const ModConst* mod) {
+    size_t total = (size_t)m.n * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N), k = (int)(i % N);
+        u64 q = mod[m.mod[limb]].q;
+        u64 idx = 2 * ((u64)gids.g[limb] * (u64)N + (u64)k);
+        u64 hi = prng_draw(seed, stream, idx), lo = prng_draw(seed, stream, idx + 1);
+        // ((hi 2^64 + lo) q) >> 128 = high word of (hi q + ((lo q) >> 64))
+        u64 a_lo = hi * q, a_hi = umulhi(hi, q);
+        u64 b = umulhi(lo, q);
+        u64 s = a_lo + b;
+        out[i] = a_hi + (s < a_lo);
+    }
+}
+
+__global__ void sample_small_kernel(u64 seed, u64 stream, int kind, u64* out, int N, LimbMap m, const ModConst* mod) {
+    size_t total = (size_t)m.n * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N), k = (int)(i % N);
+        u64 q = mod[m.mod[limb]].q;
+        u64 u = prng_draw(seed, stream, (u64)k);
+        i64 v;
+        if (kind == 0) v = (i64)umulhi(u, 3) - 1;
+        else v = (i64)__popcll(u & 0x1FFFFFULL) - (i64)__popcll((u >> 21) & 0x1FFFFFULL);
+        out[i] = v < 0 ? q - (u64)(-v) : (u64)v;
+    }
+}
+
+__global__ void scalar_mul_kernel(u64* data, int npolys, int N, LimbMap m, const ModConst* mod, const u64* s, const u64* ssh) {
+    size_t total = (size_t)npolys * m.n * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)((i / N) % m.n);
+        data[i] = mul_shoup(data[i], s[limb], ssh[limb], mod[m.mod[limb]].q);
+    }
+}
+
+__global__ void mod_reduce_kernel(u64* data, size_t total, int N, LimbMap m, const ModConst* mod) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)((i / N) % m.n);
+        data[i] = data[i] % mod[m.mod[limb]].q;
+    }
+}
+
+// ------------------------------------------------------------------------------------ rescale (C5)
+// corr_i[k] = ((c_L[k] + h) mod q_L  mod q_i  -  h mod q_i) mod q_i   (coefficient domain)
+__global__ void rescale_prep_kernel(const u64* last, i64 ls, u64* corr, int ncomp, int level, int N,
+                                    const ModConst* mod, const u64* hmod) {
+    int nl = level - 1;
+    size_t per = (size_t)nl * N, total = per * ncomp;
+    u64 qL = mod[level - 1].q, h = qL / 2;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int c = (int)(i / per);
+        size_t r = i % per;
+        int limb = (int)(r / N), k = (int)(r % N);
+        u64 qi = mod[limb].q;
+        u64 lp = add_mod(last[c * ls + k], h, qL);
+        corr[i] = sub_mod(lp % qi, hmod[limb], qi);
+    }
+}
+
+// out_i = (c_i - corr_i) q_L^{-1} mod q_i   (NTT domain; corr already transformed)
+__global__ void rescale_finish_kernel(const u64* in, i64 is, const u64* corr, u64* out, i64 os, int ncomp, int level,
+                                      int N, const ModConst* mod, const u64* inv, const u64* inv_sh) {
+    int nl = level - 1;
+    size_t per = (size_t)nl * N, total = per * ncomp;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int c = (int)(i / per);
+        size_t r = i % per;
+        int limb = (int)(r / N);
+        u64 qi = mod[limb].q;
+        u64 d = sub_mod(in[c * is + r], corr[i], qi);
+        out[c * os + r] = mul_shoup(d, inv[limb], inv_sh[limb], qi);
+    }
+}
+
+// ------------------------------------------------------------------------------------ fast base conversion (C4)
+struct OutPos { int pos[MAX_LIMBS]; };
+
+// y_t[k] = sum_i [x_i[k] vfac_i]_{q_i} wfac[i][t] mod t ; in: [n_in][N] coefficient form; out limb
+// of target t at out + pos[t]*N.  One thread per coefficient, all targets (the x_i stay in registers).
+__global__ void __launch_bounds__(TB) bconv_kernel(const u64* __restrict__ in, LimbMap im, const u64* __restrict__ vfac,
+                                                   const u64* __restrict__ vfac_sh, const u64* __restrict__ wfac,
+                                                   LimbMap om, OutPos op, u64* __restrict__ out, int N,
+                                                   const ModConst* __restrict__ mod) {
+    extern __shared__ u64 sw[];   // [n_in][n_out] wfac
+    const int nin = im.n, nout = om.n;
+    for (int i = threadIdx.x; i < nin * nout; i += blockDim.x) sw[i] = wfac[i];
+    __syncthreads();
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        u64 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (i < nin) {
+                u64 qi = mod[im.mod[i]].q;
+                v[i] = mul_shoup(in[(size_t)i * N + k], vfac[i], vfac_sh[i], qi);
+            }
+        }
+        for (int t = 0; t < nout; t++) {
+            ModConst mc = mod[om.mod[t]];
+            U128 acc{0, 0};
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
+            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------ key-switch inner product (C4)
+// acc_c[e][k] = sum_j ext_j[e][src_g(k)] * key_j[c][kl(e)][k]  over the extended limbs e of Q_L u P.
+// The Galois gather of the hoisted batch is fused into the digit loads (g = 1: identity).
+struct KeyLimb { int kl[MAX_LIMBS]; };
+
+__global__ void __launch_bounds__(TB) ks_inner_kernel(const u64* __restrict__ ext, int dnum, int nl, uint32_t g,
+                                                      const u64* __restrict__ key, int key_nl, KeyLimb klm,
+                                                      LimbMap em, u64* __restrict__ acc, int N, int logN,
+                                                      const ModConst* __restrict__ mod) {
+    const int e = blockIdx.y;
+    const ModConst mc = mod[em.mod[e]];
+    const int kle = klm.kl[e];
+    const uint32_t mask2n = 2 * N - 1;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        int src = k;
+        if (g != 1) {
+            uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+            uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+            src = brv((int)((e2 - 1) >> 1), logN);
+        }
+        U128 a0{0, 0}, a1{0, 0};
+        for (int j = 0; j < dnum; j++) {
+            u64 x = ext[((size_t)j * nl + e) * N + src];
+            const u64* kj = key + (size_t)j * 2 * key_nl * N;
+            mac128(a0, x, kj[(size_t)kle * N + k]);
+            mac128(a1, x, kj[((size_t)key_nl + kle) * N + k]);
+        }
+        acc[(size_t)e * N + k] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
+        acc[((size_t)nl + e) * N + k] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
+    }
+}
+
+// out_i = (b_i - y_i) P^{-1} (+ add0_i) mod q_i   (NTT domain)
+__global__ void moddown_finish_kernel(const u64* __restrict__ b, const u64* __restrict__ y, const u64* __restrict__ add0,
+                                      u64* __restrict__ out, int level, int N, const ModConst* __restrict__ mod,
+                                      const u64* pinv, const u64* pinv_sh) {
+    size_t total = (size_t)level * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N);
+        u64 q = mod[limb].q;
+        u64 r = mul_shoup(sub_mod(b[i], y[i], q), pinv[limb], pinv_sh[limb], q);
+        if (add0) r = add_mod(r, add0[i], q);
+        out[i] = r;
+    }
+}
+
+// ------------------------------------------------------------------------------------ lazy tensor sum
+struct PtrList { const u64* p[64]; };
+
+// out3 = sum_t (a0 b0, a0 b1 + a1 b0, a1 b1) with 128-bit lazy accumulation (reduced every 64 terms).
+__global__ void __launch_bounds__(TB) tensor_acc_kernel(const u64* const* __restrict__ A, const u64* const* __restrict__ B,
+                                                        int nterms, u64* __restrict__ out, int level, int N,
+                                                        const ModConst* __restrict__ mod) {
+    const int limb = blockIdx.y;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;   // component stride
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const size_t o = (size_t)limb * N + k;
+        u64 r0 = 0, r1 = 0, r2 = 0;
+        for (int t0 = 0; t0 < nterms; t0 += 64) {
+            U128 d0{0, 0}, d1{0, 0}, d2{0, 0};
+            int te = min(nterms, t0 + 64);
+            for (int t = t0; t < te; t++) {
+                const u64* a = A[t];
+                const u64* b = B[t];
+                u64 a0 = a[o], a1 = a[cs + o], b0 = b[o], b1 = b[cs + o];
+                mac128(d0, a0, b0);
+                mac128(d1, a0, b1);
+                mac128(d1, a1, b0);
+                mac128(d2, a1, b1);
+            }
+            r0 = add_mod(r0, barrett128(d0, mc.q, mc.rhi, mc.rlo), mc.q);
+            r1 = add_mod(r1, barrett128(d1, mc.q, mc.rhi, mc.rlo), mc.q);
+            r2 = add_mod(r2, barrett128(d2, mc.q, mc.rhi, mc.rlo), mc.q);
+        }
+        out[o] = r0;
+        out[cs + o] = r1;
+        out[2 * cs + o] = r2;
+    }
+}
+
+// out = sum_t ct_t (.) mask_t   (2-component cts [2][level][N], masks [level][N]; lazy 128-bit sums)
+__global__ void __launch_bounds__(TB) masked_sum_kernel(const u64* const* __restrict__ C, const u64* const* __restrict__ M,
+                                                        int nterms, u64* __restrict__ out, int level, int N,
+                                                        const ModConst* __restrict__ mod) {
+    const int limb = blockIdx.y;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const size_t o = (size_t)limb * N + k;
+        u64 r0 = 0, r1 = 0;
+        for (int t0 = 0; t0 < nterms; t0 += 128) {
+            U128 d0{0, 0}, d1{0, 0};
+            int te = min(nterms, t0 + 128);
+            for (int t = t0; t < te; t++) {
+                const u64* c = C[t];
+                u64 w = M[t][o];
+                mac128(d0, c[o], w);
+                mac128(d1, c[cs + o], w);
+            }
+            r0 = add_mod(r0, barrett128(d0, mc.q, mc.rhi, mc.rlo), mc.q);
+            r1 = add_mod(r1, barrett128(d1, mc.q, mc.rhi, mc.rlo), mc.q);
+        }
+        out[o] = r0;
+        out[cs + o] = r1;
+    }
+}
+
+// ------------------------------------------------------------------------------------ diagonal MAC (projection, C6 step 2)
+// acc[unit][c][l][k] = sum_{uq < nbank} bank[uq][c][l][k] * w[unit][uq][l][k]
+// A CTA owns a 64-coefficient tile of one limb: the bank tile (nbank x 2 x 64 words) is staged once in
+// shared memory and reused by every unit; the plaintext stream is read exactly once (coalesced 512-B
+// rows), accumulators stay in 128-bit registers and are reduced once per unit.
+constexpr int MAC_T = 64;     // coefficients per CTA
+constexpr int MAC_LANES = 4;  // unit lanes per CTA (blockDim = 256)
+
+__global__ void __launch_bounds__(MAC_T * MAC_LANES) diag_mac_kernel(const u64* __restrict__ bank, int nbank,
+                                                                     const u64* __restrict__ w, int units, i64 wus,
+                                                                     u64* __restrict__ acc, i64 accs, int level, int N,
+                                                                     const ModConst* __restrict__ mod) {
+    extern __shared__ u64 sb[];   // [nbank][2][MAC_T]
+    const int limb = blockIdx.y;
+    const int k0 = blockIdx.x * MAC_T;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;   // component stride inside a ciphertext
+    const size_t bs = 2 * cs;              // ciphertext stride inside the bank
+    for (int i = threadIdx.x; i < nbank * 2 * MAC_T; i += blockDim.x) {
+        int uq = i / (2 * MAC_T), r = i % (2 * MAC_T);
+        int c = r / MAC_T, kk = r % MAC_T;
+        sb[i] = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+    }
+    __syncthreads();
+    const int kk = threadIdx.x % MAC_T, lane = threadIdx.x / MAC_T;
+    const size_t wl = (size_t)limb * N + k0 + kk;
+    const size_t pstride = (size_t)level * N;   // plaintext stride inside a unit
+    for (int u = blockIdx.z * MAC_LANES + lane; u < units; u += gridDim.z * MAC_LANES) {
+        const u64* wu = w + (size_t)u * wus + wl;
+        U128 a0{0, 0}, a1{0, 0};
+        int uq = 0;
+        for (; uq + 8 <= nbank; uq += 8) {
+            u64 x[8];
+#pragma unroll
+            for (int t = 0; t < 8; t++) x[t] = __ldg(wu + (size_t)(uq + t) * pstride);
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                mac128(a0, sb[(uq + t) * 2 * MAC_T + kk], x[t]);
+                mac128(a1, sb[(uq + t) * 2 * MAC_T + MAC_T + kk], x[t]);
+            }
+        }
+        for (; uq < nbank; uq++) {
+            u64 x = __ldg(wu + (size_t)uq * pstride);
+            mac128(a0, sb[uq * 2 * MAC_T + kk], x);
+            mac128(a1, sb[uq * 2 * MAC_T + MAC_T + kk], x);
+        }
+        u64* o = acc + (size_t)u * accs + wl;
+        o[0] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
+        o[cs] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
+    }
+}
+
+// ------------------------------------------------------------------------------------ export (Alg 3 step 1)
+__global__ void export_mask_kernel(u64 seed, u64 stream, u64* c0, u64* share, int level, int N, const ModConst* mod) {
+    size_t total = (size_t)level * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N), k = (int)(i % N);
+        u64 q = mod[limb].q;
+        u64 idx = 2 * ((u64)limb * (u64)N + (u64)k);
+        u64 hi = prng_draw(seed, stream, idx), lo = prng_draw(seed, stream, idx + 1);
+        u64 a_lo = hi * q, a_hi = umulhi(hi, q), b = umulhi(lo, q);
+        u64 s = a_lo + b;
+        u64 r = a_hi + (s < a_lo);
+        c0[i] = add_mod(c0[i], r, q);
+        share[i] = r ? q - r : 0;
+    }
+}
+
+// ------------------------------------------------------------------------------------ float64 encode / decode
+// S_k = sum_e A[e] exp(sign * 2 pi i e k / 2N): iterative radix-2 FFT of length 2N in global memory
+// (preprocessing only: weights and masks are encoded once).
+__global__ void fft_bitrev_kernel(double2* a, int n2, int logn2) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) {
+        int j = (int)(__brev((unsigned)i) >> (32 - logn2));
+        if (i < j) { double2 t = a[i]; a[i] = a[j]; a[j] = t; }
+    }
+}
+
+__global__ void fft_stage_kernel(double2* a, int n2, int len, double sign) {
+    int half = len / 2;
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n2 / 2; b += gridDim.x * blockDim.x) {
+        int grp = b / half, j = b % half;
+        int i0 = grp * len + j, i1 = i0 + half;
+        double s, c;
+        sincospi(sign * 2.0 * (double)j / (double)len, &s, &c);
+        double2 u = a[i0], v = a[i1];
+        double2 t = make_double2(v.x * c - v.y * s, v.x * s + v.y * c);
+        a[i0] = make_double2(u.x + t.x, u.y + t.y);
+        a[i1] = make_double2(u.x - t.x, u.y - t.y);
+    }
+}
+
+__global__ void scatter_slots_kernel(const double* re, const double* im, int n_slots, const int* rg, double2* A) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n_slots; j += gridDim.x * blockDim.x)
+        A[rg[j]] = make_double2(re[j], im ? im[j] : 0.0);
+}
+
+__global__ void round_reduce_kernel(const double2* S, double f, int N, int level, const ModConst* mod, u64* out, int* overflow) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        double v = rint(f * S[k].x);   // round half to even
+        if (fabs(v) >= 4611686018427387904.0) { *overflow = 1; v = 0; }
+        i64 x = (i64)v;
+        for (int l = 0; l < level; l++) {
+            u64 q = mod[l].q;
+            u64 r = (u64)(x < 0 ? -x : x) % q;
+            out[(size_t)l * N + k] = (x < 0 && r) ? q - r : r;
+        }
+    }
+}
+
+__global__ void lift_limb0_kernel(const u64* c, int N, const ModConst* mod, double2* A) {
+    u64 q = mod[0].q;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < 2 * N; k += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (k < N) {
+            u64 x = c[k];
+            v = x > q / 2 ? -(double)(q - x) : (double)x;
+        }
+        A[k] = make_double2(v, 0.0);
+    }
+}
+
+__global__ void gather_slots_kernel(const double2* Z, const int* rg, int n, double inv_scale, double* re, double* im) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        double2 z = Z[rg[j]];
+        re[j] = z.x * inv_scale;
+        im[j] = z.y * inv_scale;
+    }
+}
+
+void fft2n(encf_ctx& c, double2* A, double sign, cudaStream_t s) {
+    int n2 = 2 * c.N, logn2 = c.logN + 1;
+    fft_bitrev_kernel<<<nblocks(n2), TB, 0, s>>>(A, n2, logn2);
+    for (int len = 2; len <= n2; len <<= 1) fft_stage_kernel<<<nblocks(n2 / 2), TB, 0, s>>>(A, n2, len, sign);
+}
+
+}  // namespace
+
+// ====================================================================================== launchers
+#define GRID(total) nblocks((size_t)(total))
+
+void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s) {
+    size_t total = (size_t)npolys * m.n * c.N;
+    add_kernel<<<GRID(total), TB, 0, s>>>(a, b, out, total, c.N, m, c.d_mod, sub ? 1 : 0);
+    c.st_launch++; c.st_bytes += total * 24;
+}
+
+void k_mul(encf_ctx& c, const u64* a, i64 as, const u64* b, i64 bs, u64* out, i64 os, int npolys, const LimbMap& m,
+           cudaStream_t s) {
+    size_t total = (size_t)npolys * m.n * c.N;
+    mul_kernel<<<GRID(total), TB, 0, s>>>(a, as, b, bs, out, os, npolys, c.N, m, c.d_mod);
+    c.st_launch++; c.st_bytes += total * 24;
+}
+
+void k_mul_i(encf_ctx& c, const u64* a, u64* out, int npolys, const LimbMap& m, cudaStream_t s) {
+    size_t total = (size_t)npolys * m.n * c.N;
+    mul_i_kernel<<<GRID(total), TB, 0, s>>>(a, out, total, c.N, m, c.d_mod, c.d_imag, c.d_imag_sh);
+    c.st_launch++; c.st_bytes += total * 16;
+}
+
+void k_automorph(encf_ctx& c, const u64* in, i64 is, u64* out, i64 os, int npolys, int nlimbs, uint32_t g, cudaStream_t s) {
+    size_t total = (size_t)npolys * nlimbs * c.N;
+    automorph_kernel<<<GRID(total), TB, 0, s>>>(in, is, out, os, npolys, nlimbs, c.N, c.logN, g);
+    c.st_launch++; c.st_bytes += total * 16;
+}
+
+void k_copy(const u64* in, u64* out, size_t words, cudaStream_t s) {
+    if (words && in != out) CUDA_TRY(cudaMemcpyAsync(out, in, words * 8, cudaMemcpyDeviceToDevice, s));
+}
+
+void k_sample_uniform(encf_ctx& c, u64 seed, u64 stream, u64* out, const LimbMap& m, const int* gids, cudaStream_t s) {
+    Gids g;
+    for (int i = 0; i < m.n; i++) g.g[i] = gids[i];
+    sample_uniform_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(seed, stream, out, c.N, m, g, c.d_mod);
+    c.st_launch++;
+}
+
+void k_sample_small(encf_ctx& c, u64 seed, u64 stream, int kind, u64* out, const LimbMap& m, cudaStream_t s) {
+    sample_small_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(seed, stream, kind, out, c.N, m, c.d_mod);
+    c.st_launch++;
+}
+
+void k_scalar_mul(encf_ctx& c, u64* data, int npolys, const LimbMap& m, const u64* sc, const u64* scs, cudaStream_t s) {
+    scalar_mul_kernel<<<GRID((size_t)npolys * m.n * c.N), TB, 0, s>>>(data, npolys, c.N, m, c.d_mod, sc, scs);
+    c.st_launch++;
+}
+
+void k_mod_reduce(encf_ctx& c, u64* data, int npolys, const LimbMap& m, cudaStream_t s) {
+    size_t total = (size_t)npolys * m.n * c.N;
+    mod_reduce_kernel<<<GRID(total), TB, 0, s>>>(data, total, c.N, m, c.d_mod);
+    c.st_launch++; c.st_bytes += total * 16;
+}
+
+void k_rescale_prep(encf_ctx& c, const u64* last, u64* corr, int level, int ncomp, i64 ls, cudaStream_t s) {
+    rescale_prep_kernel<<<GRID((size_t)ncomp * (level - 1) * c.N), TB, 0, s>>>(last, ls, corr, ncomp, level, c.N, c.d_mod,
+                                                                            c.rescale[level].d_hmod);
+    c.st_launch++;
+}
+
+void k_rescale_finish(encf_ctx& c, const u64* in, i64 is, const u64* corr, u64* out, i64 os, int ncomp, int level,
+                      cudaStream_t s) {
+    const RescaleTab& t = c.rescale[level];
+    rescale_finish_kernel<<<GRID((size_t)ncomp * (level - 1) * c.N), TB, 0, s>>>(in, is, corr, out, os, ncomp, level, c.N,
+                                                                              c.d_mod, t.d_inv, t.d_inv_sh);
+    c.st_launch++; c.st_bytes += (size_t)ncomp * (level - 1) * c.N * 24;
+}
+
+void k_bconv(encf_ctx& c, const u64* in, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
+             const LimbMap& om, u64* out, const int* pos, cudaStream_t s) {
+    if (im.n > 16) throw EncfError(ENCF_ERR_ARG, "bconv: at most 16 input limbs");
+    OutPos op;
+    for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
+    size_t smem = (size_t)im.n * om.n * sizeof(u64);
+    int grid = (c.N + TB - 1) / TB;
+    bconv_kernel<<<grid, TB, smem, s>>>(in, im, vf, vfs, wf, om, op, out, c.N, c.d_mod);
+    c.st_launch++; c.st_bytes += (size_t)(im.n + om.n) * c.N * 8;
+}
+
+void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const u64* key, int key_nl,
+                const LimbMap& key_limb_of, u64* acc, cudaStream_t s) {
+    KeyLimb kl;
+    LimbMap em;
+    em.n = nl;
+    for (int e = 0; e < nl; e++) { kl.kl[e] = key_limb_of.mod[e]; }
+    // extended modulus ids: first (nl - K) are q_0.., then p_0..
+    int Lq = nl - c.K;
+    for (int e = 0; e < nl; e++) em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
+    dim3 grid((c.N + TB - 1) / TB, nl);
+    ks_inner_kernel<<<grid, TB, 0, s>>>(ext, dnum, nl, g, key, key_nl, kl, em, acc, c.N, c.logN, c.d_mod);
+    c.st_launch++; c.st_bytes += (size_t)dnum * nl * c.N * 8 * 3 + (size_t)2 * nl * c.N * 8;
+}
+
+void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level, const ModDownTab& t,
+                      cudaStream_t s) {
+    size_t total = (size_t)level * c.N;
+    moddown_finish_kernel<<<GRID(total), TB, 0, s>>>(b, y, add0, out, level, c.N, c.d_mod, t.d_pinv, t.d_pinv_sh);
+    c.st_launch++; c.st_bytes += total * (add0 ? 32 : 24);
+}
+
+void k_tensor_acc(encf_ctx& c, const u64* const* A, const u64* const* B, int nterms, u64* out3, int level, cudaStream_t s) {
+    dim3 grid((c.N + TB - 1) / TB, level);
+    tensor_acc_kernel<<<grid, TB, 0, s>>>(A, B, nterms, out3, level, c.N, c.d_mod);
+    c.st_launch++; c.st_bytes += (size_t)nterms * 4 * level * c.N * 8 + (size_t)3 * level * c.N * 8;
+    c.st_ctmul += nterms;
+}
+
+void k_masked_sum(encf_ctx& c, const u64* const* C, const u64* const* M, int nterms, u64* out, int level, cudaStream_t s) {
+    dim3 grid((c.N + TB - 1) / TB, level);
+    masked_sum_kernel<<<grid, TB, 0, s>>>(C, M, nterms, out, level, c.N, c.d_mod);
+    c.st_launch++; c.st_bytes += (size_t)nterms * 3 * level * c.N * 8 + (size_t)2 * level * c.N * 8;
+    c.st_ptmul += nterms;
+}
+
+void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units, i64 wus, u64* acc, i64 accs, int level,
+                cudaStream_t s) {
+    size_t smem = (size_t)nbank * 2 * MAC_T * sizeof(u64);
+    static bool attr_set = false;
+    if (!attr_set) {
+        CUDA_TRY(cudaFuncSetAttribute(diag_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr_set = true;
+    }
+    if (smem > 200 * 1024) throw EncfError(ENCF_ERR_PLAN_SHAPE, "diag_mac: bank too large for shared memory");
+    int tiles = c.N / MAC_T;
+    int zsplit = 1;
+    while ((size_t)tiles * level * zsplit < 148 * 4 && zsplit * MAC_LANES < units) zsplit *= 2;
+    dim3 grid(tiles, level, zsplit);
+    diag_mac_kernel<<<grid, MAC_T * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs, level, c.N, c.d_mod);
+    c.st_launch++;
+    c.st_bytes += (size_t)units * nbank * level * c.N * 8 + (size_t)nbank * 2 * level * c.N * 8 + (size_t)units * 2 * level * c.N * 8;
+    c.st_ptmul += (uint64_t)units * nbank;
+}
+
+void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s) {
+    export_mask_kernel<<<GRID((size_t)level * c.N), TB, 0, s>>>(seed, stream, c0, share, level, c.N, c.d_mod);
+    c.st_launch++;
+}
+
+void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots, double scale, int level, u64* out,
+                    cudaStream_t s) {
+    Scratch sc(s);
+    double2* A = (double2*)sc.get((size_t)2 * c.N * 2);
+    int* ovf = (int*)sc.get(1);
+    CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * 2 * c.N, s));
+    CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int), s));
+    scatter_slots_kernel<<<GRID(n_slots), TB, 0, s>>>(re, im, n_slots, c.d_rot_group, A);
+    fft2n(c, A, -1.0, s);
+    round_reduce_kernel<<<GRID(c.N), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    int h_ovf = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_ovf) throw EncfError(ENCF_ERR_OVERFLOW, "encode: |coefficient| >= 2^62");
+}
+
+void k_decode_limb0(encf_ctx& c, const u64* coeff0, double scale, double* re, double* im, cudaStream_t s) {
+    Scratch sc(s);
+    double2* A = (double2*)sc.get((size_t)2 * c.N * 2);
+    lift_limb0_kernel<<<GRID(2 * c.N), TB, 0, s>>>(coeff0, c.N, c.d_mod, A);
+    fft2n(c, A, +1.0, s);
+    gather_slots_kernel<<<GRID(c.N / 2), TB, 0, s>>>(A, c.d_rot_group, c.N / 2, 1.0 / scale, re, im);
+}

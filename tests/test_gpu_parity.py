@@ -1,0 +1,286 @@
+"""T1/T2/T3 on the B200: every limb of every output of the CUDA path (through the C ABI) equals the
+oracle's, on seeded inputs; plus decryption tolerances and error codes."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ckks as O
+from oracle import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2604_09975_b200 import encf as E  # noqa: E402
+from tests.gpu_util import assert_ct_equal, dev_ct, dev_pt, install_masks, weights_tensor  # noqa: E402
+
+P12, P13, P16 = O.Params("P12"), O.Params("P13"), O.Params("P16")
+TOL = 2.0 ** -20
+
+
+def rnd(mods, N, seed):
+    g = np.random.default_rng(seed)
+    return np.stack([g.integers(0, q, N, dtype=np.uint64) for q in mods])
+
+
+@pytest.fixture(scope="module")
+def c13():
+    return E.Context("P13", 0)
+
+
+@pytest.fixture(scope="module")
+def c16():
+    return E.Context("P16", 0)
+
+
+def galois13():
+    from tests.test_oracle_kernels import _galois13
+    return _galois13()
+
+
+@pytest.fixture(scope="module")
+def keys13(c13):
+    g = galois13()
+    return O.Keys(P13, synth.SEED_KEYS, galois=g, relin=True), c13.keygen(synth.SEED_KEYS, galois=g, relin=True)
+
+
+# ------------------------------------------------------------------ NTT / ring product
+@pytest.mark.parametrize("pname", ["P12", "P13", "P16"])
+def test_ntt_roundtrip_and_ring_product(pname):
+    P = O.Params(pname)
+    ctx = E.Context(pname, 0)
+    L = min(P.L_max, 6)
+    mods = P.q[:L]
+    a, b = rnd(mods, P.N, 1), rnd(mods, P.N, 2)
+    A = ctx.pt_from_host(a, 1.0)
+    assert np.array_equal(ctx.to_host(ctx.from_ntt(ctx.to_ntt(A))), a)
+    x = ctx.to_ntt(ctx.ct_from_host(np.stack([a, a]), 1.0))
+    y = ctx.ptmul(x, ctx.to_ntt(ctx.pt_from_host(b, 1.0)))
+    ref = O.ring_mul(a, b, mods, P.N)
+    got = ctx.to_host(y)
+    assert np.array_equal(got[0], ref) and np.array_equal(got[1], ref)
+
+
+# ------------------------------------------------------------------ keys / enc / dec
+def test_keys_bit_exact(c13, keys13):
+    ok, gk = keys13
+    ML = ok.max_level
+    nl = ML + len(P13.p)
+    sk = gk.export(0).reshape(nl, P13.N)
+    assert np.array_equal(sk, ok.s)
+    for g in [galois13()[0], 0]:
+        kk = gk.export(1, g).reshape(P13.dnum(ML), 2, nl, P13.N)
+        for j in range(P13.dnum(ML)):
+            assert np.array_equal(kk[j], ok.ksk[g][j]), (g, j)
+
+
+def test_encrypt_decrypt_bit_exact(c13, keys13):
+    ok, gk = keys13
+    z = synth.complex_slots(P13.n, 3)
+    pt = O.encode(P13, z, 2.0 ** 40, 6)
+    ref = O.encrypt_sk(P13, ok, pt, 77)
+    got = c13.encrypt(gk, c13.pt_from_host(pt.m, pt.scale), 77)
+    assert_ct_equal(c13, got, ref, "encrypt")
+    d = c13.decrypt(gk, got)
+    assert np.array_equal(c13.to_host(d), O.decrypt(P13, ok, ref).m)
+
+
+def test_encode_decode_gpu_vs_oracle(c13):
+    z = synth.complex_slots(P13.n, 4)
+    ref = O.encode_coeffs(z, 2.0 ** 40, P13.N)
+    pt = c13.encode(z, 2.0 ** 40, 3)
+    got = c13.to_host(pt)
+    refq = O.from_signed(ref, P13.q[:3], P13.N)
+    diff = np.minimum((got.astype(object) - refq.astype(object)) % np.array(P13.q[:3], dtype=object)[:, None],
+                      (refq.astype(object) - got.astype(object)) % np.array(P13.q[:3], dtype=object)[:, None])
+    assert int(diff.max()) <= 1             # float64 encode: +-1 per coefficient
+    zz = c13.decode(pt)
+    assert np.abs(zz - z).max() < 1e-9
+
+
+# ------------------------------------------------------------------ key switching & friends
+@pytest.mark.parametrize("L", [8, 5, 3, 1])
+def test_rotations_conj_bit_exact(c13, keys13, L):
+    ok, gk = keys13
+    z = synth.complex_slots(P13.n, 10 + L)
+    ct = O.encrypt_sk(P13, ok, O.encode(P13, z, 2.0 ** 40, L), 5)
+    d = dev_ct(c13, ct)
+    for r in (1, 16, -3):
+        assert_ct_equal(c13, c13.rotate(gk, d, r), O.rotate(P13, ok, ct, r), "rotate %d L=%d" % (r, L))
+    steps = [1, 16, 32, -3, 0]
+    hs = c13.rotate_hoisted(gk, d, steps)
+    for r, h, ref in zip(steps, hs, O.rotate_hoisted(P13, ok, ct, steps)):
+        assert_ct_equal(c13, h, ref, "hoisted %d L=%d" % (r, L))
+    assert_ct_equal(c13, c13.conjugate(gk, d), O.conjugate(P13, ok, ct), "conj")
+
+
+def test_tensor_relin_rescale_bit_exact(c13, keys13):
+    ok, gk = keys13
+    a = O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 20), 2.0 ** 40, 7), 1)
+    b = O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 21), 2.0 ** 40, 7), 2)
+    da, db = dev_ct(c13, a), dev_ct(c13, b)
+    t = c13.tensor(da, db)
+    tr = O.tensor(P13, a, b)
+    assert_ct_equal(c13, t, tr, "tensor")
+    r = c13.relinearize(gk, t)
+    rr = O.relinearize(P13, ok, tr)
+    assert_ct_equal(c13, r, rr, "relin")
+    assert_ct_equal(c13, c13.rescale(r), O.rescale(P13, rr), "rescale")
+    assert_ct_equal(c13, c13.mod_drop(da, 4), O.mod_drop(P13, a, 4), "mod_drop")
+    assert_ct_equal(c13, c13.mul_i(da), O.mul_i(P13, a), "mul_i")
+    assert_ct_equal(c13, c13.add(da, db), O.add(P13, a, b), "add")
+    assert_ct_equal(c13, c13.add(da, db, sub=True), O.sub(P13, a, b), "sub")
+    assert_ct_equal(c13, c13.complexify(da, db), O.complexify(P13, a, b), "complexify")
+
+
+def test_keyswitch_P16_top_level(c16):
+    """Config 2 shape (L = 24, dnum = 3, alpha = 8): single and hoisted rotations bit-exact."""
+    L = 24
+    g = [O.galois_rot(P16, r) for r in (128, 256)]
+    ok = O.Keys(P16, synth.SEED_KEYS, galois=g)
+    gk = c16.keygen(synth.SEED_KEYS, galois=g)
+    ct = O.encrypt_sk(P16, ok, O.encode(P16, synth.uniform(P16.n, 60), 2.0 ** 40, L), 9)
+    d = dev_ct(c16, ct)
+    assert_ct_equal(c16, c16.rotate(gk, d, 128), O.rotate(P16, ok, ct, 128), "rotate P16 L=24")
+    for h, ref in zip(c16.rotate_hoisted(gk, d, [128, 256]), O.rotate_hoisted(P16, ok, ct, [128, 256])):
+        assert_ct_equal(c16, h, ref, "hoisted P16 L=24")
+
+
+def test_error_codes(c13, keys13):
+    ok, gk = keys13
+    a = O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 30), 2.0 ** 40, 2), 1)
+    b = O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 31), 2.0 ** 39, 2), 2)
+    with pytest.raises(E.EncfError) as e:
+        c13.add(dev_ct(c13, a), dev_ct(c13, b))
+    assert e.value.code == 3
+    one = dev_ct(c13, O.mod_drop(P13, a, 1))
+    with pytest.raises(E.EncfError) as e:
+        c13.rescale(one)
+    assert e.value.code == 5
+    with pytest.raises(E.EncfError) as e:
+        c13.rotate(gk, dev_ct(c13, a), 12345)
+    assert e.value.code == 11
+    with pytest.raises(E.EncfError) as e:
+        E.AttnPlan(c13, 15, 4, 8)
+    assert e.value.code == 7
+
+
+# ------------------------------------------------------------------ EncFormer kernels
+def _proj_case(P, ctx, okeys, gkeys, m, d_in, d_out, N1, L, seed):
+    plan = E.ProjPlan(ctx, m, d_in, d_out, N1=N1)
+    oplan = K.ProjPlan(P.n, m, d_in, d_out, N1=N1)
+    X = synth.fixed_point_uniform((m, d_in), seed)
+    W = synth.bert_weight((d_in, d_out), seed + 1)
+    xs = [O.encrypt_sk(P, okeys, O.encode(P, z, 2.0 ** 40, L), synth.seed_enc(u)) for u, z in enumerate(K.proj_inputs(X, oplan))]
+    pts = {}
+
+    def w(b, p, u, q):
+        if (b, p, u, q) not in pts:
+            pts[(b, p, u, q)] = O.encode(P, K.proj_weight_slots(W, oplan, b, p, u, q), float(P.q[L - 1]), L)
+        return pts[(b, p, u, q)]
+    ys = K.projection(K.Ev(P, okeys, m), oplan, xs, w)
+    order = [w(b, p, u, q) for b in range(oplan.B_out) for p in range(oplan.N2) for u in range(oplan.U) for q in range(oplan.N1)]
+    wd = weights_tensor(ctx, order, L)
+    got = plan.matmul(gkeys, [dev_ct(ctx, x) for x in xs], wd, float(P.q[L - 1]))
+    for b, (g, r) in enumerate(zip(got, ys)):
+        assert_ct_equal(ctx, g, r, "projection y_%d" % b)
+    Y = np.concatenate([K.seg_column_unpack(O.decode(P, O.decrypt(P, okeys, y)).real, m, oplan.C, d_out, b) for b, y in enumerate(ys)], axis=1)
+    assert np.abs(Y - X @ W).max() / np.abs(X @ W).max() < TOL
+    return plan, oplan, xs, wd, ys
+
+
+def test_projection_config1_bit_exact():
+    ctx = E.Context("P12", 0)
+    plan = E.ProjPlan(ctx, 32, 64, 64, N1=8)
+    g = plan.galois()
+    ok, gk = O.Keys(P12, synth.SEED_KEYS, galois=g), ctx.keygen(synth.SEED_KEYS, galois=g)
+    _proj_case(P12, ctx, ok, gk, 32, 64, 64, 8, 3, synth.seed_data(1))
+
+
+def test_projection_ragged_and_unit_split(c13, keys13):
+    """U = 2, G odd, ragged d_out; then the same projection split into two unit ranges (the
+    multi-GPU partition), partial accumulators summed as uint64 and mod-reduced (C2), then finalised."""
+    ok, gk = keys13
+    plan, oplan, xs, wd, ys = _proj_case(P13, c13, ok, gk, 16, 600, 300, 8, 4, 70)
+    units = plan.B_out * plan.N2
+    cut = units // 2 + 3
+    xd = [dev_ct(c13, x) for x in xs]
+    a = plan.matmul(gk, xd, wd, float(P13.q[3]), 0, cut, finalize=False)
+    b = plan.matmul(gk, xd, wd, float(P13.q[3]), cut, units, finalize=False)
+    # block containing `cut` is split across the two "ranks": add as uint64 then mod-reduce
+    bsplit = cut // plan.N2
+    accs = a[:bsplit] + [None] + b[1:]
+    s = a[bsplit].data + b[0].data    # int64 storage; q < 2^61 so the sum is exact
+    c13.mod_reduce(s, 2, a[bsplit].n_limbs)
+    a[bsplit].data = s
+    accs[bsplit] = a[bsplit]
+    yfin = plan.finalize(gk, accs, 0)
+    for bb, (g, r) in enumerate(zip(yfin, ys)):
+        assert_ct_equal(c13, g, r, "split projection y_%d" % bb)
+
+
+def test_score_and_export_bit_exact(c13, keys13):
+    ok, gk = keys13
+    m, H, dh = 16, 4, 8
+    plan = E.AttnPlan(c13, m, H, dh, C_qk=16, beta=4)
+    oplan = K.ScorePlan(P13.n, m, H, dh, C_qk=16, beta=4)
+    g = synth.rng(40)
+    Qh, Kh = g.uniform(-1, 1, (H, m, dh)), g.uniform(-1, 1, (H, m, dh))
+    perm = K.pi_S(H, dh)
+    Qp, Kp = np.concatenate(list(Qh), 1)[:, perm], np.concatenate(list(Kh), 1)[:, perm]
+    L0 = 6
+    qs = [O.encrypt_sk(P13, ok, O.encode(P13, K.score_qk_slots(Qp, oplan, l), 2.0 ** 40, L0), 100 + l) for l in range(oplan.B)]
+    ks = [O.encrypt_sk(P13, ok, O.encode(P13, K.score_qk_slots(Kp, oplan, l), 2.0 ** 40, L0), 200 + l) for l in range(oplan.B)]
+    ev = K.Ev(P13, ok, m)
+    S = K.score(ev, oplan, qs, ks)
+    Ex = K.score_export(ev, oplan, S)
+    c13.mask_clear()
+    install_masks(c13, ev)
+    gS = plan.score(gk, [dev_ct(c13, x) for x in qs], [dev_ct(c13, x) for x in ks])
+    for t, (a, b) in enumerate(zip(gS, S)):
+        assert_ct_equal(c13, a, b, "S_%d" % t)
+    gE = plan.export_stream(gk, gS)
+    for a, b in zip(gE, Ex):
+        assert_ct_equal(c13, a, b, "export stream")
+    # t-range split (multi-GPU partition of the score kernel) gives the same S_t
+    part = plan.score(gk, [dev_ct(c13, x) for x in qs], [dev_ct(c13, x) for x in ks], 3, 6)
+    for t, a in zip(range(3, 6), part):
+        assert_ct_equal(c13, a, S[t], "S_%d (range)" % t)
+    c13.mask_clear()
+
+
+def test_value_bit_exact(c13, keys13):
+    ok, gk = keys13
+    m, H, dh = 16, 4, 8
+    plan = E.AttnPlan(c13, m, H, dh, H_blk=2)
+    oplan = K.ValuePlan(P13.n, m, H, dh, H_blk=2)
+    Ph = synth.attention_probs(H, m, 41)
+    Vh = synth.uniform((H, m, dh), 42)
+    vs = [O.encrypt_sk(P13, ok, O.encode(P13, K.value_v_slots(Vh, oplan, l), 2.0 ** 40, 6), 300 + l) for l in range(oplan.B_V)]
+    ps = [O.encrypt_sk(P13, ok, O.encode(P13, K.value_p_slots(Ph, oplan, l), 2.0 ** 40, 4), 400 + l) for l in range(oplan.B_V)]
+    ev = K.Ev(P13, ok, m)
+    outs = K.value(ev, oplan, ps, vs)
+    c13.mask_clear()
+    install_masks(c13, ev)
+    got = plan.value(gk, [dev_ct(c13, x) for x in ps], [dev_ct(c13, x) for x in vs])
+    for a, b in zip(got, outs):
+        assert_ct_equal(c13, a, b, "value")
+    c13.mask_clear()
+
+
+def test_export_c2m_bit_exact(c13, keys13):
+    ok, gk = keys13
+    x, y = synth.fixed_point_uniform(P13.n, 50), synth.fixed_point_uniform(P13.n, 51)
+    cx = O.encrypt_sk(P13, ok, O.encode(P13, x, 2.0 ** 40, 5), 1)
+    cy = O.encrypt_sk(P13, ok, O.encode(P13, y, 2.0 ** 40, 5), 2)
+    ref = O.complexify(P13, cx, cy)
+    got = c13.complexify(dev_ct(c13, cx), dev_ct(c13, cy))
+    assert_ct_equal(c13, got, ref, "complexify")
+    Lc = c13.l_conv()
+    assert Lc == K.l_conv(P13)
+    masked, share = c13.export_c2m(got, Lc, synth.seed_mask(0), 0)
+    rm, rs = K.export_c2m(P13, ref, Lc, synth.seed_mask(0), 0)
+    assert np.array_equal(c13.to_host(masked, coeff=False), rm.c)
+    assert np.array_equal(share.cpu().numpy().view(np.uint64).reshape(Lc, P13.N), rs)
