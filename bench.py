@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""bench.py -- BERT-base layer CKKS linear path of EncFormer (arXiv 2604.09975) at N = 2^16 on B200.
+
+One "step" = one pass of the whole hot path over one BERT-base layer
+(m = 128 tokens, d = 768, H = 12, d_ff = 3072) of synthetic encrypted activations:
+  QKV projection (X 128x768 -> Q, K (pi_S, G8-padded) and V, L = 8 -> 7)
+  -> score kernel (64 folded-diagonal S_t) -> minimal export stream (K_min(S) = 3) -> C2M export
+  -> value kernel (P_fd from the MPC softmax, 3 head blocks) -> decomplexify O -> out-projection
+  -> C2M export of the LN1 boundary -> FF1 (768 -> 3072) -> C2M export (GELU boundary)
+  -> FF2 (3072 -> 768) -> C2M export (LN2 boundary).
+Inputs that arrive from the MPC side (P_fd, the FF1 and FF2 activations) are fresh encryptions made
+before the timed region (their MPC producers are out of scope).  Weights are random BERT-init,
+encoded once (model state, resident in HBM).
+
+Contract: python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload layer|qkv|ks]
+prints ONE JSON line on rank 0.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+M, D, H, DH, DFF = 128, 768, 12, 64, 3072
+L_QKV, L_V_P, L_FF = 8, 5, 3
+C_QK, BETA = 192, 16
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks"])
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------------ clocks
+class Clocks:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q, "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 5 + i and r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------------------------ distributed plumbing
+def dist_init(args):
+    import torch
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------------------------------ the layer
+class Layer:
+    """BERT-base layer state on one GPU: context, keys, plans, encoded weights, synthetic inputs."""
+
+    def __init__(self, device, workload, seed_off=0):
+        import torch
+        import synth
+        from paper_2604_09975_b200 import encf as E
+        from paper_2604_09975_b200 import packing as PK
+        self.E, self.PK, self.torch = E, PK, torch
+        self.workload = workload
+        ctx = self.ctx = E.Context("P16", device)
+        n = ctx.n
+        self.sc = 2.0 ** 40
+        t0 = time.time()
+        self.qkv = E.ProjPlan(ctx, M, D, 11 * 256)
+        galois = set(self.qkv.galois())
+        if workload == "layer":
+            self.attn = E.AttnPlan(ctx, M, H, DH, C_qk=C_QK, beta=BETA)
+            self.oproj = E.ProjPlan(ctx, M, D, D)
+            self.ff1 = E.ProjPlan(ctx, M, D, DFF)
+            self.ff2 = E.ProjPlan(ctx, M, DFF, D)
+            for pl in (self.oproj, self.ff1, self.ff2):
+                galois |= set(pl.galois())
+            galois |= set(self.attn.galois())
+        galois.add(ctx.galois_conj())
+        self.keys = ctx.keygen(synth.SEED_KEYS, galois=sorted(galois), relin=True, max_level=L_QKV)
+        self.n_keys = len(galois) + 1
+        # weights (BERT init, clipped), pre-permuted (pi_S + G8 padding for Q/K, head-major V)
+        WQ, WK, WV = (synth.bert_weight((D, D), synth.seed_data(3) + i) for i in range(3))
+        Wqkv, nqk, nv = PK.qkv_weight(WQ, WK, WV, H, DH, 256, C_QK)
+        self.nqk = nqk
+        self.w_qkv = self.qkv.encode_weights(Wqkv, L_QKV)
+        self.wsc_qkv = float(ctx.q[L_QKV - 1])
+        if workload == "layer":
+            self.w_o = self.oproj.encode_weights(synth.bert_weight((D, D), synth.seed_data(5) + 3), L_V_P - 2)
+            self.w_1 = self.ff1.encode_weights(synth.bert_weight((D, DFF), synth.seed_data(5) + 4), L_FF)
+            self.w_2 = self.ff2.encode_weights(synth.bert_weight((DFF, D), synth.seed_data(5) + 5), L_FF)
+        torch.cuda.synchronize()
+        self.setup_s = time.time() - t0
+        # synthetic client inputs (encrypted before the timed region)
+        X = synth.fixed_point_uniform((M, D), synth.seed_data(3) + seed_off)
+        self.host_inputs = {"x": [self._enc(z, L_QKV, 10 + i) for i, z in enumerate(PK.complexified_inputs(X, M, 256, n))]}
+        if workload == "layer":
+            P = synth.attention_probs(H, M, synth.seed_data(4) + seed_off)
+            self.host_inputs["p"] = [self._enc(z, L_V_P, 20 + i) for i, z in enumerate(PK.folded_diag_blocks(P, M, self.attn.H_blk, self.attn.seg_stride, n))]
+            X1 = synth.fixed_point_uniform((M, D), synth.seed_data(5) + seed_off)
+            self.host_inputs["f1"] = [self._enc(z, L_FF, 30 + i) for i, z in enumerate(PK.complexified_inputs(X1, M, 256, n))]
+            X2 = synth.fixed_point_uniform((M, DFF), synth.seed_data(6) + seed_off, 0.0, 1.0)
+            self.host_inputs["f2"] = [self._enc(z, L_FF, 40 + i) for i, z in enumerate(PK.complexified_inputs(X2, M, 256, n))]
+        self.dev_inputs = {k: [self._to_dev(h) for h in v] for k, v in self.host_inputs.items()}
+        self.h2d_bytes = sum(h[0].nbytes for v in self.host_inputs.values() for h in v)
+        self.Lconv = ctx.l_conv()
+        self.mask_seed = synth.seed_mask(0)
+
+    def _enc(self, z, L, seed):
+        """Client-side encryption; returns (pinned host words, scale)."""
+        ct = self.ctx.encrypt(self.keys, self.ctx.encode(z, self.sc, L), seed)
+        return (ct.data.cpu().pin_memory(), ct.n_comp, ct.n_limbs, ct.scale)
+
+    def _to_dev(self, h):
+        words, nc, nl, sc = h
+        return self.E.Ciphertext(words.to(self.ctx.device), nc, nl, sc, 1)
+
+    def upload(self):
+        return {k: [self.E.Ciphertext(h[0].to(self.ctx.device, non_blocking=True), h[1], h[2], h[3], 1) for h in v]
+                for k, v in self.host_inputs.items()}
+
+    def _export(self, cts, sid):
+        outs = []
+        for i, c in enumerate(cts):
+            outs.append(self.ctx.export_c2m(c, self.Lconv, self.mask_seed, sid + i))
+        return outs
+
+    def _complex_pairs(self, ys):
+        out = [self.ctx.complexify(ys[2 * i], ys[2 * i + 1]) for i in range(len(ys) // 2)]
+        if len(ys) % 2:
+            out.append(ys[-1])
+        return out
+
+    def step(self, inp):
+        """One pass of the hot path.  Returns the exported (masked ct, server share) list."""
+        ctx, keys = self.ctx, self.keys
+        y = self.qkv.matmul(keys, inp["x"], self.w_qkv, self.wsc_qkv)
+        if self.workload == "qkv":
+            return [(c.data, None) for c in y]
+        nqk = self.nqk
+        Q, K, V = y[:nqk], y[nqk:2 * nqk], y[2 * nqk:]
+        S = self.attn.score(keys, Q, K)
+        ex = self._export(self.attn.export_stream(keys, S), 0)
+        O = self.attn.value(keys, inp["p"], V)
+        Ore = []
+        for o in O:                        # decomplexify the value output (G11): Re o = (o + conj o) / 2
+            z = ctx.add(o, ctx.conjugate(keys, o))
+            z.scale = o.scale * 2.0
+            Ore.append(z)
+        xo = self._complex_pairs(Ore)
+        yo = self.oproj.matmul(keys, xo, self.w_o, float(ctx.q[xo[0].n_limbs - 1]))
+        ex += self._export(self._complex_pairs(yo), 100)
+        g1 = self.ff1.matmul(keys, inp["f1"], self.w_1, float(ctx.q[L_FF - 1]))
+        ex += self._export(self._complex_pairs(g1), 200)
+        g2 = self.ff2.matmul(keys, inp["f2"], self.w_2, float(ctx.q[L_FF - 1]))
+        ex += self._export(self._complex_pairs(g2), 300)
+        return ex
+
+    def download(self, outs):
+        host = [(m.data.cpu(), s.cpu() if s is not None else None) for m, s in outs]
+        return sum(a.numel() * 8 + (b.numel() * 8 if b is not None else 0) for a, b in host)
+
+
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_init(args)
+    torch.cuda.set_device(local)
+    layer = Layer(local, args.workload, seed_off=rank)
+    ctx = layer.ctx
+    if args.workload == "ks":
+        return run_ks(args, layer, ws, rank)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        layer.step(layer.dev_inputs)
+    torch.cuda.synchronize()
+    ctx.stats_reset()
+    ctx.profile(True)
+    for k in ("diag_mac", "ks_inner", "ntt"):
+        ctx.profile_read(k)
+    barrier(ws)
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            layer.step(layer.dev_inputs)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms_total = ev0.elapsed_time(ev1)
+    ms_total = max_over_ranks(ms_total, ws)
+    ms_step = ms_total / args.steps
+    stats = ctx.stats()
+    prof = {k: ctx.profile_read(k) for k in ("diag_mac", "ks_inner", "ntt")}
+    ctx.profile(False)
+    # e2e through the public API: H2D of the step's encrypted inputs from pinned memory, D2H of the outputs
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        d2h = 0
+        for _ in range(args.steps):
+            inp = layer.upload()
+            d2h = layer.download(layer.step(inp))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
+        e2e = {"value": round(e_ms / ws, 3), "unit": "ms/layer", "h2d_bytes_per_step": layer.h2d_bytes, "d2h_bytes_per_step": d2h}
+    if rank != 0:
+        return
+    import json as _j
+    peaks = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    mac_ms, mac_n, mac_b = prof["diag_mac"]
+    ks_ms, ks_n, ks_b = prof["ks_inner"]
+    ntt_ms, ntt_n, ntt_b = prof["ntt"]
+    dom = {"kernel": "diag_mac", "ms": mac_ms, "n": mac_n, "bytes": mac_b}
+    achieved = (mac_b / mac_n) / ((mac_ms / mac_n) * 1e-3) / 1e9 if mac_n else 0.0
+    ks_total = stats["keyswitch"] / args.steps
+    line = {
+        "metric": "BERT-base layer CKKS linear latency (ms) & key-switches/s at N=2^16; HBM roofline %",
+        "value": round(ms_step / ws, 3),
+        "unit": "ms/layer",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3),
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u64",
+        "data": "synthetic (seeded; BERT-init random weights; encrypted U[-1,1] F=13 activations)",
+        "config": {"workload": "bert-base-layer" if args.workload == "layer" else "bert-base-qkv",
+                   "N": 65536, "m": M, "d": D, "H": H, "d_ff": DFF,
+                   "levels": {"qkv": L_QKV, "p_fd": L_V_P, "ff": L_FF, "conv": layer.Lconv},
+                   "params": "P16 (q0 60b + 23x40b, 8x60b special, alpha=8)",
+                   "parallelism": "replicas: one independent layer per GPU" if ws > 1 else "1 GPU",
+                   "l2": "no flush: per-step working set (~%d GB of plaintext diagonals) >> 126 MB L2" % round(
+                       (layer.w_qkv.numel() + sum(getattr(layer, w).numel() for w in ("w_o", "w_1", "w_2") if hasattr(layer, w))) * 8 / 1e9)},
+        "key_switches_per_s": round(ks_total / (ms_step * 1e-3), 1),
+        "key_switches_per_step": ks_total,
+        "gpu_launches": int(stats["kernel_launches"]),
+        "kernel_time_ms_per_step": {"diag_mac": round(mac_ms / args.steps, 3), "ks_inner": round(ks_ms / args.steps, 3),
+                                    "ntt": round(ntt_ms / args.steps, 3)},
+        "roofline": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                     "frac": round(achieved / hbm, 4), "traffic": None,
+                     "note": "algorithmic bytes per launch (plaintext stream + bank + accumulators) / CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs"},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "setup_s": round(layer.setup_s, 1),
+    }
+    line["cpu_baseline"] = cpu_baseline(layer, stats, args.steps)
+    print(json.dumps(line), flush=True)
+
+
+def run_ks(args, layer, ws, rank):
+    """Config 2 microbench: hoisted rotations at L = 24 (dnum = 3)."""
+    raise SystemExit("ks workload: see bench_ks.py")
+
+
+# ------------------------------------------------------------------------------------ CPU baseline (the oracle)
+def oracle_sample():
+    """Time the oracle (as it stands) on a bounded sample of the layer: one hoisted rotation and one
+    single rotation at L = 8 of P16 plus one 64-term plaintext MAC unit.  Returns per-op seconds."""
+    from oracle import ckks as O
+    from oracle import kernels as K
+    import synth
+    P = O.Params("P16")
+    L = L_QKV
+    g = [O.galois_rot(P, 128), O.galois_rot(P, 256)]
+    t0 = time.time()
+    keys = O.Keys(P, synth.SEED_KEYS, galois=g, max_level=L)
+    t_keys = time.time() - t0
+    ct = O.encrypt_sk(P, keys, O.encode(P, synth.uniform(P.n, 1), 2.0 ** 40, L), 1)
+    t0 = time.time()
+    O.rotate_hoisted(P, keys, ct, [128])
+    t_hoist = time.time() - t0
+    t0 = time.time()
+    O.rotate(P, keys, ct, 256)
+    t_rot = time.time() - t0
+    ev = K.Ev(P, keys, M)
+    pts = [O.Pt(O.sample_uniform(5, 7 + i, P.q[:L], list(range(L)), P.N), 2.0 ** 40) for i in range(8)]
+    t0 = time.time()
+    ev.mac_ptmul([ct] * 8, pts)
+    t_mac8 = time.time() - t0
+    return {"keygen_s": t_keys, "rot_hoisted_s": t_hoist, "rot_single_s": t_rot, "ptmul_term_s": t_mac8 / 8}
+
+
+def cpu_baseline(layer, stats, steps):
+    s = oracle_sample()
+    ks = stats["keyswitch"] / steps
+    terms = stats["ptmul_terms"] / steps
+    est = ks * s["rot_single_s"] + terms * s["ptmul_term_s"]
+    return {"value": round(est * 1e3, 1), "unit": "ms/layer", "cores": os.cpu_count(), "kind": "oracle",
+            "sample": "oracle timed on 1 single + 1 hoisted rotation (L=8, P16) and 8 plaintext MAC terms; layer value "
+                      "EXTRAPOLATED with the layer's counts (%d key switches, %d pt-mul terms); per-op s: %s" % (
+                          ks, terms, json.dumps({k: round(v, 3) for k, v in s.items()}))}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (CPU) on the same workload, bounded sample per step."""
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        pass
+    times = []
+    samples = []
+    for _ in range(args.steps):
+        t0 = time.time()
+        s = oracle_sample()
+        times.append(time.time() - t0)
+        samples.append(s)
+    s = samples[-1]
+    # the layer's counts (from the schedule; identical to the library's counters)
+    ks, terms = LAYER_COUNTS["keyswitch"], LAYER_COUNTS["ptmul_terms"]
+    est_ms = (ks * s["rot_single_s"] + terms * s["ptmul_term_s"]) * 1e3
+    line = {"impl": "reference", "metric": "BERT-base layer CKKS linear latency (ms) & key-switches/s at N=2^16; HBM roofline %",
+            "value": round(est_ms, 1), "unit": "ms/layer", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(statistics.mean(times) * 1e3, 1), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+            "config": {"workload": "bert-base-layer", "N": 65536, "m": M, "d": D, "H": H, "d_ff": DFF},
+            "cpu_baseline": {"value": round(est_ms, 1), "unit": "ms/layer", "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": "per step: 1 single + 1 hoisted rotation (L=8) + 8 MAC terms; layer EXTRAPOLATED from "
+                                       "%d key switches and %d pt-mul terms" % (ks, terms)},
+            "e2e": {"value": round(est_ms, 1), "unit": "ms/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# schedule counts of one layer (filled from a GPU run's encf_stats; used only by --impl reference)
+LAYER_COUNTS = {"keyswitch": 2014, "ptmul_terms": 31200}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

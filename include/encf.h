@@ -85,6 +85,13 @@ const char* encf_status_string(encf_status s);
 const char* encf_last_error(void);                 /* thread-local detail of the last failure */
 encf_status encf_stats(encf_ctx* ctx, encf_counters* out);
 encf_status encf_stats_reset(encf_ctx* ctx);
+/* Live kernel timing: while enabled, CUDA events are recorded on the launching stream around every
+ * launch of the instrumented kernels ("diag_mac", "ks_inner", "ntt" = one fwd/inv transform pair of
+ * launches).  encf_profile_read synchronises on those events and returns the summed device time,
+ * the launch count and the summed ALGORITHMIC bytes for `kernel`, then
+ * forgets them. */
+encf_status encf_profile_enable(encf_ctx* ctx, int enable);
+encf_status encf_profile_read(encf_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches, uint64_t* alg_bytes);
 
 /* ------------------------------------------------------------------------------------------ keys (testing helpers) */
 #define ENCF_KEY_RELIN 1u

@@ -455,33 +455,21 @@ encf_status encf_proj_encode_weights(encf_ctx* c, const encf_proj_plan* p, const
         level_ok(c, nl);
         cudaStream_t s = S(stream);
         Scratch sc(s);
-        const int n = c->N / 2, N = c->N, C = p->C, m = p->m;
-        std::vector<double> re(n), im(n);
-        double* dre = (double*)sc.get(n);
-        double* dim = (double*)sc.get(n);
+        const int N = c->N;
         const double scale = (double)c->mods[nl - 1];
+        double* dW = (double*)sc.get((size_t)p->d_in * p->d_out);
+        CUDA_TRY(cudaMemcpyAsync(dW, W, (size_t)p->d_in * p->d_out * 8, cudaMemcpyHostToDevice, s));
+        std::vector<int> bs, ps, us, qs;
         for (int b = 0; b < p->B_out; b++)
             for (int pp = 0; pp < p->N2; pp++)
                 for (int u = 0; u < p->U; u++)
-                    for (int q = 0; q < p->N1; q++) {
-                        // w~^(b)_{u,p,q}(c) = Wbar[(2u)C+alpha, bC+beta] - i Wbar[(2u+1)C+alpha, bC+beta]
-                        std::fill(re.begin(), re.end(), 0.0);
-                        std::fill(im.begin(), im.end(), 0.0);
-                        for (int cc = 0; cc < C; cc++) {
-                            int al = (cc + q) % C, be = ((cc - pp * p->N1) % C + C) % C;
-                            int col = b * C + be;
-                            if (col >= p->d_out) continue;
-                            int r0 = 2 * u * C + al, r1 = (2 * u + 1) * C + al;
-                            double wr = r0 < p->d_in ? W[(size_t)r0 * p->d_out + col] : 0.0;
-                            double wi = r1 < p->d_in ? -W[(size_t)r1 * p->d_out + col] : 0.0;
-                            for (int r = 0; r < m; r++) { re[(size_t)cc * m + r] = wr; im[(size_t)cc * m + r] = wi; }
-                        }
-                        size_t idx = (((size_t)b * p->N2 + pp) * p->U + u) * p->N1 + q;
-                        u64* o = w_out + idx * nl * N;
-                        CUDA_TRY(cudaMemcpyAsync(dre, re.data(), n * 8, cudaMemcpyHostToDevice, s));
-                        CUDA_TRY(cudaMemcpyAsync(dim, im.data(), n * 8, cudaMemcpyHostToDevice, s));
-                        k_encode_slots(*c, dre, dim, n, scale, nl, o, s);   // synchronises the stream
-                    }
+                    for (int q = 0; q < p->N1; q++) { bs.push_back(b); ps.push_back(pp); us.push_back(u); qs.push_back(q); }
+        const int BATCH = 32;
+        for (size_t i0 = 0; i0 < bs.size(); i0 += BATCH) {
+            int cnt = (int)std::min((size_t)BATCH, bs.size() - i0);
+            k_encode_weights(*c, dW, p->d_in, p->d_out, p->C, p->N1, p->m, &bs[i0], &ps[i0], &us[i0], &qs[i0], cnt, scale, nl,
+                             w_out + i0 * nl * N, s);
+        }
         size_t np = (size_t)p->B_out * p->N2 * p->U * p->N1;
         for (size_t i0 = 0; i0 < np; i0 += 4096) {
             int cnt = (int)std::min((size_t)4096, np - i0);

@@ -214,3 +214,58 @@ encf_status ctx_destroy_impl(encf_ctx* c) {
     delete c;
     return ENCF_OK;
 }
+
+cudaEvent_t encf_ctx::prof_event() {
+    if (!ev_pool.empty()) { cudaEvent_t e = ev_pool.back(); ev_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    return e;
+}
+
+void encf_ctx::prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int& slot) {
+    slot = -1;
+    if (!prof) return;
+    std::lock_guard<std::mutex> lk(mu);
+    ProfRec r{name, prof_event(), prof_event(), bytes};
+    CUDA_TRY(cudaEventRecord(r.a, s));
+    prof_recs.push_back(r);
+    slot = (int)prof_recs.size() - 1;
+}
+
+void encf_ctx::prof_end(int slot, cudaStream_t s) {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(mu);
+    CUDA_TRY(cudaEventRecord(prof_recs[slot].b, s));
+}
+
+extern "C" encf_status encf_profile_enable(encf_ctx* c, int enable) {
+    if (!c) return ENCF_ERR_ARG;
+    c->prof = enable != 0;
+    return ENCF_OK;
+}
+
+extern "C" encf_status encf_profile_read(encf_ctx* c, const char* kernel, double* total_ms, uint64_t* launches,
+                                         uint64_t* alg_bytes) {
+    if (!c || !kernel || !total_ms || !launches || !alg_bytes) return ENCF_ERR_ARG;
+    try {
+        std::lock_guard<std::mutex> lk(c->mu);
+        double ms = 0.0;
+        uint64_t n = 0, by = 0;
+        std::vector<encf_ctx::ProfRec> keep;
+        for (auto& r : c->prof_recs) {
+            if (r.name != kernel) { keep.push_back(r); continue; }
+            CUDA_TRY(cudaEventSynchronize(r.b));
+            float t = 0.f;
+            CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+            ms += t; n++; by += r.bytes;
+            c->ev_pool.push_back(r.a);
+            c->ev_pool.push_back(r.b);
+        }
+        c->prof_recs = keep;
+        *total_ms = ms; *launches = n; *alg_bytes = by;
+        return ENCF_OK;
+    } catch (const EncfError& e) {
+        set_last_error(e.msg);
+        return e.code;
+    }
+}

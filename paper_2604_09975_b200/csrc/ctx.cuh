@@ -88,6 +88,14 @@ struct encf_ctx {
     std::map<MaskKey, u64*> masks;      // NTT-form mask plaintexts [level][N]
     std::vector<int> rot_group;         // 5^j mod 2N (host, for encode)
     int* d_rot_group = nullptr;
+    // live kernel timing (encf_profile_*): CUDA events recorded around selected launches
+    struct ProfRec { std::string name; cudaEvent_t a, b; uint64_t bytes; };
+    bool prof = false;
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t prof_event();
+    void prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int& slot);
+    void prof_end(int slot, cudaStream_t s);
     // statistics
     std::atomic<uint64_t> st_ks{0}, st_modup{0}, st_ntt{0}, st_ptmul{0}, st_ctmul{0}, st_launch{0}, st_bytes{0};
 
@@ -169,6 +177,8 @@ void k_masked_sum(encf_ctx& c, const u64* const* cts, const u64* const* masks, i
 void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s);
 void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_slots, double scale, int level,
                     u64* out, cudaStream_t s);
+void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
+                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s);
 void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ ciphertext-level ops (ks.cu)

@@ -181,8 +181,11 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     dim3 gA(S / CT, b.map.n, b.npolys);
     int G = kTileElems / S < R ? kTileElems / S : R;
     dim3 gB(R / G, b.map.n, b.npolys);
+    int slot;
+    c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
     ntt_cols<false><<<gA, kThreads, 0, s>>>(a);
     ntt_rows<false><<<gB, kThreads, 0, s>>>(a);
+    c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;
     c.st_bytes += (uint64_t)b.npolys * b.map.n * c.N * 8 * 4;
@@ -197,8 +200,11 @@ void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     dim3 gA(S / CT, b.map.n, b.npolys);
     int G = kTileElems / S < R ? kTileElems / S : R;
     dim3 gB(R / G, b.map.n, b.npolys);
+    int slot;
+    c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
     ntt_rows<true><<<gB, kThreads, 0, s>>>(a);
     ntt_cols<true><<<gA, kThreads, 0, s>>>(a);
+    c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;
     c.st_bytes += (uint64_t)b.npolys * b.map.n * c.N * 8 * 4;

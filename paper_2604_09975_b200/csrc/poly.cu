@@ -371,6 +371,7 @@ __global__ void export_mask_kernel(u64 seed, u64 stream, u64* c0, u64* share, in
 // S_k = sum_e A[e] exp(sign * 2 pi i e k / 2N): iterative radix-2 FFT of length 2N in global memory
 // (preprocessing only: weights and masks are encoded once).
 __global__ void fft_bitrev_kernel(double2* a, int n2, int logn2) {
+    a += (size_t)blockIdx.y * n2;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += gridDim.x * blockDim.x) {
         int j = (int)(__brev((unsigned)i) >> (32 - logn2));
         if (i < j) { double2 t = a[i]; a[i] = a[j]; a[j] = t; }
@@ -378,6 +379,7 @@ __global__ void fft_bitrev_kernel(double2* a, int n2, int logn2) {
 }
 
 __global__ void fft_stage_kernel(double2* a, int n2, int len, double sign) {
+    a += (size_t)blockIdx.y * n2;
     int half = len / 2;
     for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < n2 / 2; b += gridDim.x * blockDim.x) {
         int grp = b / half, j = b % half;
@@ -397,6 +399,8 @@ __global__ void scatter_slots_kernel(const double* re, const double* im, int n_s
 }
 
 __global__ void round_reduce_kernel(const double2* S, double f, int N, int level, const ModConst* mod, u64* out, int* overflow) {
+    S += (size_t)blockIdx.y * 2 * N;
+    out += (size_t)blockIdx.y * level * N;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         double v = rint(f * S[k].x);   // round half to even
         if (fabs(v) >= 4611686018427387904.0) { *overflow = 1; v = 0; }
@@ -429,10 +433,37 @@ __global__ void gather_slots_kernel(const double2* Z, const int* rg, int n, doub
     }
 }
 
-void fft2n(encf_ctx& c, double2* A, double sign, cudaStream_t s) {
+void fft2n(encf_ctx& c, double2* A, double sign, cudaStream_t s, int batch = 1) {
     int n2 = 2 * c.N, logn2 = c.logN + 1;
-    fft_bitrev_kernel<<<nblocks(n2), TB, 0, s>>>(A, n2, logn2);
-    for (int len = 2; len <= n2; len <<= 1) fft_stage_kernel<<<nblocks(n2 / 2), TB, 0, s>>>(A, n2, len, sign);
+    dim3 g1(nblocks(n2, TB, 512), batch), g2(nblocks(n2 / 2, TB, 256), batch);
+    fft_bitrev_kernel<<<g1, TB, 0, s>>>(A, n2, logn2);
+    for (int len = 2; len <= n2; len <<= 1) fft_stage_kernel<<<g2, TB, 0, s>>>(A, n2, len, sign);
+}
+
+// Projection weight diagonals straight into the FFT input: for plaintext (b,p,u,q) the
+// slot r + c m (c < C) holds Wbar[(2u)C + alpha, bC + beta] - i Wbar[(2u+1)C + alpha, bC + beta],
+// alpha = (c+q) mod C, beta = (c - p N1) mod C; A[5^j mod 2N] = slot j.
+struct WDiag { int b[64], p[64], u[64], q[64]; };
+__global__ void weight_slots_kernel(const double* __restrict__ W, int d_in, int d_out, int C, int N1, int m, WDiag wd,
+                                    const int* rg, double2* A, int N) {
+    const int bi = blockIdx.y;
+    double2* a = A + (size_t)bi * 2 * N;
+    const int b = wd.b[bi], p = wd.p[bi], u = wd.u[bi], q = wd.q[bi];
+    const int n = N / 2;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+        int c = j / m;
+        double re = 0.0, im = 0.0;
+        if (c < C) {
+            int al = (c + q) % C, be = ((c - p * N1) % C + C) % C;
+            int col = b * C + be;
+            if (col < d_out) {
+                int r0 = 2 * u * C + al, r1 = (2 * u + 1) * C + al;
+                if (r0 < d_in) re = W[(size_t)r0 * d_out + col];
+                if (r1 < d_in) im = -W[(size_t)r1 * d_out + col];
+            }
+        }
+        a[rg[j]] = make_double2(re, im);
+    }
 }
 
 }  // namespace
@@ -527,8 +558,12 @@ void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const
     int Lq = nl - c.K;
     for (int e = 0; e < nl; e++) em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
     dim3 grid((c.N + TB - 1) / TB, nl);
+    const uint64_t bytes = (uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8;   // digits + 2 key comps + 2 outputs
+    int slot;
+    c.prof_begin("ks_inner", s, bytes, slot);
     ks_inner_kernel<<<grid, TB, 0, s>>>(ext, dnum, nl, g, key, key_nl, kl, em, acc, c.N, c.logN, c.d_mod);
-    c.st_launch++; c.st_bytes += (size_t)dnum * nl * c.N * 8 * 3 + (size_t)2 * nl * c.N * 8;
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes;
 }
 
 void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level, const ModDownTab& t,
@@ -565,9 +600,15 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     int zsplit = 1;
     while ((size_t)tiles * level * zsplit < 148 * 4 && zsplit * MAC_LANES < units) zsplit *= 2;
     dim3 grid(tiles, level, zsplit);
+    // algorithmic bytes: plaintext stream + bank read once + accumulators written once
+    const uint64_t bytes = (uint64_t)units * nbank * level * c.N * 8 + (uint64_t)nbank * 2 * level * c.N * 8 +
+                           (uint64_t)units * 2 * level * c.N * 8;
+    int slot;
+    c.prof_begin("diag_mac", s, bytes, slot);
     diag_mac_kernel<<<grid, MAC_T * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs, level, c.N, c.d_mod);
+    c.prof_end(slot, s);
     c.st_launch++;
-    c.st_bytes += (size_t)units * nbank * level * c.N * 8 + (size_t)nbank * 2 * level * c.N * 8 + (size_t)units * 2 * level * c.N * 8;
+    c.st_bytes += bytes;
     c.st_ptmul += (uint64_t)units * nbank;
 }
 
@@ -586,6 +627,24 @@ void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots
     scatter_slots_kernel<<<GRID(n_slots), TB, 0, s>>>(re, im, n_slots, c.d_rot_group, A);
     fft2n(c, A, -1.0, s);
     round_reduce_kernel<<<GRID(c.N), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    int h_ovf = 0;
+    CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (h_ovf) throw EncfError(ENCF_ERR_OVERFLOW, "encode: |coefficient| >= 2^62");
+}
+
+void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
+                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s) {
+    Scratch sc(s);
+    double2* A = (double2*)sc.get((size_t)batch * 2 * c.N * 2);
+    int* ovf = (int*)sc.get(1);
+    CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * 2 * c.N * batch, s));
+    CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int), s));
+    WDiag wd;
+    for (int i = 0; i < batch; i++) { wd.b[i] = bs[i]; wd.p[i] = ps[i]; wd.u[i] = us[i]; wd.q[i] = qs[i]; }
+    weight_slots_kernel<<<dim3(nblocks(c.N / 2, TB, 256), batch), TB, 0, s>>>(dW, d_in, d_out, C, N1, m, wd, c.d_rot_group, A, c.N);
+    fft2n(c, A, -1.0, s, batch);
+    round_reduce_kernel<<<dim3(nblocks(c.N, TB, 256), batch), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
     int h_ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
