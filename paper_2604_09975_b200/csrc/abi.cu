@@ -497,13 +497,18 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
         proj_phase1(ev, *p, xs, w, w_scale, u0, u1, accs);
         int b_first = u0 / p->N2;
         bool fin = (flags & ENCF_PROJ_FINALIZE) && u0 == 0 && u1 == units;
-        for (size_t i = 0; i < accs.size(); i++) {
-            encf_ct* yo = &y[b_first + i];
-            if (fin) {
+        if (fin) {
+            std::vector<DCt> ys = ev.alloc_many((int)accs.size(), L - 1);
+            proj_finalize_many(ev, *p, accs, ys);
+            for (size_t i = 0; i < accs.size(); i++) {
+                encf_ct* yo = &y[b_first + i];
                 DCt o = outview(yo, L - 1, 2);
-                proj_finalize(ev, *p, accs[i], o);
+                ev.copy(ys[i], o);
                 writeback(yo, o);
-            } else {
+            }
+        } else {
+            for (size_t i = 0; i < accs.size(); i++) {
+                encf_ct* yo = &y[b_first + i];
                 DCt o = outview(yo, L, 2);
                 ev.copy(accs[i], o);
                 writeback(yo, o);
@@ -517,10 +522,13 @@ encf_status encf_pt_ct_matmul_finalize(encf_ctx* c, const encf_keys* k, const en
     return guard([&] {
         need(c && k && p && acc && y && 0 <= b0 && b0 < b1 && b1 <= p->B_out, ENCF_ERR_ARG, "finalize: bad argument");
         EV_BEGIN(k);
+        std::vector<DCt> accs;
+        for (int b = b0; b < b1; b++) accs.push_back(view(&acc[b - b0]));
+        std::vector<DCt> ys = ev.alloc_many(b1 - b0, accs[0].L - 1);
+        proj_finalize_many(ev, *p, accs, ys);
         for (int b = b0; b < b1; b++) {
-            DCt a = view(&acc[b - b0]);
-            DCt o = outview(&y[b - b0], a.L - 1, 2);
-            proj_finalize(ev, *p, a, o);
+            DCt o = outview(&y[b - b0], accs[0].L - 1, 2);
+            ev.copy(ys[b - b0], o);
             writeback(&y[b - b0], o);
         }
     });

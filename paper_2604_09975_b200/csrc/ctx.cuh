@@ -140,6 +140,29 @@ struct Scratch {   // stream-ordered device scratch, freed in the destructor (cu
     ~Scratch() { for (void* p : ptrs) cudaFreeAsync(p, s); }
 };
 
+// ------------------------------------------------------------------------------------ batched request tables
+// (passed BY VALUE as kernel parameters -- CUDA >= 12.1 allows 32 KB of parameters)
+constexpr int KS_BATCH = 128;
+struct KsInnerBatch {
+    const u64* ext[KS_BATCH];
+    const u64* key[KS_BATCH];
+    u64* acc[KS_BATCH];
+    uint32_t gather[KS_BATCH];
+};
+struct OutBatch {
+    u64* out[KS_BATCH][2];
+    const u64* add[KS_BATCH][2];
+};
+constexpr int CP_BATCH = 512;
+struct CopyBatch {
+    const u64* src[CP_BATCH];
+    uint32_t g[CP_BATCH];
+};
+struct KeyLimb { int kl[MAX_LIMBS]; };
+struct SumDev { const u64* ct; const u64* mask; };
+struct PairDev { const u64* a; const u64* b; i64 as, bs; };   // operands + component strides
+struct OutPos { int pos[MAX_LIMBS]; };
+
 // ------------------------------------------------------------------------------------ launchers (ntt.cu)
 void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
@@ -179,6 +202,20 @@ void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_s
                     u64* out, cudaStream_t s);
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
                       const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s);
+void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
+                      cudaStream_t s);
+void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
+                            const ModDownTab& t, cudaStream_t s);
+void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
+                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s);
+void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s);
+void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s);
+void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,
+                            cudaStream_t s);
+void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
+               cudaStream_t s);
+void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
+                  cudaStream_t s);
 void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ ciphertext-level ops (ks.cu)

@@ -1,12 +1,19 @@
-// encformer.cu -- the EncFormer CKKS kernels as schedules over the sm_100a primitives:
+// encformer.cu -- the EncFormer CKKS kernels as BATCHED schedules over the sm_100a primitives:
 //   projection (SCP pt-ct matmul),
 //   score (folded-diagonal QK^T) + minimal export stream,
 //   value (head-major PV),
 //   complex C2M export, GPU half (Alg 3; trimming P:863-878).
 // The schedules are exactly those of oracle/kernels.py (readings in DESIGN.md);
-// the parity tests compare every limb of every output.
+// independent ciphertexts (blocks, t, bank offsets) are processed in lockstep so that every launch
+// covers all of them.  The parity tests compare every limb of every output.
 #include <cmath>
 #include "encformer.cuh"
+
+static std::vector<const DCt*> ptrs(const std::vector<DCt>& v) {
+    std::vector<const DCt*> p;
+    for (auto& x : v) p.push_back(&x);
+    return p;
+}
 
 // ====================================================================================== projection
 void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C, int N1, uint32_t flags) {
@@ -39,98 +46,122 @@ std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p) {
     return g;
 }
 
-// C6 steps 1-3 for units [u0, u1) (row-major over (b, p)); writes acc_b (level L) for every touched b
-// into accs[b - b_first].  Step 1: hoisted baby-step bank.  Step 2: one fused MAC launch over the
-// plaintext stream.  Step 3: giant-step single rotations and adds.
+// C6 steps 1-3 for units [u0, u1) (row-major over (b, p)); accs[b - b_first] = acc_b (level L).
+//  1. bank[u][q] = HOISTED rot(x~_u, q m)            (one ModUp per input, all rotations in one batch)
+//  2. c~_{b,p} = sum_{u,q} bank[u][q] (.) w~_{b,p,u,q}  (one fused MAC launch over the plaintext stream)
+//  3. acc_b = c~_{b,0} + sum_{p>=1} rot(c~_{b,p}, p N1 m) (all giant rotations in one batch, one sum)
 void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs) {
     const int N = ev.c.N, L = x[0].L, U = p.U, N1 = p.N1;
-    for (auto& xi : x)
+    for (auto& xi : x) {
         if (xi.L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "projection inputs at different levels");
-    for (auto& xi : x) check_scale(xi.scale, x[0].scale);
+        check_scale(xi.scale, x[0].scale);
+    }
     const size_t ctw = ev.ct_words(L);
-    u64* bank = ev.sc.get(ctw * U * N1);
-    for (int u = 0; u < U; u++) {
-        std::vector<uint32_t> gs;
-        std::vector<DCt> outs;
+    std::vector<DCt> bankv = ev.alloc_many(U * N1, L);
+    std::vector<std::vector<uint32_t>> gs(U);
+    std::vector<std::vector<DCt>> outs(U);
+    for (int u = 0; u < U; u++)
         for (int q = 0; q < N1; q++) {
-            DCt o; o.d = bank + ctw * (u * N1 + q); o.L = L;
-            outs.push_back(o);
-            gs.push_back(q == 0 ? 1u : ev.galois_rot((long)q * p.m));
+            gs[u].push_back(q == 0 ? 1u : ev.galois_rot((long)q * p.m));
+            outs[u].push_back(bankv[u * N1 + q]);
         }
-        ev.rotate_hoisted(x[u], gs, outs);
-    }
+    ev.hoisted_many(ptrs(x), gs, outs);
     const int units = u1 - u0;
-    u64* cacc = ev.sc.get(ctw * units);
+    std::vector<DCt> cu = ev.alloc_many(units, L);
     const i64 wus = (i64)U * N1 * L * N;
-    k_diag_mac(ev.c, bank, U * N1, w + (size_t)u0 * wus, units, wus, cacc, (i64)ctw, L, ev.s);
+    k_diag_mac(ev.c, bankv[0].d, U * N1, w + (size_t)u0 * wus, units, wus, cu[0].d, (i64)ctw, L, ev.s);
     const double sc = x[0].scale * w_scale;
-    int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;
-    accs.assign(b_last - b_first + 1, DCt());
-    std::vector<bool> init(accs.size(), false);
-    DCt tmp = ev.alloc(L);
+    for (auto& c : cu) c.scale = sc;
+    std::vector<const DCt*> rin;
+    std::vector<uint32_t> rg;
+    std::vector<int> ridx;
     for (int un = u0; un < u1; un++) {
-        int b = un / p.N2, pp = un % p.N2;
-        DCt cu; cu.d = cacc + ctw * (un - u0); cu.L = L; cu.scale = sc;
-        DCt& a = accs[b - b_first];
-        if (!init[b - b_first]) {
-            a = ev.alloc(L, 2, sc);
-            if (pp) ev.rotate_galois(cu, ev.galois_rot((long)pp * N1 * p.m), a);
-            else ev.copy(cu, a);
-            init[b - b_first] = true;
-        } else {
-            if (pp) { ev.rotate_galois(cu, ev.galois_rot((long)pp * N1 * p.m), tmp); ev.add(a, tmp, a); }
-            else ev.add(a, cu, a);
-        }
+        int pp = un % p.N2;
+        if (pp) { rin.push_back(&cu[un - u0]); rg.push_back(ev.galois_rot((long)pp * N1 * p.m)); ridx.push_back(un - u0); }
     }
+    std::vector<DCt> rot = ev.alloc_many((int)rin.size(), L);
+    ev.rotate_many(rin, rg, rot);
+    std::vector<const DCt*> term_of(units, nullptr);
+    for (int un = 0; un < units; un++) term_of[un] = &cu[un];
+    for (size_t i = 0; i < ridx.size(); i++) term_of[ridx[i]] = &rot[i];
+    int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;
+    std::vector<std::vector<SumTerm>> terms(b_last - b_first + 1);
+    for (int un = u0; un < u1; un++) terms[un / p.N2 - b_first].push_back(SumTerm{term_of[un - u0]->d, nullptr});
+    accs = ev.alloc_many((int)terms.size(), L);
+    ev.sum_many(terms, L, 2, accs, std::vector<double>(terms.size(), sc));
 }
 
-// C6 steps 4-5: z = acc + conj(acc) (scale x2, G2/G3), y = rescale(z).
-void proj_finalize(Ev& ev, const encf_proj_plan& p, const DCt& acc, DCt& y) {
-    DCt z = ev.alloc(acc.L);
+// C6 steps 4-5 for a list of accumulators: z = acc + conj(acc) (scale x2, G2/G3), y = rescale(z).
+void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs, std::vector<DCt>& ys) {
+    const int n = (int)accs.size();
+    const int L = accs[0].L;
+    std::vector<DCt> z = ev.alloc_many(n, L);
     if (p.flags & ENCF_PROJ_DECOMPLEXIFY) {
-        ev.rotate_galois(acc, ev.galois_conj(), z);
-        ev.add(acc, z, z);
-        z.scale = acc.scale * 2.0;
+        std::vector<DCt> cj = ev.alloc_many(n, L);
+        ev.rotate_many(ptrs(accs), std::vector<uint32_t>(n, ev.galois_conj()), cj);
+        std::vector<std::vector<SumTerm>> t(n);
+        std::vector<double> sc(n);
+        for (int i = 0; i < n; i++) {
+            check_scale(accs[i].scale, cj[i].scale);
+            t[i] = {SumTerm{accs[i].d, nullptr}, SumTerm{cj[i].d, nullptr}};
+            sc[i] = accs[i].scale * 2.0;
+        }
+        ev.sum_many(t, L, 2, z, sc);
     } else {
-        ev.copy(acc, z);
+        for (int i = 0; i < n; i++) ev.copy(accs[i], z[i]);
     }
-    ev.rescale(z, y);
+    ev.rescale_many(ptrs(z), ys);
 }
 
 // ====================================================================================== shifts (App. A.1)
-// Psi^t for all t in ts from one hoisted ModUp of x (Alg A.2): rot(x,t)(.)h_t + rot(x,t-m)(.)u_t, rescale;
-// t = 0: x(.)h_0, rescale.  Optional segment restriction [seg0, seg0+nseg).
-void psi_hoisted(Ev& ev, const DCt& x, const std::vector<int>& ts, int m, int N_seg, int seg0, int nseg,
-                 std::vector<DCt>& outs) {
-    const int L = x.L;
-    std::vector<int> tt;
-    std::vector<uint32_t> gs;
-    for (int t : ts) {
-        int r = ((t % m) + m) % m;
-        tt.push_back(r);
-        if (r) { gs.push_back(ev.galois_rot(r)); gs.push_back(ev.galois_rot(r - m)); }
-    }
-    std::vector<DCt> rots(gs.size());
-    for (auto& r : rots) r = ev.alloc(L);
-    if (!gs.empty()) ev.rotate_hoisted(x, gs, rots);
-    outs.resize(ts.size());
-    size_t i = 0;
-    const double ms = ev.mask_scale(L);
-    for (size_t k = 0; k < tt.size(); k++) {
-        int t = tt[k];
-        const u64* hm = ev.mask(m, 0, m - t, seg0, 1, nseg, L);
-        DCt y = ev.alloc(L);
-        if (t == 0) {
-            ev.masked_sum({&x}, {hm}, ms, y);
-        } else {
-            const u64* um = ev.mask(m, m - t, m, seg0, 1, nseg, L);
-            ev.masked_sum({&rots[i], &rots[i + 1]}, {hm, um}, ms, y);
-            i += 2;
+// Psi^t of xs[i] for every t in ts[i] (Alg A.2): one hoisted ModUp per input, rot(x,t)(.)h_t +
+// rot(x,t-m)(.)u_t, rescale; t = 0: x(.)h_0, rescale.  Segment restriction [seg0, seg0+nseg) of the masks.
+void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
+              std::vector<std::vector<DCt>>& outs) {
+    const int n = (int)xs.size();
+    const int L = xs[0]->L;
+    std::vector<std::vector<uint32_t>> gs(n);
+    std::vector<std::vector<int>> tt(n);
+    for (int i = 0; i < n; i++)
+        for (int t : ts[i]) {
+            int r = ((t % m) + m) % m;
+            tt[i].push_back(r);
+            if (r) { gs[i].push_back(ev.galois_rot(r)); gs[i].push_back(ev.galois_rot(r - m)); }
         }
-        outs[k] = ev.alloc(L - 1);
-        ev.rescale(y, outs[k]);
+    std::vector<std::vector<DCt>> rots(n);
+    int nrot = 0;
+    for (int i = 0; i < n; i++) nrot += (int)gs[i].size();
+    std::vector<DCt> rall = ev.alloc_many(nrot, L);
+    int k = 0;
+    for (int i = 0; i < n; i++)
+        for (size_t j = 0; j < gs[i].size(); j++) rots[i].push_back(rall[k++]);
+    ev.hoisted_many(xs, gs, rots);
+    const double ms = ev.mask_scale(L);
+    std::vector<std::vector<SumTerm>> terms;
+    std::vector<double> scs;
+    for (int i = 0; i < n; i++) {
+        size_t r = 0;
+        for (int t : tt[i]) {
+            const u64* hm = ev.mask(m, 0, m - t, seg0, 1, nseg, L);
+            if (t == 0) {
+                terms.push_back({SumTerm{xs[i]->d, hm}});
+            } else {
+                const u64* um = ev.mask(m, m - t, m, seg0, 1, nseg, L);
+                terms.push_back({SumTerm{rots[i][r].d, hm}, SumTerm{rots[i][r + 1].d, um}});
+                r += 2;
+            }
+            scs.push_back(xs[i]->scale * ms);
+        }
     }
+    std::vector<DCt> y = ev.alloc_many((int)terms.size(), L);
+    ev.sum_many(terms, L, 2, y, scs);
+    std::vector<DCt> o = ev.alloc_many((int)terms.size(), L - 1);
+    ev.rescale_many(ptrs(y), o);
+    outs.assign(n, {});
+    k = 0;
+    for (int i = 0; i < n; i++)
+        for (size_t j = 0; j < tt[i].size(); j++) outs[i].push_back(o[k++]);
 }
 
 // ====================================================================================== attention plans
@@ -175,26 +206,43 @@ std::vector<uint32_t> attn_galois(Ev& ev, const encf_attn_plan& a) {
     return g;
 }
 
-// out[h] = sum_{j<k} x[h + jH] by binary rotate-add (G7; oracle kernels.route).
-static DCt route(Ev& ev, const DCt& x, int k, int H, int m) {
-    DCt result, pw = x;
+// out[h] = sum_{j<k} x[h + jH] by binary rotate-add (G7; oracle kernels.route), all xs in lockstep.
+static std::vector<DCt> route_many(Ev& ev, const std::vector<DCt>& xs, int k, int H, int m) {
+    const int n = (int)xs.size(), L = xs[0].L;
+    std::vector<DCt> result(n), pw = xs;
     bool have = false;
     int offset = 0, cnt = 1, kk = k;
-    DCt tmp = ev.alloc(x.L);
     while (kk) {
         if (kk & 1) {
-            DCt y;
-            if (offset) { y = ev.alloc(x.L); ev.rotate_galois(pw, ev.galois_rot((long)offset * H * m), y); }
-            else y = pw;
-            if (!have) { result = ev.alloc(x.L); ev.copy(y, result); have = true; }
-            else ev.add(result, y, result);
+            std::vector<DCt> y;
+            if (offset) {
+                y = ev.alloc_many(n, L);
+                ev.rotate_many(ptrs(pw), std::vector<uint32_t>(n, ev.galois_rot((long)offset * H * m)), y);
+            } else {
+                y = pw;
+            }
+            if (!have) {
+                result = y;
+                have = true;
+            } else {
+                std::vector<std::vector<SumTerm>> t(n);
+                std::vector<double> sc(n);
+                for (int i = 0; i < n; i++) { check_scale(result[i].scale, y[i].scale); t[i] = {{result[i].d, nullptr}, {y[i].d, nullptr}}; sc[i] = y[i].scale; }
+                std::vector<DCt> r2 = ev.alloc_many(n, L);
+                ev.sum_many(t, L, 2, r2, sc);
+                result = r2;
+            }
             offset += cnt;
         }
         kk >>= 1;
         if (kk) {
-            DCt npw = ev.alloc(x.L);
-            ev.rotate_galois(pw, ev.galois_rot((long)cnt * H * m), tmp);
-            ev.add(pw, tmp, npw);
+            std::vector<DCt> rt = ev.alloc_many(n, L);
+            ev.rotate_many(ptrs(pw), std::vector<uint32_t>(n, ev.galois_rot((long)cnt * H * m)), rt);
+            std::vector<std::vector<SumTerm>> t(n);
+            std::vector<double> sc(n);
+            for (int i = 0; i < n; i++) { t[i] = {{pw[i].d, nullptr}, {rt[i].d, nullptr}}; sc[i] = pw[i].scale; }
+            std::vector<DCt> npw = ev.alloc_many(n, L);
+            ev.sum_many(t, L, 2, npw, sc);
             pw = npw;
             cnt *= 2;
         }
@@ -205,139 +253,162 @@ static DCt route(Ev& ev, const DCt& x, int k, int H, int m) {
 // ====================================================================================== score (C7)
 void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, const std::vector<DCt>& ks, int t0, int t1,
                std::vector<DCt>& S) {
-    const int m = a.m, H = a.H, beta = a.beta, g = a.g, Ns = a.N_seg;
-    std::vector<std::vector<DCt>> qb(a.B);
-    std::vector<std::vector<DCt>> kb(a.B);
+    const int m = a.m, H = a.H, beta = a.beta, g = a.g, N = ev.c.N;
     std::vector<int> qts, kts;
     for (int s = 0; s < beta; s++) qts.push_back(-s);
     for (int j = 0; j < g / 2; j++) kts.push_back(j * beta);
     for (int j = 0; j < g / 2; j++) kts.push_back(m / 2 + j * beta);
-    for (int l = 0; l < a.B; l++) {
-        psi_hoisted(ev, qs[l], qts, m, Ns, 0, Ns, qb[l]);
-        psi_hoisted(ev, ks[l], kts, m, Ns, 0, Ns, kb[l]);
-    }
-    const int Lb = qb[0][0].L;
-    S.resize(t1 - t0);
+    // Q and K banks of every block from one hoisted batch
+    std::vector<const DCt*> xs;
+    std::vector<std::vector<int>> ts;
+    for (int l = 0; l < a.B; l++) { xs.push_back(&qs[l]); ts.push_back(qts); }
+    for (int l = 0; l < a.B; l++) { xs.push_back(&ks[l]); ts.push_back(kts); }
+    std::vector<std::vector<DCt>> bank;
+    psi_many(ev, xs, ts, m, 0, a.N_seg, bank);
+    const int Lb = bank[0][0].L;
+    // k_{j beta} + i k_{m/2 + j beta} for every (l, j)
+    std::vector<std::vector<DCt>> kc(a.B);
+    for (int l = 0; l < a.B; l++)
+        for (int j = 0; j < g / 2; j++) {
+            DCt im = ev.alloc(Lb), o = ev.alloc(Lb);
+            ev.mul_i(bank[a.B + l][g / 2 + j], im);
+            ev.add(bank[a.B + l][j], im, o);
+            kc[l].push_back(o);
+        }
+    const int nt = t1 - t0;
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(nt);
     for (int t = t0; t < t1; t++) {
         int j = t / beta, s = t % beta;
-        std::vector<DCt> kc(a.B);
-        std::vector<const DCt*> A, B;
-        for (int l = 0; l < a.B; l++) {
-            kc[l] = ev.alloc(Lb);
-            DCt im = ev.alloc(Lb);
-            ev.mul_i(kb[l][g / 2 + j], im);        // k_{m/2 + j beta}
-            ev.add(kb[l][j], im, kc[l]);           // k_{j beta} + i k_{m/2 + j beta}
-            A.push_back(&qb[l][s]);
-            B.push_back(&kc[l]);
-        }
-        DCt T3 = ev.alloc(Lb, 3), T2 = ev.alloc(Lb), T = ev.alloc(Lb - 1);
-        ev.tensor_sum(A, B, T3);
-        ev.relin(T3, T2);
-        ev.rescale(T2, T);
-        DCt R = route(ev, T, a.C / H, H, m);
-        std::vector<DCt> o;
-        psi_hoisted(ev, R, {s}, m, Ns, 0, H, o);
-        S[t - t0] = o[0];
+        for (int l = 0; l < a.B; l++) pairs[t - t0].push_back({&bank[l][s], &kc[l][j]});
     }
+    std::vector<DCt> T3 = ev.alloc_many(nt, Lb, 3), T2 = ev.alloc_many(nt, Lb), T = ev.alloc_many(nt, Lb - 1);
+    ev.tensor_many(pairs, T3);
+    ev.relin_many(ptrs(T3), T2);
+    ev.rescale_many(ptrs(T2), T);
+    std::vector<DCt> R = route_many(ev, T, a.C / H, H, m);
+    std::vector<std::vector<int>> st(nt);
+    for (int t = t0; t < t1; t++) st[t - t0] = {t % beta};
+    std::vector<std::vector<DCt>> al;
+    psi_many(ev, ptrs(R), st, m, 0, H, al);
+    S.resize(nt);
+    for (int i = 0; i < nt; i++) S[i] = al[i][0];
+    (void)N;
 }
 
 // Minimal export stream (oracle kernels.score_export).
 void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S, std::vector<DCt>& outs) {
     const int m = a.m, H = a.H, n = a.n;
     const long seg = (long)H * m;
-    std::vector<std::vector<const DCt*>> terms(a.n_out);
-    std::vector<std::vector<const u64*>> masks(a.n_out);
-    std::vector<DCt> rots(S.size());
     const int L = S[0].L;
+    std::vector<const DCt*> rin;
+    std::vector<uint32_t> rg;
+    std::vector<int> ridx(S.size(), -1);
+    for (size_t t = 0; t < S.size(); t++) {
+        long o = ((long)t * seg) % n;
+        if (o) { ridx[t] = (int)rin.size(); rin.push_back(&S[t]); rg.push_back(ev.galois_rot(-o)); }
+    }
+    std::vector<DCt> rot = ev.alloc_many((int)rin.size(), L);
+    ev.rotate_many(rin, rg, rot);
+    std::vector<std::vector<SumTerm>> terms(a.n_out);
     for (size_t t = 0; t < S.size(); t++) {
         long start = (long)t * seg;
         long o = start % n;
-        if (o) { rots[t] = ev.alloc(L); ev.rotate_galois(S[t], ev.galois_rot(-o), rots[t]); }
-        else rots[t] = S[t];
+        const DCt* r = ridx[t] >= 0 ? &rot[ridx[t]] : &S[t];
         int k = (int)(start / n);
         long first = std::min(seg, n - o);
-        terms[k].push_back(&rots[t]);
-        masks[k].push_back(ev.mask(m, 0, m, (int)(o / m), 1, (int)(first / m), L));
-        if (first < seg) {
-            terms[k + 1].push_back(&rots[t]);
-            masks[k + 1].push_back(ev.mask(m, 0, m, 0, 1, (int)((seg - first) / m), L));
-        }
+        terms[k].push_back(SumTerm{r->d, ev.mask(m, 0, m, (int)(o / m), 1, (int)(first / m), L)});
+        if (first < seg) terms[k + 1].push_back(SumTerm{r->d, ev.mask(m, 0, m, 0, 1, (int)((seg - first) / m), L)});
     }
-    outs.resize(a.n_out);
-    for (int k = 0; k < a.n_out; k++) {
-        DCt y = ev.alloc(L);
-        ev.masked_sum(terms[k], masks[k], ev.mask_scale(L), y);
-        outs[k] = ev.alloc(L - 1);
-        ev.rescale(y, outs[k]);
-    }
+    std::vector<DCt> y = ev.alloc_many(a.n_out, L);
+    ev.sum_many(terms, L, 2, y, std::vector<double>(a.n_out, S[0].scale * ev.mask_scale(L)));
+    outs = ev.alloc_many(a.n_out, L - 1);
+    ev.rescale_many(ptrs(y), outs);
 }
 
 // ====================================================================================== value (C8)
 void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs,
                std::vector<DCt>& outs) {
-    const int m = a.m, Ns = a.N_seg, half = m / 2;
-    outs.resize(a.B_V);
-    for (int l = 0; l < a.B_V; l++) {
-        const DCt& v = vs[l];
-        const DCt& p = ps[l];
-        const int Lv = v.L;
-        // 1. uu = v (.) e_all - i (rot(v, m/2)(.)h + rot(v, -m/2)(.)u), one rescale
-        std::vector<DCt> rv = {ev.alloc(Lv), ev.alloc(Lv)};
-        ev.rotate_hoisted(v, {ev.galois_rot(half), ev.galois_rot(half - m)}, rv);
-        const double ms = ev.mask_scale(Lv);
-        DCt sh = ev.alloc(Lv), shi = ev.alloc(Lv), ve = ev.alloc(Lv), d = ev.alloc(Lv);
-        ev.masked_sum({&rv[0], &rv[1]}, {ev.mask(m, 0, m - half, 0, 1, Ns, Lv), ev.mask(m, m - half, m, 0, 1, Ns, Lv)}, ms, sh);
-        ev.masked_sum({&v}, {ev.mask(m, 0, m, 0, 1, Ns, Lv)}, ms, ve);
-        ev.mul_i(sh, shi);
-        ev.add(ve, shi, d, /*sub=*/true);
-        DCt uu = ev.alloc(Lv - 1);
-        ev.rescale(d, uu);
-        // 2. U bank u_t = Psi^t(uu)
-        std::vector<int> ts;
-        for (int t = 0; t < half; t++) ts.push_back(t);
-        std::vector<DCt> ub;
-        psi_hoisted(ev, uu, ts, m, Ns, 0, Ns, ub);
-        // 3. Phi bank of p_fd, delta in [-(d_h-1), m/2-1]
-        const int dmin = -(a.d_h - 1);
-        std::vector<uint32_t> gs;
-        for (int dd = dmin; dd < half; dd++) if (dd) gs.push_back(ev.galois_rot((long)dd * m));
-        std::vector<DCt> pbv(gs.size());
-        for (auto& x : pbv) x = ev.alloc(p.L);
-        ev.rotate_hoisted(p, gs, pbv);
-        auto pb = [&](int dd) -> const DCt* {
-            if (dd == 0) return &p;
-            int idx = dd - dmin - (dd > 0 ? 1 : 0);
-            return &pbv[idx];
-        };
-        // 4. b_t = sum_u Phi^{t-u}(p) (.) n_u, rescale
-        const int Lp = p.L;
-        std::vector<const u64*> nmask(a.d_h);
-        for (int u = 0; u < a.d_h; u++) nmask[u] = ev.mask(m, 0, m, u, a.seg_stride, a.H_blk, Lp);
-        std::vector<DCt> bt(half);
-        for (int t = 0; t < half; t++) {
-            std::vector<const DCt*> C;
-            for (int u = 0; u < a.d_h; u++) C.push_back(pb(t - u));
-            DCt y = ev.alloc(Lp);
-            ev.masked_sum(C, nmask, ev.mask_scale(Lp), y);
-            bt[t] = ev.alloc(Lp - 1);
-            ev.rescale(y, bt[t]);
-        }
-        // 5. o = sum_t u_t (x) b_t, one relin, rescale
-        const int Lb = bt[0].L;
-        std::vector<DCt> ud(half);
-        std::vector<const DCt*> A, B;
-        for (int t = 0; t < half; t++) {
-            if (ub[t].L > Lb) { ud[t] = ev.alloc(Lb); ev.mod_drop(ub[t], Lb, ud[t]); }
-            else ud[t] = ub[t];
-            A.push_back(&ud[t]);
-            B.push_back(&bt[t]);
-        }
-        DCt o3 = ev.alloc(Lb, 3), o2 = ev.alloc(Lb);
-        ev.tensor_sum(A, B, o3);
-        ev.relin(o3, o2);
-        outs[l] = ev.alloc(Lb - 1);
-        ev.rescale(o2, outs[l]);
+    const int m = a.m, Ns = a.N_seg, half = m / 2, BV = a.B_V, N = ev.c.N;
+    const int Lv = vs[0].L, Lp = ps[0].L;
+    // 1. uu = v (.) e_all - i (rot(v, m/2)(.)h + rot(v, -m/2)(.)u), one rescale
+    std::vector<std::vector<uint32_t>> g2(BV, {ev.galois_rot(half), ev.galois_rot(half - m)});
+    std::vector<std::vector<DCt>> rv(BV);
+    std::vector<DCt> rall = ev.alloc_many(2 * BV, Lv);
+    for (int l = 0; l < BV; l++) rv[l] = {rall[2 * l], rall[2 * l + 1]};
+    ev.hoisted_many(ptrs(vs), g2, rv);
+    const double ms = ev.mask_scale(Lv);
+    const u64* hm = ev.mask(m, 0, m - half, 0, 1, Ns, Lv);
+    const u64* um = ev.mask(m, m - half, m, 0, 1, Ns, Lv);
+    const u64* em = ev.mask(m, 0, m, 0, 1, Ns, Lv);
+    std::vector<std::vector<SumTerm>> t1;
+    std::vector<double> sc1;
+    for (int l = 0; l < BV; l++) {
+        t1.push_back({SumTerm{rv[l][0].d, hm}, SumTerm{rv[l][1].d, um}});
+        sc1.push_back(vs[l].scale * ms);
     }
+    for (int l = 0; l < BV; l++) { t1.push_back({SumTerm{vs[l].d, em}}); sc1.push_back(vs[l].scale * ms); }
+    std::vector<DCt> shve = ev.alloc_many(2 * BV, Lv);
+    ev.sum_many(t1, Lv, 2, shve, sc1);
+    std::vector<DCt> d = ev.alloc_many(BV, Lv);
+    for (int l = 0; l < BV; l++) {
+        DCt shi = ev.alloc(Lv);
+        ev.mul_i(shve[l], shi);
+        ev.add(shve[BV + l], shi, d[l], /*sub=*/true);
+    }
+    std::vector<DCt> uu = ev.alloc_many(BV, Lv - 1);
+    ev.rescale_many(ptrs(d), uu);
+    // 2. U bank u_t = Psi^t(uu), t < m/2
+    std::vector<int> tsv;
+    for (int t = 0; t < half; t++) tsv.push_back(t);
+    std::vector<std::vector<DCt>> ub;
+    psi_many(ev, ptrs(uu), std::vector<std::vector<int>>(BV, tsv), m, 0, Ns, ub);
+    // 3. Phi bank of p_fd: delta in [-(d_h-1), m/2-1] \ {0}, hoisted
+    const int dmin = -(a.d_h - 1);
+    std::vector<uint32_t> dg;
+    for (int dd = dmin; dd < half; dd++) if (dd) dg.push_back(ev.galois_rot((long)dd * m));
+    std::vector<std::vector<DCt>> pb(BV);
+    std::vector<DCt> pall = ev.alloc_many((int)dg.size() * BV, Lp);
+    for (int l = 0; l < BV; l++) pb[l].assign(pall.begin() + l * dg.size(), pall.begin() + (l + 1) * dg.size());
+    ev.hoisted_many(ptrs(ps), std::vector<std::vector<uint32_t>>(BV, dg), pb);
+    auto pbi = [&](int l, int dd) -> const DCt* {
+        if (dd == 0) return &ps[l];
+        return &pb[l][dd - dmin - (dd > 0 ? 1 : 0)];
+    };
+    // 4. b_t = sum_u Phi^{t-u}(p) (.) n_u, rescale
+    std::vector<const u64*> nmask(a.d_h);
+    for (int u = 0; u < a.d_h; u++) nmask[u] = ev.mask(m, 0, m, u, a.seg_stride, a.H_blk, Lp);
+    std::vector<std::vector<SumTerm>> tb;
+    std::vector<double> scb;
+    for (int l = 0; l < BV; l++)
+        for (int t = 0; t < half; t++) {
+            std::vector<SumTerm> tt;
+            for (int u = 0; u < a.d_h; u++) tt.push_back(SumTerm{pbi(l, t - u)->d, nmask[u]});
+            tb.push_back(tt);
+            scb.push_back(ps[l].scale * ev.mask_scale(Lp));
+        }
+    std::vector<DCt> by = ev.alloc_many(BV * half, Lp);
+    ev.sum_many(tb, Lp, 2, by, scb);
+    std::vector<DCt> bt = ev.alloc_many(BV * half, Lp - 1);
+    ev.rescale_many(ptrs(by), bt);
+    // 5. o = sum_t u_t (x) b_t (u_t viewed at b_t's level: mod-drop without a copy), one relin, rescale
+    const int Lb = Lp - 1;
+    std::vector<std::vector<DCt>> ud(BV);
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(BV);
+    for (int l = 0; l < BV; l++) {
+        for (int t = 0; t < half; t++) {
+            DCt v = ub[l][t];
+            if (v.L < Lb) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "value: V below P_fd level");
+            v.cstride = (i64)v.L * N;
+            v.L = Lb;
+            ud[l].push_back(v);
+        }
+        for (int t = 0; t < half; t++) pairs[l].push_back({&ud[l][t], &bt[l * half + t]});
+    }
+    std::vector<DCt> o3 = ev.alloc_many(BV, Lb, 3), o2 = ev.alloc_many(BV, Lb);
+    ev.tensor_many(pairs, o3);
+    ev.relin_many(ptrs(o3), o2);
+    outs = ev.alloc_many(BV, Lb - 1);
+    ev.rescale_many(ptrs(o2), outs);
 }
 
 // ====================================================================================== export (Alg 3 GPU half)

@@ -17,12 +17,12 @@ void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C,
 std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p);
 void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs);
-void proj_finalize(Ev& ev, const encf_proj_plan& p, const DCt& acc, DCt& y);
+void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs, std::vector<DCt>& ys);
 
 void attn_plan_init(encf_attn_plan& a, int n, int m, int H, int d_h, int C_qk, int beta, int H_blk);
 std::vector<uint32_t> attn_galois(Ev& ev, const encf_attn_plan& a);
-void psi_hoisted(Ev& ev, const DCt& x, const std::vector<int>& ts, int m, int N_seg, int seg0, int nseg,
-                 std::vector<DCt>& outs);
+void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
+              std::vector<std::vector<DCt>>& outs);
 void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, const std::vector<DCt>& ks, int t0, int t1,
                std::vector<DCt>& S);
 void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S, std::vector<DCt>& outs);

@@ -1,5 +1,6 @@
-// eval.cu -- key switching (hybrid, dnum digits), rotations (single and hoisted), conj, relin,
-// rescale and the small ciphertext ops, as sequences of the sm_100a kernels of ntt.cu / poly.cu.
+// eval.cu -- batched key switching (hybrid, dnum digits, fast BConv, floor ModDown), rotations
+// (single and hoisted), conj, relin, rescale and lazy sums as short sequences of sm_100a launches that
+// each cover a whole list of ciphertexts.
 #include <cstring>
 #include "eval.cuh"
 
@@ -10,8 +11,7 @@ void check_scale(double a, double b) {
 uint32_t Ev::galois_rot(long steps) const {
     long n = c.N / 2;
     long r = ((steps % n) + n) % n;
-    u64 g = h_powmod(5, (u64)r, 2 * (u64)c.N);
-    return (uint32_t)g;
+    return (uint32_t)h_powmod(5, (u64)r, 2 * (u64)c.N);
 }
 
 const u64* Ev::key_for(uint32_t g, int L) const {
@@ -22,195 +22,355 @@ const u64* Ev::key_for(uint32_t g, int L) const {
     return it->second;
 }
 
-// ModUp (C4): for every digit j, inside the digit d~ = d (NTT limbs copied), elsewhere fast BConv of the
-// digit's coefficient-form limbs followed by a forward NTT.
-u64* Ev::modup(const u64* d_ntt, int L) {
-    const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L);
-    u64* dco = sc.get((size_t)L * N);
-    k_copy(d_ntt, dco, (size_t)L * N, s);
-    ntt_inverse(c, PolyBatch{dco, 0, 1, c.qmap(L)}, s);
-    u64* ext = sc.get((size_t)dn * nl * N);
+std::vector<DCt> Ev::alloc_many(int n, int L, int ncomp) {
+    std::vector<DCt> v(n);
+    if (n == 0) return v;
+    u64* base = sc.get(ct_words(L, ncomp) * n);
+    for (int i = 0; i < n; i++) { v[i].d = base + ct_words(L, ncomp) * i; v[i].L = L; v[i].ncomp = ncomp; }
+    return v;
+}
+
+// ModUp (C4) of n polynomials: inside digit j, d~ = d (NTT limbs copied); on every other modulus of
+// Q_L u P, fast BConv of the digit's coefficient-form limbs, then forward NTT.  One launch sequence for
+// all n polynomials.
+u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint32_t>& gathers, int L) {
+    const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L), n = (int)polys.size();
+    const size_t Lw = (size_t)L * N;
+    u64* dntt = sc.get(Lw * n);
+    for (int i0 = 0; i0 < n; i0 += CP_BATCH) {
+        int cnt = std::min(CP_BATCH, n - i0);
+        CopyBatch cb;
+        for (int i = 0; i < cnt; i++) { cb.src[i] = polys[i0 + i]; cb.g[i] = gathers.empty() ? 1u : gathers[i0 + i]; }
+        k_gather_copy(c, cb, cnt, dntt + Lw * i0, (i64)Lw, Lw, s);
+    }
+    u64* dco = sc.get(Lw * n);
+    CUDA_TRY(cudaMemcpyAsync(dco, dntt, Lw * n * 8, cudaMemcpyDeviceToDevice, s));
+    ntt_inverse(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, s);
+    const size_t es = ext_stride(L);
+    u64* ext = sc.get(es * n);
     LimbMap em = c.extmap(L);
     for (int j = 0; j < dn; j++) {
         const ModUpTab& t = c.modup[L][j];
         u64* ej = ext + (size_t)j * nl * N;
-        k_copy(d_ntt + (size_t)t.lo * N, ej + (size_t)t.lo * N, (size_t)(t.hi - t.lo) * N, s);
+        CUDA_TRY(cudaMemcpy2DAsync(ej + (size_t)t.lo * N, es * 8, dntt + (size_t)t.lo * N, Lw * 8, (size_t)(t.hi - t.lo) * N * 8,
+                                   n, cudaMemcpyDeviceToDevice, s));
         LimbMap im;
         im.n = t.hi - t.lo;
         for (int i = 0; i < im.n; i++) im.mod[i] = (unsigned char)(t.lo + i);
-        k_bconv(c, dco + (size_t)t.lo * N, im, t.d_vfac, t.d_vfac_sh, t.d_wfac, t.tgt, ej, t.tgt_pos.data(), s);
-        // NTT of [0, lo) and [hi, nl)
+        k_bconv_batch(c, dco + (size_t)t.lo * N, (i64)Lw, im, t.d_vfac, t.d_vfac_sh, t.d_wfac, t.tgt, ej, (i64)es,
+                      t.tgt_pos.data(), n, s);
         if (t.lo > 0) {
             LimbMap m; m.n = t.lo;
             for (int i = 0; i < t.lo; i++) m.mod[i] = em.mod[i];
-            ntt_forward(c, PolyBatch{ej, 0, 1, m}, s);
+            ntt_forward(c, PolyBatch{ej, (i64)es, n, m}, s);
         }
         if (t.hi < nl) {
             LimbMap m; m.n = nl - t.hi;
             for (int i = t.hi; i < nl; i++) m.mod[i - t.hi] = em.mod[i];
-            ntt_forward(c, PolyBatch{ej + (size_t)t.hi * N, 0, 1, m}, s);
+            ntt_forward(c, PolyBatch{ej + (size_t)t.hi * N, (i64)es, n, m}, s);
         }
     }
-    c.st_modup++;
+    c.st_modup += n;
     return ext;
 }
 
-// Inner product + ModDown (C4): (b0, b1) = sum_j d~_j ksk_j ; out_c = (b_c - fastBConv_{P->Q}([b_c]_P)) P^{-1}.
-void Ev::ks_core(const u64* ext, int L, uint32_t gg, const u64* key, u64* out0, u64* out1, const u64* add0,
-                 const u64* add1) {
+// Inner product + ModDown (C4) for a list of requests at level L.
+void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
     const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L);
     const int ML = keys->max_level, key_nl = ML + K;
-    u64* acc = sc.get((size_t)2 * nl * N);
-    LimbMap klm;   // ext limb -> key limb
+    LimbMap klm;
     klm.n = nl;
     for (int e = 0; e < nl; e++) klm.mod[e] = (unsigned char)(e < L ? e : ML + (e - L));
-    k_ks_inner(c, ext, dn, nl, gg, key, key_nl, klm, acc, s);
-    // [b]_P to coefficient form (both components in one batch)
     LimbMap pm; pm.n = K;
     for (int k = 0; k < K; k++) pm.mod[k] = (unsigned char)(c.L + k);
-    ntt_inverse(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2, pm}, s);
-    u64* y = sc.get((size_t)2 * L * N);
-    const ModDownTab& md = c.moddown[L];
     LimbMap qm = c.qmap(L);
     std::vector<int> pos(L);
     for (int i = 0; i < L; i++) pos[i] = i;
-    for (int comp = 0; comp < 2; comp++)
-        k_bconv(c, acc + (size_t)comp * nl * N + (size_t)L * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm,
-                y + (size_t)comp * L * N, pos.data(), s);
-    ntt_forward(c, PolyBatch{y, (i64)L * N, 2, qm}, s);
-    k_moddown_finish(c, acc, y, add0, out0, L, md, s);
-    k_moddown_finish(c, acc + (size_t)nl * N, y + (size_t)L * N, add1, out1, L, md, s);
-    c.st_ks++;
-}
-
-void Ev::rotate_galois(const DCt& in, uint32_t g, DCt& out) {
-    if (in.ncomp != 2) throw EncfError(ENCF_ERR_FORMAT, "rotate needs 2 components");
-    const int N = c.N, L = in.L;
-    const u64* key = key_for(g, L);
-    u64* tmp = sc.get((size_t)2 * L * N);
-    k_automorph(c, in.d, (i64)L * N, tmp, (i64)L * N, 2, L, g, s);     // sigma_g(c0), sigma_g(c1)
-    u64* ext = modup(tmp + (size_t)L * N, L);
-    out.L = L; out.ncomp = 2; out.scale = in.scale;
-    ks_core(ext, L, 1u, key, out.comp(0, N), out.comp(1, N), tmp, nullptr);
-}
-
-void Ev::rotate_hoisted(const DCt& in, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
-    if (in.ncomp != 2) throw EncfError(ENCF_ERR_FORMAT, "rotate needs 2 components");
-    const int N = c.N, L = in.L;
-    bool any = false;
-    for (uint32_t g : gs) any |= (g != 1u);
-    u64* ext = any ? modup(in.comp(1, N), L) : nullptr;
-    for (size_t i = 0; i < gs.size(); i++) {
-        DCt& o = outs[i];
-        o.L = L; o.ncomp = 2; o.scale = in.scale;
-        if (gs[i] == 1u) { copy(in, o); continue; }
-        const u64* key = key_for(gs[i], L);
-        k_automorph(c, in.comp(0, N), 0, o.comp(0, N), 0, 1, L, gs[i], s);
-        ks_core(ext, L, gs[i], key, o.comp(0, N), o.comp(1, N), o.comp(0, N), nullptr);
+    const ModDownTab& md = c.moddown[L];
+    const int n_all = (int)reqs.size();
+    for (int r0 = 0; r0 < n_all; r0 += KS_BATCH) {
+        const int n = std::min(KS_BATCH, n_all - r0);
+        u64* acc = sc.get((size_t)n * 2 * nl * N);
+        KsInnerBatch B;
+        OutBatch O;
+        for (int i = 0; i < n; i++) {
+            const KsReq& q = reqs[r0 + i];
+            B.ext[i] = q.ext; B.key[i] = q.key; B.gather[i] = q.gather; B.acc[i] = acc + (size_t)i * 2 * nl * N;
+            O.out[i][0] = q.out0; O.out[i][1] = q.out1; O.add[i][0] = q.add0; O.add[i][1] = q.add1;
+        }
+        k_ks_inner_batch(c, B, n, dn, nl, key_nl, klm, s);
+        ntt_inverse(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);     // [b]_P -> coefficient form
+        u64* y = sc.get((size_t)n * 2 * L * N);
+        k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
+                      pos.data(), 2 * n, s);
+        ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
+        k_moddown_finish_batch(c, acc, y, O, n, L, nl, md, s);
+        c.st_ks += n;
     }
 }
 
-void Ev::relin(const DCt& in, DCt& out) {
-    if (in.ncomp != 3) throw EncfError(ENCF_ERR_FORMAT, "relinearize needs 3 components");
-    const int N = c.N, L = in.L;
-    const u64* key = key_for(0u, L);
-    u64* ext = modup(in.comp(2, N), L);
-    out.L = L; out.ncomp = 2; out.scale = in.scale;
-    ks_core(ext, L, 1u, key, out.comp(0, N), out.comp(1, N), in.comp(0, N), in.comp(1, N));
+// Single (non-hoisted) rotations: sigma_g(c1) is ModUp'ed (gather fused into the ModUp copy), sigma_g(c0)
+// is added in the ModDown epilogue.
+void Ev::rotate_many(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L;
+    std::vector<const u64*> c1;
+    std::vector<uint32_t> g1;
+    std::vector<int> idx;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rotate_many: mixed levels");
+        outs[i].L = L; outs[i].ncomp = 2; outs[i].scale = ins[i]->scale; outs[i].cstride = 0;
+        if (gs[i] == 1u) { copy(*ins[i], outs[i]); continue; }
+        c1.push_back(ins[i]->comp(1, N));
+        g1.push_back(gs[i]);
+        idx.push_back(i);
+    }
+    if (idx.empty()) return;
+    const int m = (int)idx.size();
+    const size_t Lw = (size_t)L * N;
+    u64* c0g = sc.get(Lw * m);
+    for (int i0 = 0; i0 < m; i0 += CP_BATCH) {
+        int cnt = std::min(CP_BATCH, m - i0);
+        CopyBatch cb;
+        for (int i = 0; i < cnt; i++) { cb.src[i] = ins[idx[i0 + i]]->comp(0, N); cb.g[i] = g1[i0 + i]; }
+        k_gather_copy(c, cb, cnt, c0g + Lw * i0, (i64)Lw, Lw, s);
+    }
+    u64* ext = modup_many(c1, g1, L);
+    std::vector<KsReq> reqs(m);
+    for (int i = 0; i < m; i++) {
+        DCt& o = outs[idx[i]];
+        reqs[i] = KsReq{ext + ext_stride(L) * i, key_for(g1[i], L), 1u, o.comp(0, N), o.comp(1, N), c0g + Lw * i, nullptr};
+    }
+    ks_many(reqs, L);
 }
 
-// Rescale (C5) in the NTT domain: the last limb to coefficient form, correction per remaining limb,
-// forward NTT of the correction, then (c_i - corr_i) q_L^{-1}.
-void Ev::rescale(const DCt& in, DCt& out) {
-    const int N = c.N, L = in.L, nc = in.ncomp;
+// Hoisted batches: ONE ModUp per input ciphertext, then the Galois gather of each requested element is
+// fused into the inner product (SURVEY C4 hoisting; bits differ from rotate_many by design).
+void Ev::hoisted_many(const std::vector<const DCt*>& ins, const std::vector<std::vector<uint32_t>>& gs,
+                      std::vector<std::vector<DCt>>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L;
+    std::vector<const u64*> c1;
+    std::vector<int> which;   // ModUp slot per input (-1: no rotation needed)
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "hoisted_many: mixed levels");
+        bool any = false;
+        for (uint32_t g : gs[i]) any |= (g != 1u);
+        which.push_back(any ? (int)c1.size() : -1);
+        if (any) c1.push_back(ins[i]->comp(1, N));
+    }
+    u64* ext = c1.empty() ? nullptr : modup_many(c1, {}, L);
+    const size_t Lw = (size_t)L * N;
+    // sigma_g(c0) straight into the outputs' component 0 (added in the ModDown epilogue)
+    std::vector<KsReq> reqs;
+    std::vector<std::pair<const u64*, uint32_t>> c0s;
+    std::vector<u64*> c0dst;
+    for (int i = 0; i < n; i++) {
+        for (size_t k = 0; k < gs[i].size(); k++) {
+            DCt& o = outs[i][k];
+            o.L = L; o.ncomp = 2; o.scale = ins[i]->scale; o.cstride = 0;
+            if (gs[i][k] == 1u) { copy(*ins[i], o); continue; }
+            c0s.push_back({ins[i]->comp(0, N), gs[i][k]});
+            c0dst.push_back(o.comp(0, N));
+            reqs.push_back(KsReq{ext + ext_stride(L) * which[i], key_for(gs[i][k], L), gs[i][k], o.comp(0, N), o.comp(1, N),
+                                 o.comp(0, N), nullptr});
+        }
+    }
+    if (reqs.empty()) return;
+    // gather-copy c0 into a contiguous scratch then scatter-free: gather into dst pointers one batch at a time
+    const int m = (int)c0s.size();
+    u64* c0g = sc.get(Lw * m);
+    for (int i0 = 0; i0 < m; i0 += CP_BATCH) {
+        int cnt = std::min(CP_BATCH, m - i0);
+        CopyBatch cb;
+        for (int i = 0; i < cnt; i++) { cb.src[i] = c0s[i0 + i].first; cb.g[i] = c0s[i0 + i].second; }
+        k_gather_copy(c, cb, cnt, c0g + Lw * i0, (i64)Lw, Lw, s);
+    }
+    for (int i = 0; i < m; i++) reqs[i].add0 = c0g + Lw * i;
+    ks_many(reqs, L);
+}
+
+void Ev::relin_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L;
+    std::vector<const u64*> d2;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->ncomp != 3 || ins[i]->L != L) throw EncfError(ENCF_ERR_FORMAT, "relinearize needs 3 components at one level");
+        d2.push_back(ins[i]->comp(2, N));
+    }
+    const u64* key = key_for(0u, L);
+    u64* ext = modup_many(d2, {}, L);
+    std::vector<KsReq> reqs(n);
+    for (int i = 0; i < n; i++) {
+        DCt& o = outs[i];
+        o.L = L; o.ncomp = 2; o.scale = ins[i]->scale; o.cstride = 0;
+        reqs[i] = KsReq{ext + ext_stride(L) * i, key, 1u, o.comp(0, N), o.comp(1, N), ins[i]->comp(0, N), ins[i]->comp(1, N)};
+    }
+    ks_many(reqs, L);
+}
+
+// Rescale (C5) of a list of ciphertexts at one level: last limbs to coefficient form, correction per
+// remaining limb, NTT of the correction, (c_i - corr_i) q_L^{-1}.
+void Ev::rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L;
     if (L <= 1) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "rescale at one limb");
-    u64* last = sc.get((size_t)nc * N);
-    for (int comp = 0; comp < nc; comp++) k_copy(in.comp(comp, N) + (size_t)(L - 1) * N, last + (size_t)comp * N, N, s);
+    std::vector<const u64*> in_p;
+    std::vector<u64*> out_p;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rescale_many: mixed levels");
+        outs[i].L = L - 1; outs[i].ncomp = ins[i]->ncomp; outs[i].scale = ins[i]->scale / (double)c.mods[L - 1];
+        outs[i].cstride = 0;
+        for (int cc = 0; cc < ins[i]->ncomp; cc++) { in_p.push_back(ins[i]->comp(cc, N)); out_p.push_back(outs[i].comp(cc, N)); }
+    }
+    const int P = (int)in_p.size();
+    u64* last = sc.get((size_t)P * N);
+    u64* corr = sc.get((size_t)P * (L - 1) * N);
     LimbMap lm; lm.n = 1; lm.mod[0] = (unsigned char)(L - 1);
-    ntt_inverse(c, PolyBatch{last, (i64)N, nc, lm}, s);
-    u64* corr = sc.get((size_t)nc * (L - 1) * N);
-    k_rescale_prep(c, last, corr, L, nc, (i64)N, s);
-    ntt_forward(c, PolyBatch{corr, (i64)(L - 1) * N, nc, c.qmap(L - 1)}, s);
-    k_rescale_finish(c, in.d, (i64)L * N, corr, out.d, (i64)(L - 1) * N, nc, L, s);
-    out.L = L - 1; out.ncomp = nc; out.scale = in.scale / (double)c.mods[L - 1];
+    for (int p0 = 0; p0 < P; p0 += CP_BATCH) {
+        int cnt = std::min(CP_BATCH, P - p0);
+        CopyBatch cb;
+        for (int i = 0; i < cnt; i++) { cb.src[i] = in_p[p0 + i] + (size_t)(L - 1) * N; cb.g[i] = 1u; }
+        k_gather_copy(c, cb, cnt, last + (size_t)p0 * N, (i64)N, (size_t)N, s);
+    }
+    ntt_inverse(c, PolyBatch{last, (i64)N, P, lm}, s);
+    k_rescale_prep_batch(c, last, corr, L, P, s);
+    ntt_forward(c, PolyBatch{corr, (i64)(L - 1) * N, P, c.qmap(L - 1)}, s);
+    for (int p0 = 0; p0 < P; p0 += CP_BATCH) {
+        int cnt = std::min(CP_BATCH, P - p0);
+        CopyBatch ci, co;
+        for (int i = 0; i < cnt; i++) { ci.src[i] = in_p[p0 + i]; co.src[i] = out_p[p0 + i]; ci.g[i] = co.g[i] = 1u; }
+        k_rescale_finish_batch(c, ci, corr + (size_t)p0 * (L - 1) * N, co, L, cnt, s);
+    }
+}
+
+// outs[o] = sum of terms[o] (each ct times an optional mask), all at level L with ncomp components.
+void Ev::sum_many(const std::vector<std::vector<SumTerm>>& terms, int L, int ncomp, std::vector<DCt>& outs,
+                  const std::vector<double>& scales) {
+    const int n = (int)terms.size();
+    if (n == 0) return;
+    std::vector<SumDev> t;
+    std::vector<int> off{0};
+    std::vector<u64*> op;
+    for (int o = 0; o < n; o++) {
+        for (auto& x : terms[o]) t.push_back(SumDev{x.ct, x.mask});
+        off.push_back((int)t.size());
+        outs[o].L = L; outs[o].ncomp = ncomp; outs[o].scale = scales[o]; outs[o].cstride = 0;
+        op.push_back(outs[o].d);
+    }
+    for (int o0 = 0; o0 < n; o0 += 32768) {
+        int cnt = std::min(32768, n - o0);
+        std::vector<int> off2(off.begin() + o0, off.begin() + o0 + cnt + 1);
+        std::vector<u64*> op2(op.begin() + o0, op.begin() + o0 + cnt);
+        k_sum_csr(c, upload(t), upload(off2), upload(op2), cnt, off2.back() - off2.front(), ncomp, L, s);
+    }
+}
+
+void Ev::tensor_many(const std::vector<std::vector<std::pair<const DCt*, const DCt*>>>& pairs, std::vector<DCt>& outs) {
+    const int n = (int)pairs.size();
+    if (n == 0) return;
+    const int L = pairs[0][0].first->L;
+    std::vector<PairDev> t;
+    std::vector<int> off{0};
+    std::vector<u64*> op;
+    for (int o = 0; o < n; o++) {
+        double sc0 = pairs[o][0].first->scale * pairs[o][0].second->scale;
+        for (auto& pr : pairs[o]) {
+            if (pr.first->L != L || pr.second->L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "tensor: level mismatch");
+            if (pr.first->ncomp != 2 || pr.second->ncomp != 2) throw EncfError(ENCF_ERR_FORMAT, "tensor needs 2 components");
+            check_scale(pr.first->scale * pr.second->scale, sc0);
+            const i64 dflt = (i64)L * c.N;
+            t.push_back(PairDev{pr.first->d, pr.second->d, pr.first->cstride ? pr.first->cstride : dflt,
+                                pr.second->cstride ? pr.second->cstride : dflt});
+        }
+        off.push_back((int)t.size());
+        outs[o].L = L; outs[o].ncomp = 3; outs[o].scale = sc0; outs[o].cstride = 0;
+        op.push_back(outs[o].d);
+    }
+    k_tensor_csr(c, upload(t), upload(off), upload(op), n, (int)t.size(), L, s);
+}
+
+// ------------------------------------------------------------------------------------ single-item ops
+void Ev::rotate_galois(const DCt& in, uint32_t g, DCt& out) {
+    std::vector<DCt> o{out};
+    rotate_many({&in}, {g}, o);
+    out = o[0];
+}
+
+void Ev::rotate_hoisted(const DCt& in, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
+    std::vector<std::vector<DCt>> o{outs};
+    hoisted_many({&in}, {gs}, o);
+    outs = o[0];
+}
+
+void Ev::relin(const DCt& in, DCt& out) {
+    std::vector<DCt> o{out};
+    relin_many({&in}, o);
+    out = o[0];
+}
+
+void Ev::rescale(const DCt& in, DCt& out) {
+    std::vector<DCt> o{out};
+    rescale_many({&in}, o);
+    out = o[0];
 }
 
 void Ev::add(const DCt& a, const DCt& b, DCt& out, bool sub) {
     check_scale(a.scale, b.scale);
     if (a.L != b.L || a.ncomp != b.ncomp) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "add: level/component mismatch");
     k_add(c, a.d, b.d, out.d, a.ncomp, c.qmap(a.L), sub, s);
-    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale;
+    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale; out.cstride = 0;
 }
 
 void Ev::mul_i(const DCt& a, DCt& out) {
     k_mul_i(c, a.d, out.d, a.ncomp, c.qmap(a.L), s);
-    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale;
+    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale; out.cstride = 0;
 }
 
 void Ev::ptmul(const DCt& a, const u64* pt, double pt_scale, DCt& out) {
     const int N = c.N;
     k_mul(c, a.d, (i64)a.L * N, pt, 0, out.d, (i64)a.L * N, a.ncomp, c.qmap(a.L), s);
-    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale * pt_scale;
+    out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale * pt_scale; out.cstride = 0;
     c.st_ptmul++;
 }
 
 void Ev::mod_drop(const DCt& in, int L, DCt& out) {
     if (L < 1 || L > in.L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "mod_drop: bad level");
     const int N = c.N;
-    for (int comp = 0; comp < in.ncomp; comp++) {
-        if (out.d + (size_t)comp * L * N != in.d + (size_t)comp * in.L * N)
-            CUDA_TRY(cudaMemcpyAsync(out.d + (size_t)comp * L * N, in.d + (size_t)comp * in.L * N, (size_t)L * N * 8,
-                                     cudaMemcpyDeviceToDevice, s));
-    }
-    out.L = L; out.ncomp = in.ncomp; out.scale = in.scale;
+    CUDA_TRY(cudaMemcpy2DAsync(out.d, (size_t)L * N * 8, in.d, (size_t)in.L * N * 8, (size_t)L * N * 8, in.ncomp,
+                               cudaMemcpyDeviceToDevice, s));
+    out.L = L; out.ncomp = in.ncomp; out.scale = in.scale; out.cstride = 0;
 }
 
 void Ev::copy(const DCt& in, DCt& out) {
     k_copy(in.d, out.d, ct_words(in.L, in.ncomp), s);
-    out.L = in.L; out.ncomp = in.ncomp; out.scale = in.scale;
-}
-
-const u64* const* Ev::dev_ptrs(const std::vector<const u64*>& v) {
-    u64* d = sc.get(v.size());
-    CUDA_TRY(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(u64*), cudaMemcpyHostToDevice, s));
-    return (const u64* const*)d;
+    out.L = in.L; out.ncomp = in.ncomp; out.scale = in.scale; out.cstride = 0;
 }
 
 void Ev::tensor_sum(const std::vector<const DCt*>& A, const std::vector<const DCt*>& B, DCt& out3) {
-    const int L = A[0]->L;
-    double sc0 = A[0]->scale * B[0]->scale;
-    std::vector<const u64*> pa, pb;
-    for (size_t t = 0; t < A.size(); t++) {
-        if (A[t]->L != L || B[t]->L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "tensor: level mismatch");
-        check_scale(A[t]->scale * B[t]->scale, sc0);
-        pa.push_back(A[t]->d);
-        pb.push_back(B[t]->d);
-    }
-    for (size_t t0 = 0; t0 < pa.size(); t0 += 64) {   // pointer lists of at most 64 entries per launch
-        size_t te = std::min(pa.size(), t0 + 64);
-        std::vector<const u64*> a(pa.begin() + t0, pa.begin() + te), b(pb.begin() + t0, pb.begin() + te);
-        if (t0 == 0) {
-            k_tensor_acc(c, dev_ptrs(a), dev_ptrs(b), (int)a.size(), out3.d, L, s);
-        } else {
-            u64* tmp = sc.get(ct_words(L, 3));
-            k_tensor_acc(c, dev_ptrs(a), dev_ptrs(b), (int)a.size(), tmp, L, s);
-            k_add(c, out3.d, tmp, out3.d, 3, c.qmap(L), false, s);
-        }
-    }
-    out3.L = L; out3.ncomp = 3; out3.scale = sc0;
+    std::vector<std::pair<const DCt*, const DCt*>> pr;
+    for (size_t i = 0; i < A.size(); i++) pr.push_back({A[i], B[i]});
+    std::vector<DCt> o{out3};
+    tensor_many({pr}, o);
+    out3 = o[0];
 }
 
 void Ev::masked_sum(const std::vector<const DCt*>& C, const std::vector<const u64*>& M, double m_scale, DCt& out) {
     const int L = C[0]->L;
     double s0 = C[0]->scale * m_scale;
-    std::vector<const u64*> pc;
-    for (auto* x : C) {
-        if (x->L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "masked_sum: level mismatch");
-        check_scale(x->scale * m_scale, s0);
-        pc.push_back(x->d);
+    std::vector<SumTerm> t;
+    for (size_t i = 0; i < C.size(); i++) {
+        if (C[i]->L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "masked_sum: level mismatch");
+        check_scale(C[i]->scale * m_scale, s0);
+        t.push_back(SumTerm{C[i]->d, M[i]});
     }
-    k_masked_sum(c, dev_ptrs(pc), dev_ptrs(M), (int)pc.size(), out.d, L, s);
-    out.L = L; out.ncomp = 2; out.scale = s0;
+    std::vector<DCt> o{out};
+    sum_many({t}, L, 2, o, {s0});
+    out = o[0];
 }
 
 // Mask plaintexts: cached per (descriptor, level) in NTT form; encoded on the GPU on first use at

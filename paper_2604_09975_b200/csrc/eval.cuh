@@ -1,6 +1,7 @@
 // eval.cuh -- ciphertext-level operations (NTT-domain device ciphertexts) used by the ABI and the
-// EncFormer kernels.  Mirrors the schedule contract of SURVEY.md §8c C4/C5 exactly (hybrid key
-// switching with fast BConv, floor ModDown, SEAL rescale); bit-exactness against oracle/ is tested.
+// EncFormer kernels.  Every operation is BATCHED: a list of independent ciphertexts at one level is
+// processed by one launch sequence (ModUp / inner product / ModDown / rescale / lazy sums), so the
+// grid covers all of them.  Bit-exact schedule contract: SURVEY.md §8c C4/C5 (oracle/ckks.py).
 #pragma once
 #include <vector>
 #include "ctx.cuh"
@@ -9,7 +10,26 @@ struct DCt {                 // device ciphertext, NTT form, layout [comp][L][N]
     u64* d = nullptr;
     int ncomp = 2, L = 0;
     double scale = 1.0;
-    u64* comp(int c, int N) const { return d + (size_t)c * L * N; }
+    i64 cstride = 0;         // component stride in words (0 -> L * N)
+    u64* comp(int c, int N) const { return d + (size_t)c * (cstride ? cstride : (i64)L * N); }
+};
+
+// One key switch request: inner product of the (already ModUp'ed) digits `ext` with `key`, with the
+// Galois gather `gather` fused into the digit loads, then ModDown; out_c = ModDown(b_c) + add_c.
+struct KsReq {
+    const u64* ext;
+    const u64* key;
+    uint32_t gather;
+    u64* out0;
+    u64* out1;
+    const u64* add0;
+    const u64* add1;
+};
+
+// A lazy sum term: ct (2 or 3 components) times an optional mask plaintext (nullptr = 1).
+struct SumTerm {
+    const u64* ct;
+    const u64* mask;
 };
 
 struct Ev {
@@ -23,17 +43,31 @@ struct Ev {
     DCt alloc(int L, int ncomp = 2, double scale = 1.0) {
         DCt x; x.d = sc.get(ct_words(L, ncomp)); x.L = L; x.ncomp = ncomp; x.scale = scale; return x;
     }
+    std::vector<DCt> alloc_many(int n, int L, int ncomp = 2);
 
     const u64* key_for(uint32_t g, int L) const;
-    // ModUp of one NTT-form polynomial d (L limbs): returns ext [dnum][L+K][N] NTT form.
-    u64* modup(const u64* d_ntt, int L);
-    // inner product with key_g (Galois gather g fused, 1 = none) + ModDown of both components;
-    // out0 = ModDown(b0) + add0, out1 = ModDown(b1) + add1 (add may be null; may alias out).
-    void ks_core(const u64* ext, int L, uint32_t g_gather, const u64* key, u64* out0, u64* out1,
-                 const u64* add0, const u64* add1);
+    uint32_t galois_rot(long steps) const;
+    uint32_t galois_conj() const { return 2u * c.N - 1u; }
 
-    // ciphertext ops (outputs caller-provided in `out`, may alias inputs where noted)
-    void rotate_galois(const DCt& in, uint32_t g, DCt& out);                 // single (non-hoisted)
+    // ---- batched key switching core
+    // ModUp of polys[i] (NTT form, L limbs), each optionally permuted by gathers[i] first.
+    // Returns ext [n][dnum][L+K][N]; ext_stride() words per polynomial.
+    u64* modup_many(const std::vector<const u64*>& polys, const std::vector<uint32_t>& gathers, int L);
+    size_t ext_stride(int L) const { return (size_t)c.dnum(L) * (L + c.K) * c.N; }
+    void ks_many(const std::vector<KsReq>& reqs, int L);
+
+    // ---- ciphertext ops (outputs caller-provided; lists must share one level)
+    void rotate_many(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs);
+    void hoisted_many(const std::vector<const DCt*>& ins, const std::vector<std::vector<uint32_t>>& gs,
+                      std::vector<std::vector<DCt>>& outs);
+    void relin_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs);
+    void rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs);
+    void sum_many(const std::vector<std::vector<SumTerm>>& terms, int L, int ncomp, std::vector<DCt>& outs,
+                  const std::vector<double>& scales);
+    void tensor_many(const std::vector<std::vector<std::pair<const DCt*, const DCt*>>>& pairs, std::vector<DCt>& outs);
+
+    // single-item conveniences
+    void rotate_galois(const DCt& in, uint32_t g, DCt& out);
     void rotate_hoisted(const DCt& in, const std::vector<uint32_t>& gs, std::vector<DCt>& outs);
     void relin(const DCt& in3, DCt& out);
     void rescale(const DCt& in, DCt& out);
@@ -42,16 +76,18 @@ struct Ev {
     void ptmul(const DCt& a, const u64* pt, double pt_scale, DCt& out);
     void mod_drop(const DCt& in, int L, DCt& out);
     void copy(const DCt& in, DCt& out);
-    // lazy sums
     void tensor_sum(const std::vector<const DCt*>& A, const std::vector<const DCt*>& B, DCt& out3);
     void masked_sum(const std::vector<const DCt*>& C, const std::vector<const u64*>& M, double m_scale, DCt& out);
 
-    uint32_t galois_rot(long steps) const;
-    uint32_t galois_conj() const { return 2u * c.N - 1u; }
     // masks
     const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level);
     double mask_scale(int level) const { return (double)c.mods[level - 1]; }
-    const u64* const* dev_ptrs(const std::vector<const u64*>& v);
+    template <class T>
+    T* upload(const std::vector<T>& v) {
+        u64* d = sc.get((v.size() * sizeof(T) + 7) / 8 + 1);
+        CUDA_TRY(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        return (T*)d;
+    }
 };
 
 void check_scale(double a, double b);

@@ -42,56 +42,131 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u6
     X = x;
 }
 
+// Radix-4 pass over the lines held in shared memory: two consecutive stages (st, st+1) of every
+// line at once, 4 elements / 4 butterflies / 3 twiddles per work item, shift-only index math.
+// Line l of the tile sits at sm[l * LS + y], y < T = 2^lt.  `st` is the GLOBAL stage of the first of
+// the two, `gb0` the global block offset of line l at stage s0 (block index of element y at global
+// stage st is (boff(l) << (st - s0)) + (y >> (lt - (st - s0) - 1))).
+template <bool kInverse>
+__device__ __forceinline__ void radix4_pass(u64* sm, int LS, int nlines, int lt, int s0, int st, const int* boff,
+                                            const u64* __restrict__ tw, const u64* __restrict__ twp, u64 q, u64 two_q) {
+    const int sl = st - s0;                 // local stage of the first of the two
+    const int lgt = lt - sl - 1;            // log2 of span t at stage st
+    const int lh = lgt - 1;                 // log2(t/2)
+    const int per_line = 1 << (lt - 2);     // work items per line
+    const int total = nlines << (lt - 2);
+    for (int w = threadIdx.x; w < total; w += blockDim.x) {
+        const int l = w >> (lt - 2);
+        const int g = w & (per_line - 1);
+        const int i = g >> lh;              // block of size 2t at stage st
+        const int j = g & ((1 << lh) - 1);
+        const int base = l * LS + (i << (lgt + 1)) + j;
+        const int h = 1 << lh, t = 1 << lgt;
+        const int b1 = (boff[l] << sl) + i;
+        const int m1 = 1 << st;
+        const int b2 = (boff[l] << (sl + 1)) + 2 * i;
+        const int m2 = m1 << 1;
+        u64 a0 = sm[base], a1 = sm[base + h], a2 = sm[base + t], a3 = sm[base + t + h];
+        const u64 W1 = __ldg(tw + m1 + b1), W1p = __ldg(twp + m1 + b1);
+        const u64 Wa = __ldg(tw + m2 + b2), Wap = __ldg(twp + m2 + b2);
+        const u64 Wb = __ldg(tw + m2 + b2 + 1), Wbp = __ldg(twp + m2 + b2 + 1);
+        if (!kInverse) {
+            ct_bfly(a0, a2, W1, W1p, q, two_q);
+            ct_bfly(a1, a3, W1, W1p, q, two_q);
+            ct_bfly(a0, a1, Wa, Wap, q, two_q);
+            ct_bfly(a2, a3, Wb, Wbp, q, two_q);
+        } else {
+            gs_bfly(a0, a1, Wa, Wap, q, two_q);
+            gs_bfly(a2, a3, Wb, Wbp, q, two_q);
+            gs_bfly(a0, a2, W1, W1p, q, two_q);
+            gs_bfly(a1, a3, W1, W1p, q, two_q);
+        }
+        sm[base] = a0; sm[base + h] = a1; sm[base + t] = a2; sm[base + t + h] = a3;
+    }
+}
+
+template <bool kInverse>
+__device__ __forceinline__ void radix2_pass(u64* sm, int LS, int nlines, int lt, int s0, int st, const int* boff,
+                                            const u64* __restrict__ tw, const u64* __restrict__ twp, u64 q, u64 two_q) {
+    const int sl = st - s0;
+    const int lgt = lt - sl - 1;
+    const int per_line = 1 << (lt - 1);
+    const int total = nlines << (lt - 1);
+    for (int w = threadIdx.x; w < total; w += blockDim.x) {
+        const int l = w >> (lt - 1);
+        const int g = w & (per_line - 1);
+        const int i = g >> lgt;
+        const int j = g & ((1 << lgt) - 1);
+        const int base = l * LS + (i << (lgt + 1)) + j;
+        const int b = (boff[l] << sl) + i;
+        const int m = 1 << st;
+        const u64 W = __ldg(tw + m + b), Wp = __ldg(twp + m + b);
+        u64 x = sm[base], y = sm[base + (1 << lgt)];
+        if (!kInverse) ct_bfly(x, y, W, Wp, q, two_q);
+        else gs_bfly(x, y, W, Wp, q, two_q);
+        sm[base] = x; sm[base + (1 << lgt)] = y;
+    }
+}
+
+// Run stages [s0, s0 + lt) of every line (forward ascending, inverse descending) in radix-4 pairs.
+template <bool kInverse>
+__device__ __forceinline__ void run_stages(u64* sm, int LS, int nlines, int lt, int s0, const int* boff,
+                                           const u64* tw, const u64* twp, u64 q, u64 two_q) {
+    if (!kInverse) {
+        int st = s0;
+        for (; st + 1 < s0 + lt; st += 2) {
+            radix4_pass<false>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
+            __syncthreads();
+        }
+        if (st < s0 + lt) {
+            radix2_pass<false>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
+            __syncthreads();
+        }
+    } else {
+        int st = s0 + lt - 1;
+        if (lt & 1) {
+            radix2_pass<true>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
+            __syncthreads();
+            st--;
+        }
+        for (; st - 1 >= s0; st -= 2) {
+            radix4_pass<true>(sm, LS, nlines, lt, s0, st - 1, boff, tw, twp, q, two_q);
+            __syncthreads();
+        }
+    }
+}
+
 // Phase A (columns).  Forward: stages 0..s1-1.  Inverse: stages s1-1..0, then x N^{-1}, reduce.
+// Tile: R = 2^s1 rows x CT columns, loaded with 128-byte row segments, stored transposed in shared
+// memory (one padded line per column).
 template <bool kInverse>
 __global__ void __launch_bounds__(kThreads) ntt_cols(NttArgs a) {
-    __shared__ u64 sm[kTileElems];
+    extern __shared__ u64 sm[];
+    __shared__ int boff[64];
     const int limb = blockIdx.y, poly = blockIdx.z;
     const int mi = a.map.mod[limb];
     const ModConst mc = a.mod[mi];
     const u64 q = mc.q, two_q = 2 * q;
     const int R = 1 << a.s1, S = 1 << a.s2;
     const int CT = S < 16 ? S : 16;
+    const int lct = CT == 16 ? 4 : (31 - __clz(CT));
+    const int LS = R + 1;
     const int c0 = blockIdx.x * CT;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
     const u64* tw = a.tw + (size_t)mi * a.N;
     const u64* twp = a.tw_sh + (size_t)mi * a.N;
+    if (threadIdx.x < CT) boff[threadIdx.x] = 0;
     const int tot = R * CT;
     for (int e = threadIdx.x; e < tot; e += kThreads) {
-        int r = e / CT, c = e % CT;
-        sm[e] = g[(i64)r * S + c0 + c];
+        int r = e >> lct, c = e & (CT - 1);
+        sm[c * LS + r] = g[(i64)r * S + c0 + c];
     }
     __syncthreads();
-    const int nb = (R / 2) * CT;
-    if (!kInverse) {
-        for (int st = 0; st < a.s1; st++) {
-            const int m = 1 << st, t = R >> (st + 1);
-            for (int b = threadIdx.x; b < nb; b += kThreads) {
-                int c = b % CT, bb = b / CT;
-                int i = bb / t, j = bb % t;
-                int r1 = 2 * i * t + j;
-                u64 W = __ldg(tw + m + i), Wp = __ldg(twp + m + i);
-                ct_bfly(sm[r1 * CT + c], sm[(r1 + t) * CT + c], W, Wp, q, two_q);
-            }
-            __syncthreads();
-        }
-    } else {
-        for (int st = a.s1 - 1; st >= 0; st--) {
-            const int m = 1 << st, t = R >> (st + 1);
-            for (int b = threadIdx.x; b < nb; b += kThreads) {
-                int c = b % CT, bb = b / CT;
-                int i = bb / t, j = bb % t;
-                int r1 = 2 * i * t + j;
-                u64 W = __ldg(tw + m + i), Wp = __ldg(twp + m + i);
-                gs_bfly(sm[r1 * CT + c], sm[(r1 + t) * CT + c], W, Wp, q, two_q);
-            }
-            __syncthreads();
-        }
-    }
+    run_stages<kInverse>(sm, LS, CT, a.s1, 0, boff, tw, twp, q, two_q);
     const u64 ni = kInverse ? a.ninv[mi] : 0, nip = kInverse ? a.ninv_sh[mi] : 0;
     for (int e = threadIdx.x; e < tot; e += kThreads) {
-        int r = e / CT, c = e % CT;
-        u64 v = sm[e];
+        int r = e >> lct, c = e & (CT - 1);
+        u64 v = sm[c * LS + r];
         if (kInverse) v = mul_shoup(v, ni, nip, q);
         g[(i64)r * S + c0 + c] = v;   // forward: lazy [0, 4q) handed to phase B
     }
@@ -101,56 +176,31 @@ __global__ void __launch_bounds__(kThreads) ntt_cols(NttArgs a) {
 // Inverse: stages logN-1..s1 (lazy [0, 2q) output handed to phase A).
 template <bool kInverse>
 __global__ void __launch_bounds__(kThreads) ntt_rows(NttArgs a) {
-    __shared__ u64 sm[kTileElems];
+    extern __shared__ u64 sm[];
+    __shared__ int boff[64];
     const int limb = blockIdx.y, poly = blockIdx.z;
     const int mi = a.map.mod[limb];
     const ModConst mc = a.mod[mi];
     const u64 q = mc.q, two_q = 2 * q;
     const int S = 1 << a.s2;
     const int G = kTileElems / S < (1 << a.s1) ? kTileElems / S : (1 << a.s1);   // chunks per CTA
+    const int LS = S + 1;
     const int ch0 = blockIdx.x * G;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N + (i64)ch0 * S;
     const u64* tw = a.tw + (size_t)mi * a.N;
     const u64* twp = a.tw_sh + (size_t)mi * a.N;
+    if (threadIdx.x < G) boff[threadIdx.x] = ch0 + threadIdx.x;
     const int tot = G * S;
-    for (int e = threadIdx.x; e < tot; e += kThreads) sm[e] = g[e];
+    for (int e = threadIdx.x; e < tot; e += kThreads) sm[(e >> a.s2) * LS + (e & (S - 1))] = g[e];
     __syncthreads();
-    const int nb = G * (S / 2);
-    if (!kInverse) {
-        for (int st = a.s1; st < a.logN; st++) {
-            const int m = 1 << st, t = a.N >> (st + 1);
-            const int per = S / (2 * t);       // blocks per chunk
-            for (int b = threadIdx.x; b < nb; b += kThreads) {
-                int ch = b / (S / 2), bb = b % (S / 2);
-                int i = bb / t, j = bb % t;
-                int y1 = ch * S + 2 * i * t + j;
-                int blk = (ch0 + ch) * per + i;
-                u64 W = __ldg(tw + m + blk), Wp = __ldg(twp + m + blk);
-                ct_bfly(sm[y1], sm[y1 + t], W, Wp, q, two_q);
-            }
-            __syncthreads();
-        }
-        for (int e = threadIdx.x; e < tot; e += kThreads) {
-            u64 v = sm[e];
+    run_stages<kInverse>(sm, LS, G, a.s2, a.s1, boff, tw, twp, q, two_q);
+    for (int e = threadIdx.x; e < tot; e += kThreads) {
+        u64 v = sm[(e >> a.s2) * LS + (e & (S - 1))];
+        if (!kInverse) {
             v = v >= two_q ? v - two_q : v;
             v = v >= q ? v - q : v;
-            g[e] = v;
         }
-    } else {
-        for (int st = a.logN - 1; st >= a.s1; st--) {
-            const int m = 1 << st, t = a.N >> (st + 1);
-            const int per = S / (2 * t);
-            for (int b = threadIdx.x; b < nb; b += kThreads) {
-                int ch = b / (S / 2), bb = b % (S / 2);
-                int i = bb / t, j = bb % t;
-                int y1 = ch * S + 2 * i * t + j;
-                int blk = (ch0 + ch) * per + i;
-                u64 W = __ldg(tw + m + blk), Wp = __ldg(twp + m + blk);
-                gs_bfly(sm[y1], sm[y1 + t], W, Wp, q, two_q);
-            }
-            __syncthreads();
-        }
-        for (int e = threadIdx.x; e < tot; e += kThreads) g[e] = sm[e];
+        g[e] = v;
     }
 }
 
@@ -171,6 +221,18 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     return a;
 }
 
+size_t smemA(const encf_ctx& c) {
+    const int R = 1 << c.s1, S = 1 << c.s2;
+    const int CT = S < 16 ? S : 16;
+    return (size_t)CT * (R + 1) * sizeof(u64);
+}
+
+size_t smemB(const encf_ctx& c) {
+    const int R = 1 << c.s1, S = 1 << c.s2;
+    const int G = kTileElems / S < R ? kTileElems / S : R;
+    return (size_t)G * (S + 1) * sizeof(u64);
+}
+
 }  // namespace
 
 void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
@@ -183,8 +245,8 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     dim3 gB(R / G, b.map.n, b.npolys);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    ntt_cols<false><<<gA, kThreads, 0, s>>>(a);
-    ntt_rows<false><<<gB, kThreads, 0, s>>>(a);
+    ntt_cols<false><<<gA, kThreads, smemA(c), s>>>(a);
+    ntt_rows<false><<<gB, kThreads, smemB(c), s>>>(a);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;
@@ -202,8 +264,8 @@ void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     dim3 gB(R / G, b.map.n, b.npolys);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    ntt_rows<true><<<gB, kThreads, 0, s>>>(a);
-    ntt_cols<true><<<gA, kThreads, 0, s>>>(a);
+    ntt_rows<true><<<gB, kThreads, smemB(c), s>>>(a);
+    ntt_cols<true><<<gA, kThreads, smemA(c), s>>>(a);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;

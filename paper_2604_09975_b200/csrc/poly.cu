@@ -159,8 +159,6 @@ __global__ void rescale_finish_kernel(const u64* in, i64 is, const u64* corr, u6
 }
 
 // ------------------------------------------------------------------------------------ fast base conversion (C4)
-struct OutPos { int pos[MAX_LIMBS]; };
-
 // y_t[k] = sum_i [x_i[k] vfac_i]_{q_i} wfac[i][t] mod t ; in: [n_in][N] coefficient form; out limb
 // of target t at out + pos[t]*N.  One thread per coefficient, all targets (the x_i stay in registers).
 __global__ void __launch_bounds__(TB) bconv_kernel(const u64* __restrict__ in, LimbMap im, const u64* __restrict__ vfac,
@@ -194,8 +192,6 @@ __global__ void __launch_bounds__(TB) bconv_kernel(const u64* __restrict__ in, L
 // ------------------------------------------------------------------------------------ key-switch inner product (C4)
 // acc_c[e][k] = sum_j ext_j[e][src_g(k)] * key_j[c][kl(e)][k]  over the extended limbs e of Q_L u P.
 // The Galois gather of the hoisted batch is fused into the digit loads (g = 1: identity).
-struct KeyLimb { int kl[MAX_LIMBS]; };
-
 __global__ void __launch_bounds__(TB) ks_inner_kernel(const u64* __restrict__ ext, int dnum, int nl, uint32_t g,
                                                       const u64* __restrict__ key, int key_nl, KeyLimb klm,
                                                       LimbMap em, u64* __restrict__ acc, int N, int logN,
@@ -657,4 +653,287 @@ void k_decode_limb0(encf_ctx& c, const u64* coeff0, double scale, double* re, do
     lift_limb0_kernel<<<GRID(2 * c.N), TB, 0, s>>>(coeff0, c.N, c.d_mod, A);
     fft2n(c, A, +1.0, s);
     gather_slots_kernel<<<GRID(c.N / 2), TB, 0, s>>>(A, c.d_rot_group, c.N / 2, 1.0 / scale, re, im);
+}
+
+// ====================================================================================== batched key switching
+// (many independent key switches / rotations / rescales per launch: fills the 148 SMs and removes the
+// per-ciphertext launch sequence).  Request tables travel by value as kernel parameters.
+namespace {
+
+__global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
+                                                            LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
+    const int r = blockIdx.z, e = blockIdx.y;
+    const u64* __restrict__ ext = B.ext[r];
+    const u64* __restrict__ key = B.key[r];
+    u64* __restrict__ acc = B.acc[r];
+    const uint32_t g = B.gather[r];
+    const ModConst mc = mod[em.mod[e]];
+    const int kle = klm.kl[e];
+    const uint32_t mask2n = 2 * N - 1;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        int src = k;
+        if (g != 1) {
+            uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+            uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+            src = brv((int)((e2 - 1) >> 1), logN);
+        }
+        U128 a0{0, 0}, a1{0, 0};
+        for (int j = 0; j < dnum; j++) {
+            u64 x = ext[((size_t)j * nl + e) * N + src];
+            const u64* kj = key + (size_t)j * 2 * key_nl * N;
+            mac128(a0, x, kj[(size_t)kle * N + k]);
+            mac128(a1, x, kj[((size_t)key_nl + kle) * N + k]);
+        }
+        acc[(size_t)e * N + k] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
+        acc[((size_t)nl + e) * N + k] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
+    }
+}
+
+// out_c = (b_c - y_c) P^{-1} + add_c for request r = blockIdx.z / 2, component c = blockIdx.z % 2.
+// b: acc base [r][2][nl][N]; y: [r][2][L][N].
+__global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u64* __restrict__ y, OutBatch O, int level,
+                                            int nl, int N, const ModConst* __restrict__ mod, const u64* pinv,
+                                            const u64* pinv_sh) {
+    const int r = blockIdx.z >> 1, c = blockIdx.z & 1;
+    const u64* b = acc + ((size_t)r * 2 + c) * nl * N;
+    const u64* yy = y + ((size_t)r * 2 + c) * level * N;
+    u64* out = O.out[r][c];
+    const u64* add = O.add[r][c];
+    const size_t total = (size_t)level * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N);
+        u64 q = mod[limb].q;
+        u64 v = mul_shoup(sub_mod(b[i], yy[i], q), pinv[limb], pinv_sh[limb], q);
+        if (add) v = add_mod(v, add[i], q);
+        out[i] = v;
+    }
+}
+
+// bconv over a batch of polynomials: input poly p at in + p*in_stride, output at out + p*out_stride.
+__global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
+                                                         const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
+                                                         const u64* __restrict__ wfac, LimbMap om, OutPos op,
+                                                         u64* __restrict__ out, i64 out_stride, int N,
+                                                         const ModConst* __restrict__ mod) {
+    extern __shared__ u64 sw[];
+    const int nin = im.n, nout = om.n;
+    for (int i = threadIdx.x; i < nin * nout; i += blockDim.x) sw[i] = wfac[i];
+    __syncthreads();
+    in += (size_t)blockIdx.y * in_stride;
+    out += (size_t)blockIdx.y * out_stride;
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        u64 v[16];
+#pragma unroll
+        for (int i = 0; i < 16; i++) {
+            if (i < nin) {
+                u64 qi = mod[im.mod[i]].q;
+                v[i] = mul_shoup(in[(size_t)i * N + k], vfac[i], vfac_sh[i], qi);
+            }
+        }
+        for (int t = 0; t < nout; t++) {
+            ModConst mc = mod[om.mod[t]];
+            U128 acc{0, 0};
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
+            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+        }
+    }
+}
+
+// Gather-copy: dst + p*dst_stride <- src[p] (words each), optional Galois gather per item (NTT domain).
+__global__ void gather_copy_kernel(CopyBatch C, u64* dst, i64 dst_stride, size_t words, int N, int logN) {
+    const int p = blockIdx.y;
+    const u64* __restrict__ src = C.src[p];
+    const uint32_t g = C.g[p];
+    u64* d = dst + (size_t)p * dst_stride;
+    const uint32_t mask2n = 2 * N - 1;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < words; i += (size_t)gridDim.x * blockDim.x) {
+        size_t limb = i / N;
+        int k = (int)(i % N);
+        int s = k;
+        if (g != 1) {
+            uint32_t e = 2u * (uint32_t)brv(k, logN) + 1u;
+            uint32_t e2 = (uint32_t)(((uint64_t)e * g) & mask2n);
+            s = brv((int)((e2 - 1) >> 1), logN);
+        }
+        d[i] = src[limb * N + s];
+    }
+}
+
+__global__ void rescale_prep_batch_kernel(const u64* last, u64* corr, int level, int N, const ModConst* mod, const u64* hmod) {
+    const int p = blockIdx.y;
+    const int nl = level - 1;
+    const u64* lp_in = last + (size_t)p * N;
+    u64* cr = corr + (size_t)p * nl * N;
+    u64 qL = mod[level - 1].q, h = qL / 2;
+    const size_t total = (size_t)nl * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N), k = (int)(i % N);
+        u64 qi = mod[limb].q;
+        u64 lp = add_mod(lp_in[k], h, qL);
+        cr[i] = sub_mod(lp % qi, hmod[limb], qi);
+    }
+}
+
+__global__ void rescale_finish_batch_kernel(CopyBatch In, const u64* corr, CopyBatch Out, int level, int N,
+                                            const ModConst* mod, const u64* inv, const u64* inv_sh) {
+    const int p = blockIdx.y;    // polynomial (component) index
+    const int nl = level - 1;
+    const u64* in = In.src[p];
+    u64* out = (u64*)Out.src[p];
+    const u64* cr = corr + (size_t)p * nl * N;
+    const size_t total = (size_t)nl * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N);
+        u64 qi = mod[limb].q;
+        out[i] = mul_shoup(sub_mod(in[i], cr[i], qi), inv[limb], inv_sh[limb], qi);
+    }
+}
+
+}  // namespace
+
+void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
+                      cudaStream_t s) {
+    KeyLimb kl;
+    LimbMap em;
+    em.n = nl;
+    int Lq = nl - c.K;
+    for (int e = 0; e < nl; e++) {
+        kl.kl[e] = key_limb_of.mod[e];
+        em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
+    }
+    dim3 grid((c.N + TB - 1) / TB, nl, nreq);
+    const uint64_t bytes = (uint64_t)nreq * ((uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8);
+    int slot;
+    c.prof_begin("ks_inner", s, bytes, slot);
+    ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes;
+    CUDA_TRY(cudaGetLastError());
+}
+
+void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
+                            const ModDownTab& t, cudaStream_t s) {
+    dim3 grid(nblocks((size_t)level * c.N, TB, 256), 1, 2 * nreq);
+    moddown_finish_batch_kernel<<<grid, TB, 0, s>>>(acc, y, O, level, nl, c.N, c.d_mod, t.d_pinv, t.d_pinv_sh);
+    c.st_launch++; c.st_bytes += (uint64_t)nreq * 2 * level * c.N * 8 * 4;
+}
+
+void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
+                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s) {
+    if (im.n > 16) throw EncfError(ENCF_ERR_ARG, "bconv: at most 16 input limbs");
+    OutPos op;
+    for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
+    size_t smem = (size_t)im.n * om.n * sizeof(u64);
+    dim3 grid((c.N + TB - 1) / TB, npolys);
+    bconv_batch_kernel<<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod);
+    c.st_launch++; c.st_bytes += (uint64_t)npolys * (im.n + om.n) * c.N * 8;
+}
+
+void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s) {
+    dim3 grid(nblocks(words, TB, 512), n);
+    gather_copy_kernel<<<grid, TB, 0, s>>>(C, dst, dst_stride, words, c.N, c.logN);
+    c.st_launch++; c.st_bytes += (uint64_t)n * words * 16;
+}
+
+void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s) {
+    dim3 grid(nblocks((size_t)(level - 1) * c.N, TB, 256), npolys);
+    rescale_prep_batch_kernel<<<grid, TB, 0, s>>>(last, corr, level, c.N, c.d_mod, c.rescale[level].d_hmod);
+    c.st_launch++;
+}
+
+void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,
+                            cudaStream_t s) {
+    const RescaleTab& t = c.rescale[level];
+    dim3 grid(nblocks((size_t)(level - 1) * c.N, TB, 256), npolys);
+    rescale_finish_batch_kernel<<<grid, TB, 0, s>>>(In, corr, Out, level, c.N, c.d_mod, t.d_inv, t.d_inv_sh);
+    c.st_launch++; c.st_bytes += (uint64_t)npolys * (level - 1) * c.N * 8 * 3;
+}
+
+// ====================================================================================== batched lazy sums
+namespace {
+
+// outs[o] = sum_{t in [off[o], off[o+1])} ct_t (.) mask_t   (mask_t == nullptr: plain add), all
+// components, 128-bit lazy accumulation reduced every 128 terms.
+__global__ void __launch_bounds__(TB) sum_csr_kernel(const SumDev* __restrict__ terms, const int* __restrict__ off,
+                                                     u64* const* __restrict__ outs, int ncomp, int level, int N,
+                                                     const ModConst* __restrict__ mod) {
+    const int o = blockIdx.z, limb = blockIdx.y;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;
+    const int t0 = off[o], t1 = off[o + 1];
+    u64* out = outs[o];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const size_t idx = (size_t)limb * N + k;
+        for (int c = 0; c < ncomp; c++) {
+            u64 r = 0;
+            for (int ta = t0; ta < t1; ta += 128) {
+                U128 acc{0, 0};
+                const int tb = min(t1, ta + 128);
+                for (int t = ta; t < tb; t++) {
+                    const u64* ct = terms[t].ct;
+                    const u64* m = terms[t].mask;
+                    u64 x = ct[c * cs + idx];
+                    if (m) mac128(acc, x, m[idx]);
+                    else add128(acc, x);
+                }
+                r = add_mod(r, barrett128(acc, mc.q, mc.rhi, mc.rlo), mc.q);
+            }
+            out[c * cs + idx] = r;
+        }
+    }
+}
+
+// outs[o] = sum_{t in [off[o], off[o+1])} (a0 b0, a0 b1 + a1 b0, a1 b1)
+__global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restrict__ pairs, const int* __restrict__ off,
+                                                        u64* const* __restrict__ outs, int level, int N,
+                                                        const ModConst* __restrict__ mod) {
+    const int o = blockIdx.z, limb = blockIdx.y;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;
+    const int t0 = off[o], t1 = off[o + 1];
+    u64* out = outs[o];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        const size_t idx = (size_t)limb * N + k;
+        u64 r0 = 0, r1 = 0, r2 = 0;
+        for (int ta = t0; ta < t1; ta += 64) {
+            U128 d0{0, 0}, d1{0, 0}, d2{0, 0};
+            const int tb = min(t1, ta + 64);
+            for (int t = ta; t < tb; t++) {
+                const u64* a = pairs[t].a;
+                const u64* b = pairs[t].b;
+                u64 a0 = a[idx], a1 = a[pairs[t].as + idx], b0 = b[idx], b1 = b[pairs[t].bs + idx];
+                mac128(d0, a0, b0);
+                mac128(d1, a0, b1);
+                mac128(d1, a1, b0);
+                mac128(d2, a1, b1);
+            }
+            r0 = add_mod(r0, barrett128(d0, mc.q, mc.rhi, mc.rlo), mc.q);
+            r1 = add_mod(r1, barrett128(d1, mc.q, mc.rhi, mc.rlo), mc.q);
+            r2 = add_mod(r2, barrett128(d2, mc.q, mc.rhi, mc.rlo), mc.q);
+        }
+        out[idx] = r0;
+        out[cs + idx] = r1;
+        out[2 * cs + idx] = r2;
+    }
+}
+
+}  // namespace
+
+void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
+               cudaStream_t s) {
+    dim3 grid((c.N + TB - 1) / TB, level, nout);
+    sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod);
+    c.st_launch++;
+    c.st_bytes += (uint64_t)nterms * ncomp * level * c.N * 8 * 2 + (uint64_t)nout * ncomp * level * c.N * 8;
+}
+
+void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
+                  cudaStream_t s) {
+    dim3 grid((c.N + TB - 1) / TB, level, nout);
+    tensor_csr_kernel<<<grid, TB, 0, s>>>(pairs, off, outs, level, c.N, c.d_mod);
+    c.st_launch++;
+    c.st_bytes += (uint64_t)nterms * 4 * level * c.N * 8 + (uint64_t)nout * 3 * level * c.N * 8;
+    c.st_ctmul += nterms;
 }
