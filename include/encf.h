@@ -86,11 +86,12 @@ const char* encf_last_error(void);                 /* thread-local detail of the
 encf_status encf_stats(encf_ctx* ctx, encf_counters* out);
 encf_status encf_stats_reset(encf_ctx* ctx);
 /* Live kernel timing: while enabled, CUDA events are recorded on the launching stream around every
- * launch of the instrumented kernels ("diag_mac", "ks_inner", "ntt" = one fwd/inv transform pair of
- * launches).  encf_profile_read synchronises on those events and returns the summed device time,
- * the launch count and the summed ALGORITHMIC bytes for `kernel`, then
- * forgets them. */
-encf_status encf_profile_enable(encf_ctx* ctx, int enable);
+ * launch of the kernel named `which` ("*" = every kernel; NULL disables).  Names: "diag_mac",
+ * "ks_inner", "ntt" (one fwd/inv transform = a pair of launches) and the *_kernel launchers.
+ * encf_profile_read synchronises on those events and returns the summed device time, the launch
+ * count and the summed ALGORITHMIC bytes (DESIGN.md §Roofline, 0 where not defined) for `kernel`,
+ * then forgets them. */
+encf_status encf_profile_enable(encf_ctx* ctx, const char* which);
 encf_status encf_profile_read(encf_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches, uint64_t* alg_bytes);
 
 /* ------------------------------------------------------------------------------------------ keys (testing helpers) */

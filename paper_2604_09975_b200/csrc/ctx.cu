@@ -194,6 +194,12 @@ encf_status ctx_create_impl(const encf_params* params, int device, encf_ctx** ou
     try {
         c->device = device;
         CUDA_TRY(cudaSetDevice(device));
+        // keep stream-ordered scratch cached in the device pool across synchronisations (the default
+        // release threshold of 0 would unmap and re-map multi-GB scratch at every sync)
+        cudaMemPool_t pool;
+        CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = ~0ull;
+        CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
         build(*c, params);
         *out = c;
         return ENCF_OK;
@@ -225,6 +231,7 @@ cudaEvent_t encf_ctx::prof_event() {
 void encf_ctx::prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int& slot) {
     slot = -1;
     if (!prof) return;
+    if (!prof_all && prof_only != name) return;
     std::lock_guard<std::mutex> lk(mu);
     ProfRec r{name, prof_event(), prof_event(), bytes};
     CUDA_TRY(cudaEventRecord(r.a, s));
@@ -238,9 +245,12 @@ void encf_ctx::prof_end(int slot, cudaStream_t s) {
     CUDA_TRY(cudaEventRecord(prof_recs[slot].b, s));
 }
 
-extern "C" encf_status encf_profile_enable(encf_ctx* c, int enable) {
+extern "C" encf_status encf_profile_enable(encf_ctx* c, const char* which) {
     if (!c) return ENCF_ERR_ARG;
-    c->prof = enable != 0;
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->prof = which != nullptr;
+    c->prof_all = which && std::string(which) == "*";
+    c->prof_only = which ? which : "";
     return ENCF_OK;
 }
 

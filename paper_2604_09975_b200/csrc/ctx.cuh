@@ -90,7 +90,8 @@ struct encf_ctx {
     int* d_rot_group = nullptr;
     // live kernel timing (encf_profile_*): CUDA events recorded around selected launches
     struct ProfRec { std::string name; cudaEvent_t a, b; uint64_t bytes; };
-    bool prof = false;
+    bool prof = false, prof_all = false;
+    std::string prof_only;
     std::vector<ProfRec> prof_recs;
     std::vector<cudaEvent_t> ev_pool;
     cudaEvent_t prof_event();

@@ -469,26 +469,34 @@ __global__ void weight_slots_kernel(const double* __restrict__ W, int d_in, int 
 
 void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s) {
     size_t total = (size_t)npolys * m.n * c.N;
+    { int _slot; c.prof_begin("add_kernel", s, 0, _slot);
     add_kernel<<<GRID(total), TB, 0, s>>>(a, b, out, total, c.N, m, c.d_mod, sub ? 1 : 0);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 24;
 }
 
 void k_mul(encf_ctx& c, const u64* a, i64 as, const u64* b, i64 bs, u64* out, i64 os, int npolys, const LimbMap& m,
            cudaStream_t s) {
     size_t total = (size_t)npolys * m.n * c.N;
+    { int _slot; c.prof_begin("mul_kernel", s, 0, _slot);
     mul_kernel<<<GRID(total), TB, 0, s>>>(a, as, b, bs, out, os, npolys, c.N, m, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 24;
 }
 
 void k_mul_i(encf_ctx& c, const u64* a, u64* out, int npolys, const LimbMap& m, cudaStream_t s) {
     size_t total = (size_t)npolys * m.n * c.N;
+    { int _slot; c.prof_begin("mul_i_kernel", s, 0, _slot);
     mul_i_kernel<<<GRID(total), TB, 0, s>>>(a, out, total, c.N, m, c.d_mod, c.d_imag, c.d_imag_sh);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 16;
 }
 
 void k_automorph(encf_ctx& c, const u64* in, i64 is, u64* out, i64 os, int npolys, int nlimbs, uint32_t g, cudaStream_t s) {
     size_t total = (size_t)npolys * nlimbs * c.N;
+    { int _slot; c.prof_begin("automorph_kernel", s, 0, _slot);
     automorph_kernel<<<GRID(total), TB, 0, s>>>(in, is, out, os, npolys, nlimbs, c.N, c.logN, g);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 16;
 }
 
@@ -499,37 +507,49 @@ void k_copy(const u64* in, u64* out, size_t words, cudaStream_t s) {
 void k_sample_uniform(encf_ctx& c, u64 seed, u64 stream, u64* out, const LimbMap& m, const int* gids, cudaStream_t s) {
     Gids g;
     for (int i = 0; i < m.n; i++) g.g[i] = gids[i];
+    { int _slot; c.prof_begin("sample_uniform_kernel", s, 0, _slot);
     sample_uniform_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(seed, stream, out, c.N, m, g, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
 void k_sample_small(encf_ctx& c, u64 seed, u64 stream, int kind, u64* out, const LimbMap& m, cudaStream_t s) {
+    { int _slot; c.prof_begin("sample_small_kernel", s, 0, _slot);
     sample_small_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(seed, stream, kind, out, c.N, m, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
 void k_scalar_mul(encf_ctx& c, u64* data, int npolys, const LimbMap& m, const u64* sc, const u64* scs, cudaStream_t s) {
+    { int _slot; c.prof_begin("scalar_mul_kernel", s, 0, _slot);
     scalar_mul_kernel<<<GRID((size_t)npolys * m.n * c.N), TB, 0, s>>>(data, npolys, c.N, m, c.d_mod, sc, scs);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
 void k_mod_reduce(encf_ctx& c, u64* data, int npolys, const LimbMap& m, cudaStream_t s) {
     size_t total = (size_t)npolys * m.n * c.N;
+    { int _slot; c.prof_begin("mod_reduce_kernel", s, 0, _slot);
     mod_reduce_kernel<<<GRID(total), TB, 0, s>>>(data, total, c.N, m, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 16;
 }
 
 void k_rescale_prep(encf_ctx& c, const u64* last, u64* corr, int level, int ncomp, i64 ls, cudaStream_t s) {
+    { int _slot; c.prof_begin("rescale_prep_kernel", s, 0, _slot);
     rescale_prep_kernel<<<GRID((size_t)ncomp * (level - 1) * c.N), TB, 0, s>>>(last, ls, corr, ncomp, level, c.N, c.d_mod,
                                                                             c.rescale[level].d_hmod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
 void k_rescale_finish(encf_ctx& c, const u64* in, i64 is, const u64* corr, u64* out, i64 os, int ncomp, int level,
                       cudaStream_t s) {
     const RescaleTab& t = c.rescale[level];
+    { int _slot; c.prof_begin("rescale_finish_kernel", s, 0, _slot);
     rescale_finish_kernel<<<GRID((size_t)ncomp * (level - 1) * c.N), TB, 0, s>>>(in, is, corr, out, os, ncomp, level, c.N,
                                                                               c.d_mod, t.d_inv, t.d_inv_sh);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (size_t)ncomp * (level - 1) * c.N * 24;
 }
 
@@ -540,7 +560,9 @@ void k_bconv(encf_ctx& c, const u64* in, const LimbMap& im, const u64* vf, const
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
     size_t smem = (size_t)im.n * om.n * sizeof(u64);
     int grid = (c.N + TB - 1) / TB;
+    { int _slot; c.prof_begin("bconv_kernel", s, 0, _slot);
     bconv_kernel<<<grid, TB, smem, s>>>(in, im, vf, vfs, wf, om, op, out, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (size_t)(im.n + om.n) * c.N * 8;
 }
 
@@ -565,20 +587,26 @@ void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const
 void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level, const ModDownTab& t,
                       cudaStream_t s) {
     size_t total = (size_t)level * c.N;
+    { int _slot; c.prof_begin("moddown_finish_kernel", s, 0, _slot);
     moddown_finish_kernel<<<GRID(total), TB, 0, s>>>(b, y, add0, out, level, c.N, c.d_mod, t.d_pinv, t.d_pinv_sh);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * (add0 ? 32 : 24);
 }
 
 void k_tensor_acc(encf_ctx& c, const u64* const* A, const u64* const* B, int nterms, u64* out3, int level, cudaStream_t s) {
     dim3 grid((c.N + TB - 1) / TB, level);
+    { int _slot; c.prof_begin("tensor_acc_kernel", s, 0, _slot);
     tensor_acc_kernel<<<grid, TB, 0, s>>>(A, B, nterms, out3, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (size_t)nterms * 4 * level * c.N * 8 + (size_t)3 * level * c.N * 8;
     c.st_ctmul += nterms;
 }
 
 void k_masked_sum(encf_ctx& c, const u64* const* C, const u64* const* M, int nterms, u64* out, int level, cudaStream_t s) {
     dim3 grid((c.N + TB - 1) / TB, level);
+    { int _slot; c.prof_begin("masked_sum_kernel", s, 0, _slot);
     masked_sum_kernel<<<grid, TB, 0, s>>>(C, M, nterms, out, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (size_t)nterms * 3 * level * c.N * 8 + (size_t)2 * level * c.N * 8;
     c.st_ptmul += nterms;
 }
@@ -609,7 +637,9 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
 }
 
 void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s) {
+    { int _slot; c.prof_begin("export_mask_kernel", s, 0, _slot);
     export_mask_kernel<<<GRID((size_t)level * c.N), TB, 0, s>>>(seed, stream, c0, share, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
@@ -620,9 +650,13 @@ void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots
     int* ovf = (int*)sc.get(1);
     CUDA_TRY(cudaMemsetAsync(A, 0, sizeof(double2) * 2 * c.N, s));
     CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int), s));
+    { int _slot; c.prof_begin("scatter_slots_kernel", s, 0, _slot);
     scatter_slots_kernel<<<GRID(n_slots), TB, 0, s>>>(re, im, n_slots, c.d_rot_group, A);
+    c.prof_end(_slot, s); }
     fft2n(c, A, -1.0, s);
+    { int _slot; c.prof_begin("round_reduce_kernel", s, 0, _slot);
     round_reduce_kernel<<<GRID(c.N), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    c.prof_end(_slot, s); }
     int h_ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -638,9 +672,13 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
     CUDA_TRY(cudaMemsetAsync(ovf, 0, sizeof(int), s));
     WDiag wd;
     for (int i = 0; i < batch; i++) { wd.b[i] = bs[i]; wd.p[i] = ps[i]; wd.u[i] = us[i]; wd.q[i] = qs[i]; }
+    { int _slot; c.prof_begin("weight_slots_kernel", s, 0, _slot);
     weight_slots_kernel<<<dim3(nblocks(c.N / 2, TB, 256), batch), TB, 0, s>>>(dW, d_in, d_out, C, N1, m, wd, c.d_rot_group, A, c.N);
+    c.prof_end(_slot, s); }
     fft2n(c, A, -1.0, s, batch);
+    { int _slot; c.prof_begin("round_reduce_kernel", s, 0, _slot);
     round_reduce_kernel<<<dim3(nblocks(c.N, TB, 256), batch), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    c.prof_end(_slot, s); }
     int h_ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
@@ -650,9 +688,13 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
 void k_decode_limb0(encf_ctx& c, const u64* coeff0, double scale, double* re, double* im, cudaStream_t s) {
     Scratch sc(s);
     double2* A = (double2*)sc.get((size_t)2 * c.N * 2);
+    { int _slot; c.prof_begin("lift_limb0_kernel", s, 0, _slot);
     lift_limb0_kernel<<<GRID(2 * c.N), TB, 0, s>>>(coeff0, c.N, c.d_mod, A);
+    c.prof_end(_slot, s); }
     fft2n(c, A, +1.0, s);
+    { int _slot; c.prof_begin("gather_slots_kernel", s, 0, _slot);
     gather_slots_kernel<<<GRID(c.N / 2), TB, 0, s>>>(A, c.d_rot_group, c.N / 2, 1.0 / scale, re, im);
+    c.prof_end(_slot, s); }
 }
 
 // ====================================================================================== batched key switching
@@ -816,7 +858,9 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
                             const ModDownTab& t, cudaStream_t s) {
     dim3 grid(nblocks((size_t)level * c.N, TB, 256), 1, 2 * nreq);
+    { int _slot; c.prof_begin("moddown_finish_batch_kernel", s, 0, _slot);
     moddown_finish_batch_kernel<<<grid, TB, 0, s>>>(acc, y, O, level, nl, c.N, c.d_mod, t.d_pinv, t.d_pinv_sh);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)nreq * 2 * level * c.N * 8 * 4;
 }
 
@@ -827,19 +871,25 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
     size_t smem = (size_t)im.n * om.n * sizeof(u64);
     dim3 grid((c.N + TB - 1) / TB, npolys);
+    { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
     bconv_batch_kernel<<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)npolys * (im.n + om.n) * c.N * 8;
 }
 
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s) {
     dim3 grid(nblocks(words, TB, 512), n);
+    { int _slot; c.prof_begin("gather_copy_kernel", s, 0, _slot);
     gather_copy_kernel<<<grid, TB, 0, s>>>(C, dst, dst_stride, words, c.N, c.logN);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)n * words * 16;
 }
 
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s) {
     dim3 grid(nblocks((size_t)(level - 1) * c.N, TB, 256), npolys);
+    { int _slot; c.prof_begin("rescale_prep_batch_kernel", s, 0, _slot);
     rescale_prep_batch_kernel<<<grid, TB, 0, s>>>(last, corr, level, c.N, c.d_mod, c.rescale[level].d_hmod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
 }
 
@@ -847,7 +897,9 @@ void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, c
                             cudaStream_t s) {
     const RescaleTab& t = c.rescale[level];
     dim3 grid(nblocks((size_t)(level - 1) * c.N, TB, 256), npolys);
+    { int _slot; c.prof_begin("rescale_finish_batch_kernel", s, 0, _slot);
     rescale_finish_batch_kernel<<<grid, TB, 0, s>>>(In, corr, Out, level, c.N, c.d_mod, t.d_inv, t.d_inv_sh);
+    c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)npolys * (level - 1) * c.N * 8 * 3;
 }
 
@@ -924,7 +976,9 @@ __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restric
 void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
                cudaStream_t s) {
     dim3 grid((c.N + TB - 1) / TB, level, nout);
+    { int _slot; c.prof_begin("sum_csr_kernel", s, 0, _slot);
     sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
     c.st_bytes += (uint64_t)nterms * ncomp * level * c.N * 8 * 2 + (uint64_t)nout * ncomp * level * c.N * 8;
 }
@@ -932,7 +986,9 @@ void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* out
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s) {
     dim3 grid((c.N + TB - 1) / TB, level, nout);
+    { int _slot; c.prof_begin("tensor_csr_kernel", s, 0, _slot);
     tensor_csr_kernel<<<grid, TB, 0, s>>>(pairs, off, outs, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
     c.st_launch++;
     c.st_bytes += (uint64_t)nterms * 4 * level * c.N * 8 + (uint64_t)nout * 3 * level * c.N * 8;
     c.st_ctmul += nterms;

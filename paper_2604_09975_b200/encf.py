@@ -89,7 +89,7 @@ _SIG = {
     "encf_l_conv": [_p, _i32, _i32, _f64, _f64, ctypes.POINTER(_i32)],
     "encf_export_c2m": [_p, ctypes.POINTER(CT), _i32, _u64, _u64, ctypes.POINTER(CT), _p, _p],
     "encf_mod_reduce": [_p, _p, _i32, _i32, _p],
-    "encf_profile_enable": [_p, ctypes.c_int],
+    "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
 }
 for _name, _args in _SIG.items():
@@ -232,8 +232,9 @@ class Context:
     def stats_reset(self):
         _chk(_lib.encf_stats_reset(self.h), "stats_reset")
 
-    def profile(self, enable):
-        _chk(_lib.encf_profile_enable(self.h, 1 if enable else 0), "profile_enable")
+    def profile(self, which):
+        """which: kernel name to time with CUDA events, "*" for all, None to disable."""
+        _chk(_lib.encf_profile_enable(self.h, which.encode() if which else None), "profile_enable")
 
     def profile_read(self, kernel):
         ms, n, by = _f64(), _u64(), _u64()
