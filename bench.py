@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 M, D, H, DH, DFF = 128, 768, 12, 64, 3072
-PROF_KERNELS = ["diag_mac", "ks_inner", "ntt", "add_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
+PROF_KERNELS = ["diag_mac", "ks_inner", "ntt", "bcast_mac", "add_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
                 "export_mask_kernel", "gather_copy_kernel", "masked_sum_kernel", "mod_reduce_kernel",
                 "moddown_finish_batch_kernel", "moddown_finish_kernel", "mul_i_kernel", "mul_kernel",
                 "rescale_finish_batch_kernel", "rescale_prep_batch_kernel", "sum_csr_kernel", "tensor_csr_kernel",
@@ -320,6 +320,8 @@ def run_ours(args):
         "gpu_launches": int(stats["kernel_launches"]),
         "kernel_time_ms_per_step": {k: round(v[0], 3) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0]) if v[1]},
         "kernel_time_sum_ms_per_step": round(sum(v[0] for v in breakdown.values()), 3),
+        "kernel_calls_per_step": {k: v[1] for k, v in breakdown.items() if v[1]},
+        "limb_ntt_per_step": stats["limb_ntt"] // args.steps,
         "host_enqueue_ms_per_step": round(host_enqueue_ms, 3),
         "roofline": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                      "frac": round(achieved / hbm, 4), "traffic": None,

@@ -161,6 +161,12 @@ struct CopyBatch {
 };
 struct KeyLimb { int kl[MAX_LIMBS]; };
 struct SumDev { const u64* ct; const u64* mask; };
+struct BcastArgs {                 // value-kernel broadcast MAC (C8 step 4)
+    const u64* src[128];           // src[i] = Phi^{delta}(p), delta = t0 - dmax + i
+    const u64* mask[64];           // n_u, u < nu
+    u64* out[64];                  // b_{t0 + t}, t < nt
+    int nsrc, nu, nt, dmax;        // dmax = nu - 1
+};
 struct PairDev { const u64* a; const u64* b; i64 as, bs; };   // operands + component strides
 struct OutPos { int pos[MAX_LIMBS]; };
 
@@ -217,6 +223,7 @@ void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* out
                cudaStream_t s);
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s);
+void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s);
 void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ ciphertext-level ops (ks.cu)

@@ -377,17 +377,24 @@ void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, cons
     // 4. b_t = sum_u Phi^{t-u}(p) (.) n_u, rescale
     std::vector<const u64*> nmask(a.d_h);
     for (int u = 0; u < a.d_h; u++) nmask[u] = ev.mask(m, 0, m, u, a.seg_stride, a.H_blk, Lp);
-    std::vector<std::vector<SumTerm>> tb;
-    std::vector<double> scb;
-    for (int l = 0; l < BV; l++)
-        for (int t = 0; t < half; t++) {
-            std::vector<SumTerm> tt;
-            for (int u = 0; u < a.d_h; u++) tt.push_back(SumTerm{pbi(l, t - u)->d, nmask[u]});
-            tb.push_back(tt);
-            scb.push_back(ps[l].scale * ev.mask_scale(Lp));
-        }
     std::vector<DCt> by = ev.alloc_many(BV * half, Lp);
-    ev.sum_many(tb, Lp, 2, by, scb);
+    if (a.d_h > 64) throw EncfError(ENCF_ERR_PLAN_SHAPE, "value: d_h > 64 unsupported");
+    for (int l = 0; l < BV; l++)
+        for (int t0 = 0; t0 < half; t0 += 64) {
+            BcastArgs A;
+            A.nu = a.d_h;
+            A.dmax = a.d_h - 1;
+            A.nt = std::min(64, half - t0);
+            A.nsrc = A.nt + A.dmax;
+            for (int i = 0; i < A.nsrc; i++) A.src[i] = pbi(l, t0 - A.dmax + i)->d;
+            for (int u = 0; u < A.nu; u++) A.mask[u] = nmask[u];
+            for (int t = 0; t < A.nt; t++) {
+                DCt& o = by[l * half + t0 + t];
+                o.scale = ps[l].scale * ev.mask_scale(Lp);
+                A.out[t] = o.d;
+            }
+            k_bcast_mac(ev.c, A, Lp, ev.s);
+        }
     std::vector<DCt> bt = ev.alloc_many(BV * half, Lp - 1);
     ev.rescale_many(ptrs(by), bt);
     // 5. o = sum_t u_t (x) b_t (u_t viewed at b_t's level: mod-drop without a copy), one relin, rescale

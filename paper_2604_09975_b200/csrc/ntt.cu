@@ -42,166 +42,235 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u6
     X = x;
 }
 
-// Radix-4 pass over the lines held in shared memory: two consecutive stages (st, st+1) of every
-// line at once, 4 elements / 4 butterflies / 3 twiddles per work item, shift-only index math.
-// Line l of the tile sits at sm[l * LS + y], y < T = 2^lt.  `st` is the GLOBAL stage of the first of
-// the two, `gb0` the global block offset of line l at stage s0 (block index of element y at global
-// stage st is (boff(l) << (st - s0)) + (y >> (lt - (st - s0) - 1))).
-template <bool kInverse>
-__device__ __forceinline__ void radix4_pass(u64* sm, int LS, int nlines, int lt, int s0, int st, const int* boff,
-                                            const u64* __restrict__ tw, const u64* __restrict__ twp, u64 q, u64 two_q) {
-    const int sl = st - s0;                 // local stage of the first of the two
-    const int lgt = lt - sl - 1;            // log2 of span t at stage st
-    const int lh = lgt - 1;                 // log2(t/2)
-    const int per_line = 1 << (lt - 2);     // work items per line
-    const int total = nlines << (lt - 2);
-    for (int w = threadIdx.x; w < total; w += blockDim.x) {
-        const int l = w >> (lt - 2);
-        const int g = w & (per_line - 1);
-        const int i = g >> lh;              // block of size 2t at stage st
-        const int j = g & ((1 << lh) - 1);
-        const int base = l * LS + (i << (lgt + 1)) + j;
-        const int h = 1 << lh, t = 1 << lgt;
-        const int b1 = (boff[l] << sl) + i;
-        const int m1 = 1 << st;
-        const int b2 = (boff[l] << (sl + 1)) + 2 * i;
-        const int m2 = m1 << 1;
-        u64 a0 = sm[base], a1 = sm[base + h], a2 = sm[base + t], a3 = sm[base + t + h];
-        const u64 W1 = __ldg(tw + m1 + b1), W1p = __ldg(twp + m1 + b1);
-        const u64 Wa = __ldg(tw + m2 + b2), Wap = __ldg(twp + m2 + b2);
-        const u64 Wb = __ldg(tw + m2 + b2 + 1), Wbp = __ldg(twp + m2 + b2 + 1);
-        if (!kInverse) {
-            ct_bfly(a0, a2, W1, W1p, q, two_q);
-            ct_bfly(a1, a3, W1, W1p, q, two_q);
-            ct_bfly(a0, a1, Wa, Wap, q, two_q);
-            ct_bfly(a2, a3, Wb, Wbp, q, two_q);
-        } else {
-            gs_bfly(a0, a1, Wa, Wap, q, two_q);
-            gs_bfly(a2, a3, Wb, Wbp, q, two_q);
-            gs_bfly(a0, a2, W1, W1p, q, two_q);
-            gs_bfly(a1, a3, W1, W1p, q, two_q);
-        }
-        sm[base] = a0; sm[base + h] = a1; sm[base + t] = a2; sm[base + t + h] = a3;
-    }
-}
+// ---------------------------------------------------------------------------------------------
+// Register-resident sub-transforms.  A phase applies LT consecutive stages (global stages
+// [s0, s0+LT)) to independent "lines" of T = 2^LT elements.  A line is handled by TPL threads that
+// each hold E elements in registers:
+//   round A (first EA stages, large spans): thread j holds elements j + TPL*k   (k < E)
+//   round B (last EB stages, small spans):  thread j holds elements ((j*G+g) << EB) + k'
+// with one shared-memory exchange in between (padded: element x of a line sits at x + x/16, line
+// stride LSP = T + T/16 + 1, conflict-free for both mappings and for the transposed column tiles).
+template <int LT>
+struct Geo {
+    static constexpr int EA = (LT + 1) / 2;
+    static constexpr int EB = LT - EA;
+    static constexpr int E = 1 << EA;
+    static constexpr int TPL = 1 << (LT - EA);
+    static constexpr int G = 1 << (EA - EB);
+    static constexpr int T = 1 << LT;
+    static constexpr int LSP = T + T / 16 + 1;
+};
 
-template <bool kInverse>
-__device__ __forceinline__ void radix2_pass(u64* sm, int LS, int nlines, int lt, int s0, int st, const int* boff,
-                                            const u64* __restrict__ tw, const u64* __restrict__ twp, u64 q, u64 two_q) {
-    const int sl = st - s0;
-    const int lgt = lt - sl - 1;
-    const int per_line = 1 << (lt - 1);
-    const int total = nlines << (lt - 1);
-    for (int w = threadIdx.x; w < total; w += blockDim.x) {
-        const int l = w >> (lt - 1);
-        const int g = w & (per_line - 1);
-        const int i = g >> lgt;
-        const int j = g & ((1 << lgt) - 1);
-        const int base = l * LS + (i << (lgt + 1)) + j;
-        const int b = (boff[l] << sl) + i;
-        const int m = 1 << st;
-        const u64 W = __ldg(tw + m + b), Wp = __ldg(twp + m + b);
-        u64 x = sm[base], y = sm[base + (1 << lgt)];
-        if (!kInverse) ct_bfly(x, y, W, Wp, q, two_q);
-        else gs_bfly(x, y, W, Wp, q, two_q);
-        sm[base] = x; sm[base + (1 << lgt)] = y;
-    }
-}
+__device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 
-// Run stages [s0, s0 + lt) of every line (forward ascending, inverse descending) in radix-4 pairs.
-template <bool kInverse>
-__device__ __forceinline__ void run_stages(u64* sm, int LS, int nlines, int lt, int s0, const int* boff,
-                                           const u64* tw, const u64* twp, u64 q, u64 two_q) {
-    if (!kInverse) {
-        int st = s0;
-        for (; st + 1 < s0 + lt; st += 2) {
-            radix4_pass<false>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
-            __syncthreads();
-        }
-        if (st < s0 + lt) {
-            radix2_pass<false>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
-            __syncthreads();
-        }
-    } else {
-        int st = s0 + lt - 1;
-        if (lt & 1) {
-            radix2_pass<true>(sm, LS, nlines, lt, s0, st, boff, tw, twp, q, two_q);
-            __syncthreads();
-            st--;
-        }
-        for (; st - 1 >= s0; st -= 2) {
-            radix4_pass<true>(sm, LS, nlines, lt, s0, st - 1, boff, tw, twp, q, two_q);
-            __syncthreads();
+// Round A: local stages 0..EA-1 (forward ascending / inverse descending).  Local block index of the
+// pair (k, k+hs) at local stage s is k >> (EA - s); global twiddle index 2^(s0+s) + (boff << s) + blk.
+template <int LT, bool INV>
+__device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, const u64* __restrict__ tw,
+                                        const u64* __restrict__ twp, u64 q, u64 two_q) {
+    constexpr int EA = Geo<LT>::EA, E = Geo<LT>::E;
+#pragma unroll
+    for (int ss = 0; ss < EA; ss++) {
+        const int s = INV ? EA - 1 - ss : ss;
+        const int hs = E >> (s + 1);
+        const int base = (1 << (s0 + s)) + (boff << s);
+#pragma unroll
+        for (int k = 0; k < E; k++) {
+            if (k & hs) continue;
+            const int idx = base + (k >> (EA - s));
+            const u64 W = __ldg(tw + idx), Wp = __ldg(twp + idx);
+            if (!INV) ct_bfly(x[k], x[k + hs], W, Wp, q, two_q);
+            else gs_bfly(x[k], x[k + hs], W, Wp, q, two_q);
         }
     }
 }
 
-// Phase A (columns).  Forward: stages 0..s1-1.  Inverse: stages s1-1..0, then x N^{-1}, reduce.
-// Tile: R = 2^s1 rows x CT columns, loaded with 128-byte row segments, stored transposed in shared
-// memory (one padded line per column).
-template <bool kInverse>
-__global__ void __launch_bounds__(kThreads) ntt_cols(NttArgs a) {
+// Round B: local stages EA..LT-1.  Element ((j*G+g) << EB) + k'; block index at local stage EA+r is
+// ((j*G+g) << r) + (k' >> (EB - r)).
+template <int LT, bool INV>
+__device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int boff, const u64* __restrict__ tw,
+                                        const u64* __restrict__ twp, u64 q, u64 two_q) {
+    constexpr int EA = Geo<LT>::EA, EB = Geo<LT>::EB, G = Geo<LT>::G;
+    constexpr int KB = 1 << EB;
+#pragma unroll
+    for (int rr = 0; rr < EB; rr++) {
+        const int r = INV ? EB - 1 - rr : rr;
+        const int hs = KB >> (r + 1);
+        const int base = (1 << (s0 + EA + r)) + (boff << (EA + r));
+#pragma unroll
+        for (int g = 0; g < G; g++) {
+#pragma unroll
+            for (int k = 0; k < KB; k++) {
+                if (k & hs) continue;
+                const int idx = base + (((j * G + g) << r) + (k >> (EB - r)));
+                const u64 W = __ldg(tw + idx), Wp = __ldg(twp + idx);
+                if (!INV) ct_bfly(y[g * KB + k], y[g * KB + k + hs], W, Wp, q, two_q);
+                else gs_bfly(y[g * KB + k], y[g * KB + k + hs], W, Wp, q, two_q);
+            }
+        }
+    }
+}
+
+template <int LT>
+__device__ __forceinline__ void sm_put_a(u64* line, int j, const u64 (&x)[Geo<LT>::E]) {
+#pragma unroll
+    for (int k = 0; k < Geo<LT>::E; k++) line[pad(j + Geo<LT>::TPL * k)] = x[k];
+}
+template <int LT>
+__device__ __forceinline__ void sm_get_a(const u64* line, int j, u64 (&x)[Geo<LT>::E]) {
+#pragma unroll
+    for (int k = 0; k < Geo<LT>::E; k++) x[k] = line[pad(j + Geo<LT>::TPL * k)];
+}
+template <int LT>
+__device__ __forceinline__ void sm_put_b(u64* line, int j, const u64 (&y)[Geo<LT>::E]) {
+    constexpr int EB = Geo<LT>::EB, G = Geo<LT>::G, KB = 1 << EB;
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+        for (int k = 0; k < KB; k++) line[pad(((j * G + g) << EB) + k)] = y[g * KB + k];
+}
+template <int LT>
+__device__ __forceinline__ void sm_get_b(const u64* line, int j, u64 (&y)[Geo<LT>::E]) {
+    constexpr int EB = Geo<LT>::EB, G = Geo<LT>::G, KB = 1 << EB;
+#pragma unroll
+    for (int g = 0; g < G; g++)
+#pragma unroll
+        for (int k = 0; k < KB; k++) y[g * KB + k] = line[pad(((j * G + g) << EB) + k)];
+}
+
+// Phase A (columns of the R x S limb, R = 2^LT rows).  Forward: stages 0..LT-1; inverse: LT-1..0 then
+// x N^{-1} and full reduction.  A CTA owns `lines` consecutive columns (128-byte row segments).
+template <int LT, bool INV>
+__global__ void __launch_bounds__(kThreads) ntt_cols_r(NttArgs a, int lines) {
+    using GG = Geo<LT>;
     extern __shared__ u64 sm[];
-    __shared__ int boff[64];
     const int limb = blockIdx.y, poly = blockIdx.z;
     const int mi = a.map.mod[limb];
-    const ModConst mc = a.mod[mi];
-    const u64 q = mc.q, two_q = 2 * q;
-    const int R = 1 << a.s1, S = 1 << a.s2;
-    const int CT = S < 16 ? S : 16;
-    const int lct = CT == 16 ? 4 : (31 - __clz(CT));
-    const int LS = R + 1;
-    const int c0 = blockIdx.x * CT;
+    const u64 q = a.mod[mi].q, two_q = 2 * q;
+    const int S = 1 << a.s2;
+    const int c0 = blockIdx.x * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
     const u64* tw = a.tw + (size_t)mi * a.N;
     const u64* twp = a.tw_sh + (size_t)mi * a.N;
-    if (threadIdx.x < CT) boff[threadIdx.x] = 0;
-    const int tot = R * CT;
-    for (int e = threadIdx.x; e < tot; e += kThreads) {
-        int r = e >> lct, c = e & (CT - 1);
-        sm[c * LS + r] = g[(i64)r * S + c0 + c];
+    const int tot = GG::T * lines;
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int r = e / lines, c = e - r * lines;
+        sm[c * GG::LSP + pad(r)] = g[(i64)r * S + c0 + c];
     }
     __syncthreads();
-    run_stages<kInverse>(sm, LS, CT, a.s1, 0, boff, tw, twp, q, two_q);
-    const u64 ni = kInverse ? a.ninv[mi] : 0, nip = kInverse ? a.ninv_sh[mi] : 0;
-    for (int e = threadIdx.x; e < tot; e += kThreads) {
-        int r = e >> lct, c = e & (CT - 1);
-        u64 v = sm[c * LS + r];
-        if (kInverse) v = mul_shoup(v, ni, nip, q);
-        g[(i64)r * S + c0 + c] = v;   // forward: lazy [0, 4q) handed to phase B
+    const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
+    u64* line = sm + l * GG::LSP;
+    u64 x[GG::E];
+    if (!INV) {
+        sm_get_a<LT>(line, j, x);
+        round_a<LT, false>(x, 0, 0, tw, twp, q, two_q);
+        sm_put_a<LT>(line, j, x);
+        __syncthreads();
+        sm_get_b<LT>(line, j, x);
+        round_b<LT, false>(x, j, 0, 0, tw, twp, q, two_q);
+        sm_put_b<LT>(line, j, x);
+    } else {
+        sm_get_b<LT>(line, j, x);
+        round_b<LT, true>(x, j, 0, 0, tw, twp, q, two_q);
+        sm_put_b<LT>(line, j, x);
+        __syncthreads();
+        sm_get_a<LT>(line, j, x);
+        round_a<LT, true>(x, 0, 0, tw, twp, q, two_q);
+        const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) x[k] = mul_shoup(x[k], ni, nip, q);
+        sm_put_a<LT>(line, j, x);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+        const int r = e / lines, c = e - r * lines;
+        g[(i64)r * S + c0 + c] = sm[c * GG::LSP + pad(r)];   // forward: lazy [0, 4q) handed to phase B
     }
 }
 
-// Phase B (contiguous chunks of S words).  Forward: stages s1..logN-1 then reduce to [0, q).
-// Inverse: stages logN-1..s1 (lazy [0, 2q) output handed to phase A).
-template <bool kInverse>
-__global__ void __launch_bounds__(kThreads) ntt_rows(NttArgs a) {
+// Phase B (contiguous chunks of S = 2^LT words).  Forward: stages s1..logN-1 then reduce to [0, q);
+// the round-A mapping reads the chunk straight from global memory (coalesced).  Inverse: stages
+// logN-1..s1, lazy [0, 2q) output written straight from the round-A registers.
+template <int LT, bool INV>
+__global__ void __launch_bounds__(kThreads) ntt_rows_r(NttArgs a, int lines) {
+    using GG = Geo<LT>;
     extern __shared__ u64 sm[];
-    __shared__ int boff[64];
     const int limb = blockIdx.y, poly = blockIdx.z;
     const int mi = a.map.mod[limb];
-    const ModConst mc = a.mod[mi];
-    const u64 q = mc.q, two_q = 2 * q;
-    const int S = 1 << a.s2;
-    const int G = kTileElems / S < (1 << a.s1) ? kTileElems / S : (1 << a.s1);   // chunks per CTA
-    const int LS = S + 1;
-    const int ch0 = blockIdx.x * G;
-    u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N + (i64)ch0 * S;
+    const u64 q = a.mod[mi].q, two_q = 2 * q;
+    const int ch0 = blockIdx.x * lines;
+    u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N + (i64)ch0 * GG::T;
     const u64* tw = a.tw + (size_t)mi * a.N;
     const u64* twp = a.tw_sh + (size_t)mi * a.N;
-    if (threadIdx.x < G) boff[threadIdx.x] = ch0 + threadIdx.x;
-    const int tot = G * S;
-    for (int e = threadIdx.x; e < tot; e += kThreads) sm[(e >> a.s2) * LS + (e & (S - 1))] = g[e];
-    __syncthreads();
-    run_stages<kInverse>(sm, LS, G, a.s2, a.s1, boff, tw, twp, q, two_q);
-    for (int e = threadIdx.x; e < tot; e += kThreads) {
-        u64 v = sm[(e >> a.s2) * LS + (e & (S - 1))];
-        if (!kInverse) {
+    const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
+    u64* line = sm + l * GG::LSP;
+    u64* gl = g + (size_t)l * GG::T;
+    const int boff = ch0 + l;
+    const int tot = GG::T * lines;
+    u64 x[GG::E];
+    if (!INV) {
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) x[k] = gl[j + GG::TPL * k];
+        round_a<LT, false>(x, a.s1, boff, tw, twp, q, two_q);
+        sm_put_a<LT>(line, j, x);
+        __syncthreads();
+        sm_get_b<LT>(line, j, x);
+        round_b<LT, false>(x, j, a.s1, boff, tw, twp, q, two_q);
+        sm_put_b<LT>(line, j, x);
+        __syncthreads();
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+            u64 v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
             v = v >= two_q ? v - two_q : v;
             v = v >= q ? v - q : v;
+            g[e] = v;
         }
-        g[e] = v;
+    } else {
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))] = g[e];
+        __syncthreads();
+        sm_get_b<LT>(line, j, x);
+        round_b<LT, true>(x, j, a.s1, boff, tw, twp, q, two_q);
+        sm_put_b<LT>(line, j, x);
+        __syncthreads();
+        sm_get_a<LT>(line, j, x);
+        round_a<LT, true>(x, a.s1, boff, tw, twp, q, two_q);
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = x[k];
     }
+}
+
+template <bool INV>
+void launch_cols(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines) {
+    switch (LT) {
+#define C(LTV) case LTV: ntt_cols_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines); break;
+        C(2) C(3) C(4) C(5) C(6) C(7) C(8)
+#undef C
+        default: throw EncfError(ENCF_ERR_ARG, "ntt: unsupported phase size");
+    }
+}
+
+template <bool INV>
+void launch_rows(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines) {
+    switch (LT) {
+#define C(LTV) case LTV: ntt_rows_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines); break;
+        C(2) C(3) C(4) C(5) C(6) C(7) C(8)
+#undef C
+        default: throw EncfError(ENCF_ERR_ARG, "ntt: unsupported phase size");
+    }
+}
+
+struct PhaseCfg { int lines, threads, blocks; size_t smem; };
+
+PhaseCfg phase_cfg(int LT, int avail) {   // avail = number of lines of one limb in this phase
+    const int EA = (LT + 1) / 2, TPL = 1 << (LT - EA);
+    int lines = kThreads / TPL;
+    if (lines > avail) lines = avail;
+    const int T = 1 << LT;
+    PhaseCfg p;
+    p.lines = lines;
+    p.threads = lines * TPL;
+    p.blocks = avail / lines;
+    p.smem = (size_t)lines * (T + T / 16 + 1) * sizeof(u64);
+    return p;
 }
 
 NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
@@ -221,32 +290,16 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     return a;
 }
 
-size_t smemA(const encf_ctx& c) {
-    const int R = 1 << c.s1, S = 1 << c.s2;
-    const int CT = S < 16 ? S : 16;
-    return (size_t)CT * (R + 1) * sizeof(u64);
-}
-
-size_t smemB(const encf_ctx& c) {
-    const int R = 1 << c.s1, S = 1 << c.s2;
-    const int G = kTileElems / S < R ? kTileElems / S : R;
-    return (size_t)G * (S + 1) * sizeof(u64);
-}
-
 }  // namespace
 
 void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, false);
-    const int S = 1 << c.s2, R = 1 << c.s1;
-    const int CT = S < 16 ? S : 16;
-    dim3 gA(S / CT, b.map.n, b.npolys);
-    int G = kTileElems / S < R ? kTileElems / S : R;
-    dim3 gB(R / G, b.map.n, b.npolys);
+    PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    ntt_cols<false><<<gA, kThreads, smemA(c), s>>>(a);
-    ntt_rows<false><<<gB, kThreads, smemB(c), s>>>(a);
+    launch_cols<false>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
+    launch_rows<false>(c.s2, dim3(B.blocks, b.map.n, b.npolys), B.threads, B.smem, s, a, B.lines);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;
@@ -257,15 +310,11 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, true);
-    const int S = 1 << c.s2, R = 1 << c.s1;
-    const int CT = S < 16 ? S : 16;
-    dim3 gA(S / CT, b.map.n, b.npolys);
-    int G = kTileElems / S < R ? kTileElems / S : R;
-    dim3 gB(R / G, b.map.n, b.npolys);
+    PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    ntt_rows<true><<<gB, kThreads, smemB(c), s>>>(a);
-    ntt_cols<true><<<gA, kThreads, smemA(c), s>>>(a);
+    launch_rows<true>(c.s2, dim3(B.blocks, b.map.n, b.npolys), B.threads, B.smem, s, a, B.lines);
+    launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;

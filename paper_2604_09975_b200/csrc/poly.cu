@@ -993,3 +993,56 @@ void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const*
     c.st_bytes += (uint64_t)nterms * 4 * level * c.N * 8 + (uint64_t)nout * 3 * level * c.N * 8;
     c.st_ctmul += nterms;
 }
+
+// ====================================================================================== value-kernel broadcast MAC
+// b_t = sum_{u < nu} src[t - u] (.) mask_u for t in [t0, t0 + nt), src[delta] = Phi^delta(p_fd) (C8 step 4).
+// Coefficient-tiled: the whole delta window (<= 127 ciphertexts x 2 components) and the nu masks of a
+// 32-coefficient tile sit in shared memory; every bank word is read from HBM once per launch.
+namespace {
+constexpr int BC_T = 32;
+
+__global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, int N, const ModConst* __restrict__ mod) {
+    extern __shared__ u64 sb[];                 // [nsrc][2][BC_T] then [nu][BC_T]
+    const int limb = blockIdx.y, k0 = blockIdx.x * BC_T;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N;
+    const size_t lo = (size_t)limb * N + k0;
+    u64* sm_src = sb;
+    u64* sm_msk = sb + (size_t)A.nsrc * 2 * BC_T;
+    for (int i = threadIdx.x; i < A.nsrc * 2 * BC_T; i += blockDim.x) {
+        int d = i / (2 * BC_T), r = i % (2 * BC_T);
+        int c = r / BC_T, kk = r % BC_T;
+        sm_src[i] = A.src[d][c * cs + lo + kk];
+    }
+    for (int i = threadIdx.x; i < A.nu * BC_T; i += blockDim.x) sm_msk[i] = A.mask[i / BC_T][lo + i % BC_T];
+    __syncthreads();
+    const int kk = threadIdx.x % BC_T, w = threadIdx.x / BC_T, nw = blockDim.x / BC_T;
+    for (int o = w; o < A.nt * 2; o += nw) {
+        const int t = o >> 1, c = o & 1;
+        U128 acc{0, 0};
+        // src index of (t, u) = t + dmax - u  (window starts at delta = t0 - dmax)
+        const u64* sp = sm_src + (size_t)(t + A.dmax) * 2 * BC_T + c * BC_T + kk;
+#pragma unroll 8
+        for (int u = 0; u < A.nu; u++) mac128(acc, sp[-(i64)u * 2 * BC_T], sm_msk[u * BC_T + kk]);
+        A.out[t][c * cs + lo + kk] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+    }
+}
+}  // namespace
+
+void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s) {
+    const size_t smem = ((size_t)A.nsrc * 2 + A.nu) * BC_T * sizeof(u64);
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(bcast_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr = true;
+    }
+    if (smem > 220 * 1024) throw EncfError(ENCF_ERR_PLAN_SHAPE, "bcast_mac: window too large");
+    dim3 grid(c.N / BC_T, level);
+    const uint64_t bytes = ((uint64_t)A.nsrc * 2 + A.nu + (uint64_t)A.nt * 2) * level * c.N * 8;
+    int slot;
+    c.prof_begin("bcast_mac", s, bytes, slot);
+    bcast_mac_kernel<<<grid, 256, smem, s>>>(A, level, c.N, c.d_mod);
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes; c.st_ptmul += (uint64_t)A.nt * A.nu;
+    CUDA_TRY(cudaGetLastError());
+}
