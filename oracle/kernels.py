@@ -347,6 +347,34 @@ def proj_weight_index(plan, b, p, u, q):
     return ((b * plan.N2 + p) * plan.U + u) * plan.N1 + q
 
 
+def projection_partial(ev, plan, xt, w, u0, u1):
+    """C6 steps 1-3 restricted to the giant-step units [u0, u1) (row-major over (b, p)): the bank is
+    built in full, c~_{b,p} and acc_b = sum over the range's p of rot(c~_{b,p}, p N1 m) (p = 0 unrotated).
+    Returns {b: acc_b}.  Used to pin the multi-rank partition."""
+    m, N1 = plan.m, plan.N1
+    bank = []
+    for u in range(plan.U):
+        rots = ev.rot_hoisted(xt[u], [q * m for q in range(1, N1)]) if N1 > 1 else []
+        bank.append([xt[u]] + list(rots))
+    accs = {}
+    for un in range(u0, u1):
+        b, p = divmod(un, plan.N2)
+        cts = [bank[u][q] for u in range(plan.U) for q in range(N1)]
+        pts = [w(b, p, u, q) for u in range(plan.U) for q in range(N1)]
+        c = ev.mac_ptmul(cts, pts)
+        if p:
+            c = ev.rot(c, p * N1 * m)
+        accs[b] = c if b not in accs else ev.add(accs[b], c)
+    return accs
+
+
+def projection_finalize(ev, plan, acc, decomplexify=True):
+    """C6 steps 4-5: z = acc + conj(acc) (scale x2, G2/G3), y = rescale(z)."""
+    if decomplexify:
+        acc = ev.scale_mul(ev.add(acc, ev.conj(acc)), 2.0)
+    return ev.rescale(acc)
+
+
 def projection(ev, plan, xt, w, decomplexify=True):
     """C6 (P:280-301, P:1323-1331; G2/G3):
       1. bank[u][0] = x~_u ; bank[u][q] = HOISTED rot(x~_u, q m), q = 1..N1-1
