@@ -297,53 +297,64 @@ __global__ void __launch_bounds__(TB) masked_sum_kernel(const u64* const* __rest
 
 // ------------------------------------------------------------------------------------ diagonal MAC (projection, C6 step 2)
 // acc[unit][c][l][k] = sum_{uq < nbank} bank[uq][c][l][k] * w[unit][uq][l][k]
-// A CTA owns a 64-coefficient tile of one limb: the bank tile (nbank x 2 x 64 words) is staged once in
-// shared memory and reused by every unit; the plaintext stream is read exactly once (coalesced 512-B
-// rows), accumulators stay in 128-bit registers and are reduced once per unit.
-constexpr int MAC_T = 64;     // coefficients per CTA
-constexpr int MAC_LANES = 4;  // unit lanes per CTA (blockDim = 256)
+// A CTA owns a 32-coefficient tile of one limb: the bank tile (nbank x 2 x 32 words) is staged once in
+// shared memory and reused by every unit; the plaintext stream is read exactly once with 128-bit loads
+// (two coefficients per thread, 16 unit lanes per CTA), accumulators stay in 128-bit registers and are
+// reduced once per unit.
+constexpr int MAC_T = 32;      // coefficients per CTA tile
+constexpr int MAC_TPR = 16;    // threads per tile row (2 coefficients each)
+constexpr int MAC_LANES = 16;  // unit lanes per CTA (blockDim = 256)
 
-__global__ void __launch_bounds__(MAC_T * MAC_LANES) diag_mac_kernel(const u64* __restrict__ bank, int nbank,
-                                                                     const u64* __restrict__ w, int units, i64 wus,
-                                                                     u64* __restrict__ acc, i64 accs, int level, int N,
-                                                                     const ModConst* __restrict__ mod) {
-    extern __shared__ u64 sb[];   // [nbank][2][MAC_T]
+__global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64* __restrict__ bank, int nbank,
+                                                                       const u64* __restrict__ w, int units, i64 wus,
+                                                                       u64* __restrict__ acc, i64 accs, int level, int N,
+                                                                       const ModConst* __restrict__ mod) {
+    extern __shared__ ulonglong2 sb2[];   // [nbank][2][MAC_T / 2]
+    u64* sb = (u64*)sb2;
     const int limb = blockIdx.y;
     const int k0 = blockIdx.x * MAC_T;
     const ModConst mc = mod[limb];
-    const size_t cs = (size_t)level * N;   // component stride inside a ciphertext
-    const size_t bs = 2 * cs;              // ciphertext stride inside the bank
+    const size_t cs = (size_t)level * N;
+    const size_t bs = 2 * cs;
     for (int i = threadIdx.x; i < nbank * 2 * MAC_T; i += blockDim.x) {
         int uq = i / (2 * MAC_T), r = i % (2 * MAC_T);
         int c = r / MAC_T, kk = r % MAC_T;
         sb[i] = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
     }
     __syncthreads();
-    const int kk = threadIdx.x % MAC_T, lane = threadIdx.x / MAC_T;
-    const size_t wl = (size_t)limb * N + k0 + kk;
-    const size_t pstride = (size_t)level * N;   // plaintext stride inside a unit
+    const int kp = threadIdx.x % MAC_TPR, lane = threadIdx.x / MAC_TPR;
+    const size_t wl = (size_t)limb * N + k0 + 2 * kp;
+    const size_t pstride = (size_t)level * N;
     for (int u = blockIdx.z * MAC_LANES + lane; u < units; u += gridDim.z * MAC_LANES) {
         const u64* wu = w + (size_t)u * wus + wl;
-        U128 a0{0, 0}, a1{0, 0};
+        U128 a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};   // [component][coefficient]
         int uq = 0;
         for (; uq + 8 <= nbank; uq += 8) {
-            u64 x[8];
+            ulonglong2 x[8];
 #pragma unroll
-            for (int t = 0; t < 8; t++) x[t] = __ldg(wu + (size_t)(uq + t) * pstride);
+            for (int t = 0; t < 8; t++) x[t] = __ldg((const ulonglong2*)(wu + (size_t)(uq + t) * pstride));
 #pragma unroll
             for (int t = 0; t < 8; t++) {
-                mac128(a0, sb[(uq + t) * 2 * MAC_T + kk], x[t]);
-                mac128(a1, sb[(uq + t) * 2 * MAC_T + MAC_T + kk], x[t]);
+                const ulonglong2 b0 = sb2[(uq + t) * MAC_T + kp];
+                const ulonglong2 b1 = sb2[(uq + t) * MAC_T + MAC_T / 2 + kp];
+                mac128(a00, b0.x, x[t].x);
+                mac128(a01, b0.y, x[t].y);
+                mac128(a10, b1.x, x[t].x);
+                mac128(a11, b1.y, x[t].y);
             }
         }
         for (; uq < nbank; uq++) {
-            u64 x = __ldg(wu + (size_t)uq * pstride);
-            mac128(a0, sb[uq * 2 * MAC_T + kk], x);
-            mac128(a1, sb[uq * 2 * MAC_T + MAC_T + kk], x);
+            const ulonglong2 xx = __ldg((const ulonglong2*)(wu + (size_t)uq * pstride));
+            const ulonglong2 b0 = sb2[uq * MAC_T + kp];
+            const ulonglong2 b1 = sb2[uq * MAC_T + MAC_T / 2 + kp];
+            mac128(a00, b0.x, xx.x);
+            mac128(a01, b0.y, xx.y);
+            mac128(a10, b1.x, xx.x);
+            mac128(a11, b1.y, xx.y);
         }
         u64* o = acc + (size_t)u * accs + wl;
-        o[0] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
-        o[cs] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
+        *(ulonglong2*)o = make_ulonglong2(barrett128(a00, mc.q, mc.rhi, mc.rlo), barrett128(a01, mc.q, mc.rhi, mc.rlo));
+        *(ulonglong2*)(o + cs) = make_ulonglong2(barrett128(a10, mc.q, mc.rhi, mc.rlo), barrett128(a11, mc.q, mc.rhi, mc.rlo));
     }
 }
 
@@ -622,14 +633,14 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     if (smem > 200 * 1024) throw EncfError(ENCF_ERR_PLAN_SHAPE, "diag_mac: bank too large for shared memory");
     int tiles = c.N / MAC_T;
     int zsplit = 1;
-    while ((size_t)tiles * level * zsplit < 148 * 4 && zsplit * MAC_LANES < units) zsplit *= 2;
+    while ((size_t)tiles * level * zsplit < 148 * 8 && zsplit * MAC_LANES < units) zsplit *= 2;
     dim3 grid(tiles, level, zsplit);
     // algorithmic bytes: plaintext stream + bank read once + accumulators written once
     const uint64_t bytes = (uint64_t)units * nbank * level * c.N * 8 + (uint64_t)nbank * 2 * level * c.N * 8 +
                            (uint64_t)units * 2 * level * c.N * 8;
     int slot;
     c.prof_begin("diag_mac", s, bytes, slot);
-    diag_mac_kernel<<<grid, MAC_T * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs, level, c.N, c.d_mod);
+    diag_mac_kernel<<<grid, MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs, level, c.N, c.d_mod);
     c.prof_end(slot, s);
     c.st_launch++;
     c.st_bytes += bytes;
@@ -704,6 +715,8 @@ namespace {
 
 __global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
                                                             LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
+    // Two coefficients (k, k+1), k even, per thread: the Galois gather maps them to the aligned pair
+    // {s, s^1} (brv flips the low bit), so every operand moves with 128-bit loads.
     const int r = blockIdx.z, e = blockIdx.y;
     const u64* __restrict__ ext = B.ext[r];
     const u64* __restrict__ key = B.key[r];
@@ -712,22 +725,32 @@ __global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int 
     const ModConst mc = mod[em.mod[e]];
     const int kle = klm.kl[e];
     const uint32_t mask2n = 2 * N - 1;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-        int src = k;
+    for (int kp = blockIdx.x * blockDim.x + threadIdx.x; 2 * kp < N; kp += gridDim.x * blockDim.x) {
+        const int k = 2 * kp;
+        int base = k, swap = 0;
         if (g != 1) {
             uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
             uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
-            src = brv((int)((e2 - 1) >> 1), logN);
+            int src = brv((int)((e2 - 1) >> 1), logN);
+            base = src & ~1;
+            swap = src & 1;
         }
-        U128 a0{0, 0}, a1{0, 0};
+        U128 a0{0, 0}, a1{0, 0}, b0{0, 0}, b1{0, 0};
         for (int j = 0; j < dnum; j++) {
-            u64 x = ext[((size_t)j * nl + e) * N + src];
+            ulonglong2 x = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base));
+            if (swap) { u64 t = x.x; x.x = x.y; x.y = t; }
             const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            mac128(a0, x, kj[(size_t)kle * N + k]);
-            mac128(a1, x, kj[((size_t)key_nl + kle) * N + k]);
+            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)kle * N + k));
+            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + k));
+            mac128(a0, x.x, k0.x);
+            mac128(b0, x.y, k0.y);
+            mac128(a1, x.x, k1.x);
+            mac128(b1, x.y, k1.y);
         }
-        acc[(size_t)e * N + k] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
-        acc[((size_t)nl + e) * N + k] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
+        *(ulonglong2*)(acc + (size_t)e * N + k) =
+            make_ulonglong2(barrett128(a0, mc.q, mc.rhi, mc.rlo), barrett128(b0, mc.q, mc.rhi, mc.rlo));
+        *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) =
+            make_ulonglong2(barrett128(a1, mc.q, mc.rhi, mc.rlo), barrett128(b1, mc.q, mc.rhi, mc.rlo));
     }
 }
 
@@ -845,7 +868,7 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
         kl.kl[e] = key_limb_of.mod[e];
         em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
     }
-    dim3 grid((c.N + TB - 1) / TB, nl, nreq);
+    dim3 grid((c.N / 2 + TB - 1) / TB, nl, nreq);
     const uint64_t bytes = (uint64_t)nreq * ((uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8);
     int slot;
     c.prof_begin("ks_inner", s, bytes, slot);
