@@ -203,17 +203,30 @@ class Layer:
             out.append(ys[-1])
         return out
 
+    def _mark(self, name):
+        if self.marks is not None:
+            e = self.torch.cuda.Event(enable_timing=True)
+            e.record(self.torch.cuda.current_stream())
+            self.marks.append((name, e))
+
+    marks = None
+
     def step(self, inp):
         """One pass of the hot path.  Returns the exported (masked ct, server share) list."""
         ctx, keys = self.ctx, self.keys
+        self._mark("start")
         y = self.qkv.matmul(keys, inp["x"], self.w_qkv, self.wsc_qkv)
+        self._mark("qkv")
         if self.workload == "qkv":
             return [(c.data, None) for c in y]
         nqk = self.nqk
         Q, K, V = y[:nqk], y[nqk:2 * nqk], y[2 * nqk:]
         S = self.attn.score(keys, Q, K)
+        self._mark("score")
         ex = self._export(self.attn.export_stream(keys, S), 0)
+        self._mark("score_export")
         O = self.attn.value(keys, inp["p"], V)
+        self._mark("value")
         Ore = []
         for o in O:                        # decomplexify the value output (G11): Re o = (o + conj o) / 2
             z = ctx.add(o, ctx.conjugate(keys, o))
@@ -222,10 +235,13 @@ class Layer:
         xo = self._complex_pairs(Ore)
         yo = self.oproj.matmul(keys, xo, self.w_o, float(ctx.q[xo[0].n_limbs - 1]))
         ex += self._export(self._complex_pairs(yo), 100)
+        self._mark("out_proj")
         g1 = self.ff1.matmul(keys, inp["f1"], self.w_1, float(ctx.q[L_FF - 1]))
         ex += self._export(self._complex_pairs(g1), 200)
+        self._mark("ff1")
         g2 = self.ff2.matmul(keys, inp["f2"], self.w_2, float(ctx.q[L_FF - 1]))
         ex += self._export(self._complex_pairs(g2), 300)
+        self._mark("ff2")
         return ex
 
     def download(self, outs):
@@ -250,6 +266,12 @@ def run_ours(args):
     layer.step(layer.dev_inputs)
     torch.cuda.synchronize()
     breakdown = {k: ctx.profile_read(k) for k in PROF_KERNELS}
+    ctx.profile(None)
+    layer.marks = []
+    layer.step(layer.dev_inputs)
+    torch.cuda.synchronize()
+    phase_ms = {layer.marks[i][0]: round(layer.marks[i - 1][1].elapsed_time(layer.marks[i][1]), 3) for i in range(1, len(layer.marks))}
+    layer.marks = None
     # timed region: only the dominant kernel is bracketed by events (live roofline)
     ctx.stats_reset()
     ctx.profile("diag_mac")
@@ -326,6 +348,7 @@ def run_ours(args):
         "kernel_time_ms_per_step": {k: round(v[0], 3) for k, v in sorted(breakdown.items(), key=lambda kv: -kv[1][0]) if v[1]},
         "kernel_time_sum_ms_per_step": round(sum(v[0] for v in breakdown.values()), 3),
         "kernel_calls_per_step": {k: v[1] for k, v in breakdown.items() if v[1]},
+        "phase_ms": phase_ms,
         "limb_ntt_per_step": stats["limb_ntt"] // args.steps,
         "host_enqueue_ms_per_step": round(host_enqueue_ms, 3),
         "roofline": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",

@@ -11,6 +11,14 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr"]
 
 
+def build_variant(out, defines):
+    """Compile a variant library (kernel experiments; not used by the product path)."""
+    nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+    srcs = [os.path.join(CSRC, s) for s in SOURCES]
+    subprocess.check_call([nvcc] + FLAGS + ["-D" + d for d in defines] + ["-o", out] + srcs)
+    return out
+
+
 def build(force=False, verbose=False):
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]

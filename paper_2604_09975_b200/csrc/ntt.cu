@@ -140,8 +140,11 @@ __device__ __forceinline__ void sm_get_b(const u64* line, int j, u64 (&y)[Geo<LT
 
 // Phase A (columns of the R x S limb, R = 2^LT rows).  Forward: stages 0..LT-1; inverse: LT-1..0 then
 // x N^{-1} and full reduction.  A CTA owns `lines` consecutive columns (128-byte row segments).
+#ifndef NTT_MINB
+#define NTT_MINB 4
+#endif
 template <int LT, bool INV>
-__global__ void __launch_bounds__(kThreads) ntt_cols_r(NttArgs a, int lines) {
+__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int lines) {
     using GG = Geo<LT>;
     extern __shared__ u64 sm[];
     const int limb = blockIdx.y, poly = blockIdx.z;
@@ -192,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) ntt_cols_r(NttArgs a, int lines) {
 // the round-A mapping reads the chunk straight from global memory (coalesced).  Inverse: stages
 // logN-1..s1, lazy [0, 2q) output written straight from the round-A registers.
 template <int LT, bool INV>
-__global__ void __launch_bounds__(kThreads) ntt_rows_r(NttArgs a, int lines) {
+__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int lines) {
     using GG = Geo<LT>;
     extern __shared__ u64 sm[];
     const int limb = blockIdx.y, poly = blockIdx.z;

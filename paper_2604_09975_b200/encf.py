@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libencf.so")
+_SO = os.environ.get("ENCF_LIB_OVERRIDE") or os.path.join(_HERE, "libencf.so")   # override: kernel-variant experiments only
 PARAMS_DIR = os.path.join(os.path.dirname(_HERE), "params")
 
 if not os.path.exists(_SO):
