@@ -168,7 +168,9 @@ class Layer:
         self.host_inputs = {"x": [self._enc(z, L_QKV, 10 + i) for i, z in enumerate(PK.complexified_inputs(X, M, 256, n))]}
         if workload == "layer":
             P = synth.attention_probs(H, M, synth.seed_data(4) + seed_off)
-            self.host_inputs["p"] = [self._enc(z, L_V_P, 20 + i) for i, z in enumerate(PK.folded_diag_blocks(P, M, self.attn.H_blk, self.attn.seg_stride, n))]
+            # P_fd (the M2C import of the softmax output) at Delta * 2^7 (DESIGN.md R-PSCALE)
+            self.host_inputs["p"] = [self._enc(z, L_V_P, 20 + i, scale=self.sc * 2.0 ** 7)
+                                     for i, z in enumerate(PK.folded_diag_blocks(P, M, self.attn.H_blk, self.attn.seg_stride, n))]
             X1 = synth.fixed_point_uniform((M, D), synth.seed_data(5) + seed_off)
             self.host_inputs["f1"] = [self._enc(z, L_FF, 30 + i) for i, z in enumerate(PK.complexified_inputs(X1, M, 256, n))]
             X2 = synth.fixed_point_uniform((M, DFF), synth.seed_data(6) + seed_off, 0.0, 1.0)
@@ -178,9 +180,9 @@ class Layer:
         self.Lconv = ctx.l_conv()
         self.mask_seed = synth.seed_mask(0)
 
-    def _enc(self, z, L, seed):
+    def _enc(self, z, L, seed, scale=None):
         """Client-side encryption; returns (pinned host words, scale)."""
-        ct = self.ctx.encrypt(self.keys, self.ctx.encode(z, self.sc, L), seed)
+        ct = self.ctx.encrypt(self.keys, self.ctx.encode(z, scale or self.sc, L), seed)
         return (ct.data.cpu().pin_memory(), ct.n_comp, ct.n_limbs, ct.scale)
 
     def _to_dev(self, h):

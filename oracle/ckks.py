@@ -30,7 +30,7 @@ PARAMS_DIR = os.path.join(os.path.dirname(_HERE), "params")
 def build_oracle(force=False):
     src = os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(src):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-o", _SO, src])
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fopenmp", "-shared", "-fPIC", "-o", _SO, src, "-lm"])
     return _SO
 
 
@@ -53,6 +53,7 @@ def _load():
         "o_from_signed_batch": ([i64, p, i64, p, p], None),
         "o_automorph_batch": ([i64, p, i64, u64, p, p], None),
         "o_bconv": ([i64, i64, p, p, p, i64, p, p, p], None),
+        "o_bconv_round": ([i64, i64, p, p, p, i64, p, p, p, p, p], None),
         "o_rescale": ([i64, p, i64, p, p], None),
         "o_prng_draw": ([u64, u64, u64], u64),
         "o_sample_uniform": ([u64, u64, i64, p, p, i64, p], None),
@@ -265,6 +266,25 @@ def bconv(x, qin, qout, N):
     x = np.ascontiguousarray(x, dtype=np.uint64)
     out = np.empty((len(qout), N), dtype=np.uint64)
     LIB.o_bconv(N, len(qin), _ptr(_u64(qin)), _ptr(x), _ptr(_u64(vfac)), len(qout), _ptr(_u64(qout)), _ptr(_u64(wfac)), _ptr(out))
+    return out
+
+
+def bconv_round(x, qin, qout, N):
+    """Fast base conversion WITH the rounding correction (DESIGN.md R-MODDOWN): r = round(sum_i v_i/q_i) from a
+    59-bit fixed-point estimate; returns the centred residue of x mod Q' = prod(qin) in every target modulus
+    (exact unless sum_i v_i/q_i lies within 2^-56 of a half-integer)."""
+    Qp = 1
+    for q in qin:
+        Qp *= q
+    vfac = [pow(Qp // q, -1, q) for q in qin]
+    wfac = [(Qp // qi) % t for qi in qin for t in qout]
+    qprod = [Qp % t for t in qout]
+    assert all(q > (1 << 59) for q in qin), "rounded BConv needs input moduli > 2^59"
+    cfix = [(1 << 123) // q for q in qin]
+    x = np.ascontiguousarray(x, dtype=np.uint64)
+    out = np.empty((len(qout), N), dtype=np.uint64)
+    LIB.o_bconv_round(N, len(qin), _ptr(_u64(qin)), _ptr(x), _ptr(_u64(vfac)), len(qout), _ptr(_u64(qout)), _ptr(_u64(wfac)),
+                      _ptr(_u64(qprod)), _ptr(_u64(cfix)), _ptr(out))
     return out
 
 
@@ -517,9 +537,11 @@ def ks_inner(P, ext_digits, key, L):
 
 
 def moddown(P, b, L):
-    """ModDown (C4): y = fastBConv_{P->Q}([b]_P);  out_i = (b_i - y_i) * P^{-1} mod q_i  (floor style)."""
+    """ModDown (C4 with DESIGN.md R-MODDOWN): y = the centred residue [b]_P obtained by the rounded fast
+    BConv_{P->Q};  out_i = (b_i - y_i) * P^{-1} mod q_i  =  round(b / P)  (SURVEY's floor version leaves
+    an error u in [0, K) per coefficient, ~2^-19 relative after a projection -- above the 2^-20 target)."""
     N = P.N
-    y = bconv(b[L:], P.p, P.q[:L], N)
+    y = bconv_round(b[L:], P.p, P.q[:L], N)
     pinv = [pow(P.P % q, -1, q) for q in P.q[:L]]
     return pmul_scalar(psub(b[:L], y, P.q[:L], N), pinv, P.q[:L], N)
 

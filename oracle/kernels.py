@@ -164,7 +164,10 @@ class Ev:
             if key not in cache or cache[key][0] is not ct:
                 cache[key] = (ct, [O.ntt(ct.c[c], mods, N) for c in range(2)])
             ctn = cache[key][1]
-            ptn = O.ntt(pt.m, mods, N)
+            pkey = ("pt", id(pt))
+            if pkey not in cache or cache[pkey][0] is not pt:
+                cache[pkey] = (pt, O.ntt(pt.m, mods, N))
+            ptn = cache[pkey][1]
             for c in range(2):
                 acc[c] = O.padd(acc[c], O.pmul_pointwise(ctn[c], ptn, mods, N), mods, N)
         scale = cts[0].scale * pts[0].scale
@@ -439,7 +442,7 @@ def score_qk_slots(Qp, plan, l):
     return seg_column_pack(Qp, plan.m, plan.C, l, plan.n)
 
 
-def score(ev, plan, qs, ks):
+def score(ev, plan, qs, ks, ts=None):
     """C7.  Per block l: Q bank Psi^{-s} (s < beta), K bank Psi^{j beta}, Psi^{m/2 + j beta} (j < g/2),
     all hoisted from one ModUp each.  Per t = j beta + s < m/2:
       T_t = sum_l q_{-s} (x) (k_{j beta} + i k_{m/2 + j beta})   lazy tensor sum, ONE relin, rescale (G6)
@@ -454,7 +457,7 @@ def score(ev, plan, qs, ks):
         kk = Psi_hoisted(ev, ks[l], kt, m, N_seg)
         kb.append({t: c for t, c in zip(kt, kk)})
     S = []
-    for t in range(m // 2):
+    for t in (range(m // 2) if ts is None else ts):
         j, s = t // beta, t % beta
         pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in range(plan.B)]
         T = ev.rescale(ev.relin(ev.tensor_sum(pairs)))
@@ -567,7 +570,7 @@ def value_p_slots(Ph, plan, l):
     return z
 
 
-def value(ev, plan, ps, vs):
+def value(ev, plan, ps, vs, blocks=None):
     """C8 (P:425-455 with G9: u_t = Psi^{+t} u):
       1. uu = v (.) e_all - i (rot(v, m/2)(.)h_{m/2} + rot(v, -m/2)(.)u_{m/2}), ONE rescale
       2. U bank: u_t = Psi^{t}(uu), t = 0..m/2-1 (hoisted)
@@ -577,7 +580,7 @@ def value(ev, plan, ps, vs):
     m, N_seg = plan.m, plan.N_seg
     half = m // 2
     outs = []
-    for l in range(plan.B_V):
+    for l in (range(plan.B_V) if blocks is None else blocks):
         v, p = vs[l], ps[l]
         Lv = v.L
         rv = ev.rot_hoisted(v, [half, half - m])
@@ -591,12 +594,9 @@ def value(ev, plan, ps, vs):
         Lp = p.L
         bt = []
         for t in range(half):
-            acc = None
-            for u in range(plan.d_h):
-                desc = (0, m, u, plan.seg_stride, plan.H_blk)
-                y = ev.ptmul(pb[t - u], ev.mask(desc, Lp, m))
-                acc = y if acc is None else ev.add(acc, y)
-            bt.append(ev.rescale(acc))
+            cts = [pb[t - u] for u in range(plan.d_h)]
+            pts = [ev.mask((0, m, u, plan.seg_stride, plan.H_blk), Lp, m) for u in range(plan.d_h)]
+            bt.append(ev.rescale(ev.mac_ptmul(cts, pts)))     # sum_u Phi^{t-u}(p) (.) n_u (exact modular sum)
         Lb = bt[0].L
         pairs = [(ev.mod_drop(ub[t], Lb) if ub[t].L > Lb else ub[t], bt[t]) for t in range(half)]
         outs.append(ev.rescale(ev.relin(ev.tensor_sum(pairs))))

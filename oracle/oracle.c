@@ -16,6 +16,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 
 typedef uint64_t u64;
 typedef int64_t i64;
@@ -189,6 +190,30 @@ void o_bconv(i64 N, i64 n_in, const u64* qin, const u64* in, const u64* vfac,
                 acc = addmod(acc, mulmod(v, wfac[i * n_out + t] % qt, qt), qt);
             }
             out[t * N + k] = acc;
+        }
+    }
+}
+
+/* Rounded fast base conversion (ModDown with the rounding correction, DESIGN.md R-MODDOWN):
+ *   v_i = [x_i * vfac_i]_{q_i};  f_i = floor(v_i * cfix_i / 2^64) with cfix_i = floor(2^123 / q_i)
+ *   (a 59-bit fixed-point estimate of v_i / q_i; needs q_i > 2^59);
+ *   r = (sum_i f_i + 2^58) >> 59  = round(sum_i v_i / q_i) up to 2^-56;
+ *   y_t = sum_i v_i * wfac[i][t] - r * qprod[t]  (mod t),  qprod[t] = Q' mod t.
+ * y is the CENTRED residue of x mod Q', so (b - y) / P is round(b / P). */
+void o_bconv_round(i64 N, i64 n_in, const u64* qin, const u64* in, const u64* vfac,
+                   i64 n_out, const u64* qout, const u64* wfac, const u64* qprod, const u64* cfix, u64* out) {
+    #pragma omp parallel for
+    for (i64 t = 0; t < n_out; t++) {
+        u64 qt = qout[t];
+        for (i64 k = 0; k < N; k++) {
+            u64 acc = 0, fsum = 0;
+            for (i64 i = 0; i < n_in; i++) {
+                u64 v = mulmod(in[i * N + k], vfac[i], qin[i]);
+                fsum += (u64)(((u128)v * cfix[i]) >> 64);
+                acc = addmod(acc, mulmod(v, wfac[i * n_out + t] % qt, qt), qt);
+            }
+            u64 r = (fsum + (1ULL << 58)) >> 59;
+            out[t * N + k] = submod(acc, mulmod(r % qt, qprod[t] % qt, qt), qt);
         }
     }
 }

@@ -164,6 +164,20 @@ static void build(encf_ctx& c, const encf_params* p) {
         }
         md.d_vfac = upload(c, vf); md.d_vfac_sh = upload(c, vfs); md.d_wfac = upload(c, wf);
         md.d_pinv = upload(c, pinv); md.d_pinv_sh = upload(c, pinvs);
+        std::vector<u64> pmod(lev);
+        for (int i = 0; i < lev; i++) {
+            u64 qi = c.mods[i], P = 1;
+            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            pmod[i] = P;
+        }
+        md.d_pmod = upload(c, pmod);
+        std::vector<u64> cfix(c.K);
+        for (int k = 0; k < c.K; k++) {
+            u64 pk = c.mods[c.L + k];
+            if (pk <= (1ull << 59)) throw EncfError(ENCF_ERR_ARG, "special primes must exceed 2^59 (rounded ModDown)");
+            cfix[k] = (u64)(((unsigned __int128)1 << 123) / pk);
+        }
+        md.d_cfix = upload(c, cfix);
         c.moddown[lev] = md;
         // Rescale (C5) dropping q_{lev-1}
         if (lev >= 2) {

@@ -55,6 +55,8 @@ struct ModDownTab {       // P -> Q_L
     u64* d_wfac;          // [K][L] (P/p_k) mod q_i
     u64* d_pinv;          // [L]   P^{-1} mod q_i
     u64* d_pinv_sh;
+    u64* d_pmod;          // [L]   P mod q_i        (rounding correction, DESIGN.md R-MODDOWN)
+    u64* d_cfix;          // [K]   floor(2^123 / p_k)
 };
 
 struct RescaleTab {       // drop q_{L-1}
@@ -214,7 +216,8 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
                             const ModDownTab& t, cudaStream_t s);
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
-                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s);
+                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s,
+                   const u64* corr = nullptr, const u64* cfix = nullptr);
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s);
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s);
 void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,

@@ -74,7 +74,8 @@ u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint
     return ext;
 }
 
-// Inner product + ModDown (C4) for a list of requests at level L.
+// Inner product + ModDown (C4 with the rounding correction R-MODDOWN: out = round(b / P)) for a list of
+// requests at level L.
 void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
     const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L);
     const int ML = keys->max_level, key_nl = ML + K;
@@ -102,7 +103,7 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
         ntt_inverse(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);     // [b]_P -> coefficient form
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
-                      pos.data(), 2 * n, s);
+                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix);                        // rounded: y = centred [b]_P
         ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
         k_moddown_finish_batch(c, acc, y, O, n, L, nl, md, s);
         c.st_ks += n;

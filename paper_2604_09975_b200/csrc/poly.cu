@@ -775,11 +775,14 @@ __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u
 }
 
 // bconv over a batch of polynomials: input poly p at in + p*in_stride, output at out + p*out_stride.
+// corr != nullptr: rounded conversion (ModDown, DESIGN.md R-MODDOWN): r = (sum_i umulhi(v_i, cfix_i) + 2^58) >> 59
+// with cfix_i = floor(2^123 / q_i) (= round(sum_i v_i / q_i), bit-identical to oracle.c o_bconv_round), y_t -= r * corr_t.
 __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
                                                          const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
                                                          const u64* __restrict__ wfac, LimbMap om, OutPos op,
                                                          u64* __restrict__ out, i64 out_stride, int N,
-                                                         const ModConst* __restrict__ mod) {
+                                                         const ModConst* __restrict__ mod, const u64* __restrict__ corr,
+                                                         const u64* __restrict__ cfix) {
     extern __shared__ u64 sw[];
     const int nin = im.n, nout = om.n;
     for (int i = threadIdx.x; i < nin * nout; i += blockDim.x) sw[i] = wfac[i];
@@ -795,13 +798,23 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
                 v[i] = mul_shoup(in[(size_t)i * N + k], vfac[i], vfac_sh[i], qi);
             }
         }
+        u64 r = 0;
+        if (corr) {   // r = round(sum_i v_i / q_i) from 59-bit fixed-point fractions (oracle.c o_bconv_round)
+            u64 fsum = 0;
+#pragma unroll
+            for (int i = 0; i < 16; i++)
+                if (i < nin) fsum += umulhi(v[i], cfix[i]);
+            r = (fsum + (1ull << 58)) >> 59;
+        }
         for (int t = 0; t < nout; t++) {
             ModConst mc = mod[om.mod[t]];
             U128 acc{0, 0};
 #pragma unroll
             for (int i = 0; i < 16; i++)
                 if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
-            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+            u64 y = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+            if (corr) y = sub_mod(y, mulmod_barrett(r, corr[t], mc.q, mc.rhi, mc.rlo), mc.q);
+            out[(size_t)op.pos[t] * N + k] = y;
         }
     }
 }
@@ -888,14 +901,15 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 }
 
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
-                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s) {
+                   const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
+                   const u64* cfix) {
     if (im.n > 16) throw EncfError(ENCF_ERR_ARG, "bconv: at most 16 input limbs");
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
     size_t smem = (size_t)im.n * om.n * sizeof(u64);
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
-    bconv_batch_kernel<<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod);
+    bconv_batch_kernel<<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix);
     c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)npolys * (im.n + om.n) * c.N * 8;
 }

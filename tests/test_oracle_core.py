@@ -176,10 +176,18 @@ def test_moddown_explicit_crt():
     for q in P.q[:L]:
         Q *= q
     ov, _ = O.crt_lift(out[:, :K], P.q[:L], centered=False)
+    ties = 0
     for k in range(K):
-        assert (bv[k] - bp[k]) % P.P == 0
-        base = (bv[k] - bp[k]) // P.P
-        assert any(ov[k] == (base - u) % Q for u in range(len(P.p))), k
+        # rounded ModDown: out = round(b / P) (floor or ceil only when b/P sits within 1e-12 of a half-integer)
+        lo = bv[k] // P.P
+        frac = (bv[k] - lo * P.P) / P.P
+        want = lo + (1 if frac >= 0.5 else 0)
+        if abs(frac - 0.5) < 1e-12:
+            ties += 1
+            assert ov[k] in (lo % Q, (lo + 1) % Q)
+        else:
+            assert ov[k] == want % Q, k
+    assert ties <= 1
 
 
 def test_rescale_is_round_division():
