@@ -103,6 +103,15 @@ static void build(encf_ctx& c, const encf_params* p) {
     CUDA_TRY(cudaMemcpy(c.d_mod, mc.data(), M * sizeof(ModConst), cudaMemcpyHostToDevice));
     c.d_psi = upload(c, psi); c.d_psi_sh = upload(c, psi_sh);
     c.d_ipsi = upload(c, ipsi); c.d_ipsi_sh = upload(c, ipsi_sh);
+    {   // interleaved {w, w'} pairs: one 128-bit load per twiddle in the NTT kernels
+        std::vector<u64> f(2 * psi.size()), iv(2 * psi.size());
+        for (size_t i = 0; i < psi.size(); i++) {
+            f[2 * i] = psi[i]; f[2 * i + 1] = psi_sh[i];
+            iv[2 * i] = ipsi[i]; iv[2 * i + 1] = ipsi_sh[i];
+        }
+        c.d_tw2 = upload(c, f);
+        c.d_itw2 = upload(c, iv);
+    }
     c.d_ninv = upload(c, ninv); c.d_ninv_sh = upload(c, ninv_sh);
     c.d_imag = upload(c, im); c.d_imag_sh = upload(c, im_sh);
 
@@ -168,7 +177,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         for (int i = 0; i < lev; i++) {
             u64 qi = c.mods[i], P = 1;
             for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
-            pmod[i] = P;
+            pmod[i] = P ? qi - P : 0;      // stored negated: the kernel adds r * (q_i - P mod q_i)
         }
         md.d_pmod = upload(c, pmod);
         std::vector<u64> cfix(c.K);

@@ -55,7 +55,7 @@ struct ModDownTab {       // P -> Q_L
     u64* d_wfac;          // [K][L] (P/p_k) mod q_i
     u64* d_pinv;          // [L]   P^{-1} mod q_i
     u64* d_pinv_sh;
-    u64* d_pmod;          // [L]   P mod q_i        (rounding correction, DESIGN.md R-MODDOWN)
+    u64* d_pmod;          // [L]   q_i - (P mod q_i) (rounding correction, DESIGN.md R-MODDOWN)
     u64* d_cfix;          // [K]   floor(2^123 / p_k)
 };
 
@@ -80,6 +80,7 @@ struct encf_ctx {
     std::vector<u64> psi;               // chosen primitive 2N-th roots
     ModConst* d_mod = nullptr;          // [L+K]
     u64 *d_psi = nullptr, *d_psi_sh = nullptr, *d_ipsi = nullptr, *d_ipsi_sh = nullptr;   // [L+K][N]
+    u64 *d_tw2 = nullptr, *d_itw2 = nullptr;        // [L+K][N][2] interleaved {w, w'} (fwd / inv)
     u64 *d_ninv = nullptr, *d_ninv_sh = nullptr;    // [L+K]
     u64 *d_imag = nullptr, *d_imag_sh = nullptr;    // [L+K]  psi^{N/2} (a 4th root of unity)
     std::vector<std::vector<ModUpTab>> modup;       // [level][digit]

@@ -22,6 +22,7 @@ struct NttArgs {
     const ModConst* mod;
     const u64* tw;       // psi_brv (fwd) or ipsi_brv (inv): [mods][N]
     const u64* tw_sh;
+    const ulonglong2* tw2;   // interleaved {w, w'}: [mods][N]
     const u64* ninv;
     const u64* ninv_sh;
     int N, logN, s1, s2;
@@ -66,8 +67,8 @@ __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 // Round A: local stages 0..EA-1 (forward ascending / inverse descending).  Local block index of the
 // pair (k, k+hs) at local stage s is k >> (EA - s); global twiddle index 2^(s0+s) + (boff << s) + blk.
 template <int LT, bool INV>
-__device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, const u64* __restrict__ tw,
-                                        const u64* __restrict__ twp, u64 q, u64 two_q) {
+__device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, const ulonglong2* __restrict__ tw2,
+                                        u64 q, u64 two_q) {
     constexpr int EA = Geo<LT>::EA, E = Geo<LT>::E;
 #pragma unroll
     for (int ss = 0; ss < EA; ss++) {
@@ -78,9 +79,9 @@ __device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, 
         for (int k = 0; k < E; k++) {
             if (k & hs) continue;
             const int idx = base + (k >> (EA - s));
-            const u64 W = __ldg(tw + idx), Wp = __ldg(twp + idx);
-            if (!INV) ct_bfly(x[k], x[k + hs], W, Wp, q, two_q);
-            else gs_bfly(x[k], x[k + hs], W, Wp, q, two_q);
+            const ulonglong2 T = __ldg(tw2 + idx);
+            if (!INV) ct_bfly(x[k], x[k + hs], T.x, T.y, q, two_q);
+            else gs_bfly(x[k], x[k + hs], T.x, T.y, q, two_q);
         }
     }
 }
@@ -88,8 +89,8 @@ __device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, 
 // Round B: local stages EA..LT-1.  Element ((j*G+g) << EB) + k'; block index at local stage EA+r is
 // ((j*G+g) << r) + (k' >> (EB - r)).
 template <int LT, bool INV>
-__device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int boff, const u64* __restrict__ tw,
-                                        const u64* __restrict__ twp, u64 q, u64 two_q) {
+__device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int boff, const ulonglong2* __restrict__ tw2,
+                                        u64 q, u64 two_q) {
     constexpr int EA = Geo<LT>::EA, EB = Geo<LT>::EB, G = Geo<LT>::G;
     constexpr int KB = 1 << EB;
 #pragma unroll
@@ -103,9 +104,9 @@ __device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int
             for (int k = 0; k < KB; k++) {
                 if (k & hs) continue;
                 const int idx = base + (((j * G + g) << r) + (k >> (EB - r)));
-                const u64 W = __ldg(tw + idx), Wp = __ldg(twp + idx);
-                if (!INV) ct_bfly(y[g * KB + k], y[g * KB + k + hs], W, Wp, q, two_q);
-                else gs_bfly(y[g * KB + k], y[g * KB + k + hs], W, Wp, q, two_q);
+                const ulonglong2 T = __ldg(tw2 + idx);
+                if (!INV) ct_bfly(y[g * KB + k], y[g * KB + k + hs], T.x, T.y, q, two_q);
+                else gs_bfly(y[g * KB + k], y[g * KB + k + hs], T.x, T.y, q, two_q);
             }
         }
     }
@@ -153,11 +154,11 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
     const int S = 1 << a.s2;
     const int c0 = blockIdx.x * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
-    const u64* tw = a.tw + (size_t)mi * a.N;
-    const u64* twp = a.tw_sh + (size_t)mi * a.N;
+    const ulonglong2* tw2 = a.tw2 + (size_t)mi * a.N;
     const int tot = GG::T * lines;
+    const int lgl = 31 - __clz(lines);
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int r = e / lines, c = e - r * lines;
+        const int r = e >> lgl, c = e & (lines - 1);
         sm[c * GG::LSP + pad(r)] = g[(i64)r * S + c0 + c];
     }
     __syncthreads();
@@ -166,19 +167,19 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
     u64 x[GG::E];
     if (!INV) {
         sm_get_a<LT>(line, j, x);
-        round_a<LT, false>(x, 0, 0, tw, twp, q, two_q);
+        round_a<LT, false>(x, 0, 0, tw2, q, two_q);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, 0, 0, tw, twp, q, two_q);
+        round_b<LT, false>(x, j, 0, 0, tw2, q, two_q);
         sm_put_b<LT>(line, j, x);
     } else {
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, 0, 0, tw, twp, q, two_q);
+        round_b<LT, true>(x, j, 0, 0, tw2, q, two_q);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, 0, 0, tw, twp, q, two_q);
+        round_a<LT, true>(x, 0, 0, tw2, q, two_q);
         const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
 #pragma unroll
         for (int k = 0; k < GG::E; k++) x[k] = mul_shoup(x[k], ni, nip, q);
@@ -186,7 +187,7 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
     }
     __syncthreads();
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int r = e / lines, c = e - r * lines;
+        const int r = e >> lgl, c = e & (lines - 1);
         g[(i64)r * S + c0 + c] = sm[c * GG::LSP + pad(r)];   // forward: lazy [0, 4q) handed to phase B
     }
 }
@@ -203,8 +204,7 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
     const u64 q = a.mod[mi].q, two_q = 2 * q;
     const int ch0 = blockIdx.x * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N + (i64)ch0 * GG::T;
-    const u64* tw = a.tw + (size_t)mi * a.N;
-    const u64* twp = a.tw_sh + (size_t)mi * a.N;
+    const ulonglong2* tw2 = a.tw2 + (size_t)mi * a.N;
     const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
     u64* line = sm + l * GG::LSP;
     u64* gl = g + (size_t)l * GG::T;
@@ -214,11 +214,11 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
     if (!INV) {
 #pragma unroll
         for (int k = 0; k < GG::E; k++) x[k] = gl[j + GG::TPL * k];
-        round_a<LT, false>(x, a.s1, boff, tw, twp, q, two_q);
+        round_a<LT, false>(x, a.s1, boff, tw2, q, two_q);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, a.s1, boff, tw, twp, q, two_q);
+        round_b<LT, false>(x, j, a.s1, boff, tw2, q, two_q);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         for (int e = threadIdx.x; e < tot; e += blockDim.x) {
@@ -231,11 +231,11 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
         for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))] = g[e];
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, a.s1, boff, tw, twp, q, two_q);
+        round_b<LT, true>(x, j, a.s1, boff, tw2, q, two_q);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, a.s1, boff, tw, twp, q, two_q);
+        round_a<LT, true>(x, a.s1, boff, tw2, q, two_q);
 #pragma unroll
         for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = x[k];
     }
@@ -284,6 +284,7 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.mod = c.d_mod;
     a.tw = inv ? c.d_ipsi : c.d_psi;
     a.tw_sh = inv ? c.d_ipsi_sh : c.d_psi_sh;
+    a.tw2 = (const ulonglong2*)(inv ? c.d_itw2 : c.d_tw2);
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
     a.N = c.N;

@@ -812,9 +812,8 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
 #pragma unroll
             for (int i = 0; i < 16; i++)
                 if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
-            u64 y = barrett128(acc, mc.q, mc.rhi, mc.rlo);
-            if (corr) y = sub_mod(y, mulmod_barrett(r, corr[t], mc.q, mc.rhi, mc.rlo), mc.q);
-            out[(size_t)op.pos[t] * N + k] = y;
+            if (corr) mac128(acc, r, corr[t]);     // corr_t = t - (Q' mod t): adds -r Q' (mod t) before the one reduction
+            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
         }
     }
 }
