@@ -276,7 +276,7 @@ def run_ours(args):
     layer.marks = None
     # timed region: only the dominant kernel is bracketed by events (live roofline)
     ctx.stats_reset()
-    ctx.profile("diag_mac")
+    ctx.profile("ntt,diag_mac")
     barrier(ws)
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -298,7 +298,7 @@ def run_ours(args):
     ms_total = max_over_ranks(ms_total, ws)
     ms_step = ms_total / args.steps
     stats = ctx.stats()
-    prof = {k: ctx.profile_read(k) for k in ("diag_mac",)}
+    prof = {k: ctx.profile_read(k) for k in ("diag_mac", "ntt")}
     ctx.profile(None)
     # e2e through the public API: H2D of the step's encrypted inputs from pinned memory, D2H of the outputs
     e2e = None
@@ -321,8 +321,15 @@ def run_ours(args):
     peaks = _j.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
     mac_ms, mac_n, mac_b = prof["diag_mac"]
-    dom = {"kernel": "diag_mac", "ms": mac_ms, "n": mac_n, "bytes": mac_b}
     achieved = (mac_b / mac_n) / ((mac_ms / mac_n) * 1e-3) / 1e9 if mac_n else 0.0
+    # dominant kernel by time: the NTT (IMAD/ALU issue-bound).  Algorithmic work = butterflies
+    # (N/2 log2 N per limb transform); peak from unit counts x clock.
+    ntt_ms, ntt_n, ntt_bytes = prof["ntt"]
+    limb_ntts = ntt_bytes / (65536 * 8 * 4)                  # the library counts 4 limb-polys of traffic per limb transform
+    bfly = limb_ntts * (65536 // 2) * 16
+    ntt_achieved = bfly / (ntt_ms * 1e-3) / 1e9 if ntt_ms else 0.0
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    ntt_peak = 148 * 4.0 * sm_mhz * 1e6 / 1e9               # 4 butterflies / clk / SM (fma-pipe bound, 16 IMAD each)
     ks_total = stats["keyswitch"] / args.steps
     line = {
         "metric": "BERT-base layer CKKS linear latency (ms) & key-switches/s at N=2^16; HBM roofline %",
@@ -353,9 +360,17 @@ def run_ours(args):
         "phase_ms": phase_ms,
         "limb_ntt_per_step": stats["limb_ntt"] // args.steps,
         "host_enqueue_ms_per_step": round(host_enqueue_ms, 3),
-        "roofline": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                     "frac": round(achieved / hbm, 4), "traffic": None,
-                     "note": "algorithmic bytes per launch (plaintext stream + bank + accumulators) / CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs"},
+        "roofline": {"bound": "alu", "kernel": "ntt (ntt_cols_r + ntt_rows_r)", "achieved": round(ntt_achieved, 1),
+                     "peak": round(ntt_peak, 1), "unit": "Gbutterfly/s", "frac": round(ntt_achieved / ntt_peak, 4),
+                     "traffic": None, "share_of_step": round(ntt_ms / args.steps / ms_step, 3),
+                     "note": "dominant kernel by device time; achieved = NTT butterflies (N/2 log2 N per limb) / CUDA-event time of "
+                             "every transform in the timed steps; peak = 148 SMs x 4 butterflies/clk (64 IMAD lanes/clk/SM / 16 IMAD "
+                             "per 64-bit Shoup butterfly) x sm_max_mhz (DESIGN.md ALU roofline)"},
+        "roofline_hbm": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": 24.9e9,
+                         "note": "the HBM-bound plaintext-diagonal MAC: algorithmic bytes per launch (plaintext stream + bank + "
+                                 "accumulators) / CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs (burst copy); traffic = "
+                                 "ncu dram read+write bytes of the QKV launch (24.8 GB algorithmic; profiles/r01_summary.md)"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "setup_s": round(layer.setup_s, 1),
@@ -440,7 +455,7 @@ def run_reference(args):
 
 
 # schedule counts of one layer (filled from a GPU run's encf_stats; used only by --impl reference)
-LAYER_COUNTS = {"keyswitch": 2014, "ptmul_terms": 31200}
+LAYER_COUNTS = {"keyswitch": 1971, "ptmul_terms": 30208}
 
 
 def main():

@@ -86,7 +86,7 @@ const char* encf_last_error(void);                 /* thread-local detail of the
 encf_status encf_stats(encf_ctx* ctx, encf_counters* out);
 encf_status encf_stats_reset(encf_ctx* ctx);
 /* Live kernel timing: while enabled, CUDA events are recorded on the launching stream around every
- * launch of the kernel named `which` ("*" = every kernel; NULL disables).  Names: "diag_mac",
+ * launch of the kernels named in `which` (comma-separated; "*" = every kernel; NULL disables).  Names: "diag_mac",
  * "ks_inner", "ntt" (one fwd/inv transform = a pair of launches) and the *_kernel launchers.
  * encf_profile_read synchronises on those events and returns the summed device time, the launch
  * count and the summed ALGORITHMIC bytes (DESIGN.md §Roofline, 0 where not defined) for `kernel`,

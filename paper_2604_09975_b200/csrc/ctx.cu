@@ -254,7 +254,18 @@ cudaEvent_t encf_ctx::prof_event() {
 void encf_ctx::prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int& slot) {
     slot = -1;
     if (!prof) return;
-    if (!prof_all && prof_only != name) return;
+    if (!prof_all) {   // comma-separated list of kernel names
+        const std::string n(name);
+        size_t pos = 0;
+        bool hit = false;
+        while (pos <= prof_only.size()) {
+            size_t e = prof_only.find(',', pos);
+            if (e == std::string::npos) e = prof_only.size();
+            if (prof_only.compare(pos, e - pos, n) == 0 && e - pos == n.size()) { hit = true; break; }
+            pos = e + 1;
+        }
+        if (!hit) return;
+    }
     std::lock_guard<std::mutex> lk(mu);
     ProfRec r{name, prof_event(), prof_event(), bytes};
     CUDA_TRY(cudaEventRecord(r.a, s));
