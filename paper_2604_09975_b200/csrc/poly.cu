@@ -776,43 +776,49 @@ __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u
 
 // bconv over a batch of polynomials: input poly p at in + p*in_stride, output at out + p*out_stride.
 // corr != nullptr: rounded conversion (ModDown, DESIGN.md R-MODDOWN): r = (sum_i umulhi(v_i, cfix_i) + 2^58) >> 59
-// with cfix_i = floor(2^123 / q_i) (= round(sum_i v_i / q_i), bit-identical to oracle.c o_bconv_round), y_t -= r * corr_t.
+// with cfix_i = floor(2^123 / q_i) (= round(sum_i v_i / q_i), bit-identical to oracle.c o_bconv_round); the
+// correction -r Q' is folded into the 128-bit accumulator (corr_t = t - Q' mod t).  Templated on the input
+// count so no predicated-off multiply is issued.
+template <int NIN>
 __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
                                                          const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
                                                          const u64* __restrict__ wfac, LimbMap om, OutPos op,
                                                          u64* __restrict__ out, i64 out_stride, int N,
                                                          const ModConst* __restrict__ mod, const u64* __restrict__ corr,
                                                          const u64* __restrict__ cfix) {
-    extern __shared__ u64 sw[];
-    const int nin = im.n, nout = om.n;
-    for (int i = threadIdx.x; i < nin * nout; i += blockDim.x) sw[i] = wfac[i];
+    extern __shared__ u64 sw[];   // [NIN][nout] wfac, then [nout] corr
+    const int nout = om.n;
+    for (int i = threadIdx.x; i < NIN * nout; i += blockDim.x) sw[i] = wfac[i];
+    if (corr)
+        for (int i = threadIdx.x; i < nout; i += blockDim.x) sw[NIN * nout + i] = corr[i];
     __syncthreads();
     in += (size_t)blockIdx.y * in_stride;
     out += (size_t)blockIdx.y * out_stride;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-        u64 v[16];
+    u64 qin[NIN], vf[NIN], vfs[NIN], cf[NIN];
 #pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (i < nin) {
-                u64 qi = mod[im.mod[i]].q;
-                v[i] = mul_shoup(in[(size_t)i * N + k], vfac[i], vfac_sh[i], qi);
-            }
-        }
+    for (int i = 0; i < NIN; i++) {
+        qin[i] = mod[im.mod[i]].q;
+        vf[i] = vfac[i];
+        vfs[i] = vfac_sh[i];
+        cf[i] = corr ? cfix[i] : 0;
+    }
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+        u64 v[NIN];
+#pragma unroll
+        for (int i = 0; i < NIN; i++) v[i] = mul_shoup(in[(size_t)i * N + k], vf[i], vfs[i], qin[i]);
         u64 r = 0;
-        if (corr) {   // r = round(sum_i v_i / q_i) from 59-bit fixed-point fractions (oracle.c o_bconv_round)
+        if (corr) {
             u64 fsum = 0;
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (i < nin) fsum += umulhi(v[i], cfix[i]);
+            for (int i = 0; i < NIN; i++) fsum += umulhi(v[i], cf[i]);
             r = (fsum + (1ull << 58)) >> 59;
         }
         for (int t = 0; t < nout; t++) {
-            ModConst mc = mod[om.mod[t]];
+            const ModConst mc = mod[om.mod[t]];
             U128 acc{0, 0};
 #pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
-            if (corr) mac128(acc, r, corr[t]);     // corr_t = t - (Q' mod t): adds -r Q' (mod t) before the one reduction
+            for (int i = 0; i < NIN; i++) mac128(acc, v[i], sw[i * nout + t]);
+            if (corr) mac128(acc, r, sw[NIN * nout + t]);
             out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
         }
     }
@@ -902,15 +908,20 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
                    const u64* cfix) {
-    if (im.n > 16) throw EncfError(ENCF_ERR_ARG, "bconv: at most 16 input limbs");
+    if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
-    size_t smem = (size_t)im.n * om.n * sizeof(u64);
+    size_t smem = (size_t)(im.n + 1) * om.n * sizeof(u64);
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
-    bconv_batch_kernel<<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix);
+    switch (im.n) {
+#define B(NI) case NI: bconv_batch_kernel<NI><<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix); break;
+        B(1) B(2) B(3) B(4) B(5) B(6) B(7) B(8) B(9) B(10) B(11) B(12) B(13) B(14) B(15) B(16)
+#undef B
+    }
     c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)npolys * (im.n + om.n) * c.N * 8;
+    CUDA_TRY(cudaGetLastError());
 }
 
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s) {
