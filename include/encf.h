@@ -155,7 +155,7 @@ encf_status encf_complexify(encf_ctx* ctx, const encf_ct* re, const encf_ct* im,
  * s0 + k*sstride (k < scount) of an m-row segment grid, encoded at scale q_{L-1} at level L.
  * The context caches them; encf_mask_put installs an externally encoded plaintext (host coefficient
  * form [L][N]) for a descriptor -- used by the parity tests to feed the oracle's encodings. */
-typedef struct { int32_t m, r0, r1, s0, sstride, scount, level; } encf_mask_desc;
+typedef struct { int32_t m, r0, r1, s0, sstride, scount, level, ext; } encf_mask_desc;   /* ext = 1: [level + K][N], also reduced mod the special primes (lazy key switching, DESIGN R-LAZY) */
 encf_status encf_mask_put(encf_ctx* ctx, const encf_mask_desc* desc, const uint64_t* coeffs /*host [L][N]*/);
 encf_status encf_mask_clear(encf_ctx* ctx);
 

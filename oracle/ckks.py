@@ -53,7 +53,7 @@ def _load():
         "o_from_signed_batch": ([i64, p, i64, p, p], None),
         "o_automorph_batch": ([i64, p, i64, u64, p, p], None),
         "o_bconv": ([i64, i64, p, p, p, i64, p, p, p], None),
-        "o_bconv_round": ([i64, i64, p, p, p, i64, p, p, p, p, p], None),
+        "o_bconv_round": ([i64, i64, p, p, p, i64, p, p, p, p, p, p], None),
         "o_rescale": ([i64, p, i64, p, p], None),
         "o_prng_draw": ([u64, u64, u64], u64),
         "o_sample_uniform": ([u64, u64, i64, p, p, i64, p], None),
@@ -279,12 +279,12 @@ def bconv_round(x, qin, qout, N):
     vfac = [pow(Qp // q, -1, q) for q in qin]
     wfac = [(Qp // qi) % t for qi in qin for t in qout]
     qprod = [Qp % t for t in qout]
-    assert all(q > (1 << 59) for q in qin), "rounded BConv needs input moduli > 2^59"
-    cfix = [(1 << 123) // q for q in qin]
+    csh = [63 - q.bit_length() for q in qin]
+    cfix = [(1 << (123 - s)) // q for q, s in zip(qin, csh)]
     x = np.ascontiguousarray(x, dtype=np.uint64)
     out = np.empty((len(qout), N), dtype=np.uint64)
     LIB.o_bconv_round(N, len(qin), _ptr(_u64(qin)), _ptr(x), _ptr(_u64(vfac)), len(qout), _ptr(_u64(qout)), _ptr(_u64(wfac)),
-                      _ptr(_u64(qprod)), _ptr(_u64(cfix)), _ptr(out))
+                      _ptr(_u64(qprod)), _ptr(_u64(cfix)), _ptr(_u64(csh)), _ptr(out))
     return out
 
 
@@ -544,6 +544,43 @@ def moddown(P, b, L):
     y = bconv_round(b[L:], P.p, P.q[:L], N)
     pinv = [pow(P.P % q, -1, q) for q in P.q[:L]]
     return pmul_scalar(psub(b[:L], y, P.q[:L], N), pinv, P.q[:L], N)
+
+
+def lift_P(P, c, L):
+    """P * c in the extended basis Q_L u P: (P mod q_i) c_i on the q-limbs, 0 on the p-limbs."""
+    N = P.N
+    out = np.zeros((L + len(P.p), N), dtype=np.uint64)
+    out[:L] = pmul_scalar(c, [P.P % q for q in P.q[:L]], P.q[:L], N)
+    return out
+
+
+def moddown_rescale(P, x, L):
+    """Merged ModDown + rescale (DESIGN.md R-LAZY): x over Q_L u P (coefficient form) ->
+    round(x / (P q_{L-1})) mod Q_{L-1}, through ONE rounded fast base conversion from the basis
+    B' = {q_{L-1}, p_0..p_{K-1}} to Q_{L-1}."""
+    N = P.N
+    bp = [P.q[L - 1]] + P.p
+    rows = np.concatenate([x[L - 1:L], x[L:]])
+    y = bconv_round(rows, bp, P.q[:L - 1], N)
+    Bp = P.P * P.q[L - 1]
+    inv = [pow(Bp % q, -1, q) for q in P.q[:L - 1]]
+    return pmul_scalar(psub(x[:L - 1], y, P.q[:L - 1], N), inv, P.q[:L - 1], N)
+
+
+def rotate_hoisted_ext(P, keys, ct, rs):
+    """Hoisted rotations WITHOUT ModDown (DESIGN.md R-LAZY): for each r the extended-basis pair
+    (P sigma_g(c0) + b0, b1) over Q_L u P, whose ModDown is the ordinary hoisted rotation."""
+    L, N = ct.L, P.N
+    mods, emods = P.q[:L], P.ext_mods(L)
+    ext = modup(P, ct.c[1], L)
+    outs = []
+    for r in rs:
+        g = galois_rot(P, r)
+        ext_g = [automorph(dj, g, emods, N) for dj in ext]
+        b0, b1 = ks_inner(P, ext_g, keys.key_at(g, L), L)
+        c0 = automorph(ct.c[0], g, mods, N)
+        outs.append(np.stack([padd(b0, lift_P(P, c0, L), emods, N), b1]))
+    return outs
 
 
 def keyswitch(P, d, key, L):

@@ -148,6 +148,45 @@ class Ev:
         """Scale bookkeeping only (the 1/2 of decomplexification, G3): no arithmetic."""
         return O.Ct(ct.c, ct.scale * f)
 
+    # -- lazy (extended-basis) operations, DESIGN.md R-LAZY
+    def mask_ext(self, desc, L, m=None):
+        """The mask plaintext of (desc, L) extended to the special primes (same integer coefficients)."""
+        m = m or self.m
+        key = ("ext", tuple(desc), L, m)
+        if key not in self.masks:
+            z = mask_slots(desc, m, self.P.n)
+            coeffs = O.encode_coeffs(z, float(self.P.q[L - 1]), self.P.N)
+            self.masks[key] = O.Pt(O.from_signed(coeffs, self.P.ext_mods(L), self.P.N), float(self.P.q[L - 1]))
+        return self.masks[key]
+
+    def mask_scale(self, L):
+        return float(self.P.q[L - 1])
+
+    def rot_hoisted_ext(self, ct, rs):
+        self.ledger["rot"] += sum(1 for r in rs if int(r) % self.P.n)
+        self.ledger["modup_hoisted"] += 1
+        return [ExtCt(c, ct.L, ct.scale) for c in O.rotate_hoisted_ext(self.P, self.keys, ct, rs)]
+
+    def ext_masked_sum(self, xs, pts, scale):
+        """sum_i xs[i] (.) pts[i] over Q_L u P (ring products via the oracle NTT; exact)."""
+        self.ledger["ptmul"] += len(xs)
+        L = xs[0].L
+        emods = self.P.ext_mods(L)
+        N = self.P.N
+        acc = [np.zeros((len(emods), N), np.uint64) for _ in range(2)]
+        for x, pt in zip(xs, pts):
+            ptn = O.ntt(pt.m, emods, N)
+            for c in range(2):
+                acc[c] = O.padd(acc[c], O.pmul_pointwise(O.ntt(x.c[c], emods, N), ptn, emods, N), emods, N)
+        return ExtCt(np.stack([O.intt(a, emods, N) for a in acc]), L, scale)
+
+    def moddown_rescale(self, y):
+        self.ledger["moddown"] += 1
+        self.ledger["rescale"] += 1
+        L = y.L
+        c = np.stack([O.moddown_rescale(self.P, y.c[i], L) for i in range(2)])
+        return O.Ct(c, y.scale / float(self.P.q[L - 1]))
+
     def mac_ptmul(self, cts, pts):
         """sum_i cts[i] (.) pts[i]  (exact modular sum of ring products; evaluated in the oracle's NTT
         domain -- the sum of ring products is unique)."""
@@ -183,6 +222,15 @@ class Ev:
             t = self.tensor(a, b)
             out = t if out is None else O.add(self.P, out, t)
         return out
+
+
+class ExtCt:
+    """A ciphertext over the extended basis Q_L u P (coefficient form [2][L+K][N]), scale = the scale of
+    the message it carries after the pending division by P."""
+
+    def __init__(self, c, L, scale):
+        self.c, self.L, self.scale = c, L, float(scale)
+        self.ncomp = 2
 
 
 class FakeCt:
@@ -249,6 +297,24 @@ class CountEv:
         self.ledger["ptmul"] += len(cts)
         return FakeCt(cts[0].L, 1.0)
 
+    def mask_ext(self, desc, L, m=None):
+        return FakeCt(L, 1.0, 1)
+
+    def mask_scale(self, L):
+        return 1.0
+
+    def rot_hoisted_ext(self, ct, rs):
+        return self.rot_hoisted(ct, rs)
+
+    def ext_masked_sum(self, xs, pts, scale):
+        self.ledger["ptmul"] += len(xs)
+        return FakeCt(xs[0].L, scale)
+
+    def moddown_rescale(self, y):
+        self.ledger["moddown"] += 1
+        self.ledger["rescale"] += 1
+        return FakeCt(y.L - 1, y.scale)
+
     def tensor_sum(self, pairs):
         for _ in pairs:
             self.ledger["ctmul"] += 1
@@ -264,6 +330,8 @@ def Phi(ev, x, delta, m):
 def Psi_hoisted(ev, x, ts, m, N_seg, seg0=0, nseg=None):
     """Psi^t for every t in ts from ONE hoisted ModUp of x (Alg A.2):
        Psi^t(x) = rot(x; t)(.)h_t + rot(x; (t-m) mod n)(.)u_t, then rescale.
+    The two rotations stay in the extended basis Q_L u P (no ModDown), are masked there and then
+    divided by P q_{L-1} at once (lazy ModDown merged with the rescale, DESIGN.md R-LAZY).
     t = 0 (mod m) is realised as x(.)h_0 then rescale (no rotation), so every bank entry sits at the
     same level and scale (reading R-PSI0).  Optional segment restriction merges a trailing
     segment mask (used by the score align step)."""
@@ -273,18 +341,16 @@ def Psi_hoisted(ev, x, ts, m, N_seg, seg0=0, nseg=None):
     for t in tt:
         if t:
             steps += [t, t - m]
-    rots = ev.rot_hoisted(x, steps) if steps else []
+    rots = ev.rot_hoisted_ext(x, steps) if steps else []
     out, i = [], 0
     for t in tt:
         hd, ud = psi_masks(t, m, N_seg, seg0, nseg)
         if t == 0:
-            y = ev.ptmul(x, ev.mask(hd, L, m))
+            out.append(ev.rescale(ev.ptmul(x, ev.mask(hd, L, m))))
         else:
-            a = ev.ptmul(rots[i], ev.mask(hd, L, m))
-            b = ev.ptmul(rots[i + 1], ev.mask(ud, L, m))
-            y = ev.add(a, b)
+            y = ev.ext_masked_sum([rots[i], rots[i + 1]], [ev.mask_ext(hd, L, m), ev.mask_ext(ud, L, m)], x.scale * ev.mask_scale(L))
+            out.append(ev.moddown_rescale(y))
             i += 2
-        out.append(ev.rescale(y))
     return out
 
 

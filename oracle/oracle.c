@@ -195,13 +195,14 @@ void o_bconv(i64 N, i64 n_in, const u64* qin, const u64* in, const u64* vfac,
 }
 
 /* Rounded fast base conversion (ModDown with the rounding correction, DESIGN.md R-MODDOWN):
- *   v_i = [x_i * vfac_i]_{q_i};  f_i = floor(v_i * cfix_i / 2^64) with cfix_i = floor(2^123 / q_i)
- *   (a 59-bit fixed-point estimate of v_i / q_i; needs q_i > 2^59);
+ *   v_i = [x_i * vfac_i]_{q_i};  f_i = floor((v_i << s_i) * cfix_i / 2^64), s_i = 63 - bitlen(q_i),
+ *   cfix_i = floor(2^(123 - s_i) / q_i)  (a 59-bit fixed-point estimate of v_i / q_i for any q_i < 2^63);
  *   r = (sum_i f_i + 2^58) >> 59  = round(sum_i v_i / q_i) up to 2^-56;
  *   y_t = sum_i v_i * wfac[i][t] - r * qprod[t]  (mod t),  qprod[t] = Q' mod t.
  * y is the CENTRED residue of x mod Q', so (b - y) / P is round(b / P). */
 void o_bconv_round(i64 N, i64 n_in, const u64* qin, const u64* in, const u64* vfac,
-                   i64 n_out, const u64* qout, const u64* wfac, const u64* qprod, const u64* cfix, u64* out) {
+                   i64 n_out, const u64* qout, const u64* wfac, const u64* qprod, const u64* cfix, const u64* csh,
+                   u64* out) {
     #pragma omp parallel for
     for (i64 t = 0; t < n_out; t++) {
         u64 qt = qout[t];
@@ -209,7 +210,7 @@ void o_bconv_round(i64 N, i64 n_in, const u64* qin, const u64* in, const u64* vf
             u64 acc = 0, fsum = 0;
             for (i64 i = 0; i < n_in; i++) {
                 u64 v = mulmod(in[i * N + k], vfac[i], qin[i]);
-                fsum += (u64)(((u128)v * cfix[i]) >> 64);
+                fsum += (u64)(((u128)(v << csh[i]) * cfix[i]) >> 64);
                 acc = addmod(acc, mulmod(v, wfac[i * n_out + t] % qt, qt), qt);
             }
             u64 r = (fsum + (1ULL << 58)) >> 59;

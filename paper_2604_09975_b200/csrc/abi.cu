@@ -394,12 +394,13 @@ encf_status encf_mask_put(encf_ctx* c, const encf_mask_desc* d, const uint64_t* 
         need(c && d && coeffs, ENCF_ERR_ARG, "mask_put: null argument");
         level_ok(c, d->level);
         const int N = c->N, L = d->level;
+        const LimbMap lm = d->ext ? c->extmap(L) : c->qmap(L);
         u64* pt = nullptr;
-        CUDA_TRY(cudaMalloc(&pt, (size_t)L * N * 8));
-        CUDA_TRY(cudaMemcpy(pt, coeffs, (size_t)L * N * 8, cudaMemcpyHostToDevice));
-        ntt_forward(*c, PolyBatch{pt, 0, 1, c->qmap(L)}, 0);
+        CUDA_TRY(cudaMalloc(&pt, (size_t)lm.n * N * 8));
+        CUDA_TRY(cudaMemcpy(pt, coeffs, (size_t)lm.n * N * 8, cudaMemcpyHostToDevice));
+        ntt_forward(*c, PolyBatch{pt, 0, 1, lm}, 0);
         CUDA_TRY(cudaDeviceSynchronize());
-        MaskKey key{d->m, d->r0, d->r1, d->s0, d->sstride, d->scount, d->level};
+        MaskKey key{d->m, d->r0, d->r1, d->s0, d->sstride, d->scount, d->level, d->ext ? 1 : 0};
         std::lock_guard<std::mutex> lk(c->mu);
         auto it = c->masks.find(key);
         if (it != c->masks.end()) cudaFree(it->second);

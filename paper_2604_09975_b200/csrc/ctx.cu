@@ -119,6 +119,7 @@ static void build(encf_ctx& c, const encf_params* p) {
     c.modup.assign(c.L + 1, {});
     c.moddown.assign(c.L + 1, {});
     c.rescale.assign(c.L + 1, {});
+    c.mdr.assign(c.L + 1, {});
     for (int lev = 1; lev <= c.L; lev++) {
         LimbMap ext = c.extmap(lev);
         for (int j = 0; j < c.dnum(lev); j++) {
@@ -180,14 +181,52 @@ static void build(encf_ctx& c, const encf_params* p) {
             pmod[i] = P ? qi - P : 0;      // stored negated: the kernel adds r * (q_i - P mod q_i)
         }
         md.d_pmod = upload(c, pmod);
-        std::vector<u64> cfix(c.K);
+        std::vector<u64> cfix(c.K), csh(c.K);
         for (int k = 0; k < c.K; k++) {
             u64 pk = c.mods[c.L + k];
-            if (pk <= (1ull << 59)) throw EncfError(ENCF_ERR_ARG, "special primes must exceed 2^59 (rounded ModDown)");
-            cfix[k] = (u64)(((unsigned __int128)1 << 123) / pk);
+            csh[k] = 63 - (64 - __builtin_clzll(pk));
+            cfix[k] = (u64)(((unsigned __int128)1 << (123 - csh[k])) / pk);
         }
         md.d_cfix = upload(c, cfix);
+        md.d_csh = upload(c, csh);
+        std::vector<u64> pl(lev), pls(lev);
+        for (int i = 0; i < lev; i++) {
+            u64 qi = c.mods[i], P = 1;
+            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            pl[i] = P; pls[i] = shoup_pre(P, qi);
+        }
+        md.d_pl = upload(c, pl); md.d_pl_sh = upload(c, pls);
         c.moddown[lev] = md;
+        // Merged ModDown + rescale (R-LAZY): B' = {q_{lev-1}, p_0..p_{K-1}} -> q_0..q_{lev-2}
+        if (lev >= 2) {
+            std::vector<u64> bp;
+            bp.push_back(c.mods[lev - 1]);
+            for (int k = 0; k < c.K; k++) bp.push_back(c.mods[c.L + k]);
+            const int nb = (int)bp.size(), nt = lev - 1;
+            std::vector<u64> vf(nb), vfs(nb), wf((size_t)nb * nt), corr(nt), cf(nb), cs(nb), inv(nt), invs(nt);
+            for (int a = 0; a < nb; a++) {
+                u64 ba = bp[a], prod = 1;
+                for (int b2 = 0; b2 < nb; b2++) if (b2 != a) prod = h_mulmod(prod, bp[b2] % ba, ba);
+                vf[a] = h_invmod(prod, ba); vfs[a] = shoup_pre(vf[a], ba);
+                for (int t = 0; t < nt; t++) {
+                    u64 qt = c.mods[t], pr = 1;
+                    for (int b2 = 0; b2 < nb; b2++) if (b2 != a) pr = h_mulmod(pr, bp[b2] % qt, qt);
+                    wf[(size_t)a * nt + t] = pr;
+                }
+                cs[a] = 63 - (64 - __builtin_clzll(ba));
+                cf[a] = (u64)(((unsigned __int128)1 << (123 - cs[a])) / ba);
+            }
+            for (int t = 0; t < nt; t++) {
+                u64 qt = c.mods[t], B = 1;
+                for (int b2 = 0; b2 < nb; b2++) B = h_mulmod(B, bp[b2] % qt, qt);
+                corr[t] = B ? qt - B : 0;
+                inv[t] = h_invmod(B, qt); invs[t] = shoup_pre(inv[t], qt);
+            }
+            MDRTab mt;
+            mt.d_vfac = upload(c, vf); mt.d_vfac_sh = upload(c, vfs); mt.d_wfac = upload(c, wf); mt.d_corr = upload(c, corr);
+            mt.d_cfix = upload(c, cf); mt.d_csh = upload(c, cs); mt.d_inv = upload(c, inv); mt.d_inv_sh = upload(c, invs);
+            c.mdr[lev] = mt;
+        }
         // Rescale (C5) dropping q_{lev-1}
         if (lev >= 2) {
             RescaleTab rt;

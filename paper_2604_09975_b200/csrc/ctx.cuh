@@ -56,7 +56,14 @@ struct ModDownTab {       // P -> Q_L
     u64* d_pinv;          // [L]   P^{-1} mod q_i
     u64* d_pinv_sh;
     u64* d_pmod;          // [L]   q_i - (P mod q_i) (rounding correction, DESIGN.md R-MODDOWN)
-    u64* d_cfix;          // [K]   floor(2^123 / p_k)
+    u64* d_cfix;          // [K]   floor(2^(123 - s_k) / p_k)
+    u64* d_csh;           // [K]   s_k = 63 - bitlen(p_k)
+    u64* d_pl;            // [L]   P mod q_i and its Shoup quotient (extended-basis lift, R-LAZY)
+    u64* d_pl_sh;
+};
+
+struct MDRTab {           // merged ModDown + rescale (R-LAZY): basis B' = {q_{L-1}, p_0..p_{K-1}} -> Q_{L-1}
+    u64 *d_vfac, *d_vfac_sh, *d_wfac, *d_corr, *d_cfix, *d_csh, *d_inv, *d_inv_sh;
 };
 
 struct RescaleTab {       // drop q_{L-1}
@@ -66,9 +73,9 @@ struct RescaleTab {       // drop q_{L-1}
 };
 
 struct MaskKey {
-    int m, r0, r1, s0, ss, sc, level;
+    int m, r0, r1, s0, ss, sc, level, ext;
     bool operator<(const MaskKey& o) const {
-        return std::tie(m, r0, r1, s0, ss, sc, level) < std::tie(o.m, o.r0, o.r1, o.s0, o.ss, o.sc, o.level);
+        return std::tie(m, r0, r1, s0, ss, sc, level, ext) < std::tie(o.m, o.r0, o.r1, o.s0, o.ss, o.sc, o.level, o.ext);
     }
 };
 
@@ -86,6 +93,7 @@ struct encf_ctx {
     std::vector<std::vector<ModUpTab>> modup;       // [level][digit]
     std::vector<ModDownTab> moddown;                // [level]
     std::vector<RescaleTab> rescale;                // [level]
+    std::vector<MDRTab> mdr;                        // [level] (level >= 2)
     std::vector<void*> allocations;
     std::mutex mu;
     std::map<MaskKey, u64*> masks;      // NTT-form mask plaintexts [level][N]
@@ -209,7 +217,7 @@ void k_masked_sum(encf_ctx& c, const u64* const* cts, const u64* const* masks, i
                   cudaStream_t s);
 void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s);
 void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_slots, double scale, int level,
-                    u64* out, cudaStream_t s);
+                    u64* out, cudaStream_t s, const LimbMap* lmap = nullptr);
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
                       const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
@@ -218,13 +226,15 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
                             const ModDownTab& t, cudaStream_t s);
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s,
-                   const u64* corr = nullptr, const u64* cfix = nullptr);
+                   const u64* corr = nullptr, const u64* cfix = nullptr, const u64* csh = nullptr);
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s);
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s);
 void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,
                             cudaStream_t s);
 void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
-               cudaStream_t s);
+               cudaStream_t s, const LimbMap* lmap = nullptr);
+void k_lift_add(encf_ctx& c, const CopyBatch& dst, const CopyBatch& src, int n, int L, const u64* pm, const u64* pm_sh,
+                cudaStream_t s);
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s);
 void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s);

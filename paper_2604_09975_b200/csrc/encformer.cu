@@ -119,6 +119,8 @@ void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>&
 // rot(x,t-m)(.)u_t, rescale; t = 0: x(.)h_0, rescale.  Segment restriction [seg0, seg0+nseg) of the masks.
 void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
               std::vector<std::vector<DCt>>& outs) {
+    // t != 0: the two rotations stay in Q_L u P (hoisted, no ModDown), are masked there and divided by
+    // P q_{L-1} at once (lazy ModDown merged with the rescale, R-LAZY); t = 0: x (.) h_0, rescale.
     const int n = (int)xs.size();
     const int L = xs[0]->L;
     std::vector<std::vector<uint32_t>> gs(n);
@@ -129,39 +131,51 @@ void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::
             tt[i].push_back(r);
             if (r) { gs[i].push_back(ev.galois_rot(r)); gs[i].push_back(ev.galois_rot(r - m)); }
         }
-    std::vector<std::vector<DCt>> rots(n);
+    std::vector<const DCt*> rin;
+    std::vector<std::vector<uint32_t>> rgs;
+    std::vector<int> rslot(n, -1);
     int nrot = 0;
-    for (int i = 0; i < n; i++) nrot += (int)gs[i].size();
-    std::vector<DCt> rall = ev.alloc_many(nrot, L);
-    int k = 0;
     for (int i = 0; i < n; i++)
-        for (size_t j = 0; j < gs[i].size(); j++) rots[i].push_back(rall[k++]);
-    ev.hoisted_many(xs, gs, rots);
+        if (!gs[i].empty()) { rslot[i] = (int)rin.size(); rin.push_back(xs[i]); rgs.push_back(gs[i]); nrot += (int)gs[i].size(); }
+    std::vector<DCt> rall = ev.alloc_many_ext(nrot, L);
+    std::vector<std::vector<DCt>> rots(rin.size());
+    int k = 0;
+    for (size_t i = 0; i < rin.size(); i++)
+        for (size_t j2 = 0; j2 < rgs[i].size(); j2++) rots[i].push_back(rall[k++]);
+    ev.hoisted_many_ext(rin, rgs, rots);
     const double ms = ev.mask_scale(L);
-    std::vector<std::vector<SumTerm>> terms;
-    std::vector<double> scs;
+    std::vector<std::vector<SumTerm>> lazy_terms, plain_terms;
+    std::vector<double> lazy_sc, plain_sc;
+    std::vector<std::pair<int, int>> where;   // (0 = lazy / 1 = plain, index)
     for (int i = 0; i < n; i++) {
         size_t r = 0;
         for (int t : tt[i]) {
-            const u64* hm = ev.mask(m, 0, m - t, seg0, 1, nseg, L);
             if (t == 0) {
-                terms.push_back({SumTerm{xs[i]->d, hm}});
+                plain_terms.push_back({SumTerm{xs[i]->d, ev.mask(m, 0, m, seg0, 1, nseg, L)}});
+                plain_sc.push_back(xs[i]->scale * ms);
+                where.push_back({1, (int)plain_terms.size() - 1});
             } else {
-                const u64* um = ev.mask(m, m - t, m, seg0, 1, nseg, L);
-                terms.push_back({SumTerm{rots[i][r].d, hm}, SumTerm{rots[i][r + 1].d, um}});
+                const u64* hm = ev.mask_ext(m, 0, m - t, seg0, 1, nseg, L);
+                const u64* um = ev.mask_ext(m, m - t, m, seg0, 1, nseg, L);
+                const std::vector<DCt>& rr = rots[rslot[i]];
+                lazy_terms.push_back({SumTerm{rr[r].d, hm}, SumTerm{rr[r + 1].d, um}});
+                lazy_sc.push_back(xs[i]->scale * ms);
+                where.push_back({0, (int)lazy_terms.size() - 1});
                 r += 2;
             }
-            scs.push_back(xs[i]->scale * ms);
         }
     }
-    std::vector<DCt> y = ev.alloc_many((int)terms.size(), L);
-    ev.sum_many(terms, L, 2, y, scs);
-    std::vector<DCt> o = ev.alloc_many((int)terms.size(), L - 1);
-    ev.rescale_many(ptrs(y), o);
+    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy_terms.size(), L), lo = ev.alloc_many((int)lazy_terms.size(), L - 1);
+    ev.sum_many_ext(lazy_terms, L, ly, lazy_sc);
+    ev.moddown_rescale_many(ly, lo);
+    std::vector<DCt> py = ev.alloc_many((int)plain_terms.size(), L), po = ev.alloc_many((int)plain_terms.size(), L - 1);
+    ev.sum_many(plain_terms, L, 2, py, plain_sc);
+    ev.rescale_many(ptrs(py), po);
     outs.assign(n, {});
     k = 0;
     for (int i = 0; i < n; i++)
-        for (size_t j = 0; j < tt[i].size(); j++) outs[i].push_back(o[k++]);
+        for (size_t j2 = 0; j2 < tt[i].size(); j2++, k++)
+            outs[i].push_back(where[k].first == 0 ? lo[where[k].second] : po[where[k].second]);
 }
 
 // ====================================================================================== attention plans

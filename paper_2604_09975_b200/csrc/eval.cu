@@ -103,7 +103,7 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
         ntt_inverse(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);     // [b]_P -> coefficient form
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
-                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix);                        // rounded: y = centred [b]_P
+                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh);                        // rounded: y = centred [b]_P
         ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
         k_moddown_finish_batch(c, acc, y, O, n, L, nl, md, s);
         c.st_ks += n;
@@ -374,10 +374,126 @@ void Ev::masked_sum(const std::vector<const DCt*>& C, const std::vector<const u6
     out = o[0];
 }
 
-// Mask plaintexts: cached per (descriptor, level) in NTT form; encoded on the GPU on first use at
-// scale q_{level-1}, unless a plaintext was installed with encf_mask_put (parity tests).
-const u64* Ev::mask(int m, int r0, int r1, int s0, int ss, int scount, int level) {
-    MaskKey key{m, r0, r1, s0, ss, scount, level};
+// ------------------------------------------------------------------------------------ lazy (extended-basis) ops
+std::vector<DCt> Ev::alloc_many_ext(int n, int L) {
+    std::vector<DCt> v(n);
+    if (n == 0) return v;
+    const size_t w = (size_t)2 * (L + c.K) * c.N;
+    u64* base = sc.get(w * n);
+    for (int i = 0; i < n; i++) { v[i].d = base + w * i; v[i].L = L; v[i].ncomp = 2; v[i].cstride = (i64)(L + c.K) * c.N; }
+    return v;
+}
+
+// Hoisted rotations kept in the extended basis: (P sigma_g(c0) + b0, b1) over Q_L u P, i.e. the inner
+// product without its ModDown plus the lifted sigma_g(c0).
+void Ev::hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<std::vector<uint32_t>>& gs,
+                          std::vector<std::vector<DCt>>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    std::vector<const u64*> c1;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "hoisted_many_ext: mixed levels");
+        for (uint32_t g : gs[i]) if (g == 1u) throw EncfError(ENCF_ERR_ARG, "hoisted_many_ext: identity rotation");
+        c1.push_back(ins[i]->comp(1, N));
+    }
+    u64* ext = modup_many(c1, {}, L);
+    const size_t Lw = (size_t)L * N;
+    struct R { const u64* ext; const u64* key; uint32_t g; u64* out; const u64* c0; };
+    std::vector<R> rq;
+    for (int i = 0; i < n; i++)
+        for (size_t k = 0; k < gs[i].size(); k++) {
+            DCt& o = outs[i][k];
+            o.L = L; o.ncomp = 2; o.scale = ins[i]->scale; o.cstride = (i64)nl * N;
+            rq.push_back(R{ext + ext_stride(L) * i, key_for(gs[i][k], L), gs[i][k], o.d, ins[i]->comp(0, N)});
+        }
+    const int m = (int)rq.size();
+    const int ML = keys->max_level, key_nl = ML + K;
+    LimbMap klm;
+    klm.n = nl;
+    for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
+    u64* c0g = sc.get(Lw * m);
+    for (int r0 = 0; r0 < m; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, m - r0);
+        KsInnerBatch B;
+        CopyBatch cb, dst, src;
+        for (int i = 0; i < cnt; i++) {
+            const R& q = rq[r0 + i];
+            B.ext[i] = q.ext; B.key[i] = q.key; B.gather[i] = q.g; B.acc[i] = q.out;
+            cb.src[i] = q.c0; cb.g[i] = q.g;
+            dst.src[i] = q.out; dst.g[i] = 1u;
+            src.src[i] = c0g + Lw * (r0 + i); src.g[i] = 1u;
+        }
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
+        k_gather_copy(c, cb, cnt, c0g + Lw * r0, (i64)Lw, Lw, s);
+        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);   // + P sigma_g(c0) on the q-limbs
+        c.st_ks += cnt;      // a key switch whose ModDown is deferred (merged into a later moddown_rescale)
+    }
+}
+
+void Ev::sum_many_ext(const std::vector<std::vector<SumTerm>>& terms, int L, std::vector<DCt>& outs,
+                      const std::vector<double>& scales) {
+    const int n = (int)terms.size();
+    if (n == 0) return;
+    std::vector<SumDev> t;
+    std::vector<int> off{0};
+    std::vector<u64*> op;
+    for (int o = 0; o < n; o++) {
+        for (auto& x : terms[o]) t.push_back(SumDev{x.ct, x.mask});
+        off.push_back((int)t.size());
+        outs[o].L = L; outs[o].ncomp = 2; outs[o].scale = scales[o]; outs[o].cstride = (i64)(L + c.K) * c.N;
+        op.push_back(outs[o].d);
+    }
+    LimbMap em = c.extmap(L);
+    k_sum_csr(c, upload(t), upload(off), upload(op), n, (int)t.size(), 2, L + c.K, s, &em);
+}
+
+// round(x / (P q_{L-1})) mod Q_{L-1} for every extended ciphertext: limbs {q_{L-1}, p_*} to coefficient form,
+// ONE rounded fast BConv to Q_{L-1}, forward NTT, (x_i - y_i) (P q_{L-1})^{-1}.
+void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0].L, K = c.K, nl = L + K;
+    if (L < 2) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "moddown_rescale at one limb");
+    const size_t w = (size_t)2 * nl * N;
+    for (int i = 0; i < n; i++)
+        if (ins[i].d != ins[0].d + w * i || ins[i].L != L) throw EncfError(ENCF_ERR_ARG, "moddown_rescale_many: inputs must be contiguous");
+    u64* x = ins[0].d;
+    LimbMap bm;
+    bm.n = K + 1;
+    bm.mod[0] = (unsigned char)(L - 1);
+    for (int k = 0; k < K; k++) bm.mod[1 + k] = (unsigned char)(c.L + k);
+    ntt_inverse(c, PolyBatch{x + (size_t)(L - 1) * N, (i64)nl * N, 2 * n, bm}, s);
+    const MDRTab& t = c.mdr[L];
+    LimbMap qm = c.qmap(L - 1);
+    std::vector<int> pos(L - 1);
+    for (int i = 0; i < L - 1; i++) pos[i] = i;
+    u64* y = sc.get((size_t)n * 2 * (L - 1) * N);
+    k_bconv_batch(c, x + (size_t)(L - 1) * N, (i64)nl * N, bm, t.d_vfac, t.d_vfac_sh, t.d_wfac, qm, y, (i64)(L - 1) * N,
+                  pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh);
+    ntt_forward(c, PolyBatch{y, (i64)(L - 1) * N, 2 * n, qm}, s);
+    ModDownTab ft{};
+    ft.d_pinv = t.d_inv;
+    ft.d_pinv_sh = t.d_inv_sh;
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        OutBatch O;
+        for (int i = 0; i < cnt; i++) {
+            DCt& o = outs[r0 + i];
+            o.L = L - 1; o.ncomp = 2; o.scale = ins[r0 + i].scale / (double)c.mods[L - 1]; o.cstride = 0;
+            O.out[i][0] = o.comp(0, N); O.out[i][1] = o.comp(1, N);
+            O.add[i][0] = nullptr; O.add[i][1] = nullptr;
+        }
+        k_moddown_finish_batch(c, x + w * r0, y + (size_t)2 * (L - 1) * N * r0, O, cnt, L - 1, nl, ft, s);
+    }
+    c.st_ks += 0;
+}
+
+// Mask plaintexts: cached per (descriptor, level, ext) in NTT form; encoded on the GPU on first use at
+// scale q_{level-1} (ext: the same integer coefficients also reduced mod the special primes), unless a
+// plaintext was installed with encf_mask_put (parity tests).
+const u64* Ev::mask(int m, int r0, int r1, int s0, int ss, int scount, int level, int ext) {
+    MaskKey key{m, r0, r1, s0, ss, scount, level, ext};
     std::lock_guard<std::mutex> lk(c.mu);
     auto it = c.masks.find(key);
     if (it != c.masks.end()) return it->second;
@@ -387,13 +503,14 @@ const u64* Ev::mask(int m, int r0, int r1, int s0, int ss, int scount, int level
         int sg = s0 + k * ss;
         for (int r = r0; r < r1; r++) re[(size_t)sg * m + r] = 1.0;
     }
+    const LimbMap lm = ext ? c.extmap(level) : c.qmap(level);
     u64* pt = nullptr;
-    CUDA_TRY(cudaMalloc(&pt, (size_t)level * N * 8));
+    CUDA_TRY(cudaMalloc(&pt, (size_t)lm.n * N * 8));
     Scratch tmp(s);
     double* dre = (double*)tmp.get(n);
     CUDA_TRY(cudaMemcpyAsync(dre, re.data(), n * sizeof(double), cudaMemcpyHostToDevice, s));
-    k_encode_slots(c, dre, nullptr, n, (double)c.mods[level - 1], level, pt, s);
-    ntt_forward(c, PolyBatch{pt, 0, 1, c.qmap(level)}, s);
+    k_encode_slots(c, dre, nullptr, n, (double)c.mods[level - 1], level, pt, s, &lm);
+    ntt_forward(c, PolyBatch{pt, 0, 1, lm}, s);
     c.masks[key] = pt;
     return pt;
 }

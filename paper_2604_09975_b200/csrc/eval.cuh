@@ -79,8 +79,18 @@ struct Ev {
     void tensor_sum(const std::vector<const DCt*>& A, const std::vector<const DCt*>& B, DCt& out3);
     void masked_sum(const std::vector<const DCt*>& C, const std::vector<const u64*>& M, double m_scale, DCt& out);
 
+    // ---- lazy key switching over the extended basis Q_L u P (DESIGN.md R-LAZY).  An "ext" ciphertext is
+    // [2][L+K][N] (NTT form) with .L = L; its ModDown is an ordinary ciphertext.
+    std::vector<DCt> alloc_many_ext(int n, int L);
+    void hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<std::vector<uint32_t>>& gs,
+                          std::vector<std::vector<DCt>>& outs);
+    void sum_many_ext(const std::vector<std::vector<SumTerm>>& terms, int L, std::vector<DCt>& outs,
+                      const std::vector<double>& scales);
+    void moddown_rescale_many(const std::vector<DCt>& ins_ext, std::vector<DCt>& outs);   // ins contiguous (alloc_many_ext)
+
     // masks
-    const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level);
+    const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level, int ext = 0);
+    const u64* mask_ext(int m, int r0, int r1, int s0, int ss, int sc, int level) { return mask(m, r0, r1, s0, ss, sc, level, 1); }
     double mask_scale(int level) const { return (double)c.mods[level - 1]; }
     template <class T>
     T* upload(const std::vector<T>& v) {

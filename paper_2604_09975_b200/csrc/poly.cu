@@ -405,7 +405,8 @@ __global__ void scatter_slots_kernel(const double* re, const double* im, int n_s
         A[rg[j]] = make_double2(re[j], im ? im[j] : 0.0);
 }
 
-__global__ void round_reduce_kernel(const double2* S, double f, int N, int level, const ModConst* mod, u64* out, int* overflow) {
+__global__ void round_reduce_kernel(const double2* S, double f, int N, int level, const ModConst* mod, u64* out, int* overflow,
+                                    LimbMap lm) {
     S += (size_t)blockIdx.y * 2 * N;
     out += (size_t)blockIdx.y * level * N;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
@@ -413,7 +414,7 @@ __global__ void round_reduce_kernel(const double2* S, double f, int N, int level
         if (fabs(v) >= 4611686018427387904.0) { *overflow = 1; v = 0; }
         i64 x = (i64)v;
         for (int l = 0; l < level; l++) {
-            u64 q = mod[l].q;
+            u64 q = mod[lm.mod[l]].q;
             u64 r = (u64)(x < 0 ? -x : x) % q;
             out[(size_t)l * N + k] = (x < 0 && r) ? q - r : r;
         }
@@ -655,7 +656,7 @@ void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int l
 }
 
 void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots, double scale, int level, u64* out,
-                    cudaStream_t s) {
+                    cudaStream_t s, const LimbMap* lmap) {
     Scratch sc(s);
     double2* A = (double2*)sc.get((size_t)2 * c.N * 2);
     int* ovf = (int*)sc.get(1);
@@ -666,7 +667,8 @@ void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots
     c.prof_end(_slot, s); }
     fft2n(c, A, -1.0, s);
     { int _slot; c.prof_begin("round_reduce_kernel", s, 0, _slot);
-    round_reduce_kernel<<<GRID(c.N), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    round_reduce_kernel<<<GRID(c.N), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, lmap ? lmap->n : level, c.d_mod, out, ovf,
+                                              lmap ? *lmap : c.qmap(level));
     c.prof_end(_slot, s); }
     int h_ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -688,7 +690,8 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
     c.prof_end(_slot, s); }
     fft2n(c, A, -1.0, s, batch);
     { int _slot; c.prof_begin("round_reduce_kernel", s, 0, _slot);
-    round_reduce_kernel<<<dim3(nblocks(c.N, TB, 256), batch), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf);
+    round_reduce_kernel<<<dim3(nblocks(c.N, TB, 256), batch), TB, 0, s>>>(A, scale * 2.0 / c.N, c.N, level, c.d_mod, out, ovf,
+                                                                         c.qmap(level));
     c.prof_end(_slot, s); }
     int h_ovf = 0;
     CUDA_TRY(cudaMemcpyAsync(&h_ovf, ovf, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -775,8 +778,9 @@ __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u
 }
 
 // bconv over a batch of polynomials: input poly p at in + p*in_stride, output at out + p*out_stride.
-// corr != nullptr: rounded conversion (ModDown, DESIGN.md R-MODDOWN): r = (sum_i umulhi(v_i, cfix_i) + 2^58) >> 59
-// with cfix_i = floor(2^123 / q_i) (= round(sum_i v_i / q_i), bit-identical to oracle.c o_bconv_round); the
+// corr != nullptr: rounded conversion (ModDown, DESIGN.md R-MODDOWN): r = (sum_i umulhi(v_i << s_i, cfix_i) + 2^58) >> 59
+// with s_i = 63 - bitlen(q_i), cfix_i = floor(2^(123-s_i) / q_i) (= round(sum_i v_i / q_i), bit-identical to oracle.c
+// o_bconv_round); the
 // correction -r Q' is folded into the 128-bit accumulator (corr_t = t - Q' mod t).  Templated on the input
 // count so no predicated-off multiply is issued.
 template <int NIN>
@@ -785,7 +789,7 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
                                                          const u64* __restrict__ wfac, LimbMap om, OutPos op,
                                                          u64* __restrict__ out, i64 out_stride, int N,
                                                          const ModConst* __restrict__ mod, const u64* __restrict__ corr,
-                                                         const u64* __restrict__ cfix) {
+                                                         const u64* __restrict__ cfix, const u64* __restrict__ csh) {
     extern __shared__ u64 sw[];   // [NIN][nout] wfac, then [nout] corr
     const int nout = om.n;
     for (int i = threadIdx.x; i < NIN * nout; i += blockDim.x) sw[i] = wfac[i];
@@ -795,12 +799,14 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
     in += (size_t)blockIdx.y * in_stride;
     out += (size_t)blockIdx.y * out_stride;
     u64 qin[NIN], vf[NIN], vfs[NIN], cf[NIN];
+    int sh[NIN];
 #pragma unroll
     for (int i = 0; i < NIN; i++) {
         qin[i] = mod[im.mod[i]].q;
         vf[i] = vfac[i];
         vfs[i] = vfac_sh[i];
         cf[i] = corr ? cfix[i] : 0;
+        sh[i] = corr ? (int)csh[i] : 0;
     }
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         u64 v[NIN];
@@ -810,7 +816,7 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
         if (corr) {
             u64 fsum = 0;
 #pragma unroll
-            for (int i = 0; i < NIN; i++) fsum += umulhi(v[i], cf[i]);
+            for (int i = 0; i < NIN; i++) fsum += umulhi(v[i] << sh[i], cf[i]);
             r = (fsum + (1ull << 58)) >> 59;
         }
         for (int t = 0; t < nout; t++) {
@@ -907,7 +913,7 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
-                   const u64* cfix) {
+                   const u64* cfix, const u64* csh) {
     if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
@@ -915,7 +921,7 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
     switch (im.n) {
-#define B(NI) case NI: bconv_batch_kernel<NI><<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix); break;
+#define B(NI) case NI: bconv_batch_kernel<NI><<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix, csh); break;
         B(1) B(2) B(3) B(4) B(5) B(6) B(7) B(8) B(9) B(10) B(11) B(12) B(13) B(14) B(15) B(16)
 #undef B
     }
@@ -957,9 +963,9 @@ namespace {
 // components, 128-bit lazy accumulation reduced every 128 terms.
 __global__ void __launch_bounds__(TB) sum_csr_kernel(const SumDev* __restrict__ terms, const int* __restrict__ off,
                                                      u64* const* __restrict__ outs, int ncomp, int level, int N,
-                                                     const ModConst* __restrict__ mod) {
+                                                     const ModConst* __restrict__ mod, LimbMap lm) {
     const int o = blockIdx.z, limb = blockIdx.y;
-    const ModConst mc = mod[limb];
+    const ModConst mc = mod[lm.mod[limb]];
     const size_t cs = (size_t)level * N;
     const int t0 = off[o], t1 = off[o + 1];
     u64* out = outs[o];
@@ -1021,10 +1027,11 @@ __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restric
 }  // namespace
 
 void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
-               cudaStream_t s) {
+               cudaStream_t s, const LimbMap* lmap) {
+    LimbMap lm = lmap ? *lmap : c.qmap(level);
     dim3 grid((c.N + TB - 1) / TB, level, nout);
     { int _slot; c.prof_begin("sum_csr_kernel", s, 0, _slot);
-    sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod);
+    sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod, lm);
     c.prof_end(_slot, s); }
     c.st_launch++;
     c.st_bytes += (uint64_t)nterms * ncomp * level * c.N * 8 * 2 + (uint64_t)nout * ncomp * level * c.N * 8;
@@ -1092,4 +1099,29 @@ void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s) {
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes; c.st_ptmul += (uint64_t)A.nt * A.nu;
     CUDA_TRY(cudaGetLastError());
+}
+
+// ====================================================================================== lazy key switching helpers
+namespace {
+__global__ void lift_add_kernel(CopyBatch Dst, CopyBatch Src, int L, int N, const ModConst* __restrict__ mod,
+                                const u64* __restrict__ pm, const u64* __restrict__ pm_sh) {
+    const int r = blockIdx.y;
+    u64* d = (u64*)Dst.src[r];
+    const u64* s = Src.src[r];
+    const size_t total = (size_t)L * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int limb = (int)(i / N);
+        const u64 q = mod[limb].q;
+        d[i] = add_mod(d[i], mul_shoup(s[i], pm[limb], pm_sh[limb], q), q);
+    }
+}
+}  // namespace
+
+void k_lift_add(encf_ctx& c, const CopyBatch& dst, const CopyBatch& src, int n, int L, const u64* pm, const u64* pm_sh,
+                cudaStream_t s) {
+    dim3 grid(nblocks((size_t)L * c.N, TB, 256), n);
+    { int _slot; c.prof_begin("lift_add_kernel", s, 0, _slot);
+    lift_add_kernel<<<grid, TB, 0, s>>>(dst, src, L, c.N, c.d_mod, pm, pm_sh);
+    c.prof_end(_slot, s); }
+    c.st_launch++; c.st_bytes += (uint64_t)n * L * c.N * 8 * 3;
 }

@@ -39,7 +39,7 @@ class Counters(ctypes.Structure):
 
 
 class MaskDesc(ctypes.Structure):
-    _fields_ = [(n, _i32) for n in ("m", "r0", "r1", "s0", "sstride", "scount", "level")]
+    _fields_ = [(n, _i32) for n in ("m", "r0", "r1", "s0", "sstride", "scount", "level", "ext")]
 
 
 _SIG = {
@@ -350,9 +350,9 @@ class Context:
         _chk(_lib.encf_complexify(self.h, ctypes.byref(re._c()), ctypes.byref(im._c()), ctypes.byref(c), _stream()), "complexify")
         return out._update(c)
 
-    def mask_put(self, desc, m, level, coeffs):
+    def mask_put(self, desc, m, level, coeffs, ext=False):
         r0, r1, s0, ss, sc = desc
-        d = MaskDesc(m, r0, r1, s0, ss, sc, level)
+        d = MaskDesc(m, r0, r1, s0, ss, sc, level, 1 if ext else 0)
         w = np.ascontiguousarray(coeffs, dtype=np.uint64)
         _chk(_lib.encf_mask_put(self.h, ctypes.byref(d), w.ctypes.data), "mask_put")
 

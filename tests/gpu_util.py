@@ -27,8 +27,13 @@ def assert_ct_equal(ctx, got, ref, what=""):
 
 
 def install_masks(ctx, ev):
-    for (desc, L, m), pt in ev.masks.items():
-        ctx.mask_put(desc, m, L, pt.m)
+    for key, pt in ev.masks.items():
+        if key[0] == "ext":
+            _, desc, L, m = key
+            ctx.mask_put(desc, m, L, pt.m, ext=True)
+        else:
+            desc, L, m = key
+            ctx.mask_put(desc, m, L, pt.m)
 
 
 def weights_tensor(ctx, pts, L):

@@ -190,6 +190,36 @@ def test_moddown_explicit_crt():
     assert ties <= 1
 
 
+def test_moddown_rescale_explicit_crt():
+    """Merged ModDown + rescale (R-LAZY): out = round(x / (P q_{L-1})) mod Q_{L-1} (ties within 1e-12 aside)."""
+    P, L, N = P13, 5, P13.N
+    mods = P.ext_mods(L)
+    x = rand_limbs(mods, N, 23)
+    out = O.moddown_rescale(P, x, L)
+    K = 64
+    xv, _ = O.crt_lift(x[:, :K], mods, centered=False)
+    ov, Q1 = O.crt_lift(out[:, :K], P.q[:L - 1], centered=False)
+    D = P.P * P.q[L - 1]
+    for k in range(K):
+        lo = xv[k] // D
+        frac = (xv[k] - lo * D) / D
+        if abs(frac - 0.5) < 1e-12:
+            assert ov[k] in (lo % Q1, (lo + 1) % Q1)
+        else:
+            assert ov[k] == (lo + (1 if frac >= 0.5 else 0)) % Q1, k
+
+
+def test_lazy_hoisted_rotation_equals_rotation_in_value():
+    """ModDown of the extended-basis rotation pair decrypts like the ordinary hoisted rotation."""
+    keys = O.Keys(P13, 0x5EED, galois=[O.galois_rot(P13, 3)])
+    z = np.random.default_rng(33).uniform(-1, 1, P13.n)
+    ct = O.encrypt_sk(P13, keys, O.encode(P13, z, 2.0 ** 40, 6), 1)
+    e = O.rotate_hoisted_ext(P13, keys, ct, [3])[0]
+    md = O.Ct(np.stack([O.moddown(P13, e[c], 6) for c in range(2)]), ct.scale)
+    ref = O.rotate_hoisted(P13, keys, ct, [3])[0]
+    assert np.array_equal(md.c, ref.c)      # ModDown(P sigma(c0) + b0) == sigma(c0) + ModDown(b0) exactly
+
+
 def test_rescale_is_round_division():
     P, L, N = P16, 4, 32
     mods = P.q[:L]
