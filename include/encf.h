@@ -179,7 +179,8 @@ encf_status encf_proj_encode_weights(encf_ctx* ctx, const encf_proj_plan* plan, 
  * above, level L, scale w_scale).  Units (b,p) in [unit_begin, unit_end) (row-major over b, p).
  * With the full unit range and ENCF_PROJ_FINALIZE, y[b] = rescale(acc_b + conj(acc_b)) (B_out
  * outputs, level L-1).  Without FINALIZE, y[b] receives the partial giant-step sums acc_b of the
- * touched b at level L (for a cross-rank modular reduction, then encf_pt_ct_matmul_finalize). */
+ * touched b in the EXTENDED basis Q_L u P (n_limbs = L + K; the giant-step rotations are summed without ModDown,
+ * DESIGN.md R-LAZY) for a cross-rank uint64 SUM + encf_mod_reduce_ext, then encf_pt_ct_matmul_finalize. */
 #define ENCF_PROJ_FINALIZE 2u
 encf_status encf_pt_ct_matmul(encf_ctx* ctx, const encf_keys* keys, const encf_proj_plan* plan,
                               const encf_ct* x /*host array [U]*/, const uint64_t* w_pt, double w_scale,
@@ -218,6 +219,9 @@ encf_status encf_export_c2m(encf_ctx* ctx, const encf_ct* in, int32_t L_conv, ui
 /* After a cross-rank uint64 SUM (C2): reduce n_polys x [n_limbs][N] words mod q_i in place.
  * Valid while the summed value fits in 64 bits (world_size * q < 2^64). */
 encf_status encf_mod_reduce(encf_ctx* ctx, uint64_t* data, int32_t n_polys, int32_t n_limbs, void* stream);
+/* Same for polynomials over the extended basis [q_0..q_{L-1}, p_0..p_{K-1}] (the partial projection
+ * accumulators, which are exchanged across ranks in that basis so the sharded result is bit-identical). */
+encf_status encf_mod_reduce_ext(encf_ctx* ctx, uint64_t* data, int32_t n_polys, int32_t L, void* stream);
 
 #ifdef __cplusplus
 }

@@ -583,6 +583,22 @@ def rotate_hoisted_ext(P, keys, ct, rs):
     return outs
 
 
+def rotate_ext(P, keys, ct, g):
+    """Single (non-hoisted) key switch WITHOUT ModDown: sigma_g then ModUp of sigma_g(c1); returns the
+    extended pair (P sigma_g(c0) + b0, b1) over Q_L u P (DESIGN.md R-LAZY)."""
+    L, N = ct.L, P.N
+    mods, emods = P.q[:L], P.ext_mods(L)
+    c0 = automorph(ct.c[0], g, mods, N)
+    c1 = automorph(ct.c[1], g, mods, N)
+    b0, b1 = ks_inner(P, modup(P, c1, L), keys.key_at(g, L), L)
+    return np.stack([padd(b0, lift_P(P, c0, L), emods, N), b1])
+
+
+def moddown_ext(P, x, L):
+    """ModDown of both components of an extended ciphertext [2][L+K][N] -> [2][L][N]."""
+    return np.stack([moddown(P, x[c], L) for c in range(2)])
+
+
 def keyswitch(P, d, key, L):
     b0, b1 = ks_inner(P, modup(P, d, L), key, L)
     return moddown(P, b0, L), moddown(P, b1, L)

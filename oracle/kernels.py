@@ -180,6 +180,30 @@ class Ev:
                 acc[c] = O.padd(acc[c], O.pmul_pointwise(O.ntt(x.c[c], emods, N), ptn, emods, N), emods, N)
         return ExtCt(np.stack([O.intt(a, emods, N) for a in acc]), L, scale)
 
+    def lift_ext(self, ct):
+        """P * ct in the extended basis (exact)."""
+        return ExtCt(np.stack([O.lift_P(self.P, ct.c[i], ct.L) for i in range(2)]), ct.L, ct.scale)
+
+    def rot_ext(self, ct, r):
+        if int(r) % self.P.n == 0:
+            return self.lift_ext(ct)
+        self.ledger["rot"] += 1
+        return ExtCt(O.rotate_ext(self.P, self.keys, ct, O.galois_rot(self.P, r)), ct.L, ct.scale)
+
+    def conj_ext(self, ct):
+        self.ledger["conj"] += 1
+        return ExtCt(O.rotate_ext(self.P, self.keys, ct, O.galois_conj(self.P)), ct.L, ct.scale)
+
+    def ext_add(self, a, b):
+        if a.scale != b.scale:
+            raise O.OracleError("SCALE_MISMATCH")
+        em = self.P.ext_mods(a.L)
+        return ExtCt(np.stack([O.padd(a.c[i], b.c[i], em, self.P.N) for i in range(2)]), a.L, a.scale)
+
+    def moddown(self, y):
+        self.ledger["moddown"] += 1
+        return O.Ct(O.moddown_ext(self.P, y.c, y.L), y.scale)
+
     def moddown_rescale(self, y):
         self.ledger["moddown"] += 1
         self.ledger["rescale"] += 1
@@ -315,6 +339,25 @@ class CountEv:
         self.ledger["rescale"] += 1
         return FakeCt(y.L - 1, y.scale)
 
+    def lift_ext(self, ct):
+        return FakeCt(ct.L, ct.scale)
+
+    def rot_ext(self, ct, r):
+        if int(r) % self.n:
+            self.ledger["rot"] += 1
+        return FakeCt(ct.L, ct.scale)
+
+    def conj_ext(self, ct):
+        self.ledger["conj"] += 1
+        return FakeCt(ct.L, ct.scale)
+
+    def ext_add(self, a, b):
+        return FakeCt(a.L, a.scale)
+
+    def moddown(self, y):
+        self.ledger["moddown"] += 1
+        return FakeCt(y.L, y.scale)
+
     def tensor_sum(self, pairs):
         for _ in pairs:
             self.ledger["ctmul"] += 1
@@ -431,16 +474,19 @@ def projection_partial(ev, plan, xt, w, u0, u1):
         cts = [bank[u][q] for u in range(plan.U) for q in range(N1)]
         pts = [w(b, p, u, q) for u in range(plan.U) for q in range(N1)]
         c = ev.mac_ptmul(cts, pts)
-        if p:
-            c = ev.rot(c, p * N1 * m)
-        accs[b] = c if b not in accs else ev.add(accs[b], c)
-    return accs
+        e = ev.rot_ext(c, p * N1 * m)          # p = 0: P * c (exact lift); p >= 1: rotation without ModDown (R-LAZY)
+        accs[b] = e if b not in accs else ev.ext_add(accs[b], e)
+    return accs                                 # extended-basis partial accumulators (reduced across ranks as such)
 
 
-def projection_finalize(ev, plan, acc, decomplexify=True):
-    """C6 steps 4-5: z = acc + conj(acc) (scale x2, G2/G3), y = rescale(z)."""
+def projection_finalize(ev, plan, acc_ext, decomplexify=True):
+    """C6 steps 4-5 on an extended accumulator: acc = ModDown(acc_ext) (one per block, R-LAZY);
+    z = acc + conj(acc) (scale x2, G2/G3) formed in Q_L u P and divided by P q_{L-1} at once."""
+    acc = ev.moddown(acc_ext)
     if decomplexify:
-        acc = ev.scale_mul(ev.add(acc, ev.conj(acc)), 2.0)
+        z = ev.ext_add(ev.lift_ext(acc), ev.conj_ext(acc))
+        z.scale = acc.scale * 2.0
+        return ev.moddown_rescale(z)
     return ev.rescale(acc)
 
 
@@ -448,29 +494,13 @@ def projection(ev, plan, xt, w, decomplexify=True):
     """C6 (P:280-301, P:1323-1331; G2/G3):
       1. bank[u][0] = x~_u ; bank[u][q] = HOISTED rot(x~_u, q m), q = 1..N1-1
       2. c~_{b,p} = sum_{u,q} bank[u][q] (.) w~_{b,p,u,q}          (exact modular sum)
-      3. acc_b = c~_{b,0} + sum_{p>=1} rot(c~_{b,p}, p N1 m)       (single rotations)
+      3. acc_b = c~_{b,0} + sum_{p>=1} rot(c~_{b,p}, p N1 m)       (single rotations, summed in Q_L u P and
+         ModDown'ed once per block: lazy ModDown, R-LAZY)
       4. z_b = acc_b + conj(acc_b), scale x2  (decomplexify AFTER the fold, G2; the 1/2 is bookkeeping, G3)
-      5. y_b = rescale(z_b)
+      5. y_b = rescale(z_b)                    (4-5 merged: conj kept in Q_L u P, one division by P q_{L-1})
     w(b, p, u, q) -> plaintext.  Returns the B_out outputs y_b."""
-    m, N1 = plan.m, plan.N1
-    bank = []
-    for u in range(plan.U):
-        rots = ev.rot_hoisted(xt[u], [q * m for q in range(1, N1)]) if N1 > 1 else []
-        bank.append([xt[u]] + list(rots))
-    ys = []
-    for b in range(plan.B_out):
-        acc = None
-        for p in range(plan.N2):
-            cts = [bank[u][q] for u in range(plan.U) for q in range(N1)]
-            pts = [w(b, p, u, q) for u in range(plan.U) for q in range(N1)]
-            c = ev.mac_ptmul(cts, pts)
-            if p:
-                c = ev.rot(c, p * N1 * m)
-            acc = c if acc is None else ev.add(acc, c)
-        if decomplexify:
-            acc = ev.scale_mul(ev.add(acc, ev.conj(acc)), 2.0)
-        ys.append(ev.rescale(acc))
-    return ys
+    accs = projection_partial(ev, plan, xt, w, 0, plan.B_out * plan.N2)
+    return [projection_finalize(ev, plan, accs[b], decomplexify) for b in range(plan.B_out)]
 
 
 # ====================================================================================== score kernel (§3.3.1, App. A.3)

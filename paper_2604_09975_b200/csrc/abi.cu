@@ -507,12 +507,12 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
                 ev.copy(ys[i], o);
                 writeback(yo, o);
             }
-        } else {
+        } else {   // partial accumulators in the EXTENDED basis: n_limbs = L + K (R-LAZY; reduce with encf_mod_reduce_ext)
             for (size_t i = 0; i < accs.size(); i++) {
                 encf_ct* yo = &y[b_first + i];
-                DCt o = outview(yo, L, 2);
-                ev.copy(accs[i], o);
-                writeback(yo, o);
+                need(yo && yo->data, ENCF_ERR_ARG, "null output");
+                k_copy(accs[i].d, yo->data, (size_t)2 * (L + c->K) * c->N, s);
+                yo->n_comp = 2; yo->n_limbs = L + c->K; yo->scale = accs[i].scale; yo->ntt = 1;
             }
         }
     });
@@ -523,12 +523,18 @@ encf_status encf_pt_ct_matmul_finalize(encf_ctx* c, const encf_keys* k, const en
     return guard([&] {
         need(c && k && p && acc && y && 0 <= b0 && b0 < b1 && b1 <= p->B_out, ENCF_ERR_ARG, "finalize: bad argument");
         EV_BEGIN(k);
-        std::vector<DCt> accs;
-        for (int b = b0; b < b1; b++) accs.push_back(view(&acc[b - b0]));
-        std::vector<DCt> ys = ev.alloc_many(b1 - b0, accs[0].L - 1);
+        const int L = acc[0].n_limbs - c->K;     // extended partials: n_limbs = L + K
+        need(L >= 2, ENCF_ERR_LEVEL_MISMATCH, "finalize expects extended accumulators (n_limbs = L + K)");
+        std::vector<DCt> accs = ev.alloc_many_ext(b1 - b0, L);
+        for (int b = b0; b < b1; b++) {
+            need(acc[b - b0].n_limbs == L + c->K && acc[b - b0].data, ENCF_ERR_LEVEL_MISMATCH, "finalize: mixed accumulators");
+            k_copy(acc[b - b0].data, accs[b - b0].d, (size_t)2 * (L + c->K) * c->N, s);
+            accs[b - b0].scale = acc[b - b0].scale;
+        }
+        std::vector<DCt> ys = ev.alloc_many(b1 - b0, L - 1);
         proj_finalize_many(ev, *p, accs, ys);
         for (int b = b0; b < b1; b++) {
-            DCt o = outview(&y[b - b0], accs[0].L - 1, 2);
+            DCt o = outview(&y[b - b0], L - 1, 2);
             ev.copy(ys[b - b0], o);
             writeback(&y[b - b0], o);
         }
@@ -641,6 +647,14 @@ encf_status encf_export_c2m(encf_ctx* c, const encf_ct* in, int32_t Lc, uint64_t
         ntt_inverse(*c, PolyBatch{masked->data, (i64)Lc * N, 2, c->qmap(Lc)}, s);
         k_export_mask(*c, mask_seed, (0x04ull << 56) | stream_id, masked->data, share, Lc, s);
         masked->n_comp = 2; masked->n_limbs = Lc; masked->scale = x.scale; masked->ntt = 0;
+    });
+}
+
+encf_status encf_mod_reduce_ext(encf_ctx* c, uint64_t* d, int32_t np, int32_t L, void* stream) {
+    return guard([&] {
+        need(c && d && np >= 0, ENCF_ERR_ARG, "mod_reduce_ext: bad argument");
+        level_ok(c, L);
+        k_mod_reduce(*c, d, np, c->extmap(L), S(stream));
     });
 }
 

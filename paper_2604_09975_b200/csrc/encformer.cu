@@ -46,10 +46,11 @@ std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p) {
     return g;
 }
 
-// C6 steps 1-3 for units [u0, u1) (row-major over (b, p)); accs[b - b_first] = acc_b (level L).
+// C6 steps 1-3 for units [u0, u1) (row-major over (b, p)); accs[b - b_first] = EXTENDED acc_b over Q_L u P.
 //  1. bank[u][q] = HOISTED rot(x~_u, q m)            (one ModUp per input, all rotations in one batch)
 //  2. c~_{b,p} = sum_{u,q} bank[u][q] (.) w~_{b,p,u,q}  (one fused MAC launch over the plaintext stream)
-//  3. acc_b = c~_{b,0} + sum_{p>=1} rot(c~_{b,p}, p N1 m) (all giant rotations in one batch, one sum)
+//  3. acc_b = P c~_{b,0} + sum_{p>=1} rot_ext(c~_{b,p}, p N1 m): the giant rotations without ModDown, summed in
+//     Q_L u P (lazy ModDown, R-LAZY); the ModDown happens once per block in proj_finalize_many.
 void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs) {
     const int N = ev.c.N, L = x[0].L, U = p.U, N1 = p.N1;
@@ -73,45 +74,50 @@ void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, con
     k_diag_mac(ev.c, bankv[0].d, U * N1, w + (size_t)u0 * wus, units, wus, cu[0].d, (i64)ctw, L, ev.s);
     const double sc = x[0].scale * w_scale;
     for (auto& c : cu) c.scale = sc;
-    std::vector<const DCt*> rin;
+    std::vector<const DCt*> rin, lin;
     std::vector<uint32_t> rg;
-    std::vector<int> ridx;
+    std::vector<int> ridx, lidx;
     for (int un = u0; un < u1; un++) {
         int pp = un % p.N2;
         if (pp) { rin.push_back(&cu[un - u0]); rg.push_back(ev.galois_rot((long)pp * N1 * p.m)); ridx.push_back(un - u0); }
+        else { lin.push_back(&cu[un - u0]); lidx.push_back(un - u0); }
     }
-    std::vector<DCt> rot = ev.alloc_many((int)rin.size(), L);
-    ev.rotate_many(rin, rg, rot);
+    std::vector<DCt> rot = ev.alloc_many_ext((int)rin.size(), L), lif = ev.alloc_many_ext((int)lin.size(), L);
+    ev.rotate_many_ext(rin, rg, rot);
+    ev.lift_many(lin, lif);
     std::vector<const DCt*> term_of(units, nullptr);
-    for (int un = 0; un < units; un++) term_of[un] = &cu[un];
     for (size_t i = 0; i < ridx.size(); i++) term_of[ridx[i]] = &rot[i];
+    for (size_t i = 0; i < lidx.size(); i++) term_of[lidx[i]] = &lif[i];
     int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;
     std::vector<std::vector<SumTerm>> terms(b_last - b_first + 1);
     for (int un = u0; un < u1; un++) terms[un / p.N2 - b_first].push_back(SumTerm{term_of[un - u0]->d, nullptr});
-    accs = ev.alloc_many((int)terms.size(), L);
-    ev.sum_many(terms, L, 2, accs, std::vector<double>(terms.size(), sc));
+    accs = ev.alloc_many_ext((int)terms.size(), L);
+    ev.sum_many_ext(terms, L, accs, std::vector<double>(terms.size(), sc));
 }
 
-// C6 steps 4-5 for a list of accumulators: z = acc + conj(acc) (scale x2, G2/G3), y = rescale(z).
-void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs, std::vector<DCt>& ys) {
-    const int n = (int)accs.size();
-    const int L = accs[0].L;
-    std::vector<DCt> z = ev.alloc_many(n, L);
+// C6 steps 4-5 for extended accumulators (contiguous): acc = ModDown(acc_ext); z = acc + conj(acc) (scale x2,
+// G2/G3) formed in Q_L u P (P acc lifted + conj without ModDown) and divided by P q_{L-1} at once (R-LAZY).
+void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs_ext, std::vector<DCt>& ys) {
+    const int n = (int)accs_ext.size();
+    const int L = accs_ext[0].L;
+    std::vector<DCt> acc = ev.alloc_many(n, L);
+    ev.moddown_many(accs_ext, acc);
     if (p.flags & ENCF_PROJ_DECOMPLEXIFY) {
-        std::vector<DCt> cj = ev.alloc_many(n, L);
-        ev.rotate_many(ptrs(accs), std::vector<uint32_t>(n, ev.galois_conj()), cj);
+        std::vector<DCt> cj = ev.alloc_many_ext(n, L), la = ev.alloc_many_ext(n, L);
+        ev.rotate_many_ext(ptrs(acc), std::vector<uint32_t>(n, ev.galois_conj()), cj);
+        ev.lift_many(ptrs(acc), la);
         std::vector<std::vector<SumTerm>> t(n);
         std::vector<double> sc(n);
         for (int i = 0; i < n; i++) {
-            check_scale(accs[i].scale, cj[i].scale);
-            t[i] = {SumTerm{accs[i].d, nullptr}, SumTerm{cj[i].d, nullptr}};
-            sc[i] = accs[i].scale * 2.0;
+            t[i] = {SumTerm{la[i].d, nullptr}, SumTerm{cj[i].d, nullptr}};
+            sc[i] = acc[i].scale * 2.0;
         }
-        ev.sum_many(t, L, 2, z, sc);
+        std::vector<DCt> z = ev.alloc_many_ext(n, L);
+        ev.sum_many_ext(t, L, z, sc);
+        ev.moddown_rescale_many(z, ys);
     } else {
-        for (int i = 0; i < n; i++) ev.copy(accs[i], z[i]);
+        ev.rescale_many(ptrs(acc), ys);
     }
-    ev.rescale_many(ptrs(z), ys);
 }
 
 // ====================================================================================== shifts (App. A.1)

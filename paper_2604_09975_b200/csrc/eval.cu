@@ -489,6 +489,97 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
     c.st_ks += 0;
 }
 
+// ModDown of extended ciphertexts (rounded, R-MODDOWN), no rescale.
+void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0].L, K = c.K, nl = L + K;
+    const size_t w = (size_t)2 * nl * N;
+    for (int i = 0; i < n; i++)
+        if (ins[i].d != ins[0].d + w * i || ins[i].L != L) throw EncfError(ENCF_ERR_ARG, "moddown_many: inputs must be contiguous");
+    u64* x = ins[0].d;
+    LimbMap pm; pm.n = K;
+    for (int k = 0; k < K; k++) pm.mod[k] = (unsigned char)(c.L + k);
+    LimbMap qm = c.qmap(L);
+    std::vector<int> pos(L);
+    for (int i = 0; i < L; i++) pos[i] = i;
+    const ModDownTab& md = c.moddown[L];
+    ntt_inverse(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);
+    u64* y = sc.get((size_t)n * 2 * L * N);
+    k_bconv_batch(c, x + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N, pos.data(), 2 * n, s,
+                  md.d_pmod, md.d_cfix, md.d_csh);
+    ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        OutBatch O;
+        for (int i = 0; i < cnt; i++) {
+            DCt& o = outs[r0 + i];
+            o.L = L; o.ncomp = 2; o.scale = ins[r0 + i].scale; o.cstride = 0;
+            O.out[i][0] = o.comp(0, N); O.out[i][1] = o.comp(1, N);
+            O.add[i][0] = nullptr; O.add[i][1] = nullptr;
+        }
+        k_moddown_finish_batch(c, x + w * r0, y + (size_t)2 * L * N * r0, O, cnt, L, nl, md, s);
+    }
+}
+
+// Single (non-hoisted) key switches without ModDown: (P sigma_g(c0) + b0, b1) over Q_L u P.
+void Ev::rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    std::vector<const u64*> c1;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rotate_many_ext: mixed levels");
+        if (gs[i] == 1u) throw EncfError(ENCF_ERR_ARG, "rotate_many_ext: identity rotation (use lift_many)");
+        c1.push_back(ins[i]->comp(1, N));
+    }
+    u64* ext = modup_many(c1, gs, L);                 // ModUp of sigma_g(c1): the gather is fused into the copy
+    const size_t Lw = (size_t)L * N;
+    const int ML = keys->max_level, key_nl = ML + K;
+    LimbMap klm;
+    klm.n = nl;
+    for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
+    u64* c0g = sc.get(Lw * n);
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        KsInnerBatch B;
+        CopyBatch cb, dst, src;
+        for (int i = 0; i < cnt; i++) {
+            DCt& o = outs[r0 + i];
+            o.L = L; o.ncomp = 2; o.scale = ins[r0 + i]->scale; o.cstride = (i64)nl * N;
+            B.ext[i] = ext + ext_stride(L) * (r0 + i); B.key[i] = key_for(gs[r0 + i], L); B.gather[i] = 1u; B.acc[i] = o.d;
+            cb.src[i] = ins[r0 + i]->comp(0, N); cb.g[i] = gs[r0 + i];
+            dst.src[i] = o.d; dst.g[i] = 1u;
+            src.src[i] = c0g + Lw * (r0 + i); src.g[i] = 1u;
+        }
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
+        k_gather_copy(c, cb, cnt, c0g + Lw * r0, (i64)Lw, Lw, s);
+        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);
+        c.st_ks += cnt;
+    }
+}
+
+void Ev::lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L, nl = L + c.K;
+    for (int i = 0; i < n; i++) {
+        DCt& o = outs[i];
+        o.L = L; o.ncomp = 2; o.scale = ins[i]->scale; o.cstride = (i64)nl * N;
+        CUDA_TRY(cudaMemsetAsync(o.d, 0, (size_t)2 * nl * N * 8, s));
+    }
+    for (int r0 = 0; r0 < 2 * n; r0 += CP_BATCH) {
+        const int cnt = std::min(CP_BATCH, 2 * n - r0);
+        CopyBatch dst, src;
+        for (int i = 0; i < cnt; i++) {
+            const int idx = (r0 + i) / 2, comp = (r0 + i) % 2;
+            dst.src[i] = outs[idx].comp(comp, N); dst.g[i] = 1u;
+            src.src[i] = ins[idx]->comp(comp, N); src.g[i] = 1u;
+        }
+        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);
+    }
+}
+
 // Mask plaintexts: cached per (descriptor, level, ext) in NTT form; encoded on the GPU on first use at
 // scale q_{level-1} (ext: the same integer coefficients also reduced mod the special primes), unless a
 // plaintext was installed with encf_mask_put (parity tests).

@@ -87,6 +87,9 @@ struct Ev {
     void sum_many_ext(const std::vector<std::vector<SumTerm>>& terms, int L, std::vector<DCt>& outs,
                       const std::vector<double>& scales);
     void moddown_rescale_many(const std::vector<DCt>& ins_ext, std::vector<DCt>& outs);   // ins contiguous (alloc_many_ext)
+    void moddown_many(const std::vector<DCt>& ins_ext, std::vector<DCt>& outs);           // ins contiguous (alloc_many_ext)
+    void rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs_ext);
+    void lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs_ext);       // P * ct over Q_L u P
 
     // masks
     const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level, int ext = 0);

@@ -89,6 +89,7 @@ _SIG = {
     "encf_l_conv": [_p, _i32, _i32, _f64, _f64, ctypes.POINTER(_i32)],
     "encf_export_c2m": [_p, ctypes.POINTER(CT), _i32, _u64, _u64, ctypes.POINTER(CT), _p, _p],
     "encf_mod_reduce": [_p, _p, _i32, _i32, _p],
+    "encf_mod_reduce_ext": [_p, _p, _i32, _i32, _p],
     "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
 }
@@ -375,6 +376,9 @@ class Context:
     def mod_reduce(self, tensor, n_polys, n_limbs):
         _chk(_lib.encf_mod_reduce(self.h, tensor.data_ptr(), n_polys, n_limbs, _stream()), "mod_reduce")
 
+    def mod_reduce_ext(self, tensor, n_polys, L):
+        _chk(_lib.encf_mod_reduce_ext(self.h, tensor.data_ptr(), n_polys, L, _stream()), "mod_reduce_ext")
+
 
 class Keys:
     def __init__(self, ctx, h, max_level):
@@ -437,7 +441,7 @@ class ProjPlan:
         unit_end = units if unit_end is None else unit_end
         L = xs[0].n_limbs
         fin = finalize and unit_begin == 0 and unit_end == units
-        ys = [self.ctx.empty_ct(L - 1 if fin else L) for _ in range(self.B_out)]
+        ys = [self.ctx.empty_ct(L - 1 if fin else L + len(self.ctx.p)) for _ in range(self.B_out)]
         xa = (CT * len(xs))(*[x._c() for x in xs])
         ya = (CT * len(ys))(*[y._c() for y in ys])
         _chk(_lib.encf_pt_ct_matmul(self.ctx.h, keys.h, self.h, ctypes.cast(xa, _p), w.data_ptr(), float(w_scale), unit_begin,
@@ -446,7 +450,8 @@ class ProjPlan:
         return [ys[b]._update(ya[b]) for b in range(b0, b1)]
 
     def finalize(self, keys, accs, b_begin):
-        ys = [self.ctx.empty_ct(a.n_limbs - 1) for a in accs]
+        """accs: extended partial accumulators (n_limbs = L + K)."""
+        ys = [self.ctx.empty_ct(a.n_limbs - len(self.ctx.p) - 1) for a in accs]
         aa = (CT * len(accs))(*[a._c() for a in accs])
         ya = (CT * len(ys))(*[y._c() for y in ys])
         _chk(_lib.encf_pt_ct_matmul_finalize(self.ctx.h, keys.h, self.h, ctypes.cast(aa, _p), b_begin, b_begin + len(accs),

@@ -212,8 +212,9 @@ def test_projection_ragged_and_unit_split(c13, keys13):
     # block containing `cut` is split across the two "ranks": add as uint64 then mod-reduce
     bsplit = cut // plan.N2
     accs = a[:bsplit] + [None] + b[1:]
-    s = a[bsplit].data + b[0].data    # int64 storage; q < 2^61 so the sum is exact
-    c13.mod_reduce(s, 2, a[bsplit].n_limbs)
+    s = a[bsplit].data + b[0].data    # int64 storage; q < 2^61 so the sum is exact (extended-basis partials)
+    assert a[bsplit].n_limbs == 4 + len(P13.p)
+    c13.mod_reduce_ext(s, 2, 4)
     a[bsplit].data = s
     accs[bsplit] = a[bsplit]
     yfin = plan.finalize(gk, accs, 0)

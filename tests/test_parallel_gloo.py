@@ -51,7 +51,7 @@ def _worker(rank, world, port, q):
     ranges = PAR.unit_ranges(units, world)
     u0, u1 = ranges[rank]
     ev = K.Ev(P, keys, plan.m)
-    accs = K.projection_partial(ev, plan, xs, w, u0, u1)      # {b: Ct}
+    accs = K.projection_partial(ev, plan, xs, w, u0, u1)      # {b: ExtCt} extended-basis partials (R-LAZY)
     parts = {b: torch.from_numpy(a.c.view(np.int64).copy()) for b, a in accs.items()}
     PAR.reduce_partial_blocks(parts, ranges, plan.N2, plan.B_out, lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
     ys = {}
@@ -59,8 +59,8 @@ def _worker(rank, world, port, q):
         if PAR.owner_of_block(b, ranges, plan.N2) != rank:
             continue
         words = t.numpy().view(np.uint64).reshape(accs[b].c.shape)
-        mods = np.array(P.q[:accs[b].L], dtype=np.uint64)[None, :, None]
-        acc = O.Ct(words % mods, accs[b].scale)                 # the modular reduction after the uint64 SUM
+        mods = np.array(P.ext_mods(accs[b].L), dtype=np.uint64)[None, :, None]
+        acc = K.ExtCt(words % mods, accs[b].L, accs[b].scale)   # the modular reduction after the uint64 SUM
         ys[b] = K.projection_finalize(ev, plan, acc).c
     q.put((rank, ys))
     dist.barrier()
