@@ -161,6 +161,10 @@ encf_status encf_mask_clear(encf_ctx* ctx);
 
 /* ------------------------------------------------------------------------------------------ EncFormer kernels */
 #define ENCF_PROJ_DECOMPLEXIFY 1u
+/* Fused-QK mode: the G input groups are REAL ciphertexts (U = G, no complexification) and the
+ * weights are complex, W~ = Wre + i Wim (e.g. W_Q^pi_S + i W_K^pi_S); the output is Y = X Wre + i X Wim (no
+ * decomplexify; incompatible with ENCF_PROJ_DECOMPLEXIFY, G1). */
+#define ENCF_PROJ_REAL_INPUT 4u
 /* Projection plan: n/m segments, C active (C = 0 -> n/m), N1 | C (0 -> default). */
 encf_status encf_proj_plan_create(encf_ctx* ctx, int32_t m, int32_t d_in, int32_t d_out, int32_t C, int32_t N1,
                                   uint32_t flags, encf_proj_plan** out);
@@ -175,6 +179,9 @@ encf_status encf_proj_galois(encf_ctx* ctx, const encf_proj_plan* plan, uint32_t
 encf_status encf_proj_weights_size(const encf_proj_plan* plan, int32_t n_limbs, size_t* bytes);
 encf_status encf_proj_encode_weights(encf_ctx* ctx, const encf_proj_plan* plan, const double* Wbar /*host*/,
                                      int32_t n_limbs, uint64_t* w_out, void* stream);
+/* Real-input plans: w~_{b,p,g,q}(c) = Wre[gC + alpha, bC + beta] + i Wim[gC + alpha, bC + beta] (Wim may be NULL). */
+encf_status encf_proj_encode_weights_complex(encf_ctx* ctx, const encf_proj_plan* plan, const double* Wre /*host*/,
+                                             const double* Wim /*host or NULL*/, int32_t n_limbs, uint64_t* w_out, void* stream);
 /* Y = X W (C6): x[U] complexified inputs (NTT, level L); w_pt the weight stream (NTT form, layout
  * above, level L, scale w_scale).  Units (b,p) in [unit_begin, unit_end) (row-major over b, p).
  * With the full unit range and ENCF_PROJ_FINALIZE, y[b] = rescale(acc_b + conj(acc_b)) (B_out
@@ -216,6 +223,19 @@ encf_status encf_l_conv(encf_ctx* ctx, int32_t ell, int32_t sigma, double scale,
  * [L_conv][N].  masked->data must hold 2*L_conv*N words. */
 encf_status encf_export_c2m(encf_ctx* ctx, const encf_ct* in, int32_t L_conv, uint64_t mask_seed, uint64_t stream_id,
                             encf_ct* masked, uint64_t* server_share, void* stream);
+/* ------------------------------------------------------------------------------------------ import (Alg 4, GPU half) */
+/* Ring2Field local map (App. C): after Pi_Ext, party b holds m'_b in [0, 2^{ell+sigma}) per
+ * coefficient (device [N] little-endian (lo, hi) 64-bit pairs) with m'_0 + m'_1 = 2^{ell+sigma} + cl(m);
+ * out[i][k] = m'_0 mod q_i (party 0) or (m'_1 - 2^{ell+sigma}) mod q_i (party 1), i < L (coefficient form). */
+encf_status encf_ring2field_local(encf_ctx* ctx, const uint64_t* mprime, int32_t party, int32_t ell_sigma, int32_t L,
+                                  uint64_t* out, void* stream);
+/* Field2Ring local map (App. C): after the lift to Z_{2^ell'} (device [N] (lo, hi) pairs), each
+ * party reduces its share mod 2^ell (ell <= 64): out[k] = lo & (2^ell - 1). */
+encf_status encf_field2ring_local(encf_ctx* ctx, const uint64_t* share, int32_t ell, uint64_t* out, void* stream);
+/* Alg 4 step 4: P1 outputs <m> = <c> + [[t^]]_1 (c from P0, NTT form; share: plaintext over Q_L in
+ * either domain). */
+encf_status encf_import_m2c(encf_ctx* ctx, const encf_ct* c, const encf_pt* share, encf_ct* out, void* stream);
+
 /* After a cross-rank uint64 SUM (C2): reduce n_polys x [n_limbs][N] words mod q_i in place.
  * Valid while the summed value fits in 64 bits (world_size * q < 2^64). */
 encf_status encf_mod_reduce(encf_ctx* ctx, uint64_t* data, int32_t n_polys, int32_t n_limbs, void* stream);

@@ -403,12 +403,13 @@ class ProjPlan:
     C = active segments (default N_seg, G4), N1 | C (G5), N2 = C/N1, G = ceil(d_in/C),
     U = ceil(G/2) complexified inputs, B_out = ceil(d_out/C)."""
 
-    def __init__(self, n, m, d_in, d_out, C=None, N1=None):
+    def __init__(self, n, m, d_in, d_out, C=None, N1=None, real_input=False):
         self.n, self.m, self.d_in, self.d_out = n, m, d_in, d_out
         self.N_seg = n // m
         self.C = C or self.N_seg
         self.G = -(-d_in // self.C)
-        self.U = -(-self.G // 2)
+        self.real_input = real_input          # fused QK (P:1333-1341): real inputs, complex weights (G1)
+        self.U = self.G if real_input else -(-self.G // 2)
         self.B_out = -(-d_out // self.C)
         if N1 is None:
             N1 = default_n1(self.C, self.B_out, self.U)
@@ -430,9 +431,28 @@ def default_n1(C, B_out, U):
 
 
 def proj_inputs(X, plan):
-    """Complexified inputs x~_u = x^(2u) + i x^(2u+1) as slot vectors."""
+    """Complexified inputs x~_u = x^(2u) + i x^(2u+1) as slot vectors (real inputs x^(g) for a
+    fused-QK plan)."""
+    if plan.real_input:
+        return [seg_column_pack(X, plan.m, plan.C, g, plan.n) for g in range(plan.U)]
     return [seg_column_pack(X, plan.m, plan.C, 2 * u, plan.n) + 1j * seg_column_pack(X, plan.m, plan.C, 2 * u + 1, plan.n)
             for u in range(plan.U)]
+
+
+def proj_weight_slots_fused(Wre, Wim, plan, b, p, g, q):
+    """Fused-QK weights: w~(c) = Wre[gC + alpha, bC + beta] + i Wim[gC + alpha, bC + beta] so that
+    sum_{g,q} Phi^q(x^(g)) (.) w~ folds to X Wre + i X Wim (real part Q, imaginary part K for Wre = W_Q^pi_S,
+    Wim = W_K^pi_S)."""
+    C, m = plan.C, plan.m
+    d_in, d_out = Wre.shape
+    z = np.zeros(plan.n, dtype=np.complex128)
+    for c in range(C):
+        a = (c + q) % C
+        be = (c - p * plan.N1) % C
+        col, r = b * C + be, g * C + a
+        if col < d_out and r < d_in:
+            z[c * m:(c + 1) * m] = Wre[r, col] + 1j * Wim[r, col]
+    return z
 
 
 def proj_weight_slots(Wbar, plan, b, p, u, q):
@@ -730,3 +750,22 @@ def export_c2m(P, ct, L_conv, mask_seed, stream_id):
     c0 = O.padd(d.c[0], r, mods, P.N)
     share = O.pneg(r, mods, P.N)
     return O.Ct(np.stack([c0, d.c[1]]), ct.scale), share
+
+
+# ====================================================================================== conversions (App. C, Alg 4)
+def ring2field_local(P, mprime, party, ell_sigma, L):
+    """Ring2Field local map: party 0: m'_0 mod q; party 1: (m'_1 - 2^{ell+sigma}) mod q, per limb
+    of Q_L (Python integers in, coefficient-form residues out)."""
+    off = (1 << ell_sigma) if party else 0
+    return np.stack([np.array([(int(v) - off) % q for v in mprime], dtype=np.uint64) for q in P.q[:L]])
+
+
+def field2ring_local(share, ell):
+    """Field2Ring local map: reduce the lifted share modulo 2^ell."""
+    return np.array([int(v) % (1 << ell) for v in share], dtype=np.uint64)
+
+
+def import_m2c(P, ct, share_pt):
+    """Alg 4 step 4: <m> = <c> + [[t^]]_1 (plaintext share added to c0)."""
+    mods = P.q[:ct.L]
+    return O.Ct(np.stack([O.padd(ct.c[0], share_pt.m, mods, P.N), ct.c[1]]), ct.scale)

@@ -449,34 +449,49 @@ encf_status encf_proj_weights_size(const encf_proj_plan* p, int32_t nl, size_t* 
     return ENCF_OK;
 }
 
+static void encode_weights_impl(encf_ctx* c, const encf_proj_plan* p, const double* W, const double* Wim, int32_t nl,
+                                uint64_t* w_out, cudaStream_t s) {
+    need(c && p && W && w_out, ENCF_ERR_ARG, "encode_weights: null argument");
+    level_ok(c, nl);
+    const int real = (p->flags & ENCF_PROJ_REAL_INPUT) ? 1 : 0;
+    need(real || !Wim, ENCF_ERR_ARG, "complex weights need a real-input (fused-QK) plan");
+    Scratch sc(s);
+    const int N = c->N;
+    const double scale = (double)c->mods[nl - 1];
+    const size_t wsz = (size_t)p->d_in * p->d_out;
+    double* dW = (double*)sc.get(wsz);
+    CUDA_TRY(cudaMemcpyAsync(dW, W, wsz * 8, cudaMemcpyHostToDevice, s));
+    double* dWi = nullptr;
+    if (Wim) {
+        dWi = (double*)sc.get(wsz);
+        CUDA_TRY(cudaMemcpyAsync(dWi, Wim, wsz * 8, cudaMemcpyHostToDevice, s));
+    }
+    std::vector<int> bs, ps, us, qs;
+    for (int b = 0; b < p->B_out; b++)
+        for (int pp = 0; pp < p->N2; pp++)
+            for (int u = 0; u < p->U; u++)
+                for (int q = 0; q < p->N1; q++) { bs.push_back(b); ps.push_back(pp); us.push_back(u); qs.push_back(q); }
+    const int BATCH = 32;
+    for (size_t i0 = 0; i0 < bs.size(); i0 += BATCH) {
+        int cnt = (int)std::min((size_t)BATCH, bs.size() - i0);
+        k_encode_weights(*c, dW, p->d_in, p->d_out, p->C, p->N1, p->m, &bs[i0], &ps[i0], &us[i0], &qs[i0], cnt, scale, nl,
+                         w_out + i0 * nl * N, s, dWi, real);
+    }
+    size_t np = bs.size();
+    for (size_t i0 = 0; i0 < np; i0 += 4096) {
+        int cnt = (int)std::min((size_t)4096, np - i0);
+        ntt_forward(*c, PolyBatch{w_out + i0 * nl * N, (i64)nl * N, cnt, c->qmap(nl)}, s);
+    }
+}
+
 encf_status encf_proj_encode_weights(encf_ctx* c, const encf_proj_plan* p, const double* W, int32_t nl, uint64_t* w_out,
                                      void* stream) {
-    return guard([&] {
-        need(c && p && W && w_out, ENCF_ERR_ARG, "encode_weights: null argument");
-        level_ok(c, nl);
-        cudaStream_t s = S(stream);
-        Scratch sc(s);
-        const int N = c->N;
-        const double scale = (double)c->mods[nl - 1];
-        double* dW = (double*)sc.get((size_t)p->d_in * p->d_out);
-        CUDA_TRY(cudaMemcpyAsync(dW, W, (size_t)p->d_in * p->d_out * 8, cudaMemcpyHostToDevice, s));
-        std::vector<int> bs, ps, us, qs;
-        for (int b = 0; b < p->B_out; b++)
-            for (int pp = 0; pp < p->N2; pp++)
-                for (int u = 0; u < p->U; u++)
-                    for (int q = 0; q < p->N1; q++) { bs.push_back(b); ps.push_back(pp); us.push_back(u); qs.push_back(q); }
-        const int BATCH = 32;
-        for (size_t i0 = 0; i0 < bs.size(); i0 += BATCH) {
-            int cnt = (int)std::min((size_t)BATCH, bs.size() - i0);
-            k_encode_weights(*c, dW, p->d_in, p->d_out, p->C, p->N1, p->m, &bs[i0], &ps[i0], &us[i0], &qs[i0], cnt, scale, nl,
-                             w_out + i0 * nl * N, s);
-        }
-        size_t np = (size_t)p->B_out * p->N2 * p->U * p->N1;
-        for (size_t i0 = 0; i0 < np; i0 += 4096) {
-            int cnt = (int)std::min((size_t)4096, np - i0);
-            ntt_forward(*c, PolyBatch{w_out + i0 * nl * N, (i64)nl * N, cnt, c->qmap(nl)}, s);
-        }
-    });
+    return guard([&] { encode_weights_impl(c, p, W, nullptr, nl, w_out, S(stream)); });
+}
+
+encf_status encf_proj_encode_weights_complex(encf_ctx* c, const encf_proj_plan* p, const double* Wre, const double* Wim,
+                                             int32_t nl, uint64_t* w_out, void* stream) {
+    return guard([&] { encode_weights_impl(c, p, Wre, Wim, nl, w_out, S(stream)); });
 }
 
 encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_plan* p, const encf_ct* x, const uint64_t* w,
@@ -647,6 +662,46 @@ encf_status encf_export_c2m(encf_ctx* c, const encf_ct* in, int32_t Lc, uint64_t
         ntt_inverse(*c, PolyBatch{masked->data, (i64)Lc * N, 2, c->qmap(Lc)}, s);
         k_export_mask(*c, mask_seed, (0x04ull << 56) | stream_id, masked->data, share, Lc, s);
         masked->n_comp = 2; masked->n_limbs = Lc; masked->scale = x.scale; masked->ntt = 0;
+    });
+}
+
+encf_status encf_ring2field_local(encf_ctx* c, const uint64_t* mp, int32_t party, int32_t ell_sigma, int32_t L, uint64_t* out,
+                                  void* stream) {
+    return guard([&] {
+        need(c && mp && out && (party == 0 || party == 1) && ell_sigma > 0 && ell_sigma < 127, ENCF_ERR_ARG, "ring2field: bad argument");
+        level_ok(c, L);
+        R2F off;
+        for (int i = 0; i < L; i++) {
+            u64 q = c->mods[i];
+            u64 t = (u64)((((unsigned __int128)1) << ell_sigma) % q);
+            off.v[i] = party ? t : 0;
+        }
+        k_ring2field(*c, mp, out, L, off, S(stream));
+    });
+}
+
+encf_status encf_field2ring_local(encf_ctx* c, const uint64_t* share, int32_t ell, uint64_t* out, void* stream) {
+    return guard([&] {
+        need(c && share && out && ell > 0 && ell <= 64, ENCF_ERR_ARG, "field2ring: bad argument");
+        k_field2ring(*c, share, out, ell, S(stream));
+    });
+}
+
+encf_status encf_import_m2c(encf_ctx* c, const encf_ct* ct, const encf_pt* share, encf_ct* out, void* stream) {
+    return guard([&] {
+        need(c && share && share->data && out && out->data, ENCF_ERR_ARG, "import_m2c: null argument");
+        DCt x = view(ct);
+        need(x.ncomp == 2, ENCF_ERR_FORMAT, "import_m2c needs a 2-component ciphertext");
+        need(share->n_limbs == x.L, ENCF_ERR_LEVEL_MISMATCH, "import_m2c: share level != ciphertext level");
+        cudaStream_t s = S(stream);
+        Scratch sc(s);
+        const int N = c->N, L = x.L;
+        u64* t = sc.get((size_t)L * N);
+        k_copy(share->data, t, (size_t)L * N, s);
+        if (!share->ntt) ntt_forward(*c, PolyBatch{t, 0, 1, c->qmap(L)}, s);
+        k_add(*c, x.comp(0, N), t, out->data, 1, c->qmap(L), false, s);
+        k_copy(x.comp(1, N), out->data + (size_t)L * N, (size_t)L * N, s);
+        out->n_comp = 2; out->n_limbs = L; out->scale = x.scale; out->ntt = 1;
     });
 }
 

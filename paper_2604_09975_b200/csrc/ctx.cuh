@@ -178,6 +178,7 @@ struct BcastArgs {                 // value-kernel broadcast MAC (C8 step 4)
     u64* out[64];                  // b_{t0 + t}, t < nt
     int nsrc, nu, nt, dmax;        // dmax = nu - 1
 };
+struct R2F { u64 v[MAX_LIMBS]; };   // party * 2^{ell+sigma} mod q_i
 struct PairDev { const u64* a; const u64* b; i64 as, bs; };   // operands + component strides
 struct OutPos { int pos[MAX_LIMBS]; };
 
@@ -219,7 +220,8 @@ void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int l
 void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_slots, double scale, int level,
                     u64* out, cudaStream_t s, const LimbMap* lmap = nullptr);
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
-                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s);
+                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s,
+                      const double* dWim = nullptr, int real_input = 0);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s);
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
@@ -238,6 +240,8 @@ void k_lift_add(encf_ctx& c, const CopyBatch& dst, const CopyBatch& src, int n, 
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s);
 void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s);
+void k_ring2field(encf_ctx& c, const u64* mp, u64* out, int L, const R2F& off, cudaStream_t s);
+void k_field2ring(encf_ctx& c, const u64* sh, u64* out, int ell, cudaStream_t s);
 void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ ciphertext-level ops (ks.cu)

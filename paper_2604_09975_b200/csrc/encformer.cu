@@ -23,7 +23,9 @@ void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C,
     p.C = C > 0 ? C : p.N_seg;
     if (p.C > p.N_seg) throw EncfError(ENCF_ERR_PLAN_SHAPE, "C > n/m");
     p.G = (d_in + p.C - 1) / p.C;
-    p.U = (p.G + 1) / 2;
+    if ((flags & ENCF_PROJ_REAL_INPUT) && (flags & ENCF_PROJ_DECOMPLEXIFY))
+        throw EncfError(ENCF_ERR_PLAN_SHAPE, "fused-QK (real input) projections do not decomplexify (G1)");
+    p.U = (flags & ENCF_PROJ_REAL_INPUT) ? p.G : (p.G + 1) / 2;
     p.B_out = (d_out + p.C - 1) / p.C;
     if (N1 <= 0) {   // power of two dividing C nearest sqrt(B_out C / U) (G5)
         double target = std::sqrt((double)p.B_out * p.C / p.U);

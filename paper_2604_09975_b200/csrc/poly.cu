@@ -452,8 +452,9 @@ void fft2n(encf_ctx& c, double2* A, double sign, cudaStream_t s, int batch = 1) 
 // slot r + c m (c < C) holds Wbar[(2u)C + alpha, bC + beta] - i Wbar[(2u+1)C + alpha, bC + beta],
 // alpha = (c+q) mod C, beta = (c - p N1) mod C; A[5^j mod 2N] = slot j.
 struct WDiag { int b[64], p[64], u[64], q[64]; };
+// Wim != nullptr: real-input (fused-QK) plan, w~(c) = Wre[uC + alpha, col] + i Wim[uC + alpha, col].
 __global__ void weight_slots_kernel(const double* __restrict__ W, int d_in, int d_out, int C, int N1, int m, WDiag wd,
-                                    const int* rg, double2* A, int N) {
+                                    const int* rg, double2* A, int N, const double* __restrict__ Wim, int real_input) {
     const int bi = blockIdx.y;
     double2* a = A + (size_t)bi * 2 * N;
     const int b = wd.b[bi], p = wd.p[bi], u = wd.u[bi], q = wd.q[bi];
@@ -465,9 +466,14 @@ __global__ void weight_slots_kernel(const double* __restrict__ W, int d_in, int 
             int al = (c + q) % C, be = ((c - p * N1) % C + C) % C;
             int col = b * C + be;
             if (col < d_out) {
-                int r0 = 2 * u * C + al, r1 = (2 * u + 1) * C + al;
-                if (r0 < d_in) re = W[(size_t)r0 * d_out + col];
-                if (r1 < d_in) im = -W[(size_t)r1 * d_out + col];
+                if (real_input) {
+                    int r0 = u * C + al;
+                    if (r0 < d_in) { re = W[(size_t)r0 * d_out + col]; im = Wim ? Wim[(size_t)r0 * d_out + col] : 0.0; }
+                } else {
+                    int r0 = 2 * u * C + al, r1 = (2 * u + 1) * C + al;
+                    if (r0 < d_in) re = W[(size_t)r0 * d_out + col];
+                    if (r1 < d_in) im = -W[(size_t)r1 * d_out + col];
+                }
             }
         }
         a[rg[j]] = make_double2(re, im);
@@ -677,7 +683,8 @@ void k_encode_slots(encf_ctx& c, const double* re, const double* im, int n_slots
 }
 
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
-                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s) {
+                      const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s,
+                      const double* dWim, int real_input) {
     Scratch sc(s);
     double2* A = (double2*)sc.get((size_t)batch * 2 * c.N * 2);
     int* ovf = (int*)sc.get(1);
@@ -686,7 +693,8 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
     WDiag wd;
     for (int i = 0; i < batch; i++) { wd.b[i] = bs[i]; wd.p[i] = ps[i]; wd.u[i] = us[i]; wd.q[i] = qs[i]; }
     { int _slot; c.prof_begin("weight_slots_kernel", s, 0, _slot);
-    weight_slots_kernel<<<dim3(nblocks(c.N / 2, TB, 256), batch), TB, 0, s>>>(dW, d_in, d_out, C, N1, m, wd, c.d_rot_group, A, c.N);
+    weight_slots_kernel<<<dim3(nblocks(c.N / 2, TB, 256), batch), TB, 0, s>>>(dW, d_in, d_out, C, N1, m, wd, c.d_rot_group, A, c.N,
+                                                                              dWim, real_input);
     c.prof_end(_slot, s); }
     fft2n(c, A, -1.0, s, batch);
     { int _slot; c.prof_begin("round_reduce_kernel", s, 0, _slot);
@@ -1124,4 +1132,37 @@ void k_lift_add(encf_ctx& c, const CopyBatch& dst, const CopyBatch& src, int n, 
     lift_add_kernel<<<grid, TB, 0, s>>>(dst, src, L, c.N, c.d_mod, pm, pm_sh);
     c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)n * L * c.N * 8 * 3;
+}
+
+// ====================================================================================== conversion local maps (App. C)
+namespace {
+// [[m]]^(q)_b = (m'_b - party 2^{ell+sigma}) mod q_i, m'_b a 128-bit integer (lo, hi) per coefficient.
+__global__ void ring2field_kernel(const u64* __restrict__ mp, u64* __restrict__ out, int L, int N, const ModConst* __restrict__ mod,
+                                  R2F off) {
+    const size_t total = (size_t)L * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int limb = (int)(i / N), k = (int)(i % N);
+        const ModConst mc = mod[limb];
+        U128 x{mp[2 * (size_t)k], mp[2 * (size_t)k + 1]};
+        out[i] = sub_mod(barrett128(x, mc.q, mc.rhi, mc.rlo), off.v[limb], mc.q);
+    }
+}
+__global__ void field2ring_kernel(const u64* __restrict__ sh, u64* __restrict__ out, int N, u64 mask) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) out[k] = sh[2 * (size_t)k] & mask;
+}
+}  // namespace
+
+void k_ring2field(encf_ctx& c, const u64* mp, u64* out, int L, const R2F& off, cudaStream_t s) {
+    { int _slot; c.prof_begin("ring2field_kernel", s, 0, _slot);
+    ring2field_kernel<<<GRID((size_t)L * c.N), TB, 0, s>>>(mp, out, L, c.N, c.d_mod, off);
+    c.prof_end(_slot, s); }
+    c.st_launch++;
+}
+
+void k_field2ring(encf_ctx& c, const u64* sh, u64* out, int ell, cudaStream_t s) {
+    const u64 mask = ell >= 64 ? ~0ull : ((1ull << ell) - 1);
+    { int _slot; c.prof_begin("field2ring_kernel", s, 0, _slot);
+    field2ring_kernel<<<GRID((size_t)c.N), TB, 0, s>>>(sh, out, c.N, mask);
+    c.prof_end(_slot, s); }
+    c.st_launch++;
 }

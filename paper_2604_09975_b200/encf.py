@@ -77,6 +77,7 @@ _SIG = {
     "encf_proj_galois": [_p, _p, _p, _i32, ctypes.POINTER(_i32)],
     "encf_proj_weights_size": [_p, _i32, ctypes.POINTER(_sz)],
     "encf_proj_encode_weights": [_p, _p, _p, _i32, _p, _p],
+    "encf_proj_encode_weights_complex": [_p, _p, _p, _p, _i32, _p, _p],
     "encf_pt_ct_matmul": [_p, _p, _p, _p, _p, _f64, _i32, _i32, _u32, _p, _p],
     "encf_pt_ct_matmul_finalize": [_p, _p, _p, _p, _i32, _i32, _p, _p],
     "encf_attn_plan_create": [_p, _i32, _i32, _i32, _i32, _i32, _i32, ctypes.POINTER(_p)],
@@ -90,6 +91,9 @@ _SIG = {
     "encf_export_c2m": [_p, ctypes.POINTER(CT), _i32, _u64, _u64, ctypes.POINTER(CT), _p, _p],
     "encf_mod_reduce": [_p, _p, _i32, _i32, _p],
     "encf_mod_reduce_ext": [_p, _p, _i32, _i32, _p],
+    "encf_ring2field_local": [_p, _p, _i32, _i32, _i32, _p, _p],
+    "encf_field2ring_local": [_p, _p, _i32, _p, _p],
+    "encf_import_m2c": [_p, ctypes.POINTER(CT), ctypes.POINTER(PT), ctypes.POINTER(CT), _p],
     "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
 }
@@ -107,6 +111,7 @@ _lib.encf_galois_conj.argtypes = [_p]
 
 PROJ_DECOMPLEXIFY = 1
 PROJ_FINALIZE = 2
+PROJ_REAL_INPUT = 4
 KEY_RELIN = 1
 
 
@@ -376,6 +381,23 @@ class Context:
     def mod_reduce(self, tensor, n_polys, n_limbs):
         _chk(_lib.encf_mod_reduce(self.h, tensor.data_ptr(), n_polys, n_limbs, _stream()), "mod_reduce")
 
+    def ring2field_local(self, mprime_words, party, ell_sigma, L):
+        """mprime_words: device int64 tensor [N][2] (lo, hi).  Returns a coefficient-form Plaintext [L][N]."""
+        out = Plaintext(torch.empty(L * self.N, dtype=torch.int64, device=self.device), L, 1.0, 0)
+        _chk(_lib.encf_ring2field_local(self.h, mprime_words.data_ptr(), party, ell_sigma, L, out.data.data_ptr(), _stream()), "ring2field")
+        return out
+
+    def field2ring_local(self, share_words, ell):
+        out = torch.empty(self.N, dtype=torch.int64, device=self.device)
+        _chk(_lib.encf_field2ring_local(self.h, share_words.data_ptr(), ell, out.data_ptr(), _stream()), "field2ring")
+        return out
+
+    def import_m2c(self, ct, share_pt):
+        out = self.empty_ct(ct.n_limbs, 2)
+        c = out._c()
+        _chk(_lib.encf_import_m2c(self.h, ctypes.byref(ct._c()), ctypes.byref(share_pt._p()), ctypes.byref(c), _stream()), "import_m2c")
+        return out._update(c)
+
     def mod_reduce_ext(self, tensor, n_polys, L):
         _chk(_lib.encf_mod_reduce_ext(self.h, tensor.data_ptr(), n_polys, L, _stream()), "mod_reduce_ext")
 
@@ -404,9 +426,11 @@ class Keys:
 
 
 class ProjPlan:
-    def __init__(self, ctx, m, d_in, d_out, C=0, N1=0, decomplexify=True):
+    def __init__(self, ctx, m, d_in, d_out, C=0, N1=0, decomplexify=True, real_input=False):
+        """real_input=True: fused-QK plan, real inputs x^(g), complex weights, no decomplexify."""
         h = _p()
-        _chk(_lib.encf_proj_plan_create(ctx.h, m, d_in, d_out, C, N1, PROJ_DECOMPLEXIFY if decomplexify else 0, ctypes.byref(h)), "proj_plan")
+        flags = PROJ_REAL_INPUT if real_input else (PROJ_DECOMPLEXIFY if decomplexify else 0)
+        _chk(_lib.encf_proj_plan_create(ctx.h, m, d_in, d_out, C, N1, flags, ctypes.byref(h)), "proj_plan")
         self.ctx, self.h = ctx, h
         info = np.zeros(7, dtype=np.int32)
         _chk(_lib.encf_proj_plan_info(h, info.ctypes.data), "proj_plan_info")
@@ -434,6 +458,14 @@ class ProjPlan:
         W = np.ascontiguousarray(Wbar, dtype=np.float64)
         t = torch.empty(self.weights_bytes(L) // 8, dtype=torch.int64, device=self.ctx.device)
         _chk(_lib.encf_proj_encode_weights(self.ctx.h, self.h, W.ctypes.data, L, t.data_ptr(), _stream()), "encode_weights")
+        return t
+
+    def encode_weights_complex(self, Wre, Wim, L):
+        Wr = np.ascontiguousarray(Wre, dtype=np.float64)
+        Wi = np.ascontiguousarray(Wim, dtype=np.float64) if Wim is not None else None
+        t = torch.empty(self.weights_bytes(L) // 8, dtype=torch.int64, device=self.ctx.device)
+        _chk(_lib.encf_proj_encode_weights_complex(self.ctx.h, self.h, Wr.ctypes.data, Wi.ctypes.data if Wi is not None else None,
+                                                   L, t.data_ptr(), _stream()), "encode_weights_complex")
         return t
 
     def matmul(self, keys, xs, w, w_scale, unit_begin=0, unit_end=None, finalize=True):

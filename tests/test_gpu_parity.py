@@ -285,3 +285,54 @@ def test_export_c2m_bit_exact(c13, keys13):
     rm, rs = K.export_c2m(P13, ref, Lc, synth.seed_mask(0), 0)
     assert np.array_equal(c13.to_host(masked, coeff=False), rm.c)
     assert np.array_equal(share.cpu().numpy().view(np.uint64).reshape(Lc, P13.N), rs)
+
+
+def test_m2c_import_bit_exact(c13, keys13):
+    """Alg 4 GPU half: Ring2Field local maps and <c> + [[t^]]_1 equal the oracle's on every limb."""
+    ok, gk = keys13
+    P, L, ell, sig = P13, 5, 43, 40
+    rng = np.random.default_rng(70)
+    t = O.encode_coeffs(synth.complex_slots(P.n, 71), 2.0 ** 40, P.N)
+    from tests.test_oracle_kernels import _simulate_ext
+    ext = [_simulate_ext(v, ell + sig, rng) for v in t]
+    dev = {}
+    for b in (0, 1):
+        words = np.array([[e[b] & (2 ** 64 - 1), e[b] >> 64] for e in ext], dtype=np.uint64)
+        dev[b] = torch.from_numpy(words.view(np.int64).reshape(-1).copy()).to(c13.device)
+    s0 = c13.ring2field_local(dev[0], 0, ell + sig, L)
+    s1 = c13.ring2field_local(dev[1], 1, ell + sig, L)
+    r0 = K.ring2field_local(P, [e[0] for e in ext], 0, ell + sig, L)
+    r1 = K.ring2field_local(P, [e[1] for e in ext], 1, ell + sig, L)
+    assert np.array_equal(c13.to_host(s0), r0) and np.array_equal(c13.to_host(s1), r1)
+    c = O.encrypt_sk(P, ok, O.Pt(r0, 2.0 ** 40), 5)
+    got = c13.import_m2c(dev_ct(c13, c), s1)
+    assert_ct_equal(c13, got, K.import_m2c(P, c, O.Pt(r1, 2.0 ** 40)), "import_m2c")
+    lift = torch.from_numpy(np.array([[v, 0] for v in rng.integers(0, 2 ** 62, P.N)], dtype=np.uint64).view(np.int64).reshape(-1).copy()).to(c13.device)
+    f = c13.field2ring_local(lift, ell).cpu().numpy().view(np.uint64)
+    assert np.array_equal(f, K.field2ring_local(lift.cpu().numpy().view(np.uint64).reshape(-1, 2)[:, 0], ell))
+
+
+def test_fused_qk_projection_bit_exact(c13, keys13):
+    """Fused-QK plan (real inputs, complex weights): GPU encoder == oracle encoding, output bit-exact."""
+    ok, gk = keys13
+    P, m, d, L = P13, 16, 300, 4
+    plan = E.ProjPlan(c13, m, d, 256, N1=8, real_input=True)
+    oplan = K.ProjPlan(P.n, m, d, 256, N1=8, real_input=True)
+    assert (plan.U, plan.B_out, plan.N1, plan.N2) == (oplan.U, oplan.B_out, oplan.N1, oplan.N2)
+    X = synth.fixed_point_uniform((m, d), 90)
+    WQ, WK = synth.bert_weight((d, 256), 91), synth.bert_weight((d, 256), 92)
+    xs = [O.encrypt_sk(P, ok, O.encode(P, z, 2.0 ** 40, L), 20 + g) for g, z in enumerate(K.proj_inputs(X, oplan))]
+    pts = {}
+
+    def w(b, p, g, q):
+        if (b, p, g, q) not in pts:
+            pts[(b, p, g, q)] = O.encode(P, K.proj_weight_slots_fused(WQ, WK, oplan, b, p, g, q), float(P.q[L - 1]), L)
+        return pts[(b, p, g, q)]
+    ref = K.projection(K.Ev(P, ok, m), oplan, xs, w, decomplexify=False)
+    order = [w(b, p, g, q) for b in range(oplan.B_out) for p in range(oplan.N2) for g in range(oplan.U) for q in range(oplan.N1)]
+    wd = weights_tensor(c13, order, L)
+    wg = plan.encode_weights_complex(WQ, WK, L)
+    assert torch.equal(wg, wd)                        # GPU complex-weight encoder == oracle encoding, word for word
+    got = plan.matmul(gk, [dev_ct(c13, x) for x in xs], wd, float(P.q[L - 1]))
+    for a, r in zip(got, ref):
+        assert_ct_equal(c13, a, r, "fused QK")

@@ -261,3 +261,70 @@ def test_score_counts_table2():
     K.score_export(ev, plan, S)
     assert ev.ledger["ctmul"] == 448
     assert 0.8 * 630 <= ev.ledger["rot"] <= 1.2 * 630
+
+
+# ------------------------------------------------------------------ conversions (Alg 3 + Alg 4, App. C local maps)
+def _simulate_ext(value, bits, rng):
+    """Pi_Ext (OUT of scope: OT-based) simulated: shares m'_0, m'_1 in [0, 2^bits) with
+    m'_0 + m'_1 = 2^bits + value (P:1648-1651)."""
+    while True:
+        m0 = int(rng.integers(0, 2 ** 62)) * 2 ** (bits - 62) + int(rng.integers(0, 2 ** (bits - 62)))
+        m1 = 2 ** bits + int(value) - m0
+        if 0 <= m1 < 2 ** bits:
+            return m0, m1
+
+
+def test_conversion_pair_m2c_then_c2m(keys13):
+    """M2C (Alg 4) then C2M (Alg 3) at the plaintext-polynomial level, ell = 43, sigma = 40 (G19):
+    the MPC shares reconstruct the encoding of x + iy; decryption and decoding recover x and y."""
+    P, L, ell, sig = P13, 5, 43, 40
+    rng = np.random.default_rng(60)
+    x, y = synth.fixed_point_uniform(P.n, 61), synth.fixed_point_uniform(P.n, 62)
+    t = O.encode_coeffs(x + 1j * y, 2.0 ** 40, P.N)                      # t^ = Encode(x + iy, Delta), |t_k| < 2^42
+    assert np.abs(t).max() < 2 ** (ell - 1)
+    ext = [_simulate_ext(v, ell + sig, rng) for v in t]                  # Ring2Field's Pi_Ext (simulated)
+    s0 = K.ring2field_local(P, [e[0] for e in ext], 0, ell + sig, L)
+    s1 = K.ring2field_local(P, [e[1] for e in ext], 1, ell + sig, L)
+    assert np.array_equal(O.padd(s0, s1, P.q[:L], P.N), O.from_signed(t, P.q[:L], P.N))   # shares sum to t^ mod Q_L
+    c = O.encrypt_sk(P, keys13, O.Pt(s0, 2.0 ** 40), 5)                 # P0 encrypts its share
+    m = K.import_m2c(P, c, O.Pt(s1, 2.0 ** 40))                          # P1 adds its share
+    z = O.decode(P, O.decrypt(P, keys13, m))
+    assert np.abs(z.real - x).max() < 1e-6 and np.abs(z.imag - y).max() < 1e-6
+    # ... and back: C2M export at L_conv = 2, P0 decrypts, Field2Ring (simulated lift of the Z_Q shares), mod 2^ell
+    Lc = 2
+    masked, share = K.export_c2m(P, m, Lc, synth.seed_mask(1), 7)
+    t0 = O.decrypt(P, keys13, masked).m
+    v0, Q = O.crt_lift(t0, P.q[:Lc], centered=False)
+    v1, _ = O.crt_lift(share, P.q[:Lc], centered=False)
+    tot = [(a + b) % Q for a, b in zip(v0, v1)]
+    cl = [v - Q if v > Q // 2 else v for v in tot]                        # cl_Q of the reconstructed plaintext
+    lift0 = [int(rng.integers(0, 2 ** 62)) * 4 for _ in cl]             # Pi_Ext to Z_{2^ell'}, ell' = 128 (simulated)
+    lift1 = [(v - a) % 2 ** 128 for v, a in zip(cl, lift0)]
+    r0, r1 = K.field2ring_local(lift0, ell), K.field2ring_local(lift1, ell)
+    rec = [(int(a) + int(b)) % 2 ** ell for a, b in zip(r0, r1)]
+    rec = np.array([v - 2 ** ell if v >= 2 ** (ell - 1) else v for v in rec])
+    assert np.abs(rec - t).max() <= 64                                   # t^ plus the (small) encryption noise
+    z2 = O.decode_coeffs([int(v) for v in rec], 2.0 ** 40, P.N)
+    assert np.abs(z2.real - x).max() < 1e-6 and np.abs(z2.imag - y).max() < 1e-6
+
+
+def test_fused_qk_projection(keys13):
+    """Fused QK: one projection with W~ = W_Q^pi + i W_K^pi over REAL inputs gives
+    Re = X W_Q^pi and Im = X W_K^pi (no decomplexify, G1)."""
+    P, m, d, L = P13, 16, 300, 4
+    plan = K.ProjPlan(P.n, m, d, 2 * 128, N1=8, real_input=True)
+    assert (plan.U, plan.G, plan.B_out) == (2, 2, 1)
+    X = synth.fixed_point_uniform((m, d), 80)
+    WQ, WK = synth.bert_weight((d, 256), 81), synth.bert_weight((d, 256), 82)
+    xs = [enc(P, keys13, z, L, 10 + g) for g, z in enumerate(K.proj_inputs(X, plan))]
+    cache = {}
+
+    def w(b, p, g, q):
+        if (b, p, g, q) not in cache:
+            cache[(b, p, g, q)] = O.encode(P, K.proj_weight_slots_fused(WQ, WK, plan, b, p, g, q), float(P.q[L - 1]), L)
+        return cache[(b, p, g, q)]
+    ev = K.Ev(P, keys13, m)
+    y = K.projection(ev, plan, xs, w, decomplexify=False)[0]
+    Z = K.seg_column_unpack(dec(P, keys13, y), m, 256, 256, 0)
+    assert rel_err(Z.real, X @ WQ) < TOL and rel_err(Z.imag, X @ WK) < TOL
+    assert ev.ledger["conj"] == 0
