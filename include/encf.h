@@ -90,9 +90,13 @@ encf_status encf_stats_reset(encf_ctx* ctx);
  * "ks_inner", "ntt" (one fwd/inv transform = a pair of launches) and the *_kernel launchers.
  * encf_profile_read synchronises on those events and returns the summed device time, the launch
  * count and the summed ALGORITHMIC bytes (DESIGN.md §Roofline, 0 where not defined) for `kernel`,
- * then forgets them. */
+ * then forgets them.  encf_profile_peek returns the same without forgetting: for a stream CAPTURED into a
+ * CUDA graph the events are graph nodes re-recorded at every replay, so a peek after each replay reads that
+ * replay's launches.  Every entry point of the kernel path is capturable once a warm-up call has filled
+ * the mask cache (request tables are then uploaded from a persistent pinned arena). */
 encf_status encf_profile_enable(encf_ctx* ctx, const char* which);
 encf_status encf_profile_read(encf_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches, uint64_t* alg_bytes);
+encf_status encf_profile_peek(encf_ctx* ctx, const char* kernel, double* total_ms, uint64_t* launches, uint64_t* alg_bytes);
 
 /* ------------------------------------------------------------------------------------------ keys (testing helpers) */
 #define ENCF_KEY_RELIN 1u

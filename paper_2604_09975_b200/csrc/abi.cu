@@ -125,6 +125,14 @@ encf_status encf_keygen(encf_ctx* c, uint64_t seed, const uint32_t* galois, int3
         Scratch sc(s);
         u64* sp = sc.get((size_t)nl * N);
         u64* tmp = sc.get((size_t)nl * N);
+        u64* dR = sc.get(nl);
+        u64* dRs = sc.get(nl);
+        {
+            std::vector<u64> r(nl), rs(nl);
+            for (int e = 0; e < nl; e++) { u64 q = c->mods[em.mod[e]]; r[e] = c->mont_R[em.mod[e]]; rs[e] = shoup_pre(r[e], q); }
+            CUDA_TRY(cudaMemcpyAsync(dR, r.data(), nl * 8, cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaMemcpyAsync(dRs, rs.data(), nl * 8, cudaMemcpyHostToDevice, s));
+        }
         for (uint32_t g : targets) {
             need(g == 0u || (g & 1u), ENCF_ERR_ARG, "galois elements must be odd");
             if (k->ksk.count(g)) continue;
@@ -160,6 +168,7 @@ encf_status encf_keygen(encf_ctx* c, uint64_t seed, const uint32_t* galois, int3
                 k_scalar_mul(*c, tmp, 1, dm, dp, dps, s);
                 k_add(*c, b + (size_t)lo * N, tmp, b + (size_t)lo * N, 1, dm, false, s);
             }
+            k_scalar_mul(*c, key, k->dnum * 2, em, dR, dRs, s);   // stored in Montgomery form (ks_inner REDC)
             k->ksk[g] = key;
         }
         CUDA_TRY(cudaStreamSynchronize(s));
@@ -196,6 +205,17 @@ encf_status encf_keys_export(encf_ctx* c, const encf_keys* k, int32_t which, uin
             auto it = k->ksk.find(galois);
             need(it != k->ksk.end(), ENCF_ERR_MISSING_KEY, "keys_export: no such key");
             k_copy(it->second, out, (size_t)k->dnum * 2 * nl * c->N, s);
+            {   // out of Montgomery form
+                Scratch sc(s);
+                u64* dR = sc.get(nl);
+                u64* dRs = sc.get(nl);
+                std::vector<u64> r(nl), rs(nl);
+                for (int e = 0; e < nl; e++) { u64 q = c->mods[em.mod[e]]; r[e] = c->mont_Rinv[em.mod[e]]; rs[e] = shoup_pre(r[e], q); }
+                CUDA_TRY(cudaMemcpyAsync(dR, r.data(), nl * 8, cudaMemcpyHostToDevice, s));
+                CUDA_TRY(cudaMemcpyAsync(dRs, rs.data(), nl * 8, cudaMemcpyHostToDevice, s));
+                k_scalar_mul(*c, out, k->dnum * 2, em, dR, dRs, s);
+                CUDA_TRY(cudaStreamSynchronize(s));
+            }
             ntt_inverse(*c, PolyBatch{out, (i64)nl * c->N, k->dnum * 2, em}, s);
         }
     });

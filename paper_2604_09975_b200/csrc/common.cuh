@@ -61,6 +61,16 @@ HD u64 mulmod_barrett(u64 a, u64 b, u64 q, u64 rhi, u64 rlo) {
     return barrett128(x, q, rhi, rlo);
 }
 
+// Montgomery reduction, R = 2^64: T R^{-1} mod q in [0, q) for any 128-bit T < q 2^64, qinv = -q^{-1} mod 2^64.
+// T + m q = 0 mod 2^64 for m = T.lo qinv, so (T + m q) / 2^64 = T.hi + mulhi(m, q) + (T.lo != 0) < 2q.
+// Used where one factor of every product is a stored constant kept in Montgomery form (w R mod q): key
+// limbs and base-conversion matrices.  Two multiplies instead of the ~7 of barrett128.
+HD u64 redc128(U128 T, u64 q, u64 qinv) {
+    u64 m = T.lo * qinv;
+    u64 t = T.hi + umulhi(m, q) + (T.lo != 0 ? 1ull : 0ull);
+    return t >= q ? t - q : t;
+}
+
 // Shoup: a * w mod q with wp = floor(w 2^64 / q), w < q, any a < 2^64.  Lazy result in [0, 2q).
 HD u64 mul_shoup_lazy(u64 a, u64 w, u64 wp, u64 q) {
     u64 h = umulhi(a, wp);
@@ -87,6 +97,7 @@ struct ModConst {
     u64 q;
     u64 rhi, rlo;       // floor(2^128 / q)
     u64 two_q;
+    u64 qinv;           // -q^{-1} mod 2^64 (Montgomery)
 };
 
 // Host 128-bit helpers.
@@ -97,6 +108,12 @@ inline u64 h_powmod(u64 a, u64 e, u64 q) {
     return r;
 }
 inline u64 h_invmod(u64 a, u64 q) { return h_powmod(a % q, q - 2, q); }
+inline u64 h_neg_inv64(u64 q) {   // -q^{-1} mod 2^64, q odd (Newton)
+    u64 x = q;
+    for (int i = 0; i < 6; i++) x *= 2 - q * x;
+    return (u64)0 - x;
+}
+inline u64 h_mont_R(u64 q) { return (u64)(((unsigned __int128)1 << 64) % q); }
 inline void h_ratio128(u64 q, u64& rhi, u64& rlo) {
     // floor(2^128 / q) = floor((2^128 - 1) / q) for q not a power of two
     unsigned __int128 all = ~(unsigned __int128)0;

@@ -2,6 +2,7 @@
 // All constants are computed on the host with exact 128-bit modular arithmetic (no big integers
 // are needed: every CRT factor is a product of primes reduced modulo a single prime).
 #include <cstring>
+#include <cstdlib>
 #include "ctx.cuh"
 
 static thread_local std::string g_last_error;
@@ -71,6 +72,12 @@ static void build(encf_ctx& c, const encf_params* p) {
             throw EncfError(ENCF_ERR_ARG, "every modulus must be a prime < 2^61 with q = 1 mod 2N");
     }
     const int M = (int)c.mods.size(), N = c.N;
+    for (u64 q : c.mods) {
+        c.max_mod = std::max(c.max_mod, q);
+        c.mont_R.push_back(h_mont_R(q));
+        c.mont_Rinv.push_back(h_invmod(h_mont_R(q), q));
+    }
+    auto mont = [&](u64 w, u64 q) { return h_mulmod(w, h_mont_R(q), q); };   // base-conversion constants in Montgomery form
     std::vector<ModConst> mc(M);
     std::vector<u64> psi(M * (size_t)N), psi_sh(M * (size_t)N), ipsi(M * (size_t)N), ipsi_sh(M * (size_t)N);
     std::vector<u64> ninv(M), ninv_sh(M), im(M), im_sh(M);
@@ -79,6 +86,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         u64 q = c.mods[i];
         mc[i].q = q;
         mc[i].two_q = 2 * q;
+        mc[i].qinv = h_neg_inv64(q);
         h_ratio128(q, mc[i].rhi, mc[i].rlo);
         u64 ps = find_psi(q, N), ips = h_invmod(ps, q);
         c.psi[i] = ps;
@@ -111,6 +119,25 @@ static void build(encf_ctx& c, const encf_params* p) {
         }
         c.d_tw2 = upload(c, f);
         c.d_itw2 = upload(c, iv);
+        // FP64 path tables (exact integer doubles; w/q rounded to nearest by the host division)
+        std::vector<double> ff(2 * psi.size()), fi(2 * psi.size()), fpc(4 * (size_t)M);
+        for (size_t i = 0; i < psi.size(); i++) {
+            const double q = (double)c.mods[i / N];
+            ff[2 * i] = (double)psi[i]; ff[2 * i + 1] = (double)psi[i] / q;
+            fi[2 * i] = (double)ipsi[i]; fi[2 * i + 1] = (double)ipsi[i] / q;
+        }
+        for (int i = 0; i < M; i++) {
+            const double q = (double)c.mods[i];
+            fpc[4 * i] = q; fpc[4 * i + 1] = 1.0 / q;
+            fpc[4 * i + 2] = (double)ninv[i]; fpc[4 * i + 3] = (double)ninv[i] / q;
+            if (c.mods[i] < (1ull << 41) && !std::getenv("ENCF_NTT_INT_ONLY")) c.fpmask |= 1ull << i;
+        }
+        c.d_twf = (double*)c.dev_alloc(ff.size() * 8);
+        c.d_itwf = (double*)c.dev_alloc(fi.size() * 8);
+        c.d_fpc = (double*)c.dev_alloc(fpc.size() * 8);
+        CUDA_TRY(cudaMemcpy(c.d_twf, ff.data(), ff.size() * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(c.d_itwf, fi.data(), fi.size() * 8, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(c.d_fpc, fpc.data(), fpc.size() * 8, cudaMemcpyHostToDevice));
     }
     c.d_ninv = upload(c, ninv); c.d_ninv_sh = upload(c, ninv_sh);
     c.d_imag = upload(c, im); c.d_imag_sh = upload(c, im_sh);
@@ -144,7 +171,7 @@ static void build(encf_ctx& c, const encf_params* p) {
                     u64 tq = c.mods[t.tgt.mod[k]];
                     u64 pr = 1;
                     for (int b = 0; b < na; b++) if (b != a) pr = h_mulmod(pr, c.mods[t.lo + b] % tq, tq);
-                    wf[(size_t)a * t.tgt.n + k] = pr;
+                    wf[(size_t)a * t.tgt.n + k] = mont(pr, tq);
                 }
             }
             t.d_vfac = upload(c, vf); t.d_vfac_sh = upload(c, vfs); t.d_wfac = upload(c, wf);
@@ -163,7 +190,7 @@ static void build(encf_ctx& c, const encf_params* p) {
                 u64 qi = c.mods[i];
                 u64 pr = 1;
                 for (int b = 0; b < c.K; b++) if (b != k) pr = h_mulmod(pr, c.mods[c.L + b] % qi, qi);
-                wf[(size_t)k * lev + i] = pr;
+                wf[(size_t)k * lev + i] = mont(pr, qi);
             }
         }
         for (int i = 0; i < lev; i++) {
@@ -178,7 +205,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         for (int i = 0; i < lev; i++) {
             u64 qi = c.mods[i], P = 1;
             for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
-            pmod[i] = P ? qi - P : 0;      // stored negated: the kernel adds r * (q_i - P mod q_i)
+            pmod[i] = mont(P ? qi - P : 0, qi);      // stored negated: the kernel adds r * (q_i - P mod q_i)
         }
         md.d_pmod = upload(c, pmod);
         std::vector<u64> cfix(c.K), csh(c.K);
@@ -211,7 +238,7 @@ static void build(encf_ctx& c, const encf_params* p) {
                 for (int t = 0; t < nt; t++) {
                     u64 qt = c.mods[t], pr = 1;
                     for (int b2 = 0; b2 < nb; b2++) if (b2 != a) pr = h_mulmod(pr, bp[b2] % qt, qt);
-                    wf[(size_t)a * nt + t] = pr;
+                    wf[(size_t)a * nt + t] = mont(pr, qt);
                 }
                 cs[a] = 63 - (64 - __builtin_clzll(ba));
                 cf[a] = (u64)(((unsigned __int128)1 << (123 - cs[a])) / ba);
@@ -219,7 +246,7 @@ static void build(encf_ctx& c, const encf_params* p) {
             for (int t = 0; t < nt; t++) {
                 u64 qt = c.mods[t], B = 1;
                 for (int b2 = 0; b2 < nb; b2++) B = h_mulmod(B, bp[b2] % qt, qt);
-                corr[t] = B ? qt - B : 0;
+                corr[t] = mont(B ? qt - B : 0, qt);
                 inv[t] = h_invmod(B, qt); invs[t] = shoup_pre(inv[t], qt);
             }
             MDRTab mt;
@@ -279,8 +306,39 @@ encf_status ctx_destroy_impl(encf_ctx* c) {
     cudaDeviceSynchronize();
     for (auto& kv : c->masks) cudaFree(kv.second);
     for (void* p : c->allocations) cudaFree(p);
+    for (void* p : c->pinned) cudaFreeHost(p);
     delete c;
     return ENCF_OK;
+}
+
+void* encf_ctx::pinned_persistent(size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    bytes = (bytes + 255) & ~(size_t)255;
+    if (pinned.empty() || pin_used + bytes > pin_cap) {
+        const size_t cap = std::max(bytes, (size_t)8 << 20);
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;   // host allocation is legal mid-capture
+        CUDA_TRY(cudaThreadExchangeStreamCaptureMode(&mode));
+        void* p = nullptr;
+        cudaError_t e = cudaHostAlloc(&p, cap, cudaHostAllocDefault);
+        CUDA_TRY(cudaThreadExchangeStreamCaptureMode(&mode));
+        if (e != cudaSuccess) throw EncfError(ENCF_ERR_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+        pinned.push_back(p);
+        pin_used = 0;
+        pin_cap = cap;
+    }
+    void* r = (char*)pinned.back() + pin_used;
+    pin_used += bytes;
+    return r;
+}
+
+// Under CUDA-graph capture a plain cudaEventRecord only orders the capture; the EXTERNAL flag makes it an
+// event-record node that fires at every replay (timing-capable), so captured steps keep their live timing.
+static cudaError_t record_event(cudaEvent_t e, cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    cudaError_t err = cudaStreamIsCapturing(s, &st);
+    if (err != cudaSuccess) return err;
+    if (st == cudaStreamCaptureStatusActive) return cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    return cudaEventRecord(e, s);
 }
 
 cudaEvent_t encf_ctx::prof_event() {
@@ -307,7 +365,7 @@ void encf_ctx::prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int&
     }
     std::lock_guard<std::mutex> lk(mu);
     ProfRec r{name, prof_event(), prof_event(), bytes};
-    CUDA_TRY(cudaEventRecord(r.a, s));
+    CUDA_TRY(record_event(r.a, s));
     prof_recs.push_back(r);
     slot = (int)prof_recs.size() - 1;
 }
@@ -315,7 +373,7 @@ void encf_ctx::prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int&
 void encf_ctx::prof_end(int slot, cudaStream_t s) {
     if (slot < 0) return;
     std::lock_guard<std::mutex> lk(mu);
-    CUDA_TRY(cudaEventRecord(prof_recs[slot].b, s));
+    CUDA_TRY(record_event(prof_recs[slot].b, s));
 }
 
 extern "C" encf_status encf_profile_enable(encf_ctx* c, const char* which) {
@@ -327,8 +385,8 @@ extern "C" encf_status encf_profile_enable(encf_ctx* c, const char* which) {
     return ENCF_OK;
 }
 
-extern "C" encf_status encf_profile_read(encf_ctx* c, const char* kernel, double* total_ms, uint64_t* launches,
-                                         uint64_t* alg_bytes) {
+static encf_status profile_collect(encf_ctx* c, const char* kernel, double* total_ms, uint64_t* launches,
+                                   uint64_t* alg_bytes, bool forget) {
     if (!c || !kernel || !total_ms || !launches || !alg_bytes) return ENCF_ERR_ARG;
     try {
         std::lock_guard<std::mutex> lk(c->mu);
@@ -341,8 +399,12 @@ extern "C" encf_status encf_profile_read(encf_ctx* c, const char* kernel, double
             float t = 0.f;
             CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
             ms += t; n++; by += r.bytes;
-            c->ev_pool.push_back(r.a);
-            c->ev_pool.push_back(r.b);
+            if (forget) {
+                c->ev_pool.push_back(r.a);
+                c->ev_pool.push_back(r.b);
+            } else {
+                keep.push_back(r);
+            }
         }
         c->prof_recs = keep;
         *total_ms = ms; *launches = n; *alg_bytes = by;
@@ -351,4 +413,14 @@ extern "C" encf_status encf_profile_read(encf_ctx* c, const char* kernel, double
         set_last_error(e.msg);
         return e.code;
     }
+}
+
+extern "C" encf_status encf_profile_read(encf_ctx* c, const char* kernel, double* total_ms, uint64_t* launches,
+                                         uint64_t* alg_bytes) {
+    return profile_collect(c, kernel, total_ms, launches, alg_bytes, true);
+}
+
+extern "C" encf_status encf_profile_peek(encf_ctx* c, const char* kernel, double* total_ms, uint64_t* launches,
+                                         uint64_t* alg_bytes) {
+    return profile_collect(c, kernel, total_ms, launches, alg_bytes, false);
 }

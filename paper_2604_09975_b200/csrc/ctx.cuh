@@ -84,10 +84,17 @@ struct encf_ctx {
     int N = 0, logN = 0, L = 0, K = 0, alpha = 0;
     int s1 = 0, s2 = 0;                 // NTT phase split: N = 2^s1 (rows) x 2^s2 (columns)
     std::vector<u64> mods;              // q_0..q_{L-1}, p_0..p_{K-1}
+    u64 max_mod = 0;
+    std::vector<u64> mont_R, mont_Rinv; // 2^64 mod q and its inverse, per modulus id
     std::vector<u64> psi;               // chosen primitive 2N-th roots
     ModConst* d_mod = nullptr;          // [L+K]
     u64 *d_psi = nullptr, *d_psi_sh = nullptr, *d_ipsi = nullptr, *d_ipsi_sh = nullptr;   // [L+K][N]
     u64 *d_tw2 = nullptr, *d_itw2 = nullptr;        // [L+K][N][2] interleaved {w, w'} (fwd / inv)
+    // FP64-pipe NTT path (ntt.cu) for moduli q < 2^41: twiddles as exact doubles {w, w/q}, per-modulus
+    // {q, 1/q, N^-1, N^-1/q}; bit m of fpmask set <=> modulus id m takes the FP64 path
+    double *d_twf = nullptr, *d_itwf = nullptr;     // [L+K][N][2]
+    double* d_fpc = nullptr;                        // [L+K][4]
+    u64 fpmask = 0;
     u64 *d_ninv = nullptr, *d_ninv_sh = nullptr;    // [L+K]
     u64 *d_imag = nullptr, *d_imag_sh = nullptr;    // [L+K]  psi^{N/2} (a 4th root of unity)
     std::vector<std::vector<ModUpTab>> modup;       // [level][digit]
@@ -125,6 +132,11 @@ struct encf_ctx {
     }
     size_t limb_words() const { return (size_t)N; }
     void* dev_alloc(size_t bytes);
+    // persistent pinned host arena: request tables uploaded while a stream is being CAPTURED into a CUDA
+    // graph must outlive the capture (the memcpy node re-reads them at every replay); freed at destroy.
+    std::vector<void*> pinned;
+    size_t pin_used = 0, pin_cap = 0;
+    void* pinned_persistent(size_t bytes);
 };
 
 // key material (device, NTT form)
@@ -204,10 +216,6 @@ void k_rescale_prep(encf_ctx& c, const u64* last_coeff, u64* corr, int level, in
                     cudaStream_t s);
 void k_rescale_finish(encf_ctx& c, const u64* in, i64 in_stride, const u64* corr, u64* out, i64 out_stride,
                       int ncomp, int level, cudaStream_t s);
-void k_bconv(encf_ctx& c, const u64* in, const LimbMap& in_map, const u64* d_vfac, const u64* d_vfac_sh,
-             const u64* d_wfac, const LimbMap& out_map, u64* out, const int* out_pos, cudaStream_t s);
-void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const u64* key, int key_nl,
-                const LimbMap& key_limb_of, u64* acc, cudaStream_t s);
 void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level,
                       const ModDownTab& t, cudaStream_t s);
 void k_tensor_acc(encf_ctx& c, const u64* const* a, const u64* const* b, int nterms, u64* out3, int level,

@@ -3,6 +3,7 @@
 // processed by one launch sequence (ModUp / inner product / ModDown / rescale / lazy sums), so the
 // grid covers all of them.  Bit-exact schedule contract: SURVEY.md §8c C4/C5 (oracle/ckks.py).
 #pragma once
+#include <cstring>
 #include <vector>
 #include "ctx.cuh"
 
@@ -97,8 +98,20 @@ struct Ev {
     double mask_scale(int level) const { return (double)c.mods[level - 1]; }
     template <class T>
     T* upload(const std::vector<T>& v) {
-        u64* d = sc.get((v.size() * sizeof(T) + 7) / 8 + 1);
-        CUDA_TRY(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        // eager: pageable copy (staged by the driver, so v may die at once); under CUDA-graph capture the
+        // table is copied into the context's persistent pinned arena, which the memcpy node re-reads at replay
+        const size_t bytes = v.size() * sizeof(T);
+        u64* d = sc.get((bytes + 7) / 8 + 1);
+        if (!bytes) return (T*)d;
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        CUDA_TRY(cudaStreamIsCapturing(s, &st));
+        const void* src = v.data();
+        if (st == cudaStreamCaptureStatusActive) {
+            void* h = c.pinned_persistent(bytes);
+            std::memcpy(h, v.data(), bytes);
+            src = h;
+        }
+        CUDA_TRY(cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, s));
         return (T*)d;
     }
 };

@@ -8,6 +8,8 @@
 //   phase B: the last s2 stages stay inside contiguous chunks of S words -> a CTA stages a
 //            group of chunks.
 // (Inverse runs B then A.)  One launch per phase covers every limb of every polynomial of a batch.
+#include <cstdlib>
+#include <type_traits>
 #include "ctx.cuh"
 
 namespace {
@@ -23,11 +25,16 @@ struct NttArgs {
     const u64* tw;       // psi_brv (fwd) or ipsi_brv (inv): [mods][N]
     const u64* tw_sh;
     const ulonglong2* tw2;   // interleaved {w, w'}: [mods][N]
+    const double2* twf;      // FP64 path: {w, w/q}: [mods][N]
+    const double* fpc;       // FP64 path: [mods][4] = {q, 1/q, N^-1, N^-1/q}
+    u64 fpmask;              // modulus ids on the FP64 path
     const u64* ninv;
     const u64* ninv_sh;
     int N, logN, s1, s2;
 };
 
+// ---------------------------------------------------------------------------------------------
+// Integer path (any q < 2^61): Harvey lazy butterflies, Shoup twiddles, values in [0, 4q).
 __device__ __forceinline__ void ct_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u64 two_q) {
     u64 x = X >= two_q ? X - two_q : X;
     u64 t = mul_shoup_lazy(Y, W, Wp, q);
@@ -42,6 +49,62 @@ __device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u6
     Y = mul_shoup_lazy(t, W, Wp, q);
     X = x;
 }
+
+struct IntOps {
+    using T = u64;
+    using TW = ulonglong2;
+    u64 q, two_q;
+    __device__ __forceinline__ void ct(u64& X, u64& Y, TW w) const { ct_bfly(X, Y, w.x, w.y, q, two_q); }
+    __device__ __forceinline__ void gs(u64& X, u64& Y, TW w) const { gs_bfly(X, Y, w.x, w.y, q, two_q); }
+};
+
+// ---------------------------------------------------------------------------------------------
+// FP64 path (q < 2^41; sm_100a runs DFMA/DMUL/DADD at 64 lanes/clk/SM on the fp64 pipe, while a 64-bit
+// Shoup product costs ~32 fmaheavy cycles per warp on the integer side -- tools/micro/pipes.cu).
+// Values are integer-valued doubles, SIGNED, |x| < 2^50.  Product a*w mod q (w in [0,q), wq = fl(w/q)):
+//   ph = fl(a w), pl = a w - ph (exact by FMA), qt = round(a wq) (exact via the 1.5*2^52 shifter,
+//   |a wq| < 2^51), r = fma(-qt, q, ph) + pl = a w - qt q EXACTLY (|.| < 2^53), |qt - a w/q| < 1 => |r| < q.
+// Forward (CT): X' = X + r, Y' = X - r -> the bound grows by q per stage (17q < 2^46 after 16 stages).
+// Inverse (GS): X' = X + Y doubles per stage -> a centred reduction after the first phase (2^8 * 2q < 2^50).
+// Results are canonical [0, q) at the end of every transform: bit-identical to the integer path.
+constexpr double kShift = 6755399441055744.0;   // 1.5 * 2^52
+constexpr double kTwo52 = 4503599627370496.0;
+
+__device__ __forceinline__ double fp_mulmod(double a, double w, double wq, double q) {
+    const double ph = __dmul_rn(a, w);
+    const double pl = __fma_rn(a, w, -ph);
+    const double qt = __dsub_rn(__fma_rn(a, wq, kShift), kShift);
+    return __dadd_rn(__fma_rn(-qt, q, ph), pl);
+}
+__device__ __forceinline__ double fp_center(double x, double q, double qinv) {   // |result| <= q/2 + 1
+    const double qt = __dsub_rn(__fma_rn(x, qinv, kShift), kShift);
+    return __fma_rn(-qt, q, x);
+}
+__device__ __forceinline__ u64 fp_canon(double r, double q) {   // |r| < q + 1 -> [0, q) as u64
+    r = r < 0.0 ? __dadd_rn(r, q) : r;
+    r = r >= q ? __dsub_rn(r, q) : r;
+    return (u64)__double_as_longlong(__dadd_rn(r, kTwo52)) & ((1ull << 52) - 1);
+}
+__device__ __forceinline__ double fp_from_u64(u64 v) {   // v < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(v | 0x4330000000000000ull)), kTwo52);
+}
+
+struct FpOps {
+    using T = double;
+    using TW = double2;
+    double q;
+    __device__ __forceinline__ void ct(double& X, double& Y, TW w) const {
+        const double t = fp_mulmod(Y, w.x, w.y, q);
+        const double x = X;
+        X = __dadd_rn(x, t);
+        Y = __dsub_rn(x, t);
+    }
+    __device__ __forceinline__ void gs(double& X, double& Y, TW w) const {
+        const double sm = __dadd_rn(X, Y), df = __dsub_rn(X, Y);
+        Y = fp_mulmod(df, w.x, w.y, q);
+        X = sm;
+    }
+};
 
 // ---------------------------------------------------------------------------------------------
 // Register-resident sub-transforms.  A phase applies LT consecutive stages (global stages
@@ -66,9 +129,9 @@ __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 
 // Round A: local stages 0..EA-1 (forward ascending / inverse descending).  Local block index of the
 // pair (k, k+hs) at local stage s is k >> (EA - s); global twiddle index 2^(s0+s) + (boff << s) + blk.
-template <int LT, bool INV>
-__device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, const ulonglong2* __restrict__ tw2,
-                                        u64 q, u64 two_q) {
+template <int LT, bool INV, class Ops>
+__device__ __forceinline__ void round_a(typename Ops::T (&x)[Geo<LT>::E], int s0, int boff,
+                                        const typename Ops::TW* __restrict__ tw2, const Ops& ops) {
     constexpr int EA = Geo<LT>::EA, E = Geo<LT>::E;
 #pragma unroll
     for (int ss = 0; ss < EA; ss++) {
@@ -79,18 +142,18 @@ __device__ __forceinline__ void round_a(u64 (&x)[Geo<LT>::E], int s0, int boff, 
         for (int k = 0; k < E; k++) {
             if (k & hs) continue;
             const int idx = base + (k >> (EA - s));
-            const ulonglong2 T = __ldg(tw2 + idx);
-            if (!INV) ct_bfly(x[k], x[k + hs], T.x, T.y, q, two_q);
-            else gs_bfly(x[k], x[k + hs], T.x, T.y, q, two_q);
+            const typename Ops::TW T = __ldg(tw2 + idx);
+            if (!INV) ops.ct(x[k], x[k + hs], T);
+            else ops.gs(x[k], x[k + hs], T);
         }
     }
 }
 
 // Round B: local stages EA..LT-1.  Element ((j*G+g) << EB) + k'; block index at local stage EA+r is
 // ((j*G+g) << r) + (k' >> (EB - r)).
-template <int LT, bool INV>
-__device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int boff, const ulonglong2* __restrict__ tw2,
-                                        u64 q, u64 two_q) {
+template <int LT, bool INV, class Ops>
+__device__ __forceinline__ void round_b(typename Ops::T (&y)[Geo<LT>::E], int j, int s0, int boff,
+                                        const typename Ops::TW* __restrict__ tw2, const Ops& ops) {
     constexpr int EA = Geo<LT>::EA, EB = Geo<LT>::EB, G = Geo<LT>::G;
     constexpr int KB = 1 << EB;
 #pragma unroll
@@ -104,34 +167,34 @@ __device__ __forceinline__ void round_b(u64 (&y)[Geo<LT>::E], int j, int s0, int
             for (int k = 0; k < KB; k++) {
                 if (k & hs) continue;
                 const int idx = base + (((j * G + g) << r) + (k >> (EB - r)));
-                const ulonglong2 T = __ldg(tw2 + idx);
-                if (!INV) ct_bfly(y[g * KB + k], y[g * KB + k + hs], T.x, T.y, q, two_q);
-                else gs_bfly(y[g * KB + k], y[g * KB + k + hs], T.x, T.y, q, two_q);
+                const typename Ops::TW T = __ldg(tw2 + idx);
+                if (!INV) ops.ct(y[g * KB + k], y[g * KB + k + hs], T);
+                else ops.gs(y[g * KB + k], y[g * KB + k + hs], T);
             }
         }
     }
 }
 
-template <int LT>
-__device__ __forceinline__ void sm_put_a(u64* line, int j, const u64 (&x)[Geo<LT>::E]) {
+template <int LT, class T>
+__device__ __forceinline__ void sm_put_a(T* line, int j, const T (&x)[Geo<LT>::E]) {
 #pragma unroll
     for (int k = 0; k < Geo<LT>::E; k++) line[pad(j + Geo<LT>::TPL * k)] = x[k];
 }
-template <int LT>
-__device__ __forceinline__ void sm_get_a(const u64* line, int j, u64 (&x)[Geo<LT>::E]) {
+template <int LT, class T>
+__device__ __forceinline__ void sm_get_a(const T* line, int j, T (&x)[Geo<LT>::E]) {
 #pragma unroll
     for (int k = 0; k < Geo<LT>::E; k++) x[k] = line[pad(j + Geo<LT>::TPL * k)];
 }
-template <int LT>
-__device__ __forceinline__ void sm_put_b(u64* line, int j, const u64 (&y)[Geo<LT>::E]) {
+template <int LT, class T>
+__device__ __forceinline__ void sm_put_b(T* line, int j, const T (&y)[Geo<LT>::E]) {
     constexpr int EB = Geo<LT>::EB, G = Geo<LT>::G, KB = 1 << EB;
 #pragma unroll
     for (int g = 0; g < G; g++)
 #pragma unroll
         for (int k = 0; k < KB; k++) line[pad(((j * G + g) << EB) + k)] = y[g * KB + k];
 }
-template <int LT>
-__device__ __forceinline__ void sm_get_b(const u64* line, int j, u64 (&y)[Geo<LT>::E]) {
+template <int LT, class T>
+__device__ __forceinline__ void sm_get_b(const T* line, int j, T (&y)[Geo<LT>::E]) {
     constexpr int EB = Geo<LT>::EB, G = Geo<LT>::G, KB = 1 << EB;
 #pragma unroll
     for (int g = 0; g < G; g++)
@@ -139,105 +202,183 @@ __device__ __forceinline__ void sm_get_b(const u64* line, int j, u64 (&y)[Geo<LT
         for (int k = 0; k < KB; k++) y[g * KB + k] = line[pad(((j * G + g) << EB) + k)];
 }
 
-// Phase A (columns of the R x S limb, R = 2^LT rows).  Forward: stages 0..LT-1; inverse: LT-1..0 then
-// x N^{-1} and full reduction.  A CTA owns `lines` consecutive columns (128-byte row segments).
+// global word <-> working value.  FIRST: the transform's first phase reads canonical u64 words; later
+// phases of the FP64 path read/write raw double bits (signed intermediates), the integer path lazy u64.
+__device__ __forceinline__ u64 ld_val(u64 v, const IntOps&, bool) { return v; }
+__device__ __forceinline__ double ld_val(u64 v, const FpOps&, bool first) {
+    return first ? fp_from_u64(v) : __longlong_as_double((long long)v);
+}
+__device__ __forceinline__ u64 st_raw(u64 v) { return v; }
+__device__ __forceinline__ u64 st_raw(double v) { return (u64)__double_as_longlong(v); }
+
+// Phase A (columns of the R x S limb, R = 2^LT rows).  Forward: stages 0..LT-1 (first phase); inverse:
+// LT-1..0 then x N^{-1} and full reduction (last phase).  A CTA owns `lines` consecutive columns.
 #ifndef NTT_MINB
 #define NTT_MINB 4
 #endif
-template <int LT, bool INV>
-__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int lines) {
+template <int LT, bool INV, class Ops>
+__device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops& ops, const typename Ops::TW* tw2, int mi) {
     using GG = Geo<LT>;
-    extern __shared__ u64 sm[];
+    using T = typename Ops::T;
+    extern __shared__ u64 sm_raw[];
+    T* sm = reinterpret_cast<T*>(sm_raw);
     const int limb = blockIdx.y, poly = blockIdx.z;
-    const int mi = a.map.mod[limb];
-    const u64 q = a.mod[mi].q, two_q = 2 * q;
     const int S = 1 << a.s2;
     const int c0 = blockIdx.x * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
-    const ulonglong2* tw2 = a.tw2 + (size_t)mi * a.N;
     const int tot = GG::T * lines;
     const int lgl = 31 - __clz(lines);
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int r = e >> lgl, c = e & (lines - 1);
-        sm[c * GG::LSP + pad(r)] = g[(i64)r * S + c0 + c];
+    {   // all E loads of a thread in flight before the first use (tot = E * blockDim.x)
+        u64 v[GG::E];
+#pragma unroll
+        for (int it = 0; it < GG::E; it++) {
+            const int e = threadIdx.x + it * blockDim.x;
+            v[it] = g[(i64)(e >> lgl) * S + c0 + (e & (lines - 1))];
+        }
+#pragma unroll
+        for (int it = 0; it < GG::E; it++) {
+            const int e = threadIdx.x + it * blockDim.x;
+            sm[(e & (lines - 1)) * GG::LSP + pad(e >> lgl)] = ld_val(v[it], ops, !INV);
+        }
     }
     __syncthreads();
     const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
-    u64* line = sm + l * GG::LSP;
-    u64 x[GG::E];
+    T* line = sm + l * GG::LSP;
+    T x[GG::E];
     if (!INV) {
         sm_get_a<LT>(line, j, x);
-        round_a<LT, false>(x, 0, 0, tw2, q, two_q);
+        round_a<LT, false>(x, 0, 0, tw2, ops);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, 0, 0, tw2, q, two_q);
+        round_b<LT, false>(x, j, 0, 0, tw2, ops);
         sm_put_b<LT>(line, j, x);
     } else {
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, 0, 0, tw2, q, two_q);
+        round_b<LT, true>(x, j, 0, 0, tw2, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, 0, 0, tw2, q, two_q);
-        const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
+        round_a<LT, true>(x, 0, 0, tw2, ops);
+        if constexpr (std::is_same<T, u64>::value) {
+            const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
 #pragma unroll
-        for (int k = 0; k < GG::E; k++) x[k] = mul_shoup(x[k], ni, nip, q);
+            for (int k = 0; k < GG::E; k++) x[k] = mul_shoup(x[k], ni, nip, ops.q);
+        } else {
+            const double ni = a.fpc[4 * mi + 2], niq = a.fpc[4 * mi + 3];
+#pragma unroll
+            for (int k = 0; k < GG::E; k++) x[k] = fp_mulmod(x[k], ni, niq, ops.q);   // |x| < q: canonicalised on store
+        }
         sm_put_a<LT>(line, j, x);
     }
     __syncthreads();
     for (int e = threadIdx.x; e < tot; e += blockDim.x) {
         const int r = e >> lgl, c = e & (lines - 1);
-        g[(i64)r * S + c0 + c] = sm[c * GG::LSP + pad(r)];   // forward: lazy [0, 4q) handed to phase B
+        const T v = sm[c * GG::LSP + pad(r)];
+        u64 w;
+        if constexpr (std::is_same<T, u64>::value) w = v;                  // forward: lazy [0, 4q) to phase B
+        else w = INV ? fp_canon(v, ops.q) : st_raw(v);
+        g[(i64)r * S + c0 + c] = w;
     }
 }
 
-// Phase B (contiguous chunks of S = 2^LT words).  Forward: stages s1..logN-1 then reduce to [0, q);
-// the round-A mapping reads the chunk straight from global memory (coalesced).  Inverse: stages
-// logN-1..s1, lazy [0, 2q) output written straight from the round-A registers.
 template <int LT, bool INV>
-__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int lines) {
+__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int lines) {
+    const int mi = a.map.mod[blockIdx.y];
+    if ((a.fpmask >> mi) & 1ull) {
+        cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
+    } else {
+        const u64 q = a.mod[mi].q;
+        cols_body<LT, INV>(a, lines, IntOps{q, 2 * q}, a.tw2 + (size_t)mi * a.N, mi);
+    }
+}
+
+// Phase B (contiguous chunks of S = 2^LT words).  Forward: stages s1..logN-1 then reduce to [0, q)
+// (last phase); the round-A mapping reads the chunk straight from global memory (coalesced).  Inverse:
+// stages logN-1..s1 (first phase), lazy output written straight from the round-A registers.
+// Line l of a CTA = chunk (blockIdx.x << lgc) + (l & (LC-1)) of polynomial (blockIdx.z << lgp) + (l >> lgc),
+// LC = 2^lgc chunks x LP = lines / LC polynomials: with LC = 1 every line of the CTA is the SAME chunk of a
+// different polynomial, so all lines share one twiddle set (L1-resident) instead of 16 distinct ones.
+template <int LT, bool INV, class Ops>
+__device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, const Ops& ops, const typename Ops::TW* tw2,
+                                          int mi) {
     using GG = Geo<LT>;
-    extern __shared__ u64 sm[];
-    const int limb = blockIdx.y, poly = blockIdx.z;
-    const int mi = a.map.mod[limb];
-    const u64 q = a.mod[mi].q, two_q = 2 * q;
-    const int ch0 = blockIdx.x * lines;
-    u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N + (i64)ch0 * GG::T;
-    const ulonglong2* tw2 = a.tw2 + (size_t)mi * a.N;
+    using T = typename Ops::T;
+    extern __shared__ u64 sm_raw[];
+    T* sm = reinterpret_cast<T*>(sm_raw);
+    const int limb = blockIdx.y;
+    const int cmask = (1 << lgc) - 1;
+    u64* g0 = a.base + (i64)limb * a.N;
+    auto line_ptr = [&](int ll) -> u64* {
+        return g0 + (i64)(((int)blockIdx.z << (31 - __clz(lines) - lgc)) + (ll >> lgc)) * a.poly_stride +
+               (i64)(((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T;
+    };
     const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
-    u64* line = sm + l * GG::LSP;
-    u64* gl = g + (size_t)l * GG::T;
-    const int boff = ch0 + l;
+    T* line = sm + l * GG::LSP;
+    u64* gl = line_ptr(l);
+    const int boff = ((int)blockIdx.x << lgc) + (l & cmask);
     const int tot = GG::T * lines;
-    u64 x[GG::E];
+    T x[GG::E];
     if (!INV) {
 #pragma unroll
-        for (int k = 0; k < GG::E; k++) x[k] = gl[j + GG::TPL * k];
-        round_a<LT, false>(x, a.s1, boff, tw2, q, two_q);
+        for (int k = 0; k < GG::E; k++) x[k] = ld_val(gl[j + GG::TPL * k], ops, false);
+        round_a<LT, false>(x, a.s1, boff, tw2, ops);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, a.s1, boff, tw2, q, two_q);
+        round_b<LT, false>(x, j, a.s1, boff, tw2, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-            u64 v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
-            v = v >= two_q ? v - two_q : v;
-            v = v >= q ? v - q : v;
-            g[e] = v;
+            const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
+            u64* ge = line_ptr(e >> LT) + (e & (GG::T - 1));
+            if constexpr (std::is_same<T, u64>::value) {
+                const u64 q = ops.q, two_q = ops.two_q;
+                u64 w = v >= two_q ? v - two_q : v;
+                *ge = w >= q ? w - q : w;
+            } else {
+                const double q = ops.q, qinv = a.fpc[4 * mi + 1];
+                *ge = fp_canon(fp_center(v, q, qinv), q);
+            }
         }
     } else {
-        for (int e = threadIdx.x; e < tot; e += blockDim.x) sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))] = g[e];
+        u64 v[GG::E];   // all E loads in flight before the first use (tot = E * blockDim.x)
+#pragma unroll
+        for (int it = 0; it < GG::E; it++) {
+            const int e = threadIdx.x + it * blockDim.x;
+            v[it] = line_ptr(e >> LT)[e & (GG::T - 1)];
+        }
+#pragma unroll
+        for (int it = 0; it < GG::E; it++) {
+            const int e = threadIdx.x + it * blockDim.x;
+            sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))] = ld_val(v[it], ops, true);
+        }
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, a.s1, boff, tw2, q, two_q);
+        round_b<LT, true>(x, j, a.s1, boff, tw2, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, a.s1, boff, tw2, q, two_q);
+        round_a<LT, true>(x, a.s1, boff, tw2, ops);
+        if constexpr (std::is_same<T, u64>::value) {
 #pragma unroll
-        for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = x[k];
+            for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = x[k];
+        } else {
+            const double qinv = a.fpc[4 * mi + 1];
+#pragma unroll
+            for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = st_raw(fp_center(x[k], ops.q, qinv));
+        }
+    }
+}
+
+template <int LT, bool INV>
+__global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int lines, int lgc) {
+    const int mi = a.map.mod[blockIdx.y];
+    if ((a.fpmask >> mi) & 1ull) {
+        rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
+    } else {
+        const u64 q = a.mod[mi].q;
+        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 2 * q}, a.tw2 + (size_t)mi * a.N, mi);
     }
 }
 
@@ -252,9 +393,9 @@ void launch_cols(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, co
 }
 
 template <bool INV>
-void launch_rows(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines) {
+void launch_rows(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines, int lgc) {
     switch (LT) {
-#define C(LTV) case LTV: ntt_rows_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines); break;
+#define C(LTV) case LTV: ntt_rows_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines, lgc); break;
         C(2) C(3) C(4) C(5) C(6) C(7) C(8)
 #undef C
         default: throw EncfError(ENCF_ERR_ARG, "ntt: unsupported phase size");
@@ -276,6 +417,20 @@ PhaseCfg phase_cfg(int LT, int avail) {   // avail = number of lines of one limb
     return p;
 }
 
+// Rows-phase grid: LP polynomials x LC chunks per CTA (LP = the largest power of two <= lines dividing npolys,
+// unless ENCF_NTT_ROWS_CHUNK_MAJOR is set).
+struct RowsCfg { dim3 grid; int lgc; };
+RowsCfg rows_cfg(const PhaseCfg& B, int nchunks, int npolys, int nlimbs) {
+    int lp = 1;
+    static const bool chunk_major = std::getenv("ENCF_NTT_ROWS_CHUNK_MAJOR") != nullptr;
+    if (!chunk_major)
+        while (lp * 2 <= B.lines && npolys % (lp * 2) == 0) lp *= 2;
+    const int lc = B.lines / lp;
+    int lgc = 0;
+    while ((1 << lgc) < lc) lgc++;
+    return RowsCfg{dim3(nchunks / lc, nlimbs, npolys / lp), lgc};
+}
+
 NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     NttArgs a;
     a.base = b.base;
@@ -285,6 +440,9 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.tw = inv ? c.d_ipsi : c.d_psi;
     a.tw_sh = inv ? c.d_ipsi_sh : c.d_psi_sh;
     a.tw2 = (const ulonglong2*)(inv ? c.d_itw2 : c.d_tw2);
+    a.twf = (const double2*)(inv ? c.d_itwf : c.d_twf);
+    a.fpc = c.d_fpc;
+    a.fpmask = c.fpmask;
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
     a.N = c.N;
@@ -303,7 +461,8 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
     launch_cols<false>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
-    launch_rows<false>(c.s2, dim3(B.blocks, b.map.n, b.npolys), B.threads, B.smem, s, a, B.lines);
+    const RowsCfg R = rows_cfg(B, 1 << c.s1, b.npolys, b.map.n);
+    launch_rows<false>(c.s2, R.grid, B.threads, B.smem, s, a, B.lines, R.lgc);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     c.st_launch += 2;
@@ -317,7 +476,8 @@ void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    launch_rows<true>(c.s2, dim3(B.blocks, b.map.n, b.npolys), B.threads, B.smem, s, a, B.lines);
+    const RowsCfg R = rows_cfg(B, 1 << c.s1, b.npolys, b.map.n);
+    launch_rows<true>(c.s2, R.grid, B.threads, B.smem, s, a, B.lines, R.lgc);
     launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;

@@ -158,67 +158,6 @@ __global__ void rescale_finish_kernel(const u64* in, i64 is, const u64* corr, u6
     }
 }
 
-// ------------------------------------------------------------------------------------ fast base conversion (C4)
-// y_t[k] = sum_i [x_i[k] vfac_i]_{q_i} wfac[i][t] mod t ; in: [n_in][N] coefficient form; out limb
-// of target t at out + pos[t]*N.  One thread per coefficient, all targets (the x_i stay in registers).
-__global__ void __launch_bounds__(TB) bconv_kernel(const u64* __restrict__ in, LimbMap im, const u64* __restrict__ vfac,
-                                                   const u64* __restrict__ vfac_sh, const u64* __restrict__ wfac,
-                                                   LimbMap om, OutPos op, u64* __restrict__ out, int N,
-                                                   const ModConst* __restrict__ mod) {
-    extern __shared__ u64 sw[];   // [n_in][n_out] wfac
-    const int nin = im.n, nout = om.n;
-    for (int i = threadIdx.x; i < nin * nout; i += blockDim.x) sw[i] = wfac[i];
-    __syncthreads();
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-        u64 v[16];
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-            if (i < nin) {
-                u64 qi = mod[im.mod[i]].q;
-                v[i] = mul_shoup(in[(size_t)i * N + k], vfac[i], vfac_sh[i], qi);
-            }
-        }
-        for (int t = 0; t < nout; t++) {
-            ModConst mc = mod[om.mod[t]];
-            U128 acc{0, 0};
-#pragma unroll
-            for (int i = 0; i < 16; i++)
-                if (i < nin) mac128(acc, v[i], sw[i * nout + t]);
-            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
-        }
-    }
-}
-
-// ------------------------------------------------------------------------------------ key-switch inner product (C4)
-// acc_c[e][k] = sum_j ext_j[e][src_g(k)] * key_j[c][kl(e)][k]  over the extended limbs e of Q_L u P.
-// The Galois gather of the hoisted batch is fused into the digit loads (g = 1: identity).
-__global__ void __launch_bounds__(TB) ks_inner_kernel(const u64* __restrict__ ext, int dnum, int nl, uint32_t g,
-                                                      const u64* __restrict__ key, int key_nl, KeyLimb klm,
-                                                      LimbMap em, u64* __restrict__ acc, int N, int logN,
-                                                      const ModConst* __restrict__ mod) {
-    const int e = blockIdx.y;
-    const ModConst mc = mod[em.mod[e]];
-    const int kle = klm.kl[e];
-    const uint32_t mask2n = 2 * N - 1;
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
-        int src = k;
-        if (g != 1) {
-            uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
-            uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
-            src = brv((int)((e2 - 1) >> 1), logN);
-        }
-        U128 a0{0, 0}, a1{0, 0};
-        for (int j = 0; j < dnum; j++) {
-            u64 x = ext[((size_t)j * nl + e) * N + src];
-            const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            mac128(a0, x, kj[(size_t)kle * N + k]);
-            mac128(a1, x, kj[((size_t)key_nl + kle) * N + k]);
-        }
-        acc[(size_t)e * N + k] = barrett128(a0, mc.q, mc.rhi, mc.rlo);
-        acc[((size_t)nl + e) * N + k] = barrett128(a1, mc.q, mc.rhi, mc.rlo);
-    }
-}
-
 // out_i = (b_i - y_i) P^{-1} (+ add0_i) mod q_i   (NTT domain)
 __global__ void moddown_finish_kernel(const u64* __restrict__ b, const u64* __restrict__ y, const u64* __restrict__ add0,
                                       u64* __restrict__ out, int level, int N, const ModConst* __restrict__ mod,
@@ -571,37 +510,6 @@ void k_rescale_finish(encf_ctx& c, const u64* in, i64 is, const u64* corr, u64* 
     c.st_launch++; c.st_bytes += (size_t)ncomp * (level - 1) * c.N * 24;
 }
 
-void k_bconv(encf_ctx& c, const u64* in, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
-             const LimbMap& om, u64* out, const int* pos, cudaStream_t s) {
-    if (im.n > 16) throw EncfError(ENCF_ERR_ARG, "bconv: at most 16 input limbs");
-    OutPos op;
-    for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
-    size_t smem = (size_t)im.n * om.n * sizeof(u64);
-    int grid = (c.N + TB - 1) / TB;
-    { int _slot; c.prof_begin("bconv_kernel", s, 0, _slot);
-    bconv_kernel<<<grid, TB, smem, s>>>(in, im, vf, vfs, wf, om, op, out, c.N, c.d_mod);
-    c.prof_end(_slot, s); }
-    c.st_launch++; c.st_bytes += (size_t)(im.n + om.n) * c.N * 8;
-}
-
-void k_ks_inner(encf_ctx& c, const u64* ext, int dnum, int nl, uint32_t g, const u64* key, int key_nl,
-                const LimbMap& key_limb_of, u64* acc, cudaStream_t s) {
-    KeyLimb kl;
-    LimbMap em;
-    em.n = nl;
-    for (int e = 0; e < nl; e++) { kl.kl[e] = key_limb_of.mod[e]; }
-    // extended modulus ids: first (nl - K) are q_0.., then p_0..
-    int Lq = nl - c.K;
-    for (int e = 0; e < nl; e++) em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
-    dim3 grid((c.N + TB - 1) / TB, nl);
-    const uint64_t bytes = (uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8;   // digits + 2 key comps + 2 outputs
-    int slot;
-    c.prof_begin("ks_inner", s, bytes, slot);
-    ks_inner_kernel<<<grid, TB, 0, s>>>(ext, dnum, nl, g, key, key_nl, kl, em, acc, c.N, c.logN, c.d_mod);
-    c.prof_end(slot, s);
-    c.st_launch++; c.st_bytes += bytes;
-}
-
 void k_moddown_finish(encf_ctx& c, const u64* b, const u64* y, const u64* add0, u64* out, int level, const ModDownTab& t,
                       cudaStream_t s) {
     size_t total = (size_t)level * c.N;
@@ -758,10 +666,9 @@ __global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int 
             mac128(a1, x.x, k1.x);
             mac128(b1, x.y, k1.y);
         }
-        *(ulonglong2*)(acc + (size_t)e * N + k) =
-            make_ulonglong2(barrett128(a0, mc.q, mc.rhi, mc.rlo), barrett128(b0, mc.q, mc.rhi, mc.rlo));
-        *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) =
-            make_ulonglong2(barrett128(a1, mc.q, mc.rhi, mc.rlo), barrett128(b1, mc.q, mc.rhi, mc.rlo));
+        // keys are stored in Montgomery form (k R mod q, R = 2^64): one REDC returns sum_j x_j k_j mod q
+        *(ulonglong2*)(acc + (size_t)e * N + k) = make_ulonglong2(redc128(a0, mc.q, mc.qinv), redc128(b0, mc.q, mc.qinv));
+        *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(a1, mc.q, mc.qinv), redc128(b1, mc.q, mc.qinv));
     }
 }
 
@@ -833,7 +740,7 @@ __global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__
 #pragma unroll
             for (int i = 0; i < NIN; i++) mac128(acc, v[i], sw[i * nout + t]);
             if (corr) mac128(acc, r, sw[NIN * nout + t]);
-            out[(size_t)op.pos[t] * N + k] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+            out[(size_t)op.pos[t] * N + k] = redc128(acc, mc.q, mc.qinv);   // wfac / corr in Montgomery form
         }
     }
 }
@@ -892,6 +799,8 @@ __global__ void rescale_finish_batch_kernel(CopyBatch In, const u64* corr, CopyB
 
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s) {
+    if ((unsigned __int128)dnum * c.max_mod >= ((unsigned __int128)1 << 64))
+        throw EncfError(ENCF_ERR_ARG, "ks_inner: dnum * q too large for one Montgomery reduction");
     KeyLimb kl;
     LimbMap em;
     em.n = nl;
@@ -923,6 +832,11 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
                    const u64* cfix, const u64* csh) {
     if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
+    {   // Montgomery bound of the lazy sum: sum_i q_i + (n_in + 1) <= 2^64 (then T < q_t 2^64)
+        unsigned __int128 tot = (unsigned __int128)im.n + 1;
+        for (int i = 0; i < im.n; i++) tot += c.mods[im.mod[i]];
+        if (tot >> 64) throw EncfError(ENCF_ERR_ARG, "bconv: input moduli too large for the 128-bit lazy sum");
+    }
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
     size_t smem = (size_t)(im.n + 1) * om.n * sizeof(u64);

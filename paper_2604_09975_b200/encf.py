@@ -96,6 +96,7 @@ _SIG = {
     "encf_import_m2c": [_p, ctypes.POINTER(CT), ctypes.POINTER(PT), ctypes.POINTER(CT), _p],
     "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
+    "encf_profile_peek": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
 }
 for _name, _args in _SIG.items():
     _f = getattr(_lib, _name)
@@ -242,9 +243,12 @@ class Context:
         """which: kernel name to time with CUDA events, "*" for all, None to disable."""
         _chk(_lib.encf_profile_enable(self.h, which.encode() if which else None), "profile_enable")
 
-    def profile_read(self, kernel):
+    def profile_read(self, kernel, keep=False):
+        """(ms, launches, algorithmic bytes) of the recorded launches of `kernel`; keep=True: do not forget them
+        (graph replays re-record the same events)."""
         ms, n, by = _f64(), _u64(), _u64()
-        _chk(_lib.encf_profile_read(self.h, kernel.encode(), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by)), "profile_read")
+        f = _lib.encf_profile_peek if keep else _lib.encf_profile_read
+        _chk(f(self.h, kernel.encode(), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by)), "profile_read")
         return ms.value, n.value, by.value
 
     def galois_rot(self, steps):

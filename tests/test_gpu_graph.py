@@ -1,0 +1,77 @@
+"""CUDA-graph execution of the hot path (paper_2604_09975_b200.graphs.GraphedStep, the bench's timed
+path): a captured step replays to the SAME words as the eager calls, and a replay on new inputs equals
+the oracle on those inputs (every limb)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import ckks as O
+from oracle import kernels as K
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2604_09975_b200 import encf as E  # noqa: E402
+from paper_2604_09975_b200.graphs import GraphedStep  # noqa: E402
+from tests.gpu_util import assert_ct_equal, dev_ct, weights_tensor  # noqa: E402
+
+P13 = O.Params("P13")
+
+
+def test_graph_replay_projection_attention_export():
+    ctx = E.Context("P13", 0)
+    m, H, dh, d_in, d_out, L = 16, 4, 8, 64, 96, 6
+    proj = E.ProjPlan(ctx, m, d_in, d_out, N1=8)
+    attn = E.AttnPlan(ctx, m, H, dh, C_qk=16, beta=4)
+    galois = sorted(set(proj.galois()) | set(attn.galois()) | {ctx.galois_conj()})
+    ok = O.Keys(P13, synth.SEED_KEYS, galois=galois, relin=True)
+    gk = ctx.keygen(synth.SEED_KEYS, galois=galois, relin=True)
+    oplan = K.ProjPlan(P13.n, m, d_in, d_out, N1=8)
+    W = synth.bert_weight((d_in, d_out), 91)
+    pts = [O.encode(P13, K.proj_weight_slots(W, oplan, b, p, u, q), float(P13.q[L - 1]), L)
+           for b in range(oplan.B_out) for p in range(oplan.N2) for u in range(oplan.U) for q in range(oplan.N1)]
+    wd = weights_tensor(ctx, pts, L)
+
+    def inputs(seed):
+        X = synth.fixed_point_uniform((m, d_in), seed)
+        xs = [O.encrypt_sk(P13, ok, O.encode(P13, z, 2.0 ** 40, L), synth.seed_enc(u) + seed)
+              for u, z in enumerate(K.proj_inputs(X, oplan))]
+        g = synth.rng(seed + 1)
+        qk = [O.encrypt_sk(P13, ok, O.encode(P13, g.uniform(-1, 1, P13.n), 2.0 ** 40, L), 500 + seed + i) for i in range(4)]
+        return xs, qk
+
+    def step(inp):
+        y = proj.matmul(gk, inp["x"], wd, float(P13.q[L - 1]))
+        S = attn.score(gk, inp["q"], inp["k"])
+        ex = [ctx.export_c2m(c, 2, 7, i) for i, c in enumerate(attn.export_stream(gk, S))]
+        return [(c.data, None) for c in y] + [(a.data, b) for a, b in ex]
+
+    xs0, qk0 = inputs(10)
+    d0 = {"x": [dev_ct(ctx, x) for x in xs0], "q": [dev_ct(ctx, c) for c in qk0[:2]], "k": [dev_ct(ctx, c) for c in qk0[2:]]}
+    eager0 = [(a.clone(), b.clone() if b is not None else None) for a, b in step(d0)]     # warm-up (mask cache)
+    g = GraphedStep(step, d0)
+    out = g()
+    torch.cuda.synchronize()
+    for (a, b), (ea, eb) in zip(out, eager0):
+        assert torch.equal(a, ea)
+        assert (b is None) or torch.equal(b, eb)
+    # new inputs through the static buffers: the replay equals the oracle's projection on them
+    xs1, qk1 = inputs(20)
+    host = {"x": [dev_ct(ctx, x).data.cpu().pin_memory() for x in xs1],
+            "q": [dev_ct(ctx, c).data.cpu().pin_memory() for c in qk1[:2]],
+            "k": [dev_ct(ctx, c).data.cpu().pin_memory() for c in qk1[2:]]}
+    out1 = g(host)
+    torch.cuda.synchronize()
+    ys = K.projection(K.Ev(P13, ok, m), oplan, xs1, lambda b, p, u, q: pts[((b * oplan.N2 + p) * oplan.U + u) * oplan.N1 + q])
+    for b, y in enumerate(ys):
+        got = E.Ciphertext(out1[b][0], 2, L - 1, y.scale, 1)
+        assert_ct_equal(ctx, got, y, "graph-replayed projection y_%d" % b)
+    # and the eager path on the same new inputs gives the same export words
+    d1 = {k: [E.Ciphertext(h.to(ctx.device), 2, L, 2.0 ** 40, 1) for h in v] for k, v in host.items()}
+    eager1 = step(d1)
+    for (a, b), (ea, eb) in zip(out1, eager1):
+        assert torch.equal(a, ea)
+        assert (b is None) or torch.equal(b, eb)

@@ -336,3 +336,38 @@ def test_fused_qk_projection_bit_exact(c13, keys13):
     got = plan.matmul(gk, [dev_ct(c13, x) for x in xs], wd, float(P.q[L - 1]))
     for a, r in zip(got, ref):
         assert_ct_equal(c13, a, r, "fused QK")
+
+
+# ------------------------------------------------------------------ NTT: FP64-pipe path == integer path
+def test_ntt_fp64_path_equals_integer_path(monkeypatch):
+    """The 40-bit limbs of P16 run the NTT on the FP64 pipe (ntt.cu FpOps); the 60-bit ones on the integer
+    Shoup path.  Forcing the integer path everywhere (ENCF_NTT_INT_ONLY) must give the same words, for
+    random limbs, all-(q-1) and all-zero limbs, forward and inverse."""
+    P = P16
+    L = P.L_max
+    mods = list(P.q) + list(P.p)
+    a = rnd(mods, P.N, 5)
+    a[1, :] = mods[1] - 1
+    a[2, :] = 0
+    ctx_fp = E.Context("P16", 0)
+    monkeypatch.setenv("ENCF_NTT_INT_ONLY", "1")
+    ctx_int = E.Context("P16", 0)
+    monkeypatch.delenv("ENCF_NTT_INT_ONLY")
+    nl = L  # ciphertext-basis limbs (q_0..q_23): 23 of them on the FP64 path
+    x = a[:nl]
+    outs = []
+    for ctx in (ctx_fp, ctx_int):
+        t = ctx.pt_from_host(x, 1.0)
+        ctx.to_ntt(t)
+        f = t.data.cpu().numpy().view(np.uint64).reshape(nl, P.N).copy()
+        ctx.from_ntt(t)
+        b = ctx.to_host(t, coeff=False)
+        outs.append((f, b))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], x) and np.array_equal(outs[1][1], x)
+    # inverse of NTT-domain words (canonical) on both paths
+    for ctx in (ctx_fp, ctx_int):
+        t = ctx.pt_from_host(x, 1.0, ntt=1)
+        ctx.from_ntt(t)
+        outs.append(ctx.to_host(t, coeff=False))
+    assert np.array_equal(outs[2], outs[3])
