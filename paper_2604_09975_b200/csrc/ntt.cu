@@ -216,6 +216,9 @@ __device__ __forceinline__ u64 st_raw(double v) { return (u64)__double_as_longlo
 #ifndef NTT_MINB
 #define NTT_MINB 4
 #endif
+// Thread t of the CTA is (line l = t % lines, j = t / lines): a warp's 32 threads cover consecutive COLUMNS,
+// so the round-A register mapping (rows j + TPL k of column l) is read (forward) / written (inverse) straight
+// from/to global memory in coalesced row segments; only the round-B mapping goes through shared memory.
 template <int LT, bool INV, class Ops>
 __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops& ops, const typename Ops::TW* tw2, int mi) {
     using GG = Geo<LT>;
@@ -226,34 +229,48 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
     const int S = 1 << a.s2;
     const int c0 = blockIdx.x * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
-    const int tot = GG::T * lines;
     const int lgl = 31 - __clz(lines);
-    {   // all E loads of a thread in flight before the first use (tot = E * blockDim.x)
-        u64 v[GG::E];
-#pragma unroll
-        for (int it = 0; it < GG::E; it++) {
-            const int e = threadIdx.x + it * blockDim.x;
-            v[it] = g[(i64)(e >> lgl) * S + c0 + (e & (lines - 1))];
-        }
-#pragma unroll
-        for (int it = 0; it < GG::E; it++) {
-            const int e = threadIdx.x + it * blockDim.x;
-            sm[(e & (lines - 1)) * GG::LSP + pad(e >> lgl)] = ld_val(v[it], ops, !INV);
-        }
-    }
-    __syncthreads();
-    const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
+    const int l = threadIdx.x & (lines - 1), j = threadIdx.x >> lgl;
     T* line = sm + l * GG::LSP;
+    u64* gc = g + c0 + l + (i64)j * S;            // row j of column c0 + l
+    const i64 rs = (i64)GG::TPL * S;              // TPL rows
     T x[GG::E];
     if (!INV) {
-        sm_get_a<LT>(line, j, x);
+        {
+            u64 v[GG::E];
+#pragma unroll
+            for (int k = 0; k < GG::E; k++) v[k] = gc[k * rs];
+#pragma unroll
+            for (int k = 0; k < GG::E; k++) x[k] = ld_val(v[k], ops, true);
+        }
         round_a<LT, false>(x, 0, 0, tw2, ops);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
         round_b<LT, false>(x, j, 0, 0, tw2, ops);
         sm_put_b<LT>(line, j, x);
+        __syncthreads();
+        const int tot = GG::T * lines;
+        for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+            const int r = e >> lgl, c = e & (lines - 1);
+            const T v = sm[c * GG::LSP + pad(r)];
+            g[(i64)r * S + c0 + c] = st_raw(v);    // forward: lazy u64 [0, 4q) / raw double bits to phase B
+        }
     } else {
+        {   // all E loads of a thread in flight before the first use (tot = E * blockDim.x)
+            u64 v[GG::E];
+#pragma unroll
+            for (int it = 0; it < GG::E; it++) {
+                const int e = threadIdx.x + it * blockDim.x;
+                v[it] = g[(i64)(e >> lgl) * S + c0 + (e & (lines - 1))];
+            }
+#pragma unroll
+            for (int it = 0; it < GG::E; it++) {
+                const int e = threadIdx.x + it * blockDim.x;
+                sm[(e & (lines - 1)) * GG::LSP + pad(e >> lgl)] = ld_val(v[it], ops, false);
+            }
+        }
+        __syncthreads();
         sm_get_b<LT>(line, j, x);
         round_b<LT, true>(x, j, 0, 0, tw2, ops);
         sm_put_b<LT>(line, j, x);
@@ -263,22 +280,12 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
         if constexpr (std::is_same<T, u64>::value) {
             const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
 #pragma unroll
-            for (int k = 0; k < GG::E; k++) x[k] = mul_shoup(x[k], ni, nip, ops.q);
+            for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], ni, nip, ops.q);
         } else {
             const double ni = a.fpc[4 * mi + 2], niq = a.fpc[4 * mi + 3];
 #pragma unroll
-            for (int k = 0; k < GG::E; k++) x[k] = fp_mulmod(x[k], ni, niq, ops.q);   // |x| < q: canonicalised on store
+            for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_mulmod(x[k], ni, niq, ops.q), ops.q);
         }
-        sm_put_a<LT>(line, j, x);
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
-        const int r = e >> lgl, c = e & (lines - 1);
-        const T v = sm[c * GG::LSP + pad(r)];
-        u64 w;
-        if constexpr (std::is_same<T, u64>::value) w = v;                  // forward: lazy [0, 4q) to phase B
-        else w = INV ? fp_canon(v, ops.q) : st_raw(v);
-        g[(i64)r * S + c0 + c] = w;
     }
 }
 
