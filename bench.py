@@ -37,6 +37,7 @@ PROF_KERNELS = ["diag_mac", "ks_inner", "ntt", "bcast_mac", "add_kernel", "autom
                 "tensor_acc_kernel", "rescale_prep_kernel", "rescale_finish_kernel"]
 L_QKV, L_V_P, L_FF = 8, 5, 3
 C_QK, BETA = 192, 16
+NTT_TRAFFIC = None   # ncu dram__bytes (read + write) per limb transform, filled from profiles/r01_summary.md
 
 
 def parse():
@@ -345,13 +346,21 @@ def run_ours(args):
     mac_ms, mac_n, mac_b = prof["diag_mac"]
     ntt_ms, ntt_n, ntt_bytes = prof["ntt"]
     achieved = (mac_b / mac_n) / ((mac_ms / mac_n) * 1e-3) / 1e9 if mac_n else 0.0
-    # dominant kernel by time: the NTT (IMAD/ALU issue-bound).  Algorithmic work = butterflies
-    # (N/2 log2 N per limb transform); peak from unit counts x clock.
+    # dominant kernel by time: the NTT, bound by arithmetic pipes.  Algorithmic work =
+    # butterflies (N/2 log2 N per limb transform).  Peak for the step's own limb mix, from SASS op counts per
+    # butterfly and the measured unit rates (tools/micro/pipes.cu, profiles/r01_pipes_micro.txt):
+    #   FP64 path (q < 2^41): 8 DFMA/DMUL/DADD per butterfly at 64 lanes/clk/SM  -> 8 butterflies/clk/SM
+    #   integer path (60-bit q): 6.4 half-rate IMAD.WIDE/HI + 10.3 full-rate IMAD-family -> 2.77 butterflies/clk/SM
     limb_ntts = ntt_bytes / (65536 * 8 * 4)                  # the library counts 4 limb-polys of traffic per limb transform
-    bfly = limb_ntts * (65536 // 2) * 16
+    bpl = (65536 // 2) * 16
+    bfly = limb_ntts * bpl
     ntt_achieved = bfly / (ntt_ms * 1e-3) / 1e9 if ntt_ms else 0.0
     sm_mhz = peaks.get("sm_max_mhz", 1965.0)
-    ntt_peak = 148 * 4.0 * sm_mhz * 1e6 / 1e9               # 4 butterflies / clk / SM (fma-pipe bound, 16 IMAD each)
+    n_fp = stats["limb_ntt_fp64"] / args.steps
+    n_all = stats["limb_ntt"] / args.steps
+    rate_fp, rate_int = 148 * 8.0 * sm_mhz * 1e6, 148 * 2.77 * sm_mhz * 1e6          # butterflies / s
+    t_peak = bpl * (n_fp / rate_fp + (n_all - n_fp) / rate_int)
+    ntt_peak = bpl * n_all / t_peak / 1e9 if n_all else 1.0
     ks_total = stats["keyswitch"] / args.steps
     line = {
         "metric": "BERT-base layer CKKS linear latency (ms) & key-switches/s at N=2^16; HBM roofline %",
@@ -385,10 +394,15 @@ def run_ours(args):
         "execution": "CUDA graph of the whole step (captured once in %.2f s), replayed per step" % capture_s,
         "roofline": {"bound": "alu", "kernel": "ntt (ntt_cols_r + ntt_rows_r)", "achieved": round(ntt_achieved, 1),
                      "peak": round(ntt_peak, 1), "unit": "Gbutterfly/s", "frac": round(ntt_achieved / ntt_peak, 4),
-                     "traffic": None, "share_of_step": round(ntt_ms / args.steps / ms_step, 3),
+                     "traffic": NTT_TRAFFIC, "share_of_step": round(ntt_ms / args.steps / ms_step, 3),
+                     "limb_transforms_per_step": {"fp64_path": n_fp, "int_path": n_all - n_fp},
+                     "hbm_floor_frac": round((limb_ntts * 4 * 65536 * 8 / (ntt_ms * 1e-3) / 1e9) / hbm, 4) if ntt_ms else None,
                      "note": "dominant kernel by device time; achieved = NTT butterflies (N/2 log2 N per limb) / CUDA-event time of "
-                             "every transform in the timed steps; peak = 148 SMs x 4 butterflies/clk (64 IMAD lanes/clk/SM / 16 IMAD "
-                             "per 64-bit Shoup butterfly) x sm_max_mhz (DESIGN.md ALU roofline)"},
+                             "every transform in the timed steps (graph event nodes); peak = the step's limb mix at the pipe bound: "
+                             "FP64-path limbs 8 butterflies/clk/SM (8 fp64-pipe ops each), integer-path limbs 2.77/clk/SM "
+                             "(fmaheavy-bound), x 148 SMs x sm_max_mhz (DESIGN.md ALU roofline); hbm_floor_frac = the 4 limb-poly "
+                             "passes per transform against the measured HBM peak; traffic = ncu dram bytes per limb transform "
+                             "(profiles/r01_summary.md)"},
         "roofline_hbm": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": 24.9e9,
                          "note": "the HBM-bound plaintext-diagonal MAC: algorithmic bytes per launch (plaintext stream + bank + "

@@ -75,6 +75,7 @@ typedef struct {
     uint64_t ctmul;          /* ciphertext tensor products */
     uint64_t kernel_launches;
     uint64_t alg_bytes;      /* algorithmic HBM bytes of the launched kernels */
+    uint64_t limb_ntt_fp64;  /* of limb_ntt: transforms of limbs whose modulus runs the FP64-pipe path (q < 2^41) */
 } encf_counters;
 
 /* ------------------------------------------------------------------------------------------ context */

@@ -558,11 +558,11 @@ def score_qk_slots(Qp, plan, l):
     return seg_column_pack(Qp, plan.m, plan.C, l, plan.n)
 
 
-def score(ev, plan, qs, ks, ts=None):
+def score(ev, plan, qs, ks, ts=None, route_hoisted=True):
     """C7.  Per block l: Q bank Psi^{-s} (s < beta), K bank Psi^{j beta}, Psi^{m/2 + j beta} (j < g/2),
     all hoisted from one ModUp each.  Per t = j beta + s < m/2:
       T_t = sum_l q_{-s} (x) (k_{j beta} + i k_{m/2 + j beta})   lazy tensor sum, ONE relin, rescale (G6)
-      route: x <- x + Phi^{stride}(x) for stride = C/2, C/4, ..., H segments  (Phi^{c - (c mod H)}, G7)
+      route: sum_{j < C/H} Phi^{jH}(x)  (Phi^{c - (c mod H)}, G7; hoisted sum R-ROUTE, or the paper's tree)
       S_t = Psi^{s}(route) restricted to segments [0, H)  (align + e_[0,H) mask merged, one rescale)
     Returns [S_0 .. S_{m/2-1}]."""
     m, H, beta, g, N_seg = plan.m, plan.H, plan.beta, plan.g, plan.N_seg
@@ -577,15 +577,27 @@ def score(ev, plan, qs, ks, ts=None):
         j, s = t // beta, t % beta
         pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in range(plan.B)]
         T = ev.rescale(ev.relin(ev.tensor_sum(pairs)))
-        T = route(ev, T, plan.C // H, H, m)
+        T = route(ev, T, plan.C // H, H, m, hoisted=route_hoisted)
         S.append(Psi_hoisted(ev, T, [s], m, N_seg, 0, H)[0])
     return S
 
 
-def route(ev, x, k, H, m):
+def route(ev, x, k, H, m, hoisted=True):
     """Fold segment c onto c mod H: out[h] = sum_{j<k} x[h + jH] (the paper's sum_c Phi^{c - (c mod H)}
-    (x (.) m_c) with the sign of P:397 corrected, G7), as a binary rotate-add: O(log k) single rotations
-    (the m log C term of #rot_S).  Segments >= H hold garbage and are masked by the caller."""
+    (x (.) m_c) with the sign of P:397 corrected, G7).  Segments >= H hold garbage and are masked by the
+    caller.
+    hoisted=True (the build's schedule, DESIGN.md R-ROUTE): the k-1 shifts Phi^{jH} (j = 1..k-1) of the SAME
+    x from ONE hoisted ModUp, kept in the extended basis, summed with P x and ModDown'ed ONCE:
+        out = ModDown(P x + sum_{j=1}^{k-1} rot_ext(x, j H m)).
+    hoisted=False (the paper's schedule): a binary rotate-add, O(log k) sequential single rotations (the
+    m log C term of #rot_S)."""
+    if hoisted:
+        if k == 1:
+            return x
+        acc = ev.lift_ext(x)
+        for r in ev.rot_hoisted_ext(x, [j * H * m for j in range(1, k)]):
+            acc = ev.ext_add(acc, r)
+        return ev.moddown(acc)
     result, offset, cnt, pw = None, 0, 1, x
     kk = k
     while kk:

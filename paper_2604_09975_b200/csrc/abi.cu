@@ -82,13 +82,13 @@ encf_status encf_ctx_destroy(encf_ctx* ctx) { return ctx_destroy_impl(ctx); }
 encf_status encf_stats(encf_ctx* c, encf_counters* o) {
     if (!c || !o) return ENCF_ERR_ARG;
     o->keyswitch = c->st_ks; o->modup = c->st_modup; o->limb_ntt = c->st_ntt; o->ptmul_terms = c->st_ptmul;
-    o->ctmul = c->st_ctmul; o->kernel_launches = c->st_launch; o->alg_bytes = c->st_bytes;
+    o->ctmul = c->st_ctmul; o->kernel_launches = c->st_launch; o->alg_bytes = c->st_bytes; o->limb_ntt_fp64 = c->st_ntt_fp;
     return ENCF_OK;
 }
 
 encf_status encf_stats_reset(encf_ctx* c) {
     if (!c) return ENCF_ERR_ARG;
-    c->st_ks = 0; c->st_modup = 0; c->st_ntt = 0; c->st_ptmul = 0; c->st_ctmul = 0; c->st_launch = 0; c->st_bytes = 0;
+    c->st_ks = 0; c->st_modup = 0; c->st_ntt = 0; c->st_ptmul = 0; c->st_ctmul = 0; c->st_launch = 0; c->st_bytes = 0; c->st_ntt_fp = 0;
     return ENCF_OK;
 }
 

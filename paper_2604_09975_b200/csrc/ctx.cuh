@@ -116,7 +116,7 @@ struct encf_ctx {
     void prof_begin(const char* name, cudaStream_t s, uint64_t bytes, int& slot);
     void prof_end(int slot, cudaStream_t s);
     // statistics
-    std::atomic<uint64_t> st_ks{0}, st_modup{0}, st_ntt{0}, st_ptmul{0}, st_ctmul{0}, st_launch{0}, st_bytes{0};
+    std::atomic<uint64_t> st_ks{0}, st_modup{0}, st_ntt{0}, st_ptmul{0}, st_ctmul{0}, st_launch{0}, st_bytes{0}, st_ntt_fp{0};
 
     int dnum(int level) const { return (level + alpha - 1) / alpha; }
     LimbMap qmap(int level) const {
@@ -183,6 +183,15 @@ struct CopyBatch {
     uint32_t g[CP_BATCH];
 };
 struct KeyLimb { int kl[MAX_LIMBS]; };
+constexpr int RS_TERMS = 32;
+struct RotSumBatch {               // hoisted rotation sums (R-ROUTE): per request r, terms i share ModUp(c1_r)
+    const u64* ext[KS_BATCH];
+    const u64* c0[KS_BATCH];
+    const u64* c1[KS_BATCH];
+    u64* acc[KS_BATCH];
+    const u64* key[RS_TERMS];
+    uint32_t g[RS_TERMS];
+};
 struct SumDev { const u64* ct; const u64* mask; };
 struct BcastArgs {                 // value-kernel broadcast MAC (C8 step 4)
     const u64* src[128];           // src[i] = Phi^{delta}(p), delta = t0 - dmax + i
@@ -230,6 +239,7 @@ void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_s
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
                       const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s,
                       const double* dWim = nullptr, int real_input = 0);
+void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s);
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,

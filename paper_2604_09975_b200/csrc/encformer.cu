@@ -228,48 +228,16 @@ std::vector<uint32_t> attn_galois(Ev& ev, const encf_attn_plan& a) {
     return g;
 }
 
-// out[h] = sum_{j<k} x[h + jH] by binary rotate-add (G7; oracle kernels.route), all xs in lockstep.
+// out[h] = sum_{j<k} x[h + jH] (G7; oracle kernels.route, hoisted): ONE ModUp of x, the k-1 shifts Phi^{jH}
+// as extended-basis inner products summed with P x in one fused launch, ONE ModDown (DESIGN.md R-ROUTE).
 static std::vector<DCt> route_many(Ev& ev, const std::vector<DCt>& xs, int k, int H, int m) {
+    if (k == 1) return xs;
     const int n = (int)xs.size(), L = xs[0].L;
-    std::vector<DCt> result(n), pw = xs;
-    bool have = false;
-    int offset = 0, cnt = 1, kk = k;
-    while (kk) {
-        if (kk & 1) {
-            std::vector<DCt> y;
-            if (offset) {
-                y = ev.alloc_many(n, L);
-                ev.rotate_many(ptrs(pw), std::vector<uint32_t>(n, ev.galois_rot((long)offset * H * m)), y);
-            } else {
-                y = pw;
-            }
-            if (!have) {
-                result = y;
-                have = true;
-            } else {
-                std::vector<std::vector<SumTerm>> t(n);
-                std::vector<double> sc(n);
-                for (int i = 0; i < n; i++) { check_scale(result[i].scale, y[i].scale); t[i] = {{result[i].d, nullptr}, {y[i].d, nullptr}}; sc[i] = y[i].scale; }
-                std::vector<DCt> r2 = ev.alloc_many(n, L);
-                ev.sum_many(t, L, 2, r2, sc);
-                result = r2;
-            }
-            offset += cnt;
-        }
-        kk >>= 1;
-        if (kk) {
-            std::vector<DCt> rt = ev.alloc_many(n, L);
-            ev.rotate_many(ptrs(pw), std::vector<uint32_t>(n, ev.galois_rot((long)cnt * H * m)), rt);
-            std::vector<std::vector<SumTerm>> t(n);
-            std::vector<double> sc(n);
-            for (int i = 0; i < n; i++) { t[i] = {{pw[i].d, nullptr}, {rt[i].d, nullptr}}; sc[i] = pw[i].scale; }
-            std::vector<DCt> npw = ev.alloc_many(n, L);
-            ev.sum_many(t, L, 2, npw, sc);
-            pw = npw;
-            cnt *= 2;
-        }
-    }
-    return result;
+    std::vector<uint32_t> gs;
+    for (int j = 1; j < k; j++) gs.push_back(ev.galois_rot((long)j * H * m));
+    std::vector<DCt> out = ev.alloc_many(n, L);
+    ev.rotsum_many(ptrs(xs), gs, out);
+    return out;
 }
 
 // ====================================================================================== score (C7)

@@ -559,6 +559,38 @@ void Ev::rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<u
     }
 }
 
+void Ev::rotsum_many(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L, dn = c.dnum(L);
+    std::vector<const u64*> c1;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rotsum_many: mixed levels");
+        check_scale(ins[i]->scale, ins[0]->scale);
+        c1.push_back(ins[i]->comp(1, N));
+    }
+    for (uint32_t g : gs) if (g == 1u) throw EncfError(ENCF_ERR_ARG, "rotsum_many: identity rotation");
+    if ((int)gs.size() > RS_TERMS) throw EncfError(ENCF_ERR_ARG, "rotsum_many: more than RS_TERMS shifts");
+    u64* ext = modup_many(c1, {}, L);
+    std::vector<DCt> acc = alloc_many_ext(n, L);
+    for (int i = 0; i < n; i++) acc[i].scale = ins[i]->scale;
+    const int key_nl = keys->max_level + c.K;
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        RotSumBatch B;
+        for (int i = 0; i < cnt; i++) {
+            B.ext[i] = ext + ext_stride(L) * (r0 + i);
+            B.c0[i] = ins[r0 + i]->comp(0, N);
+            B.c1[i] = ins[r0 + i]->comp(1, N);
+            B.acc[i] = acc[r0 + i].d;
+        }
+        for (size_t t = 0; t < gs.size(); t++) { B.key[t] = key_for(gs[t], L); B.g[t] = gs[t]; }
+        k_ks_rotsum(c, B, cnt, (int)gs.size(), dn, L, key_nl, s);
+    }
+    c.st_ks += (uint64_t)n * gs.size();
+    moddown_many(acc, outs);
+}
+
 void Ev::lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;

@@ -91,6 +91,8 @@ struct Ev {
     void moddown_many(const std::vector<DCt>& ins_ext, std::vector<DCt>& outs);           // ins contiguous (alloc_many_ext)
     void rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs_ext);
     void lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs_ext);       // P * ct over Q_L u P
+    // outs[i] = ModDown(P x_i + sum_{g in gs} rot_ext(x_i, g)): one hoisted ModUp + one ModDown per input (R-ROUTE)
+    void rotsum_many(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs);
 
     // masks
     const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level, int ext = 0);

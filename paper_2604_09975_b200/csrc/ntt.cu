@@ -472,6 +472,11 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     launch_rows<false>(c.s2, R.grid, B.threads, B.smem, s, a, B.lines, R.lgc);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
+    {
+        int nfp = 0;
+        for (int i = 0; i < b.map.n; i++) nfp += (int)((c.fpmask >> b.map.mod[i]) & 1ull);
+        c.st_ntt_fp += (uint64_t)b.npolys * nfp;
+    }
     c.st_launch += 2;
     c.st_bytes += (uint64_t)b.npolys * b.map.n * c.N * 8 * 4;
     CUDA_TRY(cudaGetLastError());
@@ -488,6 +493,11 @@ void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
     launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
+    {
+        int nfp = 0;
+        for (int i = 0; i < b.map.n; i++) nfp += (int)((c.fpmask >> b.map.mod[i]) & 1ull);
+        c.st_ntt_fp += (uint64_t)b.npolys * nfp;
+    }
     c.st_launch += 2;
     c.st_bytes += (uint64_t)b.npolys * b.map.n * c.N * 8 * 4;
     CUDA_TRY(cudaGetLastError());

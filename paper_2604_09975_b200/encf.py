@@ -35,7 +35,8 @@ class Params(ctypes.Structure):
 
 
 class Counters(ctypes.Structure):
-    _fields_ = [(n, _u64) for n in ("keyswitch", "modup", "limb_ntt", "ptmul_terms", "ctmul", "kernel_launches", "alg_bytes")]
+    _fields_ = [(n, _u64) for n in ("keyswitch", "modup", "limb_ntt", "ptmul_terms", "ctmul", "kernel_launches", "alg_bytes",
+                                       "limb_ntt_fp64")]
 
 
 class MaskDesc(ctypes.Structure):

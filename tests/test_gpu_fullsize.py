@@ -105,10 +105,8 @@ def test_score_config4_sampled_t_bit_exact(ctx):
         s = t % oplan.beta
         if s:
             steps |= {s, s - M}
-    k = 1
-    while k < oplan.C // H:
+    for k in range(1, oplan.C // H):    # routing shifts Phi^{kH} (hoisted sum, DESIGN.md R-ROUTE)
         steps.add(k * H * M)
-        k *= 2
     og = sorted({O.galois_rot(P, r) for r in steps if r % P.n})
     okeys = O.Keys(P, synth.SEED_KEYS, galois=og, relin=True, max_level=L)
     gkeys = ctx.keygen(synth.SEED_KEYS, galois=plan.galois(), relin=True, max_level=L)

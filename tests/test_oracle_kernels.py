@@ -257,10 +257,23 @@ def test_score_counts_table2():
     plan = K.ScorePlan(16384, 128, 12, 64, C_qk=120, beta=16)
     assert plan.B == 7 and plan.g == 8
     ev = K.CountEv(16384)
-    S = K.score(ev, plan, [K.FakeCt(7)] * 7, [K.FakeCt(7)] * 7)
+    S = K.score(ev, plan, [K.FakeCt(7)] * 7, [K.FakeCt(7)] * 7, route_hoisted=False)   # the paper's routing tree
     K.score_export(ev, plan, S)
     assert ev.ledger["ctmul"] == 448
     assert 0.8 * 630 <= ev.ledger["rot"] <= 1.2 * 630
+
+
+def test_score_counts_hoisted_route():
+    """The build's routing (R-ROUTE): per t, C/H - 1 = 9 hoisted shifts from ONE ModUp and ONE ModDown
+    instead of the tree's 4 sequential key switches (each with its own ModUp and ModDown)."""
+    plan = K.ScorePlan(16384, 128, 12, 64, C_qk=120, beta=16)
+    tree, hoist = K.CountEv(16384), K.CountEv(16384)
+    K.score(tree, plan, [K.FakeCt(7)] * 7, [K.FakeCt(7)] * 7, route_hoisted=False)
+    K.score(hoist, plan, [K.FakeCt(7)] * 7, [K.FakeCt(7)] * 7)
+    k = plan.C // plan.H                      # 10 channel groups -> tree: 10 = 1010b -> 3 doublings + 1 offset
+    assert hoist.ledger["ctmul"] == tree.ledger["ctmul"] == 448
+    assert hoist.ledger["rot"] - tree.ledger["rot"] == (plan.m // 2) * ((k - 1) - 4)
+    assert hoist.ledger["moddown"] - tree.ledger["moddown"] == plan.m // 2
 
 
 # ------------------------------------------------------------------ conversions (Alg 3 + Alg 4, App. C local maps)
