@@ -632,7 +632,7 @@ void k_decode_limb0(encf_ctx& c, const u64* coeff0, double scale, double* re, do
 // per-ciphertext launch sequence).  Request tables travel by value as kernel parameters.
 namespace {
 
-__global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
+__global__ void __launch_bounds__(TB, 4) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
                                                             LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
     // Two coefficients (k, k+1), k even, per thread: the Galois gather maps them to the aligned pair
     // {s, s^1} (brv flips the low bit), so every operand moves with 128-bit loads.
@@ -672,6 +672,82 @@ __global__ void __launch_bounds__(TB) ks_inner_batch_kernel(KsInnerBatch B, int 
     }
 }
 
+// Hoisted rotation SUM (DESIGN.md R-ROUTE) without ModDown, for request r = blockIdx.x (fastest, so the CTAs
+// running together share each key tile through L2), coefficient pair tile blockIdx.y, extended limb e = blockIdx.z:
+//   acc_0 = sum_i sum_j sigma_{g_i}(ext_j) key_i[j][0] + P (c0 + sum_i sigma_{g_i}(c0))   (P term on q-limbs only)
+//   acc_1 = sum_i sum_j sigma_{g_i}(ext_j) key_i[j][1] + P c1
+// i.e. P x + sum_i rot_ext(x, g_i) over Q_L u P (oracle kernels.route, hoisted).  Keys are in Montgomery form;
+// products are accumulated in 128 bits and REDC'ed every <= 8 products (8 q < 2^64).
+__global__ void __launch_bounds__(TB) ks_rotsum_kernel(RotSumBatch B, int nterms, int dnum, int nl, int L, int key_nl,
+                                                       KeyLimb klm, LimbMap em, int N, int logN,
+                                                       const ModConst* __restrict__ mod, const u64* __restrict__ pl,
+                                                       const u64* __restrict__ pl_sh) {
+    const int r = blockIdx.x, e = blockIdx.z;
+    const int kp = blockIdx.y * blockDim.x + threadIdx.x;
+    if (2 * kp >= N) return;
+    const int k = 2 * kp;
+    const ModConst mc = mod[em.mod[e]];
+    const u64 q = mc.q;
+    const int kle = klm.kl[e];
+    const u64* __restrict__ ext = B.ext[r];
+    const u64* __restrict__ c0 = B.c0[r];
+    const bool qlimb = e < L;
+    const uint32_t mask2n = 2 * N - 1;
+    u64 s00 = 0, s01 = 0, s10 = 0, s11 = 0;
+    U128 a0{0, 0}, b0{0, 0}, a1{0, 0}, b1{0, 0};
+    int cnt = 0;
+    u64 cs0 = 0, cs1 = 0;
+    if (qlimb) {
+        const ulonglong2 v = __ldg((const ulonglong2*)(c0 + (size_t)e * N + k));
+        cs0 = v.x; cs1 = v.y;
+    }
+    for (int i = 0; i < nterms; i++) {
+        const uint32_t g = B.g[i];
+        const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+        const int src = brv((int)((e2 - 1) >> 1), logN);
+        const int base = src & ~1, swap = src & 1;
+        const u64* key = B.key[i];
+        for (int j = 0; j < dnum; j++) {
+            if (cnt + 1 > 8) {
+                s00 = add_mod(s00, redc128(a0, q, mc.qinv), q); s01 = add_mod(s01, redc128(b0, q, mc.qinv), q);
+                s10 = add_mod(s10, redc128(a1, q, mc.qinv), q); s11 = add_mod(s11, redc128(b1, q, mc.qinv), q);
+                a0 = b0 = a1 = b1 = U128{0, 0};
+                cnt = 0;
+            }
+            ulonglong2 x = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base));
+            if (swap) { u64 t = x.x; x.x = x.y; x.y = t; }
+            const u64* kj = key + (size_t)j * 2 * key_nl * N;
+            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)kle * N + k));
+            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + k));
+            mac128(a0, x.x, k0.x);
+            mac128(b0, x.y, k0.y);
+            mac128(a1, x.x, k1.x);
+            mac128(b1, x.y, k1.y);
+            cnt++;
+        }
+        if (qlimb) {
+            ulonglong2 y = __ldg((const ulonglong2*)(c0 + (size_t)e * N + base));
+            if (swap) { u64 t = y.x; y.x = y.y; y.y = t; }
+            cs0 = add_mod(cs0, y.x, q);
+            cs1 = add_mod(cs1, y.y, q);
+        }
+    }
+    s00 = add_mod(s00, redc128(a0, q, mc.qinv), q); s01 = add_mod(s01, redc128(b0, q, mc.qinv), q);
+    s10 = add_mod(s10, redc128(a1, q, mc.qinv), q); s11 = add_mod(s11, redc128(b1, q, mc.qinv), q);
+    if (qlimb) {
+        const u64 p = pl[e], psh = pl_sh[e];
+        const ulonglong2 v1 = __ldg((const ulonglong2*)(B.c1[r] + (size_t)e * N + k));
+        s00 = add_mod(s00, mul_shoup(cs0, p, psh, q), q);
+        s01 = add_mod(s01, mul_shoup(cs1, p, psh, q), q);
+        s10 = add_mod(s10, mul_shoup(v1.x, p, psh, q), q);
+        s11 = add_mod(s11, mul_shoup(v1.y, p, psh, q), q);
+    }
+    u64* acc = B.acc[r];
+    *(ulonglong2*)(acc + (size_t)e * N + k) = make_ulonglong2(s00, s01);
+    *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) = make_ulonglong2(s10, s11);
+}
+
 // out_c = (b_c - y_c) P^{-1} + add_c for request r = blockIdx.z / 2, component c = blockIdx.z % 2.
 // b: acc base [r][2][nl][N]; y: [r][2][L][N].
 __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u64* __restrict__ y, OutBatch O, int level,
@@ -699,48 +775,57 @@ __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u
 // correction -r Q' is folded into the 128-bit accumulator (corr_t = t - Q' mod t).  Templated on the input
 // count so no predicated-off multiply is issued.
 template <int NIN>
-__global__ void __launch_bounds__(TB) bconv_batch_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
-                                                         const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
-                                                         const u64* __restrict__ wfac, LimbMap om, OutPos op,
-                                                         u64* __restrict__ out, i64 out_stride, int N,
-                                                         const ModConst* __restrict__ mod, const u64* __restrict__ corr,
-                                                         const u64* __restrict__ cfix, const u64* __restrict__ csh) {
-    extern __shared__ u64 sw[];   // [NIN][nout] wfac, then [nout] corr
+__global__ void __launch_bounds__(TB, 4) bconv_batch_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
+                                                            const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
+                                                            const u64* __restrict__ wfac, LimbMap om, OutPos op,
+                                                            u64* __restrict__ out, i64 out_stride, int N,
+                                                            const ModConst* __restrict__ mod, const u64* __restrict__ corr,
+                                                            const u64* __restrict__ cfix, const u64* __restrict__ csh) {
+    // shared: [NIN][nout] wfac | [nout] corr | [nout] q_t | [nout] qinv_t | [NIN] q_i | vf | vfs | cfix | shift | [nout] pos
+    // (uniform constants live in shared memory, not in registers: 4 CTAs/SM instead of 2)
+    extern __shared__ u64 sw[];
     const int nout = om.n;
+    u64* s_corr = sw + NIN * nout;
+    u64* s_q = s_corr + nout;
+    u64* s_qi = s_q + nout;
+    u64* s_in = s_qi + nout;
+    u64* s_pos = s_in + 5 * NIN;
     for (int i = threadIdx.x; i < NIN * nout; i += blockDim.x) sw[i] = wfac[i];
-    if (corr)
-        for (int i = threadIdx.x; i < nout; i += blockDim.x) sw[NIN * nout + i] = corr[i];
+    for (int t = threadIdx.x; t < nout; t += blockDim.x) s_pos[t] = (u64)op.pos[t] * (u64)N;
+    for (int t = threadIdx.x; t < nout; t += blockDim.x) {
+        s_corr[t] = corr ? corr[t] : 0;
+        s_q[t] = mod[om.mod[t]].q;
+        s_qi[t] = mod[om.mod[t]].qinv;
+    }
+    for (int i = threadIdx.x; i < NIN; i += blockDim.x) {
+        s_in[i] = mod[im.mod[i]].q;
+        s_in[NIN + i] = vfac[i];
+        s_in[2 * NIN + i] = vfac_sh[i];
+        s_in[3 * NIN + i] = corr ? cfix[i] : 0;
+        s_in[4 * NIN + i] = corr ? csh[i] : 0;
+    }
     __syncthreads();
     in += (size_t)blockIdx.y * in_stride;
     out += (size_t)blockIdx.y * out_stride;
-    u64 qin[NIN], vf[NIN], vfs[NIN], cf[NIN];
-    int sh[NIN];
-#pragma unroll
-    for (int i = 0; i < NIN; i++) {
-        qin[i] = mod[im.mod[i]].q;
-        vf[i] = vfac[i];
-        vfs[i] = vfac_sh[i];
-        cf[i] = corr ? cfix[i] : 0;
-        sh[i] = corr ? (int)csh[i] : 0;
-    }
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
         u64 v[NIN];
 #pragma unroll
-        for (int i = 0; i < NIN; i++) v[i] = mul_shoup(in[(size_t)i * N + k], vf[i], vfs[i], qin[i]);
+        for (int i = 0; i < NIN; i++) v[i] = __ldg(in + (size_t)i * N + k);
+#pragma unroll
+        for (int i = 0; i < NIN; i++) v[i] = mul_shoup(v[i], s_in[NIN + i], s_in[2 * NIN + i], s_in[i]);
         u64 r = 0;
         if (corr) {
             u64 fsum = 0;
 #pragma unroll
-            for (int i = 0; i < NIN; i++) fsum += umulhi(v[i] << sh[i], cf[i]);
+            for (int i = 0; i < NIN; i++) fsum += umulhi(v[i] << (int)s_in[4 * NIN + i], s_in[3 * NIN + i]);
             r = (fsum + (1ull << 58)) >> 59;
         }
         for (int t = 0; t < nout; t++) {
-            const ModConst mc = mod[om.mod[t]];
             U128 acc{0, 0};
 #pragma unroll
             for (int i = 0; i < NIN; i++) mac128(acc, v[i], sw[i * nout + t]);
-            if (corr) mac128(acc, r, sw[NIN * nout + t]);
-            out[(size_t)op.pos[t] * N + k] = redc128(acc, mc.q, mc.qinv);   // wfac / corr in Montgomery form
+            if (corr) mac128(acc, r, s_corr[t]);
+            out[s_pos[t] + k] = redc128(acc, s_q[t], s_qi[t]);   // wfac / corr in Montgomery form
         }
     }
 }
@@ -819,6 +904,23 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
     CUDA_TRY(cudaGetLastError());
 }
 
+void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s) {
+    if (nterms > RS_TERMS) throw EncfError(ENCF_ERR_ARG, "rotation sum: too many terms");
+    const int nl = L + c.K;
+    KeyLimb kl;
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    const LimbMap em = c.extmap(L);
+    dim3 grid(nreq, (c.N / 2 + TB - 1) / TB, nl);
+    const uint64_t bytes = (uint64_t)nterms * dnum * 2 * nl * c.N * 8 + (uint64_t)nreq * (dnum * nl + 2 * L + 2 * nl) * c.N * 8;
+    int slot;
+    c.prof_begin("ks_rotsum", s, bytes, slot);
+    ks_rotsum_kernel<<<grid, TB, 0, s>>>(B, nterms, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod, c.moddown[L].d_pl,
+                                         c.moddown[L].d_pl_sh);
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes;
+    CUDA_TRY(cudaGetLastError());
+}
+
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
                             const ModDownTab& t, cudaStream_t s) {
     dim3 grid(nblocks((size_t)level * c.N, TB, 256), 1, 2 * nreq);
@@ -839,7 +941,7 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
     }
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
-    size_t smem = (size_t)(im.n + 1) * om.n * sizeof(u64);
+    size_t smem = ((size_t)im.n * om.n + 4 * om.n + 5 * im.n) * sizeof(u64);
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
     switch (im.n) {
