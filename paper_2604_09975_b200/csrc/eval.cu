@@ -104,8 +104,16 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
                       pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh);                        // rounded: y = centred [b]_P
-        ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
-        k_moddown_finish_batch(c, acc, y, O, n, L, nl, md, s);
+        std::vector<const u64*> esrc(2 * n), eadd(2 * n);
+        std::vector<u64*> eout(2 * n);
+        for (int i = 0; i < n; i++)
+            for (int cc = 0; cc < 2; cc++) {
+                esrc[2 * i + cc] = acc + ((size_t)i * 2 + cc) * nl * N;
+                eout[2 * i + cc] = O.out[i][cc];
+                eadd[2 * i + cc] = O.add[i][cc];
+            }
+        NttEpilogue E{upload(esrc), upload(eout), upload(eadd), md.d_pinv, md.d_pinv_sh};
+        ntt_forward_epi(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, &E, s);   // + (b - y) P^{-1} (+ add) fused
         c.st_ks += n;
     }
 }
@@ -240,13 +248,10 @@ void Ev::rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs
     }
     ntt_inverse(c, PolyBatch{last, (i64)N, P, lm}, s);
     k_rescale_prep_batch(c, last, corr, L, P, s);
-    ntt_forward(c, PolyBatch{corr, (i64)(L - 1) * N, P, c.qmap(L - 1)}, s);
-    for (int p0 = 0; p0 < P; p0 += CP_BATCH) {
-        int cnt = std::min(CP_BATCH, P - p0);
-        CopyBatch ci, co;
-        for (int i = 0; i < cnt; i++) { ci.src[i] = in_p[p0 + i]; co.src[i] = out_p[p0 + i]; ci.g[i] = co.g[i] = 1u; }
-        k_rescale_finish_batch(c, ci, corr + (size_t)p0 * (L - 1) * N, co, L, cnt, s);
-    }
+    std::vector<const u64*> eadd(P, nullptr);
+    const RescaleTab& rt = c.rescale[L];
+    NttEpilogue E{upload(in_p), upload(out_p), upload(eadd), rt.d_inv, rt.d_inv_sh};
+    ntt_forward_epi(c, PolyBatch{corr, (i64)(L - 1) * N, P, c.qmap(L - 1)}, &E, s);   // (c_i - corr_i) q_L^{-1} fused
 }
 
 // outs[o] = sum of terms[o] (each ct times an optional mask), all at level L with ncomp components.
@@ -471,22 +476,18 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
     u64* y = sc.get((size_t)n * 2 * (L - 1) * N);
     k_bconv_batch(c, x + (size_t)(L - 1) * N, (i64)nl * N, bm, t.d_vfac, t.d_vfac_sh, t.d_wfac, qm, y, (i64)(L - 1) * N,
                   pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh);
-    ntt_forward(c, PolyBatch{y, (i64)(L - 1) * N, 2 * n, qm}, s);
-    ModDownTab ft{};
-    ft.d_pinv = t.d_inv;
-    ft.d_pinv_sh = t.d_inv_sh;
-    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
-        const int cnt = std::min(KS_BATCH, n - r0);
-        OutBatch O;
-        for (int i = 0; i < cnt; i++) {
-            DCt& o = outs[r0 + i];
-            o.L = L - 1; o.ncomp = 2; o.scale = ins[r0 + i].scale / (double)c.mods[L - 1]; o.cstride = 0;
-            O.out[i][0] = o.comp(0, N); O.out[i][1] = o.comp(1, N);
-            O.add[i][0] = nullptr; O.add[i][1] = nullptr;
+    std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
+    std::vector<u64*> eout(2 * n);
+    for (int i = 0; i < n; i++) {
+        DCt& o = outs[i];
+        o.L = L - 1; o.ncomp = 2; o.scale = ins[i].scale / (double)c.mods[L - 1]; o.cstride = 0;
+        for (int cc = 0; cc < 2; cc++) {
+            esrc[2 * i + cc] = x + w * i + (size_t)cc * nl * N;
+            eout[2 * i + cc] = o.comp(cc, N);
         }
-        k_moddown_finish_batch(c, x + w * r0, y + (size_t)2 * (L - 1) * N * r0, O, cnt, L - 1, nl, ft, s);
     }
-    c.st_ks += 0;
+    NttEpilogue E{upload(esrc), upload(eout), upload(eadd), t.d_inv, t.d_inv_sh};
+    ntt_forward_epi(c, PolyBatch{y, (i64)(L - 1) * N, 2 * n, qm}, &E, s);   // (x - y) (P q_{L-1})^{-1} fused
 }
 
 // ModDown of extended ciphertexts (rounded, R-MODDOWN), no rescale.
@@ -508,18 +509,18 @@ void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     u64* y = sc.get((size_t)n * 2 * L * N);
     k_bconv_batch(c, x + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N, pos.data(), 2 * n, s,
                   md.d_pmod, md.d_cfix, md.d_csh);
-    ntt_forward(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, s);
-    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
-        const int cnt = std::min(KS_BATCH, n - r0);
-        OutBatch O;
-        for (int i = 0; i < cnt; i++) {
-            DCt& o = outs[r0 + i];
-            o.L = L; o.ncomp = 2; o.scale = ins[r0 + i].scale; o.cstride = 0;
-            O.out[i][0] = o.comp(0, N); O.out[i][1] = o.comp(1, N);
-            O.add[i][0] = nullptr; O.add[i][1] = nullptr;
+    std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
+    std::vector<u64*> eout(2 * n);
+    for (int i = 0; i < n; i++) {
+        DCt& o = outs[i];
+        o.L = L; o.ncomp = 2; o.scale = ins[i].scale; o.cstride = 0;
+        for (int cc = 0; cc < 2; cc++) {
+            esrc[2 * i + cc] = x + w * i + (size_t)cc * nl * N;
+            eout[2 * i + cc] = o.comp(cc, N);
         }
-        k_moddown_finish_batch(c, x + w * r0, y + (size_t)2 * L * N * r0, O, cnt, L, nl, md, s);
     }
+    NttEpilogue E{upload(esrc), upload(eout), upload(eadd), md.d_pinv, md.d_pinv_sh};
+    ntt_forward_epi(c, PolyBatch{y, (i64)L * N, 2 * n, qm}, &E, s);   // (x - y) P^{-1} fused
 }
 
 // Single (non-hoisted) key switches without ModDown: (P sigma_g(c0) + b0, b1) over Q_L u P.

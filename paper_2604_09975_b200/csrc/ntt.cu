@@ -28,6 +28,13 @@ struct NttArgs {
     const double2* twf;      // FP64 path: {w, w/q}: [mods][N]
     const double* fpc;       // FP64 path: [mods][4] = {q, 1/q, N^-1, N^-1/q}
     u64 fpmask;              // modulus ids on the FP64 path
+    // optional forward epilogue (ModDown / rescale finish fused into the last phase): for polynomial p, limb i,
+    // instead of the transform y: out_p[i] = (src_p[i] - y) * f_i (+ add_p[i]) mod q_i   (device tables)
+    const u64* const* epi_src;
+    u64* const* epi_out;
+    const u64* const* epi_add;
+    const u64* epi_f;
+    const u64* epi_fsh;
     const u64* ninv;
     const u64* ninv_sh;
     int N, logN, s1, s2;
@@ -336,16 +343,29 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
         round_b<LT, false>(x, j, a.s1, boff, tw2, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
+        const u64 qi = a.mod[mi].q;
+        const int lgp = 31 - __clz(lines) - lgc;
         for (int e = threadIdx.x; e < tot; e += blockDim.x) {
             const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
-            u64* ge = line_ptr(e >> LT) + (e & (GG::T - 1));
+            u64 w;
             if constexpr (std::is_same<T, u64>::value) {
                 const u64 q = ops.q, two_q = ops.two_q;
-                u64 w = v >= two_q ? v - two_q : v;
-                *ge = w >= q ? w - q : w;
+                w = v >= two_q ? v - two_q : v;
+                w = w >= q ? w - q : w;
             } else {
                 const double q = ops.q, qinv = a.fpc[4 * mi + 1];
-                *ge = fp_canon(fp_center(v, q, qinv), q);
+                w = fp_canon(fp_center(v, q, qinv), q);
+            }
+            const int ll = e >> LT;
+            if (a.epi_out) {
+                const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
+                const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
+                u64 r = mul_shoup(sub_mod(a.epi_src[p][off], w, qi), a.epi_f[limb], a.epi_fsh[limb], qi);
+                const u64* ad = a.epi_add[p];
+                if (ad) r = add_mod(r, ad[off], qi);
+                a.epi_out[p][off] = r;
+            } else {
+                line_ptr(ll)[e & (GG::T - 1)] = w;
             }
         }
     } else {
@@ -452,6 +472,10 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.fpmask = c.fpmask;
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
+    a.epi_src = nullptr;
+    a.epi_out = nullptr;
+    a.epi_add = nullptr;
+    a.epi_f = a.epi_fsh = nullptr;
     a.N = c.N;
     a.logN = c.logN;
     a.s1 = c.s1;
@@ -461,9 +485,14 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
 
 }  // namespace
 
-void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
+void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s) { ntt_forward_epi(c, b, nullptr, s); }
+
+void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cudaStream_t s) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, false);
+    if (epi) {
+        a.epi_src = epi->src; a.epi_out = epi->out; a.epi_add = epi->add; a.epi_f = epi->f; a.epi_fsh = epi->fsh;
+    }
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
