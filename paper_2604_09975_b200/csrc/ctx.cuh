@@ -205,6 +205,10 @@ struct OutPos { int pos[MAX_LIMBS]; };
 
 // ------------------------------------------------------------------------------------ launchers (ntt.cu)
 void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
+// Forward NTT whose last phase writes out_p = (src_p - NTT(y_p)) f (+ add_p) instead of NTT(y_p): the ModDown /
+// rescale finish fused into the transform (device tables: per-polynomial src/out/add pointers, per-limb f + Shoup).
+struct NttEpilogue { const u64* const* src; u64* const* out; const u64* const* add; const u64* f; const u64* fsh; };
+void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cudaStream_t s);
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ launchers (poly.cu)
@@ -240,6 +244,16 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
                       const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s,
                       const double* dWim = nullptr, int real_input = 0);
 void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
+constexpr int PSI_BATCH = 128;
+struct PsiBatch {                  // masked shift Psi^t without ModDown: h (.) rot_ext(x, g0) + u (.) rot_ext(x, g1)
+    const u64* ext[PSI_BATCH];
+    const u64* c0[PSI_BATCH];
+    u64* out[PSI_BATCH];
+    const u64* key[PSI_BATCH][2];
+    const u64* mask[PSI_BATCH][2];
+    uint32_t g[PSI_BATCH][2];
+};
+void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key_nl, cudaStream_t s);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s);
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,

@@ -6,6 +6,7 @@
 // The schedules are exactly those of oracle/kernels.py (readings in DESIGN.md);
 // independent ciphertexts (blocks, t, bank offsets) are processed in lockstep so that every launch
 // covers all of them.  The parity tests compare every limb of every output.
+#include <algorithm>
 #include <cmath>
 #include "encformer.cuh"
 
@@ -128,59 +129,73 @@ void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>&
 void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
               std::vector<std::vector<DCt>>& outs) {
     // t != 0: the two rotations stay in Q_L u P (hoisted, no ModDown), are masked there and divided by
-    // P q_{L-1} at once (lazy ModDown merged with the rescale, R-LAZY); t = 0: x (.) h_0, rescale.
+    // P q_{L-1} at once (lazy ModDown merged with the rescale, R-LAZY).  The two inner products, the c0 lifts
+    // and the masked sum run as ONE fused launch per batch (ks_psi_kernel); t = 0: x (.) h_0, rescale.
     const int n = (int)xs.size();
-    const int L = xs[0]->L;
-    std::vector<std::vector<uint32_t>> gs(n);
+    const int L = xs[0]->L, N = ev.c.N;
     std::vector<std::vector<int>> tt(n);
-    for (int i = 0; i < n; i++)
+    std::vector<const u64*> c1;
+    std::vector<int> rslot(n, -1);
+    for (int i = 0; i < n; i++) {
+        if (xs[i]->L != L || xs[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "psi_many: mixed levels");
+        bool any = false;
         for (int t : ts[i]) {
             int r = ((t % m) + m) % m;
             tt[i].push_back(r);
-            if (r) { gs[i].push_back(ev.galois_rot(r)); gs[i].push_back(ev.galois_rot(r - m)); }
+            any |= r != 0;
         }
-    std::vector<const DCt*> rin;
-    std::vector<std::vector<uint32_t>> rgs;
-    std::vector<int> rslot(n, -1);
-    int nrot = 0;
-    for (int i = 0; i < n; i++)
-        if (!gs[i].empty()) { rslot[i] = (int)rin.size(); rin.push_back(xs[i]); rgs.push_back(gs[i]); nrot += (int)gs[i].size(); }
-    std::vector<DCt> rall = ev.alloc_many_ext(nrot, L);
-    std::vector<std::vector<DCt>> rots(rin.size());
-    int k = 0;
-    for (size_t i = 0; i < rin.size(); i++)
-        for (size_t j2 = 0; j2 < rgs[i].size(); j2++) rots[i].push_back(rall[k++]);
-    ev.hoisted_many_ext(rin, rgs, rots);
+        if (any) { rslot[i] = (int)c1.size(); c1.push_back(xs[i]->comp(1, N)); }
+    }
+    u64* ext = c1.empty() ? nullptr : ev.modup_many(c1, {}, L);
     const double ms = ev.mask_scale(L);
-    std::vector<std::vector<SumTerm>> lazy_terms, plain_terms;
-    std::vector<double> lazy_sc, plain_sc;
+    struct Req { int i, t; };
+    std::vector<Req> lazy;
+    std::vector<std::vector<SumTerm>> plain_terms;
+    std::vector<double> plain_sc;
     std::vector<std::pair<int, int>> where;   // (0 = lazy / 1 = plain, index)
-    for (int i = 0; i < n; i++) {
-        size_t r = 0;
+    for (int i = 0; i < n; i++)
         for (int t : tt[i]) {
             if (t == 0) {
                 plain_terms.push_back({SumTerm{xs[i]->d, ev.mask(m, 0, m, seg0, 1, nseg, L)}});
                 plain_sc.push_back(xs[i]->scale * ms);
                 where.push_back({1, (int)plain_terms.size() - 1});
             } else {
-                const u64* hm = ev.mask_ext(m, 0, m - t, seg0, 1, nseg, L);
-                const u64* um = ev.mask_ext(m, m - t, m, seg0, 1, nseg, L);
-                const std::vector<DCt>& rr = rots[rslot[i]];
-                lazy_terms.push_back({SumTerm{rr[r].d, hm}, SumTerm{rr[r + 1].d, um}});
-                lazy_sc.push_back(xs[i]->scale * ms);
-                where.push_back({0, (int)lazy_terms.size() - 1});
-                r += 2;
+                lazy.push_back(Req{i, t});
+                where.push_back({0, (int)lazy.size() - 1});
             }
         }
+    // lazy requests ordered t-major so that consecutive CTAs (request index fastest) share the two keys in L2
+    std::vector<int> order(lazy.size());
+    for (size_t k = 0; k < order.size(); k++) order[k] = (int)k;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lazy[a].t < lazy[b].t; });
+    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy.size(), L), lo = ev.alloc_many((int)lazy.size(), L - 1);
+    const int key_nl = ev.keys->max_level + ev.c.K, dn = ev.c.dnum(L);
+    for (size_t r0 = 0; r0 < order.size(); r0 += PSI_BATCH) {
+        const int cnt = (int)std::min((size_t)PSI_BATCH, order.size() - r0);
+        PsiBatch B;
+        for (int k = 0; k < cnt; k++) {
+            const Req& q = lazy[order[r0 + k]];
+            DCt& o = ly[order[r0 + k]];
+            o.scale = xs[q.i]->scale * ms;
+            B.ext[k] = ext + ev.ext_stride(L) * rslot[q.i];
+            B.c0[k] = xs[q.i]->comp(0, N);
+            B.out[k] = o.d;
+            B.g[k][0] = ev.galois_rot(q.t);
+            B.g[k][1] = ev.galois_rot(q.t - m);
+            B.key[k][0] = ev.key_for(B.g[k][0], L);
+            B.key[k][1] = ev.key_for(B.g[k][1], L);
+            B.mask[k][0] = ev.mask_ext(m, 0, m - q.t, seg0, 1, nseg, L);
+            B.mask[k][1] = ev.mask_ext(m, m - q.t, m, seg0, 1, nseg, L);
+        }
+        k_ks_psi(ev.c, B, cnt, dn, L, key_nl, ev.s);
+        ev.c.st_ks += 2 * (uint64_t)cnt;      // two key switches whose ModDown is merged into the rescale
     }
-    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy_terms.size(), L), lo = ev.alloc_many((int)lazy_terms.size(), L - 1);
-    ev.sum_many_ext(lazy_terms, L, ly, lazy_sc);
     ev.moddown_rescale_many(ly, lo);
     std::vector<DCt> py = ev.alloc_many((int)plain_terms.size(), L), po = ev.alloc_many((int)plain_terms.size(), L - 1);
     ev.sum_many(plain_terms, L, 2, py, plain_sc);
     ev.rescale_many(ptrs(py), po);
     outs.assign(n, {});
-    k = 0;
+    int k = 0;
     for (int i = 0; i < n; i++)
         for (size_t j2 = 0; j2 < tt[i].size(); j2++, k++)
             outs[i].push_back(where[k].first == 0 ? lo[where[k].second] : po[where[k].second]);
