@@ -37,12 +37,20 @@ def test_shift_definitions_toy():
     assert np.array_equal(K.vec(K.mat(x, 2)), x)
 
 
+def _golden(key):
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "paper_values.json")) as f:
+        return json.load(f)[key]["value"]
+
+
 def test_k_min_paper_table4():
-    # Table 4: Softmax 6, LN1 3, GELU 12, LN2 3 at n = 16384
+    # Table 4: Softmax 6, LN1 3, GELU 12, LN2 3 at n = 16384 (tests/golden/paper_values.json)
     n = 16384
-    assert K.k_min(12 * 128 * 128, n) == 6
-    assert K.k_min(128 * 768, n) == 3
-    assert K.k_min(128 * 3072, n) == 12
+    g = _golden("k_min_minimal_stream")
+    assert K.k_min(12 * 128 * 128, n) == g["softmax"]
+    assert K.k_min(128 * 768, n) == g["ln1"] == g["ln2"]
+    assert K.k_min(128 * 3072, n) == g["gelu"]
     # N_seg=256 at N=2^16, m=128: K_min(S) = 3
     assert K.k_min(12 * 128 * 128, 32768) == 3
 
@@ -247,8 +255,8 @@ def test_value_counts_table2():
     assert plan.B_V == 6
     ev = K.CountEv(16384)
     K.value(ev, plan, [K.FakeCt(4)] * 6, [K.FakeCt(7)] * 6)
-    assert ev.ledger["rot"] == 1524
-    assert ev.ledger["ctmul"] == 384
+    assert ev.ledger["rot"] == _golden("value_rotations_bert_base")
+    assert ev.ledger["ctmul"] == _golden("value_ctmul_bert_base")
 
 
 def test_score_counts_table2():
@@ -259,8 +267,9 @@ def test_score_counts_table2():
     ev = K.CountEv(16384)
     S = K.score(ev, plan, [K.FakeCt(7)] * 7, [K.FakeCt(7)] * 7, route_hoisted=False)   # the paper's routing tree
     K.score_export(ev, plan, S)
-    assert ev.ledger["ctmul"] == 448
-    assert 0.8 * 630 <= ev.ledger["rot"] <= 1.2 * 630
+    assert ev.ledger["ctmul"] == _golden("score_ctmul_bert_base")
+    r = _golden("score_rotations_bert_base")
+    assert 0.8 * r <= ev.ledger["rot"] <= 1.2 * r
 
 
 def test_score_counts_hoisted_route():
@@ -341,3 +350,12 @@ def test_fused_qk_projection(keys13):
     Z = K.seg_column_unpack(dec(P, keys13, y), m, 256, 256, 0)
     assert rel_err(Z.real, X @ WQ) < TOL and rel_err(Z.imag, X @ WK) < TOL
     assert ev.ledger["conj"] == 0
+
+
+def test_conversion_payload_paper_value():
+    """10.49 MB per complex conversion pair (one ciphertext per direction) and 20.97 MB for the real
+    baseline (two per direction) at N = 65536: ct_bytes = 2 * L * N * 8 with L = 5 limbs."""
+    g = _golden("conversion_payload_MB")
+    ct = 2 * 5 * 65536 * 8
+    assert round(2 * ct / 1e6, 2) == g["complex"]
+    assert abs(4 * ct / 1e6 - g["real"]) < 0.01
