@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks"])
+    ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear"])
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
@@ -139,6 +139,8 @@ class Layer:
         n = ctx.n
         self.sc = 2.0 ** 40
         t0 = time.time()
+        if workload == "gpt2-linear":
+            return self._init_gpt2(device, seed_off, t0)
         self.qkv = E.ProjPlan(ctx, M, D, 11 * 256)
         galois = set(self.qkv.galois())
         if workload == "layer":
@@ -176,6 +178,49 @@ class Layer:
             self.host_inputs["f1"] = [self._enc(z, L_FF, 30 + i) for i, z in enumerate(PK.complexified_inputs(X1, M, 256, n))]
             X2 = synth.fixed_point_uniform((M, DFF), synth.seed_data(6) + seed_off, 0.0, 1.0)
             self.host_inputs["f2"] = [self._enc(z, L_FF, 40 + i) for i, z in enumerate(PK.complexified_inputs(X2, M, 256, n))]
+        self.dev_inputs = {k: [self._to_dev(h) for h in v] for k, v in self.host_inputs.items()}
+        self.h2d_bytes = sum(h[0].nbytes for v in self.host_inputs.values() for h in v)
+        self.Lconv = ctx.l_conv()
+        self.mask_seed = synth.seed_mask(0)
+
+    def _init_gpt2(self, device, seed_off, t0):
+        """Config 5 (BASELINE configs[4]): GPT-2 small linear path, m = 256 tokens (N_seg = 128, C = 128):
+        QKV 768 -> 2304 (U = 3, B_out = 18) at L = 8; out-projection on the (decomplexified) attention output
+        O at L = 5 (U = 3); FF1 768 -> 3072 and FF2 3072 -> 768 at L = 3; complexify + C2M export of the LN1
+        (3), GELU (12) and LN2 (3) boundary tensors at L_conv (SURVEY 8d cfg 5; attention itself is the
+        optional part of cfg 5 and is not in this step).  Inputs arriving from the MPC side (O, FF1/FF2
+        activations) are fresh encryptions made before the timed region."""
+        import synth
+        E, PK, ctx, torch = self.E, self.PK, self.ctx, self.torch
+        m, d, dff, n = 256, 768, 3072, ctx.n
+        C = n // m
+        self.m = m
+        self.qkv = E.ProjPlan(ctx, m, d, 3 * d)
+        self.oproj = E.ProjPlan(ctx, m, d, d)
+        self.ff1 = E.ProjPlan(ctx, m, d, dff)
+        self.ff2 = E.ProjPlan(ctx, m, dff, d)
+        galois = set()
+        for pl in (self.qkv, self.oproj, self.ff1, self.ff2):
+            galois |= set(pl.galois())
+        galois.add(ctx.galois_conj())
+        self.keys = ctx.keygen(synth.SEED_KEYS, galois=sorted(galois), relin=True, max_level=L_QKV)
+        self.n_keys = len(galois) + 1
+        Wqkv = np.concatenate([synth.bert_weight((d, d), synth.seed_data(5) + i) for i in range(3)], axis=1)
+        self.w_qkv = self.qkv.encode_weights(Wqkv, L_QKV)
+        self.wsc_qkv = float(ctx.q[L_QKV - 1])
+        self.w_o = self.oproj.encode_weights(synth.bert_weight((d, d), synth.seed_data(5) + 13), 5)
+        self.w_1 = self.ff1.encode_weights(synth.bert_weight((d, dff), synth.seed_data(5) + 14), L_FF)
+        self.w_2 = self.ff2.encode_weights(synth.bert_weight((dff, d), synth.seed_data(5) + 15), L_FF)
+        torch.cuda.synchronize()
+        self.setup_s = time.time() - t0
+        X = synth.fixed_point_uniform((m, d), synth.seed_data(5) + seed_off)
+        Oa = synth.fixed_point_uniform((m, d), synth.seed_data(5) + 100 + seed_off)
+        X1 = synth.fixed_point_uniform((m, d), synth.seed_data(5) + 200 + seed_off)
+        X2 = synth.fixed_point_uniform((m, dff), synth.seed_data(5) + 300 + seed_off, 0.0, 1.0)
+        self.host_inputs = {"x": [self._enc(z, L_QKV, 10 + i) for i, z in enumerate(PK.complexified_inputs(X, m, C, n))],
+                            "o": [self._enc(z, 5, 50 + i) for i, z in enumerate(PK.complexified_inputs(Oa, m, C, n))],
+                            "f1": [self._enc(z, L_FF, 60 + i) for i, z in enumerate(PK.complexified_inputs(X1, m, C, n))],
+                            "f2": [self._enc(z, L_FF, 70 + i) for i, z in enumerate(PK.complexified_inputs(X2, m, C, n))]}
         self.dev_inputs = {k: [self._to_dev(h) for h in v] for k, v in self.host_inputs.items()}
         self.h2d_bytes = sum(h[0].nbytes for v in self.host_inputs.values() for h in v)
         self.Lconv = ctx.l_conv()
@@ -220,6 +265,18 @@ class Layer:
         self._mark("start")
         y = self.qkv.matmul(keys, inp["x"], self.w_qkv, self.wsc_qkv)
         self._mark("qkv")
+        if self.workload == "gpt2-linear":
+            ex = [(c.data, None) for c in y]          # Q, K, V stay encrypted for the (optional) attention
+            yo = self.oproj.matmul(keys, inp["o"], self.w_o, float(ctx.q[4]))
+            ex += self._export(self._complex_pairs(yo), 100)
+            self._mark("out_proj")
+            g1 = self.ff1.matmul(keys, inp["f1"], self.w_1, float(ctx.q[L_FF - 1]))
+            ex += self._export(self._complex_pairs(g1), 200)
+            self._mark("ff1")
+            g2 = self.ff2.matmul(keys, inp["f2"], self.w_2, float(ctx.q[L_FF - 1]))
+            ex += self._export(self._complex_pairs(g2), 300)
+            self._mark("ff2")
+            return ex
         if self.workload == "qkv":
             return [(c.data, None) for c in y]
         nqk = self.nqk
@@ -375,9 +432,10 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded; BERT-init random weights; encrypted U[-1,1] F=13 activations)",
-        "config": {"workload": "bert-base-layer" if args.workload == "layer" else "bert-base-qkv",
-                   "N": 65536, "m": M, "d": D, "H": H, "d_ff": DFF,
-                   "levels": {"qkv": L_QKV, "p_fd": L_V_P, "ff": L_FF, "conv": layer.Lconv},
+        "config": {"workload": {"layer": "bert-base-layer", "qkv": "bert-base-qkv", "gpt2-linear": "gpt2-small-linear-path"}[args.workload],
+                   "N": 65536, "m": getattr(layer, "m", M), "d": D, "H": H, "d_ff": DFF,
+                   "levels": {"qkv": L_QKV, "p_fd": L_V_P, "out_proj": 5 if args.workload == "gpt2-linear" else L_V_P - 2,
+                              "ff": L_FF, "conv": layer.Lconv},
                    "params": "P16 (q0 60b + 23x40b, K=6 x 60b special, alpha=8)",
                    "parallelism": "replicas: one independent layer per GPU" if ws > 1 else "1 GPU",
                    "l2": "no flush: per-step working set (~%d GB of plaintext diagonals) >> 126 MB L2" % round(
@@ -404,7 +462,7 @@ def run_ours(args):
                              "passes per transform against the measured HBM peak; traffic = ncu dram bytes per limb transform "
                              "(profiles/r01_summary.md)"},
         "roofline_hbm": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": 24.9e9,
+                         "frac": round(achieved / hbm, 4), "traffic": 24.9e9 if args.workload in ("layer", "qkv") else None,
                          "note": "the HBM-bound plaintext-diagonal MAC: algorithmic bytes per launch (plaintext stream + bank + "
                                  "accumulators) / CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs (burst copy); traffic = "
                                  "ncu dram read+write bytes of the QKV launch (24.8 GB algorithmic; profiles/r01_summary.md)"},

@@ -165,3 +165,42 @@ def test_value_config4_block0_bit_exact(ctx):
                 s = hh * oplan.seg_stride + u
                 assert np.abs(got[s * M:(s + 1) * M] - ref[h][:, u]).max() / np.abs(ref).max() < TOL, (l, h, u)
     ctx.mask_clear()
+
+
+def test_gpt2_ff2_projection_config5_block0_bit_exact(ctx):
+    """Config 5 (GPT-2 small linear path, m = 256 tokens, N_seg = C = 128): the FF2 projection 3072 -> 768
+    at L = 3 (U = 12 complexified inputs, B_out = 6) exactly as bench.py --workload gpt2-linear launches it;
+    output block 0 computed by the oracle must agree on every limb, every block must decrypt to X W."""
+    L, m, din, dout = 3, 256, 3072, 768
+    X = synth.fixed_point_uniform((m, din), synth.seed_data(5) + 300, 0.0, 1.0)
+    W = synth.bert_weight((din, dout), synth.seed_data(5) + 15)
+    plan = E.ProjPlan(ctx, m, din, dout)
+    oplan = K.ProjPlan(P.n, m, din, dout)
+    assert (plan.C, plan.U, plan.B_out, plan.N1, plan.N2) == (oplan.C, oplan.U, oplan.B_out, oplan.N1, oplan.N2)
+    assert (plan.C, plan.U, plan.B_out) == (128, 12, 6)
+    g_oracle = [O.galois_rot(P, q * m) for q in range(1, oplan.N1)] + \
+               [O.galois_rot(P, p * oplan.N1 * m) for p in range(1, oplan.N2)] + [O.galois_conj(P)]
+    okeys = O.Keys(P, synth.SEED_KEYS, galois=g_oracle, max_level=L)
+    gkeys = ctx.keygen(synth.SEED_KEYS, galois=plan.galois(), max_level=L)
+    xs = [O.encrypt_sk(P, okeys, O.encode(P, z, 2.0 ** 40, L), synth.seed_enc(u)) for u, z in enumerate(K.proj_inputs(X, oplan))]
+    cache = {}
+
+    def w(b, p, u, q):
+        if (b, p, u, q) not in cache:
+            cache[(b, p, u, q)] = O.encode(P, K.proj_weight_slots(W, oplan, b, p, u, q), float(P.q[L - 1]), L)
+        return cache[(b, p, u, q)]
+    ev = K.Ev(P, okeys, m)
+    y0 = K.projection_finalize(ev, oplan, K.projection_partial(ev, oplan, xs, w, 0, oplan.N2)[0])
+    wd = plan.encode_weights(W, L)
+    n0 = oplan.N2 * oplan.U * oplan.N1
+    pts = [w(0, p, u, q) for p in range(oplan.N2) for u in range(oplan.U) for q in range(oplan.N1)]
+    blk = torch.from_numpy(np.ascontiguousarray(np.stack([pt.m for pt in pts])).view(np.int64).reshape(-1).copy()).to(ctx.device)
+    ctx.poly_to_ntt(blk, n0, L)
+    wd[:blk.numel()] = blk
+    ys = plan.matmul(gkeys, [dev_ct(ctx, x) for x in xs], wd, float(P.q[L - 1]))
+    assert_ct_equal(ctx, ys[0], y0, "GPT-2 FF2 y_0 (N=2^16, m=256, L=3)")
+    Y = X @ W
+    for b, y in enumerate(ys):
+        got = K.seg_column_unpack(_dec(okeys, O.Ct(ctx.to_host(y), y.scale)).real, m, 128, dout, b)
+        ref = Y[:, b * 128:(b + 1) * 128]
+        assert np.abs(got - ref).max() / np.abs(Y).max() < TOL, b
