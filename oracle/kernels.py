@@ -616,14 +616,17 @@ def score_export(ev, plan, S):
     """Minimal export stream (A20; t-major order S:181): stream slot (t H + h) m + j
     -> ciphertext floor(./n), slot (. mod n).  S_t is rotated right by its offset o (single KS) and
     masked by the slot range(s) it covers in each ciphertext (straddling pieces split by masks; the
-    tail is zero).  One rescale per output ciphertext.  Returns K_min(S) ciphertexts."""
+    tail is zero).  The rotations are consumed only by these masked sums, so they stay in the extended
+    basis Q_L u P (no ModDown; t with o = 0 enters as P S_t) and every output ciphertext is divided by
+    P q_{L-1} at once (lazy ModDown merged with the rescale, DESIGN.md R-LAZY / R-EXP).  Returns K_min(S)
+    ciphertexts."""
     m, H, n = plan.m, plan.H, plan.n
     seg = H * m
-    outs = [None] * plan.n_out
+    terms = [[] for _ in range(plan.n_out)]
     for t, st in enumerate(S):
         start = t * seg
         o = start % n
-        r = ev.rot(st, -o) if o else st
+        r = ev.rot_ext(st, -o) if o else ev.lift_ext(st)
         k = start // n
         first = min(seg, n - o)
         pieces = [(k, o, o + first)]
@@ -631,9 +634,10 @@ def score_export(ev, plan, S):
             pieces.append((k + 1, 0, seg - first))
         for (ci, a, b) in pieces:
             desc = (0, m, a // m, 1, (b - a) // m)
-            y = ev.ptmul(r, ev.mask(desc, r.L, m))
-            outs[ci] = y if outs[ci] is None else ev.add(outs[ci], y)
-    return [ev.rescale(y) for y in outs]
+            terms[ci].append((r, ev.mask_ext(desc, r.L, m)))
+    L = S[0].L
+    sc = S[0].scale * ev.mask_scale(L)
+    return [ev.moddown_rescale(ev.ext_masked_sum([x for x, _ in tt], [p for _, p in tt], sc)) for tt in terms]
 
 
 def score_reference(Qh, Kh):

@@ -300,34 +300,37 @@ void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, cons
     (void)N;
 }
 
-// Minimal export stream (oracle kernels.score_export).
+// Minimal export stream (oracle kernels.score_export): the offset rotations stay in the extended basis, the
+// masked pieces are summed there, and each output is divided by P q_{L-1} once (R-LAZY / R-EXP).
 void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S, std::vector<DCt>& outs) {
     const int m = a.m, H = a.H, n = a.n;
     const long seg = (long)H * m;
     const int L = S[0].L;
-    std::vector<const DCt*> rin;
+    std::vector<const DCt*> rin, lin;
     std::vector<uint32_t> rg;
-    std::vector<int> ridx(S.size(), -1);
+    std::vector<int> ridx(S.size(), -1), lidx(S.size(), -1);
     for (size_t t = 0; t < S.size(); t++) {
         long o = ((long)t * seg) % n;
         if (o) { ridx[t] = (int)rin.size(); rin.push_back(&S[t]); rg.push_back(ev.galois_rot(-o)); }
+        else { lidx[t] = (int)lin.size(); lin.push_back(&S[t]); }
     }
-    std::vector<DCt> rot = ev.alloc_many((int)rin.size(), L);
-    ev.rotate_many(rin, rg, rot);
+    std::vector<DCt> rot = ev.alloc_many_ext((int)rin.size(), L), lif = ev.alloc_many_ext((int)lin.size(), L);
+    ev.rotate_many_ext(rin, rg, rot);
+    ev.lift_many(lin, lif);
     std::vector<std::vector<SumTerm>> terms(a.n_out);
     for (size_t t = 0; t < S.size(); t++) {
         long start = (long)t * seg;
         long o = start % n;
-        const DCt* r = ridx[t] >= 0 ? &rot[ridx[t]] : &S[t];
+        const DCt* r = ridx[t] >= 0 ? &rot[ridx[t]] : &lif[lidx[t]];
         int k = (int)(start / n);
         long first = std::min(seg, n - o);
-        terms[k].push_back(SumTerm{r->d, ev.mask(m, 0, m, (int)(o / m), 1, (int)(first / m), L)});
-        if (first < seg) terms[k + 1].push_back(SumTerm{r->d, ev.mask(m, 0, m, 0, 1, (int)((seg - first) / m), L)});
+        terms[k].push_back(SumTerm{r->d, ev.mask_ext(m, 0, m, (int)(o / m), 1, (int)(first / m), L)});
+        if (first < seg) terms[k + 1].push_back(SumTerm{r->d, ev.mask_ext(m, 0, m, 0, 1, (int)((seg - first) / m), L)});
     }
-    std::vector<DCt> y = ev.alloc_many(a.n_out, L);
-    ev.sum_many(terms, L, 2, y, std::vector<double>(a.n_out, S[0].scale * ev.mask_scale(L)));
+    std::vector<DCt> y = ev.alloc_many_ext(a.n_out, L);
+    ev.sum_many_ext(terms, L, y, std::vector<double>(a.n_out, S[0].scale * ev.mask_scale(L)));
     outs = ev.alloc_many(a.n_out, L - 1);
-    ev.rescale_many(ptrs(y), outs);
+    ev.moddown_rescale_many(y, outs);
 }
 
 // ====================================================================================== value (C8)

@@ -6,6 +6,7 @@
 //   projection, masked sums (Psi shifts, broadcasts), export masking, and float64 encode/decode.
 // Integer work runs on the IMAD pipe with 64x64->128 products; every kernel is HBM- or IMAD-bound
 // (no dense contraction here: DESIGN.md "Why no tensor cores").
+#include <cstdlib>
 #include "ctx.cuh"
 
 namespace {
@@ -244,26 +245,85 @@ constexpr int MAC_T = 32;      // coefficients per CTA tile
 constexpr int MAC_TPR = 16;    // threads per tile row (2 coefficients each)
 constexpr int MAC_LANES = 16;  // unit lanes per CTA (blockDim = 256)
 
+// Narrow limbs (q < 2^41): both factors split at 20 bits, x = xh 2^20 + xl, and the product formed Karatsuba-
+// style from THREE 32x32->64 products (xh yh, xl yl, (xh+xl)(yh+yl)) accumulated in 64 bits without carries
+// (each < 2^43, 64 terms < 2^49): 3 IMAD.WIDE per product instead of the ~6 half-rate ops + carry chain of a
+// 64x64->128 MAC, so the kernel stays HBM-bound.  The bank tile is pre-split in shared memory.
+__device__ __forceinline__ u64 kara_combine(u64 hh, u64 ll, u64 ss, u64 q, u64 rhi, u64 rlo, u64 t40) {
+    const u64 mid = ss - hh - ll;                         // = sum (xh yl + xl yh) < 2^48
+    U128 acc{ll, 0};
+    mac128(acc, hh, t40);                                 // hh * (2^40 mod q)
+    add128(acc, mid << 20);                               // mid 2^20 < 2^68: split
+    acc.hi += mid >> 44;
+    return barrett128(acc, q, rhi, rlo);
+}
+
+template <bool NARROW>
 __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64* __restrict__ bank, int nbank,
                                                                        const u64* __restrict__ w, int units, i64 wus,
                                                                        u64* __restrict__ acc, i64 accs, int level, int N,
-                                                                       const ModConst* __restrict__ mod) {
-    extern __shared__ ulonglong2 sb2[];   // [nbank][2][MAC_T / 2]
+                                                                       const ModConst* __restrict__ mod, int limb0) {
+    extern __shared__ ulonglong2 sb2[];   // wide: [nbank][2][MAC_T / 2] u64 pairs; narrow: [nbank][2][MAC_T] uint2 {h, l}
     u64* sb = (u64*)sb2;
-    const int limb = blockIdx.y;
+    const int limb = limb0 + blockIdx.y;
     const int k0 = blockIdx.x * MAC_T;
     const ModConst mc = mod[limb];
+    constexpr bool narrow = NARROW;
     const size_t cs = (size_t)level * N;
     const size_t bs = 2 * cs;
+    const int kp = threadIdx.x % MAC_TPR, lane = threadIdx.x / MAC_TPR;
+    const size_t wl = (size_t)limb * N + k0 + 2 * kp;
+    const size_t pstride = (size_t)level * N;
+    if constexpr (narrow) {
+        uint2* sn = (uint2*)sb2;          // [uq][c][kk]
+        for (int i = threadIdx.x; i < nbank * 2 * MAC_T; i += blockDim.x) {
+            int uq = i / (2 * MAC_T), r = i % (2 * MAC_T);
+            int c = r / MAC_T, kk = r % MAC_T;
+            const u64 x = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+            const uint32_t h = (uint32_t)(x >> 20), l = (uint32_t)(x & 0xFFFFF);
+            sn[i] = make_uint2(h, l);
+        }
+        __syncthreads();
+        const u64 t40 = (1ull << 40) % mc.q;
+        for (int u = blockIdx.z * MAC_LANES + lane; u < units; u += gridDim.z * MAC_LANES) {
+            const u64* wu = w + (size_t)u * wus + wl;
+            // [component][coefficient] x {hh, ll, ss}
+            u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
+            for (int uq0 = 0; uq0 < nbank; uq0 += 8) {
+                const int cnt = min(8, nbank - uq0);
+                ulonglong2 x[8];
+#pragma unroll
+                for (int t = 0; t < 8; t++)
+                    if (t < cnt) x[t] = __ldg((const ulonglong2*)(wu + (size_t)(uq0 + t) * pstride));
+#pragma unroll
+                for (int t = 0; t < 8; t++) {
+                    if (t >= cnt) break;
+                    const int uq = uq0 + t;
+                    const uint32_t ah = (uint32_t)(x[t].x >> 20), al = (uint32_t)(x[t].x & 0xFFFFF);
+                    const uint32_t bh = (uint32_t)(x[t].y >> 20), bl = (uint32_t)(x[t].y & 0xFFFFF);
+                    const uint32_t as = ah + al, bsum = bh + bl;
+                    const uint4 pp = *(const uint4*)&sn[(uq * 2 + 0) * MAC_T + 2 * kp];   // {h, l} of k, k+1
+                    const uint4 rr = *(const uint4*)&sn[(uq * 2 + 1) * MAC_T + 2 * kp];
+                    h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
+                    h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
+                    h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
+                    h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
+                }
+            }
+            u64* o = acc + (size_t)u * accs + wl;
+            *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
+                                              kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
+            *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
+                                                     kara_combine(h11, l11, s11, mc.q, mc.rhi, mc.rlo, t40));
+        }
+        return;
+    }
     for (int i = threadIdx.x; i < nbank * 2 * MAC_T; i += blockDim.x) {
         int uq = i / (2 * MAC_T), r = i % (2 * MAC_T);
         int c = r / MAC_T, kk = r % MAC_T;
         sb[i] = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
     }
     __syncthreads();
-    const int kp = threadIdx.x % MAC_TPR, lane = threadIdx.x / MAC_TPR;
-    const size_t wl = (size_t)limb * N + k0 + 2 * kp;
-    const size_t pstride = (size_t)level * N;
     for (int u = blockIdx.z * MAC_LANES + lane; u < units; u += gridDim.z * MAC_LANES) {
         const u64* wu = w + (size_t)u * wus + wl;
         U128 a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};   // [component][coefficient]
@@ -539,23 +599,38 @@ void k_masked_sum(encf_ctx& c, const u64* const* C, const u64* const* M, int nte
 
 void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units, i64 wus, u64* acc, i64 accs, int level,
                 cudaStream_t s) {
-    size_t smem = (size_t)nbank * 2 * MAC_T * sizeof(u64);
+    size_t smem = (size_t)nbank * 2 * MAC_T * sizeof(u64);   // narrow limbs: pre-split {h, l} uint2 per bank word
+    if (nbank > 4096) throw EncfError(ENCF_ERR_PLAN_SHAPE, "diag_mac: more than 4096 bank ciphertexts (64-bit split sums)");
+    static const int allow_narrow = std::getenv("ENCF_MAC_WIDE_ONLY") ? 0 : 1;   // experiment switch: 128-bit path everywhere
     static bool attr_set = false;
     if (!attr_set) {
-        CUDA_TRY(cudaFuncSetAttribute(diag_mac_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(diag_mac_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        CUDA_TRY(cudaFuncSetAttribute(diag_mac_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attr_set = true;
     }
     if (smem > 200 * 1024) throw EncfError(ENCF_ERR_PLAN_SHAPE, "diag_mac: bank too large for shared memory");
     int tiles = c.N / MAC_T;
     int zsplit = 1;
     while ((size_t)tiles * level * zsplit < 148 * 8 && zsplit * MAC_LANES < units) zsplit *= 2;
-    dim3 grid(tiles, level, zsplit);
+    // limbs [0, nw) on the 128-bit path, [nw, level) (q < 2^41) on the 20-bit Karatsuba path when enabled
+    int nw = level;
+    if (allow_narrow) {
+        nw = 0;
+        while (nw < level && c.mods[nw] >= (1ull << 41)) nw++;
+        for (int i = nw; i < level; i++)
+            if (c.mods[i] >= (1ull << 41)) { nw = level; break; }
+    }
     // algorithmic bytes: plaintext stream + bank read once + accumulators written once
     const uint64_t bytes = (uint64_t)units * nbank * level * c.N * 8 + (uint64_t)nbank * 2 * level * c.N * 8 +
                            (uint64_t)units * 2 * level * c.N * 8;
     int slot;
     c.prof_begin("diag_mac", s, bytes, slot);
-    diag_mac_kernel<<<grid, MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs, level, c.N, c.d_mod);
+    if (nw > 0)
+        diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
+                                                                                        level, c.N, c.d_mod, 0);
+    if (nw < level)
+        diag_mac_kernel<true><<<dim3(tiles, level - nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc,
+                                                                                               accs, level, c.N, c.d_mod, nw);
     c.prof_end(slot, s);
     c.st_launch++;
     c.st_bytes += bytes;
@@ -1158,9 +1233,10 @@ namespace {
 constexpr int BC_T = 32;
 
 __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, int N, const ModConst* __restrict__ mod) {
-    extern __shared__ u64 sb[];                 // [nsrc][2][BC_T] then [nu][BC_T]
+    extern __shared__ u64 sb[];                 // [nsrc][2][BC_T] then [nu][BC_T]  (narrow limbs: uint2 {h, l} per word)
     const int limb = blockIdx.y, k0 = blockIdx.x * BC_T;
     const ModConst mc = mod[limb];
+    const bool narrow = mc.q < (1ull << 41);   // 20-bit Karatsuba split (see diag_mac_kernel)
     const size_t cs = (size_t)level * N;
     const size_t lo = (size_t)limb * N + k0;
     u64* sm_src = sb;
@@ -1168,11 +1244,34 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
     for (int i = threadIdx.x; i < A.nsrc * 2 * BC_T; i += blockDim.x) {
         int d = i / (2 * BC_T), r = i % (2 * BC_T);
         int c = r / BC_T, kk = r % BC_T;
-        sm_src[i] = A.src[d][c * cs + lo + kk];
+        const u64 x = A.src[d][c * cs + lo + kk];
+        sm_src[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : x;
     }
-    for (int i = threadIdx.x; i < A.nu * BC_T; i += blockDim.x) sm_msk[i] = A.mask[i / BC_T][lo + i % BC_T];
+    for (int i = threadIdx.x; i < A.nu * BC_T; i += blockDim.x) {
+        const u64 x = A.mask[i / BC_T][lo + i % BC_T];
+        sm_msk[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : x;
+    }
     __syncthreads();
     const int kk = threadIdx.x % BC_T, w = threadIdx.x / BC_T, nw = blockDim.x / BC_T;
+    if (narrow) {
+        const u64 t40 = (1ull << 40) % mc.q;
+        const uint2* ss = (const uint2*)sm_src;
+        const uint2* sk = (const uint2*)sm_msk;
+        for (int o = w; o < A.nt * 2; o += nw) {
+            const int t = o >> 1, c = o & 1;
+            u64 hh = 0, ll = 0, sum = 0;
+            const uint2* sp = ss + (size_t)(t + A.dmax) * 2 * BC_T + c * BC_T + kk;
+#pragma unroll 8
+            for (int u = 0; u < A.nu; u++) {
+                const uint2 x = sp[-(i64)u * 2 * BC_T], m = sk[u * BC_T + kk];
+                hh += (u64)x.x * m.x;
+                ll += (u64)x.y * m.y;
+                sum += (u64)(x.x + x.y) * (m.x + m.y);
+            }
+            A.out[t][c * cs + lo + kk] = kara_combine(hh, ll, sum, mc.q, mc.rhi, mc.rlo, t40);
+        }
+        return;
+    }
     for (int o = w; o < A.nt * 2; o += nw) {
         const int t = o >> 1, c = o & 1;
         U128 acc{0, 0};
