@@ -37,6 +37,11 @@ PROF_KERNELS = ["diag_mac", "ks_inner", "ks_psi", "ks_rotsum", "ntt", "bcast_mac
                 "tensor_acc_kernel", "rescale_prep_kernel", "rescale_finish_kernel"]
 L_QKV, L_V_P, L_FF = 8, 5, 3
 C_QK, BETA = 192, 16
+# layer shapes: BERT-base and the NEXT-row second workload BERT-large; C_qk = 192 used
+# segments of 256 = 16 channels x 12 heads (base) / 12 channels x 16 heads (large), all phases 0 (G8)
+MODELS = {"layer": dict(name="bert-base-layer", d=768, H=12, dff=3072),
+          "qkv": dict(name="bert-base-qkv", d=768, H=12, dff=3072),
+          "bert-large-layer": dict(name="bert-large-layer", d=1024, H=16, dff=4096)}
 NTT_TRAFFIC = None   # ncu dram__bytes (read + write) per limb transform, filled from profiles/r01_summary.md
 
 
@@ -46,7 +51,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear"])
+    ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear", "bert-large-layer"])
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
 
@@ -141,9 +146,14 @@ class Layer:
         t0 = time.time()
         if workload == "gpt2-linear":
             return self._init_gpt2(device, seed_off, t0)
-        self.qkv = E.ProjPlan(ctx, M, D, 11 * 256)
+        mdl = MODELS[workload]
+        D, H, DFF = mdl["d"], mdl["H"], mdl["dff"]
+        self.d, self.H, self.dff = D, H, DFF
+        self.full = workload != "qkv"
+        nblk = 2 * -(-(H * DH) // C_QK) + -(-D // 256)
+        self.qkv = E.ProjPlan(ctx, M, D, nblk * 256)
         galois = set(self.qkv.galois())
-        if workload == "layer":
+        if self.full:
             self.attn = E.AttnPlan(ctx, M, H, DH, C_qk=C_QK, beta=BETA)
             self.oproj = E.ProjPlan(ctx, M, D, D)
             self.ff1 = E.ProjPlan(ctx, M, D, DFF)
@@ -160,7 +170,7 @@ class Layer:
         self.nqk = nqk
         self.w_qkv = self.qkv.encode_weights(Wqkv, L_QKV)
         self.wsc_qkv = float(ctx.q[L_QKV - 1])
-        if workload == "layer":
+        if self.full:
             self.w_o = self.oproj.encode_weights(synth.bert_weight((D, D), synth.seed_data(5) + 3), L_V_P - 2)
             self.w_1 = self.ff1.encode_weights(synth.bert_weight((D, DFF), synth.seed_data(5) + 4), L_FF)
             self.w_2 = self.ff2.encode_weights(synth.bert_weight((DFF, D), synth.seed_data(5) + 5), L_FF)
@@ -169,7 +179,7 @@ class Layer:
         # synthetic client inputs (encrypted before the timed region)
         X = synth.fixed_point_uniform((M, D), synth.seed_data(3) + seed_off)
         self.host_inputs = {"x": [self._enc(z, L_QKV, 10 + i) for i, z in enumerate(PK.complexified_inputs(X, M, 256, n))]}
-        if workload == "layer":
+        if self.full:
             P = synth.attention_probs(H, M, synth.seed_data(4) + seed_off)
             # P_fd (the M2C import of the softmax output) at Delta * 2^7 (DESIGN.md R-PSCALE)
             self.host_inputs["p"] = [self._enc(z, L_V_P, 20 + i, scale=self.sc * 2.0 ** 7)
@@ -432,8 +442,10 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "u64",
         "data": "synthetic (seeded; BERT-init random weights; encrypted U[-1,1] F=13 activations)",
-        "config": {"workload": {"layer": "bert-base-layer", "qkv": "bert-base-qkv", "gpt2-linear": "gpt2-small-linear-path"}[args.workload],
-                   "N": 65536, "m": getattr(layer, "m", M), "d": D, "H": H, "d_ff": DFF,
+        "config": {"workload": {"layer": "bert-base-layer", "qkv": "bert-base-qkv", "gpt2-linear": "gpt2-small-linear-path",
+                                "bert-large-layer": "bert-large-layer"}[args.workload],
+                   "N": 65536, "m": getattr(layer, "m", M), "d": getattr(layer, "d", D), "H": getattr(layer, "H", H),
+                   "d_ff": getattr(layer, "dff", DFF),
                    "levels": {"qkv": L_QKV, "p_fd": L_V_P, "out_proj": 5 if args.workload == "gpt2-linear" else L_V_P - 2,
                               "ff": L_FF, "conv": layer.Lconv},
                    "params": "P16 (q0 60b + 23x40b, K=6 x 60b special, alpha=8)",

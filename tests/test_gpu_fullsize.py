@@ -84,18 +84,16 @@ def test_qkv_projection_config3_block0_bit_exact(ctx):
         assert np.abs(got - ref).max() / np.abs(Y).max() < TOL, b
 
 
-def test_score_config4_sampled_t_bit_exact(ctx):
-    """Config 4 score: Q, K in 4 padded blocks (C_qk = 192 of 256 segments), beta = 16, L = 7."""
+def _score_case(ctx, H, ts, B_nout):
     L = 7
     plan = E.AttnPlan(ctx, M, H, DH, C_qk=192, beta=16)
     oplan = K.ScorePlan(P.n, M, H, DH, C_qk=192, beta=16)
-    assert (plan.B, plan.n_out) == (oplan.B, oplan.n_out) == (4, 3)
-    g = synth.rng(synth.seed_data(4))
+    assert (plan.B, plan.n_out) == (oplan.B, oplan.n_out) == B_nout
+    g = synth.rng(synth.seed_data(4) + H)
     Qh = g.uniform(-1, 1, (H, M, DH)) / np.sqrt(8)
     Kh = g.uniform(-1, 1, (H, M, DH)) / np.sqrt(8)
     perm = K.pi_S(H, DH)
     Qp, Kp = np.concatenate(list(Qh), 1)[:, perm], np.concatenate(list(Kh), 1)[:, perm]
-    ts = [0, 17, 63]
     steps = set()
     for s in range(1, oplan.beta):
         steps |= {M - s, -s}           # Psi^{-s}: rot by t' = (-s mod m) = m - s and t' - m = -s
@@ -129,6 +127,18 @@ def test_score_config4_sampled_t_bit_exact(ctx):
     want = np.concatenate(ref_diag)
     assert np.abs(stream[:len(want)] - want).max() / scale < TOL
     ctx.mask_clear()
+
+
+def test_score_config4_sampled_t_bit_exact(ctx):
+    """Config 4 score: Q, K in 4 padded blocks (C_qk = 192 of 256 segments = 16 channels x 12 heads), beta = 16,
+    L = 7; sampled t in {0, 17, 63} against the oracle, every t against brute force, K_min(S) = 3 exports."""
+    _score_case(ctx, H, [0, 17, 63], (4, 3))
+
+
+def test_score_bert_large_sampled_t_bit_exact(ctx):
+    """NEXT-row workload BERT-large (H = 16, d = 1024): the same kernel with a new plan --
+    C_qk = 192 = 12 channels x 16 heads (phases 0), B = 6 blocks, K_min(S) = 4 exports."""
+    _score_case(ctx, 16, [0, 63], (6, 4))
 
 
 def test_value_config4_block0_bit_exact(ctx):
