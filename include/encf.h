@@ -240,6 +240,17 @@ encf_status encf_field2ring_local(encf_ctx* ctx, const uint64_t* share, int32_t 
 /* Alg 4 step 4: P1 outputs <m> = <c> + [[t^]]_1 (c from P0, NTT form; share: plaintext over Q_L in
  * either domain). */
 encf_status encf_import_m2c(encf_ctx* ctx, const encf_ct* c, const encf_pt* share, encf_ct* out, void* stream);
+/* ------------------------------------------------------------------------------------------ GELU pre-evaluation */
+/* Alg 5 steps 1-3, the CKKS half of secure GELU: for each complex x[i] = x^(0) + i x^(1) (level L >= 4,
+ * all inputs at one level and scale): x^(0) = (x + conj x)/2, x^(1) = (x - conj x)/(2i) (the 1/2 as scale x 2,
+ * G3); per channel x^2, x^3, x^4 (tensor + relin + rescale each) and the Eq. B.2 candidates
+ * F0 = a x^4 - b x^3 + c x^2 + (0.5 - d) x + e, F1 = a x^4 + b x^3 + c x^2 + (0.5 + d) x + e with the public
+ * coef = {a, b, c, d, e} applied as integers round_half_even(coef * Delta) (DESIGN.md R-GELU);
+ * f0[i] = F0^(0) + i F0^(1), f1[i] = F1^(0) + i F1^(1) at level L - 3 (caller buffers, 2 components).
+ * Keys: conj + relin.  Errors: ARG, LEVEL_EXHAUSTED (L < 4), LEVEL_MISMATCH / SCALE_MISMATCH (mixed inputs),
+ * MISSING_KEY. */
+encf_status encf_gelu_preeval(encf_ctx* ctx, const encf_keys* keys, const encf_ct* x, int32_t n, const double* coef,
+                              encf_ct* f0, encf_ct* f1, void* stream);
 
 /* After a cross-rank uint64 SUM (C2): reduce n_polys x [n_limbs][N] words mod q_i in place.
  * Valid while the summed value fits in 64 bits (world_size * q < 2^64). */

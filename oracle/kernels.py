@@ -785,3 +785,84 @@ def import_m2c(P, ct, share_pt):
     """Alg 4 step 4: <m> = <c> + [[t^]]_1 (plaintext share added to c0)."""
     mods = P.q[:ct.L]
     return O.Ct(np.stack([O.padd(ct.c[0], share_pt.m, mods, P.N), ct.c[1]]), ct.scale)
+
+
+# ====================================================================================== GELU pre-evaluation (NEXT row 2)
+def gelu_exact(x):
+    import math
+    return np.array([0.5 * v * (1.0 + math.erf(v / math.sqrt(2.0))) for v in np.asarray(x, dtype=float).ravel()])
+
+
+def gelu_fit():
+    """Coefficients (a, b, c, d, e) of ApproxGELU's mid-range branch a|x|^4 + b|x|^3 + c|x|^2 + d|x| + e + 0.5x
+    (Eq. B.1).  The paper uses BOLT's coefficients without printing them; reading R-GELU
+    (SPEC's decision): the least-squares quartic in |x| fitted to GELU(x) - 0.5x on [0, 2.7] (2701
+    points, numpy lstsq), frozen by this function."""
+    t = np.linspace(0.0, 2.7, 2701)
+    target = gelu_exact(t) - 0.5 * t
+    A = np.stack([t ** 4, t ** 3, t ** 2, t, np.ones_like(t)], axis=1)
+    coef, *_ = np.linalg.lstsq(A, target, rcond=None)
+    return tuple(float(v) for v in coef)
+
+
+def approx_gelu(x, coef):
+    """Eq. B.1 in float64 (pass-through above 2.7, zero below -2.7, quartic in |x| plus 0.5x inside)."""
+    a, b, c, d, e = coef
+    x = np.asarray(x, dtype=float)
+    ax = np.abs(x)
+    mid = a * ax ** 4 + b * ax ** 3 + c * ax ** 2 + d * ax + e + 0.5 * x
+    return np.where(x > 2.7, x, np.where(x < -2.7, 0.0, mid))
+
+
+def const_mul_rescale(ev, ct, c, target):
+    """ct x (public constant c), then rescale: c enters as the INTEGER k = round_half_even(c * Delta) on every
+    coefficient (a constant plaintext at scale Delta = target q_{L-1} / scale), so the rescaled result
+    carries the tracked scale `target` (set exactly; the true scale differs by |k - c Delta| / (c Delta),
+    below 2^-30 here; reading R-GELU)."""
+    L, N = ct.L, ev.P.N
+    delta = target * float(ev.P.q[L - 1]) / ct.scale
+    k = int(round(c * delta))
+    mods = ev.P.q[:L]
+    cc = np.stack([O.pmul_scalar(ct.c[i], [k % q for q in mods], mods, N) for i in range(ct.ncomp)])
+    ev.ledger["ptmul"] += 1
+    y = ev.rescale(O.Ct(cc, ct.scale))
+    return O.Ct(y.c, target)
+
+
+def add_const(ev, ct, e):
+    """ct + e (public constant): E = round_half_even(e * scale) added to the constant coefficient of c0."""
+    L = ct.L
+    E = int(round(e * ct.scale))
+    c = ct.c.copy()
+    for i, q in enumerate(ev.P.q[:L]):
+        c[0][i][0] = np.uint64((int(c[0][i][0]) + E) % q)
+    return O.Ct(c, ct.scale)
+
+
+def gelu_preeval(ev, x, coef):
+    """Alg 5 steps 1-3, the CKKS half of secure GELU with pre-evaluation.
+       1. x^(0) = (x + conj x)/2, x^(1) = (x - conj x)/(2i) = i (conj x - x)/2   (the 1/2 is scale bookkeeping, G3)
+       2. per j: x^2, x^3 = x^2 x, x^4 = x^2 x^2 (each one tensor + relin + rescale), then
+          F0 = a x^4 - b x^3 + c x^2 + (0.5 - d) x + e,  F1 = a x^4 + b x^3 + c x^2 + (0.5 + d) x + e  (Eq. B.2)
+          with every term brought to level L-3 and one common scale (const_mul_rescale / mod_drop)
+       3. F0^C = F0^(0) + i F0^(1), F1^C = F1^(0) + i F1^(1)   (i = X^{N/2}, exact)
+    Input: complex x at level L >= 4.  Returns (F0^C, F1^C) at level L-3."""
+    a, b, c, d, e = coef
+    L = x.L
+    xc = ev.conj(x)
+    xs = [ev.scale_mul(ev.add(x, xc), 2.0), ev.scale_mul(ev.mul_i(ev.sub(xc, x)), 2.0)]
+    F0, F1 = [], []
+    for xj in xs:
+        T = xj.scale
+        x2 = ev.rescale(ev.relin(ev.tensor(xj, xj)))
+        x3 = ev.rescale(ev.relin(ev.tensor(x2, ev.mod_drop(xj, L - 1))))
+        x4 = ev.rescale(ev.relin(ev.tensor(x2, x2)))
+        A = const_mul_rescale(ev, x4, a, T)
+        B = const_mul_rescale(ev, x3, b, T)
+        C = ev.mod_drop(const_mul_rescale(ev, x2, c, T), L - 3)
+        D0 = ev.mod_drop(const_mul_rescale(ev, xj, 0.5 - d, T), L - 3)
+        D1 = ev.mod_drop(const_mul_rescale(ev, xj, 0.5 + d, T), L - 3)
+        base = ev.add(A, C)
+        F0.append(add_const(ev, ev.add(ev.sub(base, B), D0), e))
+        F1.append(add_const(ev, ev.add(ev.add(base, B), D1), e))
+    return ev.add(F0[0], ev.mul_i(F0[1])), ev.add(F1[0], ev.mul_i(F1[1]))

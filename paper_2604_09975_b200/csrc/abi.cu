@@ -658,6 +658,26 @@ encf_status encf_ct_ct_attn_value(encf_ctx* c, const encf_keys* k, const encf_at
     });
 }
 
+// ------------------------------------------------------------------------------------ GELU pre-evaluation
+encf_status encf_gelu_preeval(encf_ctx* c, const encf_keys* k, const encf_ct* x, int32_t n, const double* coef, encf_ct* f0,
+                              encf_ct* f1, void* stream) {
+    return guard([&] {
+        need(c && k && x && coef && f0 && f1 && n > 0, ENCF_ERR_ARG, "gelu_preeval: null argument");
+        EV_BEGIN(k);
+        std::vector<DCt> xs;
+        for (int i = 0; i < n; i++) xs.push_back(view(&x[i]));
+        std::vector<DCt> a, b;
+        gelu_preeval_run(ev, xs, coef, a, b);
+        for (int i = 0; i < n; i++) {
+            DCt oa = outview(&f0[i], a[i].L, 2), ob = outview(&f1[i], b[i].L, 2);
+            ev.copy(a[i], oa);
+            ev.copy(b[i], ob);
+            writeback(&f0[i], oa);
+            writeback(&f1[i], ob);
+        }
+    });
+}
+
 // ------------------------------------------------------------------------------------ export
 encf_status encf_l_conv(encf_ctx* c, int32_t ell, int32_t sigma, double scale, double B_max, int32_t* L) {
     if (!c || !L) return ENCF_ERR_ARG;

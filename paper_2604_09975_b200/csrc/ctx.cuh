@@ -222,6 +222,7 @@ void k_copy(const u64* in, u64* out, size_t words, cudaStream_t s);
 void k_sample_uniform(encf_ctx& c, u64 seed, u64 stream, u64* out, const LimbMap& m, const int* gids, cudaStream_t s);
 void k_sample_small(encf_ctx& c, u64 seed, u64 stream, int kind /*0 ternary, 1 cbd21*/, u64* out, const LimbMap& m,
                     cudaStream_t s);
+void k_add_scalar(encf_ctx& c, u64* data, const LimbMap& m, const u64* d_scal, cudaStream_t s);
 void k_scalar_mul(encf_ctx& c, u64* data, int npolys, const LimbMap& m, const u64* d_scal, const u64* d_scal_sh,
                   cudaStream_t s);
 void k_mod_reduce(encf_ctx& c, u64* data, int npolys, const LimbMap& m, cudaStream_t s);

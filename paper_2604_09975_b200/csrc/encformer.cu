@@ -435,3 +435,132 @@ int l_conv_rule(const encf_ctx& c, int ell, int sigma, double scale, double B_ma
     }
     return -1;
 }
+
+// ====================================================================================== GELU pre-evaluation (Alg 5 steps 1-3)
+// Oracle: kernels.gelu_preeval (same schedule, same integer constants).  All inputs share one level and scale;
+// every step is batched over the 2n real channels.
+namespace {
+// c x ct (public constant as the integer k = round_half_even(c target q_{L-1} / scale)), rescale, scale := target
+void const_mul_rescale_many(Ev& ev, const std::vector<const DCt*>& ins, double c, double target, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    const int L = ins[0]->L, N = ev.c.N;
+    const double delta = target * (double)ev.c.mods[L - 1] / ins[0]->scale;
+    const long long k = (long long)std::nearbyint(c * delta);
+    std::vector<u64> sc(L), sh(L);
+    for (int i = 0; i < L; i++) {
+        const u64 q = ev.c.mods[i];
+        long long r = k % (long long)q;
+        if (r < 0) r += (long long)q;
+        sc[i] = (u64)r;
+        sh[i] = shoup_pre(sc[i], q);
+    }
+    const u64* dsc = ev.upload(sc);
+    const u64* dsh = ev.upload(sh);
+    std::vector<DCt> tmp = ev.alloc_many(n, L);
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->L != L || ins[i]->scale != ins[0]->scale) throw EncfError(ENCF_ERR_SCALE_MISMATCH, "gelu: mixed inputs");
+        ev.copy(*ins[i], tmp[i]);
+    }
+    k_scalar_mul(ev.c, tmp[0].d, 2 * n, ev.c.qmap(L), dsc, dsh, ev.s);     // tmp is contiguous [n][2][L][N]
+    ev.c.st_ptmul += n;
+    outs = ev.alloc_many(n, L - 1);
+    ev.rescale_many(ptrs(tmp), outs);
+    for (auto& o : outs) o.scale = target;
+    (void)N;
+}
+
+std::vector<DCt> drop_many(Ev& ev, const std::vector<DCt>& xs, int L) {
+    std::vector<DCt> out = ev.alloc_many((int)xs.size(), L);
+    for (size_t i = 0; i < xs.size(); i++) ev.mod_drop(xs[i], L, out[i]);
+    return out;
+}
+
+void add_const_many(Ev& ev, std::vector<DCt>& xs, double e) {
+    const int L = xs[0].L;
+    const long long E = (long long)std::nearbyint(e * xs[0].scale);
+    std::vector<u64> sc(L);
+    for (int i = 0; i < L; i++) {
+        long long r = E % (long long)ev.c.mods[i];
+        if (r < 0) r += (long long)ev.c.mods[i];
+        sc[i] = (u64)r;
+    }
+    const u64* dsc = ev.upload(sc);
+    for (auto& x : xs) {
+        if (x.scale != xs[0].scale || x.L != L) throw EncfError(ENCF_ERR_SCALE_MISMATCH, "gelu: mixed candidates");
+        k_add_scalar(ev.c, x.d, ev.c.qmap(L), dsc, ev.s);      // NTT of the constant polynomial E is E everywhere
+    }
+}
+}  // namespace
+
+void gelu_preeval_run(Ev& ev, const std::vector<DCt>& xs, const double coef[5], std::vector<DCt>& f0, std::vector<DCt>& f1) {
+    const int n = (int)xs.size();
+    const int L = xs[0].L;
+    const double a = coef[0], b = coef[1], c = coef[2], d = coef[3], e = coef[4];
+    if (L < 4) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "gelu pre-evaluation needs 3 levels above the output");
+    for (auto& x : xs)
+        if (x.L != L || x.scale != xs[0].scale || x.ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "gelu: inputs must share level and scale");
+    // 1. real / imaginary channels: x0 = x + conj x, x1 = i (conj x - x), scale x 2 (G3)
+    std::vector<DCt> xc = ev.alloc_many(n, L);
+    ev.rotate_many(ptrs(xs), std::vector<uint32_t>(n, ev.galois_conj()), xc);
+    std::vector<DCt> xj = ev.alloc_many(2 * n, L);      // [j][i]
+    for (int i = 0; i < n; i++) {
+        ev.add(xs[i], xc[i], xj[i]);
+        DCt t = ev.alloc(L);
+        ev.add(xc[i], xs[i], t, /*sub=*/true);
+        ev.mul_i(t, xj[n + i]);
+    }
+    for (auto& x : xj) x.scale *= 2.0;
+    // 2. powers: x^2 = x x; x^3 = x^2 (x dropped to L-1); x^4 = x^2 x^2 (tensor, relin, rescale each)
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pp(2 * n);
+    for (int i = 0; i < 2 * n; i++) pp[i] = {{&xj[i], &xj[i]}};
+    std::vector<DCt> t3 = ev.alloc_many(2 * n, L, 3), t2 = ev.alloc_many(2 * n, L), x2 = ev.alloc_many(2 * n, L - 1);
+    ev.tensor_many(pp, t3);
+    ev.relin_many(ptrs(t3), t2);
+    ev.rescale_many(ptrs(t2), x2);
+    std::vector<DCt> xd = drop_many(ev, xj, L - 1);
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> p34(4 * n);
+    for (int i = 0; i < 2 * n; i++) {
+        p34[i] = {{&x2[i], &xd[i]}};
+        p34[2 * n + i] = {{&x2[i], &x2[i]}};
+    }
+    std::vector<DCt> u3 = ev.alloc_many(4 * n, L - 1, 3), u2 = ev.alloc_many(4 * n, L - 1), x34 = ev.alloc_many(4 * n, L - 2);
+    ev.tensor_many(p34, u3);
+    ev.relin_many(ptrs(u3), u2);
+    ev.rescale_many(ptrs(u2), x34);
+    const double T = xj[0].scale;
+    auto slice = [](std::vector<DCt>& v, int a0, int a1) {
+        std::vector<const DCt*> r;
+        for (int i = a0; i < a1; i++) r.push_back(&v[i]);
+        return r;
+    };
+    std::vector<DCt> A, B, C, D0, D1;
+    const_mul_rescale_many(ev, slice(x34, 2 * n, 4 * n), a, T, A);       // a x^4 -> L-3
+    const_mul_rescale_many(ev, slice(x34, 0, 2 * n), b, T, B);           // b x^3 -> L-3
+    const_mul_rescale_many(ev, slice(x2, 0, 2 * n), c, T, C);            // c x^2 -> L-2
+    const_mul_rescale_many(ev, slice(xj, 0, 2 * n), 0.5 - d, T, D0);     // (0.5-d) x -> L-1
+    const_mul_rescale_many(ev, slice(xj, 0, 2 * n), 0.5 + d, T, D1);     // (0.5+d) x -> L-1
+    C = drop_many(ev, C, L - 3);
+    D0 = drop_many(ev, D0, L - 3);
+    D1 = drop_many(ev, D1, L - 3);
+    std::vector<DCt> F0 = ev.alloc_many(2 * n, L - 3), F1 = ev.alloc_many(2 * n, L - 3);
+    for (int i = 0; i < 2 * n; i++) {
+        DCt base = ev.alloc(L - 3), t = ev.alloc(L - 3), u = ev.alloc(L - 3);
+        ev.add(A[i], C[i], base);
+        ev.add(base, B[i], t, /*sub=*/true);
+        ev.add(t, D0[i], F0[i]);
+        ev.add(base, B[i], u);
+        ev.add(u, D1[i], F1[i]);
+    }
+    add_const_many(ev, F0, e);
+    add_const_many(ev, F1, e);
+    // 3. complex packing F^C = F^(0) + i F^(1)
+    f0 = ev.alloc_many(n, L - 3);
+    f1 = ev.alloc_many(n, L - 3);
+    for (int i = 0; i < n; i++) {
+        DCt t = ev.alloc(L - 3), u = ev.alloc(L - 3);
+        ev.mul_i(F0[n + i], t);
+        ev.add(F0[i], t, f0[i]);
+        ev.mul_i(F1[n + i], u);
+        ev.add(F1[i], u, f1[i]);
+    }
+}

@@ -120,6 +120,14 @@ __global__ void scalar_mul_kernel(u64* data, int npolys, int N, LimbMap m, const
     }
 }
 
+__global__ void add_scalar_kernel(u64* data, int N, LimbMap m, const ModConst* mod, const u64* sc) {
+    const size_t total = (size_t)m.n * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int limb = (int)(i / N);
+        data[i] = add_mod(data[i], sc[limb], mod[m.mod[limb]].q);
+    }
+}
+
 __global__ void mod_reduce_kernel(u64* data, size_t total, int N, LimbMap m, const ModConst* mod) {
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
         int limb = (int)((i / N) % m.n);
@@ -285,36 +293,54 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
         }
         __syncthreads();
         const u64 t40 = (1ull << 40) % mc.q;
-        for (int u = blockIdx.z * MAC_LANES + lane; u < units; u += gridDim.z * MAC_LANES) {
-            const u64* wu = w + (size_t)u * wus + wl;
-            // [component][coefficient] x {hh, ll, ss}
-            u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
-            for (int uq0 = 0; uq0 < nbank; uq0 += 8) {
-                const int cnt = min(8, nbank - uq0);
-                ulonglong2 x[8];
+        // software-pipelined stream: the 8 plaintext words of the NEXT (unit, chunk) are in flight while the
+        // current chunk is multiplied (keeps ~128 B per thread outstanding -> HBM-bound, not latency-bound)
+        const int nch = (nbank + 7) / 8, ustride = gridDim.z * MAC_LANES;
+        int u = blockIdx.z * MAC_LANES + lane, ch = 0;
+        if (u >= units) return;
+        ulonglong2 cur[8], nxt[8];
+#pragma unroll
+        for (int t = 0; t < 8; t++)
+            if (t < nbank) cur[t] = __ldg((const ulonglong2*)(w + (size_t)u * wus + wl + (size_t)t * pstride));
+        u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
+        while (true) {
+            int nu = u, nc = ch + 1;
+            if (nc == nch) { nu = u + ustride; nc = 0; }
+            const bool more = nu < units;
+            if (more) {
+                const u64* wn = w + (size_t)nu * wus + wl + (size_t)(nc * 8) * pstride;
+                const int cn = min(8, nbank - nc * 8);
 #pragma unroll
                 for (int t = 0; t < 8; t++)
-                    if (t < cnt) x[t] = __ldg((const ulonglong2*)(wu + (size_t)(uq0 + t) * pstride));
-#pragma unroll
-                for (int t = 0; t < 8; t++) {
-                    if (t >= cnt) break;
-                    const int uq = uq0 + t;
-                    const uint32_t ah = (uint32_t)(x[t].x >> 20), al = (uint32_t)(x[t].x & 0xFFFFF);
-                    const uint32_t bh = (uint32_t)(x[t].y >> 20), bl = (uint32_t)(x[t].y & 0xFFFFF);
-                    const uint32_t as = ah + al, bsum = bh + bl;
-                    const uint4 pp = *(const uint4*)&sn[(uq * 2 + 0) * MAC_T + 2 * kp];   // {h, l} of k, k+1
-                    const uint4 rr = *(const uint4*)&sn[(uq * 2 + 1) * MAC_T + 2 * kp];
-                    h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
-                    h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
-                    h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
-                    h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
-                }
+                    if (t < cn) nxt[t] = __ldg((const ulonglong2*)(wn + (size_t)t * pstride));
             }
-            u64* o = acc + (size_t)u * accs + wl;
-            *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
-                                              kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
-            *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
-                                                     kara_combine(h11, l11, s11, mc.q, mc.rhi, mc.rlo, t40));
+            const int cnt = min(8, nbank - ch * 8);
+#pragma unroll
+            for (int t = 0; t < 8; t++) {
+                if (t >= cnt) break;
+                const int uq = ch * 8 + t;
+                const uint32_t ah = (uint32_t)(cur[t].x >> 20), al = (uint32_t)(cur[t].x & 0xFFFFF);
+                const uint32_t bh = (uint32_t)(cur[t].y >> 20), bl = (uint32_t)(cur[t].y & 0xFFFFF);
+                const uint32_t as = ah + al, bsum = bh + bl;
+                const uint4 pp = *(const uint4*)&sn[(uq * 2 + 0) * MAC_T + 2 * kp];   // {h, l} of k, k+1
+                const uint4 rr = *(const uint4*)&sn[(uq * 2 + 1) * MAC_T + 2 * kp];
+                h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
+                h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
+                h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
+                h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
+            }
+            if (ch == nch - 1) {
+                u64* o = acc + (size_t)u * accs + wl;
+                *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
+                                                  kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
+                *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
+                                                         kara_combine(h11, l11, s11, mc.q, mc.rhi, mc.rlo, t40));
+                h00 = l00 = s00 = h01 = l01 = s01 = h10 = l10 = s10 = h11 = l11 = s11 = 0;
+            }
+            if (!more) break;
+            u = nu; ch = nc;
+#pragma unroll
+            for (int t = 0; t < 8; t++) cur[t] = nxt[t];
         }
         return;
     }
@@ -535,6 +561,13 @@ void k_sample_small(encf_ctx& c, u64 seed, u64 stream, int kind, u64* out, const
     sample_small_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(seed, stream, kind, out, c.N, m, c.d_mod);
     c.prof_end(_slot, s); }
     c.st_launch++;
+}
+
+// + sc_limb on every (NTT-domain) coefficient of one polynomial: a public constant added to the message
+void k_add_scalar(encf_ctx& c, u64* data, const LimbMap& m, const u64* sc, cudaStream_t s) {
+    add_scalar_kernel<<<GRID((size_t)m.n * c.N), TB, 0, s>>>(data, c.N, m, c.d_mod, sc);
+    c.st_launch++;
+    CUDA_TRY(cudaGetLastError());
 }
 
 void k_scalar_mul(encf_ctx& c, u64* data, int npolys, const LimbMap& m, const u64* sc, const u64* scs, cudaStream_t s) {

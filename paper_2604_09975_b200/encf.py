@@ -95,6 +95,7 @@ _SIG = {
     "encf_ring2field_local": [_p, _p, _i32, _i32, _i32, _p, _p],
     "encf_field2ring_local": [_p, _p, _i32, _p, _p],
     "encf_import_m2c": [_p, ctypes.POINTER(CT), ctypes.POINTER(PT), ctypes.POINTER(CT), _p],
+    "encf_gelu_preeval": [_p, _p, _p, ctypes.c_int32, _p, _p, _p, _p],
     "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
     "encf_profile_peek": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
@@ -402,6 +403,19 @@ class Context:
         c = out._c()
         _chk(_lib.encf_import_m2c(self.h, ctypes.byref(ct._c()), ctypes.byref(share_pt._p()), ctypes.byref(c), _stream()), "import_m2c")
         return out._update(c)
+
+    def gelu_preeval(self, keys, xs, coef):
+        """Alg 5 steps 1-3 on complex ciphertexts xs (one level and scale): returns (F0^C list, F1^C list) at L - 3."""
+        L = xs[0].n_limbs
+        f0 = [self.empty_ct(L - 3) for _ in xs]
+        f1 = [self.empty_ct(L - 3) for _ in xs]
+        xa = (CT * len(xs))(*[x._c() for x in xs])
+        a0 = (CT * len(xs))(*[o._c() for o in f0])
+        a1 = (CT * len(xs))(*[o._c() for o in f1])
+        cf = np.ascontiguousarray(np.array(coef, dtype=np.float64))
+        _chk(_lib.encf_gelu_preeval(self.h, keys.h, ctypes.cast(xa, _p), len(xs), cf.ctypes.data, ctypes.cast(a0, _p),
+                                    ctypes.cast(a1, _p), _stream()), "gelu_preeval")
+        return [o._update(a0[i]) for i, o in enumerate(f0)], [o._update(a1[i]) for i, o in enumerate(f1)]
 
     def mod_reduce_ext(self, tensor, n_polys, L):
         _chk(_lib.encf_mod_reduce_ext(self.h, tensor.data_ptr(), n_polys, L, _stream()), "mod_reduce_ext")

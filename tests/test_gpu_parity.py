@@ -371,3 +371,26 @@ def test_ntt_fp64_path_equals_integer_path(monkeypatch):
         ctx.from_ntt(t)
         outs.append(ctx.to_host(t, coeff=False))
     assert np.array_equal(outs[2], outs[3])
+
+
+# ------------------------------------------------------------------ GELU pre-evaluation (Alg 5 steps 1-3)
+def test_gelu_preeval_bit_exact(c13, keys13):
+    """encf_gelu_preeval on two complex inputs at L = 5 (N = 2^13): both candidate ciphertexts F0^C, F1^C
+    equal the oracle's on every limb, and decrypt to Eq. B.2 of the real and imaginary channels."""
+    ok, gk = keys13
+    coef = K.gelu_fit()
+    g = synth.rng(91)
+    xs_h, refs = [], []
+    for i in range(2):
+        x0, x1 = g.uniform(-2.7, 2.7, P13.n), g.uniform(-2.7, 2.7, P13.n)
+        x = O.encrypt_sk(P13, ok, O.encode(P13, x0 + 1j * x1, 2.0 ** 40, 5), 500 + i)
+        xs_h.append((x, x0, x1))
+        refs.append(K.gelu_preeval(K.Ev(P13, ok, 16), x, coef))
+    f0, f1 = c13.gelu_preeval(gk, [dev_ct(c13, x) for x, _, _ in xs_h], coef)
+    a, b, c, d, e = coef
+    for i, ((x, x0, x1), (r0, r1)) in enumerate(zip(xs_h, refs)):
+        assert_ct_equal(c13, f0[i], r0, "F0^C[%d]" % i)
+        assert_ct_equal(c13, f1[i], r1, "F1^C[%d]" % i)
+        z = O.decode(P13, O.decrypt(P13, ok, O.Ct(c13.to_host(f1[i]), f1[i].scale)))
+        F1 = lambda v: a * v ** 4 + b * v ** 3 + c * v ** 2 + (0.5 + d) * v + e
+        assert np.abs(z - (F1(x0) + 1j * F1(x1))).max() < 1e-5

@@ -359,3 +359,37 @@ def test_conversion_payload_paper_value():
     ct = 2 * 5 * 65536 * 8
     assert round(2 * ct / 1e6, 2) == g["complex"]
     assert abs(4 * ct / 1e6 - g["real"]) < 0.01
+
+
+# ------------------------------------------------------------------ GELU pre-evaluation (Alg 5 steps 1-3, NEXT row 2)
+def test_gelu_fit_quality():
+    """R-GELU: the frozen least-squares quartic reproduces GELU within 0.01 on [-4, 4] (SPEC's acceptance)
+    and its mid-range branch is Eq. B.1's shape (odd terms flip sign with x: F0 for x < 0, F1 for x >= 0)."""
+    c = K.gelu_fit()
+    x = np.linspace(-4, 4, 801)
+    assert np.abs(K.approx_gelu(x, c) - K.gelu_exact(x)).max() < 0.01
+    a, b, cc, d, e = c
+    for v in (-2.0, -0.5, 0.3, 1.7):
+        f0 = a * v ** 4 - b * v ** 3 + cc * v ** 2 + (0.5 - d) * v + e
+        f1 = a * v ** 4 + b * v ** 3 + cc * v ** 2 + (0.5 + d) * v + e
+        assert abs((f0 if v < 0 else f1) - K.approx_gelu([v], c)[0]) < 1e-12
+
+
+def test_gelu_preeval_decrypts_to_candidates(keys13):
+    """Alg 5 steps 1-3 at N = 2^13: Dec(F0^C) = F0(x^(0)) + i F0(x^(1)) and Dec(F1^C) likewise (Eq. B.2), from a
+    complex x^C = x^(0) + i x^(1) at L = 5; outputs at L - 3 = 2 (the export level); 2 x 3 ct-ct products."""
+    ok = keys13
+    coef = K.gelu_fit()
+    g = synth.rng(77)
+    x0, x1 = g.uniform(-2.7, 2.7, P13.n), g.uniform(-2.7, 2.7, P13.n)
+    x = O.encrypt_sk(P13, ok, O.encode(P13, x0 + 1j * x1, 2.0 ** 40, 5), 88)
+    ev = K.Ev(P13, ok, 16)
+    f0, f1 = K.gelu_preeval(ev, x, coef)
+    assert f0.L == f1.L == 2 and ev.ledger["ctmul"] == 6 and ev.ledger["conj"] == 1
+    a, b, c, d, e = coef
+    F0 = lambda v: a * v ** 4 - b * v ** 3 + c * v ** 2 + (0.5 - d) * v + e
+    F1 = lambda v: a * v ** 4 + b * v ** 3 + c * v ** 2 + (0.5 + d) * v + e
+    z0 = O.decode(P13, O.decrypt(P13, ok, f0))
+    z1 = O.decode(P13, O.decrypt(P13, ok, f1))
+    assert np.abs(z0 - (F0(x0) + 1j * F0(x1))).max() < 1e-5
+    assert np.abs(z1 - (F1(x0) + 1j * F1(x1))).max() < 1e-5
