@@ -42,7 +42,7 @@ C_QK, BETA = 192, 16
 MODELS = {"layer": dict(name="bert-base-layer", d=768, H=12, dff=3072),
           "qkv": dict(name="bert-base-qkv", d=768, H=12, dff=3072),
           "bert-large-layer": dict(name="bert-large-layer", d=1024, H=16, dff=4096)}
-NTT_TRAFFIC = None   # ncu dram__bytes (read + write) per limb transform, filled from profiles/r01_summary.md
+NTT_TRAFFIC = 1.94e6  # ncu dram__bytes (read + write) per limb transform (fwd cols+rows, 384-limb batch; profiles/r01_ncu_ntt_fp64_vs_int.txt)
 
 
 def parse():
@@ -644,7 +644,7 @@ def run_reference(args):
 
 
 # schedule counts of one layer (filled from a GPU run's encf_stats; used only by --impl reference)
-LAYER_COUNTS = {"keyswitch": 1971, "ptmul_terms": 30208}
+LAYER_COUNTS = {"keyswitch": 2675, "ptmul_terms": 30882}
 
 
 def main():
