@@ -1290,18 +1290,35 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         const u64 t40 = (1ull << 40) % mc.q;
         const uint2* ss = (const uint2*)sm_src;
         const uint2* sk = (const uint2*)sm_msk;
-        for (int o = w; o < A.nt * 2; o += nw) {
-            const int t = o >> 1, c = o & 1;
-            u64 hh = 0, ll = 0, sum = 0;
-            const uint2* sp = ss + (size_t)(t + A.dmax) * 2 * BC_T + c * BC_T + kk;
-#pragma unroll 8
+        // register blocking: a thread computes TR = 4 consecutive t of one component, so each mask word
+        // (and its split sum) is loaded once per 4 products
+        constexpr int TR = 4;
+        const int ngrp = (A.nt + TR - 1) / TR;
+        for (int o = w; o < ngrp * 2; o += nw) {
+            const int t0 = (o >> 1) * TR, c = o & 1;
+            u64 hh[TR], ll[TR], sum[TR];
+#pragma unroll
+            for (int j = 0; j < TR; j++) hh[j] = ll[j] = sum[j] = 0;
+            const uint2* sp = ss + (size_t)(t0 + A.dmax) * 2 * BC_T + c * BC_T + kk;
+            const int jmax = min(TR, A.nt - t0);
+#pragma unroll 4
             for (int u = 0; u < A.nu; u++) {
-                const uint2 x = sp[-(i64)u * 2 * BC_T], m = sk[u * BC_T + kk];
-                hh += (u64)x.x * m.x;
-                ll += (u64)x.y * m.y;
-                sum += (u64)(x.x + x.y) * (m.x + m.y);
+                const uint2 m = sk[u * BC_T + kk];
+                const uint32_t ms = m.x + m.y;
+                const uint2* su = sp - (i64)u * 2 * BC_T;
+#pragma unroll
+                for (int j = 0; j < TR; j++) {
+                    if (j < jmax) {
+                        const uint2 x = su[(i64)j * 2 * BC_T];
+                        hh[j] += (u64)x.x * m.x;
+                        ll[j] += (u64)x.y * m.y;
+                        sum[j] += (u64)(x.x + x.y) * ms;
+                    }
+                }
             }
-            A.out[t][c * cs + lo + kk] = kara_combine(hh, ll, sum, mc.q, mc.rhi, mc.rlo, t40);
+#pragma unroll
+            for (int j = 0; j < TR; j++)
+                if (j < jmax) A.out[t0 + j][c * cs + lo + kk] = kara_combine(hh[j], ll[j], sum[j], mc.q, mc.rhi, mc.rlo, t40);
         }
         return;
     }
