@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 M, D, H, DH, DFF = 128, 768, 12, 64, 3072
-PROF_KERNELS = ["diag_mac", "ks_inner", "ks_psi", "ks_rotsum", "ntt", "bcast_mac", "add_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
+PROF_KERNELS = ["diag_mac", "ks_inner", "ks_psi", "ks_rotsum", "ks_rma", "ntt", "bcast_mac", "add_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
                 "export_mask_kernel", "gather_copy_kernel", "masked_sum_kernel", "mod_reduce_kernel",
                 "moddown_finish_batch_kernel", "moddown_finish_kernel", "mul_i_kernel", "mul_kernel",
                 "rescale_finish_batch_kernel", "rescale_prep_batch_kernel", "sum_csr_kernel", "tensor_csr_kernel",
@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear", "bert-large-layer"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ablation", default=None, choices=[None, "wo-scp"],
+                    help="wo-scp: insert the Halevi-Shoup RMA repack at the three FHE->FHE edges (App. G; Table 11 ablation)")
     return ap.parse_args()
 
 
@@ -133,7 +135,9 @@ def max_over_ranks(x, ws):
 class Layer:
     """BERT-base layer state on one GPU: context, keys, plans, encoded weights, synthetic inputs."""
 
-    def __init__(self, device, workload, seed_off=0):
+    ablation = None
+
+    def __init__(self, device, workload, seed_off=0, ablation=None):
         import torch
         import synth
         from paper_2604_09975_b200 import encf as E
@@ -162,6 +166,9 @@ class Layer:
                 galois |= set(pl.galois())
             galois |= set(self.attn.galois())
         galois.add(ctx.galois_conj())
+        self.ablation = ablation
+        if ablation == "wo-scp":
+            galois |= {ctx.galois_rot(1 << k) for k in range(M.bit_length() - 1)}
         self.keys = ctx.keygen(synth.SEED_KEYS, galois=sorted(galois), relin=True, max_level=L_QKV)
         self.n_keys = len(galois) + 1
         # weights (BERT init, clipped), pre-permuted (pi_S + G8 padding for Q/K, head-major V)
@@ -291,11 +298,15 @@ class Layer:
             return [(c.data, None) for c in y]
         nqk = self.nqk
         Q, K, V = y[:nqk], y[nqk:2 * nqk], y[2 * nqk:]
+        if self.ablation == "wo-scp":       # edges (1) QKV -> score and (2) QKV -> value (App. G), cost only
+            ctx.repack_rma(keys, Q + K + V, M)
         S = self.attn.score(keys, Q, K)
         self._mark("score")
         ex = self._export(self.attn.export_stream(keys, S), 0)
         self._mark("score_export")
         O = self.attn.value(keys, inp["p"], V)
+        if self.ablation == "wo-scp":       # edge (3) value -> out-projection
+            ctx.repack_rma(keys, O, M)
         self._mark("value")
         Ore = []
         for o in O:                        # decomplexify the value output (G11): Re o = (o + conj o) / 2
@@ -325,7 +336,7 @@ def run_ours(args):
         return run_ks(args)
     ws, rank, local = dist_init(args)
     torch.cuda.set_device(local)
-    layer = Layer(local, args.workload, seed_off=rank)
+    layer = Layer(local, args.workload, seed_off=rank, ablation=args.ablation)
     ctx = layer.ctx
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
@@ -450,6 +461,7 @@ def run_ours(args):
                               "ff": L_FF, "conv": layer.Lconv},
                    "params": "P16 (q0 60b + 23x40b, K=6 x 60b special, alpha=8)",
                    "parallelism": "replicas: one independent layer per GPU" if ws > 1 else "1 GPU",
+                   "ablation": args.ablation,
                    "l2": "no flush: per-step working set (~%d GB of plaintext diagonals) >> 126 MB L2" % round(
                        (layer.w_qkv.numel() + sum(getattr(layer, w).numel() for w in ("w_o", "w_1", "w_2") if hasattr(layer, w))) * 8 / 1e9)},
         "key_switches_per_s": round(ks_total / (ms_step * 1e-3), 1),

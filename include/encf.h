@@ -240,6 +240,15 @@ encf_status encf_field2ring_local(encf_ctx* ctx, const uint64_t* share, int32_t 
 /* Alg 4 step 4: P1 outputs <m> = <c> + [[t^]]_1 (c from P0, NTT form; share: plaintext over Q_L in
  * either domain). */
 encf_status encf_import_m2c(encf_ctx* ctx, const encf_ct* c, const encf_pt* share, encf_ct* out, void* stream);
+/* ------------------------------------------------------------------------------------------ w/o-SCP ablation */
+/* Halevi-Shoup rotation-mask-accumulate repack (App. G), used only by the w/o-SCP ablation:
+ * out[i] = sum_{k < log2 m} Rot(x[i], 2^k) (.) m_k with m_k = rows [round(k m / log2 m), round((k+1) m / log2 m))
+ * of every m-slot segment (DESIGN.md R-RMA), i.e. slot s m + j receives slot s m + j + 2^{k(j)}.  One hoisted
+ * ModUp per input, one fused masked inner-product launch, one merged ModDown + rescale: out at level L - 1.
+ * Keys: left rotations by 2^k, k < log2 m.  Errors: ARG, PLAN_SHAPE (m not a power of two), LEVEL_EXHAUSTED,
+ * LEVEL_MISMATCH, MISSING_KEY. */
+encf_status encf_repack_rma(encf_ctx* ctx, const encf_keys* keys, const encf_ct* x, int32_t n, int32_t m, encf_ct* out,
+                            void* stream);
 /* ------------------------------------------------------------------------------------------ GELU pre-evaluation */
 /* Alg 5 steps 1-3, the CKKS half of secure GELU: for each complex x[i] = x^(0) + i x^(1) (level L >= 4,
  * all inputs at one level and scale): x^(0) = (x + conj x)/2, x^(1) = (x - conj x)/(2i) (the 1/2 as scale x 2,

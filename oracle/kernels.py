@@ -866,3 +866,37 @@ def gelu_preeval(ev, x, coef):
         F0.append(add_const(ev, ev.add(ev.sub(base, B), D0), e))
         F1.append(add_const(ev, ev.add(ev.add(base, B), D1), e))
     return ev.add(F0[0], ev.mul_i(F0[1])), ev.add(F1[0], ev.mul_i(F1[1]))
+
+
+# ====================================================================================== w/o-SCP ablation (NEXT row 3)
+def rma_bands(m):
+    """Row bands of the RMA masks: log2 m contiguous bands of the m rows of every segment; band k is moved
+    by the rotation 2^k (reading R-RMA: App. G gives only the RMA form)."""
+    K = int(np.log2(m))
+    edges = [round(k * m / K) for k in range(K + 1)]
+    return [(edges[k], edges[k + 1]) for k in range(K)]
+
+
+def repack_rma(ev, x, m):
+    """Halevi-Shoup rotation-mask-accumulate repack of the w/o-SCP ablation (App. G):
+        Repack(v) = sum_{k < log2 m} Rot(v, 2^k) (.) m_k
+    with m_k = the rows of band k (rma_bands) in every segment, i.e. out[s m + j] = v[s m + j + 2^{k(j)}].
+    log2 m rotations from ONE hoisted ModUp, kept in the extended basis, masked and summed there, ONE merged
+    ModDown + rescale (R-LAZY)."""
+    K = int(np.log2(m))
+    nseg = ev.P.n // m
+    rots = ev.rot_hoisted_ext(x, [1 << k for k in range(K)])
+    masks = [ev.mask_ext((r0, r1, 0, 1, nseg), x.L, m) for (r0, r1) in rma_bands(m)]
+    return ev.moddown_rescale(ev.ext_masked_sum(rots, masks, x.scale * ev.mask_scale(x.L)))
+
+
+def repack_rma_reference(v, m):
+    """The slot map the RMA repack realises (brute force): out[i] = v[(i + 2^{k(i mod m)}) mod n]."""
+    n = len(v)
+    out = np.empty_like(v)
+    band = np.empty(m, dtype=int)
+    for k, (r0, r1) in enumerate(rma_bands(m)):
+        band[r0:r1] = k
+    for i in range(n):
+        out[i] = v[(i + (1 << band[i % m])) % n]
+    return out

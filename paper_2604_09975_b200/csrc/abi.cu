@@ -658,6 +658,23 @@ encf_status encf_ct_ct_attn_value(encf_ctx* c, const encf_keys* k, const encf_at
     });
 }
 
+// ------------------------------------------------------------------------------------ w/o-SCP ablation repack
+encf_status encf_repack_rma(encf_ctx* c, const encf_keys* k, const encf_ct* x, int32_t n, int32_t m, encf_ct* out, void* stream) {
+    return guard([&] {
+        need(c && k && x && out && n > 0, ENCF_ERR_ARG, "repack_rma: null argument");
+        EV_BEGIN(k);
+        std::vector<DCt> xs;
+        for (int i = 0; i < n; i++) xs.push_back(view(&x[i]));
+        std::vector<DCt> ys;
+        repack_rma_run(ev, xs, m, ys);
+        for (int i = 0; i < n; i++) {
+            DCt o = outview(&out[i], ys[i].L, 2);
+            ev.copy(ys[i], o);
+            writeback(&out[i], o);
+        }
+    });
+}
+
 // ------------------------------------------------------------------------------------ GELU pre-evaluation
 encf_status encf_gelu_preeval(encf_ctx* c, const encf_keys* k, const encf_ct* x, int32_t n, const double* coef, encf_ct* f0,
                               encf_ct* f1, void* stream) {

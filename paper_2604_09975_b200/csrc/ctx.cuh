@@ -191,6 +191,7 @@ struct RotSumBatch {               // hoisted rotation sums (R-ROUTE): per reque
     u64* acc[KS_BATCH];
     const u64* key[RS_TERMS];
     uint32_t g[RS_TERMS];
+    const u64* mask[RS_TERMS];     // ks_rma: per-term extended-basis mask (NTT form)
 };
 struct SumDev { const u64* ct; const u64* mask; };
 struct BcastArgs {                 // value-kernel broadcast MAC (C8 step 4)
@@ -245,6 +246,7 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
                       const int* us, const int* qs, int batch, double scale, int level, u64* out, cudaStream_t s,
                       const double* dWim = nullptr, int real_input = 0);
 void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
+void k_ks_rma(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
 constexpr int PSI_BATCH = 128;
 struct PsiBatch {                  // masked shift Psi^t without ModDown: h (.) rot_ext(x, g0) + u (.) rot_ext(x, g1)
     const u64* ext[PSI_BATCH];

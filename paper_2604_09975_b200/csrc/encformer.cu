@@ -564,3 +564,45 @@ void gelu_preeval_run(Ev& ev, const std::vector<DCt>& xs, const double coef[5], 
         ev.add(F1[i], u, f1[i]);
     }
 }
+
+// ====================================================================================== w/o-SCP ablation (App. G)
+// Halevi-Shoup RMA repack (oracle kernels.repack_rma): ONE hoisted ModUp per input, the log2 m shifts 2^k as
+// extended-basis inner products masked by band k (rows [r_k, r_{k+1}) of every segment) and summed in ONE fused
+// launch (ks_rma_kernel), then ONE merged ModDown + rescale.
+void repack_rma_run(Ev& ev, const std::vector<DCt>& xs, int m, std::vector<DCt>& outs) {
+    const int n = (int)xs.size(), L = xs[0].L, N = ev.c.N;
+    int K = 0;
+    while ((1 << (K + 1)) <= m) K++;
+    if ((1 << K) != m || K < 1) throw EncfError(ENCF_ERR_PLAN_SHAPE, "rma: m must be a power of two");
+    if (L < 2) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "rma: needs one level");
+    std::vector<const u64*> c1;
+    for (auto& x : xs) {
+        if (x.L != L || x.ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rma: mixed inputs");
+        c1.push_back(x.comp(1, N));
+    }
+    u64* ext = ev.modup_many(c1, {}, L);
+    std::vector<DCt> acc = ev.alloc_many_ext(n, L);
+    const int key_nl = ev.keys->max_level + ev.c.K;
+    const int nseg = ev.c.N / 2 / m;
+    RotSumBatch B;
+    for (int k = 0; k < K; k++) {
+        const int r0 = (int)std::nearbyint((double)k * m / K), r1 = (int)std::nearbyint((double)(k + 1) * m / K);   // = Python round
+        B.g[k] = ev.galois_rot(1L << k);
+        B.key[k] = ev.key_for(B.g[k], L);
+        B.mask[k] = ev.mask_ext(m, r0, r1, 0, 1, nseg, L);
+    }
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        for (int i = 0; i < cnt; i++) {
+            B.ext[i] = ext + ev.ext_stride(L) * (r0 + i);
+            B.c0[i] = xs[r0 + i].comp(0, N);
+            B.c1[i] = xs[r0 + i].comp(1, N);
+            B.acc[i] = acc[r0 + i].d;
+            acc[r0 + i].scale = xs[r0 + i].scale * ev.mask_scale(L);
+        }
+        k_ks_rma(ev.c, B, cnt, K, ev.c.dnum(L), L, key_nl, ev.s);
+        ev.c.st_ks += (uint64_t)cnt * K;
+    }
+    outs = ev.alloc_many(n, L - 1);
+    ev.moddown_rescale_many(acc, outs);
+}

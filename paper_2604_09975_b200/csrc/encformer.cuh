@@ -29,4 +29,5 @@ void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S
 void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs,
                std::vector<DCt>& outs);
 int l_conv_rule(const encf_ctx& c, int ell, int sigma, double scale, double B_max);
+void repack_rma_run(Ev& ev, const std::vector<DCt>& xs, int m, std::vector<DCt>& outs);
 void gelu_preeval_run(Ev& ev, const std::vector<DCt>& xs, const double coef[5], std::vector<DCt>& f0, std::vector<DCt>& f1);

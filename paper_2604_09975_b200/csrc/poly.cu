@@ -917,6 +917,60 @@ __global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl
         make_ulonglong2(barrett128(A10, q, mc.rhi, mc.rlo), barrett128(A11, q, mc.rhi, mc.rlo));
 }
 
+// Rotation-mask-accumulate (Halevi-Shoup repack of the w/o-SCP ablation, oracle kernels.repack_rma) without
+// ModDown: acc_c = sum_i mask_i (.) ( sum_j sigma_{g_i}(ext_j) key_i[j][c] + [c == 0] P sigma_{g_i}(c0) ).
+__global__ void __launch_bounds__(TB) ks_rma_kernel(RotSumBatch B, int nterms, int dnum, int nl, int L, int key_nl,
+                                                    KeyLimb klm, LimbMap em, int N, int logN,
+                                                    const ModConst* __restrict__ mod, const u64* __restrict__ pl,
+                                                    const u64* __restrict__ pl_sh) {
+    const int r = blockIdx.x, e = blockIdx.z;
+    const int kp = blockIdx.y * blockDim.x + threadIdx.x;
+    if (2 * kp >= N) return;
+    const int k = 2 * kp;
+    const ModConst mc = mod[em.mod[e]];
+    const u64 q = mc.q;
+    const int kle = klm.kl[e];
+    const u64* __restrict__ ext = B.ext[r];
+    const bool qlimb = e < L;
+    const uint32_t mask2n = 2 * N - 1;
+    const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+    u64 s00 = 0, s01 = 0, s10 = 0, s11 = 0;
+    for (int i = 0; i < nterms; i++) {
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * B.g[i]) & mask2n);
+        const int src = brv((int)((e2 - 1) >> 1), logN);
+        const int base = src & ~1, swap = src & 1;
+        const u64* key = B.key[i];
+        U128 a0{0, 0}, b0{0, 0}, a1{0, 0}, b1{0, 0};
+        for (int j = 0; j < dnum; j++) {
+            ulonglong2 x = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base));
+            if (swap) { u64 t = x.x; x.x = x.y; x.y = t; }
+            const u64* kj = key + (size_t)j * 2 * key_nl * N;
+            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)kle * N + k));
+            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + k));
+            mac128(a0, x.x, k0.x);
+            mac128(b0, x.y, k0.y);
+            mac128(a1, x.x, k1.x);
+            mac128(b1, x.y, k1.y);
+        }
+        u64 t00 = redc128(a0, q, mc.qinv), t01 = redc128(b0, q, mc.qinv);
+        const u64 t10 = redc128(a1, q, mc.qinv), t11 = redc128(b1, q, mc.qinv);
+        if (qlimb) {
+            ulonglong2 y = __ldg((const ulonglong2*)(B.c0[r] + (size_t)e * N + base));
+            if (swap) { u64 t = y.x; y.x = y.y; y.y = t; }
+            t00 = add_mod(t00, mul_shoup(y.x, pl[e], pl_sh[e], q), q);
+            t01 = add_mod(t01, mul_shoup(y.y, pl[e], pl_sh[e], q), q);
+        }
+        const ulonglong2 m = __ldg((const ulonglong2*)(B.mask[i] + (size_t)e * N + k));
+        s00 = add_mod(s00, mulmod_barrett(t00, m.x, q, mc.rhi, mc.rlo), q);
+        s01 = add_mod(s01, mulmod_barrett(t01, m.y, q, mc.rhi, mc.rlo), q);
+        s10 = add_mod(s10, mulmod_barrett(t10, m.x, q, mc.rhi, mc.rlo), q);
+        s11 = add_mod(s11, mulmod_barrett(t11, m.y, q, mc.rhi, mc.rlo), q);
+    }
+    u64* acc = B.acc[r];
+    *(ulonglong2*)(acc + (size_t)e * N + k) = make_ulonglong2(s00, s01);
+    *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) = make_ulonglong2(s10, s11);
+}
+
 // out_c = (b_c - y_c) P^{-1} + add_c for request r = blockIdx.z / 2, component c = blockIdx.z % 2.
 // b: acc base [r][2][nl][N]; y: [r][2][L][N].
 __global__ void moddown_finish_batch_kernel(const u64* __restrict__ acc, const u64* __restrict__ y, OutBatch O, int level,
@@ -1104,6 +1158,23 @@ void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
     c.st_ptmul += 2 * (uint64_t)nreq;
+    CUDA_TRY(cudaGetLastError());
+}
+
+void k_ks_rma(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s) {
+    if (nterms > RS_TERMS) throw EncfError(ENCF_ERR_ARG, "rma: too many terms");
+    const int nl = L + c.K;
+    KeyLimb kl;
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    const LimbMap em = c.extmap(L);
+    dim3 grid(nreq, (c.N / 2 + TB - 1) / TB, nl);
+    int slot;
+    c.prof_begin("ks_rma", s, 0, slot);
+    ks_rma_kernel<<<grid, TB, 0, s>>>(B, nterms, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod, c.moddown[L].d_pl,
+                                      c.moddown[L].d_pl_sh);
+    c.prof_end(slot, s);
+    c.st_launch++;
+    c.st_ptmul += (uint64_t)nreq * nterms;
     CUDA_TRY(cudaGetLastError());
 }
 

@@ -96,6 +96,7 @@ _SIG = {
     "encf_field2ring_local": [_p, _p, _i32, _p, _p],
     "encf_import_m2c": [_p, ctypes.POINTER(CT), ctypes.POINTER(PT), ctypes.POINTER(CT), _p],
     "encf_gelu_preeval": [_p, _p, _p, ctypes.c_int32, _p, _p, _p, _p],
+    "encf_repack_rma": [_p, _p, _p, ctypes.c_int32, ctypes.c_int32, _p, _p],
     "encf_profile_enable": [_p, ctypes.c_char_p],
     "encf_profile_read": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
     "encf_profile_peek": [_p, ctypes.c_char_p, ctypes.POINTER(_f64), ctypes.POINTER(_u64), ctypes.POINTER(_u64)],
@@ -403,6 +404,15 @@ class Context:
         c = out._c()
         _chk(_lib.encf_import_m2c(self.h, ctypes.byref(ct._c()), ctypes.byref(share_pt._p()), ctypes.byref(c), _stream()), "import_m2c")
         return out._update(c)
+
+    def repack_rma(self, keys, xs, m):
+        """w/o-SCP ablation: Halevi-Shoup RMA repack of each ciphertext (one level consumed)."""
+        outs = [self.empty_ct(x.n_limbs - 1) for x in xs]
+        xa = (CT * len(xs))(*[x._c() for x in xs])
+        oa = (CT * len(xs))(*[o._c() for o in outs])
+        _chk(_lib.encf_repack_rma(self.h, keys.h, ctypes.cast(xa, _p), len(xs), int(m), ctypes.cast(oa, _p), _stream()),
+             "repack_rma")
+        return [o._update(oa[i]) for i, o in enumerate(outs)]
 
     def gelu_preeval(self, keys, xs, coef):
         """Alg 5 steps 1-3 on complex ciphertexts xs (one level and scale): returns (F0^C list, F1^C list) at L - 3."""

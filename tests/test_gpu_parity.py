@@ -394,3 +394,23 @@ def test_gelu_preeval_bit_exact(c13, keys13):
         z = O.decode(P13, O.decrypt(P13, ok, O.Ct(c13.to_host(f1[i]), f1[i].scale)))
         F1 = lambda v: a * v ** 4 + b * v ** 3 + c * v ** 2 + (0.5 + d) * v + e
         assert np.abs(z - (F1(x0) + 1j * F1(x1))).max() < 1e-5
+
+
+# ------------------------------------------------------------------ w/o-SCP ablation: RMA repack
+def test_repack_rma_bit_exact(c13, keys13):
+    """encf_repack_rma (App. G) on two ciphertexts at L = 5, m = 16: every limb equals the oracle's."""
+    ok, gk = keys13
+    g = synth.rng(56)
+    xs, refs = [], []
+    for i in range(2):
+        v = g.uniform(-1, 1, P13.n) + 1j * g.uniform(-1, 1, P13.n)
+        x = O.encrypt_sk(P13, ok, O.encode(P13, v, 2.0 ** 40, 5), 600 + i)
+        xs.append(x)
+        ev = K.Ev(P13, ok, 16)
+        refs.append(K.repack_rma(ev, x, 16))
+    c13.mask_clear()
+    install_masks(c13, ev)
+    got = c13.repack_rma(gk, [dev_ct(c13, x) for x in xs], 16)
+    for a, b in zip(got, refs):
+        assert_ct_equal(c13, a, b, "RMA repack")
+    c13.mask_clear()

@@ -393,3 +393,19 @@ def test_gelu_preeval_decrypts_to_candidates(keys13):
     z1 = O.decode(P13, O.decrypt(P13, ok, f1))
     assert np.abs(z0 - (F0(x0) + 1j * F0(x1))).max() < 1e-5
     assert np.abs(z1 - (F1(x0) + 1j * F1(x1))).max() < 1e-5
+
+
+# ------------------------------------------------------------------ w/o-SCP ablation: Halevi-Shoup RMA repack
+def test_repack_rma_matches_slot_map(keys13):
+    """App. G RMA repack at N = 2^13, m = 16: log2 m = 4 rotations, 4 masked products, one merged ModDown +
+    rescale; decrypts to the brute-force slot map out[i] = v[i + 2^{k(i mod m)}] within 2^-20."""
+    ok = keys13
+    g = synth.rng(55)
+    v = g.uniform(-1, 1, P13.n) + 1j * g.uniform(-1, 1, P13.n)
+    x = O.encrypt_sk(P13, ok, O.encode(P13, v, 2.0 ** 40, 5), 66)
+    ev = K.Ev(P13, ok, 16)
+    y = K.repack_rma(ev, x, 16)
+    assert y.L == 4 and ev.ledger["rot"] == 4 and ev.ledger["ptmul"] == 4
+    got = O.decode(P13, O.decrypt(P13, ok, y))
+    ref = K.repack_rma_reference(v, 16)
+    assert np.abs(got - ref).max() / np.abs(ref).max() < TOL
