@@ -1,3 +1,4 @@
+#include <atomic>
 // abi.cu -- extern "C" entry points of libencf (include/encf.h).  Host-side validation happens before
 // any launch; C++ exceptions never cross the boundary.
 #include <cstring>
@@ -108,6 +109,8 @@ encf_status encf_keygen(encf_ctx* c, uint64_t seed, const uint32_t* galois, int3
         cudaStream_t s = S(stream);
         const int N = c->N, K = c->K, ML = max_level, nl = ML + K;
         encf_keys* k = new encf_keys();
+        static std::atomic<uint64_t> next_id{1};
+        k->id = next_id++;
         k->max_level = ML;
         k->dnum = c->dnum(ML);
         k->device = c->device;
@@ -434,6 +437,8 @@ encf_status encf_mask_clear(encf_ctx* c) {
     std::lock_guard<std::mutex> lk(c->mu);
     for (auto& kv : c->masks) cudaFree(kv.second);
     c->masks.clear();
+    for (auto& kv : c->kmasks) cudaFree(kv.second);
+    c->kmasks.clear();
     return ENCF_OK;
 }
 

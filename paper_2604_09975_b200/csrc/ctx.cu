@@ -305,6 +305,7 @@ encf_status ctx_destroy_impl(encf_ctx* c) {
     cudaSetDevice(c->device);
     cudaDeviceSynchronize();
     for (auto& kv : c->masks) cudaFree(kv.second);
+    for (auto& kv : c->kmasks) cudaFree(kv.second);
     for (void* p : c->allocations) cudaFree(p);
     for (void* p : c->pinned) cudaFreeHost(p);
     delete c;

@@ -79,6 +79,17 @@ struct MaskKey {
     }
 };
 
+struct KMKey {   // pre-masked key cache entry: (keys object, Galois element, mask descriptor)
+    uint64_t keys_id;
+    uint32_t g;
+    MaskKey mk;
+    bool operator<(const KMKey& o) const {
+        if (keys_id != o.keys_id) return keys_id < o.keys_id;
+        if (g != o.g) return g < o.g;
+        return mk < o.mk;
+    }
+};
+
 struct encf_ctx {
     int device = 0;
     int N = 0, logN = 0, L = 0, K = 0, alpha = 0;
@@ -104,6 +115,7 @@ struct encf_ctx {
     std::vector<void*> allocations;
     std::mutex mu;
     std::map<MaskKey, u64*> masks;      // NTT-form mask plaintexts [level][N]
+    std::map<KMKey, u64*> kmasks;       // pre-masked keys (key (.) mask, Montgomery) + P (.) mask, per (keys, g, mask)
     std::vector<int> rot_group;         // 5^j mod 2N (host, for encode)
     int* d_rot_group = nullptr;
     // live kernel timing (encf_profile_*): CUDA events recorded around selected launches
@@ -141,6 +153,7 @@ struct encf_ctx {
 
 // key material (device, NTT form)
 struct encf_keys {
+    uint64_t id = 0;                    // unique per keygen (pre-masked key cache)
     int max_level = 0;
     int dnum = 0;
     u64* sk = nullptr;                  // [max_level + K][N]
@@ -257,6 +270,9 @@ struct PsiBatch {                  // masked shift Psi^t without ModDown: h (.) 
     uint32_t g[PSI_BATCH][2];
 };
 void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key_nl, cudaStream_t s);
+// pre-masked key of (key of g, ext mask at level L): km [dnum][2][L+K][N] = key (.) m (Montgomery form kept),
+// pm [L][N] = (P R mod q) (.) m; one allocation km | pm
+void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnum, int L, u64* out, cudaStream_t s);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s);
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,

@@ -182,10 +182,9 @@ void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::
             B.out[k] = o.d;
             B.g[k][0] = ev.galois_rot(q.t);
             B.g[k][1] = ev.galois_rot(q.t - m);
-            B.key[k][0] = ev.key_for(B.g[k][0], L);
-            B.key[k][1] = ev.key_for(B.g[k][1], L);
-            B.mask[k][0] = ev.mask_ext(m, 0, m - q.t, seg0, 1, nseg, L);
-            B.mask[k][1] = ev.mask_ext(m, m - q.t, m, seg0, 1, nseg, L);
+            // pre-masked keys: key (.) h_t and key (.) u_t (cached), and P (.) mask for the c0 lift
+            B.key[k][0] = ev.keymask(B.g[k][0], m, 0, m - q.t, seg0, 1, nseg, L, &B.mask[k][0]);
+            B.key[k][1] = ev.keymask(B.g[k][1], m, m - q.t, m, seg0, 1, nseg, L, &B.mask[k][1]);
         }
         k_ks_psi(ev.c, B, cnt, dn, L, key_nl, ev.s);
         ev.c.st_ks += 2 * (uint64_t)cnt;      // two key switches whose ModDown is merged into the rescale

@@ -638,3 +638,23 @@ const u64* Ev::mask(int m, int r0, int r1, int s0, int ss, int scount, int level
     c.masks[key] = pt;
     return pt;
 }
+
+const u64* Ev::keymask(uint32_t g, int m, int r0, int r1, int s0, int ss, int sc, int L, const u64** pm) {
+    const int nl = L + c.K, dn = c.dnum(L);
+    const size_t kmw = (size_t)dn * 2 * nl * c.N;
+    KMKey key{keys->id, g, MaskKey{m, r0, r1, s0, ss, sc, L, 1}};
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.kmasks.find(key);
+        if (it != c.kmasks.end()) { *pm = it->second + kmw; return it->second; }
+    }
+    const u64* mk = mask_ext(m, r0, r1, s0, ss, sc, L);
+    const u64* kk = key_for(g, L);
+    u64* buf = nullptr;
+    CUDA_TRY(cudaMalloc(&buf, (kmw + (size_t)nl * c.N) * 8));
+    k_keymask(c, kk, keys->max_level + c.K, mk, dn, L, buf, s);
+    std::lock_guard<std::mutex> lk(c.mu);
+    c.kmasks[key] = buf;
+    *pm = buf + kmw;
+    return buf;
+}

@@ -98,6 +98,9 @@ struct Ev {
     const u64* mask(int m, int r0, int r1, int s0, int ss, int sc, int level, int ext = 0);
     const u64* mask_ext(int m, int r0, int r1, int s0, int ss, int sc, int level) { return mask(m, r0, r1, s0, ss, sc, level, 1); }
     double mask_scale(int level) const { return (double)c.mods[level - 1]; }
+    // cached pre-masked key of Galois element g with the ext mask (m, r0, r1, s0, ss, sc) at level L:
+    // returns km ([dnum][2][L+K][N]); *pm = km + dnum*2*(L+K)*N ([L][N], P R (.) mask)
+    const u64* keymask(uint32_t g, int m, int r0, int r1, int s0, int ss, int sc, int L, const u64** pm);
     template <class T>
     T* upload(const std::vector<T>& v) {
         // eager: pageable copy (staged by the driver, so v may die at once); under CUDA-graph capture the

@@ -859,23 +859,22 @@ __global__ void __launch_bounds__(TB) ks_rotsum_kernel(RotSumBatch B, int nterms
 // Masked shift Psi^t in the extended basis (DESIGN.md R-LAZY), fused: for request r = blockIdx.x, pair tile
 // blockIdx.y, extended limb e = blockIdx.z,
 //   out_c = sum_{i<2} mask_i (.) ( sum_j sigma_{g_i}(ext_j) key_i[j][c] + [c == 0] P sigma_{g_i}(c0) )
-// = h_t (.) rot_ext(x, t) + u_t (.) rot_ext(x, t - m) without materialising the two rotations (replaces two
-// inner products, the c0 gathers/lifts and the masked sum).  Keys in Montgomery form (REDC per term); the
-// mask products are summed in 128 bits and Barrett-reduced once.
-__global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl, int L, int key_nl, KeyLimb klm,
-                                                    LimbMap em, int N, int logN, const ModConst* __restrict__ mod,
-                                                    const u64* __restrict__ pl, const u64* __restrict__ pl_sh) {
+// = h_t (.) rot_ext(x, t) + u_t (.) rot_ext(x, t - m) without materialising the two rotations.  The masks are
+// folded into PRE-MASKED keys (B.key[r][i] = key_i (.) mask_i, Montgomery form, cached per (keys, g, mask)) and
+// B.mask[r][i] = (P R) (.) mask_i, so both terms, all digits and the c0 lift accumulate in ONE 128-bit sum per
+// output (<= 2 dnum + 2 <= 8 products, 8 q < 2^64) reduced by ONE Montgomery REDC.
+__global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl, int L, LimbMap em, int N, int logN,
+                                                    const ModConst* __restrict__ mod) {
     const int r = blockIdx.x, e = blockIdx.z;
     const int kp = blockIdx.y * blockDim.x + threadIdx.x;
     if (2 * kp >= N) return;
     const int k = 2 * kp;
     const ModConst mc = mod[em.mod[e]];
     const u64 q = mc.q;
-    const int kle = klm.kl[e];
     const u64* __restrict__ ext = B.ext[r];
     const bool qlimb = e < L;
     const uint32_t mask2n = 2 * N - 1;
-    U128 A00{0, 0}, A01{0, 0}, A10{0, 0}, A11{0, 0};
+    U128 A0{0, 0}, B0{0, 0}, A1{0, 0}, B1{0, 0};
     const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
 #pragma unroll
     for (int i = 0; i < 2; i++) {
@@ -883,38 +882,51 @@ __global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl
         const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
         const int src = brv((int)((e2 - 1) >> 1), logN);
         const int base = src & ~1, swap = src & 1;
-        const u64* key = B.key[r][i];
-        U128 a0{0, 0}, b0{0, 0}, a1{0, 0}, b1{0, 0};
+        const u64* km = B.key[r][i];
         for (int j = 0; j < dnum; j++) {
             ulonglong2 x = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base));
             if (swap) { u64 t = x.x; x.x = x.y; x.y = t; }
-            const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)kle * N + k));
-            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + k));
-            mac128(a0, x.x, k0.x);
-            mac128(b0, x.y, k0.y);
-            mac128(a1, x.x, k1.x);
-            mac128(b1, x.y, k1.y);
+            const u64* kj = km + (size_t)j * 2 * nl * N;
+            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)e * N + k));
+            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)nl + e) * N + k));
+            mac128(A0, x.x, k0.x);
+            mac128(B0, x.y, k0.y);
+            mac128(A1, x.x, k1.x);
+            mac128(B1, x.y, k1.y);
         }
-        u64 t00 = redc128(a0, q, mc.qinv), t01 = redc128(b0, q, mc.qinv);
-        const u64 t10 = redc128(a1, q, mc.qinv), t11 = redc128(b1, q, mc.qinv);
         if (qlimb) {
             ulonglong2 y = __ldg((const ulonglong2*)(B.c0[r] + (size_t)e * N + base));
             if (swap) { u64 t = y.x; y.x = y.y; y.y = t; }
-            t00 = add_mod(t00, mul_shoup(y.x, pl[e], pl_sh[e], q), q);
-            t01 = add_mod(t01, mul_shoup(y.y, pl[e], pl_sh[e], q), q);
+            const ulonglong2 pm = __ldg((const ulonglong2*)(B.mask[r][i] + (size_t)e * N + k));
+            mac128(A0, y.x, pm.x);
+            mac128(B0, y.y, pm.y);
         }
-        const ulonglong2 m = __ldg((const ulonglong2*)(B.mask[r][i] + (size_t)e * N + k));
-        mac128(A00, t00, m.x);
-        mac128(A01, t01, m.y);
-        mac128(A10, t10, m.x);
-        mac128(A11, t11, m.y);
     }
     u64* out = B.out[r];
-    *(ulonglong2*)(out + (size_t)e * N + k) =
-        make_ulonglong2(barrett128(A00, q, mc.rhi, mc.rlo), barrett128(A01, q, mc.rhi, mc.rlo));
-    *(ulonglong2*)(out + ((size_t)nl + e) * N + k) =
-        make_ulonglong2(barrett128(A10, q, mc.rhi, mc.rlo), barrett128(A11, q, mc.rhi, mc.rlo));
+    *(ulonglong2*)(out + (size_t)e * N + k) = make_ulonglong2(redc128(A0, q, mc.qinv), redc128(B0, q, mc.qinv));
+    *(ulonglong2*)(out + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(A1, q, mc.qinv), redc128(B1, q, mc.qinv));
+}
+
+// km[j][c][e][k] = key[j][c][kl(e)][k] (.) mask[e][k] mod q_e (the key's Montgomery factor is kept);
+// pm[e][k] = PR_e (.) mask[e][k] mod q_e for e < L (PR_e = P R mod q_e).
+__global__ void keymask_kernel(const u64* __restrict__ key, int key_nl, const u64* __restrict__ mask, int dnum, int L, int nl,
+                               KeyLimb klm, LimbMap em, const u64* __restrict__ pr, u64* __restrict__ out, int N,
+                               const ModConst* __restrict__ mod) {
+    const size_t total = (size_t)(dnum * 2 + 1) * nl * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % N);
+        const size_t row = i / N;
+        const int e = (int)(row % nl), jc = (int)(row / nl);
+        const ModConst mc = mod[em.mod[e]];
+        const u64 m = mask[(size_t)e * N + k];
+        if (jc < dnum * 2) {
+            const int j = jc >> 1, c = jc & 1;
+            const u64 kv = key[((size_t)j * 2 + c) * key_nl * N + (size_t)klm.kl[e] * N + k];
+            out[i] = mulmod_barrett(kv, m, mc.q, mc.rhi, mc.rlo);
+        } else if (e < L) {
+            out[i] = mulmod_barrett(pr[e], m, mc.q, mc.rhi, mc.rlo);
+        }
+    }
 }
 
 // Rotation-mask-accumulate (Halevi-Shoup repack of the w/o-SCP ablation, oracle kernels.repack_rma) without
@@ -1146,18 +1158,40 @@ void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dn
 
 void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key_nl, cudaStream_t s) {
     const int nl = L + c.K;
-    KeyLimb kl;
-    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    if ((unsigned __int128)(2 * dnum + 2) * c.max_mod >= ((unsigned __int128)1 << 64))
+        throw EncfError(ENCF_ERR_ARG, "ks_psi: too many products for one Montgomery reduction");
     const LimbMap em = c.extmap(L);
     dim3 grid(nreq, (c.N / 2 + TB - 1) / TB, nl);
-    const uint64_t bytes = (uint64_t)nreq * (2 * dnum * nl + 2 * 2 * dnum * nl + 2 * L + 2 * nl + 2 * nl) * c.N * 8;
+    const uint64_t bytes = (uint64_t)nreq * (2 * dnum * nl + 2 * 2 * dnum * nl + 2 * L + 2 * L + 2 * nl) * c.N * 8;
     int slot;
     c.prof_begin("ks_psi", s, bytes, slot);
-    ks_psi_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod, c.moddown[L].d_pl,
-                                      c.moddown[L].d_pl_sh);
+    ks_psi_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
     c.st_ptmul += 2 * (uint64_t)nreq;
+    (void)key_nl;
+    CUDA_TRY(cudaGetLastError());
+}
+
+void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnum, int L, u64* out, cudaStream_t s) {
+    const int nl = L + c.K;
+    KeyLimb kl;
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    const LimbMap em = c.extmap(L);
+    std::vector<u64> pr(L);
+    for (int i = 0; i < L; i++) {
+        const u64 q = c.mods[i];
+        u64 P = 1;
+        for (int kk = 0; kk < c.K; kk++) P = h_mulmod(P, c.mods[c.L + kk] % q, q);
+        pr[i] = h_mulmod(P, c.mont_R[i], q);
+    }
+    u64* dpr = nullptr;
+    CUDA_TRY(cudaMallocAsync((void**)&dpr, L * 8, s));
+    CUDA_TRY(cudaMemcpyAsync(dpr, pr.data(), L * 8, cudaMemcpyHostToDevice, s));
+    keymask_kernel<<<GRID((size_t)(dnum * 2 + 1) * nl * c.N), TB, 0, s>>>(key, key_nl, mask, dnum, L, nl, kl, em, dpr, out, c.N,
+                                                                        c.d_mod);
+    CUDA_TRY(cudaFreeAsync(dpr, s));
+    c.st_launch++;
     CUDA_TRY(cudaGetLastError());
 }
 
