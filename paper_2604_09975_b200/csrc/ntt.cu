@@ -37,6 +37,7 @@ struct NttArgs {
     const u64* epi_fsh;
     const u64* ninv;
     const u64* ninv_sh;
+    int apply_ninv;          // 0: inverse leaves the factor N (the consumer's base-conversion constants absorb N^{-1})
     int N, logN, s1, s2;
 };
 
@@ -285,13 +286,24 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
         sm_get_a<LT>(line, j, x);
         round_a<LT, true>(x, 0, 0, tw2, ops);
         if constexpr (std::is_same<T, u64>::value) {
-            const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
+            if (a.apply_ninv) {
+                const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
 #pragma unroll
-            for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], ni, nip, ops.q);
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], ni, nip, ops.q);
+            } else {
+#pragma unroll
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = x[k] >= ops.q ? x[k] - ops.q : x[k];   // GS outputs in [0, 2q)
+            }
         } else {
-            const double ni = a.fpc[4 * mi + 2], niq = a.fpc[4 * mi + 3];
+            if (a.apply_ninv) {
+                const double ni = a.fpc[4 * mi + 2], niq = a.fpc[4 * mi + 3];
 #pragma unroll
-            for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_mulmod(x[k], ni, niq, ops.q), ops.q);
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_mulmod(x[k], ni, niq, ops.q), ops.q);
+            } else {
+                const double qinv = a.fpc[4 * mi + 1];
+#pragma unroll
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_center(x[k], ops.q, qinv), ops.q);
+            }
         }
     }
 }
@@ -345,6 +357,44 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
         __syncthreads();
         const u64 qi = a.mod[mi].q;
         const int lgp = 31 - __clz(lines) - lgc;
+        if (a.epi_out) {
+            // fused ModDown / rescale finish: all E (src, add) loads of a thread in flight before the first use
+            const u64 f = a.epi_f[limb], fsh = a.epi_fsh[limb];
+            constexpr int HB = GG::E >= 8 ? 8 : GG::E;      // batches of 8 items: 16 loads in flight per thread
+#pragma unroll
+            for (int b0 = 0; b0 < GG::E; b0 += HB) {
+                u64 sv[HB], av[HB];
+#pragma unroll
+                for (int i2 = 0; i2 < HB; i2++) {
+                    const int e = threadIdx.x + (b0 + i2) * blockDim.x;
+                    const int ll = e >> LT;
+                    const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
+                    const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
+                    sv[i2] = a.epi_src[p][off];
+                    const u64* ad = a.epi_add[p];
+                    av[i2] = ad ? ad[off] : 0;
+                }
+#pragma unroll
+                for (int i2 = 0; i2 < HB; i2++) {
+                    const int e = threadIdx.x + (b0 + i2) * blockDim.x;
+                    const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
+                    u64 w;
+                    if constexpr (std::is_same<T, u64>::value) {
+                        const u64 q = ops.q, two_q = ops.two_q;
+                        w = v >= two_q ? v - two_q : v;
+                        w = w >= q ? w - q : w;
+                    } else {
+                        const double q = ops.q, qinv = a.fpc[4 * mi + 1];
+                        w = fp_canon(fp_center(v, q, qinv), q);
+                    }
+                    const int ll = e >> LT;
+                    const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
+                    const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
+                    a.epi_out[p][off] = add_mod(mul_shoup(sub_mod(sv[i2], w, qi), f, fsh, qi), av[i2], qi);
+                }
+            }
+            return;
+        }
         for (int e = threadIdx.x; e < tot; e += blockDim.x) {
             const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
             u64 w;
@@ -356,17 +406,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
                 const double q = ops.q, qinv = a.fpc[4 * mi + 1];
                 w = fp_canon(fp_center(v, q, qinv), q);
             }
-            const int ll = e >> LT;
-            if (a.epi_out) {
-                const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
-                const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
-                u64 r = mul_shoup(sub_mod(a.epi_src[p][off], w, qi), a.epi_f[limb], a.epi_fsh[limb], qi);
-                const u64* ad = a.epi_add[p];
-                if (ad) r = add_mod(r, ad[off], qi);
-                a.epi_out[p][off] = r;
-            } else {
-                line_ptr(ll)[e & (GG::T - 1)] = w;
-            }
+            line_ptr(e >> LT)[e & (GG::T - 1)] = w;
         }
     } else {
         u64 v[GG::E];   // all E loads in flight before the first use (tot = E * blockDim.x)
@@ -472,6 +512,7 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.fpmask = c.fpmask;
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
+    a.apply_ninv = 1;
     a.epi_src = nullptr;
     a.epi_out = nullptr;
     a.epi_add = nullptr;
@@ -511,9 +552,12 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
     CUDA_TRY(cudaGetLastError());
 }
 
-void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) {
+void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) { ntt_inverse_scaled(c, b, true, s); }
+
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, true);
+    a.apply_ninv = apply_ninv ? 1 : 0;
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
