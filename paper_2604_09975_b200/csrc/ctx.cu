@@ -165,7 +165,7 @@ static void build(encf_ctx& c, const encf_params* p) {
                 u64 qi = c.mods[t.lo + a];
                 u64 prod = 1;   // Q_j / q_i mod q_i
                 for (int b = 0; b < na; b++) if (b != a) prod = h_mulmod(prod, c.mods[t.lo + b] % qi, qi);
-                vf[a] = h_invmod(prod, qi);
+                vf[a] = h_mulmod(h_invmod(prod, qi), ninv[t.lo + a], qi);   // x N^{-1}: the iNTT in front skips it
                 vfs[a] = shoup_pre(vf[a], qi);
                 for (int k = 0; k < t.tgt.n; k++) {
                     u64 tq = c.mods[t.tgt.mod[k]];
@@ -184,7 +184,7 @@ static void build(encf_ctx& c, const encf_params* p) {
             u64 pk = c.mods[c.L + k];
             u64 prod = 1;
             for (int b = 0; b < c.K; b++) if (b != k) prod = h_mulmod(prod, c.mods[c.L + b] % pk, pk);
-            vf[k] = h_invmod(prod, pk);
+            vf[k] = h_mulmod(h_invmod(prod, pk), ninv[c.L + k], pk);      // x N^{-1} (iNTT without it)
             vfs[k] = shoup_pre(vf[k], pk);
             for (int i = 0; i < lev; i++) {
                 u64 qi = c.mods[i];
@@ -234,7 +234,8 @@ static void build(encf_ctx& c, const encf_params* p) {
             for (int a = 0; a < nb; a++) {
                 u64 ba = bp[a], prod = 1;
                 for (int b2 = 0; b2 < nb; b2++) if (b2 != a) prod = h_mulmod(prod, bp[b2] % ba, ba);
-                vf[a] = h_invmod(prod, ba); vfs[a] = shoup_pre(vf[a], ba);
+                const int mid = a == 0 ? lev - 1 : c.L + (a - 1);
+                vf[a] = h_mulmod(h_invmod(prod, ba), ninv[mid], ba); vfs[a] = shoup_pre(vf[a], ba);   // x N^{-1}
                 for (int t = 0; t < nt; t++) {
                     u64 qt = c.mods[t], pr = 1;
                     for (int b2 = 0; b2 < nb; b2++) if (b2 != a) pr = h_mulmod(pr, bp[b2] % qt, qt);

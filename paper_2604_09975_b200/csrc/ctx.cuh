@@ -224,6 +224,9 @@ void ntt_forward(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
 struct NttEpilogue { const u64* const* src; u64* const* out; const u64* const* add; const u64* f; const u64* fsh; };
 void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cudaStream_t s);
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
+// apply_ninv = false: returns N x (the coefficients); used only in front of the fast base conversions, whose
+// vfac constants (ModUp / ModDown / merged ModDown+rescale tables) carry the N^{-1}
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s);
 
 // ------------------------------------------------------------------------------------ launchers (poly.cu)
 void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s);

@@ -45,7 +45,7 @@ u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint
     }
     u64* dco = sc.get(Lw * n);
     CUDA_TRY(cudaMemcpyAsync(dco, dntt, Lw * n * 8, cudaMemcpyDeviceToDevice, s));
-    ntt_inverse(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, s);
+    ntt_inverse_scaled(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, false, s);   // N^{-1} folded into the ModUp vfac
     const size_t es = ext_stride(L);
     u64* ext = sc.get(es * n);
     LimbMap em = c.extmap(L);
@@ -100,7 +100,7 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
             O.out[i][0] = q.out0; O.out[i][1] = q.out1; O.add[i][0] = q.add0; O.add[i][1] = q.add1;
         }
         k_ks_inner_batch(c, B, n, dn, nl, key_nl, klm, s);
-        ntt_inverse(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);     // [b]_P -> coefficient form
+        ntt_inverse_scaled(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // [b]_P (x N; vfac has N^{-1})
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
                       pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh);                        // rounded: y = centred [b]_P
@@ -468,7 +468,7 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
     bm.n = K + 1;
     bm.mod[0] = (unsigned char)(L - 1);
     for (int k = 0; k < K; k++) bm.mod[1 + k] = (unsigned char)(c.L + k);
-    ntt_inverse(c, PolyBatch{x + (size_t)(L - 1) * N, (i64)nl * N, 2 * n, bm}, s);
+    ntt_inverse_scaled(c, PolyBatch{x + (size_t)(L - 1) * N, (i64)nl * N, 2 * n, bm}, false, s);   // vfac has N^{-1}
     const MDRTab& t = c.mdr[L];
     LimbMap qm = c.qmap(L - 1);
     std::vector<int> pos(L - 1);
@@ -505,7 +505,7 @@ void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     std::vector<int> pos(L);
     for (int i = 0; i < L; i++) pos[i] = i;
     const ModDownTab& md = c.moddown[L];
-    ntt_inverse(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, s);
+    ntt_inverse_scaled(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // vfac has N^{-1}
     u64* y = sc.get((size_t)n * 2 * L * N);
     k_bconv_batch(c, x + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N, pos.data(), 2 * n, s,
                   md.d_pmod, md.d_cfix, md.d_csh);
