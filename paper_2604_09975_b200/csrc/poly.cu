@@ -1055,10 +1055,28 @@ __global__ void __launch_bounds__(TB, 4) bconv_batch_kernel(const u64* __restric
             for (int i = 0; i < NIN; i++) fsum += umulhi(v[i] << (int)s_in[4 * NIN + i], s_in[3 * NIN + i]);
             r = (fsum + (1ull << 58)) >> 59;
         }
-        for (int t = 0; t < nout; t++) {
-            U128 acc{0, 0};
+        // 30-bit split (all moduli < 2^60, checked on the host): v = vh 2^30 + vl, w = wh 2^30 + wl, four
+        // 32x32->64 products accumulated carry-free in 64 bits (each < 2^60, <= 8 terms), combined once per output
+        uint32_t vh[NIN], vl[NIN];
 #pragma unroll
-            for (int i = 0; i < NIN; i++) mac128(acc, v[i], sw[i * nout + t]);
+        for (int i = 0; i < NIN; i++) { vh[i] = (uint32_t)(v[i] >> 30); vl[i] = (uint32_t)(v[i] & 0x3FFFFFFFu); }
+        for (int t = 0; t < nout; t++) {
+            u64 hh = 0, hl = 0, lh = 0, ll = 0;
+#pragma unroll
+            for (int i = 0; i < NIN; i++) {
+                const u64 w = sw[i * nout + t];
+                const uint32_t wh = (uint32_t)(w >> 30), wlo = (uint32_t)(w & 0x3FFFFFFFu);
+                hh += (u64)vh[i] * wh;
+                hl += (u64)vh[i] * wlo;
+                lh += (u64)vl[i] * wh;
+                ll += (u64)vl[i] * wlo;
+            }
+            U128 acc{ll, 0};
+            const u64 mid = hl + lh;                        // < 2^64
+            add128(acc, mid << 30);
+            acc.hi += mid >> 34;
+            add128(acc, hh << 60);
+            acc.hi += hh >> 4;
             if (corr) mac128(acc, r, s_corr[t]);
             out[s_pos[t] + k] = redc128(acc, s_q[t], s_qi[t]);   // wfac / corr in Montgomery form
         }
@@ -1225,6 +1243,7 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
                    const u64* cfix, const u64* csh) {
     if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
+    if (c.max_mod >= (1ull << 60) || im.n > 8) throw EncfError(ENCF_ERR_ARG, "bconv: the 30-bit split needs moduli < 2^60 and <= 8 inputs");
     {   // Montgomery bound of the lazy sum: sum_i q_i + (n_in + 1) <= 2^64 (then T < q_t 2^64)
         unsigned __int128 tot = (unsigned __int128)im.n + 1;
         for (int i = 0; i < im.n; i++) tot += c.mods[im.mod[i]];
