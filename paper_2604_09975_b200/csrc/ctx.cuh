@@ -226,7 +226,8 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
 // apply_ninv = false: returns N x (the coefficients); used only in front of the fast base conversions, whose
 // vfac constants (ModUp / ModDown / merged ModDown+rescale tables) carry the N^{-1}
-void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s);
+// src != nullptr: out-of-place (reads src with b's layout, writes b)
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src = nullptr);
 
 // ------------------------------------------------------------------------------------ launchers (poly.cu)
 void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s);

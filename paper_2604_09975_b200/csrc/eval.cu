@@ -44,8 +44,7 @@ u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint
         k_gather_copy(c, cb, cnt, dntt + Lw * i0, (i64)Lw, Lw, s);
     }
     u64* dco = sc.get(Lw * n);
-    CUDA_TRY(cudaMemcpyAsync(dco, dntt, Lw * n * 8, cudaMemcpyDeviceToDevice, s));
-    ntt_inverse_scaled(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, false, s);   // N^{-1} folded into the ModUp vfac
+    ntt_inverse_scaled(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, false, s, dntt);   // out of place; N^{-1} in the ModUp vfac
     const size_t es = ext_stride(L);
     u64* ext = sc.get(es * n);
     LimbMap em = c.extmap(L);

@@ -20,6 +20,7 @@ constexpr int kTileElems = 4096;   // 32 KB of shared memory per CTA
 struct NttArgs {
     u64* base;
     i64 poly_stride;
+    const u64* src_base;     // inverse only: the first phase reads from here (same layout) -> out-of-place transform
     LimbMap map;
     const ModConst* mod;
     const u64* tw;       // psi_brv (fwd) or ipsi_brv (inv): [mods][N]
@@ -413,7 +414,9 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
 #pragma unroll
         for (int it = 0; it < GG::E; it++) {
             const int e = threadIdx.x + it * blockDim.x;
-            v[it] = line_ptr(e >> LT)[e & (GG::T - 1)];
+            const u64* lp = line_ptr(e >> LT);
+            if (a.src_base) lp = a.src_base + (lp - a.base);
+            v[it] = lp[e & (GG::T - 1)];
         }
 #pragma unroll
         for (int it = 0; it < GG::E; it++) {
@@ -513,6 +516,7 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
     a.apply_ninv = 1;
+    a.src_base = nullptr;
     a.epi_src = nullptr;
     a.epi_out = nullptr;
     a.epi_add = nullptr;
@@ -554,10 +558,11 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
 
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) { ntt_inverse_scaled(c, b, true, s); }
 
-void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s) {
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, true);
     a.apply_ninv = apply_ninv ? 1 : 0;
+    a.src_base = src;
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
