@@ -295,13 +295,14 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
         const u64 t40 = (1ull << 40) % mc.q;
         // software-pipelined stream: the 8 plaintext words of the NEXT (unit, chunk) are in flight while the
         // current chunk is multiplied (keeps ~128 B per thread outstanding -> HBM-bound, not latency-bound)
-        const int nch = (nbank + 7) / 8, ustride = gridDim.z * MAC_LANES;
+        // (the host routes a bank size that is not a multiple of 8 to the 128-bit path: no tail checks here)
+        const int nch = nbank >> 3, ustride = gridDim.z * MAC_LANES;
         int u = blockIdx.z * MAC_LANES + lane, ch = 0;
         if (u >= units) return;
+        const uint4* sbase = (const uint4*)sn + kp;    // {h, l} pairs of coefficients (k, k+1) of this thread
         ulonglong2 cur[8], nxt[8];
 #pragma unroll
-        for (int t = 0; t < 8; t++)
-            if (t < nbank) cur[t] = __ldg((const ulonglong2*)(w + (size_t)u * wus + wl + (size_t)t * pstride));
+        for (int t = 0; t < 8; t++) cur[t] = __ldg((const ulonglong2*)(w + (size_t)u * wus + wl + (size_t)t * pstride));
         u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
         while (true) {
             int nu = u, nc = ch + 1;
@@ -309,21 +310,17 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
             const bool more = nu < units;
             if (more) {
                 const u64* wn = w + (size_t)nu * wus + wl + (size_t)(nc * 8) * pstride;
-                const int cn = min(8, nbank - nc * 8);
 #pragma unroll
-                for (int t = 0; t < 8; t++)
-                    if (t < cn) nxt[t] = __ldg((const ulonglong2*)(wn + (size_t)t * pstride));
+                for (int t = 0; t < 8; t++) nxt[t] = __ldg((const ulonglong2*)(wn + (size_t)t * pstride));
             }
-            const int cnt = min(8, nbank - ch * 8);
+            const uint4* sb8 = sbase + (size_t)(ch * 8) * 2 * (MAC_T / 2);
 #pragma unroll
             for (int t = 0; t < 8; t++) {
-                if (t >= cnt) break;
-                const int uq = ch * 8 + t;
                 const uint32_t ah = (uint32_t)(cur[t].x >> 20), al = (uint32_t)(cur[t].x & 0xFFFFF);
                 const uint32_t bh = (uint32_t)(cur[t].y >> 20), bl = (uint32_t)(cur[t].y & 0xFFFFF);
                 const uint32_t as = ah + al, bsum = bh + bl;
-                const uint4 pp = *(const uint4*)&sn[(uq * 2 + 0) * MAC_T + 2 * kp];   // {h, l} of k, k+1
-                const uint4 rr = *(const uint4*)&sn[(uq * 2 + 1) * MAC_T + 2 * kp];
+                const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];   // {h, l} of k, k+1 (component 0)
+                const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];   // component 1
                 h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
                 h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
                 h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
@@ -647,7 +644,7 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     while ((size_t)tiles * level * zsplit < 148 * 8 && zsplit * MAC_LANES < units) zsplit *= 2;
     // limbs [0, nw) on the 128-bit path, [nw, level) (q < 2^41) on the 20-bit Karatsuba path when enabled
     int nw = level;
-    if (allow_narrow) {
+    if (allow_narrow && nbank % 8 == 0) {
         nw = 0;
         while (nw < level && c.mods[nw] >= (1ull << 41)) nw++;
         for (int i = nw; i < level; i++)
