@@ -63,6 +63,29 @@ def test_ntt_roundtrip_and_ring_product(pname):
     assert np.array_equal(got[0], ref) and np.array_equal(got[1], ref)
 
 
+@pytest.mark.parametrize("fill", ["max", "mixed"])
+def test_ntt_lazy_bounds_extreme_inputs(fill):
+    """Worst-case words for the lazy butterfly ranges ([0, 8q) forward, [0, 4q) inverse, approximate-high
+    Shoup products): all-(q-1) limbs and alternating 0 / q-1, on the 60-bit q_0 (integer path) and the 40-bit
+    limbs, through the ring product against the oracle's schoolbook-pinned ring_mul."""
+    P = P16
+    ctx = E.Context("P16", 0)
+    mods = P.q[:4]
+    if fill == "max":
+        a = np.stack([np.full(P.N, q - 1, dtype=np.uint64) for q in mods])
+    else:
+        a = np.stack([np.where(np.arange(P.N) % 2 == 0, 0, q - 1).astype(np.uint64) for q in mods])
+    b = a.copy()
+    b[:, ::3] = 1
+    A = ctx.pt_from_host(a, 1.0)
+    assert np.array_equal(ctx.to_host(ctx.from_ntt(ctx.to_ntt(A))), a)
+    x = ctx.to_ntt(ctx.ct_from_host(np.stack([a, a]), 1.0))
+    y = ctx.ptmul(x, ctx.to_ntt(ctx.pt_from_host(b, 1.0)))
+    ref = O.ring_mul(a, b, mods, P.N)
+    got = ctx.to_host(y)
+    assert np.array_equal(got[0], ref) and np.array_equal(got[1], ref)
+
+
 # ------------------------------------------------------------------ keys / enc / dec
 def test_keys_bit_exact(c13, keys13):
     ok, gk = keys13
