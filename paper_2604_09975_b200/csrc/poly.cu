@@ -662,7 +662,7 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         diag_mac_kernel<true><<<dim3(tiles, level - nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc,
                                                                                                accs, level, c.N, c.d_mod, nw);
     c.prof_end(slot, s);
-    c.st_launch++;
+    c.st_launch += (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // the 128-bit and the narrow launch
     c.st_bytes += bytes;
     c.st_ptmul += (uint64_t)units * nbank;
 }
