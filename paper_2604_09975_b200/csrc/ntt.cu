@@ -1,6 +1,6 @@
 // ntt.cu -- negacyclic NTT / iNTT over 64-bit RNS limbs (the ring isomorphism of P:82) for sm_100a.
 //
-// Forward: merged-twiddle Cooley-Tukey (bit-reversed output), Harvey lazy butterflies in [0, 4q),
+// Forward: merged-twiddle Cooley-Tukey (bit-reversed output), Harvey lazy butterflies in [0, 8q),
 // Shoup twiddles.  Inverse: Gentleman-Sande with psi^{-brv(k)} and a final N^{-1}.
 // A limb of N = 2^logN words is split N = R x S (R = 2^s1 rows, S = 2^s2 columns):
 //   phase A: the first s1 stages only pair elements of one column (stride S) -> a CTA stages a
@@ -43,28 +43,57 @@ struct NttArgs {
 };
 
 // ---------------------------------------------------------------------------------------------
-// Integer path (any q < 2^61): Harvey lazy butterflies, Shoup twiddles, values in [0, 4q).
-__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u64 two_q) {
-    u64 x = X >= two_q ? X - two_q : X;
-    u64 t = mul_shoup_lazy(Y, W, Wp, q);
-    X = x + t;
-    Y = x - t + two_q;
+// Integer path (any q < 2^61): Harvey lazy butterflies, Shoup twiddles with an APPROXIMATE high product.
+// h' = a1 w1' + hi32(a1 w0') + hi32(a0 w1') (dropping a0 w0' and the carries out of the low word) lies in
+// [h - 2, h] for the exact h = hi64(a w'), so a w - h' q = (a w - h q) + (h - h') q is in [0, 4q) (exact Shoup:
+// [0, 2q)).  Written in PTX as 3 IMAD.HI + 1 IMAD + carry ops with no 64-bit addend, so ptxas needs no register-pair
+// moves (the C form cost IMAD.MOV shuffles on the fmaheavy pipe, which bounds this path at 77 %: profiles/r01_summary.md).
+// The wider product range is absorbed by widening the lazy bounds: forward values in [0, 8q), inverse in [0, 4q).
+__device__ __forceinline__ u64 mul_shoup_lazy4(u64 a, u64 w, u64 wp, u64 q) {   // [0, 4q)
+    unsigned hl, hh;
+    asm("{\n\t.reg .u32 a0, a1, p0, p1, t0, t1, c;\n\t"
+        "mov.b64 {a0, a1}, %2;\n\t"
+        "mov.b64 {p0, p1}, %3;\n\t"
+        "mul.hi.u32 t0, a1, p0;\n\t"
+        "mad.hi.cc.u32 t1, a0, p1, t0;\n\t"
+        "addc.u32 c, 0, 0;\n\t"
+        "mad.lo.cc.u32 %0, a1, p1, t1;\n\t"
+        "madc.hi.u32 %1, a1, p1, c;\n\t}"
+        : "=r"(hl), "=r"(hh) : "l"(a), "l"(wp));
+    const u64 h = ((u64)hh << 32) | hl;
+    return a * w - h * q;
 }
 
-__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u64 two_q) {
+// Forward (CT): X, Y in [0, 8q) -> x = X mod' 4q in [0, 4q), t in [0, 4q): X' = x + t, Y' = x - t + 4q in [0, 8q).
+__device__ __forceinline__ void ct_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u64 four_q) {
+    u64 x = X >= four_q ? X - four_q : X;
+    u64 t = mul_shoup_lazy4(Y, W, Wp, q);
+    X = x + t;
+    Y = x - t + four_q;
+}
+
+// Inverse (GS): X, Y in [0, 4q) -> X' = (X + Y) mod' 4q, Y' = (X - Y + 4q) W in [0, 4q).
+__device__ __forceinline__ void gs_bfly(u64& X, u64& Y, u64 W, u64 Wp, u64 q, u64 four_q) {
     u64 x = X + Y;
-    x = x >= two_q ? x - two_q : x;
-    u64 t = X - Y + two_q;
-    Y = mul_shoup_lazy(t, W, Wp, q);
+    x = x >= four_q ? x - four_q : x;
+    u64 t = X - Y + four_q;
+    Y = mul_shoup_lazy4(t, W, Wp, q);
     X = x;
+}
+
+// [0, 8q) -> [0, q)
+__device__ __forceinline__ u64 canon8(u64 v, u64 q) {
+    v = v >= 4 * q ? v - 4 * q : v;
+    v = v >= 2 * q ? v - 2 * q : v;
+    return v >= q ? v - q : v;
 }
 
 struct IntOps {
     using T = u64;
     using TW = ulonglong2;
-    u64 q, two_q;
-    __device__ __forceinline__ void ct(u64& X, u64& Y, TW w) const { ct_bfly(X, Y, w.x, w.y, q, two_q); }
-    __device__ __forceinline__ void gs(u64& X, u64& Y, TW w) const { gs_bfly(X, Y, w.x, w.y, q, two_q); }
+    u64 q, four_q;
+    __device__ __forceinline__ void ct(u64& X, u64& Y, TW w) const { ct_bfly(X, Y, w.x, w.y, q, four_q); }
+    __device__ __forceinline__ void gs(u64& X, u64& Y, TW w) const { gs_bfly(X, Y, w.x, w.y, q, four_q); }
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -263,7 +292,7 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
         for (int e = threadIdx.x; e < tot; e += blockDim.x) {
             const int r = e >> lgl, c = e & (lines - 1);
             const T v = sm[c * GG::LSP + pad(r)];
-            g[(i64)r * S + c0 + c] = st_raw(v);    // forward: lazy u64 [0, 4q) / raw double bits to phase B
+            g[(i64)r * S + c0 + c] = st_raw(v);    // forward: lazy u64 [0, 8q) / raw double bits to phase B
         }
     } else {
         {   // all E loads of a thread in flight before the first use (tot = E * blockDim.x)
@@ -293,7 +322,7 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
                 for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], ni, nip, ops.q);
             } else {
 #pragma unroll
-                for (int k = 0; k < GG::E; k++) gc[k * rs] = x[k] >= ops.q ? x[k] - ops.q : x[k];   // GS outputs in [0, 2q)
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = canon8(x[k], ops.q);   // GS outputs in [0, 4q)
             }
         } else {
             if (a.apply_ninv) {
@@ -316,7 +345,7 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
         cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
     } else {
         const u64 q = a.mod[mi].q;
-        cols_body<LT, INV>(a, lines, IntOps{q, 2 * q}, a.tw2 + (size_t)mi * a.N, mi);
+        cols_body<LT, INV>(a, lines, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi);
     }
 }
 
@@ -381,9 +410,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
                     const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
                     u64 w;
                     if constexpr (std::is_same<T, u64>::value) {
-                        const u64 q = ops.q, two_q = ops.two_q;
-                        w = v >= two_q ? v - two_q : v;
-                        w = w >= q ? w - q : w;
+                        w = canon8(v, ops.q);
                     } else {
                         const double q = ops.q, qinv = a.fpc[4 * mi + 1];
                         w = fp_canon(fp_center(v, q, qinv), q);
@@ -400,9 +427,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
             const T v = sm[(e >> LT) * GG::LSP + pad(e & (GG::T - 1))];
             u64 w;
             if constexpr (std::is_same<T, u64>::value) {
-                const u64 q = ops.q, two_q = ops.two_q;
-                w = v >= two_q ? v - two_q : v;
-                w = w >= q ? w - q : w;
+                w = canon8(v, ops.q);
             } else {
                 const double q = ops.q, qinv = a.fpc[4 * mi + 1];
                 w = fp_canon(fp_center(v, q, qinv), q);
@@ -448,7 +473,7 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
         rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
     } else {
         const u64 q = a.mod[mi].q;
-        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 2 * q}, a.tw2 + (size_t)mi * a.N, mi);
+        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi);
     }
 }
 
