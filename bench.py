@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 import numpy as np  # noqa: E402
 
 M, D, H, DH, DFF = 128, 768, 12, 64, 3072
-PROF_KERNELS = ["diag_mac", "ks_inner", "ks_psi", "ks_rotsum", "ks_rma", "ntt", "bcast_mac", "add_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
+PROF_KERNELS = ["diag_mac", "ks_inner", "ks_psi", "ks_rotsum", "ks_rma", "ntt", "bcast_mac", "add_kernel", "add_i_batch_kernel", "automorph_kernel", "bconv_batch_kernel", "bconv_kernel",
                 "export_mask_kernel", "gather_copy_kernel", "masked_sum_kernel", "mod_reduce_kernel",
                 "moddown_finish_batch_kernel", "moddown_finish_kernel", "mul_i_kernel", "mul_kernel",
                 "rescale_finish_batch_kernel", "rescale_prep_batch_kernel", "sum_csr_kernel", "tensor_csr_kernel",

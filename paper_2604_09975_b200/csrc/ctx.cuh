@@ -191,6 +191,9 @@ struct OutBatch {
     const u64* add[KS_BATCH][2];
 };
 constexpr int CP_BATCH = 512;
+constexpr int ADDI_BATCH = 32;
+struct AddIBatch { const u64* a[ADDI_BATCH]; const u64* b[ADDI_BATCH]; u64* out[ADDI_BATCH]; };
+void k_add_i_batch(encf_ctx& c, const AddIBatch& B, int n, int npolys, const LimbMap& m, bool sub, cudaStream_t s);
 struct CopyBatch {
     const u64* src[CP_BATCH];
     uint32_t g[CP_BATCH];

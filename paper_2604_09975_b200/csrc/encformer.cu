@@ -272,13 +272,15 @@ void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, cons
     const int Lb = bank[0][0].L;
     // k_{j beta} + i k_{m/2 + j beta} for every (l, j)
     std::vector<std::vector<DCt>> kc(a.B);
-    for (int l = 0; l < a.B; l++)
-        for (int j = 0; j < g / 2; j++) {
-            DCt im = ev.alloc(Lb), o = ev.alloc(Lb);
-            ev.mul_i(bank[a.B + l][g / 2 + j], im);
-            ev.add(bank[a.B + l][j], im, o);
-            kc[l].push_back(o);
-        }
+    {
+        std::vector<const DCt*> ka, kb;
+        for (int l = 0; l < a.B; l++)
+            for (int j = 0; j < g / 2; j++) { ka.push_back(&bank[a.B + l][j]); kb.push_back(&bank[a.B + l][g / 2 + j]); }
+        std::vector<DCt> ko = ev.alloc_many((int)ka.size(), Lb);
+        ev.add_i_many(ka, kb, ko);
+        for (int l = 0; l < a.B; l++)
+            for (int j = 0; j < g / 2; j++) kc[l].push_back(ko[l * (g / 2) + j]);
+    }
     const int nt = t1 - t0;
     std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(nt);
     for (int t = t0; t < t1; t++) {
@@ -357,10 +359,10 @@ void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, cons
     std::vector<DCt> shve = ev.alloc_many(2 * BV, Lv);
     ev.sum_many(t1, Lv, 2, shve, sc1);
     std::vector<DCt> d = ev.alloc_many(BV, Lv);
-    for (int l = 0; l < BV; l++) {
-        DCt shi = ev.alloc(Lv);
-        ev.mul_i(shve[l], shi);
-        ev.add(shve[BV + l], shi, d[l], /*sub=*/true);
+    {
+        std::vector<const DCt*> da, db;
+        for (int l = 0; l < BV; l++) { da.push_back(&shve[BV + l]); db.push_back(&shve[l]); }
+        ev.add_i_many(da, db, d, /*sub=*/true);
     }
     std::vector<DCt> uu = ev.alloc_many(BV, Lv - 1);
     ev.rescale_many(ptrs(d), uu);

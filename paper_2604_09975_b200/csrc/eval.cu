@@ -336,6 +336,28 @@ void Ev::mul_i(const DCt& a, DCt& out) {
     out.L = a.L; out.ncomp = a.ncomp; out.scale = a.scale; out.cstride = 0;
 }
 
+void Ev::add_i_many(const std::vector<const DCt*>& a, const std::vector<const DCt*>& b, std::vector<DCt>& outs, bool sub) {
+    const int n = (int)a.size();
+    if ((int)b.size() != n || (int)outs.size() != n) throw EncfError(ENCF_ERR_ARG, "add_i_many: length mismatch");
+    if (n == 0) return;
+    const int L = a[0]->L, nc = a[0]->ncomp;
+    for (int r = 0; r < n; r++) {
+        check_scale(a[r]->scale, b[r]->scale);
+        for (const DCt* x : {a[r], b[r]})
+            if (x->L != L || x->ncomp != nc || (x->cstride != 0 && x->cstride != (i64)L * c.N))
+                throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "add_i_many: level/component/layout mismatch");
+    }
+    for (int r0 = 0; r0 < n; r0 += ADDI_BATCH) {
+        const int nb = std::min(ADDI_BATCH, n - r0);
+        AddIBatch B;
+        for (int r = 0; r < nb; r++) { B.a[r] = a[r0 + r]->d; B.b[r] = b[r0 + r]->d; B.out[r] = outs[r0 + r].d; }
+        k_add_i_batch(c, B, nb, nc, c.qmap(L), sub, s);
+    }
+    for (int r = 0; r < n; r++) {
+        outs[r].L = L; outs[r].ncomp = nc; outs[r].scale = a[r]->scale; outs[r].cstride = 0;
+    }
+}
+
 void Ev::ptmul(const DCt& a, const u64* pt, double pt_scale, DCt& out) {
     const int N = c.N;
     k_mul(c, a.d, (i64)a.L * N, pt, 0, out.d, (i64)a.L * N, a.ncomp, c.qmap(a.L), s);

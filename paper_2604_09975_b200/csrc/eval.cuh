@@ -74,6 +74,8 @@ struct Ev {
     void rescale(const DCt& in, DCt& out);
     void add(const DCt& a, const DCt& b, DCt& out, bool sub = false);
     void mul_i(const DCt& a, DCt& out);
+    // outs[r] = a[r] +- X^{N/2} b[r] (= add(a, mul_i(b)) bit for bit), batched launches
+    void add_i_many(const std::vector<const DCt*>& a, const std::vector<const DCt*>& b, std::vector<DCt>& outs, bool sub = false);
     void ptmul(const DCt& a, const u64* pt, double pt_scale, DCt& out);
     void mod_drop(const DCt& in, int L, DCt& out);
     void copy(const DCt& in, DCt& out);

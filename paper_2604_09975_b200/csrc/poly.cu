@@ -56,6 +56,24 @@ __global__ void mul_i_kernel(const u64* __restrict__ a, u64* __restrict__ out, s
     }
 }
 
+// out_r = a_r +- X^{N/2} b_r for a batch of same-shape ciphertexts (one launch instead of a mul_i and an add per
+// pair; the same two modular operations per word as mul_i_kernel followed by add_kernel, so bit-identical).
+__global__ void add_i_batch_kernel(AddIBatch B, int n, size_t per, int N, LimbMap m, const ModConst* mod, const u64* im,
+                                   const u64* im_sh, int sub) {
+    const size_t total = per * n;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / per);
+        const size_t j = i - (size_t)r * per;
+        const int limb = (int)((j / N) % m.n), k = (int)(j % N);
+        const int mi = m.mod[limb];
+        const u64 q = mod[mi].q;
+        u64 t = mul_shoup(B.b[r][j], im[mi], im_sh[mi], q);
+        if (k >= N / 2) t = t ? q - t : 0;
+        const u64 x = B.a[r][j];
+        B.out[r][j] = sub ? sub_mod(x, t, q) : add_mod(x, t, q);
+    }
+}
+
 // sigma_g in the NTT domain: out[i] = in[brv(((e_i g mod 2N) - 1) / 2)], e_i = 2 brv(i) + 1.
 // Within an aligned block of 2^k indices the sources are a permutation of an aligned block, so warp
 // accesses stay inside one 256-byte segment (coalesced gather).
@@ -530,6 +548,14 @@ void k_mul_i(encf_ctx& c, const u64* a, u64* out, int npolys, const LimbMap& m, 
     mul_i_kernel<<<GRID(total), TB, 0, s>>>(a, out, total, c.N, m, c.d_mod, c.d_imag, c.d_imag_sh);
     c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += total * 16;
+}
+
+void k_add_i_batch(encf_ctx& c, const AddIBatch& B, int n, int npolys, const LimbMap& m, bool sub, cudaStream_t s) {
+    const size_t per = (size_t)npolys * m.n * c.N, total = per * n;
+    { int _slot; c.prof_begin("add_i_batch_kernel", s, 0, _slot);
+    add_i_batch_kernel<<<GRID(total), TB, 0, s>>>(B, n, per, c.N, m, c.d_mod, c.d_imag, c.d_imag_sh, sub ? 1 : 0);
+    c.prof_end(_slot, s); }
+    c.st_launch++; c.st_bytes += total * 24;
 }
 
 void k_automorph(encf_ctx& c, const u64* in, i64 is, u64* out, i64 os, int npolys, int nlimbs, uint32_t g, cudaStream_t s) {
