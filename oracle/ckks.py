@@ -655,6 +655,18 @@ def relinearize(P, keys, ct):
     return Ct(np.stack([padd(ct.c[0], k0, mods, N), padd(ct.c[1], k1, mods, N)]), ct.scale)
 
 
+def relinearize_ext(P, keys, ct):
+    """Relinearisation WITHOUT its ModDown (DESIGN.md R-RELRS, the R-LAZY idea applied to relin): the extended
+    pair (P d0 + b0, P d1 + b1) over Q_L u P, (b0, b1) = the inner product of ModUp(d2) with the relinearisation
+    key.  Its ModDown is relinearize(); moddown_rescale() of it is relin followed by rescale, rounded once."""
+    if ct.ncomp != 3:
+        raise OracleError("FORMAT: relinearize needs 3 components")
+    L, N = ct.L, P.N
+    emods = P.ext_mods(L)
+    b0, b1 = ks_inner(P, modup(P, ct.c[2], L), keys.key_at(0, L), L)
+    return np.stack([padd(b0, lift_P(P, ct.c[0], L), emods, N), padd(b1, lift_P(P, ct.c[1], L), emods, N)])
+
+
 # ------------------------------------------------------------------------------------ arithmetic
 def add(P, a, b):
     if a.scale != b.scale:

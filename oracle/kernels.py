@@ -211,6 +211,12 @@ class Ev:
         c = np.stack([O.moddown_rescale(self.P, y.c[i], L) for i in range(2)])
         return O.Ct(c, y.scale / float(self.P.q[L - 1]))
 
+    def relin_rescale(self, ct):
+        """rescale(relin(ct)) with ONE rounding (R-RELRS): the relin key switch kept in the extended basis and
+        divided by P q_{L-1} at once."""
+        self.ledger["relin"] += 1
+        return self.moddown_rescale(ExtCt(O.relinearize_ext(self.P, self.keys, ct), ct.L, ct.scale))
+
     def mac_ptmul(self, cts, pts):
         """sum_i cts[i] (.) pts[i]  (exact modular sum of ring products; evaluated in the oracle's NTT
         domain -- the sum of ring products is unique)."""
@@ -338,6 +344,10 @@ class CountEv:
         self.ledger["moddown"] += 1
         self.ledger["rescale"] += 1
         return FakeCt(y.L - 1, y.scale)
+
+    def relin_rescale(self, ct):
+        self.ledger["relin"] += 1
+        return self.moddown_rescale(FakeCt(ct.L, ct.scale))
 
     def lift_ext(self, ct):
         return FakeCt(ct.L, ct.scale)
@@ -576,7 +586,7 @@ def score(ev, plan, qs, ks, ts=None, route_hoisted=True):
     for t in (range(m // 2) if ts is None else ts):
         j, s = t // beta, t % beta
         pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in range(plan.B)]
-        T = ev.rescale(ev.relin(ev.tensor_sum(pairs)))
+        T = ev.relin_rescale(ev.tensor_sum(pairs))          # lazy relin merged with the rescale (R-RELRS)
         T = route(ev, T, plan.C // H, H, m, hoisted=route_hoisted)
         S.append(Psi_hoisted(ev, T, [s], m, N_seg, 0, H)[0])
     return S
@@ -731,7 +741,7 @@ def value(ev, plan, ps, vs, blocks=None):
             bt.append(ev.rescale(ev.mac_ptmul(cts, pts)))     # sum_u Phi^{t-u}(p) (.) n_u (exact modular sum)
         Lb = bt[0].L
         pairs = [(ev.mod_drop(ub[t], Lb) if ub[t].L > Lb else ub[t], bt[t]) for t in range(half)]
-        outs.append(ev.rescale(ev.relin(ev.tensor_sum(pairs))))
+        outs.append(ev.relin_rescale(ev.tensor_sum(pairs)))     # lazy relin merged with the rescale (R-RELRS)
     return outs
 
 

@@ -287,10 +287,9 @@ void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, cons
         int j = t / beta, s = t % beta;
         for (int l = 0; l < a.B; l++) pairs[t - t0].push_back({&bank[l][s], &kc[l][j]});
     }
-    std::vector<DCt> T3 = ev.alloc_many(nt, Lb, 3), T2 = ev.alloc_many(nt, Lb), T = ev.alloc_many(nt, Lb - 1);
+    std::vector<DCt> T3 = ev.alloc_many(nt, Lb, 3), T = ev.alloc_many(nt, Lb - 1);
     ev.tensor_many(pairs, T3);
-    ev.relin_many(ptrs(T3), T2);
-    ev.rescale_many(ptrs(T2), T);
+    ev.relin_rescale_many(ptrs(T3), T);      // lazy relin merged with the rescale (R-RELRS)
     std::vector<DCt> R = route_many(ev, T, a.C / H, H, m);
     std::vector<std::vector<int>> st(nt);
     for (int t = t0; t < t1; t++) st[t - t0] = {t % beta};
@@ -420,11 +419,10 @@ void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, cons
         }
         for (int t = 0; t < half; t++) pairs[l].push_back({&ud[l][t], &bt[l * half + t]});
     }
-    std::vector<DCt> o3 = ev.alloc_many(BV, Lb, 3), o2 = ev.alloc_many(BV, Lb);
+    std::vector<DCt> o3 = ev.alloc_many(BV, Lb, 3);
     ev.tensor_many(pairs, o3);
-    ev.relin_many(ptrs(o3), o2);
     outs = ev.alloc_many(BV, Lb - 1);
-    ev.rescale_many(ptrs(o2), outs);
+    ev.relin_rescale_many(ptrs(o3), outs);   // lazy relin merged with the rescale (R-RELRS)
 }
 
 // ====================================================================================== export (Alg 3 GPU half)

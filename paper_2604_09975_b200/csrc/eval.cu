@@ -613,6 +613,47 @@ void Ev::rotsum_many(const std::vector<const DCt*>& ins, const std::vector<uint3
     moddown_many(acc, outs);
 }
 
+// rescale(relin(ct)) rounded once (R-RELRS; oracle ckks.relinearize_ext + moddown_rescale): the relin key switch
+// kept in the extended basis as (P d0 + b0, P d1 + b1), then ONE merged ModDown + rescale.
+void Ev::relin_rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
+    const int n = (int)ins.size();
+    if (n == 0) return;
+    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    std::vector<const u64*> d2;
+    for (int i = 0; i < n; i++) {
+        if (ins[i]->ncomp != 3 || ins[i]->L != L) throw EncfError(ENCF_ERR_FORMAT, "relinearize needs 3 components at one level");
+        d2.push_back(ins[i]->comp(2, N));
+    }
+    const u64* key = key_for(0u, L);
+    u64* ext = modup_many(d2, {}, L);
+    std::vector<DCt> acc = alloc_many_ext(n, L);
+    const int ML = keys->max_level, key_nl = ML + K;
+    LimbMap klm;
+    klm.n = nl;
+    for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
+    for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
+        const int cnt = std::min(KS_BATCH, n - r0);
+        KsInnerBatch B;
+        for (int i = 0; i < cnt; i++) {
+            acc[r0 + i].scale = ins[r0 + i]->scale;
+            B.ext[i] = ext + ext_stride(L) * (r0 + i); B.key[i] = key; B.gather[i] = 1u; B.acc[i] = acc[r0 + i].d;
+        }
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
+        c.st_ks += cnt;
+    }
+    for (int r0 = 0; r0 < 2 * n; r0 += CP_BATCH) {       // + P d0, P d1 on the q-limbs
+        const int cnt = std::min(CP_BATCH, 2 * n - r0);
+        CopyBatch dst, src;
+        for (int i = 0; i < cnt; i++) {
+            const int idx = (r0 + i) / 2, comp = (r0 + i) % 2;
+            dst.src[i] = acc[idx].comp(comp, N); dst.g[i] = 1u;
+            src.src[i] = ins[idx]->comp(comp, N); src.g[i] = 1u;
+        }
+        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);
+    }
+    moddown_rescale_many(acc, outs);
+}
+
 void Ev::lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;

@@ -62,6 +62,7 @@ struct Ev {
     void hoisted_many(const std::vector<const DCt*>& ins, const std::vector<std::vector<uint32_t>>& gs,
                       std::vector<std::vector<DCt>>& outs);
     void relin_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs);
+    void relin_rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs);   // rescale(relin) rounded once
     void rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs);
     void sum_many(const std::vector<std::vector<SumTerm>>& terms, int L, int ncomp, std::vector<DCt>& outs,
                   const std::vector<double>& scales);
