@@ -257,10 +257,9 @@ class Layer:
                 for k, v in self.host_inputs.items()}
 
     def _export(self, cts, sid):
-        outs = []
-        for i, c in enumerate(cts):
-            outs.append(self.ctx.export_c2m(c, self.Lconv, self.mask_seed, sid + i))
-        return outs
+        if not cts:
+            return []
+        return self.ctx.export_c2m_many(cts, self.Lconv, self.mask_seed, sid)   # ciphertext i: stream id sid + i
 
     def _complex_pairs(self, ys):
         out = [self.ctx.complexify(ys[2 * i], ys[2 * i + 1]) for i in range(len(ys) // 2)]
@@ -308,11 +307,7 @@ class Layer:
         if self.ablation == "wo-scp":       # edge (3) value -> out-projection
             ctx.repack_rma(keys, O, M)
         self._mark("value")
-        Ore = []
-        for o in O:                        # decomplexify the value output (G11): Re o = (o + conj o) / 2
-            z = ctx.add(o, ctx.conjugate(keys, o))
-            z.scale = o.scale * 2.0
-            Ore.append(z)
+        Ore = ctx.decomplexify(keys, O)    # decomplexify the value output (G11): Re o = (o + conj o) / 2, batched
         xo = self._complex_pairs(Ore)
         yo = self.oproj.matmul(keys, xo, self.w_o, float(ctx.q[xo[0].n_limbs - 1]))
         ex += self._export(self._complex_pairs(yo), 100)

@@ -149,6 +149,12 @@ encf_status encf_rotate(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in,
 encf_status encf_rotate_hoisted(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in, const int32_t* steps /*host*/,
                                 int32_t n, encf_ct* outs /*host array of n*/, void* stream);
 encf_status encf_conjugate(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in, encf_ct* out, void* stream);
+/* Decomplexify (DESIGN G3): out[i] = in[i] + conj(in[i]) with scale 2 scale(in[i]) (the 1/2 of
+ * (c + conj c)/2 is scale bookkeeping, no level).  n ciphertexts (host array, each 2 components, same level) in
+ * one batched conjugation (the single-KS conj of encf_conjugate, bit for bit) + one batched add.  outs: host array
+ * of n caller buffers at the input level.  Errors ARG (n < 1), LEVEL_MISMATCH (mixed levels), MISSING_KEY. */
+encf_status encf_decomplexify(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in /*host array of n*/, int32_t n,
+                              encf_ct* outs /*host array of n*/, void* stream);
 /* Divide-and-round by q_{L-1} (SEAL style, C5); out has n_limbs - 1 limbs.  Error LEVEL_EXHAUSTED. */
 encf_status encf_rescale(encf_ctx* ctx, const encf_ct* in, encf_ct* out, void* stream);
 /* ModSwitchToNext repeated: keep the first n_limbs limbs, scale unchanged. */
@@ -228,6 +234,13 @@ encf_status encf_l_conv(encf_ctx* ctx, int32_t ell, int32_t sigma, double scale,
  * [L_conv][N].  masked->data must hold 2*L_conv*N words. */
 encf_status encf_export_c2m(encf_ctx* ctx, const encf_ct* in, int32_t L_conv, uint64_t mask_seed, uint64_t stream_id,
                             encf_ct* masked, uint64_t* server_share, void* stream);
+/* Batched export (the same steps as encf_export_c2m for each of n ciphertexts of one level): ciphertext i uses
+ * stream id stream_id0 + i.  masked: device [n][2][L_conv][N] (coefficient form, caller-owned), shares: device
+ * [n][L_conv][N].  One inverse-NTT launch pair for all 2n polynomials.  Errors as encf_export_c2m, plus
+ * LEVEL_MISMATCH when the inputs' levels differ. */
+encf_status encf_export_c2m_many(encf_ctx* ctx, const encf_ct* in /*host array of n*/, int32_t n, int32_t L_conv,
+                                 uint64_t mask_seed, uint64_t stream_id0, uint64_t* masked, uint64_t* shares,
+                                 void* stream);
 /* ------------------------------------------------------------------------------------------ import (Alg 4, GPU half) */
 /* Ring2Field local map (App. C): after Pi_Ext, party b holds m'_b in [0, 2^{ell+sigma}) per
  * coefficient (device [N] little-endian (lo, hi) 64-bit pairs) with m'_0 + m'_1 = 2^{ell+sigma} + cl(m);

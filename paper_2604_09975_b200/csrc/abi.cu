@@ -394,6 +394,28 @@ encf_status encf_rotate_hoisted(encf_ctx* c, const encf_keys* k, const encf_ct* 
 encf_status encf_conjugate(encf_ctx* c, const encf_keys* k, const encf_ct* in, encf_ct* out, void* stream) {
     return guard([&] { EV_BEGIN(k); DCt x = view(in); DCt o = outview(out, x.L, 2); ev.rotate_galois(x, ev.galois_conj(), o); writeback(out, o); });
 }
+encf_status encf_decomplexify(encf_ctx* c, const encf_keys* k, const encf_ct* in, int32_t n, encf_ct* outs, void* stream) {
+    return guard([&] {
+        EV_BEGIN(k);
+        need(in != nullptr && outs != nullptr && n >= 1, ENCF_ERR_ARG, "decomplexify: n >= 1 ciphertexts");
+        std::vector<DCt> xs, cj, os;
+        std::vector<const DCt*> xp;
+        for (int i = 0; i < n; i++) xs.push_back(view(&in[i]));
+        for (int i = 0; i < n; i++) {
+            need(xs[i].ncomp == 2, ENCF_ERR_FORMAT, "decomplexify: 2-component ciphertexts");
+            need(xs[i].L == xs[0].L, ENCF_ERR_LEVEL_MISMATCH, "decomplexify: mixed levels");
+            xp.push_back(&xs[i]);
+            os.push_back(outview(&outs[i], xs[i].L, 2));
+        }
+        cj = ev.alloc_many(n, xs[0].L);
+        ev.rotate_many(xp, std::vector<uint32_t>(n, ev.galois_conj()), cj);
+        for (int i = 0; i < n; i++) {
+            ev.add(xs[i], cj[i], os[i]);
+            os[i].scale = 2.0 * xs[i].scale;
+            writeback(&outs[i], os[i]);
+        }
+    });
+}
 encf_status encf_rescale(encf_ctx* c, const encf_ct* in, encf_ct* out, void* stream) {
     return guard([&] { EV_BEGIN(nullptr); DCt x = view(in); need(x.L > 1, ENCF_ERR_LEVEL_EXHAUSTED, "rescale at one limb"); DCt o = outview(out, x.L - 1, x.ncomp); ev.rescale(x, o); writeback(out, o); });
 }
@@ -724,6 +746,31 @@ encf_status encf_export_c2m(encf_ctx* c, const encf_ct* in, int32_t Lc, uint64_t
         ntt_inverse(*c, PolyBatch{masked->data, (i64)Lc * N, 2, c->qmap(Lc)}, s);
         k_export_mask(*c, mask_seed, (0x04ull << 56) | stream_id, masked->data, share, Lc, s);
         masked->n_comp = 2; masked->n_limbs = Lc; masked->scale = x.scale; masked->ntt = 0;
+    });
+}
+
+encf_status encf_export_c2m_many(encf_ctx* c, const encf_ct* in, int32_t n, int32_t Lc, uint64_t mask_seed, uint64_t stream_id0,
+                                 uint64_t* masked, uint64_t* shares, void* stream) {
+    return guard([&] {
+        need(c && in && masked && shares && n >= 1, ENCF_ERR_ARG, "export_many: null argument or n < 1");
+        need(stream_id0 + (uint64_t)n <= (1ull << 56), ENCF_ERR_ARG, "export_many: stream ids must be < 2^56");
+        cudaStream_t s = S(stream);
+        const int N = c->N;
+        const size_t cw = (size_t)2 * Lc * N;
+        int L0 = -1;
+        for (int i = 0; i < n; i++) {
+            DCt x = view(&in[i]);
+            need(x.ncomp == 2, ENCF_ERR_FORMAT, "export needs 2 components");
+            need(Lc >= 1 && Lc <= x.L, ENCF_ERR_LEVEL_MISMATCH, "export: L_conv above the ciphertext level");
+            if (L0 < 0) L0 = x.L;
+            need(x.L == L0, ENCF_ERR_LEVEL_MISMATCH, "export_many: mixed levels");
+            for (int comp = 0; comp < 2; comp++)
+                k_copy(x.comp(comp, N), masked + cw * i + (size_t)comp * Lc * N, (size_t)Lc * N, s);
+        }
+        ntt_inverse(*c, PolyBatch{masked, (i64)Lc * N, 2 * n, c->qmap(Lc)}, s);
+        for (int i = 0; i < n; i++)
+            k_export_mask(*c, mask_seed, (0x04ull << 56) | (stream_id0 + (uint64_t)i), masked + cw * i,
+                          shares + (size_t)i * Lc * N, Lc, s);
     });
 }
 

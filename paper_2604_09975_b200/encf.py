@@ -67,6 +67,8 @@ _SIG = {
     "encf_rotate": [_p, _p, ctypes.POINTER(CT), _i32, ctypes.POINTER(CT), _p],
     "encf_rotate_hoisted": [_p, _p, ctypes.POINTER(CT), _p, _i32, _p, _p],
     "encf_conjugate": [_p, _p, ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
+    "encf_decomplexify": [_p, _p, _p, _i32, _p, _p],
+    "encf_export_c2m_many": [_p, _p, _i32, _i32, _u64, _u64, _p, _p, _p],
     "encf_rescale": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
     "encf_mod_drop": [_p, ctypes.POINTER(CT), _i32, ctypes.POINTER(CT), _p],
     "encf_complexify": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
@@ -345,6 +347,15 @@ class Context:
         _chk(_lib.encf_conjugate(self.h, keys.h, ctypes.byref(a._c()), ctypes.byref(c), _stream()), "conjugate")
         return out._update(c)
 
+    def decomplexify(self, keys, cts):
+        """[c + conj(c) (scale x 2) for c in cts] in one batched conjugation (encf_decomplexify)."""
+        n = len(cts)
+        ins = (CT * n)(*[c._c() for c in cts])
+        outs_py = [self.empty_ct(c.n_limbs, 2) for c in cts]
+        outs = (CT * n)(*[o._c() for o in outs_py])
+        _chk(_lib.encf_decomplexify(self.h, keys.h, ctypes.cast(ins, _p), n, ctypes.cast(outs, _p), _stream()), "decomplexify")
+        return [o._update(outs[i]) for i, o in enumerate(outs_py)]
+
     def rescale(self, a):
         out = self.empty_ct(max(a.n_limbs - 1, 1), a.n_comp)
         c = out._c()
@@ -384,6 +395,19 @@ class Context:
         _chk(_lib.encf_export_c2m(self.h, ctypes.byref(ct._c()), int(L_conv), int(mask_seed), int(stream_id), ctypes.byref(c),
                                   share.data_ptr(), _stream()), "export_c2m")
         return masked._update(c), share
+
+    def export_c2m_many(self, cts, L_conv, mask_seed, stream_id0):
+        """Batched encf_export_c2m: ciphertext i with stream id stream_id0 + i.  Returns [(masked ct, share)]
+        as views into two contiguous device buffers."""
+        n, N = len(cts), self.N
+        masked = torch.empty(n * 2 * L_conv * N, dtype=torch.int64, device=self.device)
+        shares = torch.empty(n * L_conv * N, dtype=torch.int64, device=self.device)
+        ins = (CT * n)(*[c._c() for c in cts])
+        _chk(_lib.encf_export_c2m_many(self.h, ctypes.cast(ins, _p), n, int(L_conv), int(mask_seed), int(stream_id0),
+                                       masked.data_ptr(), shares.data_ptr(), _stream()), "export_c2m_many")
+        w = 2 * L_conv * N
+        return [(Ciphertext(masked[i * w:(i + 1) * w], 2, L_conv, cts[i].scale, 0), shares[i * L_conv * N:(i + 1) * L_conv * N])
+                for i in range(n)]
 
     def mod_reduce(self, tensor, n_polys, n_limbs):
         _chk(_lib.encf_mod_reduce(self.h, tensor.data_ptr(), n_polys, n_limbs, _stream()), "mod_reduce")

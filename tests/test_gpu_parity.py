@@ -139,6 +139,19 @@ def test_rotations_conj_bit_exact(c13, keys13, L):
     assert_ct_equal(c13, c13.conjugate(gk, d), O.conjugate(P13, ok, ct), "conj")
 
 
+def test_decomplexify_batched_bit_exact(c13, keys13):
+    """encf_decomplexify (G3): c + conj(c) for a batch of ciphertexts in one conjugation launch
+    sequence equals the oracle's add(c, conjugate(c)) on every limb; the scale doubles."""
+    ok, gk = keys13
+    L = 4
+    cts = [O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 40 + i), 2.0 ** 40, L), 60 + i)
+           for i in range(3)]
+    outs = c13.decomplexify(gk, [dev_ct(c13, ct) for ct in cts])
+    for i, (ct, got) in enumerate(zip(cts, outs)):
+        ref = O.Ct(O.add(P13, ct, O.conjugate(P13, ok, ct)).c, 2.0 * ct.scale)   # scale x 2 (G3)
+        assert_ct_equal(c13, got, ref, "decomplexify %d" % i)
+
+
 def test_tensor_relin_rescale_bit_exact(c13, keys13):
     ok, gk = keys13
     a = O.encrypt_sk(P13, ok, O.encode(P13, synth.complex_slots(P13.n, 20), 2.0 ** 40, 7), 1)
@@ -308,6 +321,19 @@ def test_export_c2m_bit_exact(c13, keys13):
     rm, rs = K.export_c2m(P13, ref, Lc, synth.seed_mask(0), 0)
     assert np.array_equal(c13.to_host(masked, coeff=False), rm.c)
     assert np.array_equal(share.cpu().numpy().view(np.uint64).reshape(Lc, P13.N), rs)
+
+
+def test_export_c2m_many_bit_exact(c13, keys13):
+    """Batched export (encf_export_c2m_many): ciphertext i with stream id 7 + i equals the oracle's export of it."""
+    ok, gk = keys13
+    cts = [O.encrypt_sk(P13, ok, O.encode(P13, synth.fixed_point_uniform(P13.n, 70 + i), 2.0 ** 40, 4), 80 + i)
+           for i in range(3)]
+    Lc = c13.l_conv()
+    outs = c13.export_c2m_many([dev_ct(c13, ct) for ct in cts], Lc, synth.seed_mask(1), 7)
+    for i, (ct, (masked, share)) in enumerate(zip(cts, outs)):
+        rm, rs = K.export_c2m(P13, ct, Lc, synth.seed_mask(1), 7 + i)
+        assert np.array_equal(c13.to_host(masked, coeff=False), rm.c), i
+        assert np.array_equal(share.cpu().numpy().view(np.uint64).reshape(Lc, P13.N), rs), i
 
 
 def test_m2c_import_bit_exact(c13, keys13):
