@@ -763,7 +763,14 @@ void k_decode_limb0(encf_ctx& c, const u64* coeff0, double scale, double* re, do
 // per-ciphertext launch sequence).  Request tables travel by value as kernel parameters.
 namespace {
 
-__global__ void __launch_bounds__(TB, 4) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
+#ifndef KS_PAIRS_V
+#define KS_PAIRS_V 2
+#endif
+constexpr int KS_PAIRS = KS_PAIRS_V;
+#ifndef KS_MINB
+#define KS_MINB 2
+#endif
+__global__ void __launch_bounds__(TB, KS_MINB) ks_inner_batch_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
                                                             LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
     // Two coefficients (k, k+1), k even, per thread: the Galois gather maps them to the aligned pair
     // {s, s^1} (brv flips the low bit), so every operand moves with 128-bit loads.
@@ -775,31 +782,57 @@ __global__ void __launch_bounds__(TB, 4) ks_inner_batch_kernel(KsInnerBatch B, i
     const ModConst mc = mod[em.mod[e]];
     const int kle = klm.kl[e];
     const uint32_t mask2n = 2 * N - 1;
-    for (int kp = blockIdx.x * blockDim.x + threadIdx.x; 2 * kp < N; kp += gridDim.x * blockDim.x) {
-        const int k = 2 * kp;
-        int base = k, swap = 0;
-        if (g != 1) {
-            uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
-            uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
-            int src = brv((int)((e2 - 1) >> 1), logN);
-            base = src & ~1;
-            swap = src & 1;
+    // KS_PAIRS coefficient pairs per thread (kp, kp + stride, ...): every pair's ext and key loads are issued
+    // before the first multiply (the one-pair loop was long_scoreboard-bound at 3.6 TB/s, profiles/r01_ncu_top_kernels_s4.md)
+    const int stride = gridDim.x * blockDim.x;
+    for (int kp0 = blockIdx.x * blockDim.x + threadIdx.x; 2 * kp0 < N; kp0 += KS_PAIRS * stride) {
+        int kk[KS_PAIRS], base[KS_PAIRS], swap[KS_PAIRS];
+        bool ok[KS_PAIRS];
+#pragma unroll
+        for (int p = 0; p < KS_PAIRS; p++) {
+            const int k = 2 * (kp0 + p * stride);
+            ok[p] = k < N;
+            kk[p] = ok[p] ? k : 0;
+            base[p] = kk[p];
+            swap[p] = 0;
+            if (g != 1) {
+                uint32_t ee = 2u * (uint32_t)brv(kk[p], logN) + 1u;
+                uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+                int src = brv((int)((e2 - 1) >> 1), logN);
+                base[p] = src & ~1;
+                swap[p] = src & 1;
+            }
         }
-        U128 a0{0, 0}, a1{0, 0}, b0{0, 0}, b1{0, 0};
+        U128 a0[KS_PAIRS], a1[KS_PAIRS], b0[KS_PAIRS], b1[KS_PAIRS];
+#pragma unroll
+        for (int p = 0; p < KS_PAIRS; p++) a0[p] = a1[p] = b0[p] = b1[p] = U128{0, 0};
         for (int j = 0; j < dnum; j++) {
-            ulonglong2 x = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base));
-            if (swap) { u64 t = x.x; x.x = x.y; x.y = t; }
             const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            const ulonglong2 k0 = __ldg((const ulonglong2*)(kj + (size_t)kle * N + k));
-            const ulonglong2 k1 = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + k));
-            mac128(a0, x.x, k0.x);
-            mac128(b0, x.y, k0.y);
-            mac128(a1, x.x, k1.x);
-            mac128(b1, x.y, k1.y);
+            ulonglong2 x[KS_PAIRS], k0[KS_PAIRS], k1[KS_PAIRS];
+#pragma unroll
+            for (int p = 0; p < KS_PAIRS; p++) {
+                x[p] = __ldg((const ulonglong2*)(ext + ((size_t)j * nl + e) * N + base[p]));
+                k0[p] = __ldg((const ulonglong2*)(kj + (size_t)kle * N + kk[p]));
+                k1[p] = __ldg((const ulonglong2*)(kj + ((size_t)key_nl + kle) * N + kk[p]));
+            }
+#pragma unroll
+            for (int p = 0; p < KS_PAIRS; p++) {
+                if (swap[p]) { u64 t = x[p].x; x[p].x = x[p].y; x[p].y = t; }
+                mac128(a0[p], x[p].x, k0[p].x);
+                mac128(b0[p], x[p].y, k0[p].y);
+                mac128(a1[p], x[p].x, k1[p].x);
+                mac128(b1[p], x[p].y, k1[p].y);
+            }
         }
         // keys are stored in Montgomery form (k R mod q, R = 2^64): one REDC returns sum_j x_j k_j mod q
-        *(ulonglong2*)(acc + (size_t)e * N + k) = make_ulonglong2(redc128(a0, mc.q, mc.qinv), redc128(b0, mc.q, mc.qinv));
-        *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(a1, mc.q, mc.qinv), redc128(b1, mc.q, mc.qinv));
+#pragma unroll
+        for (int p = 0; p < KS_PAIRS; p++) {
+            if (!ok[p]) continue;
+            *(ulonglong2*)(acc + (size_t)e * N + kk[p]) =
+                make_ulonglong2(redc128(a0[p], mc.q, mc.qinv), redc128(b0[p], mc.q, mc.qinv));
+            *(ulonglong2*)(acc + ((size_t)nl + e) * N + kk[p]) =
+                make_ulonglong2(redc128(a1[p], mc.q, mc.qinv), redc128(b1[p], mc.q, mc.qinv));
+        }
     }
 }
 
@@ -1170,7 +1203,7 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
         kl.kl[e] = key_limb_of.mod[e];
         em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
     }
-    dim3 grid((c.N / 2 + TB - 1) / TB, nl, nreq);
+    dim3 grid((c.N / 2 + TB * KS_PAIRS - 1) / (TB * KS_PAIRS), nl, nreq);
     const uint64_t bytes = (uint64_t)nreq * ((uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8);
     int slot;
     c.prof_begin("ks_inner", s, bytes, slot);
