@@ -340,6 +340,7 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
 
 template <int LT, bool INV>
 __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int lines) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // predecessor's writes visible (PDL)
     const int mi = a.map.mod[blockIdx.y];
     if ((a.fpmask >> mi) & 1ull) {
         cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
@@ -468,6 +469,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
 
 template <int LT, bool INV>
 __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int lines, int lgc) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // predecessor's writes visible (PDL)
     const int mi = a.map.mod[blockIdx.y];
     if ((a.fpmask >> mi) & 1ull) {
         rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
@@ -477,10 +479,31 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
     }
 }
 
+// Programmatic dependent launch (ENCF_PDL, default on): every NTT phase kernel is launched with the programmatic
+// stream-serialization attribute and waits (griddepcontrol.wait) for its predecessor's memory before its first
+// load, so its CTA launch and index set-up overlap the predecessor's tail instead of a full launch gap.
+#ifndef NTT_PDL
+#define NTT_PDL 1
+#endif
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, int threads, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = NTT_PDL;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+}
+
 template <bool INV>
 void launch_cols(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines) {
     switch (LT) {
-#define C(LTV) case LTV: ntt_cols_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines); break;
+#define C(LTV) case LTV: launch_pdl(ntt_cols_r<LTV, INV>, grid, threads, smem, s, a, lines); break;
         C(2) C(3) C(4) C(5) C(6) C(7) C(8)
 #undef C
         default: throw EncfError(ENCF_ERR_ARG, "ntt: unsupported phase size");
@@ -490,7 +513,7 @@ void launch_cols(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, co
 template <bool INV>
 void launch_rows(int LT, dim3 grid, int threads, size_t smem, cudaStream_t s, const NttArgs& a, int lines, int lgc) {
     switch (LT) {
-#define C(LTV) case LTV: ntt_rows_r<LTV, INV><<<grid, threads, smem, s>>>(a, lines, lgc); break;
+#define C(LTV) case LTV: launch_pdl(ntt_rows_r<LTV, INV>, grid, threads, smem, s, a, lines, lgc); break;
         C(2) C(3) C(4) C(5) C(6) C(7) C(8)
 #undef C
         default: throw EncfError(ENCF_ERR_ARG, "ntt: unsupported phase size");
