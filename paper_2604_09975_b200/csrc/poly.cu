@@ -1380,6 +1380,56 @@ __global__ void __launch_bounds__(TB) sum_csr_kernel(const SumDev* __restrict__ 
     }
 }
 
+// Two-component variant: two coefficients per thread (128-bit loads), both components in one pass over the terms
+// (one term-descriptor load per term instead of two), and the next term's three loads issued before the current
+// term's products (the one-word loop was latency-bound at ~2.5 TB/s).
+__global__ void __launch_bounds__(TB) sum_csr2_kernel(const SumDev* __restrict__ terms, const int* __restrict__ off,
+                                                      u64* const* __restrict__ outs, int level, int N,
+                                                      const ModConst* __restrict__ mod, LimbMap lm) {
+    const int o = blockIdx.z, limb = blockIdx.y;
+    const ModConst mc = mod[lm.mod[limb]];
+    const size_t cs = (size_t)level * N;
+    const int t0 = off[o], t1 = off[o + 1];
+    u64* out = outs[o];
+    for (int kp = blockIdx.x * blockDim.x + threadIdx.x; 2 * kp < N; kp += gridDim.x * blockDim.x) {
+        const size_t idx = (size_t)limb * N + 2 * kp;
+        u64 r00 = 0, r01 = 0, r10 = 0, r11 = 0;   // [component][coefficient]
+        for (int ta = t0; ta < t1; ta += 128) {
+            U128 a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
+            const int tb = min(t1, ta + 128);
+            int t = ta;
+            for (; t + 2 <= tb; t += 2) {
+                const SumDev d0 = terms[t], d1 = terms[t + 1];
+                const ulonglong2 x0 = __ldg((const ulonglong2*)(d0.ct + idx));
+                const ulonglong2 y0 = __ldg((const ulonglong2*)(d0.ct + cs + idx));
+                const ulonglong2 x1 = __ldg((const ulonglong2*)(d1.ct + idx));
+                const ulonglong2 y1 = __ldg((const ulonglong2*)(d1.ct + cs + idx));
+                const ulonglong2 m0 = d0.mask ? __ldg((const ulonglong2*)(d0.mask + idx)) : make_ulonglong2(0, 0);
+                const ulonglong2 m1 = d1.mask ? __ldg((const ulonglong2*)(d1.mask + idx)) : make_ulonglong2(0, 0);
+                if (d0.mask) { mac128(a00, x0.x, m0.x); mac128(a01, x0.y, m0.y); mac128(a10, y0.x, m0.x); mac128(a11, y0.y, m0.y); }
+                else { add128(a00, x0.x); add128(a01, x0.y); add128(a10, y0.x); add128(a11, y0.y); }
+                if (d1.mask) { mac128(a00, x1.x, m1.x); mac128(a01, x1.y, m1.y); mac128(a10, y1.x, m1.x); mac128(a11, y1.y, m1.y); }
+                else { add128(a00, x1.x); add128(a01, x1.y); add128(a10, y1.x); add128(a11, y1.y); }
+            }
+            if (t < tb) {
+                const SumDev d0 = terms[t];
+                const ulonglong2 x0 = __ldg((const ulonglong2*)(d0.ct + idx));
+                const ulonglong2 y0 = __ldg((const ulonglong2*)(d0.ct + cs + idx));
+                if (d0.mask) {
+                    const ulonglong2 m0 = __ldg((const ulonglong2*)(d0.mask + idx));
+                    mac128(a00, x0.x, m0.x); mac128(a01, x0.y, m0.y); mac128(a10, y0.x, m0.x); mac128(a11, y0.y, m0.y);
+                } else { add128(a00, x0.x); add128(a01, x0.y); add128(a10, y0.x); add128(a11, y0.y); }
+            }
+            r00 = add_mod(r00, barrett128(a00, mc.q, mc.rhi, mc.rlo), mc.q);
+            r01 = add_mod(r01, barrett128(a01, mc.q, mc.rhi, mc.rlo), mc.q);
+            r10 = add_mod(r10, barrett128(a10, mc.q, mc.rhi, mc.rlo), mc.q);
+            r11 = add_mod(r11, barrett128(a11, mc.q, mc.rhi, mc.rlo), mc.q);
+        }
+        *(ulonglong2*)(out + idx) = make_ulonglong2(r00, r01);
+        *(ulonglong2*)(out + cs + idx) = make_ulonglong2(r10, r11);
+    }
+}
+
 // outs[o] = sum_{t in [off[o], off[o+1])} (a0 b0, a0 b1 + a1 b0, a1 b1)
 __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restrict__ pairs, const int* __restrict__ off,
                                                         u64* const* __restrict__ outs, int level, int N,
@@ -1419,9 +1469,14 @@ __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restric
 void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* outs, int nout, int nterms, int ncomp, int level,
                cudaStream_t s, const LimbMap* lmap) {
     LimbMap lm = lmap ? *lmap : c.qmap(level);
-    dim3 grid((c.N + TB - 1) / TB, level, nout);
     { int _slot; c.prof_begin("sum_csr_kernel", s, 0, _slot);
-    sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod, lm);
+    if (ncomp == 2) {
+        dim3 grid((c.N / 2 + TB - 1) / TB, level, nout);
+        sum_csr2_kernel<<<grid, TB, 0, s>>>(terms, off, outs, level, c.N, c.d_mod, lm);
+    } else {
+        dim3 grid((c.N + TB - 1) / TB, level, nout);
+        sum_csr_kernel<<<grid, TB, 0, s>>>(terms, off, outs, ncomp, level, c.N, c.d_mod, lm);
+    }
     c.prof_end(_slot, s); }
     c.st_launch++;
     c.st_bytes += (uint64_t)nterms * ncomp * level * c.N * 8 * 2 + (uint64_t)nout * ncomp * level * c.N * 8;
