@@ -1159,6 +1159,33 @@ __global__ void gather_copy_kernel(CopyBatch C, u64* dst, i64 dst_stride, size_t
     }
 }
 
+// Same copy, two coefficients (k, k+1), k even, per thread with 128-bit loads/stores: the Galois gather maps them
+// to the aligned source pair {s, s^1} (brv flips the lowest bit), as in ks_inner_batch_kernel.
+__global__ void gather_copy2_kernel(CopyBatch C, u64* dst, i64 dst_stride, size_t words, int N, int logN) {
+    const int p = blockIdx.y;
+    const u64* __restrict__ src = C.src[p];
+    const uint32_t g = C.g[p];
+    u64* d = dst + (size_t)p * dst_stride;
+    const uint32_t mask2n = 2 * N - 1;
+    const size_t pairs = words / 2;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < pairs; i += (size_t)gridDim.x * blockDim.x) {
+        const size_t w = 2 * i;
+        const size_t limb = w / N;
+        const int k = (int)(w % N);
+        int base = k, swap = 0;
+        if (g != 1) {
+            const uint32_t e = 2u * (uint32_t)brv(k, logN) + 1u;
+            const uint32_t e2 = (uint32_t)(((uint64_t)e * g) & mask2n);
+            const int sidx = brv((int)((e2 - 1) >> 1), logN);
+            base = sidx & ~1;
+            swap = sidx & 1;
+        }
+        ulonglong2 x = __ldg((const ulonglong2*)(src + limb * N + base));
+        if (swap) { const u64 t = x.x; x.x = x.y; x.y = t; }
+        *(ulonglong2*)(d + w) = x;
+    }
+}
+
 __global__ void rescale_prep_batch_kernel(const u64* last, u64* corr, int level, int N, const ModConst* mod, const u64* hmod) {
     const int p = blockIdx.y;
     const int nl = level - 1;
@@ -1321,9 +1348,16 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
 }
 
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s) {
-    dim3 grid(nblocks(words, TB, 512), n);
     { int _slot; c.prof_begin("gather_copy_kernel", s, 0, _slot);
-    gather_copy_kernel<<<grid, TB, 0, s>>>(C, dst, dst_stride, words, c.N, c.logN);
+    bool aligned = (words % 2 == 0) && (dst_stride % 2 == 0) && ((uintptr_t)dst % 16 == 0);
+    for (int i = 0; i < n; i++) aligned = aligned && ((uintptr_t)C.src[i] % 16 == 0);
+    if (aligned) {
+        dim3 grid(nblocks(words / 2, TB, 512), n);
+        gather_copy2_kernel<<<grid, TB, 0, s>>>(C, dst, dst_stride, words, c.N, c.logN);
+    } else {
+        dim3 grid(nblocks(words, TB, 512), n);
+        gather_copy_kernel<<<grid, TB, 0, s>>>(C, dst, dst_stride, words, c.N, c.logN);
+    }
     c.prof_end(_slot, s); }
     c.st_launch++; c.st_bytes += (uint64_t)n * words * 16;
 }
