@@ -1192,12 +1192,15 @@ __global__ void rescale_prep_batch_kernel(const u64* last, u64* corr, int level,
     const u64* lp_in = last + (size_t)p * N;
     u64* cr = corr + (size_t)p * nl * N;
     u64 qL = mod[level - 1].q, h = qL / 2;
-    const size_t total = (size_t)nl * N;
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-        int limb = (int)(i / N), k = (int)(i % N);
-        u64 qi = mod[limb].q;
-        u64 lp = add_mod(lp_in[k], h, qL);
-        cr[i] = sub_mod(lp % qi, hmod[limb], qi);
+    const size_t pairs = (size_t)nl * N / 2;   // two coefficients per thread, 128-bit accesses
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < pairs; i += (size_t)gridDim.x * blockDim.x) {
+        const int limb = (int)(2 * i / N), k = (int)(2 * i % N);
+        const ModConst mc = mod[limb];
+        const ulonglong2 x = __ldg((const ulonglong2*)(lp_in + k));
+        const u64 l0 = add_mod(x.x, h, qL), l1 = add_mod(x.y, h, qL);
+        // l mod q_i by Barrett (the 64-bit % was a software division per word)
+        const u64 r0 = barrett128(U128{l0, 0}, mc.q, mc.rhi, mc.rlo), r1 = barrett128(U128{l1, 0}, mc.q, mc.rhi, mc.rlo);
+        ((ulonglong2*)cr)[i] = make_ulonglong2(sub_mod(r0, hmod[limb], mc.q), sub_mod(r1, hmod[limb], mc.q));
     }
 }
 
@@ -1363,7 +1366,7 @@ void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_str
 }
 
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s) {
-    dim3 grid(nblocks((size_t)(level - 1) * c.N, TB, 256), npolys);
+    dim3 grid(nblocks((size_t)(level - 1) * c.N / 2, TB, 256), npolys);
     { int _slot; c.prof_begin("rescale_prep_batch_kernel", s, 0, _slot);
     rescale_prep_batch_kernel<<<grid, TB, 0, s>>>(last, corr, level, c.N, c.d_mod, c.rescale[level].d_hmod);
     c.prof_end(_slot, s); }
