@@ -164,9 +164,9 @@ __global__ void rescale_prep_kernel(const u64* last, i64 ls, u64* corr, int ncom
         int c = (int)(i / per);
         size_t r = i % per;
         int limb = (int)(r / N), k = (int)(r % N);
-        u64 qi = mod[limb].q;
+        const ModConst mc = mod[limb];
         u64 lp = add_mod(last[c * ls + k], h, qL);
-        corr[i] = sub_mod(lp % qi, hmod[limb], qi);
+        corr[i] = sub_mod(barrett128(U128{lp, 0}, mc.q, mc.rhi, mc.rlo), hmod[limb], mc.q);
     }
 }
 
