@@ -407,6 +407,86 @@ def Psi_hoisted(ev, x, ts, m, N_seg, seg0=0, nseg=None):
     return out
 
 
+def slot_range_desc(lo, hi, m):
+    """Mask descriptor + row grid of the slot range [lo, hi): the m-row grid when the range is segment
+    aligned, else the 1-row grid (every slot its own 'segment')."""
+    if lo % m == 0 and hi % m == 0:
+        return (0, m, lo // m, 1, (hi - lo) // m), m
+    return (0, 1, lo, 1, hi - lo), 1
+
+
+def rotfirst_masks(Ls, tau, m):
+    """a_{L,tau} = 1{0 <= i < L - tau}, b_{L,tau} = 1{L - tau <= i < L}  (Alg A.3 line 2), as
+    (descriptor, grid) pairs; b is None for tau = 0."""
+    a = slot_range_desc(0, Ls - tau, m)
+    b = slot_range_desc(Ls - tau, Ls, m) if tau else None
+    return a, b
+
+
+def rotfirst_reference(x, Ls, tau):
+    """Slot-level definition of RotFirst_L(x; tau) (Alg A.3 Ensure, with G21: slots >= L come out zero):
+    out[i] = x[(i + tau) mod L] for i < L, 0 otherwise."""
+    x = np.asarray(x)
+    out = np.zeros_like(x)
+    idx = (np.arange(Ls) + tau) % Ls
+    out[:Ls] = x[idx]
+    return out
+
+
+def RotFirst_hoisted(ev, x, Ls, taus, m):
+    """RotFirst_L(x; tau) for every tau in taus from ONE hoisted ModUp of x (Alg A.3):
+        tau <- tau mod L;  y1 = rot(x; tau) (.) a_{L,tau};  y2 = rot(x; (tau - L) mod n) (.) b_{L,tau};  y1 + y2,
+    then rescale (the masks are plaintexts at scale q_{L-1}, DESIGN.md R-MASK).  As for Psi (R-LAZY) the two
+    rotations stay in Q_L u P, are masked there and divided by P q_{L-1} at once.  tau = 0 is x (.) a_{L,0}
+    then rescale (Alg A.3 with rot(x; 0) and an empty b; no key switch), so every output shares one level."""
+    L = x.L
+    tt = [int(t) % Ls for t in taus]
+    steps = []
+    for t in tt:
+        if t:
+            steps += [t, t - Ls]
+    rots = ev.rot_hoisted_ext(x, steps) if steps else []
+    out, i = [], 0
+    for t in tt:
+        (ad, am), bb = rotfirst_masks(Ls, t, m)
+        if t == 0:
+            out.append(ev.rescale(ev.ptmul(x, ev.mask(ad, L, am))))
+        else:
+            bd, bm = bb
+            y = ev.ext_masked_sum([rots[i], rots[i + 1]], [ev.mask_ext(ad, L, am), ev.mask_ext(bd, L, bm)],
+                                  x.scale * ev.mask_scale(L))
+            out.append(ev.moddown_rescale(y))
+            i += 2
+    return out
+
+
+def rotfirst_ext(ev, c, Ls, tau, m):
+    """RotFirst_L(c; tau) BEFORE its ModDown and rescale: the extended-basis masked pair
+    rot_ext(c, tau) (.) a + rot_ext(c, tau - L) (.) b (both rotations from one hoisted ModUp; tau = 0: P c (.) a).
+    Its moddown_rescale is RotFirst_hoisted(c, [tau]); sums of such terms are ModDown'ed once (R-LAZY)."""
+    L = c.L
+    tau = int(tau) % Ls
+    (ad, am), bb = rotfirst_masks(Ls, tau, m)
+    sc = c.scale * ev.mask_scale(L)
+    if tau == 0:
+        return ev.ext_masked_sum([ev.lift_ext(c)], [ev.mask_ext(ad, L, am)], sc)
+    r = ev.rot_hoisted_ext(c, [tau, tau - Ls])
+    bd, bm = bb
+    return ev.ext_masked_sum(r, [ev.mask_ext(ad, L, am), ev.mask_ext(bd, L, bm)], sc)
+
+
+def Phi_C(ev, x, deltas, C, m, N_seg):
+    """Phi_C^Delta (Alg A.4, P:1258-1270): C <- min(C, N_seg), Delta <- Delta mod C, RotFirst_{Cm}(x; Delta m);
+    one hoisted batch over deltas."""
+    C = min(C, N_seg)
+    return RotFirst_hoisted(ev, x, C * m, [(int(d) % C) * m for d in deltas], m)
+
+
+def Align(ev, x, H, r, m):
+    """Block phase correction Align_r(x) = RotFirst_{Hm}(x, (H - r) m)  (App. A.3)."""
+    return RotFirst_hoisted(ev, x, H * m, [(H - r) * m], m)[0]
+
+
 # ====================================================================================== projection (§3.2, App. A.2)
 class ProjPlan:
     """Plan of the shared pt-ct projection Y = X W.
@@ -421,10 +501,23 @@ class ProjPlan:
         self.real_input = real_input          # fused QK: real inputs, complex weights (G1)
         self.U = self.G if real_input else -(-self.G // 2)
         self.B_out = -(-d_out // self.C)
+        if self.C > self.N_seg:
+            raise O.OracleError("PLAN_SHAPE: C > n/m")
         if N1 is None:
             N1 = default_n1(self.C, self.B_out, self.U)
         assert self.C % N1 == 0
         self.N1, self.N2 = N1, self.C // N1
+        # C < N_seg: the segment shifts wrap modulo the C active segments (Phi_C = RotFirst_{Cm}, Alg A.4); the
+        # bank and the giant fold each spend one level (masks), so y_b lands 3 levels below x (reading R-PHIC)
+        self.restricted = self.C < self.N_seg
+
+    def weight_level(self, L):
+        """Level of the weight plaintexts for inputs at level L (the bank's level)."""
+        return L - 1 if self.restricted else L
+
+    def out_levels(self):
+        """Levels the projection consumes (input level - output level)."""
+        return 3 if self.restricted else 1
 
 
 def default_n1(C, B_out, U):
@@ -496,6 +589,9 @@ def projection_partial(ev, plan, xt, w, u0, u1):
     m, N1 = plan.m, plan.N1
     bank = []
     for u in range(plan.U):
+        if plan.restricted:                     # bank[u][q] = Phi_C^q(x~_u) (Alg A.4), one level
+            bank.append(Phi_C(ev, xt[u], list(range(N1)), plan.C, m, plan.N_seg))
+            continue
         rots = ev.rot_hoisted(xt[u], [q * m for q in range(1, N1)]) if N1 > 1 else []
         bank.append([xt[u]] + list(rots))
     accs = {}
@@ -504,7 +600,10 @@ def projection_partial(ev, plan, xt, w, u0, u1):
         cts = [bank[u][q] for u in range(plan.U) for q in range(N1)]
         pts = [w(b, p, u, q) for u in range(plan.U) for q in range(N1)]
         c = ev.mac_ptmul(cts, pts)
-        e = ev.rot_ext(c, p * N1 * m)          # p = 0: P * c (exact lift); p >= 1: rotation without ModDown (R-LAZY)
+        if plan.restricted:                     # Phi_C^{p N1}(c~_{b,p}) = RotFirst_{Cm}(c; p N1 m), masked in Q_L u P
+            e = rotfirst_ext(ev, c, plan.C * m, p * N1 * m, m)
+        else:
+            e = ev.rot_ext(c, p * N1 * m)      # p = 0: P * c (exact lift); p >= 1: rotation without ModDown (R-LAZY)
         accs[b] = e if b not in accs else ev.ext_add(accs[b], e)
     return accs                                 # extended-basis partial accumulators (reduced across ranks as such)
 
@@ -512,7 +611,7 @@ def projection_partial(ev, plan, xt, w, u0, u1):
 def projection_finalize(ev, plan, acc_ext, decomplexify=True):
     """C6 steps 4-5 on an extended accumulator: acc = ModDown(acc_ext) (one per block, R-LAZY);
     z = acc + conj(acc) (scale x2, G2/G3) formed in Q_L u P and divided by P q_{L-1} at once."""
-    acc = ev.moddown(acc_ext)
+    acc = ev.moddown_rescale(acc_ext) if plan.restricted else ev.moddown(acc_ext)   # restricted: fold masks' level
     if decomplexify:
         z = ev.ext_add(ev.lift_ext(acc), ev.conj_ext(acc))
         z.scale = acc.scale * 2.0
@@ -548,8 +647,13 @@ class ScorePlan:
             while C_qk * 2 <= self.N_seg and C_qk < H * d_h:
                 C_qk *= 2
         self.C = C_qk
-        assert C_qk % H == 0 and C_qk <= self.N_seg, "C_qk must be a multiple of H (phases r_l = 0, G8)"
+        if not (H <= C_qk <= self.N_seg):
+            raise O.OracleError("PLAN_SHAPE: need H <= C_qk <= n/m")
         self.B = -(-(H * d_h) // C_qk)
+        # head phase of block l: r_l = l C mod H (App. A.3); C mod H != 0 -> Align_r per phase group
+        self.phases = [(l * C_qk) % H for l in range(self.B)]
+        self.aligned = any(self.phases)
+        self.k_route = -(-C_qk // H)                 # channel groups folded onto the H head segments
         self.beta = beta or default_beta(m)
         self.g = m // self.beta
         assert m % self.beta == 0 and self.g % 2 == 0
@@ -583,13 +687,39 @@ def score(ev, plan, qs, ks, ts=None, route_hoisted=True):
         kk = Psi_hoisted(ev, ks[l], kt, m, N_seg)
         kb.append({t: c for t, c in zip(kt, kk)})
     S = []
+    groups = score_phase_groups(plan)
     for t in (range(m // 2) if ts is None else ts):
         j, s = t // beta, t % beta
-        pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in range(plan.B)]
-        T = ev.relin_rescale(ev.tensor_sum(pairs))          # lazy relin merged with the rescale (R-RELRS)
-        T = route(ev, T, plan.C // H, H, m, hoisted=route_hoisted)
+        routed = {}
+        for r, ls in groups.items():          # one lazy tensor sum per head phase (all blocks when C mod H = 0)
+            pairs = [(qb[l][s], ev.add(kb[l][j * beta], ev.mul_i(kb[l][m // 2 + j * beta]))) for l in ls]
+            T = ev.relin_rescale(ev.tensor_sum(pairs))          # lazy relin merged with the rescale (R-RELRS)
+            routed[r] = route(ev, T, plan.k_route, H, m, hoisted=route_hoisted)
+        if plan.aligned:
+            T = align_sum(ev, routed, H, m)
+        else:
+            T = routed[0]
         S.append(Psi_hoisted(ev, T, [s], m, N_seg, 0, H)[0])
     return S
+
+
+def score_phase_groups(plan):
+    """{r: [blocks l with l C mod H = r]} (App. A.3 "We sum score contributions by phase")."""
+    groups = {}
+    for l, r in enumerate(plan.phases):
+        groups.setdefault(r, []).append(l)
+    return groups
+
+
+def align_sum(ev, routed, H, m):
+    """sum_r Align_r(x_r) = sum_r RotFirst_{Hm}(x_r, (H - r) m)  (applied before combining phases):
+    every Align_r kept in Q_L u P (rotfirst_ext; r = 0 is the mask a_{Hm,0} alone), the phase terms summed there
+    and divided by P q_{L-1} ONCE (R-LAZY)."""
+    acc = None
+    for r in sorted(routed):
+        e = rotfirst_ext(ev, routed[r], H * m, (H - r) * m, m)
+        acc = e if acc is None else ev.ext_add(acc, e)
+    return ev.moddown_rescale(acc)
 
 
 def route(ev, x, k, H, m, hoisted=True):
