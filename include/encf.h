@@ -176,7 +176,10 @@ encf_status encf_mask_clear(encf_ctx* ctx);
  * weights are complex, W~ = Wre + i Wim (e.g. W_Q^pi_S + i W_K^pi_S); the output is Y = X Wre + i X Wim (no
  * decomplexify; incompatible with ENCF_PROJ_DECOMPLEXIFY, G1). */
 #define ENCF_PROJ_REAL_INPUT 4u
-/* Projection plan: n/m segments, C active (C = 0 -> n/m), N1 | C (0 -> default). */
+/* Projection plan: n/m segments, C active (C = 0 -> n/m), N1 | C (0 -> default).  C < n/m makes the
+ * plan RESTRICTED: the baby bank is Phi_C^q (RotFirst_{Cm}, Alg A.4) and the giant fold Phi_C^{pN1}, each spending a
+ * level, so the weights are encoded at level L - 1 (the bank level) and y_b lands at level L - 3 instead of L - 1
+ * (DESIGN.md R-PHIC).  Errors: PLAN_SHAPE (C > n/m, N1 not dividing C, fused-QK with DECOMPLEXIFY). */
 encf_status encf_proj_plan_create(encf_ctx* ctx, int32_t m, int32_t d_in, int32_t d_out, int32_t C, int32_t N1,
                                   uint32_t flags, encf_proj_plan** out);
 encf_status encf_proj_plan_destroy(encf_proj_plan* plan);
@@ -207,23 +210,53 @@ encf_status encf_pt_ct_matmul(encf_ctx* ctx, const encf_keys* keys, const encf_p
 encf_status encf_pt_ct_matmul_finalize(encf_ctx* ctx, const encf_keys* keys, const encf_proj_plan* plan,
                                        const encf_ct* acc, int32_t b_begin, int32_t b_end, encf_ct* y, void* stream);
 
-/* Attention plan: score (C_qk used segments per block, beta | m) and value (H_blk heads per block). */
+/* Attention plan: score (C_qk used segments per block, H <= C_qk <= n/m, beta | m with m/beta even) and value
+ * (H_blk heads per block).  Errors: ODD_SEQ (odd m), PLAN_SHAPE. */
 encf_status encf_attn_plan_create(encf_ctx* ctx, int32_t m, int32_t H, int32_t d_h, int32_t C_qk, int32_t beta,
                                   int32_t H_blk, encf_attn_plan** out);
 encf_status encf_attn_plan_destroy(encf_attn_plan* plan);
 /* out[0..7] = {B, beta, g, n_out (=K_min(S)), H_blk, B_V, seg_stride, C_qk} */
 encf_status encf_attn_plan_info(const encf_attn_plan* plan, int32_t* out8);
 encf_status encf_attn_galois(encf_ctx* ctx, const encf_attn_plan* plan, uint32_t* out, int32_t cap, int32_t* n);
-/* Score kernel (C7): q[B], k[B] at level L -> s_t[t] for t in [t_begin, t_end), level L-3. */
+/* Score kernel (C7): q[B], k[B] at level L -> s_t[t] for t in [t_begin, t_end), level L-3.  When
+ * C_qk mod H != 0 the blocks carry head phases r_l = l C_qk mod H: the lazy tensor sums are formed per
+ * phase, routed, aligned by Align_r = RotFirst_{Hm}(., (H - r) m) and summed (one extra level: s_t at L-4). */
 encf_status encf_ct_ct_attn_score(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
                                   const encf_ct* q, const encf_ct* k, int32_t t_begin, int32_t t_end,
                                   encf_ct* s_t, void* stream);
 /* Minimal export stream (App. A.3): s_t[m/2] -> s_min[K_min(S)] at level L-1 of s_t. */
 encf_status encf_attn_export_stream(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
                                     const encf_ct* s_t, encf_ct* s_min, void* stream);
-/* Value kernel (C8): p_fd[B_V] (level Lp), v[B_V] (level Lv >= Lp + 2) -> o[B_V] at level Lp - 2. */
+/* Value kernel (C8): p_fd[B_V] (level Lp >= 3), v[B_V] (level Lv >= Lp + 1) -> o[B_V] at
+ * level Lp - 2.  Errors: LEVEL_MISMATCH (level plan), MISSING_KEY. */
 encf_status encf_ct_ct_attn_value(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
                                   const encf_ct* p_fd, const encf_ct* v, encf_ct* o, void* stream);
+/* Sharded value kernel: units (l, t), flattened l (m/2) + t, in [unit_begin, unit_end).  For every
+ * block l the range touches (in increasing l) o3[i] receives the UNRELINEARISED partial sum_{t in range} u_t (x) b_t
+ * (3 components, level Lp - 1, caller buffers of 3 (Lp - 1) N words).  Partials of one block from several ranks are
+ * summed as uint64 (world_size q < 2^64) + encf_mod_reduce, then encf_attn_value_finalize gives exactly the bits of
+ * encf_ct_ct_attn_value.  Errors as encf_ct_ct_attn_value, plus ARG (bad range). */
+encf_status encf_ct_ct_attn_value_partial(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
+                                          const encf_ct* p_fd, const encf_ct* v, int32_t unit_begin, int32_t unit_end,
+                                          encf_ct* o3, void* stream);
+/* o[i] = rescale(relin(o3[i])) rounded once (R-RELRS) for n complete 3-component value partials at one level. */
+encf_status encf_attn_value_finalize(encf_ctx* ctx, const encf_keys* keys, const encf_ct* o3, int32_t n, encf_ct* o,
+                                     void* stream);
+
+/* ------------------------------------------------------------------------------------------ ciphertext shifts (App. A.1) */
+/* RotFirst_L(x; tau) for every tau in taus[0..n-1] (Alg A.3; G21: slots >= L come out zero):
+ * tau <- tau mod L, rot(x; tau) (.) a_{L,tau} + rot(x; tau - L) (.) b_{L,tau} with a = 1{i < L - tau},
+ * b = 1{L - tau <= i < L}, then rescale (masks at scale q_{L-1}); tau = 0 is x (.) a_{L,0}.  One hoisted ModUp,
+ * the rotations kept in Q_L u P and divided by P q_{L-1} at once (DESIGN.md R-LAZY).  Phi_C^Delta (Alg A.4) is
+ * L = C m, tau = (Delta mod C) m; Align_r is L = H m, tau = (H - r) m.  m: the segment grid used for
+ * the mask descriptors of segment-aligned ranges (other ranges use the 1-slot grid).  outs: n caller buffers,
+ * level L_in - 1.  Keys: left rotations tau and tau - L.  Errors: ARG, LEVEL_EXHAUSTED, MISSING_KEY. */
+encf_status encf_rotfirst(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in, int32_t L_slots, const int32_t* taus /*host*/,
+                          int32_t n, int32_t m, encf_ct* outs /*host array of n*/, void* stream);
+/* Psi^t(x) for every t in ts[0..n-1] (Alg A.2): rot(x; t) (.) h_t + rot(x; t - m) (.) u_t, rescale;
+ * t = 0 mod m is x (.) h_0 (DESIGN.md R-PSI0).  Same conventions as encf_rotfirst; m must divide n. */
+encf_status encf_psi(encf_ctx* ctx, const encf_keys* keys, const encf_ct* in, int32_t m, const int32_t* ts /*host*/, int32_t n,
+                     encf_ct* outs /*host array of n*/, void* stream);
 
 /* ------------------------------------------------------------------------------------------ export (Alg 3, GPU half) */
 /* L_conv rule: smallest L with log2 Q_L >= ell + sigma + 1 and Q_L / 2 > scale * B_max.

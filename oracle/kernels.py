@@ -842,36 +842,53 @@ def value_p_slots(Ph, plan, l):
     return z
 
 
-def value(ev, plan, ps, vs, blocks=None):
-    """C8 (P:425-455 with G9: u_t = Psi^{+t} u):
+def value_partial(ev, plan, ps, vs, u0, u1):
+    """C8 steps 1-5 for the units (l, t), flattened l (m/2) + t, in [u0, u1) -- the multi-GPU partition of the
+    value kernel: {l: o3_l} with o3_l = sum over the range's t of u_t (x) b_t, UNRELINEARISED.  Every
+    object of a unit (u_t, the Phi-bank rotations Phi^{t-u}(p), b_t) has the same bits as in the full kernel (each
+    hoisted rotation depends only on its input and offset), so summing the partials of a block over a partition of
+    its t (exact modular sum) gives the full kernel's relinearisation input.
       1. uu = v (.) e_all - i (rot(v, m/2)(.)h_{m/2} + rot(v, -m/2)(.)u_{m/2}), ONE rescale
-      2. U bank: u_t = Psi^{t}(uu), t = 0..m/2-1 (hoisted)
-      3. Phi bank of p_fd: delta in [-(d_h-1), m/2-1] (hoisted single rotations by delta m)
+      2. U bank: u_t = Psi^{t}(uu) (hoisted; G9: +t)
+      3. Phi bank of p_fd: delta in [t_lo - (d_h - 1), t_hi - 1] (hoisted single rotations by delta m)
       4. b_t = sum_u Phi^{t-u}(p_fd) (.) n_u, rescale
-      5. o = sum_t u_t (x) b_t (u_t mod-dropped to b_t's level), ONE relin, rescale."""
+      5. sum_t u_t (x) b_t (u_t mod-dropped to b_t's level)"""
     m, N_seg = plan.m, plan.N_seg
     half = m // 2
-    outs = []
-    for l in (range(plan.B_V) if blocks is None else blocks):
+    out = {}
+    for l in range(plan.B_V):
+        ta, tb = max(u0 - l * half, 0), min(u1 - l * half, half)
+        if ta >= tb:
+            continue
         v, p = vs[l], ps[l]
         Lv = v.L
         rv = ev.rot_hoisted(v, [half, half - m])
         hd, ud = psi_masks(half, m, N_seg)
         sh = ev.add(ev.ptmul(rv[0], ev.mask(hd, Lv, m)), ev.ptmul(rv[1], ev.mask(ud, Lv, m)))
         uu = ev.rescale(ev.sub(ev.ptmul(v, ev.mask((0, m, 0, 1, N_seg), Lv, m)), ev.mul_i(sh)))
-        ub = Psi_hoisted(ev, uu, list(range(half)), m, N_seg)
-        deltas = [d for d in range(-(plan.d_h - 1), half) if d != 0]
+        ub = dict(zip(range(ta, tb), Psi_hoisted(ev, uu, list(range(ta, tb)), m, N_seg)))
+        deltas = [d for d in range(ta - (plan.d_h - 1), tb) if d != 0]
         pb = dict(zip(deltas, ev.rot_hoisted(p, [d * m for d in deltas])))
         pb[0] = p
         Lp = p.L
-        bt = []
-        for t in range(half):
+        pairs = []
+        for t in range(ta, tb):
             cts = [pb[t - u] for u in range(plan.d_h)]
             pts = [ev.mask((0, m, u, plan.seg_stride, plan.H_blk), Lp, m) for u in range(plan.d_h)]
-            bt.append(ev.rescale(ev.mac_ptmul(cts, pts)))     # sum_u Phi^{t-u}(p) (.) n_u (exact modular sum)
-        Lb = bt[0].L
-        pairs = [(ev.mod_drop(ub[t], Lb) if ub[t].L > Lb else ub[t], bt[t]) for t in range(half)]
-        outs.append(ev.relin_rescale(ev.tensor_sum(pairs)))     # lazy relin merged with the rescale (R-RELRS)
+            bt = ev.rescale(ev.mac_ptmul(cts, pts))     # sum_u Phi^{t-u}(p) (.) n_u (exact modular sum)
+            pairs.append((ev.mod_drop(ub[t], bt.L) if ub[t].L > bt.L else ub[t], bt))
+        out[l] = ev.tensor_sum(pairs)
+    return out
+
+
+def value(ev, plan, ps, vs, blocks=None):
+    """C8 (P:425-455 with G9: u_t = Psi^{+t} u): value_partial over every unit of the requested blocks, then
+    o = ONE relin merged with the rescale (R-RELRS) per block."""
+    half = plan.m // 2
+    outs = []
+    for l in (range(plan.B_V) if blocks is None else blocks):
+        o3 = value_partial(ev, plan, ps, vs, l * half, (l + 1) * half)[l]
+        outs.append(ev.relin_rescale(o3))          # lazy relin merged with the rescale (R-RELRS)
     return outs
 
 

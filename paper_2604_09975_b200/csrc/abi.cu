@@ -30,19 +30,26 @@ void need(bool cond, encf_status code, const char* msg) {
     if (!cond) throw EncfError(code, msg);
 }
 
-DCt view(const encf_ct* c) {
+void level_ok(const encf_ctx* c, int L) { need(L >= 1 && L <= c->L, ENCF_ERR_LEVEL_MISMATCH, "n_limbs out of range"); }
+
+// Every ciphertext entering the library is validated here, before any launch: non-null context and data, NTT form,
+// 2 or 3 components, 1 <= n_limbs <= L_max (qmap() / the per-level tables are indexed by it), 16-byte aligned
+// data (the vectorised kernels use 128-bit accesses).
+DCt view(const encf_ctx* ctx, const encf_ct* c) {
+    need(ctx != nullptr, ENCF_ERR_ARG, "null context");
     need(c && c->data, ENCF_ERR_ARG, "null ciphertext");
     need(c->ntt == 1, ENCF_ERR_FORMAT, "homomorphic ops need NTT-form ciphertexts (ntt = 1)");
+    need(((uintptr_t)c->data & 15) == 0, ENCF_ERR_ARG, "ciphertext data must be 16-byte aligned");
     DCt d;
     d.d = c->data; d.ncomp = c->n_comp; d.L = c->n_limbs; d.scale = c->scale;
     need(d.ncomp == 2 || d.ncomp == 3, ENCF_ERR_FORMAT, "n_comp must be 2 or 3");
+    level_ok(ctx, d.L);
     return d;
 }
 
-void level_ok(encf_ctx* c, int L) { need(L >= 1 && L <= c->L, ENCF_ERR_LEVEL_MISMATCH, "n_limbs out of range"); }
-
 DCt outview(encf_ct* o, int L, int ncomp) {
     need(o && o->data, ENCF_ERR_ARG, "null output");
+    need(((uintptr_t)o->data & 15) == 0, ENCF_ERR_ARG, "output data must be 16-byte aligned");
     DCt d; d.d = o->data; d.L = L; d.ncomp = ncomp; return d;
 }
 
@@ -256,7 +263,7 @@ encf_status encf_encrypt_sk(encf_ctx* c, const encf_keys* k, const encf_pt* pt, 
 encf_status encf_decrypt(encf_ctx* c, const encf_keys* k, const encf_ct* ct, encf_pt* out, void* stream) {
     return guard([&] {
         need(c && k && out && out->data, ENCF_ERR_ARG, "decrypt: null argument");
-        DCt x = view(ct);
+        DCt x = view(c, ct);
         const int L = x.L, N = c->N;
         need(L <= k->max_level, ENCF_ERR_LEVEL_MISMATCH, "decrypt: level above key");
         cudaStream_t s = S(stream);
@@ -329,23 +336,24 @@ encf_status encf_poly_from_ntt(encf_ctx* c, uint64_t* d, int32_t np, int32_t nl,
 }
 
 #define EV_BEGIN(keys)            \
+    need(c != nullptr, ENCF_ERR_ARG, "null context"); \
     cudaStream_t s = S(stream);   \
     Scratch sc(s);                \
     Ev ev(*c, keys, s, sc);
 
 encf_status encf_add(encf_ctx* c, const encf_ct* a, const encf_ct* b, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(nullptr); DCt x = view(a), y = view(b); DCt o = outview(out, x.L, x.ncomp); ev.add(x, y, o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(nullptr); DCt x = view(c, a), y = view(c, b); DCt o = outview(out, x.L, x.ncomp); ev.add(x, y, o); writeback(out, o); });
 }
 encf_status encf_sub(encf_ctx* c, const encf_ct* a, const encf_ct* b, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(nullptr); DCt x = view(a), y = view(b); DCt o = outview(out, x.L, x.ncomp); ev.add(x, y, o, true); writeback(out, o); });
+    return guard([&] { EV_BEGIN(nullptr); DCt x = view(c, a), y = view(c, b); DCt o = outview(out, x.L, x.ncomp); ev.add(x, y, o, true); writeback(out, o); });
 }
 encf_status encf_mul_i(encf_ctx* c, const encf_ct* a, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(nullptr); DCt x = view(a); DCt o = outview(out, x.L, x.ncomp); ev.mul_i(x, o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(nullptr); DCt x = view(c, a); DCt o = outview(out, x.L, x.ncomp); ev.mul_i(x, o); writeback(out, o); });
 }
 encf_status encf_ptmul(encf_ctx* c, const encf_ct* a, const encf_pt* w, encf_ct* out, void* stream) {
     return guard([&] {
         EV_BEGIN(nullptr);
-        DCt x = view(a);
+        DCt x = view(c, a);
         need(w && w->data && w->ntt == 1, ENCF_ERR_FORMAT, "ptmul needs an NTT-form plaintext");
         need(w->n_limbs == x.L, ENCF_ERR_LEVEL_MISMATCH, "ptmul: level mismatch");
         DCt o = outview(out, x.L, x.ncomp);
@@ -356,7 +364,7 @@ encf_status encf_ptmul(encf_ctx* c, const encf_ct* a, const encf_pt* w, encf_ct*
 encf_status encf_tensor(encf_ctx* c, const encf_ct* a, const encf_ct* b, encf_ct* out3, void* stream) {
     return guard([&] {
         EV_BEGIN(nullptr);
-        DCt x = view(a), y = view(b);
+        DCt x = view(c, a), y = view(c, b);
         need(x.ncomp == 2 && y.ncomp == 2, ENCF_ERR_FORMAT, "tensor needs 2-component inputs");
         need(x.L == y.L, ENCF_ERR_LEVEL_MISMATCH, "tensor: level mismatch");
         DCt o = outview(out3, x.L, 3);
@@ -365,12 +373,12 @@ encf_status encf_tensor(encf_ctx* c, const encf_ct* a, const encf_ct* b, encf_ct
     });
 }
 encf_status encf_relinearize(encf_ctx* c, const encf_keys* k, const encf_ct* in3, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(k); DCt x = view(in3); DCt o = outview(out, x.L, 2); ev.relin(x, o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(k); DCt x = view(c, in3); DCt o = outview(out, x.L, 2); ev.relin(x, o); writeback(out, o); });
 }
 encf_status encf_rotate(encf_ctx* c, const encf_keys* k, const encf_ct* in, int32_t steps, encf_ct* out, void* stream) {
     return guard([&] {
         EV_BEGIN(k);
-        DCt x = view(in);
+        DCt x = view(c, in);
         DCt o = outview(out, x.L, 2);
         uint32_t g = ev.galois_rot(steps);
         if (g == 1u) ev.copy(x, o);
@@ -383,7 +391,7 @@ encf_status encf_rotate_hoisted(encf_ctx* c, const encf_keys* k, const encf_ct* 
     return guard([&] {
         EV_BEGIN(k);
         need(steps && outs && n >= 1, ENCF_ERR_ARG, "rotate_hoisted: bad argument");
-        DCt x = view(in);
+        DCt x = view(c, in);
         std::vector<uint32_t> gs;
         std::vector<DCt> os;
         for (int i = 0; i < n; i++) { gs.push_back(ev.galois_rot(steps[i])); os.push_back(outview(&outs[i], x.L, 2)); }
@@ -392,7 +400,7 @@ encf_status encf_rotate_hoisted(encf_ctx* c, const encf_keys* k, const encf_ct* 
     });
 }
 encf_status encf_conjugate(encf_ctx* c, const encf_keys* k, const encf_ct* in, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(k); DCt x = view(in); DCt o = outview(out, x.L, 2); ev.rotate_galois(x, ev.galois_conj(), o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(k); DCt x = view(c, in); DCt o = outview(out, x.L, 2); ev.rotate_galois(x, ev.galois_conj(), o); writeback(out, o); });
 }
 encf_status encf_decomplexify(encf_ctx* c, const encf_keys* k, const encf_ct* in, int32_t n, encf_ct* outs, void* stream) {
     return guard([&] {
@@ -400,7 +408,7 @@ encf_status encf_decomplexify(encf_ctx* c, const encf_keys* k, const encf_ct* in
         need(in != nullptr && outs != nullptr && n >= 1, ENCF_ERR_ARG, "decomplexify: n >= 1 ciphertexts");
         std::vector<DCt> xs, cj, os;
         std::vector<const DCt*> xp;
-        for (int i = 0; i < n; i++) xs.push_back(view(&in[i]));
+        for (int i = 0; i < n; i++) xs.push_back(view(c, &in[i]));
         for (int i = 0; i < n; i++) {
             need(xs[i].ncomp == 2, ENCF_ERR_FORMAT, "decomplexify: 2-component ciphertexts");
             need(xs[i].L == xs[0].L, ENCF_ERR_LEVEL_MISMATCH, "decomplexify: mixed levels");
@@ -417,15 +425,15 @@ encf_status encf_decomplexify(encf_ctx* c, const encf_keys* k, const encf_ct* in
     });
 }
 encf_status encf_rescale(encf_ctx* c, const encf_ct* in, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(nullptr); DCt x = view(in); need(x.L > 1, ENCF_ERR_LEVEL_EXHAUSTED, "rescale at one limb"); DCt o = outview(out, x.L - 1, x.ncomp); ev.rescale(x, o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(nullptr); DCt x = view(c, in); need(x.L > 1, ENCF_ERR_LEVEL_EXHAUSTED, "rescale at one limb"); DCt o = outview(out, x.L - 1, x.ncomp); ev.rescale(x, o); writeback(out, o); });
 }
 encf_status encf_mod_drop(encf_ctx* c, const encf_ct* in, int32_t n_limbs, encf_ct* out, void* stream) {
-    return guard([&] { EV_BEGIN(nullptr); DCt x = view(in); DCt o = outview(out, n_limbs, x.ncomp); ev.mod_drop(x, n_limbs, o); writeback(out, o); });
+    return guard([&] { EV_BEGIN(nullptr); DCt x = view(c, in); DCt o = outview(out, n_limbs, x.ncomp); ev.mod_drop(x, n_limbs, o); writeback(out, o); });
 }
 encf_status encf_complexify(encf_ctx* c, const encf_ct* re, const encf_ct* im, encf_ct* out, void* stream) {
     return guard([&] {
         EV_BEGIN(nullptr);
-        DCt a = view(re), b = view(im);
+        DCt a = view(c, re), b = view(c, im);
         DCt t = ev.alloc(b.L, b.ncomp);
         ev.mul_i(b, t);
         DCt o = outview(out, a.L, a.ncomp);
@@ -551,7 +559,7 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
         EV_BEGIN(k);
         std::vector<DCt> xs;
         for (int u = 0; u < p->U; u++) {
-            xs.push_back(view(&x[u]));
+            xs.push_back(view(c, &x[u]));
             need(xs.back().ncomp == 2, ENCF_ERR_FORMAT, "inputs must have 2 components");
         }
         const int L = xs[0].L;
@@ -569,12 +577,14 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
                 ev.copy(ys[i], o);
                 writeback(yo, o);
             }
-        } else {   // partial accumulators in the EXTENDED basis: n_limbs = L + K (R-LAZY; reduce with encf_mod_reduce_ext)
+        } else {   // partial accumulators in the EXTENDED basis at the bank level La (= L, or L - 1 for a restricted
+                   // plan): n_limbs = La + K (R-LAZY; reduce with encf_mod_reduce_ext)
+            const int La = accs[0].L;
             for (size_t i = 0; i < accs.size(); i++) {
                 encf_ct* yo = &y[b_first + i];
                 need(yo && yo->data, ENCF_ERR_ARG, "null output");
-                k_copy(accs[i].d, yo->data, (size_t)2 * (L + c->K) * c->N, s);
-                yo->n_comp = 2; yo->n_limbs = L + c->K; yo->scale = accs[i].scale; yo->ntt = 1;
+                k_copy(accs[i].d, yo->data, (size_t)2 * (La + c->K) * c->N, s);
+                yo->n_comp = 2; yo->n_limbs = La + c->K; yo->scale = accs[i].scale; yo->ntt = 1;
             }
         }
     });
@@ -636,7 +646,7 @@ encf_status encf_ct_ct_attn_score(encf_ctx* c, const encf_keys* k, const encf_at
         need(c && k && a && q && kk && s_t && 0 <= t0 && t0 < t1 && t1 <= a->m / 2, ENCF_ERR_ARG, "score: bad argument");
         EV_BEGIN(k);
         std::vector<DCt> qs, ks;
-        for (int l = 0; l < a->B; l++) { qs.push_back(view(&q[l])); ks.push_back(view(&kk[l])); }
+        for (int l = 0; l < a->B; l++) { qs.push_back(view(c, &q[l])); ks.push_back(view(c, &kk[l])); }
         std::vector<DCt> S;
         score_run(ev, *a, qs, ks, t0, t1, S);
         for (int t = 0; t < t1 - t0; t++) {
@@ -653,7 +663,7 @@ encf_status encf_attn_export_stream(encf_ctx* c, const encf_keys* k, const encf_
         need(c && k && a && s_t && s_min, ENCF_ERR_ARG, "export_stream: null argument");
         EV_BEGIN(k);
         std::vector<DCt> S;
-        for (int t = 0; t < a->m / 2; t++) S.push_back(view(&s_t[t]));
+        for (int t = 0; t < a->m / 2; t++) S.push_back(view(c, &s_t[t]));
         std::vector<DCt> outs;
         score_export_run(ev, *a, S, outs);
         for (int i = 0; i < a->n_out; i++) {
@@ -671,8 +681,8 @@ encf_status encf_ct_ct_attn_value(encf_ctx* c, const encf_keys* k, const encf_at
         EV_BEGIN(k);
         std::vector<DCt> ps, vs;
         for (int l = 0; l < a->B_V; l++) {
-            ps.push_back(view(&p_fd[l]));
-            vs.push_back(view(&v[l]));
+            ps.push_back(view(c, &p_fd[l]));
+            vs.push_back(view(c, &v[l]));
             need(vs.back().L >= ps.back().L + 1 && ps.back().L >= 3, ENCF_ERR_LEVEL_MISMATCH, "value: level plan (Lv > Lp >= 3)");
         }
         std::vector<DCt> outs;
@@ -685,13 +695,98 @@ encf_status encf_ct_ct_attn_value(encf_ctx* c, const encf_keys* k, const encf_at
     });
 }
 
+encf_status encf_ct_ct_attn_value_partial(encf_ctx* c, const encf_keys* k, const encf_attn_plan* a, const encf_ct* p_fd,
+                                          const encf_ct* v, int32_t u0, int32_t u1, encf_ct* o3, void* stream) {
+    return guard([&] {
+        need(c && k && a && p_fd && v && o3, ENCF_ERR_ARG, "value_partial: null argument");
+        need(0 <= u0 && u0 < u1 && u1 <= a->B_V * (a->m / 2), ENCF_ERR_ARG, "value_partial: bad unit range");
+        EV_BEGIN(k);
+        std::vector<DCt> ps, vs;
+        for (int l = 0; l < a->B_V; l++) {
+            ps.push_back(view(c, &p_fd[l]));
+            vs.push_back(view(c, &v[l]));
+            need(vs.back().L >= ps.back().L + 1 && ps.back().L >= 3, ENCF_ERR_LEVEL_MISMATCH, "value: level plan (Lv > Lp >= 3)");
+        }
+        std::vector<int> blocks;
+        std::vector<DCt> o3s;
+        value_partial_run(ev, *a, ps, vs, u0, u1, blocks, o3s);
+        for (size_t i = 0; i < blocks.size(); i++) {
+            DCt oo = outview(&o3[i], o3s[i].L, 3);
+            ev.copy(o3s[i], oo);
+            writeback(&o3[i], oo);
+        }
+    });
+}
+
+encf_status encf_attn_value_finalize(encf_ctx* c, const encf_keys* k, const encf_ct* o3, int32_t n, encf_ct* o, void* stream) {
+    return guard([&] {
+        need(c && k && o3 && o && n >= 1, ENCF_ERR_ARG, "value_finalize: bad argument");
+        EV_BEGIN(k);
+        std::vector<DCt> xs;
+        for (int i = 0; i < n; i++) {
+            xs.push_back(view(c, &o3[i]));
+            need(xs.back().ncomp == 3 && xs.back().L == xs[0].L, ENCF_ERR_FORMAT, "value_finalize: 3-component partials at one level");
+            need(xs.back().L >= 2, ENCF_ERR_LEVEL_EXHAUSTED, "value_finalize: one limb");
+        }
+        std::vector<DCt> ys = ev.alloc_many(n, xs[0].L - 1);
+        std::vector<const DCt*> xp;
+        for (auto& x : xs) xp.push_back(&x);
+        ev.relin_rescale_many(xp, ys);
+        for (int i = 0; i < n; i++) {
+            DCt oo = outview(&o[i], ys[i].L, 2);
+            ev.copy(ys[i], oo);
+            writeback(&o[i], oo);
+        }
+    });
+}
+
+// ------------------------------------------------------------------------------------ ciphertext shifts (App. A.1)
+encf_status encf_rotfirst(encf_ctx* c, const encf_keys* k, const encf_ct* in, int32_t L_slots, const int32_t* taus, int32_t n,
+                          int32_t m, encf_ct* outs, void* stream) {
+    return guard([&] {
+        EV_BEGIN(k);
+        need(taus && outs && n >= 1 && m >= 1, ENCF_ERR_ARG, "rotfirst: bad argument");
+        need(L_slots >= 1 && L_slots <= c->N / 2, ENCF_ERR_ARG, "rotfirst: L must be in [1, n]");
+        DCt x = view(c, in);
+        need(x.ncomp == 2, ENCF_ERR_FORMAT, "rotfirst: 2-component input");
+        need(x.L >= 2, ENCF_ERR_LEVEL_EXHAUSTED, "rotfirst: needs one level");
+        std::vector<ShiftReq> reqs;
+        for (int i = 0; i < n; i++) reqs.push_back(rotfirst_req(0, L_slots, taus[i], m));
+        std::vector<DCt> os = ev.alloc_many(n, x.L - 1);
+        shift_many(ev, {&x}, reqs, os);
+        for (int i = 0; i < n; i++) {
+            DCt oo = outview(&outs[i], os[i].L, 2);
+            ev.copy(os[i], oo);
+            writeback(&outs[i], oo);
+        }
+    });
+}
+
+encf_status encf_psi(encf_ctx* c, const encf_keys* k, const encf_ct* in, int32_t m, const int32_t* ts, int32_t n, encf_ct* outs,
+                     void* stream) {
+    return guard([&] {
+        EV_BEGIN(k);
+        need(ts && outs && n >= 1 && m >= 1 && (c->N / 2) % m == 0, ENCF_ERR_ARG, "psi: bad argument");
+        DCt x = view(c, in);
+        need(x.ncomp == 2, ENCF_ERR_FORMAT, "psi: 2-component input");
+        need(x.L >= 2, ENCF_ERR_LEVEL_EXHAUSTED, "psi: needs one level");
+        std::vector<std::vector<DCt>> os;
+        psi_many(ev, {&x}, {std::vector<int>(ts, ts + n)}, m, 0, c->N / 2 / m, os);
+        for (int i = 0; i < n; i++) {
+            DCt oo = outview(&outs[i], os[0][i].L, 2);
+            ev.copy(os[0][i], oo);
+            writeback(&outs[i], oo);
+        }
+    });
+}
+
 // ------------------------------------------------------------------------------------ w/o-SCP ablation repack
 encf_status encf_repack_rma(encf_ctx* c, const encf_keys* k, const encf_ct* x, int32_t n, int32_t m, encf_ct* out, void* stream) {
     return guard([&] {
         need(c && k && x && out && n > 0, ENCF_ERR_ARG, "repack_rma: null argument");
         EV_BEGIN(k);
         std::vector<DCt> xs;
-        for (int i = 0; i < n; i++) xs.push_back(view(&x[i]));
+        for (int i = 0; i < n; i++) xs.push_back(view(c, &x[i]));
         std::vector<DCt> ys;
         repack_rma_run(ev, xs, m, ys);
         for (int i = 0; i < n; i++) {
@@ -709,7 +804,7 @@ encf_status encf_gelu_preeval(encf_ctx* c, const encf_keys* k, const encf_ct* x,
         need(c && k && x && coef && f0 && f1 && n > 0, ENCF_ERR_ARG, "gelu_preeval: null argument");
         EV_BEGIN(k);
         std::vector<DCt> xs;
-        for (int i = 0; i < n; i++) xs.push_back(view(&x[i]));
+        for (int i = 0; i < n; i++) xs.push_back(view(c, &x[i]));
         std::vector<DCt> a, b;
         gelu_preeval_run(ev, xs, coef, a, b);
         for (int i = 0; i < n; i++) {
@@ -735,7 +830,7 @@ encf_status encf_export_c2m(encf_ctx* c, const encf_ct* in, int32_t Lc, uint64_t
                             uint64_t* share, void* stream) {
     return guard([&] {
         need(c && masked && masked->data && share, ENCF_ERR_ARG, "export: null argument");
-        DCt x = view(in);
+        DCt x = view(c, in);
         need(x.ncomp == 2, ENCF_ERR_FORMAT, "export needs 2 components");
         need(Lc >= 1 && Lc <= x.L, ENCF_ERR_LEVEL_MISMATCH, "export: L_conv above the ciphertext level");
         need(stream_id < (1ull << 56), ENCF_ERR_ARG, "export: stream_id must be < 2^56");
@@ -759,7 +854,7 @@ encf_status encf_export_c2m_many(encf_ctx* c, const encf_ct* in, int32_t n, int3
         const size_t cw = (size_t)2 * Lc * N;
         int L0 = -1;
         for (int i = 0; i < n; i++) {
-            DCt x = view(&in[i]);
+            DCt x = view(c, &in[i]);
             need(x.ncomp == 2, ENCF_ERR_FORMAT, "export needs 2 components");
             need(Lc >= 1 && Lc <= x.L, ENCF_ERR_LEVEL_MISMATCH, "export: L_conv above the ciphertext level");
             if (L0 < 0) L0 = x.L;
@@ -799,7 +894,7 @@ encf_status encf_field2ring_local(encf_ctx* c, const uint64_t* share, int32_t el
 encf_status encf_import_m2c(encf_ctx* c, const encf_ct* ct, const encf_pt* share, encf_ct* out, void* stream) {
     return guard([&] {
         need(c && share && share->data && out && out->data, ENCF_ERR_ARG, "import_m2c: null argument");
-        DCt x = view(ct);
+        DCt x = view(c, ct);
         need(x.ncomp == 2, ENCF_ERR_FORMAT, "import_m2c needs a 2-component ciphertext");
         need(share->n_limbs == x.L, ENCF_ERR_LEVEL_MISMATCH, "import_m2c: share level != ciphertext level");
         cudaStream_t s = S(stream);

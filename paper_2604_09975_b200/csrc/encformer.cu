@@ -39,12 +39,22 @@ void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C,
     if (p.C % N1) throw EncfError(ENCF_ERR_PLAN_SHAPE, "N1 must divide C");
     p.N1 = N1;
     p.N2 = p.C / N1;
+    p.restricted = p.C < p.N_seg;
 }
 
 std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p) {
+    std::vector<long> steps;
+    for (int q = 1; q < p.N1; q++) steps.push_back((long)q * p.m);
+    for (int pp = 1; pp < p.N2; pp++) steps.push_back((long)pp * p.N1 * p.m);
+    if (p.restricted) {   // RotFirst_{Cm}: the wrap-around rotation tau - Cm of every baby / giant shift
+        for (int q = 1; q < p.N1; q++) steps.push_back((long)(q - p.C) * p.m);
+        for (int pp = 1; pp < p.N2; pp++) steps.push_back((long)(pp * p.N1 - p.C) * p.m);
+    }
     std::vector<uint32_t> g;
-    for (int q = 1; q < p.N1; q++) g.push_back(ev.galois_rot((long)q * p.m));
-    for (int pp = 1; pp < p.N2; pp++) g.push_back(ev.galois_rot((long)pp * p.N1 * p.m));
+    for (long st : steps) {
+        uint32_t x = ev.galois_rot(st);
+        if (x != 1u && std::find(g.begin(), g.end(), x) == g.end()) g.push_back(x);
+    }
     g.push_back(ev.galois_conj());
     return g;
 }
@@ -56,27 +66,49 @@ std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p) {
 //     Q_L u P (lazy ModDown, R-LAZY); the ModDown happens once per block in proj_finalize_many.
 void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs) {
-    const int N = ev.c.N, L = x[0].L, U = p.U, N1 = p.N1;
+    const int N = ev.c.N, L0 = x[0].L, U = p.U, N1 = p.N1;
     for (auto& xi : x) {
-        if (xi.L != L) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "projection inputs at different levels");
+        if (xi.L != L0) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "projection inputs at different levels");
         check_scale(xi.scale, x[0].scale);
     }
+    const int L = p.restricted ? L0 - 1 : L0;          // bank level (= weight level)
+    if (L < 2) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "projection: not enough levels");
     const size_t ctw = ev.ct_words(L);
     std::vector<DCt> bankv = ev.alloc_many(U * N1, L);
-    std::vector<std::vector<uint32_t>> gs(U);
-    std::vector<std::vector<DCt>> outs(U);
-    for (int u = 0; u < U; u++)
-        for (int q = 0; q < N1; q++) {
-            gs[u].push_back(q == 0 ? 1u : ev.galois_rot((long)q * p.m));
-            outs[u].push_back(bankv[u * N1 + q]);
-        }
-    ev.hoisted_many(ptrs(x), gs, outs);
+    if (p.restricted) {
+        // bank[u][q] = Phi_C^q(x~_u) = RotFirst_{Cm}(x~_u; q m) (Alg A.4): one hoisted ModUp per input, one fused
+        // masked-pair launch, one merged ModDown + rescale (oracle kernels.Phi_C)
+        std::vector<ShiftReq> reqs;
+        for (int u = 0; u < U; u++)
+            for (int q = 0; q < N1; q++) reqs.push_back(rotfirst_req(u, (long)p.C * p.m, (long)q * p.m, p.m));
+        shift_many(ev, ptrs(x), reqs, bankv);
+    } else {
+        std::vector<std::vector<uint32_t>> gs(U);
+        std::vector<std::vector<DCt>> outs(U);
+        for (int u = 0; u < U; u++)
+            for (int q = 0; q < N1; q++) {
+                gs[u].push_back(q == 0 ? 1u : ev.galois_rot((long)q * p.m));
+                outs[u].push_back(bankv[u * N1 + q]);
+            }
+        ev.hoisted_many(ptrs(x), gs, outs);
+    }
     const int units = u1 - u0;
     std::vector<DCt> cu = ev.alloc_many(units, L);
     const i64 wus = (i64)U * N1 * L * N;
     k_diag_mac(ev.c, bankv[0].d, U * N1, w + (size_t)u0 * wus, units, wus, cu[0].d, (i64)ctw, L, ev.s);
-    const double sc = x[0].scale * w_scale;
+    const double sc = bankv[0].scale * w_scale;
     for (auto& c : cu) c.scale = sc;
+    int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;
+    if (p.restricted) {
+        // acc_b = sum_p Phi_C^{p N1}(c~_{b,p}), every RotFirst kept in Q_L u P and summed there (oracle
+        // kernels.rotfirst_ext); divided by P q_{L-1} once per block in proj_finalize_many
+        std::vector<std::vector<ShiftReq>> terms(b_last - b_first + 1);
+        for (int un = u0; un < u1; un++)
+            terms[un / p.N2 - b_first].push_back(rotfirst_req(un - u0, (long)p.C * p.m, (long)(un % p.N2) * N1 * p.m, p.m));
+        accs = ev.alloc_many_ext((int)terms.size(), L);
+        shift_sum_ext_many(ev, ptrs(cu), terms, accs);
+        return;
+    }
     std::vector<const DCt*> rin, lin;
     std::vector<uint32_t> rg;
     std::vector<int> ridx, lidx;
@@ -91,7 +123,6 @@ void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, con
     std::vector<const DCt*> term_of(units, nullptr);
     for (size_t i = 0; i < ridx.size(); i++) term_of[ridx[i]] = &rot[i];
     for (size_t i = 0; i < lidx.size(); i++) term_of[lidx[i]] = &lif[i];
-    int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;
     std::vector<std::vector<SumTerm>> terms(b_last - b_first + 1);
     for (int un = u0; un < u1; un++) terms[un / p.N2 - b_first].push_back(SumTerm{term_of[un - u0]->d, nullptr});
     accs = ev.alloc_many_ext((int)terms.size(), L);
@@ -103,10 +134,13 @@ void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, con
 void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs_ext, std::vector<DCt>& ys) {
     const int n = (int)accs_ext.size();
     const int L = accs_ext[0].L;
-    std::vector<DCt> acc = ev.alloc_many(n, L);
-    ev.moddown_many(accs_ext, acc);
+    std::vector<DCt> acc = ev.alloc_many(n, p.restricted ? L - 1 : L);
+    if (p.restricted) ev.moddown_rescale_many(accs_ext, acc);     // the fold's RotFirst masks spend a level (R-PHIC)
+    else ev.moddown_many(accs_ext, acc);
+    const int La = acc[0].L;
+    if (La < 2) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "projection: not enough levels to finalize");
     if (p.flags & ENCF_PROJ_DECOMPLEXIFY) {
-        std::vector<DCt> cj = ev.alloc_many_ext(n, L), la = ev.alloc_many_ext(n, L);
+        std::vector<DCt> cj = ev.alloc_many_ext(n, La), la = ev.alloc_many_ext(n, La);
         ev.rotate_many_ext(ptrs(acc), std::vector<uint32_t>(n, ev.galois_conj()), cj);
         ev.lift_many(ptrs(acc), la);
         std::vector<std::vector<SumTerm>> t(n);
@@ -115,8 +149,8 @@ void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>&
             t[i] = {SumTerm{la[i].d, nullptr}, SumTerm{cj[i].d, nullptr}};
             sc[i] = acc[i].scale * 2.0;
         }
-        std::vector<DCt> z = ev.alloc_many_ext(n, L);
-        ev.sum_many_ext(t, L, z, sc);
+        std::vector<DCt> z = ev.alloc_many_ext(n, La);
+        ev.sum_many_ext(t, La, z, sc);
         ev.moddown_rescale_many(z, ys);
     } else {
         ev.rescale_many(ptrs(acc), ys);
@@ -124,80 +158,170 @@ void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>&
 }
 
 // ====================================================================================== shifts (App. A.1)
-// Psi^t of xs[i] for every t in ts[i] (Alg A.2): one hoisted ModUp per input, rot(x,t)(.)h_t +
-// rot(x,t-m)(.)u_t, rescale; t = 0: x(.)h_0, rescale.  Segment restriction [seg0, seg0+nseg) of the masks.
-void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
-              std::vector<std::vector<DCt>>& outs) {
-    // t != 0: the two rotations stay in Q_L u P (hoisted, no ModDown), are masked there and divided by
-    // P q_{L-1} at once (lazy ModDown merged with the rescale, R-LAZY).  The two inner products, the c0 lifts
-    // and the masked sum run as ONE fused launch per batch (ks_psi_kernel); t = 0: x (.) h_0, rescale.
-    const int n = (int)xs.size();
+// Slot range [lo, hi) as a mask descriptor: the m-row grid when segment aligned, else the 1-row grid
+// (oracle kernels.slot_range_desc).
+static MaskD slot_range(long lo, long hi, int m) {
+    if (lo % m == 0 && hi % m == 0) return MaskD{m, 0, m, (int)(lo / m), 1, (int)((hi - lo) / m)};
+    return MaskD{1, 0, 1, (int)lo, 1, (int)(hi - lo)};
+}
+
+// RotFirst_L(x_i; tau) (Alg A.3): tau mod L; rot(x; tau) (.) a_{L,tau} + rot(x; tau - L) (.) b_{L,tau};
+// tau = 0: x (.) a_{L,0} (no rotation).  oracle kernels.RotFirst_hoisted.
+ShiftReq rotfirst_req(int i, long Ls, long tau, int m) {
+    tau = ((tau % Ls) + Ls) % Ls;
+    ShiftReq r;
+    r.i = i;
+    r.mk[0] = slot_range(0, Ls - tau, m);
+    r.plain = tau == 0;
+    r.rot[0] = tau;
+    r.rot[1] = tau - Ls;
+    if (tau) r.mk[1] = slot_range(Ls - tau, Ls, m);
+    return r;
+}
+
+// Psi^t (Alg A.2) with masks restricted to segments [seg0, seg0 + nseg): rot(x; t) (.) h_t +
+// rot(x; t - m) (.) u_t; t = 0 (mod m): x (.) h_0 (R-PSI0).  oracle kernels.Psi_hoisted.
+static ShiftReq psi_req(int i, int t, int m, int seg0, int nseg) {
+    const int r = ((t % m) + m) % m;
+    ShiftReq q;
+    q.i = i;
+    q.plain = r == 0;
+    q.rot[0] = r;
+    q.rot[1] = r - m;
+    q.mk[0] = MaskD{m, 0, m - r, seg0, 1, nseg};
+    q.mk[1] = MaskD{m, m - r, m, seg0, 1, nseg};
+    return q;
+}
+
+// The rotation requests (plain == false) as extended-basis masked pairs h (.) rot_ext(x, g0) + u (.) rot_ext(x, g1)
+// (P sigma(c0) lifts included) BEFORE ModDown: one hoisted ModUp per input, the two inner products, the c0 lifts
+// and the masked sum in ONE fused launch per batch (ks_psi_kernel, pre-masked keys).  ly: alloc_many_ext(reqs).
+void shift_ext_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<ShiftReq>& reqs, std::vector<DCt>& ly) {
     const int L = xs[0]->L, N = ev.c.N;
-    std::vector<std::vector<int>> tt(n);
+    std::vector<int> rslot(xs.size(), -1);
     std::vector<const u64*> c1;
-    std::vector<int> rslot(n, -1);
-    for (int i = 0; i < n; i++) {
-        if (xs[i]->L != L || xs[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "psi_many: mixed levels");
-        bool any = false;
-        for (int t : ts[i]) {
-            int r = ((t % m) + m) % m;
-            tt[i].push_back(r);
-            any |= r != 0;
-        }
-        if (any) { rslot[i] = (int)c1.size(); c1.push_back(xs[i]->comp(1, N)); }
+    for (auto& q : reqs) {
+        if (q.plain) throw EncfError(ENCF_ERR_ARG, "shift_ext_many: plain request");
+        const DCt* x = xs[q.i];
+        if (x->L != L || x->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "shift: mixed levels");
+        if (rslot[q.i] < 0) { rslot[q.i] = (int)c1.size(); c1.push_back(x->comp(1, N)); }
     }
-    u64* ext = c1.empty() ? nullptr : ev.modup_many(c1, {}, L);
+    if (reqs.empty()) return;
+    u64* ext = ev.modup_many(c1, {}, L);
     const double ms = ev.mask_scale(L);
-    struct Req { int i, t; };
-    std::vector<Req> lazy;
-    std::vector<std::vector<SumTerm>> plain_terms;
-    std::vector<double> plain_sc;
-    std::vector<std::pair<int, int>> where;   // (0 = lazy / 1 = plain, index)
-    for (int i = 0; i < n; i++)
-        for (int t : tt[i]) {
-            if (t == 0) {
-                plain_terms.push_back({SumTerm{xs[i]->d, ev.mask(m, 0, m, seg0, 1, nseg, L)}});
-                plain_sc.push_back(xs[i]->scale * ms);
-                where.push_back({1, (int)plain_terms.size() - 1});
-            } else {
-                lazy.push_back(Req{i, t});
-                where.push_back({0, (int)lazy.size() - 1});
-            }
-        }
-    // lazy requests ordered t-major so that consecutive CTAs (request index fastest) share the two keys in L2
-    std::vector<int> order(lazy.size());
+    // requests ordered by rotation so that consecutive CTAs (request index fastest) share the two keys in L2
+    std::vector<int> order(reqs.size());
     for (size_t k = 0; k < order.size(); k++) order[k] = (int)k;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return lazy[a].t < lazy[b].t; });
-    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy.size(), L), lo = ev.alloc_many((int)lazy.size(), L - 1);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return reqs[a].rot[0] < reqs[b].rot[0]; });
     const int key_nl = ev.keys->max_level + ev.c.K, dn = ev.c.dnum(L);
     for (size_t r0 = 0; r0 < order.size(); r0 += PSI_BATCH) {
         const int cnt = (int)std::min((size_t)PSI_BATCH, order.size() - r0);
         PsiBatch B;
         for (int k = 0; k < cnt; k++) {
-            const Req& q = lazy[order[r0 + k]];
+            const ShiftReq& q = reqs[order[r0 + k]];
             DCt& o = ly[order[r0 + k]];
             o.scale = xs[q.i]->scale * ms;
             B.ext[k] = ext + ev.ext_stride(L) * rslot[q.i];
             B.c0[k] = xs[q.i]->comp(0, N);
             B.out[k] = o.d;
-            B.g[k][0] = ev.galois_rot(q.t);
-            B.g[k][1] = ev.galois_rot(q.t - m);
-            // pre-masked keys: key (.) h_t and key (.) u_t (cached), and P (.) mask for the c0 lift
-            B.key[k][0] = ev.keymask(B.g[k][0], m, 0, m - q.t, seg0, 1, nseg, L, &B.mask[k][0]);
-            B.key[k][1] = ev.keymask(B.g[k][1], m, m - q.t, m, seg0, 1, nseg, L, &B.mask[k][1]);
+            for (int j = 0; j < 2; j++) {
+                const MaskD& d = q.mk[j];
+                B.g[k][j] = ev.galois_rot(q.rot[j]);
+                // pre-masked keys: key (.) mask (cached), and P (.) mask for the c0 lift
+                B.key[k][j] = ev.keymask(B.g[k][j], d.m, d.r0, d.r1, d.s0, d.ss, d.sc, L, &B.mask[k][j]);
+            }
         }
         k_ks_psi(ev.c, B, cnt, dn, L, key_nl, ev.s);
-        ev.c.st_ks += 2 * (uint64_t)cnt;      // two key switches whose ModDown is merged into the rescale
+        ev.c.st_ks += 2 * (uint64_t)cnt;      // two key switches whose ModDown is merged into a later division
     }
+}
+
+// outs[k] = the masked shift reqs[k] of xs[reqs[k].i], rescaled (level L-1; caller-allocated outputs): rotation
+// requests divided by P q_{L-1} at once (merged ModDown + rescale, R-LAZY), plain requests x (.) mask, rescale.
+void shift_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<ShiftReq>& reqs, std::vector<DCt>& outs) {
+    const int L = xs[0]->L;
+    std::vector<ShiftReq> lazy;
+    std::vector<int> lidx, pidx;
+    for (size_t k = 0; k < reqs.size(); k++) {
+        if (reqs[k].plain) pidx.push_back((int)k);
+        else { lidx.push_back((int)k); lazy.push_back(reqs[k]); }
+    }
+    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy.size(), L);
+    shift_ext_many(ev, xs, lazy, ly);
+    std::vector<DCt> lo(lidx.size());
+    for (size_t k = 0; k < lidx.size(); k++) lo[k] = outs[lidx[k]];
     ev.moddown_rescale_many(ly, lo);
-    std::vector<DCt> py = ev.alloc_many((int)plain_terms.size(), L), po = ev.alloc_many((int)plain_terms.size(), L - 1);
-    ev.sum_many(plain_terms, L, 2, py, plain_sc);
+    for (size_t k = 0; k < lidx.size(); k++) outs[lidx[k]] = lo[k];
+    const double ms = ev.mask_scale(L);
+    std::vector<std::vector<SumTerm>> pt;
+    std::vector<double> psc;
+    for (int k : pidx) {
+        const MaskD& d = reqs[k].mk[0];
+        const DCt* x = xs[reqs[k].i];
+        if (x->L != L || x->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "shift: mixed levels");
+        pt.push_back({SumTerm{x->d, ev.mask(d.m, d.r0, d.r1, d.s0, d.ss, d.sc, L)}});
+        psc.push_back(x->scale * ms);
+    }
+    std::vector<DCt> py = ev.alloc_many((int)pt.size(), L), po(pidx.size());
+    ev.sum_many(pt, L, 2, py, psc);
+    for (size_t k = 0; k < pidx.size(); k++) po[k] = outs[pidx[k]];
     ev.rescale_many(ptrs(py), po);
+    for (size_t k = 0; k < pidx.size(); k++) outs[pidx[k]] = po[k];
+}
+
+// Psi^t of xs[i] for every t in ts[i] (Alg A.2) through shift_many.
+void psi_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<int>>& ts, int m, int seg0, int nseg,
+              std::vector<std::vector<DCt>>& outs) {
+    const int n = (int)xs.size();
+    const int L = xs[0]->L;
+    std::vector<ShiftReq> reqs;
+    for (int i = 0; i < n; i++) {
+        if (xs[i]->L != L || xs[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "psi_many: mixed levels");
+        for (int t : ts[i]) reqs.push_back(psi_req(i, t, m, seg0, nseg));
+    }
+    std::vector<DCt> o = ev.alloc_many((int)reqs.size(), L - 1);
+    shift_many(ev, xs, reqs, o);
     outs.assign(n, {});
-    int k = 0;
+    size_t k = 0;
     for (int i = 0; i < n; i++)
-        for (size_t j2 = 0; j2 < tt[i].size(); j2++, k++)
-            outs[i].push_back(where[k].first == 0 ? lo[where[k].second] : po[where[k].second]);
+        for (size_t j = 0; j < ts[i].size(); j++) outs[i].push_back(o[k++]);
+}
+
+// outs_ext[o] = sum over terms[o] of the extended-basis masked shifts (input, request) BEFORE the division by
+// P q_{L-1} (R-LAZY); plain requests enter as P x (.) mask.  outs_ext: alloc_many_ext(terms.size()) by the caller.
+// Used by the restricted giant fold (Phi_C^{p N1}, oracle kernels.rotfirst_ext) and by Align_r (align_sum).
+void shift_sum_ext_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector<std::vector<ShiftReq>>& terms,
+                               std::vector<DCt>& outs_ext) {
+    const int L = xs[0]->L;
+    std::vector<ShiftReq> lazy;
+    std::vector<const DCt*> plain_in;
+    std::vector<MaskD> plain_mk;
+    for (auto& tv : terms)
+        for (auto& q : tv) {
+            if (q.plain) { plain_in.push_back(xs[q.i]); plain_mk.push_back(q.mk[0]); }
+            else lazy.push_back(q);
+        }
+    std::vector<DCt> ly = ev.alloc_many_ext((int)lazy.size(), L), lf = ev.alloc_many_ext((int)plain_in.size(), L);
+    shift_ext_many(ev, xs, lazy, ly);
+    ev.lift_many(plain_in, lf);
+    const double ms = ev.mask_scale(L);
+    std::vector<std::vector<SumTerm>> st(terms.size());
+    std::vector<double> sc(terms.size());
+    size_t il = 0, ip = 0;
+    for (size_t o = 0; o < terms.size(); o++) {
+        if (terms[o].empty()) throw EncfError(ENCF_ERR_ARG, "shift_sum_ext_many: empty sum");
+        for (auto& q : terms[o]) {
+            if (q.plain) {
+                const MaskD& d = plain_mk[ip];
+                st[o].push_back(SumTerm{lf[ip++].d, ev.mask_ext(d.m, d.r0, d.r1, d.s0, d.ss, d.sc, L)});
+            } else {
+                st[o].push_back(SumTerm{ly[il++].d, nullptr});
+            }
+        }
+        sc[o] = xs[terms[o][0].i]->scale * ms;
+        for (auto& q : terms[o]) check_scale(xs[q.i]->scale * ms, sc[o]);
+    }
+    ev.sum_many_ext(st, L, outs_ext, sc);
 }
 
 // ====================================================================================== attention plans
@@ -210,9 +334,17 @@ void attn_plan_init(encf_attn_plan& a, int n, int m, int H, int d_h, int C_qk, i
         C_qk = H;
         while (C_qk * 2 <= a.N_seg && C_qk < H * d_h) C_qk *= 2;
     }
-    if (C_qk % H || C_qk > a.N_seg) throw EncfError(ENCF_ERR_PLAN_SHAPE, "C_qk must be a multiple of H and <= n/m");
+    if (C_qk < H || C_qk > a.N_seg) throw EncfError(ENCF_ERR_PLAN_SHAPE, "need H <= C_qk <= n/m");
     a.C = C_qk;
     a.B = (H * d_h + C_qk - 1) / C_qk;
+    a.k_route = (C_qk + H - 1) / H;
+    a.phases.clear();
+    a.aligned = false;
+    for (int l = 0; l < a.B; l++) {          // head phase r_l = l C mod H (App. A.3)
+        a.phases.push_back((int)(((long)l * C_qk) % H));
+        a.aligned |= a.phases.back() != 0;
+    }
+    if (a.k_route - 1 > RS_TERMS) throw EncfError(ENCF_ERR_PLAN_SHAPE, "C_qk / H too large for the routing sum");
     if (beta <= 0) { beta = 1; while (beta * beta < m) beta *= 2; }
     a.beta = beta;
     if (m % beta || (m / beta) % 2) throw EncfError(ENCF_ERR_PLAN_SHAPE, "beta | m with g = m/beta even");
@@ -230,8 +362,10 @@ std::vector<uint32_t> attn_galois(Ev& ev, const encf_attn_plan& a) {
     const int m = a.m;
     for (int t = 1; t < m; t++) { steps.push_back(t); steps.push_back(t - m); }
     for (int d = -(a.d_h - 1); d < m / 2; d++) steps.push_back((long)d * m);
-    for (int k = 1; k <= a.C / a.H; k *= 2) steps.push_back((long)k * a.H * m);
-    for (int k = 1; k < a.C / a.H; k++) steps.push_back((long)k * a.H * m);
+    for (int k = 1; k <= a.k_route; k *= 2) steps.push_back((long)k * a.H * m);
+    for (int k = 1; k < a.k_route; k++) steps.push_back((long)k * a.H * m);
+    for (int r : a.phases)                  // Align_r = RotFirst_{Hm}(., (H - r) m): rotations (H - r) m and -r m
+        if (r) { steps.push_back((long)(a.H - r) * m); steps.push_back(-(long)r * m); }
     const long seg = (long)a.H * m;
     for (int t = 0; t < m / 2; t++) steps.push_back(-((t * seg) % a.n));
     std::vector<uint32_t> g;
@@ -282,15 +416,35 @@ void score_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& qs, cons
             for (int j = 0; j < g / 2; j++) kc[l].push_back(ko[l * (g / 2) + j]);
     }
     const int nt = t1 - t0;
-    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(nt);
+    // one lazy tensor sum per (t, head phase r): all blocks when C mod H = 0 (oracle kernels.score_phase_groups)
+    std::vector<int> rs;
+    for (int r : a.phases) if (std::find(rs.begin(), rs.end(), r) == rs.end()) rs.push_back(r);
+    std::sort(rs.begin(), rs.end());
+    const int nr = (int)rs.size();
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(nt * nr);
     for (int t = t0; t < t1; t++) {
         int j = t / beta, s = t % beta;
-        for (int l = 0; l < a.B; l++) pairs[t - t0].push_back({&bank[l][s], &kc[l][j]});
+        for (int ri = 0; ri < nr; ri++)
+            for (int l = 0; l < a.B; l++)
+                if (a.phases[l] == rs[ri]) pairs[(t - t0) * nr + ri].push_back({&bank[l][s], &kc[l][j]});
     }
-    std::vector<DCt> T3 = ev.alloc_many(nt, Lb, 3), T = ev.alloc_many(nt, Lb - 1);
+    std::vector<DCt> T3 = ev.alloc_many(nt * nr, Lb, 3), T = ev.alloc_many(nt * nr, Lb - 1);
     ev.tensor_many(pairs, T3);
     ev.relin_rescale_many(ptrs(T3), T);      // lazy relin merged with the rescale (R-RELRS)
-    std::vector<DCt> R = route_many(ev, T, a.C / H, H, m);
+    std::vector<DCt> R = route_many(ev, T, a.k_route, H, m);
+    if (a.aligned) {
+        // sum_r Align_r(R_{t,r}) = sum_r RotFirst_{Hm}(R_{t,r}, (H - r) m), every term in Q_L u P, one merged
+        // ModDown + rescale per t (oracle kernels.align_sum)
+        std::vector<std::vector<ShiftReq>> terms(nt);
+        for (int i = 0; i < nt; i++)
+            for (int ri = 0; ri < nr; ri++)
+                terms[i].push_back(rotfirst_req(i * nr + ri, (long)H * m, (long)(H - rs[ri]) * m, m));
+        const int Lr = R[0].L;
+        std::vector<DCt> ax = ev.alloc_many_ext(nt, Lr), A = ev.alloc_many(nt, Lr - 1);
+        shift_sum_ext_many(ev, ptrs(R), terms, ax);
+        ev.moddown_rescale_many(ax, A);
+        R = A;
+    }
     std::vector<std::vector<int>> st(nt);
     for (int t = t0; t < t1; t++) st[t - t0] = {t % beta};
     std::vector<std::vector<DCt>> al;
@@ -334,94 +488,125 @@ void score_export_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& S
 }
 
 // ====================================================================================== value (C8)
-void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs,
-               std::vector<DCt>& outs) {
-    const int m = a.m, Ns = a.N_seg, half = m / 2, BV = a.B_V, N = ev.c.N;
+// Units (l, t), flattened l (m/2) + t, in [u0, u1): for every touched block l the UNRELINEARISED partial
+// o3_l = sum_{t in range} u_t (x) b_t (3 components, level Lp - 1; oracle kernels.value_partial).  The 1-GPU value
+// kernel is the full range followed by one relin merged with its rescale per block; a sharded run sums the
+// partials of a block across ranks (exact uint64 SUM + encf_mod_reduce), so the relin input and output are the
+// same bits.  blocks: the touched blocks in order.
+void value_partial_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs, int u0, int u1,
+                       std::vector<int>& blocks, std::vector<DCt>& o3) {
+    const int m = a.m, Ns = a.N_seg, half = m / 2, N = ev.c.N;
     const int Lv = vs[0].L, Lp = ps[0].L;
+    if (a.d_h > 64) throw EncfError(ENCF_ERR_PLAN_SHAPE, "value: d_h > 64 unsupported");
+    blocks.clear();
+    std::vector<int> ta, tb;     // t-range per touched block
+    for (int l = 0; l < a.B_V; l++) {
+        const int lo = std::max(u0 - l * half, 0), hi = std::min(u1 - l * half, half);
+        if (lo < hi) { blocks.push_back(l); ta.push_back(lo); tb.push_back(hi); }
+    }
+    const int nb = (int)blocks.size();
+    std::vector<const DCt*> vb, pbin;
+    for (int l : blocks) { vb.push_back(&vs[l]); pbin.push_back(&ps[l]); }
     // 1. uu = v (.) e_all - i (rot(v, m/2)(.)h + rot(v, -m/2)(.)u), one rescale
-    std::vector<std::vector<uint32_t>> g2(BV, {ev.galois_rot(half), ev.galois_rot(half - m)});
-    std::vector<std::vector<DCt>> rv(BV);
-    std::vector<DCt> rall = ev.alloc_many(2 * BV, Lv);
-    for (int l = 0; l < BV; l++) rv[l] = {rall[2 * l], rall[2 * l + 1]};
-    ev.hoisted_many(ptrs(vs), g2, rv);
+    std::vector<std::vector<uint32_t>> g2(nb, {ev.galois_rot(half), ev.galois_rot(half - m)});
+    std::vector<std::vector<DCt>> rv(nb);
+    std::vector<DCt> rall = ev.alloc_many(2 * nb, Lv);
+    for (int i = 0; i < nb; i++) rv[i] = {rall[2 * i], rall[2 * i + 1]};
+    ev.hoisted_many(vb, g2, rv);
     const double ms = ev.mask_scale(Lv);
     const u64* hm = ev.mask(m, 0, m - half, 0, 1, Ns, Lv);
     const u64* um = ev.mask(m, m - half, m, 0, 1, Ns, Lv);
     const u64* em = ev.mask(m, 0, m, 0, 1, Ns, Lv);
     std::vector<std::vector<SumTerm>> t1;
     std::vector<double> sc1;
-    for (int l = 0; l < BV; l++) {
-        t1.push_back({SumTerm{rv[l][0].d, hm}, SumTerm{rv[l][1].d, um}});
-        sc1.push_back(vs[l].scale * ms);
+    for (int i = 0; i < nb; i++) {
+        t1.push_back({SumTerm{rv[i][0].d, hm}, SumTerm{rv[i][1].d, um}});
+        sc1.push_back(vb[i]->scale * ms);
     }
-    for (int l = 0; l < BV; l++) { t1.push_back({SumTerm{vs[l].d, em}}); sc1.push_back(vs[l].scale * ms); }
-    std::vector<DCt> shve = ev.alloc_many(2 * BV, Lv);
+    for (int i = 0; i < nb; i++) { t1.push_back({SumTerm{vb[i]->d, em}}); sc1.push_back(vb[i]->scale * ms); }
+    std::vector<DCt> shve = ev.alloc_many(2 * nb, Lv);
     ev.sum_many(t1, Lv, 2, shve, sc1);
-    std::vector<DCt> d = ev.alloc_many(BV, Lv);
+    std::vector<DCt> d = ev.alloc_many(nb, Lv);
     {
         std::vector<const DCt*> da, db;
-        for (int l = 0; l < BV; l++) { da.push_back(&shve[BV + l]); db.push_back(&shve[l]); }
+        for (int i = 0; i < nb; i++) { da.push_back(&shve[nb + i]); db.push_back(&shve[i]); }
         ev.add_i_many(da, db, d, /*sub=*/true);
     }
-    std::vector<DCt> uu = ev.alloc_many(BV, Lv - 1);
+    std::vector<DCt> uu = ev.alloc_many(nb, Lv - 1);
     ev.rescale_many(ptrs(d), uu);
-    // 2. U bank u_t = Psi^t(uu), t < m/2
-    std::vector<int> tsv;
-    for (int t = 0; t < half; t++) tsv.push_back(t);
+    // 2. U bank u_t = Psi^t(uu), t in the block's range
+    std::vector<std::vector<int>> tsv(nb);
+    for (int i = 0; i < nb; i++) for (int t = ta[i]; t < tb[i]; t++) tsv[i].push_back(t);
     std::vector<std::vector<DCt>> ub;
-    psi_many(ev, ptrs(uu), std::vector<std::vector<int>>(BV, tsv), m, 0, Ns, ub);
-    // 3. Phi bank of p_fd: delta in [-(d_h-1), m/2-1] \ {0}, hoisted
-    const int dmin = -(a.d_h - 1);
-    std::vector<uint32_t> dg;
-    for (int dd = dmin; dd < half; dd++) if (dd) dg.push_back(ev.galois_rot((long)dd * m));
-    std::vector<std::vector<DCt>> pb(BV);
-    std::vector<DCt> pall = ev.alloc_many((int)dg.size() * BV, Lp);
-    for (int l = 0; l < BV; l++) pb[l].assign(pall.begin() + l * dg.size(), pall.begin() + (l + 1) * dg.size());
-    ev.hoisted_many(ptrs(ps), std::vector<std::vector<uint32_t>>(BV, dg), pb);
-    auto pbi = [&](int l, int dd) -> const DCt* {
-        if (dd == 0) return &ps[l];
-        return &pb[l][dd - dmin - (dd > 0 ? 1 : 0)];
+    psi_many(ev, ptrs(uu), tsv, m, 0, Ns, ub);
+    // 3. Phi bank of p_fd over the offsets the range needs: delta = t - u, u < d_h (hoisted, delta = 0 is p itself)
+    const int dmax = a.d_h - 1;
+    std::vector<int> dlo(nb), dhi(nb);
+    std::vector<std::vector<uint32_t>> dg(nb);
+    int nrot = 0;
+    for (int i = 0; i < nb; i++) {
+        dlo[i] = ta[i] - dmax; dhi[i] = tb[i] - 1;
+        for (int dd = dlo[i]; dd <= dhi[i]; dd++) if (dd) { dg[i].push_back(ev.galois_rot((long)dd * m)); nrot++; }
+    }
+    std::vector<std::vector<DCt>> pb(nb);
+    std::vector<DCt> pall = ev.alloc_many(nrot, Lp);
+    for (int i = 0, k = 0; i < nb; i++) { pb[i].assign(pall.begin() + k, pall.begin() + k + dg[i].size()); k += (int)dg[i].size(); }
+    ev.hoisted_many(pbin, dg, pb);
+    auto pbi = [&](int i, int dd) -> const DCt* {
+        if (dd == 0) return pbin[i];
+        return &pb[i][dd - dlo[i] - ((dd > 0 && dlo[i] <= 0) ? 1 : 0)];
     };
     // 4. b_t = sum_u Phi^{t-u}(p) (.) n_u, rescale
     std::vector<const u64*> nmask(a.d_h);
     for (int u = 0; u < a.d_h; u++) nmask[u] = ev.mask(m, 0, m, u, a.seg_stride, a.H_blk, Lp);
-    std::vector<DCt> by = ev.alloc_many(BV * half, Lp);
-    if (a.d_h > 64) throw EncfError(ENCF_ERR_PLAN_SHAPE, "value: d_h > 64 unsupported");
-    for (int l = 0; l < BV; l++)
-        for (int t0 = 0; t0 < half; t0 += 64) {
+    int ntot = 0;
+    for (int i = 0; i < nb; i++) ntot += tb[i] - ta[i];
+    std::vector<DCt> by = ev.alloc_many(ntot, Lp);
+    for (int i = 0, k0 = 0; i < nb; i++) {
+        for (int t0 = ta[i]; t0 < tb[i]; t0 += 64) {
             BcastArgs A;
             A.nu = a.d_h;
-            A.dmax = a.d_h - 1;
-            A.nt = std::min(64, half - t0);
+            A.dmax = dmax;
+            A.nt = std::min(64, tb[i] - t0);
             A.nsrc = A.nt + A.dmax;
-            for (int i = 0; i < A.nsrc; i++) A.src[i] = pbi(l, t0 - A.dmax + i)->d;
+            for (int j = 0; j < A.nsrc; j++) A.src[j] = pbi(i, t0 - A.dmax + j)->d;
             for (int u = 0; u < A.nu; u++) A.mask[u] = nmask[u];
             for (int t = 0; t < A.nt; t++) {
-                DCt& o = by[l * half + t0 + t];
-                o.scale = ps[l].scale * ev.mask_scale(Lp);
+                DCt& o = by[k0 + t0 - ta[i] + t];
+                o.scale = ps[blocks[i]].scale * ev.mask_scale(Lp);
                 A.out[t] = o.d;
             }
             k_bcast_mac(ev.c, A, Lp, ev.s);
         }
-    std::vector<DCt> bt = ev.alloc_many(BV * half, Lp - 1);
+        k0 += tb[i] - ta[i];
+    }
+    std::vector<DCt> bt = ev.alloc_many(ntot, Lp - 1);
     ev.rescale_many(ptrs(by), bt);
-    // 5. o = sum_t u_t (x) b_t (u_t viewed at b_t's level: mod-drop without a copy), one relin, rescale
+    // 5. o3 = sum_t u_t (x) b_t (u_t viewed at b_t's level: mod-drop without a copy)
     const int Lb = Lp - 1;
-    std::vector<std::vector<DCt>> ud(BV);
-    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(BV);
-    for (int l = 0; l < BV; l++) {
-        for (int t = 0; t < half; t++) {
-            DCt v = ub[l][t];
+    std::vector<std::vector<DCt>> ud(nb);
+    std::vector<std::vector<std::pair<const DCt*, const DCt*>>> pairs(nb);
+    for (int i = 0, k0 = 0; i < nb; i++) {
+        for (size_t t = 0; t < ub[i].size(); t++) {
+            DCt v = ub[i][t];
             if (v.L < Lb) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "value: V below P_fd level");
             v.cstride = (i64)v.L * N;
             v.L = Lb;
-            ud[l].push_back(v);
+            ud[i].push_back(v);
         }
-        for (int t = 0; t < half; t++) pairs[l].push_back({&ud[l][t], &bt[l * half + t]});
+        for (size_t t = 0; t < ub[i].size(); t++) pairs[i].push_back({&ud[i][t], &bt[k0 + t]});
+        k0 += tb[i] - ta[i];
     }
-    std::vector<DCt> o3 = ev.alloc_many(BV, Lb, 3);
+    o3 = ev.alloc_many(nb, Lb, 3);
     ev.tensor_many(pairs, o3);
-    outs = ev.alloc_many(BV, Lb - 1);
+}
+
+void value_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& ps, const std::vector<DCt>& vs,
+               std::vector<DCt>& outs) {
+    std::vector<int> blocks;
+    std::vector<DCt> o3;
+    value_partial_run(ev, a, ps, vs, 0, a.B_V * (a.m / 2), blocks, o3);
+    outs = ev.alloc_many(a.B_V, o3[0].L - 1);
     ev.relin_rescale_many(ptrs(o3), outs);   // lazy relin merged with the rescale (R-RELRS)
 }
 

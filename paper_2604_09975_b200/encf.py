@@ -90,6 +90,10 @@ _SIG = {
     "encf_ct_ct_attn_score": [_p, _p, _p, _p, _p, _i32, _i32, _p, _p],
     "encf_attn_export_stream": [_p, _p, _p, _p, _p, _p],
     "encf_ct_ct_attn_value": [_p, _p, _p, _p, _p, _p, _p],
+    "encf_ct_ct_attn_value_partial": [_p, _p, _p, _p, _p, _i32, _i32, _p, _p],
+    "encf_attn_value_finalize": [_p, _p, _p, _i32, _p, _p],
+    "encf_rotfirst": [_p, _p, ctypes.POINTER(CT), _i32, _p, _i32, _i32, _p, _p],
+    "encf_psi": [_p, _p, ctypes.POINTER(CT), _i32, _p, _i32, _p, _p],
     "encf_l_conv": [_p, _i32, _i32, _f64, _f64, ctypes.POINTER(_i32)],
     "encf_export_c2m": [_p, ctypes.POINTER(CT), _i32, _u64, _u64, ctypes.POINTER(CT), _p, _p],
     "encf_mod_reduce": [_p, _p, _i32, _i32, _p],
@@ -150,7 +154,10 @@ class Ciphertext:
         return CT(self.data.data_ptr(), self.n_comp, self.n_limbs, self.scale, self.ntt)
 
     def _update(self, c):
+        N = self.data.numel() // (self.n_comp * self.n_limbs)
         self.n_comp, self.n_limbs, self.scale, self.ntt = c.n_comp, c.n_limbs, c.scale, c.ntt
+        if self.data.numel() > self.n_comp * self.n_limbs * N:     # the library wrote fewer limbs than allocated
+            self.data = self.data[: self.n_comp * self.n_limbs * N]
         return self
 
     @property
@@ -339,6 +346,23 @@ class Context:
         arr = (CT * len(steps))(*[o._c() for o in outs])
         st = np.ascontiguousarray(np.array(steps, dtype=np.int32))
         _chk(_lib.encf_rotate_hoisted(self.h, keys.h, ctypes.byref(a._c()), st.ctypes.data, len(steps), ctypes.cast(arr, _p), _stream()), "rotate_hoisted")
+        return [o._update(arr[i]) for i, o in enumerate(outs)]
+
+    def rotfirst(self, keys, a, L_slots, taus, m):
+        """RotFirst_{L_slots}(a; tau) for every tau (Alg A.3), one hoisted batch; outputs one level down."""
+        outs = [self.empty_ct(a.n_limbs - 1, 2) for _ in taus]
+        arr = (CT * len(taus))(*[o._c() for o in outs])
+        tt = np.ascontiguousarray(np.array(taus, dtype=np.int32))
+        _chk(_lib.encf_rotfirst(self.h, keys.h, ctypes.byref(a._c()), L_slots, tt.ctypes.data, len(taus), m,
+                                ctypes.cast(arr, _p), _stream()), "rotfirst")
+        return [o._update(arr[i]) for i, o in enumerate(outs)]
+
+    def psi(self, keys, a, m, ts):
+        """Psi^t(a) for every t (Alg A.2), one hoisted batch; outputs one level down."""
+        outs = [self.empty_ct(a.n_limbs - 1, 2) for _ in ts]
+        arr = (CT * len(ts))(*[o._c() for o in outs])
+        tt = np.ascontiguousarray(np.array(ts, dtype=np.int32))
+        _chk(_lib.encf_psi(self.h, keys.h, ctypes.byref(a._c()), m, tt.ctypes.data, len(ts), ctypes.cast(arr, _p), _stream()), "psi")
         return [o._update(arr[i]) for i, o in enumerate(outs)]
 
     def conjugate(self, keys, a):
@@ -592,6 +616,30 @@ class AttnPlan:
         oa = (CT * len(outs))(*[o._c() for o in outs])
         _chk(_lib.encf_ct_ct_attn_value(self.ctx.h, keys.h, self.h, ctypes.cast(pa, _p), ctypes.cast(va, _p), ctypes.cast(oa, _p),
                                         _stream()), "attn_value")
+        return [o._update(oa[i]) for i, o in enumerate(outs)]
+
+    def value_blocks(self, unit_begin, unit_end):
+        """Blocks touched by the value units [unit_begin, unit_end) (units flattened l (m/2) + t)."""
+        half = self.m // 2
+        return [l for l in range(self.B_V) if max(unit_begin - l * half, 0) < min(unit_end - l * half, half)]
+
+    def value_partial(self, keys, ps, vs, unit_begin, unit_end):
+        """Unrelinearised 3-component partial sums of the touched blocks (encf_ct_ct_attn_value_partial)."""
+        L = ps[0].n_limbs
+        outs = [self.ctx.empty_ct(L - 1, 3) for _ in self.value_blocks(unit_begin, unit_end)]
+        pa = (CT * len(ps))(*[x._c() for x in ps])
+        va = (CT * len(vs))(*[x._c() for x in vs])
+        oa = (CT * len(outs))(*[o._c() for o in outs])
+        _chk(_lib.encf_ct_ct_attn_value_partial(self.ctx.h, keys.h, self.h, ctypes.cast(pa, _p), ctypes.cast(va, _p), unit_begin,
+                                                unit_end, ctypes.cast(oa, _p), _stream()), "attn_value_partial")
+        return [o._update(oa[i]) for i, o in enumerate(outs)]
+
+    def value_finalize(self, keys, o3s):
+        outs = [self.ctx.empty_ct(o.n_limbs - 1) for o in o3s]
+        ia = (CT * len(o3s))(*[x._c() for x in o3s])
+        oa = (CT * len(outs))(*[o._c() for o in outs])
+        _chk(_lib.encf_attn_value_finalize(self.ctx.h, keys.h, ctypes.cast(ia, _p), len(o3s), ctypes.cast(oa, _p), _stream()),
+             "attn_value_finalize")
         return [o._update(oa[i]) for i, o in enumerate(outs)]
 
 
