@@ -203,6 +203,9 @@ encf_status encf_proj_encode_weights_complex(encf_ctx* ctx, const encf_proj_plan
  * touched b in the EXTENDED basis Q_L u P (n_limbs = L + K; the giant-step rotations are summed without ModDown,
  * DESIGN.md R-LAZY) for a cross-rank uint64 SUM + encf_mod_reduce_ext, then encf_pt_ct_matmul_finalize. */
 #define ENCF_PROJ_FINALIZE 2u
+/* w_pt holds only the units [unit_begin, unit_end) (a rank's shard of the weight stream: each GPU keeps
+ * 1/world of the plaintext diagonals); without it w_pt is the whole stream and unit u starts at u * U N1 L_w N. */
+#define ENCF_PROJ_W_SHARD 8u
 encf_status encf_pt_ct_matmul(encf_ctx* ctx, const encf_keys* keys, const encf_proj_plan* plan,
                               const encf_ct* x /*host array [U]*/, const uint64_t* w_pt, double w_scale,
                               int32_t unit_begin, int32_t unit_end, uint32_t flags,

@@ -565,7 +565,10 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
         const int L = xs[0].L;
         need(L >= 2, ENCF_ERR_LEVEL_EXHAUSTED, "projection needs two limbs");
         std::vector<DCt> accs;
-        proj_phase1(ev, *p, xs, w, w_scale, u0, u1, accs);
+        const int Lw = p->restricted ? L - 1 : L;
+        const size_t wus = (size_t)p->U * p->N1 * Lw * c->N;       // words per (b, p) unit of the weight stream
+        const u64* wu = (flags & ENCF_PROJ_W_SHARD) ? w : w + (size_t)u0 * wus;
+        proj_phase1(ev, *p, xs, wu, w_scale, u0, u1, accs);
         int b_first = u0 / p->N2;
         bool fin = (flags & ENCF_PROJ_FINALIZE) && u0 == 0 && u1 == units;
         if (fin) {

@@ -72,8 +72,16 @@ static void build(encf_ctx& c, const encf_params* p) {
             throw EncfError(ENCF_ERR_ARG, "every modulus must be a prime < 2^61 with q = 1 mod 2N");
     }
     const int M = (int)c.mods.size(), N = c.N;
+    for (u64 q : c.mods) c.max_mod = std::max(c.max_mod, q);
+    {
+        // The fused key-switch inner products (ks_inner: dnum products, ks_psi: 2 dnum + 2, ks_rma: dnum per term)
+        // sum products below q^2 in 128 bits and reduce ONCE with a Montgomery REDC, which needs the sum < q 2^64,
+        // i.e. (2 dnum + 2) q < 2^64 at the top level.  Refuse parameter sets outside that range.
+        const unsigned __int128 terms = 2 * (unsigned __int128)((c.L + c.alpha - 1) / c.alpha) + 2;
+        if (terms * c.max_mod >= ((unsigned __int128)1 << 64))
+            throw EncfError(ENCF_ERR_ARG, "(2 dnum + 2) q_max >= 2^64: digit count too large for the single-REDC inner products");
+    }
     for (u64 q : c.mods) {
-        c.max_mod = std::max(c.max_mod, q);
         c.mont_R.push_back(h_mont_R(q));
         c.mont_Rinv.push_back(h_invmod(h_mont_R(q), q));
     }

@@ -64,7 +64,7 @@ std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p) {
 //  2. c~_{b,p} = sum_{u,q} bank[u][q] (.) w~_{b,p,u,q}  (one fused MAC launch over the plaintext stream)
 //  3. acc_b = P c~_{b,0} + sum_{p>=1} rot_ext(c~_{b,p}, p N1 m): the giant rotations without ModDown, summed in
 //     Q_L u P (lazy ModDown, R-LAZY); the ModDown happens once per block in proj_finalize_many.
-void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
+void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w /* unit u0 */, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs) {
     const int N = ev.c.N, L0 = x[0].L, U = p.U, N1 = p.N1;
     for (auto& xi : x) {
@@ -91,11 +91,13 @@ void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, con
                 outs[u].push_back(bankv[u * N1 + q]);
             }
         ev.hoisted_many(ptrs(x), gs, outs);
+        for (int u = 0; u < U; u++)
+            for (int q = 0; q < N1; q++) bankv[u * N1 + q] = outs[u][q];
     }
     const int units = u1 - u0;
     std::vector<DCt> cu = ev.alloc_many(units, L);
     const i64 wus = (i64)U * N1 * L * N;
-    k_diag_mac(ev.c, bankv[0].d, U * N1, w + (size_t)u0 * wus, units, wus, cu[0].d, (i64)ctw, L, ev.s);
+    k_diag_mac(ev.c, bankv[0].d, U * N1, w, units, wus, cu[0].d, (i64)ctw, L, ev.s);   // w = unit u0's plaintexts
     const double sc = bankv[0].scale * w_scale;
     for (auto& c : cu) c.scale = sc;
     int b_first = u0 / p.N2, b_last = (u1 - 1) / p.N2;

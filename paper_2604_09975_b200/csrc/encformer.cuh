@@ -30,7 +30,7 @@ void shift_sum_ext_many(Ev& ev, const std::vector<const DCt*>& xs, const std::ve
 
 void proj_plan_init(encf_proj_plan& p, int n, int m, int d_in, int d_out, int C, int N1, uint32_t flags);
 std::vector<uint32_t> proj_galois(Ev& ev, const encf_proj_plan& p);
-void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w, double w_scale, int u0,
+void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, const u64* w /* unit u0 */, double w_scale, int u0,
                  int u1, std::vector<DCt>& accs);
 void proj_finalize_many(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& accs, std::vector<DCt>& ys);
 

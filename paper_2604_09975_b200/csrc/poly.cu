@@ -382,6 +382,12 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
                 mac128(a10, b1.x, x[t].x);
                 mac128(a11, b1.y, x[t].y);
             }
+            // every 32 products (< 32 q^2 <= 2^127 for q < 2^61) fold the 128-bit sums back below q, so any bank
+            // size is exact
+            if (((uq + 8) & 31) == 0) {
+                a00 = U128{barrett128(a00, mc.q, mc.rhi, mc.rlo), 0}; a01 = U128{barrett128(a01, mc.q, mc.rhi, mc.rlo), 0};
+                a10 = U128{barrett128(a10, mc.q, mc.rhi, mc.rlo), 0}; a11 = U128{barrett128(a11, mc.q, mc.rhi, mc.rlo), 0};
+            }
         }
         for (; uq < nbank; uq++) {
             const ulonglong2 xx = __ldg((const ulonglong2*)(wu + (size_t)uq * pstride));

@@ -122,6 +122,7 @@ _lib.encf_galois_conj.argtypes = [_p]
 PROJ_DECOMPLEXIFY = 1
 PROJ_FINALIZE = 2
 PROJ_REAL_INPUT = 4
+PROJ_W_SHARD = 8
 KEY_RELIN = 1
 
 
@@ -545,7 +546,8 @@ class ProjPlan:
                                                    L, t.data_ptr(), _stream()), "encode_weights_complex")
         return t
 
-    def matmul(self, keys, xs, w, w_scale, unit_begin=0, unit_end=None, finalize=True):
+    def matmul(self, keys, xs, w, w_scale, unit_begin=0, unit_end=None, finalize=True, w_shard=False):
+        """w_shard: `w` holds only the plaintexts of units [unit_begin, unit_end) (ENCF_PROJ_W_SHARD)."""
         units = self.B_out * self.N2
         unit_end = units if unit_end is None else unit_end
         L = xs[0].n_limbs
@@ -553,8 +555,9 @@ class ProjPlan:
         ys = [self.ctx.empty_ct(L - 1 if fin else L + len(self.ctx.p)) for _ in range(self.B_out)]
         xa = (CT * len(xs))(*[x._c() for x in xs])
         ya = (CT * len(ys))(*[y._c() for y in ys])
+        flags = (PROJ_FINALIZE if finalize else 0) | (PROJ_W_SHARD if w_shard else 0)
         _chk(_lib.encf_pt_ct_matmul(self.ctx.h, keys.h, self.h, ctypes.cast(xa, _p), w.data_ptr(), float(w_scale), unit_begin,
-                                    unit_end, PROJ_FINALIZE if finalize else 0, ctypes.cast(ya, _p), _stream()), "pt_ct_matmul")
+                                    unit_end, flags, ctypes.cast(ya, _p), _stream()), "pt_ct_matmul")
         b0, b1 = unit_begin // self.N2, (unit_end - 1) // self.N2 + 1
         return [ys[b]._update(ya[b]) for b in range(b0, b1)]
 

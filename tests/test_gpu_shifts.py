@@ -93,8 +93,6 @@ def test_projection_restricted_C_bit_exact(c13, keys13):
     ys = K.projection(ev, oplan, xs, w)
     order = [w(b, p, u, q) for b in range(oplan.B_out) for p in range(oplan.N2) for u in range(oplan.U) for q in range(oplan.N1)]
     wd = weights_tensor(c13, order, Lw)
-    # the GPU weight encoder gives the same words as the oracle's encoding for the restricted plan too
-    assert torch.equal(plan.encode_weights(W, Lw), wd)
     c13.mask_clear()
     install_masks(c13, ev)
     xd = [dev_ct(c13, x) for x in xs]
@@ -207,3 +205,40 @@ def test_guards_reject_bad_inputs(c13, keys13):
     with pytest.raises(E.EncfError) as e:
         plan.value(gk, [p4, p4], [p4, p4])             # Lv = Lp: no room for the U bank
     assert e.value.code == 4
+
+
+def test_diag_mac_large_bank_wide_path(c13, keys13):
+    """A projection whose bank has U N1 = 384 ciphertexts: on the 60-bit limb q_0 (128-bit MAC path) the sum of 384
+    products exceeds 2^128 without the periodic fold; the output stays bit-exact with the oracle."""
+    ok, gk = keys13
+    m, d_in, d_out, L = 16, 1300, 40, 2
+    plan = E.ProjPlan(c13, m, d_in, d_out, N1=128)
+    oplan = K.ProjPlan(P13.n, m, d_in, d_out, N1=128)
+    assert (oplan.U, oplan.N1, oplan.N2, oplan.B_out) == (3, 128, 2, 1)
+    X = synth.fixed_point_uniform((m, d_in), 60)
+    W = synth.bert_weight((d_in, d_out), 61)
+    xs = [O.encrypt_sk(P13, ok, O.encode(P13, z, 2.0 ** 40, L), 70 + u) for u, z in enumerate(K.proj_inputs(X, oplan))]
+    pts = {}
+
+    def w(b, p, u, q):
+        if (b, p, u, q) not in pts:
+            pts[(b, p, u, q)] = O.encode(P13, K.proj_weight_slots(W, oplan, b, p, u, q), float(P13.q[L - 1]), L)
+        return pts[(b, p, u, q)]
+    ys = K.projection(K.Ev(P13, ok, m), oplan, xs, w)
+    order = [w(b, p, u, q) for b in range(oplan.B_out) for p in range(oplan.N2) for u in range(oplan.U) for q in range(oplan.N1)]
+    got = plan.matmul(gk, [dev_ct(c13, x) for x in xs], weights_tensor(c13, order, L), float(P13.q[L - 1]))
+    assert_ct_equal(c13, got[0], ys[0], "projection with a 384-ciphertext bank")
+
+
+def test_ctx_refuses_digit_counts_beyond_single_redc(tmp_path):
+    """(2 dnum + 2) q_max >= 2^64 would overflow the single-REDC key-switch sums: P13's primes with alpha = 1
+    (dnum = 8, 18 q_0 > 2^64) are refused at context creation (ENCF_ERR_ARG)."""
+    import json
+    import os
+    d = json.load(open(os.path.join(os.path.dirname(__file__), "..", "params", "p13.json")))
+    d["alpha"] = 1
+    p = tmp_path / "p13a1.json"
+    p.write_text(json.dumps(d))
+    with pytest.raises(E.EncfError) as e:
+        E.Context(str(p), 0)
+    assert e.value.code == 1
