@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear", "bert-large-layer"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: one independent layer per GPU (weak scaling) instead of ONE layer sharded over the N GPUs")
     ap.add_argument("--ablation", default=None, choices=[None, "wo-scp"],
                     help="wo-scp: insert the Halevi-Shoup RMA repack at the three FHE->FHE edges (App. G; Table 11 ablation)")
     return ap.parse_args()
@@ -331,6 +333,8 @@ def run_ours(args):
         return run_ks(args)
     ws, rank, local = dist_init(args)
     torch.cuda.set_device(local)
+    if ws > 1 and args.workload in ("layer", "bert-large-layer") and not args.replicas:
+        return run_sharded(args, ws, rank, local)
     layer = Layer(local, args.workload, seed_off=rank, ablation=args.ablation)
     ctx = layer.ctx
     stream = torch.cuda.current_stream()
@@ -490,6 +494,90 @@ def run_ours(args):
         "setup_s": round(layer.setup_s, 1),
     }
     line["cpu_baseline"] = cpu_baseline(layer, stats, args.steps)
+    print(json.dumps(line), flush=True)
+
+
+def run_sharded(args, ws, rank, local):
+    """ONE BERT layer sharded over the ws GPUs (paper_2604_09975_b200/layer.py): projection (b, p) units
+    with weight-stream shards + an extended-basis uint64 NCCL all-reduce, score t-ranges + all-gather, value
+    (block, t) partials + all-reduce, owner finalisation + all-gathers.  value = per-layer latency (max over
+    ranks), strong scaling (the layer is fixed as N grows).  The step, collectives included, is captured into a
+    CUDA graph when NCCL allows it (else replayed eagerly, said in the JSON)."""
+    import torch
+    from paper_2604_09975_b200 import layer as LY
+    spec = LY.BERT_BASE if args.workload == "layer" else LY.BERT_LARGE
+    t0 = time.time()
+    layer = LY.ShardedLayer(spec, local, LY.Comm(None))
+    setup_s = time.time() - t0
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 1)):
+        layer.step(layer.dev_inputs)
+    torch.cuda.synchronize()
+    ctx = layer.ctx
+    ctx.stats_reset()
+    mode = "cuda-graph"
+    try:
+        from paper_2604_09975_b200.graphs import GraphedStep
+        gstep = GraphedStep(layer.step, layer.dev_inputs)
+        run = gstep
+    except Exception as e:          # NCCL capture unavailable: eager replay
+        mode = "eager (graph capture failed: %s)" % str(e)[:120]
+        torch.cuda.synchronize()
+
+        def run(host=None):
+            if host is not None:
+                for k, hs in host.items():
+                    for dst, h in zip(layer.dev_inputs[k], hs):
+                        dst.data.copy_(h, non_blocking=True)
+            return layer.step(layer.dev_inputs)
+    stats = ctx.stats()
+    for _ in range(2):
+        run()
+    torch.cuda.synchronize()
+    barrier(ws)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            outs = run()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms_step = max_over_ranks(ev0.elapsed_time(ev1), ws) / args.steps
+    e2e = None
+    if not args.no_e2e:
+        outs_h = [(torch.empty(m.data.shape, dtype=m.data.dtype, pin_memory=True), torch.empty(s.shape, dtype=s.dtype, pin_memory=True))
+                  for _, _, (m, s) in outs]
+        d2h = sum(a.numel() * 8 + b.numel() * 8 for a, b in outs_h)
+        d2h = int(max_over_ranks(float(d2h), ws))
+        torch.cuda.synchronize()
+        barrier(ws)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            o = run({k: [h[0] for h in v] for k, v in layer.host_inputs.items()})
+            for (_, _, (m, s)), (hm, hs) in zip(o, outs_h):
+                hm.copy_(m.data, non_blocking=True)
+                hs.copy_(s, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e = {"value": round(max_over_ranks(e0.elapsed_time(e1), ws) / args.steps, 3), "unit": "ms/layer",
+               "h2d_bytes_per_step": layer.h2d_bytes, "d2h_bytes_per_step": d2h,
+               "path": "per rank: H2D(pinned) of the replicated client inputs -> sharded step -> D2H of this rank's exports; max over ranks"}
+    if rank != 0:
+        return
+    line = {
+        "metric": "BERT-base layer CKKS linear latency (ms) & key-switches/s at N=2^16; HBM roofline %",
+        "value": round(ms_step, 3), "unit": "ms/layer", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_step, 3), "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (seeded; BERT-init random weights; encrypted U[-1,1] F=13 activations)",
+        "config": {"workload": spec.name, "N": 65536, "m": spec.m, "d": spec.d, "H": spec.H, "d_ff": spec.dff,
+                   "parallelism": "one layer sharded over %d GPUs: projection (b,p) units (weight shards), score t-ranges, "
+                                  "value (block,t) units; NCCL uint64 all-reduce of partials + all-gather of outputs" % ws,
+                   "execution": mode, "l2": "no flush: plaintext stream per rank >> 126 MB L2"},
+        "key_switches_per_step_rank0": stats["keyswitch"], "gpu_launches": int(stats["kernel_launches"]),
+        "clocks": clk.summary(), "e2e": e2e, "setup_s": round(setup_s, 1),
+    }
     print(json.dumps(line), flush=True)
 
 

@@ -85,12 +85,21 @@ class Comm:
         self.dist.all_gather(parts, t.contiguous(), group=self.group)
         return torch.cat(parts)
 
-    def max_(self, x):
+    def max_(self, x, key=None):
+        """Max over ranks of a host double (ciphertext scales a rank without outputs cannot compute).  Scales are
+        the same at every step, so with `key` the value is exchanged once and cached: later (CUDA-graph captured)
+        steps issue no host-synchronising collective."""
         if self.world == 1:
             return x
+        cache = self.__dict__.setdefault("_cache", {})
+        if key is not None and key in cache:
+            return cache[key]
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
-        return float(t.item())
+        v = float(t.item())
+        if key is not None:
+            cache[key] = v
+        return v
 
 
 def _owned(n, world, rank):
@@ -143,7 +152,7 @@ class ShardedProjection:
             for i, y in enumerate(ys):
                 out[i].copy_(y.data[:2 * Ly * N])
             scale = ys[0].scale
-        scale = comm.max_(scale)
+        scale = comm.max_(scale, ("proj", id(self)))
         allys = comm.all_gather(out)
         return [E.Ciphertext(allys[r * cnt + i], 2, Ly, scale, 1)
                 for r in range(comm.world) for i in range(_owned(plan.B_out, comm.world, r)[1] - _owned(plan.B_out, comm.world, r)[0])]
@@ -224,7 +233,7 @@ class ShardedLayer:
         buf = torch.zeros((cnt, 2 * Ls * N), dtype=torch.int64, device=ctx.device)
         for i, s in enumerate(S):
             buf[i].copy_(s.data[:2 * Ls * N])
-        scale = comm.max_(S[0].scale if S else 0.0)
+        scale = comm.max_(S[0].scale if S else 0.0, "score")
         allS = comm.all_gather(buf)
         out = []
         for r, (a, b) in enumerate(unit_ranges(half, comm.world)):
@@ -245,7 +254,7 @@ class ShardedLayer:
         for l, pr in zip(blocks, parts):
             buf[l].copy_(pr.data[:w3])
         comm.all_reduce_sum_(buf)
-        o3_scale = comm.max_(parts[0].scale if parts else 0.0)
+        o3_scale = comm.max_(parts[0].scale if parts else 0.0, "value_o3")
         b0, b1, cnt = _owned(attn.B_V, comm.world, comm.rank)
         out = torch.zeros((cnt, 2 * (Lb - 1) * N), dtype=torch.int64, device=ctx.device)
         scale = 0.0
@@ -256,7 +265,7 @@ class ShardedLayer:
             for i, o in enumerate(os):
                 out[i].copy_(o.data[:2 * (Lb - 1) * N])
             scale = os[0].scale
-        scale = comm.max_(scale)
+        scale = comm.max_(scale, "value_o")
         allo = comm.all_gather(out)
         res = []
         for r in range(comm.world):
