@@ -549,6 +549,16 @@ RowsCfg rows_cfg(const PhaseCfg& B, int nchunks, int npolys, int nlimbs) {
     return RowsCfg{dim3(nchunks / lc, nlimbs, npolys / lp), lgc};
 }
 
+// Polynomials per launch pair: ENCF_NTT_CHUNK_MB (default 32) MB of limbs, at least one polynomial; 0 = the whole
+// batch in one pair.  Splitting at polynomial granularity keeps every launch's grid identical in shape, so the
+// results are the same words either way.
+int ntt_chunk_polys(const encf_ctx& c, const PolyBatch& b) {
+    static const long mb = [] { const char* e = std::getenv("ENCF_NTT_CHUNK_MB"); return e ? std::atol(e) : 32L; }();
+    if (mb <= 0) return b.npolys;
+    const long per = (long)b.map.n * c.N * 8;
+    return (int)std::max(1L, std::min((long)b.npolys, mb * (1L << 20) / per));
+}
+
 NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     NttArgs a;
     a.base = b.base;
@@ -589,9 +599,20 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    launch_cols<false>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
-    const RowsCfg R = rows_cfg(B, 1 << c.s1, b.npolys, b.map.n);
-    launch_rows<false>(c.s2, R.grid, B.threads, B.smem, s, a, B.lines, R.lgc);
+    // L2-sized chunks of polynomials: the rows phase of a chunk re-reads what the columns phase just wrote while it
+    // is still in the 126 MB L2, instead of after a whole multi-hundred-MB batch has streamed through
+    const int cp = ntt_chunk_polys(c, b);
+    for (int p0 = 0; p0 < b.npolys; p0 += cp) {
+        const int np = std::min(cp, b.npolys - p0);
+        NttArgs ac = a;
+        ac.base = a.base + (i64)p0 * a.poly_stride;
+        if (epi) { ac.epi_src = a.epi_src + p0; ac.epi_out = a.epi_out + p0; ac.epi_add = a.epi_add + p0; }
+        launch_cols<false>(c.s1, dim3(A.blocks, b.map.n, np), A.threads, A.smem, s, ac, A.lines);
+        const RowsCfg R = rows_cfg(B, 1 << c.s1, np, b.map.n);
+        launch_rows<false>(c.s2, R.grid, B.threads, B.smem, s, ac, B.lines, R.lgc);
+        c.st_launch += 2;
+    }
+    c.st_launch -= 2;
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     {
@@ -614,9 +635,18 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    const RowsCfg R = rows_cfg(B, 1 << c.s1, b.npolys, b.map.n);
-    launch_rows<true>(c.s2, R.grid, B.threads, B.smem, s, a, B.lines, R.lgc);
-    launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, b.npolys), A.threads, A.smem, s, a, A.lines);
+    const int cp = ntt_chunk_polys(c, b);      // L2-sized chunks (see ntt_forward_epi)
+    for (int p0 = 0; p0 < b.npolys; p0 += cp) {
+        const int np = std::min(cp, b.npolys - p0);
+        NttArgs ac = a;
+        ac.base = a.base + (i64)p0 * a.poly_stride;
+        if (src) ac.src_base = a.src_base + (i64)p0 * a.poly_stride;
+        const RowsCfg R = rows_cfg(B, 1 << c.s1, np, b.map.n);
+        launch_rows<true>(c.s2, R.grid, B.threads, B.smem, s, ac, B.lines, R.lgc);
+        launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, np), A.threads, A.smem, s, ac, A.lines);
+        c.st_launch += 2;
+    }
+    c.st_launch -= 2;
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     {

@@ -404,6 +404,163 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
     }
 }
 
+// ------------------------------------------------------------------------------------ diagonal MAC, bulk-copy pipeline
+// Same arithmetic and output words as diag_mac_kernel; the plaintext stream reaches shared memory through
+// cp.async.bulk (the TMA engine, SASS UBLKCP) into a DM_STAGES-deep ring of 32 KB stages guarded by mbarriers, so a
+// CTA keeps up to DM_STAGES x 32 KB of HBM reads in flight with no register staging (the register double buffer of
+// diag_mac_kernel limited it to 2 CTAs/SM and ~64 KB per SM).  Stage s = (unit group g of 16 units, bank chunk c of 8
+// rows): 128 rows of 32 coefficients (256 B each, one bulk copy per row, issued by 128 threads), consumed by the 16
+// unit lanes x 16 threads (2 coefficients each) of the CTA; one __syncthreads per stage returns the slot to the ring.
+constexpr int DM_ROWS = 8;
+constexpr int DM_STAGE_WORDS = MAC_LANES * DM_ROWS * MAC_T;   // 4096 words = 32 KB
+constexpr int DM_MAX_STAGES = 5;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+template <bool NARROW>
+__global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(const u64* __restrict__ bank, int nbank,
+                                                                             const u64* __restrict__ w, int units, i64 wus,
+                                                                             u64* __restrict__ acc, i64 accs, int level, int N,
+                                                                             const ModConst* __restrict__ mod, int limb0,
+                                                                             int nstages) {
+    extern __shared__ __align__(128) u64 dm_sm[];
+    u64* stg = dm_sm;                                            // [nstages][16 lanes][8 rows][32 coefficients]
+    u64* sb = stg + (size_t)nstages * DM_STAGE_WORDS;            // bank tile, layout of diag_mac_kernel
+    uint64_t* bars = (uint64_t*)(sb + (size_t)nbank * 2 * MAC_T);
+    const int limb = limb0 + blockIdx.y;
+    const int k0 = blockIdx.x * MAC_T;
+    const ModConst mc = mod[limb];
+    const size_t cs = (size_t)level * N, bs = 2 * cs, pstride = (size_t)level * N;
+    const int tid = threadIdx.x, kp = tid % MAC_TPR, lane = tid / MAC_TPR;
+    if (tid == 0) {
+        for (int i = 0; i < nstages; i++) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // bank tile (read once per CTA; L2-resident across the tiles of one launch)
+    if constexpr (NARROW) {
+        uint2* sn = (uint2*)sb;
+        for (int i = tid; i < nbank * 2 * MAC_T; i += blockDim.x) {
+            const int uq = i / (2 * MAC_T), r = i % (2 * MAC_T), c = r / MAC_T, kk = r % MAC_T;
+            const u64 x = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+            sn[i] = make_uint2((uint32_t)(x >> 20), (uint32_t)(x & 0xFFFFF));
+        }
+    } else {
+        for (int i = tid; i < nbank * 2 * MAC_T; i += blockDim.x) {
+            const int uq = i / (2 * MAC_T), r = i % (2 * MAC_T), c = r / MAC_T, kk = r % MAC_T;
+            sb[i] = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+        }
+    }
+    __syncthreads();
+    const int ngroups = (units + MAC_LANES - 1) / MAC_LANES;
+    const int nch = (nbank + DM_ROWS - 1) / DM_ROWS;
+    const int mygroups = blockIdx.z < ngroups ? (ngroups - 1 - blockIdx.z) / gridDim.z + 1 : 0;
+    const int total = mygroups * nch;
+    const u64* wl = w + (size_t)limb * N + k0;
+    auto issue = [&](int s) {
+        const int g = blockIdx.z + (s / nch) * gridDim.z, c = s % nch;
+        const int rows = min(DM_ROWS, nbank - c * DM_ROWS), ul = min(MAC_LANES, units - g * MAC_LANES);
+        const int slot = s % nstages;
+        if (tid == 0) mbar_arrive_expect_tx(&bars[slot], (uint32_t)(ul * rows * MAC_T * 8));
+        if (tid < MAC_LANES * DM_ROWS) {
+            const int u = tid / DM_ROWS, r = tid % DM_ROWS;
+            if (u < ul && r < rows)
+                bulk_g2s(stg + (size_t)slot * DM_STAGE_WORDS + ((size_t)u * DM_ROWS + r) * MAC_T,
+                         wl + (size_t)(g * MAC_LANES + u) * wus + (size_t)(c * DM_ROWS + r) * pstride, MAC_T * 8, &bars[slot]);
+        }
+    };
+    for (int s = 0; s < nstages - 1 && s < total; s++) issue(s);
+    const u64 t40 = (1ull << 40) % mc.q;
+    u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
+    U128 a00{0, 0}, a01{0, 0}, a10{0, 0}, a11{0, 0};
+    for (int s = 0; s < total; s++) {
+        if (s + nstages - 1 < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of the slot before its refill
+            issue(s + nstages - 1);
+        }
+        const int slot = s % nstages;
+        mbar_wait(&bars[slot], (uint32_t)((s / nstages) & 1));
+        const int g = blockIdx.z + (s / nch) * gridDim.z, c = s % nch;
+        const int rows = min(DM_ROWS, nbank - c * DM_ROWS);
+        const int u = g * MAC_LANES + lane;
+        if (u < units) {
+            const ulonglong2* xr = (const ulonglong2*)(stg + (size_t)slot * DM_STAGE_WORDS + (size_t)lane * DM_ROWS * MAC_T) + kp;
+            if constexpr (NARROW) {
+                const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * DM_ROWS) * 2 * (MAC_T / 2);
+#pragma unroll
+                for (int t = 0; t < DM_ROWS; t++) {
+                    if (t < rows) {
+                        const ulonglong2 x = xr[t * (MAC_T / 2)];
+                        const uint32_t ah = (uint32_t)(x.x >> 20), al = (uint32_t)(x.x & 0xFFFFF);
+                        const uint32_t bh = (uint32_t)(x.y >> 20), bl = (uint32_t)(x.y & 0xFFFFF);
+                        const uint32_t as = ah + al, bsum = bh + bl;
+                        const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
+                        const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
+                        h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
+                        h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
+                        h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
+                        h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
+                    }
+                }
+            } else {
+                const ulonglong2* sbw = (const ulonglong2*)sb;
+#pragma unroll
+                for (int t = 0; t < DM_ROWS; t++) {
+                    if (t < rows) {
+                        const int uq = c * DM_ROWS + t;
+                        const ulonglong2 x = xr[t * (MAC_T / 2)];
+                        const ulonglong2 b0 = sbw[uq * MAC_T + kp];
+                        const ulonglong2 b1 = sbw[uq * MAC_T + MAC_T / 2 + kp];
+                        mac128(a00, b0.x, x.x);
+                        mac128(a01, b0.y, x.y);
+                        mac128(a10, b1.x, x.x);
+                        mac128(a11, b1.y, x.y);
+                    }
+                }
+                if ((c & 3) == 3) {     // every 32 products (< 32 q^2 <= 2^127 for q < 2^61): fold below q
+                    a00 = U128{barrett128(a00, mc.q, mc.rhi, mc.rlo), 0}; a01 = U128{barrett128(a01, mc.q, mc.rhi, mc.rlo), 0};
+                    a10 = U128{barrett128(a10, mc.q, mc.rhi, mc.rlo), 0}; a11 = U128{barrett128(a11, mc.q, mc.rhi, mc.rlo), 0};
+                }
+            }
+            if (c == nch - 1) {
+                u64* o = acc + (size_t)u * accs + (size_t)limb * N + k0 + 2 * kp;
+                if constexpr (NARROW) {
+                    *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
+                                                      kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
+                    *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
+                                                             kara_combine(h11, l11, s11, mc.q, mc.rhi, mc.rlo, t40));
+                    h00 = l00 = s00 = h01 = l01 = s01 = h10 = l10 = s10 = h11 = l11 = s11 = 0;
+                } else {
+                    *(ulonglong2*)o = make_ulonglong2(barrett128(a00, mc.q, mc.rhi, mc.rlo), barrett128(a01, mc.q, mc.rhi, mc.rlo));
+                    *(ulonglong2*)(o + cs) = make_ulonglong2(barrett128(a10, mc.q, mc.rhi, mc.rlo),
+                                                             barrett128(a11, mc.q, mc.rhi, mc.rlo));
+                    a00 = a01 = a10 = a11 = U128{0, 0};
+                }
+            }
+        }
+        __syncthreads();     // every thread is done with this slot: it may be refilled
+    }
+}
+
 // ------------------------------------------------------------------------------------ export (Alg 3 step 1)
 __global__ void export_mask_kernel(u64 seed, u64 stream, u64* c0, u64* share, int level, int N, const ModConst* mod) {
     size_t total = (size_t)level * N;
@@ -687,12 +844,37 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
                            (uint64_t)units * 2 * level * c.N * 8;
     int slot;
     c.prof_begin("diag_mac", s, bytes, slot);
-    if (nw > 0)
-        diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
-                                                                                        level, c.N, c.d_mod, 0);
-    if (nw < level)
-        diag_mac_kernel<true><<<dim3(tiles, level - nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc,
-                                                                                               accs, level, c.N, c.d_mod, nw);
+    // bulk-copy (TMA) pipeline when the bank tile leaves room for >= 2 stages of 32 KB (ENCF_MAC_LEGACY: register path)
+    static const bool legacy = std::getenv("ENCF_MAC_LEGACY") != nullptr;
+    constexpr size_t kMaxSmem = 227 * 1024;
+    const size_t bank_b = (size_t)nbank * 2 * MAC_T * 8;
+    const int nst = bank_b + 2 * DM_STAGE_WORDS * 8 + 64 <= kMaxSmem
+                        ? (int)std::min<size_t>(DM_MAX_STAGES, (kMaxSmem - bank_b - 64) / (DM_STAGE_WORDS * 8)) : 0;
+    if (!legacy && nst >= 2) {
+        static bool tma_attr = false;
+        if (!tma_attr) {
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+            tma_attr = true;
+        }
+        const size_t tsm = (size_t)nst * DM_STAGE_WORDS * 8 + bank_b + (size_t)nst * 8;
+        const int groups = (units + MAC_LANES - 1) / MAC_LANES;
+        int zs = 1;
+        while ((size_t)tiles * level * zs < 148 && zs < groups) zs *= 2;
+        if (nw > 0)
+            diag_mac_tma_kernel<false><<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(bank, nbank, w, units, wus, acc, accs,
+                                                                                           level, c.N, c.d_mod, 0, nst);
+        if (nw < level)
+            diag_mac_tma_kernel<true><<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(bank, nbank, w, units, wus, acc,
+                                                                                                  accs, level, c.N, c.d_mod, nw, nst);
+    } else {
+        if (nw > 0)
+            diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
+                                                                                            level, c.N, c.d_mod, 0);
+        if (nw < level)
+            diag_mac_kernel<true><<<dim3(tiles, level - nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc,
+                                                                                                   accs, level, c.N, c.d_mod, nw);
+    }
     c.prof_end(slot, s);
     c.st_launch += (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // the 128-bit and the narrow launch
     c.st_bytes += bytes;
