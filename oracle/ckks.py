@@ -131,9 +131,11 @@ class Params:
         self.alpha = int(d["alpha"])
         self.L_max = len(self.q)
         self.log2_scale = int(d["log2_scale"])
-        self.P = 1
+        self.P = 1                      # the product of ALL special primes (keys are generated for it)
         for pk in self.p:
             self.P *= pk
+        # K(L): special primes a key switch at level L extends by (DESIGN.md R-KL; data in the param file, else all)
+        self.K_of_level = [int(k) for k in d.get("K_of_level", [len(self.p)] * self.L_max)]
 
     def dnum(self, L):
         return -(-L // self.alpha)
@@ -141,12 +143,22 @@ class Params:
     def digit(self, j, L):
         return j * self.alpha, min((j + 1) * self.alpha, L)
 
+    def K(self, L):
+        return self.K_of_level[L - 1]
+
+    def P_of(self, L):
+        """P_{K(L)} = p_0 ... p_{K(L)-1}: the special modulus of a key switch at level L."""
+        out = 1
+        for pk in self.p[:self.K(L)]:
+            out *= pk
+        return out
+
     # global limb ids: q_i -> i ; p_k -> L_max + k  (PRNG index layout and key limb layout)
     def ext_mods(self, L):
-        return self.q[:L] + self.p
+        return self.q[:L] + self.p[:self.K(L)]
 
     def ext_gids(self, L):
-        return list(range(L)) + [self.L_max + k for k in range(len(self.p))]
+        return list(range(L)) + [self.L_max + k for k in range(self.K(L))]
 
     def psi(self, q):
         return primitive_root_2n(q, self.N)
@@ -442,6 +454,7 @@ class Keys:
         mods = P.ext_mods(self.max_level)
         self.s = from_signed(self.s_signed, mods, N)          # over Q_max * P
         self.ksk = {}
+        self._sp = {}
         self._ntt_cache = {}
         targets = list(galois) + ([0] if relin else [])
         for g in targets:
@@ -452,28 +465,49 @@ class Keys:
         ML = self.max_level
         mods, gids = P.ext_mods(ML), P.ext_gids(ML)
         sp = ring_mul(self.s, self.s, mods, N) if g == 0 else automorph(self.s, g, mods, N)
+        self._sp[g] = sp
+        PK = P.P_of(ML)
         out = []
         for j in range(P.dnum(ML)):
             lo, hi = P.digit(j, ML)
             a = sample_uniform(self.seed, stream_ksk(g, j, 0), mods, gids, N)
             e = from_signed(sample_cbd21(self.seed, stream_ksk(g, j, 1), N), mods, N)
-            gfac = [(P.P % t) if lo <= i < hi else 0 for i, t in enumerate(mods)]
+            gfac = [(PK % t) if lo <= i < hi else 0 for i, t in enumerate(mods)]
             b = padd(psub(e, ring_mul(a, self.s, mods, N), mods, N), pmul_scalar(sp, gfac, mods, N), mods, N)
             out.append(np.stack([b, a]))
-        return out                     # list over digits of [2][ML+alpha][N]
+        return out                     # list over digits of [2][ML+K(ML)][N]
+
+    _sp = None
 
     def s_at(self, L):
         return np.ascontiguousarray(self.s[:L])
 
     def key_at(self, g, L):
-        """Key for Galois element g restricted to level L: digits j < dnum(L), limbs Q_L u P."""
+        """Key for Galois element g at level L: digits j < dnum(L), limbs Q_L u P_{K(L)}.  When L's special-prime
+        class K(L) is below the generated class K(ML) (DESIGN.md R-KL) the key of the smaller special modulus
+        P_{K(L)} is ksk_j = (-a_j s + e_j + g_j^{(K(L))} s', a_j) with the SAME a_j, e_j restricted to the smaller
+        basis: b_j += (P_{K(L)} - P_{K(ML)}) s' on digit j's q-limbs."""
         if g not in self.ksk:
             raise OracleError("MISSING_KEY g=%d" % g)
         ML = self.max_level
         if L > ML:
             raise OracleError("LEVEL_MISMATCH: key generated up to level %d" % ML)
-        idx = list(range(L)) + list(range(ML, ML + len(self.P.p)))
-        return [np.ascontiguousarray(k[:, idx]) for k in self.ksk[g][: self.P.dnum(L)]]
+        P = self.P
+        ck = (g, L)
+        cache = self.__dict__.setdefault("_key_cache", {})
+        if ck in cache:
+            return cache[ck]
+        KL = P.K(L)
+        idx = list(range(L)) + list(range(ML, ML + KL))
+        out = [np.ascontiguousarray(k[:, idx]) for k in self.ksk[g][: P.dnum(L)]]
+        if KL != P.K(ML):
+            d = P.P_of(L) - P.P_of(ML)
+            for j, kj in enumerate(out):
+                lo, hi = P.digit(j, L)
+                mods = P.q[lo:hi]
+                kj[0][lo:hi] = padd(kj[0][lo:hi], pmul_scalar(self._sp[g][lo:hi], [d % q for q in mods], mods, P.N), mods, P.N)
+        cache[ck] = out
+        return out
 
 
 def galois_rot(P, r):
@@ -541,28 +575,30 @@ def moddown(P, b, L):
     BConv_{P->Q};  out_i = (b_i - y_i) * P^{-1} mod q_i  =  round(b / P)  (SURVEY's floor version leaves
     an error u in [0, K) per coefficient, ~2^-19 relative after a projection -- above the 2^-20 target)."""
     N = P.N
-    y = bconv_round(b[L:], P.p, P.q[:L], N)
-    pinv = [pow(P.P % q, -1, q) for q in P.q[:L]]
+    PK = P.P_of(L)                    # the special modulus of level L (R-KL)
+    y = bconv_round(b[L:], P.p[:P.K(L)], P.q[:L], N)
+    pinv = [pow(PK % q, -1, q) for q in P.q[:L]]
     return pmul_scalar(psub(b[:L], y, P.q[:L], N), pinv, P.q[:L], N)
 
 
 def lift_P(P, c, L):
-    """P * c in the extended basis Q_L u P: (P mod q_i) c_i on the q-limbs, 0 on the p-limbs."""
+    """P * c in the extended basis Q_L u P (P = P_{K(L)}): (P mod q_i) c_i on the q-limbs, 0 on the p-limbs."""
     N = P.N
-    out = np.zeros((L + len(P.p), N), dtype=np.uint64)
-    out[:L] = pmul_scalar(c, [P.P % q for q in P.q[:L]], P.q[:L], N)
+    PK = P.P_of(L)
+    out = np.zeros((L + P.K(L), N), dtype=np.uint64)
+    out[:L] = pmul_scalar(c, [PK % q for q in P.q[:L]], P.q[:L], N)
     return out
 
 
 def moddown_rescale(P, x, L):
     """Merged ModDown + rescale (DESIGN.md R-LAZY): x over Q_L u P (coefficient form) ->
     round(x / (P q_{L-1})) mod Q_{L-1}, through ONE rounded fast base conversion from the basis
-    B' = {q_{L-1}, p_0..p_{K-1}} to Q_{L-1}."""
+    B' = {q_{L-1}, p_0..p_{K(L)-1}} to Q_{L-1}."""
     N = P.N
-    bp = [P.q[L - 1]] + P.p
+    bp = [P.q[L - 1]] + P.p[:P.K(L)]
     rows = np.concatenate([x[L - 1:L], x[L:]])
     y = bconv_round(rows, bp, P.q[:L - 1], N)
-    Bp = P.P * P.q[L - 1]
+    Bp = P.P_of(L) * P.q[L - 1]
     inv = [pow(Bp % q, -1, q) for q in P.q[:L - 1]]
     return pmul_scalar(psub(x[:L - 1], y, P.q[:L - 1], N), inv, P.q[:L - 1], N)
 

@@ -73,18 +73,26 @@ class Params:
         self.p = [int(x) for x in d["p"]]
         self.alpha = int(d["alpha"])
         self.Lmax = len(self.q)
-        self.P = 1
-        for x in self.p:
-            self.P *= x
+        self.Kl = [int(k) for k in d.get("K_of_level", [len(self.p)] * self.Lmax)]
 
     def dnum(self, L):
         return -(-L // self.alpha)
 
+    def K(self, L):
+        """Special primes of a key switch at level L (DESIGN.md R-KL)."""
+        return self.Kl[L - 1]
+
+    def PK(self, L):
+        out = 1
+        for x in self.p[:self.K(L)]:
+            out *= x
+        return out
+
     def ext(self, L):
-        return self.q[:L] + self.p
+        return self.q[:L] + self.p[:self.K(L)]
 
     def gids(self, L):
-        return list(range(L)) + [self.Lmax + k for k in range(len(self.p))]
+        return list(range(L)) + [self.Lmax + k for k in range(self.K(L))]
 
 
 def negacyclic(a, b, q):
@@ -157,15 +165,21 @@ class Keys:
         self.s_signed = ternary(seed, S_SK, N)
         mods = P.ext(self.ML)
         self.s = [[v % t for v in self.s_signed] for t in mods]
-        self.ksk = {}
-        for g in list(galois) + ([0] if relin else []):
-            self.ksk[g] = self._gen(g)
+        self.galois = list(galois) + ([0] if relin else [])
+        self._cls = {}
+        self.ksk = {g: self._gen(g, P.K(self.ML)) for g in self.galois}
 
-    def _gen(self, g):
+    def _gen(self, g, K):
+        """The key of special modulus P_K = p_0..p_{K-1} over Q_ML u P_K, generated from its definition (each class
+        K of DESIGN.md R-KL on its own: same streams, so the a_j / e_j draws are shared by construction)."""
         P, ML = self.P, self.ML
-        mods, gids = P.ext(ML), P.gids(ML)
-        sp = [negacyclic(s, s, t) for s, t in zip(self.s, mods)] if g == 0 else \
-             [automorph(s, g, t) for s, t in zip(self.s, mods)]
+        mods = self.P.q[:ML] + self.P.p[:K]
+        gids = list(range(ML)) + [P.Lmax + k for k in range(K)]
+        PK = 1
+        for x in P.p[:K]:
+            PK *= x
+        s = [[v % t for v in self.s_signed] for t in mods]
+        sp = [negacyclic(si, si, t) for si, t in zip(s, mods)] if g == 0 else [automorph(si, g, t) for si, t in zip(s, mods)]
         out = []
         for j in range(P.dnum(ML)):
             lo, hi = j * P.alpha, min((j + 1) * P.alpha, ML)
@@ -173,9 +187,9 @@ class Keys:
             b, a = [], []
             for i, (t, gid) in enumerate(zip(mods, gids)):
                 ai = uniform(self.seed, s_ksk(g, j, 0), t, gid, P.N)
-                bi = psub([v % t for v in e], negacyclic(ai, self.s[i], t), t)
+                bi = psub([v % t for v in e], negacyclic(ai, s[i], t), t)
                 if lo <= i < hi:
-                    bi = padd(bi, smul(sp[i], P.P % t, t), t)
+                    bi = padd(bi, smul(sp[i], PK % t, t), t)
                 b.append(bi)
                 a.append(ai)
             out.append((b, a))
@@ -185,9 +199,11 @@ class Keys:
         return self.s[:L]
 
     def key_at(self, g, L):
-        ML, K = self.ML, len(self.P.p)
+        ML, K = self.ML, self.P.K(L)
+        if (g, K) not in self._cls:
+            self._cls[(g, K)] = self.ksk[g] if K == self.P.K(ML) else self._gen(g, K)
         idx = list(range(L)) + list(range(ML, ML + K))
-        return [([b[i] for i in idx], [a[i] for i in idx]) for (b, a) in self.ksk[g][: self.P.dnum(L)]]
+        return [([b[i] for i in idx], [a[i] for i in idx]) for (b, a) in self._cls[(g, K)][: self.P.dnum(L)]]
 
 
 class Ct:
@@ -292,15 +308,16 @@ def div_round(x, L, P, base_idx, keep):
 
 
 def moddown(P, b, L):
-    return div_round(b, L, P, list(range(L, L + len(P.p))), L)
+    return div_round(b, L, P, list(range(L, L + P.K(L))), L)
 
 
 def moddown_rescale(P, x, L):
-    return div_round(x, L, P, [L - 1] + list(range(L, L + len(P.p))), L - 1)
+    return div_round(x, L, P, [L - 1] + list(range(L, L + P.K(L))), L - 1)
 
 
 def lift_P(P, c, L):
-    return [smul(c[i], P.P % P.q[i], P.q[i]) for i in range(L)] + [[0] * P.N for _ in P.p]
+    PK = P.PK(L)
+    return [smul(c[i], PK % P.q[i], P.q[i]) for i in range(L)] + [[0] * P.N for _ in range(P.K(L))]
 
 
 def rotate_ext(P, keys, ct, g, ext=None):

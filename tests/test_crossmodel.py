@@ -133,6 +133,50 @@ def test_bconv_round_fixed_point_is_exact_rounding():
             assert [yy % q for q in outq] == [int(got[i][k]) for i in range(len(outq))]
 
 
+# ------------------------------------------------------------------ per-level special-prime count K(L) (DESIGN.md R-KL)
+def test_k_of_level_definition_and_classes():
+    """P5A6 (alpha = 6, five 60-bit special primes): K(L) is the smallest K with P_K >= 2^16 max_j Q_j(L), and at
+    every level the cross-model -- which generates each special-prime class's key from its definition -- equals the
+    oracle -- which derives it from the top class's key -- on keys, single / hoisted rotations, conj, relin, the
+    merged ModDown + rescale and the projection and value schedules."""
+    PA, XA = O.Params("P5A6"), X.Params("P5A6")
+    for L in range(1, PA.L_max + 1):
+        D = 1
+        for i in range(L):
+            D *= PA.q[i]
+        KL = PA.K(L)
+        assert PA.P_of(L) >= D << 16 and (KL == 1 or PA.P_of(L) // PA.p[KL - 1] < D << 16), L
+        assert PA.ext_mods(L) == XA.ext(L) and len(PA.ext_mods(L)) == L + KL
+    assert len(set(PA.K_of_level)) >= 3
+    g = [O.galois_rot(PA, r) for r in (1, 2, -1, 4)] + [O.galois_conj(PA)]
+    ok, xk = O.Keys(PA, 7, galois=g, relin=True), X.Keys(XA, 7, galois=g, relin=True)
+    for L in range(1, PA.L_max + 1):
+        for gg in g + [0]:
+            ko, kx = ok.key_at(gg, L), xk.key_at(gg, L)
+            for j in range(len(ko)):
+                assert np.array_equal(ko[j], to_np(list(kx[j]))), (L, gg, j)
+        m = O.encode(PA, synth.complex_slots(PA.n, 50 + L), 2.0 ** 40, L)
+        oc = O.encrypt_sk(PA, ok, m, 9)
+        xc = X.encrypt_sk(XA, xk, [[int(v) for v in limb] for limb in m.m], 2.0 ** 40, 9)
+        same(X.rotate(XA, xk, xc, X.galois_rot(XA, 1)), O.rotate(PA, ok, oc, 1), "rotate L=%d" % L)
+        ext = X.modup(XA, xc.c[1], L)
+        for r, oh in zip([2, -1], O.rotate_hoisted(PA, ok, oc, [2, -1])):
+            same(X.rotate(XA, xk, xc, X.galois_rot(XA, r), ext), oh, "hoisted L=%d" % L)
+        same(X.rotate(XA, xk, xc, 2 * XA.N - 1), O.conjugate(PA, ok, oc), "conj L=%d" % L)
+        if L > 1:
+            oe = O.rotate_hoisted_ext(PA, ok, oc, [4])[0]
+            xe = X.rotate_ext(XA, xk, xc, X.galois_rot(XA, 4), ext)
+            assert np.array_equal(to_np(xe), oe)
+            assert np.array_equal(to_np([X.moddown_rescale(XA, xe[c], L) for c in range(2)]),
+                                  np.stack([O.moddown_rescale(PA, oe[c], L) for c in range(2)]))
+            xev = X.XEv(XA, xk, 4, None)
+            t = O.tensor(PA, oc, oc)
+            same(xev.relin_rescale(xev.tensor(xc, xc)), K.Ev(PA, ok, 4).relin_rescale(t), "relin_rescale L=%d" % L)
+            # decryption after the key switch stays exact to the noise (the class key is a valid key for P_K(L))
+            z = O.decode(PA, O.decrypt(PA, ok, O.rotate(PA, ok, oc, 1)))
+            assert np.abs(z - np.roll(synth.complex_slots(PA.n, 50 + L), -1)).max() < 1e-6
+
+
 # ------------------------------------------------------------------ the kernels' schedules on both arithmetics
 def _xw(pt):
     return ([[int(v) for v in limb] for limb in pt.m], pt.scale)
