@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear", "bert-large-layer"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the oracle timing (A/B kernel experiments only)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent layer per GPU (weak scaling) instead of ONE layer sharded over the N GPUs")
     ap.add_argument("--ablation", default=None, choices=[None, "wo-scp"],
@@ -260,10 +261,23 @@ class Layer:
         return {k: [self.E.Ciphertext(h[0].to(self.ctx.device, non_blocking=True), h[1], h[2], h[3], 1) for h in v]
                 for k, v in self.host_inputs.items()}
 
+    MASK_EPOCH = 1 << 32
+
     def _export(self, cts, sid):
+        """C2M export: ciphertext i of boundary `sid` draws its mask from stream (epoch 2^32 + sid + i) with the
+        (seed, base) read from a DEVICE buffer that every step advances by one epoch (also inside the replayed CUDA
+        graph), so no one-time pad is ever reused across inferences."""
         if not cts:
             return []
-        return self.ctx.export_c2m_many(cts, self.Lconv, self.mask_seed, sid)   # ciphertext i: stream id sid + i
+        if getattr(self, "mask_state", None) is None:
+            self.mask_state = {}
+        if sid not in self.mask_state:
+            self.mask_state[sid] = self.torch.tensor([self.mask_seed, sid], dtype=self.torch.int64, device=self.ctx.device)
+        return self.ctx.export_c2m_many(cts, self.Lconv, self.mask_state[sid], 0)
+
+    def _advance_masks(self):
+        for t in (getattr(self, "mask_state", None) or {}).values():
+            t[1:].add_(self.MASK_EPOCH)
 
     def _complex_pairs(self, ys):
         out = [self.ctx.complexify(ys[2 * i], ys[2 * i + 1]) for i in range(len(ys) // 2)]
@@ -296,6 +310,7 @@ class Layer:
             g2 = self.ff2.matmul(keys, inp["f2"], self.w_2, float(ctx.q[L_FF - 1]))
             ex += self._export(self._complex_pairs(g2), 300)
             self._mark("ff2")
+            self._advance_masks()
             return ex
         if self.workload == "qkv":
             return [(c.data, None) for c in y]
@@ -322,6 +337,7 @@ class Layer:
         g2 = self.ff2.matmul(keys, inp["f2"], self.w_2, float(ctx.q[L_FF - 1]))
         ex += self._export(self._complex_pairs(g2), 300)
         self._mark("ff2")
+        self._advance_masks()                # next inference: fresh C2M masks (device-side, captured in the graph)
         return ex
 
     def download(self, outs):
@@ -503,7 +519,7 @@ def run_ours(args):
         "setup_s": round(layer.setup_s, 1),
     }
     if args.workload in ("layer", "bert-large-layer"):
-        parts = layer_model_bytes(ctx.N, len(ctx.p), ctx.alpha, None,
+        parts = layer_model_bytes(ctx.N, ctx.K, ctx.alpha, None,
                                   [("qkv", layer.qkv, L_QKV), ("out_proj", layer.oproj, L_V_P - 2), ("ff1", layer.ff1, L_FF),
                                    ("ff2", layer.ff2, L_FF)], layer.attn, {"score": L_QKV - 1, "p": L_V_P, "v": L_QKV - 1})
         tot = sum(parts.values())
@@ -521,7 +537,7 @@ def run_ours(args):
             line["ks_config2"] = ks_config2(ctx, 0x5EED, hbm)
         except Exception as e:       # the microbench is an extra key; never lose the main line
             line["ks_config2"] = {"error": str(e)[:200]}
-    line["cpu_baseline"] = cpu_baseline(layer, stats, args.steps)
+    line["cpu_baseline"] = None if args.no_cpu_baseline else cpu_baseline(layer, stats, args.steps)
     print(json.dumps(line), flush=True)
 
 
@@ -622,7 +638,7 @@ def run_ks(args):
     torch.cuda.set_device(local)
     ctx = E.Context("P16", local)
     L, m = 24, M
-    K = len(ctx.p)
+    K = ctx.K(L)
     steps32 = [k * m for k in range(1, 32)]
     galois = sorted({ctx.galois_rot(s) for s in steps32} | {ctx.galois_conj()})
     t0 = time.time()
@@ -700,7 +716,7 @@ def run_ks(args):
 def layer_model_bytes(N, K, alpha, spec, pplans, attn, L_lv):
     """Algorithmic HBM bytes of one layer from SURVEY §8(d)'s per-unit formulas (what the METHOD must move; the
     dense work it avoids and the implementation's own extra passes are not counted).  limb = N 8 B;
-    ct(L) = 2 L limb, pt(L) = L limb, key(L) = dnum(L) 2 (L + K) limb.
+    ct(L) = 2 L limb, pt(L) = L limb, key(L) = dnum(L) 2 (L + K(L)) limb (K(L): the level's special primes, R-KL).
       projection: B_out U C pt(L) + 2 U N1 ct(L) + U (N1-1)(key + ct) + B_out N2 ct + B_out N2 (key + 2 ct) + B_out (ct(L) + ct(L-1))
       hoisted rotation: key(L) + ct(L) (+ ct(L) once per input); single KS: key(L) + 2 ct(L); relin: key + 5 L limb
       tensor: 2 ct(L) per operand pair + 3 L limb out; masked plaintexts pt(L) per distinct mask; export: 2 ct(Lc) + pt(Lc).
@@ -709,7 +725,7 @@ def layer_model_bytes(N, K, alpha, spec, pplans, attn, L_lv):
     dnum = lambda L: -(-L // alpha)                       # noqa: E731
     ct = lambda L: 2 * L * limb                            # noqa: E731
     pt = lambda L: L * limb                                # noqa: E731
-    key = lambda L: dnum(L) * 2 * (L + K) * limb           # noqa: E731
+    key = lambda L: dnum(L) * 2 * (L + K(L)) * limb        # noqa: E731
     hoist = lambda n, L: n * (key(L) + ct(L)) + ct(L)      # noqa: E731
     parts = {}
     for name, pl, L in pplans:
@@ -757,7 +773,7 @@ def ks_config2(ctx, keys_seed, hbm, reps=3):
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / reps
     limb = ctx.N * 8
-    key_b = 3 * 2 * (L + len(ctx.p)) * limb
+    key_b = 3 * 2 * (L + ctx.K(L)) * limb
     hb = 31 * (key_b + 2 * L * limb) + 2 * L * limb
     keys.close()
     gbs = hb / (ms * 1e-3) / 1e9

@@ -63,8 +63,12 @@ typedef struct { uint64_t* data; int32_t n_comp; int32_t n_limbs; double scale; 
 typedef struct { uint64_t* data; int32_t n_limbs; double scale; int32_t ntt; } encf_pt;
 
 /* Parameter set (params/*.json): N a power of two in [2^4, 2^16]; q[0..L-1] body primes, p[0..K-1]
- * special primes, all < 2^61, = 1 mod 2N; alpha = limbs per key-switching digit (hybrid KS). */
-typedef struct { int32_t N; int32_t L; int32_t K; int32_t alpha; const uint64_t* q; const uint64_t* p; } encf_params;
+ * special primes, all < 2^61, = 1 mod 2N; alpha = limbs per key-switching digit (hybrid KS).
+ * K_of_level (host [L], may be NULL): a key switch at level l extends by the first K_of_level[l-1] special primes
+ * (non-decreasing, in [1, K]; DESIGN.md R-KL); NULL = all K at every level.  Extended-basis objects at level l
+ * (partial projection accumulators, ext masks) have l + K_of_level[l-1] limbs.  Errors: ARG. */
+typedef struct { int32_t N; int32_t L; int32_t K; int32_t alpha; const uint64_t* q; const uint64_t* p;
+                 const int32_t* K_of_level; } encf_params;
 
 /* Counters (SURVEY §5 "Tracing"): accumulated since context creation. */
 typedef struct {
@@ -277,6 +281,13 @@ encf_status encf_export_c2m(encf_ctx* ctx, const encf_ct* in, int32_t L_conv, ui
 encf_status encf_export_c2m_many(encf_ctx* ctx, const encf_ct* in /*host array of n*/, int32_t n, int32_t L_conv,
                                  uint64_t mask_seed, uint64_t stream_id0, uint64_t* masked, uint64_t* shares,
                                  void* stream);
+/* encf_export_c2m_many with (mask_seed, stream_id0) read from DEVICE memory d_seed_sid [2] when the kernels run:
+ * ciphertext i uses seed d_seed_sid[0] and stream id (d_seed_sid[1] + i) mod 2^56.  A step captured into a CUDA
+ * graph that advances d_seed_sid[1] every replay draws fresh masks r^ per inference (a replayed constant seed would
+ * reuse the one-time pad: the difference of two masked exports would leak the difference of the messages). */
+encf_status encf_export_c2m_many_dev(encf_ctx* ctx, const encf_ct* in /*host array of n*/, int32_t n, int32_t L_conv,
+                                     const uint64_t* d_seed_sid /*device [2]*/, uint64_t* masked, uint64_t* shares,
+                                     void* stream);
 /* ------------------------------------------------------------------------------------------ import (Alg 4, GPU half) */
 /* Ring2Field local map (App. C): after Pi_Ext, party b holds m'_b in [0, 2^{ell+sigma}) per
  * coefficient (device [N] little-endian (lo, hi) 64-bit pairs) with m'_0 + m'_1 = 2^{ell+sigma} + cl(m);

@@ -114,13 +114,15 @@ encf_status encf_keygen(encf_ctx* c, uint64_t seed, const uint32_t* galois, int3
         need(c && out && (n_galois == 0 || galois), ENCF_ERR_ARG, "keygen: null argument");
         level_ok(c, max_level);
         cudaStream_t s = S(stream);
-        const int N = c->N, K = c->K, ML = max_level, nl = ML + K;
+        // keys of the top class K(max_level) (R-KL); lower classes are derived on first use (Ev::key_for)
+        const int N = c->N, ML = max_level, K = c->Kof(ML), nl = ML + K;
         encf_keys* k = new encf_keys();
         static std::atomic<uint64_t> next_id{1};
         k->id = next_id++;
         k->max_level = ML;
         k->dnum = c->dnum(ML);
         k->device = c->device;
+        k->ctx = c;
         auto alloc = [&](size_t words) { void* p; CUDA_TRY(cudaMalloc(&p, words * 8)); k->allocations.push_back(p); return (u64*)p; };
         LimbMap em = c->extmap(ML);
         std::vector<int> gids(nl);
@@ -190,6 +192,13 @@ encf_status encf_keys_destroy(encf_keys* k) {
     if (!k) return ENCF_ERR_ARG;
     cudaSetDevice(k->device);
     cudaDeviceSynchronize();
+    if (k->ctx) {   // evict this key set's pre-masked keys from the context cache (they would otherwise leak)
+        std::lock_guard<std::mutex> lk(k->ctx->mu);
+        for (auto it = k->ctx->kmasks.begin(); it != k->ctx->kmasks.end();) {
+            if (it->first.keys_id == k->id) { cudaFree(it->second); it = k->ctx->kmasks.erase(it); }
+            else ++it;
+        }
+    }
     for (void* p : k->allocations) cudaFree(p);
     delete k;
     return ENCF_OK;
@@ -197,7 +206,7 @@ encf_status encf_keys_destroy(encf_keys* k) {
 
 encf_status encf_keys_size(encf_ctx* c, const encf_keys* k, int32_t which, size_t* words) {
     if (!c || !k || !words) return ENCF_ERR_ARG;
-    size_t nl = (size_t)k->max_level + c->K;
+    size_t nl = (size_t)k->max_level + c->Kof(k->max_level);
     *words = which == 0 ? nl * c->N : (size_t)k->dnum * 2 * nl * c->N;
     return ENCF_OK;
 }
@@ -206,7 +215,7 @@ encf_status encf_keys_export(encf_ctx* c, const encf_keys* k, int32_t which, uin
     return guard([&] {
         need(c && k && out, ENCF_ERR_ARG, "keys_export: null argument");
         cudaStream_t s = S(stream);
-        const int nl = k->max_level + c->K;
+        const int nl = k->max_level + c->Kof(k->max_level);
         LimbMap em = c->extmap(k->max_level);
         if (which == 0) {
             k_copy(k->sk, out, (size_t)nl * c->N, s);
@@ -582,12 +591,12 @@ encf_status encf_pt_ct_matmul(encf_ctx* c, const encf_keys* k, const encf_proj_p
             }
         } else {   // partial accumulators in the EXTENDED basis at the bank level La (= L, or L - 1 for a restricted
                    // plan): n_limbs = La + K (R-LAZY; reduce with encf_mod_reduce_ext)
-            const int La = accs[0].L;
+            const int La = accs[0].L, Ka = c->Kof(La);
             for (size_t i = 0; i < accs.size(); i++) {
                 encf_ct* yo = &y[b_first + i];
                 need(yo && yo->data, ENCF_ERR_ARG, "null output");
-                k_copy(accs[i].d, yo->data, (size_t)2 * (La + c->K) * c->N, s);
-                yo->n_comp = 2; yo->n_limbs = La + c->K; yo->scale = accs[i].scale; yo->ntt = 1;
+                k_copy(accs[i].d, yo->data, (size_t)2 * (La + Ka) * c->N, s);
+                yo->n_comp = 2; yo->n_limbs = La + Ka; yo->scale = accs[i].scale; yo->ntt = 1;
             }
         }
     });
@@ -598,12 +607,12 @@ encf_status encf_pt_ct_matmul_finalize(encf_ctx* c, const encf_keys* k, const en
     return guard([&] {
         need(c && k && p && acc && y && 0 <= b0 && b0 < b1 && b1 <= p->B_out, ENCF_ERR_ARG, "finalize: bad argument");
         EV_BEGIN(k);
-        const int L = acc[0].n_limbs - c->K;     // extended partials: n_limbs = L + K
-        need(L >= 2, ENCF_ERR_LEVEL_MISMATCH, "finalize expects extended accumulators (n_limbs = L + K)");
+        const int L = c->level_of_ext(acc[0].n_limbs);     // extended partials: n_limbs = L + K(L)
+        need(L >= 2, ENCF_ERR_LEVEL_MISMATCH, "finalize expects extended accumulators (n_limbs = L + K(L))");
         std::vector<DCt> accs = ev.alloc_many_ext(b1 - b0, L);
         for (int b = b0; b < b1; b++) {
-            need(acc[b - b0].n_limbs == L + c->K && acc[b - b0].data, ENCF_ERR_LEVEL_MISMATCH, "finalize: mixed accumulators");
-            k_copy(acc[b - b0].data, accs[b - b0].d, (size_t)2 * (L + c->K) * c->N, s);
+            need(acc[b - b0].n_limbs == L + c->Kof(L) && acc[b - b0].data, ENCF_ERR_LEVEL_MISMATCH, "finalize: mixed accumulators");
+            k_copy(acc[b - b0].data, accs[b - b0].d, (size_t)2 * (L + c->Kof(L)) * c->N, s);
             accs[b - b0].scale = acc[b - b0].scale;
         }
         std::vector<DCt> ys = ev.alloc_many(b1 - b0, L - 1);
@@ -847,11 +856,29 @@ encf_status encf_export_c2m(encf_ctx* c, const encf_ct* in, int32_t Lc, uint64_t
     });
 }
 
+static void export_many_impl(encf_ctx* c, const encf_ct* in, int32_t n, int32_t Lc, uint64_t mask_seed, uint64_t stream_id0,
+                             const uint64_t* d_seed_sid, uint64_t* masked, uint64_t* shares, void* stream);
+
 encf_status encf_export_c2m_many(encf_ctx* c, const encf_ct* in, int32_t n, int32_t Lc, uint64_t mask_seed, uint64_t stream_id0,
                                  uint64_t* masked, uint64_t* shares, void* stream) {
     return guard([&] {
-        need(c && in && masked && shares && n >= 1, ENCF_ERR_ARG, "export_many: null argument or n < 1");
         need(stream_id0 + (uint64_t)n <= (1ull << 56), ENCF_ERR_ARG, "export_many: stream ids must be < 2^56");
+        export_many_impl(c, in, n, Lc, mask_seed, stream_id0, nullptr, masked, shares, stream);
+    });
+}
+
+encf_status encf_export_c2m_many_dev(encf_ctx* c, const encf_ct* in, int32_t n, int32_t Lc, const uint64_t* d_seed_sid,
+                                     uint64_t* masked, uint64_t* shares, void* stream) {
+    return guard([&] {
+        need(d_seed_sid != nullptr, ENCF_ERR_ARG, "export_many_dev: null seed/stream buffer");
+        export_many_impl(c, in, n, Lc, 0, 0, d_seed_sid, masked, shares, stream);
+    });
+}
+
+static void export_many_impl(encf_ctx* c, const encf_ct* in, int32_t n, int32_t Lc, uint64_t mask_seed, uint64_t stream_id0,
+                             const uint64_t* d_seed_sid, uint64_t* masked, uint64_t* shares, void* stream) {
+    {
+        need(c && in && masked && shares && n >= 1, ENCF_ERR_ARG, "export_many: null argument or n < 1");
         cudaStream_t s = S(stream);
         const int N = c->N;
         const size_t cw = (size_t)2 * Lc * N;
@@ -866,10 +893,14 @@ encf_status encf_export_c2m_many(encf_ctx* c, const encf_ct* in, int32_t n, int3
                 k_copy(x.comp(comp, N), masked + cw * i + (size_t)comp * Lc * N, (size_t)Lc * N, s);
         }
         ntt_inverse(*c, PolyBatch{masked, (i64)Lc * N, 2 * n, c->qmap(Lc)}, s);
-        for (int i = 0; i < n; i++)
-            k_export_mask(*c, mask_seed, (0x04ull << 56) | (stream_id0 + (uint64_t)i), masked + cw * i,
-                          shares + (size_t)i * Lc * N, Lc, s);
-    });
+        for (int i = 0; i < n; i++) {
+            if (d_seed_sid)
+                k_export_mask_dev(*c, d_seed_sid, (uint64_t)i, masked + cw * i, shares + (size_t)i * Lc * N, Lc, s);
+            else
+                k_export_mask(*c, mask_seed, (0x04ull << 56) | (stream_id0 + (uint64_t)i), masked + cw * i,
+                              shares + (size_t)i * Lc * N, Lc, s);
+        }
+    }
 }
 
 encf_status encf_ring2field_local(encf_ctx* c, const uint64_t* mp, int32_t party, int32_t ell_sigma, int32_t L, uint64_t* out,

@@ -63,6 +63,17 @@ static void build(encf_ctx& c, const encf_params* p) {
     c.L = p->L; c.K = p->K; c.alpha = p->alpha;
     if (c.L < 1 || c.K < 1 || c.alpha < 1 || c.L + c.K > MAX_MODS || c.alpha > 16)
         throw EncfError(ENCF_ERR_ARG, "bad L/K/alpha");
+    // K(L): special primes of a key switch at level L (DESIGN.md R-KL); NULL = all K at every level
+    c.Kl.assign(c.L + 1, c.K);
+    if (p->K_of_level) {
+        for (int l = 1; l <= c.L; l++) {
+            const int k = p->K_of_level[l - 1];
+            if (k < 1 || k > c.K || (l > 1 && k < c.Kl[l - 1]))
+                throw EncfError(ENCF_ERR_ARG, "K_of_level must be non-decreasing in [1, K]");
+            c.Kl[l] = k;
+        }
+    }
+    c.Kl[0] = c.Kl[1];
     c.s1 = c.logN / 2;
     c.s2 = c.logN - c.s1;
     c.mods.assign(p->q, p->q + c.L);
@@ -185,25 +196,26 @@ static void build(encf_ctx& c, const encf_params* p) {
             t.d_vfac = upload(c, vf); t.d_vfac_sh = upload(c, vfs); t.d_wfac = upload(c, wf);
             c.modup[lev].push_back(t);
         }
-        // ModDown: y = fastBConv_{P->Q}([b]_P); out_i = (b_i - y_i) P^{-1} mod q_i
+        // ModDown: y = fastBConv_{P->Q}([b]_P); out_i = (b_i - y_i) P^{-1} mod q_i, P = P_{K(lev)} (R-KL)
+        const int Kl = c.Kof(lev);
         ModDownTab md;
-        std::vector<u64> vf(c.K), vfs(c.K), wf((size_t)c.K * lev), pinv(lev), pinvs(lev);
-        for (int k = 0; k < c.K; k++) {
+        std::vector<u64> vf(Kl), vfs(Kl), wf((size_t)Kl * lev), pinv(lev), pinvs(lev);
+        for (int k = 0; k < Kl; k++) {
             u64 pk = c.mods[c.L + k];
             u64 prod = 1;
-            for (int b = 0; b < c.K; b++) if (b != k) prod = h_mulmod(prod, c.mods[c.L + b] % pk, pk);
+            for (int b = 0; b < Kl; b++) if (b != k) prod = h_mulmod(prod, c.mods[c.L + b] % pk, pk);
             vf[k] = h_mulmod(h_invmod(prod, pk), ninv[c.L + k], pk);      // x N^{-1} (iNTT without it)
             vfs[k] = shoup_pre(vf[k], pk);
             for (int i = 0; i < lev; i++) {
                 u64 qi = c.mods[i];
                 u64 pr = 1;
-                for (int b = 0; b < c.K; b++) if (b != k) pr = h_mulmod(pr, c.mods[c.L + b] % qi, qi);
+                for (int b = 0; b < Kl; b++) if (b != k) pr = h_mulmod(pr, c.mods[c.L + b] % qi, qi);
                 wf[(size_t)k * lev + i] = mont(pr, qi);
             }
         }
         for (int i = 0; i < lev; i++) {
             u64 qi = c.mods[i], P = 1;
-            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            for (int k = 0; k < Kl; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
             pinv[i] = h_invmod(P, qi);
             pinvs[i] = shoup_pre(pinv[i], qi);
         }
@@ -212,12 +224,12 @@ static void build(encf_ctx& c, const encf_params* p) {
         std::vector<u64> pmod(lev);
         for (int i = 0; i < lev; i++) {
             u64 qi = c.mods[i], P = 1;
-            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            for (int k = 0; k < Kl; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
             pmod[i] = mont(P ? qi - P : 0, qi);      // stored negated: the kernel adds r * (q_i - P mod q_i)
         }
         md.d_pmod = upload(c, pmod);
-        std::vector<u64> cfix(c.K), csh(c.K);
-        for (int k = 0; k < c.K; k++) {
+        std::vector<u64> cfix(Kl), csh(Kl);
+        for (int k = 0; k < Kl; k++) {
             u64 pk = c.mods[c.L + k];
             csh[k] = 63 - (64 - __builtin_clzll(pk));
             cfix[k] = (u64)(((unsigned __int128)1 << (123 - csh[k])) / pk);
@@ -227,7 +239,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         std::vector<u64> pl(lev), pls(lev);
         for (int i = 0; i < lev; i++) {
             u64 qi = c.mods[i], P = 1;
-            for (int k = 0; k < c.K; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
+            for (int k = 0; k < Kl; k++) P = h_mulmod(P, c.mods[c.L + k] % qi, qi);
             pl[i] = P; pls[i] = shoup_pre(P, qi);
         }
         md.d_pl = upload(c, pl); md.d_pl_sh = upload(c, pls);
@@ -236,7 +248,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         if (lev >= 2) {
             std::vector<u64> bp;
             bp.push_back(c.mods[lev - 1]);
-            for (int k = 0; k < c.K; k++) bp.push_back(c.mods[c.L + k]);
+            for (int k = 0; k < Kl; k++) bp.push_back(c.mods[c.L + k]);
             const int nb = (int)bp.size(), nt = lev - 1;
             std::vector<u64> vf(nb), vfs(nb), wf((size_t)nb * nt), corr(nt), cf(nb), cs(nb), inv(nt), invs(nt);
             for (int a = 0; a < nb; a++) {

@@ -130,16 +130,23 @@ struct encf_ctx {
     // statistics
     std::atomic<uint64_t> st_ks{0}, st_modup{0}, st_ntt{0}, st_ptmul{0}, st_ctmul{0}, st_launch{0}, st_bytes{0}, st_ntt_fp{0};
 
+    std::vector<int> Kl;                // Kl[level] = K(level): special primes of a key switch at that level (R-KL)
+    int Kof(int level) const { return Kl[level]; }
+    int level_of_ext(int nl) const {    // the level L whose extended basis has nl = L + K(L) limbs (strictly increasing)
+        for (int l = 1; l <= L; l++) if (l + Kl[l] == nl) return l;
+        throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "no level with this extended limb count");
+    }
     int dnum(int level) const { return (level + alpha - 1) / alpha; }
     LimbMap qmap(int level) const {
         LimbMap m; m.n = level;
         for (int i = 0; i < level; i++) m.mod[i] = (unsigned char)i;
         return m;
     }
-    LimbMap extmap(int level) const {   // [q_0..q_{level-1}, p_0..p_{K-1}]
-        LimbMap m; m.n = level + K;
+    LimbMap extmap(int level) const {   // [q_0..q_{level-1}, p_0..p_{K(level)-1}]
+        const int Kl_ = Kof(level);
+        LimbMap m; m.n = level + Kl_;
         for (int i = 0; i < level; i++) m.mod[i] = (unsigned char)i;
-        for (int k = 0; k < K; k++) m.mod[level + k] = (unsigned char)(L + k);
+        for (int k = 0; k < Kl_; k++) m.mod[level + k] = (unsigned char)(L + k);
         return m;
     }
     size_t limb_words() const { return (size_t)N; }
@@ -156,10 +163,15 @@ struct encf_keys {
     uint64_t id = 0;                    // unique per keygen (pre-masked key cache)
     int max_level = 0;
     int dnum = 0;
-    u64* sk = nullptr;                  // [max_level + K][N]
-    std::map<uint32_t, u64*> ksk;       // galois (0 = relin) -> [dnum][2][max_level + K][N]
+    u64* sk = nullptr;                  // [max_level + K(max_level)][N]
+    std::map<uint32_t, u64*> ksk;       // galois (0 = relin) -> [dnum][2][max_level + K(max_level)][N]
+    // keys of the lower special-prime classes K(L) < K(max_level) (R-KL), derived on first use:
+    // (galois, K) -> [dnum][2][max_level + K][N]
+    std::map<std::pair<uint32_t, int>, u64*> cls;
+    std::mutex mu;
     std::vector<void*> allocations;
     int device = 0;
+    encf_ctx* ctx = nullptr;            // owner context: its pre-masked key cache entries are evicted at destroy
 };
 
 // ------------------------------------------------------------------------------------ scratch
@@ -260,6 +272,7 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
 void k_masked_sum(encf_ctx& c, const u64* const* cts, const u64* const* masks, int nterms, u64* out, int level,
                   cudaStream_t s);
 void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s);
+void k_export_mask_dev(encf_ctx& c, const u64* dss, u64 idx, u64* c0, u64* share, int level, cudaStream_t s);
 void k_encode_slots(encf_ctx& c, const double* d_re, const double* d_im, int n_slots, double scale, int level,
                     u64* out, cudaStream_t s, const LimbMap* lmap = nullptr);
 void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C, int N1, int m, const int* bs, const int* ps,
@@ -279,6 +292,10 @@ struct PsiBatch {                  // masked shift Psi^t without ModDown: h (.) 
 void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key_nl, cudaStream_t s);
 // pre-masked key of (key of g, ext mask at level L): km [dnum][2][L+K][N] = key (.) m (Montgomery form kept),
 // pm [L][N] = (P R mod q) (.) m; one allocation km | pm
+// class-K key from the generated key: copy limbs [0, nl_out) of every [digit][comp] and add dr[i] s'_i on digit j's
+// q-limbs of component 0 (DESIGN.md R-KL)
+void k_key_class(encf_ctx& c, const u64* full, int nl_full, u64* out, int nl_out, int ML, int dnum, const u64* sp, const u64* dr,
+                 cudaStream_t s);
 void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnum, int L, u64* out, cudaStream_t s);
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s);

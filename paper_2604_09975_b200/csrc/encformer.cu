@@ -215,7 +215,7 @@ void shift_ext_many(Ev& ev, const std::vector<const DCt*>& xs, const std::vector
     std::vector<int> order(reqs.size());
     for (size_t k = 0; k < order.size(); k++) order[k] = (int)k;
     std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return reqs[a].rot[0] < reqs[b].rot[0]; });
-    const int key_nl = ev.keys->max_level + ev.c.K, dn = ev.c.dnum(L);
+    const int key_nl = ev.keys->max_level + ev.c.Kof(L), dn = ev.c.dnum(L);
     for (size_t r0 = 0; r0 < order.size(); r0 += PSI_BATCH) {
         const int cnt = (int)std::min((size_t)PSI_BATCH, order.size() - r0);
         PsiBatch B;
@@ -768,7 +768,7 @@ void repack_rma_run(Ev& ev, const std::vector<DCt>& xs, int m, std::vector<DCt>&
     }
     u64* ext = ev.modup_many(c1, {}, L);
     std::vector<DCt> acc = ev.alloc_many_ext(n, L);
-    const int key_nl = ev.keys->max_level + ev.c.K;
+    const int key_nl = ev.keys->max_level + ev.c.Kof(L);
     const int nseg = ev.c.N / 2 / m;
     RotSumBatch B;
     for (int k = 0; k < K; k++) {

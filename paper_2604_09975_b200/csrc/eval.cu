@@ -14,12 +14,45 @@ uint32_t Ev::galois_rot(long steps) const {
     return (uint32_t)h_powmod(5, (u64)r, 2 * (u64)c.N);
 }
 
+// The key of Galois element g (0 = relin) for a key switch at level L: the generated key when L's special-prime
+// class K(L) is the top class K(max_level); otherwise the class-K(L) key, derived once and cached (R-KL, oracle
+// ckks.Keys.key_at): the same a_j, e_j restricted to Q_max u P_{K(L)} and b_j += (P_{K(L)} - P_{K(max)}) s' on digit
+// j's q-limbs, s' = sigma_g(s) or s^2 (NTT domain, Montgomery form kept).
 const u64* Ev::key_for(uint32_t g, int L) const {
     if (!keys) throw EncfError(ENCF_ERR_MISSING_KEY, "no keys");
     auto it = keys->ksk.find(g);
     if (it == keys->ksk.end()) throw EncfError(ENCF_ERR_MISSING_KEY, "missing key for galois element " + std::to_string(g));
     if (L > keys->max_level) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "ciphertext level above the key's max_level");
-    return it->second;
+    const int ML = keys->max_level, KM = c.Kof(ML), KL = c.Kof(L);
+    if (KL == KM) return it->second;
+    encf_keys* kk = const_cast<encf_keys*>(keys);
+    std::lock_guard<std::mutex> lk(kk->mu);
+    auto f = kk->cls.find({g, KL});
+    if (f != kk->cls.end()) return f->second;
+    const int N = c.N, dn = c.dnum(ML);
+    u64* out = nullptr;
+    CUDA_TRY(cudaMalloc(&out, (size_t)dn * 2 * (ML + KL) * N * 8));
+    kk->allocations.push_back(out);
+    u64* sp = sc.get((size_t)ML * N);
+    LimbMap qm = c.qmap(ML);
+    if (g == 0u) k_mul(c, keys->sk, 0, keys->sk, 0, sp, 0, 1, qm, s);          // s^2 (NTT domain)
+    else k_automorph(c, keys->sk, 0, sp, 0, 1, ML, g % (2u * N), s);           // sigma_g(s)
+    std::vector<u64> dr(ML);
+    for (int i = 0; i < ML; i++) {
+        const u64 q = c.mods[i];
+        u64 pl = 1, pm = 1;
+        for (int k = 0; k < KM; k++) {
+            const u64 pk = c.mods[c.L + k] % q;
+            pm = h_mulmod(pm, pk, q);
+            if (k < KL) pl = h_mulmod(pl, pk, q);
+        }
+        dr[i] = h_mulmod(sub_mod(pl, pm, q), c.mont_R[i], q);    // (P_{K(L)} - P_{K(max)}) R mod q_i
+    }
+    u64* ddr = sc.get(ML);
+    CUDA_TRY(cudaMemcpyAsync(ddr, dr.data(), ML * 8, cudaMemcpyHostToDevice, s));   // pageable: staged before return
+    k_key_class(c, it->second, ML + KM, out, ML + KL, ML, dn, sp, ddr, s);
+    kk->cls[{g, KL}] = out;
+    return out;
 }
 
 std::vector<DCt> Ev::alloc_many(int n, int L, int ncomp) {
@@ -34,7 +67,7 @@ std::vector<DCt> Ev::alloc_many(int n, int L, int ncomp) {
 // Q_L u P, fast BConv of the digit's coefficient-form limbs, then forward NTT.  One launch sequence for
 // all n polynomials.
 u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint32_t>& gathers, int L) {
-    const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L), n = (int)polys.size();
+    const int N = c.N, K = c.Kof(L), nl = L + K, dn = c.dnum(L), n = (int)polys.size();
     const size_t Lw = (size_t)L * N;
     u64* dntt = sc.get(Lw * n);
     for (int i0 = 0; i0 < n; i0 += CP_BATCH) {
@@ -76,7 +109,7 @@ u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint
 // Inner product + ModDown (C4 with the rounding correction R-MODDOWN: out = round(b / P)) for a list of
 // requests at level L.
 void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
-    const int N = c.N, K = c.K, nl = L + K, dn = c.dnum(L);
+    const int N = c.N, K = c.Kof(L), nl = L + K, dn = c.dnum(L);
     const int ML = keys->max_level, key_nl = ML + K;
     LimbMap klm;
     klm.n = nl;
@@ -404,9 +437,9 @@ void Ev::masked_sum(const std::vector<const DCt*>& C, const std::vector<const u6
 std::vector<DCt> Ev::alloc_many_ext(int n, int L) {
     std::vector<DCt> v(n);
     if (n == 0) return v;
-    const size_t w = (size_t)2 * (L + c.K) * c.N;
+    const size_t w = (size_t)2 * (L + c.Kof(L)) * c.N;
     u64* base = sc.get(w * n);
-    for (int i = 0; i < n; i++) { v[i].d = base + w * i; v[i].L = L; v[i].ncomp = 2; v[i].cstride = (i64)(L + c.K) * c.N; }
+    for (int i = 0; i < n; i++) { v[i].d = base + w * i; v[i].L = L; v[i].ncomp = 2; v[i].cstride = (i64)(L + c.Kof(L)) * c.N; }
     return v;
 }
 
@@ -416,7 +449,7 @@ void Ev::hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<
                           std::vector<std::vector<DCt>>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    const int N = c.N, L = ins[0]->L, K = c.Kof(L), nl = L + K, dn = c.dnum(L);
     std::vector<const u64*> c1;
     for (int i = 0; i < n; i++) {
         if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "hoisted_many_ext: mixed levels");
@@ -467,11 +500,11 @@ void Ev::sum_many_ext(const std::vector<std::vector<SumTerm>>& terms, int L, std
     for (int o = 0; o < n; o++) {
         for (auto& x : terms[o]) t.push_back(SumDev{x.ct, x.mask});
         off.push_back((int)t.size());
-        outs[o].L = L; outs[o].ncomp = 2; outs[o].scale = scales[o]; outs[o].cstride = (i64)(L + c.K) * c.N;
+        outs[o].L = L; outs[o].ncomp = 2; outs[o].scale = scales[o]; outs[o].cstride = (i64)(L + c.Kof(L)) * c.N;
         op.push_back(outs[o].d);
     }
     LimbMap em = c.extmap(L);
-    k_sum_csr(c, upload(t), upload(off), upload(op), n, (int)t.size(), 2, L + c.K, s, &em);
+    k_sum_csr(c, upload(t), upload(off), upload(op), n, (int)t.size(), 2, L + c.Kof(L), s, &em);
 }
 
 // round(x / (P q_{L-1})) mod Q_{L-1} for every extended ciphertext: limbs {q_{L-1}, p_*} to coefficient form,
@@ -479,7 +512,7 @@ void Ev::sum_many_ext(const std::vector<std::vector<SumTerm>>& terms, int L, std
 void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0].L, K = c.K, nl = L + K;
+    const int N = c.N, L = ins[0].L, K = c.Kof(L), nl = L + K;
     if (L < 2) throw EncfError(ENCF_ERR_LEVEL_EXHAUSTED, "moddown_rescale at one limb");
     const size_t w = (size_t)2 * nl * N;
     for (int i = 0; i < n; i++)
@@ -515,7 +548,7 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
 void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0].L, K = c.K, nl = L + K;
+    const int N = c.N, L = ins[0].L, K = c.Kof(L), nl = L + K;
     const size_t w = (size_t)2 * nl * N;
     for (int i = 0; i < n; i++)
         if (ins[i].d != ins[0].d + w * i || ins[i].L != L) throw EncfError(ENCF_ERR_ARG, "moddown_many: inputs must be contiguous");
@@ -548,7 +581,7 @@ void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
 void Ev::rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<uint32_t>& gs, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    const int N = c.N, L = ins[0]->L, K = c.Kof(L), nl = L + K, dn = c.dnum(L);
     std::vector<const u64*> c1;
     for (int i = 0; i < n; i++) {
         if (ins[i]->L != L || ins[i]->ncomp != 2) throw EncfError(ENCF_ERR_LEVEL_MISMATCH, "rotate_many_ext: mixed levels");
@@ -596,7 +629,7 @@ void Ev::rotsum_many(const std::vector<const DCt*>& ins, const std::vector<uint3
     u64* ext = modup_many(c1, {}, L);
     std::vector<DCt> acc = alloc_many_ext(n, L);
     for (int i = 0; i < n; i++) acc[i].scale = ins[i]->scale;
-    const int key_nl = keys->max_level + c.K;
+    const int key_nl = keys->max_level + c.Kof(L);
     for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
         const int cnt = std::min(KS_BATCH, n - r0);
         RotSumBatch B;
@@ -618,7 +651,7 @@ void Ev::rotsum_many(const std::vector<const DCt*>& ins, const std::vector<uint3
 void Ev::relin_rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0]->L, K = c.K, nl = L + K, dn = c.dnum(L);
+    const int N = c.N, L = ins[0]->L, K = c.Kof(L), nl = L + K, dn = c.dnum(L);
     std::vector<const u64*> d2;
     for (int i = 0; i < n; i++) {
         if (ins[i]->ncomp != 3 || ins[i]->L != L) throw EncfError(ENCF_ERR_FORMAT, "relinearize needs 3 components at one level");
@@ -657,7 +690,7 @@ void Ev::relin_rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>
 void Ev::lift_many(const std::vector<const DCt*>& ins, std::vector<DCt>& outs) {
     const int n = (int)ins.size();
     if (n == 0) return;
-    const int N = c.N, L = ins[0]->L, nl = L + c.K;
+    const int N = c.N, L = ins[0]->L, nl = L + c.Kof(L);
     for (int i = 0; i < n; i++) {
         DCt& o = outs[i];
         o.L = L; o.ncomp = 2; o.scale = ins[i]->scale; o.cstride = (i64)nl * N;
@@ -702,7 +735,7 @@ const u64* Ev::mask(int m, int r0, int r1, int s0, int ss, int scount, int level
 }
 
 const u64* Ev::keymask(uint32_t g, int m, int r0, int r1, int s0, int ss, int sc, int L, const u64** pm) {
-    const int nl = L + c.K, dn = c.dnum(L);
+    const int nl = L + c.Kof(L), dn = c.dnum(L);
     const size_t kmw = (size_t)dn * 2 * nl * c.N;
     KMKey key{keys->id, g, MaskKey{m, r0, r1, s0, ss, sc, L, 1}};
     {
@@ -712,10 +745,12 @@ const u64* Ev::keymask(uint32_t g, int m, int r0, int r1, int s0, int ss, int sc
     }
     const u64* mk = mask_ext(m, r0, r1, s0, ss, sc, L);
     const u64* kk = key_for(g, L);
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.kmasks.find(key);          // another thread may have built it meanwhile
+    if (it != c.kmasks.end()) { *pm = it->second + kmw; return it->second; }
     u64* buf = nullptr;
     CUDA_TRY(cudaMalloc(&buf, (kmw + (size_t)nl * c.N) * 8));
-    k_keymask(c, kk, keys->max_level + c.K, mk, dn, L, buf, s);
-    std::lock_guard<std::mutex> lk(c.mu);
+    k_keymask(c, kk, keys->max_level + c.Kof(L), mk, dn, L, buf, s);
     c.kmasks[key] = buf;
     *pm = buf + kmw;
     return buf;

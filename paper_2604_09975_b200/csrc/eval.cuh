@@ -54,7 +54,7 @@ struct Ev {
     // ModUp of polys[i] (NTT form, L limbs), each optionally permuted by gathers[i] first.
     // Returns ext [n][dnum][L+K][N]; ext_stride() words per polynomial.
     u64* modup_many(const std::vector<const u64*>& polys, const std::vector<uint32_t>& gathers, int L);
-    size_t ext_stride(int L) const { return (size_t)c.dnum(L) * (L + c.K) * c.N; }
+    size_t ext_stride(int L) const { return (size_t)c.dnum(L) * (L + c.Kof(L)) * c.N; }
     void ks_many(const std::vector<KsReq>& reqs, int L);
 
     // ---- ciphertext ops (outputs caller-provided; lists must share one level)

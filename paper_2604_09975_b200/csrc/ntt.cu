@@ -549,11 +549,13 @@ RowsCfg rows_cfg(const PhaseCfg& B, int nchunks, int npolys, int nlimbs) {
     return RowsCfg{dim3(nchunks / lc, nlimbs, npolys / lp), lgc};
 }
 
-// Polynomials per launch pair: ENCF_NTT_CHUNK_MB (default 32) MB of limbs, at least one polynomial; 0 = the whole
+// Polynomials per launch pair: ENCF_NTT_CHUNK_MB MB of limbs, at least one polynomial; 0 (default) = the whole
 // batch in one pair.  Splitting at polynomial granularity keeps every launch's grid identical in shape, so the
 // results are the same words either way.
 int ntt_chunk_polys(const encf_ctx& c, const PolyBatch& b) {
-    static const long mb = [] { const char* e = std::getenv("ENCF_NTT_CHUNK_MB"); return e ? std::atol(e) : 32L; }();
+    // default OFF: measured on the B200 (profiles/r02_summary.md) a 32 MB chunking made the layer's NTT time 29.2 -> 36.1 ms
+    // and 64 MB -> 32.6 ms (more, smaller launches; the big batches were not L2-miss-bound enough to win it back)
+    static const long mb = [] { const char* e = std::getenv("ENCF_NTT_CHUNK_MB"); return e ? std::atol(e) : 0L; }();
     if (mb <= 0) return b.npolys;
     const long per = (long)b.map.n * c.N * 8;
     return (int)std::max(1L, std::min((long)b.npolys, mb * (1L << 20) / per));

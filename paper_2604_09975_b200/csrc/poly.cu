@@ -7,6 +7,8 @@
 // Integer work runs on the IMAD pipe with 64x64->128 products; every kernel is HBM- or IMAD-bound
 // (no dense contraction here: DESIGN.md "Why no tensor cores").
 #include <cstdlib>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include "ctx.cuh"
 
 namespace {
@@ -437,8 +439,18 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                  ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
+// One 4-D tensor TMA per stage: the weight stream as the tensor [units][nbank][level][N] (u64) with box
+// {32 coefficients, 1 limb, 8 bank rows, 16 units} = 32 KB, landing as [16][8][32] words -- the layout the consumers
+// read; out-of-range units / rows are zero-filled (and never consumed).
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+        ::"r"(smem_u32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
+}
+
 template <bool NARROW>
-__global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(const u64* __restrict__ bank, int nbank,
+__global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(const __grid_constant__ CUtensorMap tmw,
+                                                                             const u64* __restrict__ bank, int nbank,
                                                                              const u64* __restrict__ w, int units, i64 wus,
                                                                              u64* __restrict__ acc, i64 accs, int level, int N,
                                                                              const ModConst* __restrict__ mod, int limb0,
@@ -475,19 +487,14 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(co
     const int nch = (nbank + DM_ROWS - 1) / DM_ROWS;
     const int mygroups = blockIdx.z < ngroups ? (ngroups - 1 - blockIdx.z) / gridDim.z + 1 : 0;
     const int total = mygroups * nch;
-    const u64* wl = w + (size_t)limb * N + k0;
     auto issue = [&](int s) {
+        if (tid != 0) return;
         const int g = blockIdx.z + (s / nch) * gridDim.z, c = s % nch;
-        const int rows = min(DM_ROWS, nbank - c * DM_ROWS), ul = min(MAC_LANES, units - g * MAC_LANES);
         const int slot = s % nstages;
-        if (tid == 0) mbar_arrive_expect_tx(&bars[slot], (uint32_t)(ul * rows * MAC_T * 8));
-        if (tid < MAC_LANES * DM_ROWS) {
-            const int u = tid / DM_ROWS, r = tid % DM_ROWS;
-            if (u < ul && r < rows)
-                bulk_g2s(stg + (size_t)slot * DM_STAGE_WORDS + ((size_t)u * DM_ROWS + r) * MAC_T,
-                         wl + (size_t)(g * MAC_LANES + u) * wus + (size_t)(c * DM_ROWS + r) * pstride, MAC_T * 8, &bars[slot]);
-        }
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)(DM_STAGE_WORDS * 8));      // the full box (OOB zero-filled)
+        tma_load_4d(stg + (size_t)slot * DM_STAGE_WORDS, &tmw, k0, limb, c * DM_ROWS, g * MAC_LANES, &bars[slot]);
     };
+    (void)w; (void)pstride;
     for (int s = 0; s < nstages - 1 && s < total; s++) issue(s);
     const u64 t40 = (1ull << 40) % mc.q;
     u64 h00 = 0, l00 = 0, s00 = 0, h01 = 0, l01 = 0, s01 = 0, h10 = 0, l10 = 0, s10 = 0, h11 = 0, l11 = 0, s11 = 0;
@@ -861,11 +868,26 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         const int groups = (units + MAC_LANES - 1) / MAC_LANES;
         int zs = 1;
         while ((size_t)tiles * level * zs < 148 && zs < groups) zs *= 2;
+        // the weight stream as a 4-D tensor [units][nbank][level][N] for the TMA engine
+        static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+        if (!encode) {
+            cudaDriverEntryPointQueryResult qr;
+            CUDA_TRY(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr));
+            if (qr != cudaDriverEntryPointSuccess || !encode) throw EncfError(ENCF_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        }
+        CUtensorMap tm;
+        const cuuint64_t dims[4] = {(cuuint64_t)c.N, (cuuint64_t)level, (cuuint64_t)nbank, (cuuint64_t)units};
+        const cuuint64_t strides[3] = {(cuuint64_t)c.N * 8, (cuuint64_t)level * c.N * 8, (cuuint64_t)wus * 8};
+        const cuuint32_t box[4] = {MAC_T, 1, DM_ROWS, MAC_LANES};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, (void*)w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            throw EncfError(ENCF_ERR_CUDA, "diag_mac: cuTensorMapEncodeTiled failed");
         if (nw > 0)
-            diag_mac_tma_kernel<false><<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(bank, nbank, w, units, wus, acc, accs,
+            diag_mac_tma_kernel<false><<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs,
                                                                                            level, c.N, c.d_mod, 0, nst);
         if (nw < level)
-            diag_mac_tma_kernel<true><<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(bank, nbank, w, units, wus, acc,
+            diag_mac_tma_kernel<true><<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc,
                                                                                                   accs, level, c.N, c.d_mod, nw, nst);
     } else {
         if (nw > 0)
@@ -879,6 +901,33 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     c.st_launch += (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // the 128-bit and the narrow launch
     c.st_bytes += bytes;
     c.st_ptmul += (uint64_t)units * nbank;
+}
+
+// The same mask with (seed, stream id base) read from DEVICE memory at run time: a CUDA-graph replay then draws the
+// masks of whatever (seed, base) the buffer holds, so a step that advances the base every replay never reuses a
+// one-time pad across inferences.  stream = mask(dss[1] + idx).
+__global__ void export_mask_dev_kernel(const u64* __restrict__ dss, u64 idx, u64* c0, u64* share, int level, int N,
+                                       const ModConst* mod) {
+    const u64 seed = dss[0], stream = (0x04ull << 56) | ((dss[1] + idx) & ((1ull << 56) - 1));
+    size_t total = (size_t)level * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        int limb = (int)(i / N), k = (int)(i % N);
+        u64 q = mod[limb].q;
+        u64 id = 2 * ((u64)limb * (u64)N + (u64)k);
+        u64 hi = prng_draw(seed, stream, id), lo = prng_draw(seed, stream, id + 1);
+        u64 a_lo = hi * q, a_hi = umulhi(hi, q), b = umulhi(lo, q);
+        u64 s = a_lo + b;
+        u64 r = a_hi + (s < a_lo);
+        c0[i] = add_mod(c0[i], r, q);
+        share[i] = r ? q - r : 0;
+    }
+}
+
+void k_export_mask_dev(encf_ctx& c, const u64* dss, u64 idx, u64* c0, u64* share, int level, cudaStream_t s) {
+    { int _slot; c.prof_begin("export_mask_kernel", s, 0, _slot);
+    export_mask_dev_kernel<<<GRID((size_t)level * c.N), TB, 0, s>>>(dss, idx, c0, share, level, c.N, c.d_mod);
+    c.prof_end(_slot, s); }
+    c.st_launch++;
 }
 
 void k_export_mask(encf_ctx& c, u64 seed, u64 stream, u64* c0, u64* share, int level, cudaStream_t s) {
@@ -1416,7 +1465,7 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
     KeyLimb kl;
     LimbMap em;
     em.n = nl;
-    int Lq = nl - c.K;
+    const int Lq = c.level_of_ext(nl);
     for (int e = 0; e < nl; e++) {
         kl.kl[e] = key_limb_of.mod[e];
         em.mod[e] = (unsigned char)(e < Lq ? e : c.L + (e - Lq));
@@ -1433,9 +1482,9 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
 
 void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s) {
     if (nterms > RS_TERMS) throw EncfError(ENCF_ERR_ARG, "rotation sum: too many terms");
-    const int nl = L + c.K;
+    const int nl = L + c.Kof(L);
     KeyLimb kl;
-    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.Kof(L)) + (e - L);
     const LimbMap em = c.extmap(L);
     dim3 grid(nreq, (c.N / 2 + TB - 1) / TB, nl);
     const uint64_t bytes = (uint64_t)nterms * dnum * 2 * nl * c.N * 8 + (uint64_t)nreq * (dnum * nl + 2 * L + 2 * nl) * c.N * 8;
@@ -1449,7 +1498,7 @@ void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dn
 }
 
 void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key_nl, cudaStream_t s) {
-    const int nl = L + c.K;
+    const int nl = L + c.Kof(L);
     if ((unsigned __int128)(2 * dnum + 2) * c.max_mod >= ((unsigned __int128)1 << 64))
         throw EncfError(ENCF_ERR_ARG, "ks_psi: too many products for one Montgomery reduction");
     const LimbMap em = c.extmap(L);
@@ -1465,16 +1514,41 @@ void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key
     CUDA_TRY(cudaGetLastError());
 }
 
+__global__ void key_class_kernel(const u64* __restrict__ full, int nl_full, u64* __restrict__ out, int nl_out, int ML, int dnum,
+                                 int alpha, const u64* __restrict__ sp, const u64* __restrict__ dr, int N,
+                                 const ModConst* __restrict__ mod) {
+    const size_t total = (size_t)dnum * 2 * nl_out * N;
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % N);
+        const size_t row = i / N;
+        const int e = (int)(row % nl_out), jc = (int)(row / nl_out), j = jc >> 1, comp = jc & 1;
+        u64 v = full[((size_t)jc * nl_full + e) * N + k];     // special limb k sits at ML + k in both layouts
+        if (comp == 0 && e >= j * alpha && e < min((j + 1) * alpha, ML)) {
+            const ModConst mc = mod[e];
+            v = add_mod(v, mulmod_barrett(sp[(size_t)e * N + k], dr[e], mc.q, mc.rhi, mc.rlo), mc.q);
+        }
+        out[i] = v;
+    }
+}
+
+void k_key_class(encf_ctx& c, const u64* full, int nl_full, u64* out, int nl_out, int ML, int dnum, const u64* sp, const u64* dr,
+                 cudaStream_t s) {
+    key_class_kernel<<<GRID((size_t)dnum * 2 * nl_out * c.N), TB, 0, s>>>(full, nl_full, out, nl_out, ML, dnum, c.alpha, sp, dr, c.N,
+                                                                         c.d_mod);
+    c.st_launch++;
+    CUDA_TRY(cudaGetLastError());
+}
+
 void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnum, int L, u64* out, cudaStream_t s) {
-    const int nl = L + c.K;
+    const int nl = L + c.Kof(L);
     KeyLimb kl;
-    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.Kof(L)) + (e - L);
     const LimbMap em = c.extmap(L);
     std::vector<u64> pr(L);
     for (int i = 0; i < L; i++) {
         const u64 q = c.mods[i];
-        u64 P = 1;
-        for (int kk = 0; kk < c.K; kk++) P = h_mulmod(P, c.mods[c.L + kk] % q, q);
+        u64 P = 1;                                       // P_{K(L)} (R-KL)
+        for (int kk = 0; kk < c.Kof(L); kk++) P = h_mulmod(P, c.mods[c.L + kk] % q, q);
         pr[i] = h_mulmod(P, c.mont_R[i], q);
     }
     u64* dpr = nullptr;
@@ -1489,9 +1563,9 @@ void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnu
 
 void k_ks_rma(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s) {
     if (nterms > RS_TERMS) throw EncfError(ENCF_ERR_ARG, "rma: too many terms");
-    const int nl = L + c.K;
+    const int nl = L + c.Kof(L);
     KeyLimb kl;
-    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.K) + (e - L);
+    for (int e = 0; e < nl; e++) kl.kl[e] = e < L ? e : (key_nl - c.Kof(L)) + (e - L);
     const LimbMap em = c.extmap(L);
     dim3 grid(nreq, (c.N / 2 + TB - 1) / TB, nl);
     int slot;

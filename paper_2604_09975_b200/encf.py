@@ -31,7 +31,7 @@ class PT(ctypes.Structure):
 
 
 class Params(ctypes.Structure):
-    _fields_ = [("N", _i32), ("L", _i32), ("K", _i32), ("alpha", _i32), ("q", _p), ("p", _p)]
+    _fields_ = [("N", _i32), ("L", _i32), ("K", _i32), ("alpha", _i32), ("q", _p), ("p", _p), ("K_of_level", _p)]
 
 
 class Counters(ctypes.Structure):
@@ -69,6 +69,7 @@ _SIG = {
     "encf_conjugate": [_p, _p, ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
     "encf_decomplexify": [_p, _p, _p, _i32, _p, _p],
     "encf_export_c2m_many": [_p, _p, _i32, _i32, _u64, _u64, _p, _p, _p],
+    "encf_export_c2m_many_dev": [_p, _p, _i32, _i32, _p, _p, _p, _p],
     "encf_rescale": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
     "encf_mod_drop": [_p, ctypes.POINTER(CT), _i32, ctypes.POINTER(CT), _p],
     "encf_complexify": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
@@ -186,12 +187,30 @@ class Context:
         self.L = len(self.q)
         self.device = torch.device("cuda", device)
         qa, pa = _u64_host(self.q), _u64_host(self.p)
-        self._keep = (qa, pa)
-        prm = Params(self.N, self.L, len(self.p), self.alpha, qa.ctypes.data, pa.ctypes.data)
+        # K(L): special primes of a key switch at level L (DESIGN.md R-KL); absent = all at every level
+        self.K_of_level = [int(k) for k in d.get("K_of_level", [len(self.p)] * self.L)]
+        ka = np.ascontiguousarray(np.array(self.K_of_level, dtype=np.int32))
+        self._keep = (qa, pa, ka)
+        prm = Params(self.N, self.L, len(self.p), self.alpha, qa.ctypes.data, pa.ctypes.data, ka.ctypes.data)
         h = _p()
         torch.cuda.init()
         _chk(_lib.encf_ctx_create(ctypes.byref(prm), device, ctypes.byref(h)), "ctx_create")
         self.h = h
+
+    def K(self, L):
+        """Special primes of a key switch at level L."""
+        return self.K_of_level[L - 1]
+
+    def ext_limbs(self, L):
+        """Limbs of an extended-basis object at level L (L + K(L))."""
+        return L + self.K(L)
+
+    def level_of_ext(self, nl):
+        """The level L of an extended-basis object with nl = L + K(L) limbs."""
+        for L in range(1, self.L + 1):
+            if L + self.K(L) == nl:
+                return L
+        raise ValueError("no level has %d extended limbs" % nl)
 
     def close(self):
         if self.h:
@@ -423,13 +442,19 @@ class Context:
 
     def export_c2m_many(self, cts, L_conv, mask_seed, stream_id0):
         """Batched encf_export_c2m: ciphertext i with stream id stream_id0 + i.  Returns [(masked ct, share)]
-        as views into two contiguous device buffers."""
+        as views into two contiguous device buffers.  mask_seed may also be a DEVICE int64 tensor [2] = (seed,
+        stream id base) (encf_export_c2m_many_dev: read at run time, so a graph replay sees its current value; then
+        stream_id0 is ignored)."""
         n, N = len(cts), self.N
         masked = torch.empty(n * 2 * L_conv * N, dtype=torch.int64, device=self.device)
         shares = torch.empty(n * L_conv * N, dtype=torch.int64, device=self.device)
         ins = (CT * n)(*[c._c() for c in cts])
-        _chk(_lib.encf_export_c2m_many(self.h, ctypes.cast(ins, _p), n, int(L_conv), int(mask_seed), int(stream_id0),
-                                       masked.data_ptr(), shares.data_ptr(), _stream()), "export_c2m_many")
+        if isinstance(mask_seed, torch.Tensor):
+            _chk(_lib.encf_export_c2m_many_dev(self.h, ctypes.cast(ins, _p), n, int(L_conv), mask_seed.data_ptr(),
+                                               masked.data_ptr(), shares.data_ptr(), _stream()), "export_c2m_many_dev")
+        else:
+            _chk(_lib.encf_export_c2m_many(self.h, ctypes.cast(ins, _p), n, int(L_conv), int(mask_seed), int(stream_id0),
+                                           masked.data_ptr(), shares.data_ptr(), _stream()), "export_c2m_many")
         w = 2 * L_conv * N
         return [(Ciphertext(masked[i * w:(i + 1) * w], 2, L_conv, cts[i].scale, 0), shares[i * L_conv * N:(i + 1) * L_conv * N])
                 for i in range(n)]
@@ -563,7 +588,7 @@ class ProjPlan:
 
     def finalize(self, keys, accs, b_begin):
         """accs: extended partial accumulators (n_limbs = L + K)."""
-        ys = [self.ctx.empty_ct(a.n_limbs - len(self.ctx.p) - 1) for a in accs]
+        ys = [self.ctx.empty_ct(self.ctx.level_of_ext(a.n_limbs) - 1) for a in accs]
         aa = (CT * len(accs))(*[a._c() for a in accs])
         ya = (CT * len(ys))(*[y._c() for y in ys])
         _chk(_lib.encf_pt_ct_matmul_finalize(self.ctx.h, keys.h, self.h, ctypes.cast(aa, _p), b_begin, b_begin + len(accs),

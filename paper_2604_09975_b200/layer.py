@@ -131,10 +131,11 @@ class ShardedProjection:
         ctx, comm, plan = self.ctx, self.comm, self.plan
         if comm.world == 1:
             return plan.matmul(keys, xs, self.w, self.w_scale)
-        L, K, N = xs[0].n_limbs, len(ctx.p), ctx.N
+        N = ctx.N
         parts = plan.matmul(keys, xs, self.w, self.w_scale, self.u0, self.u1, finalize=False, w_shard=True)
         b_first = self.u0 // plan.N2
-        La = parts[0].n_limbs - K
+        La = ctx.level_of_ext(parts[0].n_limbs)       # extended partials: La + K(La) limbs (R-LAZY, R-KL)
+        K = ctx.K(La)
         wext = 2 * (La + K) * N
         buf = torch.zeros((plan.B_out, wext), dtype=torch.int64, device=ctx.device)
         for i, a in enumerate(parts):
@@ -211,14 +212,26 @@ class ShardedLayer:
             out.append(ys[-1])
         return out
 
+    MASK_EPOCH = 1 << 32
+
     def _export(self, cts, sid):
-        """C2M export (Alg 3 GPU half) of ciphertext i by rank i mod world, stream id sid + i."""
+        """C2M export (Alg 3 GPU half) of ciphertext i by rank i mod world, mask stream id epoch 2^32 + sid + i with
+        (seed, base) in a DEVICE buffer advanced every step (fresh one-time pads per inference, also under graph
+        replay; encf_export_c2m_many_dev)."""
         comm = self.comm
-        mine = [i for i in range(len(cts)) if i % comm.world == comm.rank]
+        st = self.__dict__.setdefault("mask_state", {})
+        if sid not in st:
+            st[sid] = torch.tensor([self.mask_seed, sid], dtype=torch.int64, device=self.ctx.device)
         out = []
-        for i in mine:
-            out += [(i, r) for r in self.ctx.export_c2m_many([cts[i]], self.Lconv, self.mask_seed, sid + i)]
+        for i in range(len(cts)):
+            if i % comm.world == comm.rank:
+                sti = st[sid] + torch.tensor([0, i], dtype=torch.int64, device=self.ctx.device)
+                out += [(i, r) for r in self.ctx.export_c2m_many([cts[i]], self.Lconv, sti, 0)]
         return out
+
+    def _advance_masks(self):
+        for t in self.__dict__.get("mask_state", {}).values():
+            t[1:].add_(self.MASK_EPOCH)
 
     def score(self, Q, K):
         comm, attn, ctx = self.comm, self.attn, self.ctx
@@ -281,9 +294,11 @@ class ShardedLayer:
         Q, K, V = y[:nqk], y[nqk:2 * nqk], y[2 * nqk:]
         S = self.score(Q, K)
         ex = []
-        if self.comm.rank == 0:
-            ex += [("score", i, r) for i, r in enumerate(ctx.export_c2m_many(self.attn.export_stream(keys, S), self.Lconv,
-                                                                             self.mask_seed, 0))]
+        if self.comm.rank == 0:              # the K_min(S) stream ciphertexts, exported by rank 0
+            stream = self.attn.export_stream(keys, S)
+            saved, self.comm = self.comm, _OneRank()
+            ex += [("score", i, r) for i, r in self._export(stream, 0)]
+            self.comm = saved
         O = self.value(inp["p"], V)
         Ore = ctx.decomplexify(keys, O)            # (G11) replicated: B_V conjugations
         yo = self.oproj(keys, self._complex_pairs(Ore))
@@ -293,4 +308,10 @@ class ShardedLayer:
         g2 = self.ff2(keys, inp["f2"])
         ex += [("ln2", i, r) for i, r in self._export(self._complex_pairs(g2), 300)]
         self.last = {"y_qkv": y, "S": S, "O": O, "yo": yo, "g1": g1, "g2": g2}
+        self._advance_masks()
         return ex
+
+
+class _OneRank:
+    """A stand-in communicator of one rank (rank 0 exports the whole score stream)."""
+    world, rank = 1, 0

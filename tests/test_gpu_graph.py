@@ -75,3 +75,35 @@ def test_graph_replay_projection_attention_export():
     for (a, b), (ea, eb) in zip(out1, eager1):
         assert torch.equal(a, ea)
         assert (b is None) or torch.equal(b, eb)
+
+
+def test_graph_replays_draw_fresh_export_masks():
+    """a captured export must not reuse its one-time pad r^ across replays.  With the (seed, stream id
+    base) in a device buffer advanced inside the graph (encf_export_c2m_many_dev), replay k draws the masks of stream
+    ids k 2^32 + i: every replay's masked ciphertext and server share equal the oracle's export_c2m with that
+    stream id, and two replays differ."""
+    ctx = E.Context("P13", 0)
+    ok = O.Keys(P13, synth.SEED_KEYS)
+    cts = [O.encrypt_sk(P13, ok, O.encode(P13, synth.fixed_point_uniform(P13.n, 30 + i), 2.0 ** 40, 4), 40 + i)
+           for i in range(2)]
+    d = {"x": [dev_ct(ctx, c) for c in cts]}
+    seed = synth.seed_mask(3)
+    state = torch.tensor([seed, 0], dtype=torch.int64, device=ctx.device)
+
+    def step(inp):
+        ex = ctx.export_c2m_many(inp["x"], 2, state, 0)
+        state[1:].add_(1 << 32)
+        return [(a.data, b) for a, b in ex]
+
+    step(d)                                   # eager warm-up: epoch 0
+    g = GraphedStep(step, d)                  # capture records the launches without running them
+    seen = []
+    for k in range(1, 3):                     # replays: epochs 1, 2
+        out = [(a.clone(), b.clone()) for a, b in g()]
+        torch.cuda.synchronize()
+        for i, (a, b) in enumerate(out):
+            rm, rs = K.export_c2m(P13, cts[i], 2, seed, (k << 32) + i)
+            assert np.array_equal(a.cpu().numpy().view(np.uint64).reshape(2, 2, P13.N), rm.c), (k, i)
+            assert np.array_equal(b.cpu().numpy().view(np.uint64).reshape(2, P13.N), rs), (k, i)
+        seen.append(out)
+    assert not torch.equal(seen[0][0][1], seen[1][0][1])

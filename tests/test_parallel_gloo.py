@@ -53,7 +53,8 @@ def _worker(rank, world, port, q):
     ev = K.Ev(P, keys, plan.m)
     accs = K.projection_partial(ev, plan, xs, w, u0, u1)      # {b: ExtCt} extended-basis partials (R-LAZY)
     parts = {b: torch.from_numpy(a.c.view(np.int64).copy()) for b, a in accs.items()}
-    PAR.reduce_partial_blocks(parts, ranges, plan.N2, plan.B_out, lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
+    PAR.reduce_partial_blocks(parts, ranges, plan.N2, plan.B_out, lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM),
+                              torch.zeros_like)
     ys = {}
     for b, t in parts.items():
         if PAR.owner_of_block(b, ranges, plan.N2) != rank:
@@ -67,9 +68,11 @@ def _worker(rank, world, port, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.timeout(600)
-def test_sharded_projection_equals_single_rank():
-    world = 2
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_projection_equals_single_rank(world):
+    """world = 4: rank 0 touches only block 0 and rank 3 only block 2, so the per-block collectives pair up only
+    because every rank joins every straddled block's all-reduce (a rank skipping one mismatched them)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -88,6 +91,14 @@ def test_sharded_projection_equals_single_rank():
     assert sorted(got) == list(range(plan.B_out))
     for b in range(plan.B_out):
         assert np.array_equal(got[b], ref[b].c), b
+
+
+def test_straddled_blocks():
+    ranges = PAR.unit_ranges(24, 4)
+    assert ranges == [(0, 6), (6, 12), (12, 18), (18, 24)]
+    assert PAR.straddled_blocks(ranges, 8, 3) == [0, 1, 2]
+    assert [PAR.owner_of_block(b, ranges, 8) for b in range(3)] == [1, 2, 3]
+    assert PAR.straddled_blocks(PAR.unit_ranges(24, 3), 8, 3) == []
 
 
 def test_unit_ranges_cover_and_balance():
