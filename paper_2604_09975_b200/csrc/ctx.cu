@@ -23,6 +23,28 @@ static u64* upload(encf_ctx& c, const std::vector<u64>& v) {
     return d;
 }
 
+// Base-conversion matrix wf ([na][nt], Montgomery form, targets tq) as the byte matrix of the tensor-core path
+// (poly.cu bconv_tc_kernel): W'[i][a][t] = 2^{8a} wf[i][t] mod q_t, byte b of it at row n = 8 t + b, K byte kk = 8 i + a,
+// in the canonical K-major no-swizzle layout [kk / 16][n][kk % 16]; nb = 8 x (nt rounded up to even) rows, inputs
+// i >= na (and the padding target) are zero.  Returns null when the shape does not fit (na > 8 or nt > 32).
+static uint8_t* bconv_wbytes(encf_ctx& c, const std::vector<u64>& wf, int na, int nt, const std::vector<u64>& tq) {
+    if (na > 8 || nt > 32 || na < 1 || nt < 1) return nullptr;
+    const int nb = 8 * ((nt + 1) & ~1);
+    std::vector<uint8_t> wb((size_t)nb * 64, 0);
+    for (int i = 0; i < na; i++)
+        for (int a = 0; a < 8; a++)
+            for (int t = 0; t < nt; t++) {
+                const u64 wp = h_mulmod(wf[(size_t)i * nt + t], h_powmod(2, 8 * a, tq[t]), tq[t]);
+                for (int b = 0; b < 8; b++) {
+                    const int n = 8 * t + b, kk = 8 * i + a;
+                    wb[(size_t)(kk / 16) * nb * 16 + (size_t)n * 16 + kk % 16] = (uint8_t)(wp >> (8 * b));
+                }
+            }
+    uint8_t* d = (uint8_t*)c.dev_alloc(wb.size());
+    CUDA_TRY(cudaMemcpy(d, wb.data(), wb.size(), cudaMemcpyHostToDevice));
+    return d;
+}
+
 static int bitrev(int x, int bits) {
     int r = 0;
     for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
@@ -194,6 +216,11 @@ static void build(encf_ctx& c, const encf_params* p) {
                 }
             }
             t.d_vfac = upload(c, vf); t.d_vfac_sh = upload(c, vfs); t.d_wfac = upload(c, wf);
+            {
+                std::vector<u64> tq(t.tgt.n);
+                for (int k = 0; k < t.tgt.n; k++) tq[k] = c.mods[t.tgt.mod[k]];
+                t.d_wb = bconv_wbytes(c, wf, na, t.tgt.n, tq);
+            }
             c.modup[lev].push_back(t);
         }
         // ModDown: y = fastBConv_{P->Q}([b]_P); out_i = (b_i - y_i) P^{-1} mod q_i, P = P_{K(lev)} (R-KL)
@@ -220,6 +247,7 @@ static void build(encf_ctx& c, const encf_params* p) {
             pinvs[i] = shoup_pre(pinv[i], qi);
         }
         md.d_vfac = upload(c, vf); md.d_vfac_sh = upload(c, vfs); md.d_wfac = upload(c, wf);
+        md.d_wb = bconv_wbytes(c, wf, Kl, lev, std::vector<u64>(c.mods.begin(), c.mods.begin() + lev));
         md.d_pinv = upload(c, pinv); md.d_pinv_sh = upload(c, pinvs);
         std::vector<u64> pmod(lev);
         for (int i = 0; i < lev; i++) {
@@ -272,6 +300,7 @@ static void build(encf_ctx& c, const encf_params* p) {
             }
             MDRTab mt;
             mt.d_vfac = upload(c, vf); mt.d_vfac_sh = upload(c, vfs); mt.d_wfac = upload(c, wf); mt.d_corr = upload(c, corr);
+            mt.d_wb = bconv_wbytes(c, wf, nb, nt, std::vector<u64>(c.mods.begin(), c.mods.begin() + nt));
             mt.d_cfix = upload(c, cf); mt.d_csh = upload(c, cs); mt.d_inv = upload(c, inv); mt.d_inv_sh = upload(c, invs);
             c.mdr[lev] = mt;
         }

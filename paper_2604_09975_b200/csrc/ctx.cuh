@@ -47,6 +47,7 @@ struct ModUpTab {         // fast BConv of digit j at level L: digit limbs [lo,h
     u64* d_vfac;          // [alpha]      (Q_j/q_i)^{-1} mod q_i
     u64* d_vfac_sh;
     u64* d_wfac;          // [alpha][ntgt] (Q_j/q_i) mod t
+    uint8_t* d_wb = nullptr;    // d_wfac as the tensor-core byte matrix (bconv_wbytes), or null
 };
 
 struct ModDownTab {       // P -> Q_L
@@ -60,10 +61,12 @@ struct ModDownTab {       // P -> Q_L
     u64* d_csh;           // [K]   s_k = 63 - bitlen(p_k)
     u64* d_pl;            // [L]   P mod q_i and its Shoup quotient (extended-basis lift, R-LAZY)
     u64* d_pl_sh;
+    uint8_t* d_wb = nullptr;    // d_wfac as the tensor-core byte matrix
 };
 
 struct MDRTab {           // merged ModDown + rescale (R-LAZY): basis B' = {q_{L-1}, p_0..p_{K-1}} -> Q_{L-1}
     u64 *d_vfac, *d_vfac_sh, *d_wfac, *d_corr, *d_cfix, *d_csh, *d_inv, *d_inv_sh;
+    uint8_t* d_wb = nullptr;    // d_wfac as the tensor-core byte matrix
 };
 
 struct RescaleTab {       // drop q_{L-1}
@@ -303,7 +306,8 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
                             const ModDownTab& t, cudaStream_t s);
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s,
-                   const u64* corr = nullptr, const u64* cfix = nullptr, const u64* csh = nullptr);
+                   const u64* corr = nullptr, const u64* cfix = nullptr, const u64* csh = nullptr,
+                   const uint8_t* wb = nullptr);   // wb: byte matrix of wf for the tensor-core path (bconv_wbytes)
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s);
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s);
 void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,

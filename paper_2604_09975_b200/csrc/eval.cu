@@ -90,7 +90,7 @@ u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint
         im.n = t.hi - t.lo;
         for (int i = 0; i < im.n; i++) im.mod[i] = (unsigned char)(t.lo + i);
         k_bconv_batch(c, dco + (size_t)t.lo * N, (i64)Lw, im, t.d_vfac, t.d_vfac_sh, t.d_wfac, t.tgt, ej, (i64)es,
-                      t.tgt_pos.data(), n, s);
+                      t.tgt_pos.data(), n, s, nullptr, nullptr, nullptr, t.d_wb);
         if (t.lo > 0) {
             LimbMap m; m.n = t.lo;
             for (int i = 0; i < t.lo; i++) m.mod[i] = em.mod[i];
@@ -135,7 +135,7 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
         ntt_inverse_scaled(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // [b]_P (x N; vfac has N^{-1})
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
-                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh);                        // rounded: y = centred [b]_P
+                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh, md.d_wb);              // rounded: y = centred [b]_P
         std::vector<const u64*> esrc(2 * n), eadd(2 * n);
         std::vector<u64*> eout(2 * n);
         for (int i = 0; i < n; i++)
@@ -529,7 +529,7 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
     for (int i = 0; i < L - 1; i++) pos[i] = i;
     u64* y = sc.get((size_t)n * 2 * (L - 1) * N);
     k_bconv_batch(c, x + (size_t)(L - 1) * N, (i64)nl * N, bm, t.d_vfac, t.d_vfac_sh, t.d_wfac, qm, y, (i64)(L - 1) * N,
-                  pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh);
+                  pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh, t.d_wb);
     std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
     std::vector<u64*> eout(2 * n);
     for (int i = 0; i < n; i++) {
@@ -562,7 +562,7 @@ void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     ntt_inverse_scaled(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // vfac has N^{-1}
     u64* y = sc.get((size_t)n * 2 * L * N);
     k_bconv_batch(c, x + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N, pos.data(), 2 * n, s,
-                  md.d_pmod, md.d_cfix, md.d_csh);
+                  md.d_pmod, md.d_cfix, md.d_csh, md.d_wb);
     std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
     std::vector<u64*> eout(2 * n);
     for (int i = 0; i < n; i++) {

@@ -164,10 +164,16 @@ struct Geo {
 };
 
 __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
+#ifndef NTT_SMTW
+#define NTT_SMTW 1   // shared-memory twiddle tables (fill_tw_table); 0 = per-butterfly __ldg (A/B variant)
+#endif
+// entry e of a shared twiddle table sits at e + e/8: round B reads entries j << r apart (r <= 3) across the threads j
+// of a line, which would otherwise all fall in one 16-byte bank group
+__device__ __forceinline__ int tw_pad(int e) { return e + (e >> 3); }
 
 // Round A: local stages 0..EA-1 (forward ascending / inverse descending).  Local block index of the
 // pair (k, k+hs) at local stage s is k >> (EA - s); global twiddle index 2^(s0+s) + (boff << s) + blk.
-template <int LT, bool INV, class Ops>
+template <int LT, bool INV, class Ops, bool SMTW = false>
 __device__ __forceinline__ void round_a(typename Ops::T (&x)[Geo<LT>::E], int s0, int boff,
                                         const typename Ops::TW* __restrict__ tw2, const Ops& ops) {
     constexpr int EA = Geo<LT>::EA, E = Geo<LT>::E;
@@ -180,7 +186,7 @@ __device__ __forceinline__ void round_a(typename Ops::T (&x)[Geo<LT>::E], int s0
         for (int k = 0; k < E; k++) {
             if (k & hs) continue;
             const int idx = base + (k >> (EA - s));
-            const typename Ops::TW T = __ldg(tw2 + idx);
+            const typename Ops::TW T = SMTW ? tw2[tw_pad(idx)] : __ldg(tw2 + idx);
             if (!INV) ops.ct(x[k], x[k + hs], T);
             else ops.gs(x[k], x[k + hs], T);
         }
@@ -189,7 +195,7 @@ __device__ __forceinline__ void round_a(typename Ops::T (&x)[Geo<LT>::E], int s0
 
 // Round B: local stages EA..LT-1.  Element ((j*G+g) << EB) + k'; block index at local stage EA+r is
 // ((j*G+g) << r) + (k' >> (EB - r)).
-template <int LT, bool INV, class Ops>
+template <int LT, bool INV, class Ops, bool SMTW = false>
 __device__ __forceinline__ void round_b(typename Ops::T (&y)[Geo<LT>::E], int j, int s0, int boff,
                                         const typename Ops::TW* __restrict__ tw2, const Ops& ops) {
     constexpr int EA = Geo<LT>::EA, EB = Geo<LT>::EB, G = Geo<LT>::G;
@@ -205,7 +211,7 @@ __device__ __forceinline__ void round_b(typename Ops::T (&y)[Geo<LT>::E], int j,
             for (int k = 0; k < KB; k++) {
                 if (k & hs) continue;
                 const int idx = base + (((j * G + g) << r) + (k >> (EB - r)));
-                const typename Ops::TW T = __ldg(tw2 + idx);
+                const typename Ops::TW T = SMTW ? tw2[tw_pad(idx)] : __ldg(tw2 + idx);
                 if (!INV) ops.ct(y[g * KB + k], y[g * KB + k + hs], T);
                 else ops.gs(y[g * KB + k], y[g * KB + k + hs], T);
             }
@@ -240,6 +246,22 @@ __device__ __forceinline__ void sm_get_b(const T* line, int j, T (&y)[Geo<LT>::E
         for (int k = 0; k < KB; k++) y[g * KB + k] = line[pad(((j * G + g) << EB) + k)];
 }
 
+// Shared-memory twiddle table of one phase (the L1TEX pipe bounded the rows phase at 84 % with a per-butterfly
+// __ldg of its chunk's twiddles, profiles/r02_summary.md): entry i = 2^t + blk (t < LT, blk < 2^t) holds the twiddle of
+// local stage t, block blk of chunk c at global stage s0 + t, i.e. tw[2^(s0+t) + (c << t) + blk]; the rounds then index
+// it with s0 = 0, boff = 0.  Placed after the phase's data tile (lines x LSP words, rounded to 16 bytes).
+template <int LT, class TW>
+__device__ __forceinline__ TW* fill_tw_table(u64* sm_raw, int lines, const TW* __restrict__ tw2, int s0, int c) {
+    const int data_words = (lines * Geo<LT>::LSP + 1) & ~1;
+    TW* stw = reinterpret_cast<TW*>(sm_raw + data_words);
+    for (int i = threadIdx.x + 1; i < (1 << LT); i += blockDim.x) {
+        const int t = 31 - __clz(i), blk = i - (1 << t);
+        stw[tw_pad(i)] = __ldg(tw2 + (1 << (s0 + t)) + (c << t) + blk);
+    }
+    __syncthreads();
+    return stw;
+}
+
 // global word <-> working value.  FIRST: the transform's first phase reads canonical u64 words; later
 // phases of the FP64 path read/write raw double bits (signed intermediates), the integer path lazy u64.
 __device__ __forceinline__ u64 ld_val(u64 v, const IntOps&, bool) { return v; }
@@ -258,34 +280,41 @@ __device__ __forceinline__ u64 st_raw(double v) { return (u64)__double_as_longlo
 // so the round-A register mapping (rows j + TPL k of column l) is read (forward) / written (inverse) straight
 // from/to global memory in coalesced row segments; only the round-B mapping goes through shared memory.
 template <int LT, bool INV, class Ops>
-__device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops& ops, const typename Ops::TW* tw2, int mi) {
+__device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops& ops, const typename Ops::TW* tw2, int mi,
+                                          int bx, int by, int bz) {
     using GG = Geo<LT>;
     using T = typename Ops::T;
     extern __shared__ u64 sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
-    const int limb = blockIdx.y, poly = blockIdx.z;
+    const int limb = by, poly = bz;
     const int S = 1 << a.s2;
-    const int c0 = blockIdx.x * lines;
+    const int c0 = bx * lines;
     u64* g = a.base + (i64)poly * a.poly_stride + (i64)limb * a.N;
     const int lgl = 31 - __clz(lines);
     const int l = threadIdx.x & (lines - 1), j = threadIdx.x >> lgl;
     T* line = sm + l * GG::LSP;
     u64* gc = g + c0 + l + (i64)j * S;            // row j of column c0 + l
+    using TWT = typename Ops::TW;
+#if NTT_SMTW
+    const TWT* stw = fill_tw_table<LT>(sm_raw, lines, tw2, 0, 0);
+#else
+    const TWT* stw = tw2;   // variant: per-butterfly __ldg twiddles (index formula with s0 = 0, boff = 0 is the same)
+#endif
     const i64 rs = (i64)GG::TPL * S;              // TPL rows
     T x[GG::E];
     if (!INV) {
         {
             u64 v[GG::E];
 #pragma unroll
-            for (int k = 0; k < GG::E; k++) v[k] = gc[k * rs];
+            for (int k = 0; k < GG::E; k++) v[k] = __ldcg(gc + k * rs);
 #pragma unroll
             for (int k = 0; k < GG::E; k++) x[k] = ld_val(v[k], ops, true);
         }
-        round_a<LT, false>(x, 0, 0, tw2, ops);
+        round_a<LT, false, Ops, NTT_SMTW>(x, 0, 0, stw, ops);
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, 0, 0, tw2, ops);
+        round_b<LT, false, Ops, NTT_SMTW>(x, j, 0, 0, stw, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         const int tot = GG::T * lines;
@@ -300,7 +329,7 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
 #pragma unroll
             for (int it = 0; it < GG::E; it++) {
                 const int e = threadIdx.x + it * blockDim.x;
-                v[it] = g[(i64)(e >> lgl) * S + c0 + (e & (lines - 1))];
+                v[it] = __ldcg(g + (i64)(e >> lgl) * S + c0 + (e & (lines - 1)));
             }
 #pragma unroll
             for (int it = 0; it < GG::E; it++) {
@@ -310,11 +339,11 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
         }
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, 0, 0, tw2, ops);
+        round_b<LT, true, Ops, NTT_SMTW>(x, j, 0, 0, stw, ops);
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, 0, 0, tw2, ops);
+        round_a<LT, true, Ops, NTT_SMTW>(x, 0, 0, stw, ops);
         if constexpr (std::is_same<T, u64>::value) {
             if (a.apply_ninv) {
                 const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
@@ -343,10 +372,10 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
     asm volatile("griddepcontrol.wait;" ::: "memory");   // predecessor's writes visible (PDL)
     const int mi = a.map.mod[blockIdx.y];
     if ((a.fpmask >> mi) & 1ull) {
-        cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
+        cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     } else {
         const u64 q = a.mod[mi].q;
-        cols_body<LT, INV>(a, lines, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi);
+        cols_body<LT, INV>(a, lines, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     }
 }
 
@@ -358,32 +387,43 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
 // different polynomial, so all lines share one twiddle set (L1-resident) instead of 16 distinct ones.
 template <int LT, bool INV, class Ops>
 __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, const Ops& ops, const typename Ops::TW* tw2,
-                                          int mi) {
+                                          int mi, int bx, int by, int bz) {
     using GG = Geo<LT>;
     using T = typename Ops::T;
     extern __shared__ u64 sm_raw[];
     T* sm = reinterpret_cast<T*>(sm_raw);
-    const int limb = blockIdx.y;
+    const int limb = by;
     const int cmask = (1 << lgc) - 1;
     u64* g0 = a.base + (i64)limb * a.N;
     auto line_ptr = [&](int ll) -> u64* {
-        return g0 + (i64)(((int)blockIdx.z << (31 - __clz(lines) - lgc)) + (ll >> lgc)) * a.poly_stride +
-               (i64)(((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T;
+        return g0 + (i64)((bz << (31 - __clz(lines) - lgc)) + (ll >> lgc)) * a.poly_stride +
+               (i64)((bx << lgc) + (ll & cmask)) * GG::T;
     };
     const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
     T* line = sm + l * GG::LSP;
     u64* gl = line_ptr(l);
-    const int boff = ((int)blockIdx.x << lgc) + (l & cmask);
+    const int boff = (bx << lgc) + (l & cmask);
     const int tot = GG::T * lines;
     T x[GG::E];
+    // every line of the CTA is the same chunk (lgc = 0): its twiddles go through a shared-memory table
+    using TWT = typename Ops::TW;
+    const TWT* stw = NTT_SMTW && lgc == 0 ? fill_tw_table<LT>(sm_raw, lines, tw2, a.s1, bx) : nullptr;
+    auto rA = [&](auto inv_tag) {
+        constexpr bool I = decltype(inv_tag)::value;
+        if (stw) round_a<LT, I, Ops, true>(x, 0, 0, stw, ops); else round_a<LT, I>(x, a.s1, boff, tw2, ops);
+    };
+    auto rB = [&](auto inv_tag) {
+        constexpr bool I = decltype(inv_tag)::value;
+        if (stw) round_b<LT, I, Ops, true>(x, j, 0, 0, stw, ops); else round_b<LT, I>(x, j, a.s1, boff, tw2, ops);
+    };
     if (!INV) {
 #pragma unroll
-        for (int k = 0; k < GG::E; k++) x[k] = ld_val(gl[j + GG::TPL * k], ops, false);
-        round_a<LT, false>(x, a.s1, boff, tw2, ops);
+        for (int k = 0; k < GG::E; k++) x[k] = ld_val(__ldcg(gl + j + GG::TPL * k), ops, false);
+        rA(std::false_type{});
         sm_put_a<LT>(line, j, x);
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, false>(x, j, a.s1, boff, tw2, ops);
+        rB(std::false_type{});
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         const u64 qi = a.mod[mi].q;
@@ -399,8 +439,8 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
                 for (int i2 = 0; i2 < HB; i2++) {
                     const int e = threadIdx.x + (b0 + i2) * blockDim.x;
                     const int ll = e >> LT;
-                    const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
-                    const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
+                    const int p = (bz << lgp) + (ll >> lgc);
+                    const size_t off = (size_t)limb * a.N + (size_t)(((bx << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
                     sv[i2] = a.epi_src[p][off];
                     const u64* ad = a.epi_add[p];
                     av[i2] = ad ? ad[off] : 0;
@@ -417,8 +457,8 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
                         w = fp_canon(fp_center(v, q, qinv), q);
                     }
                     const int ll = e >> LT;
-                    const int p = ((int)blockIdx.z << lgp) + (ll >> lgc);
-                    const size_t off = (size_t)limb * a.N + (size_t)((((int)blockIdx.x << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
+                    const int p = (bz << lgp) + (ll >> lgc);
+                    const size_t off = (size_t)limb * a.N + (size_t)(((bx << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
                     a.epi_out[p][off] = add_mod(mul_shoup(sub_mod(sv[i2], w, qi), f, fsh, qi), av[i2], qi);
                 }
             }
@@ -442,7 +482,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
             const int e = threadIdx.x + it * blockDim.x;
             const u64* lp = line_ptr(e >> LT);
             if (a.src_base) lp = a.src_base + (lp - a.base);
-            v[it] = lp[e & (GG::T - 1)];
+            v[it] = __ldcg(lp + (e & (GG::T - 1)));
         }
 #pragma unroll
         for (int it = 0; it < GG::E; it++) {
@@ -451,11 +491,11 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
         }
         __syncthreads();
         sm_get_b<LT>(line, j, x);
-        round_b<LT, true>(x, j, a.s1, boff, tw2, ops);
+        rB(std::true_type{});
         sm_put_b<LT>(line, j, x);
         __syncthreads();
         sm_get_a<LT>(line, j, x);
-        round_a<LT, true>(x, a.s1, boff, tw2, ops);
+        rA(std::true_type{});
         if constexpr (std::is_same<T, u64>::value) {
 #pragma unroll
             for (int k = 0; k < GG::E; k++) gl[j + GG::TPL * k] = x[k];
@@ -472,10 +512,79 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
     asm volatile("griddepcontrol.wait;" ::: "memory");   // predecessor's writes visible (PDL)
     const int mi = a.map.mod[blockIdx.y];
     if ((a.fpmask >> mi) & 1ull) {
-        rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi);
+        rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     } else {
         const u64 q = a.mod[mi].q;
-        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi);
+        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
+    }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Fused two-phase transform (ENCF_NTT_FUSED=1; off by default, see ntt_fused): ONE persistent launch runs both
+// phases of every limb transform of a batch.  A unit = (limb e, group of LP polynomials) has T1 first-phase tiles and
+// T2 second-phase tiles (the same tiles the two-launch path runs).  CTAs draw tickets from a global counter in the
+// order [first phase of units 0..D-1] then, per k, [first phase of unit k+D | second phase of unit k]: a unit's
+// second phase starts ~D units after its first phase, while the intermediate words (D x LP x 512 KB, ~24 MB) are
+// still in the 126 MB L2 -- so the transform reads and writes HBM once instead of twice.  A second-phase tile waits
+// (acquire) until the T1 first-phase tiles of its unit have signalled (release); tickets are drawn in order by
+// resident CTAs, so every awaited tile is already running (no deadlock).  Data loads bypass L1 (ld.global.cg).
+struct FusedSched {
+    int* ticket;     // [1] ticket counter, zeroed before the launch
+    int* cnt;        // [U] finished first-phase tiles per unit, zeroed before the launch
+    int U, D, T1, T2, total;
+    int nlimbs, LP, Ab;        // units: u = pg * nlimbs + e; cols tiles per unit = Ab x LP
+    int lines_c, lines_r, lgc; // cols-phase lines, rows-phase lines, rows-phase log2(chunks per CTA)
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+template <int LTC, int LTR, bool INV>
+#ifndef NTT_FUSED_MINB
+#define NTT_FUSED_MINB 3
+#endif
+__global__ void __launch_bounds__(kThreads, NTT_FUSED_MINB) ntt_fused_r(NttArgs a, FusedSched f) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // predecessor's writes visible (PDL)
+    __shared__ int s_t;
+    const int nP1 = f.D * f.T1, nMid = (f.U - f.D) * (f.T1 + f.T2);
+    while (true) {
+        __syncthreads();                                   // previous tile's shared-memory reads are done
+        if (threadIdx.x == 0) s_t = atomicAdd(f.ticket, 1);
+        __syncthreads();
+        const int t = s_t;
+        if (t >= f.total) break;
+        int phase, u, r;
+        if (t < nP1) { phase = 1; u = t / f.T1; r = t % f.T1; }
+        else if (t - nP1 < nMid) {
+            const int t1 = t - nP1, k = t1 / (f.T1 + f.T2), rr = t1 % (f.T1 + f.T2);
+            if (rr < f.T1) { phase = 1; u = k + f.D; r = rr; } else { phase = 2; u = k; r = rr - f.T1; }
+        } else {
+            const int t2 = t - nP1 - nMid;
+            phase = 2; u = f.U - f.D + t2 / f.T2; r = t2 % f.T2;
+        }
+        if (phase == 2) {
+            if (threadIdx.x == 0)
+                while (ld_acquire_gpu(f.cnt + u) < f.T1) __nanosleep(64);
+            __syncthreads();
+        }
+        const int e = u % f.nlimbs, pg = u / f.nlimbs;
+        const int mi = a.map.mod[e];
+        const bool fp = (a.fpmask >> mi) & 1ull;
+        if ((phase == 1) != INV) {    // columns phase (forward first / inverse second)
+            const int bx = r % f.Ab, bz = pg * f.LP + r / f.Ab;
+            if (fp) cols_body<LTC, INV>(a, f.lines_c, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, bx, e, bz);
+            else { const u64 q = a.mod[mi].q; cols_body<LTC, INV>(a, f.lines_c, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, bx, e, bz); }
+        } else {
+            if (fp) rows_body<LTR, INV>(a, f.lines_r, f.lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, r, e, pg);
+            else { const u64 q = a.mod[mi].q; rows_body<LTR, INV>(a, f.lines_r, f.lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, r, e, pg); }
+        }
+        if (phase == 1) {
+            __syncthreads();                               // every thread's words are ordered before thread 0's release
+            if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(f.cnt + u) : "memory");
+        }
     }
 }
 
@@ -531,7 +640,7 @@ PhaseCfg phase_cfg(int LT, int avail) {   // avail = number of lines of one limb
     p.lines = lines;
     p.threads = lines * TPL;
     p.blocks = avail / lines;
-    p.smem = (size_t)lines * (T + T / 16 + 1) * sizeof(u64);
+    p.smem = ((size_t)lines * (T + T / 16 + 1) + 1) / 2 * 2 * sizeof(u64) + (size_t)(T + T / 8) * 16;   // data | twiddles
     return p;
 }
 
@@ -559,6 +668,66 @@ int ntt_chunk_polys(const encf_ctx& c, const PolyBatch& b) {
     if (mb <= 0) return b.npolys;
     const long per = (long)b.map.n * c.N * 8;
     return (int)std::max(1L, std::min((long)b.npolys, mb * (1L << 20) / per));
+}
+
+// Fused persistent launch (see ntt_fused_r) for 2^12 <= N <= 2^16; returns false when not applicable.
+template <int LTC, int LTR>
+bool fused_launch(encf_ctx& c, const NttArgs& a, const PolyBatch& b, bool inv, cudaStream_t s) {
+    const PhaseCfg A = phase_cfg(LTC, 1 << LTR), B = phase_cfg(LTR, 1 << LTC);
+    if (A.threads != kThreads || B.threads != kThreads) return false;
+    const RowsCfg R = rows_cfg(B, 1 << LTC, b.npolys, b.map.n);
+    const int LP = (int)R.grid.z == 0 ? 1 : b.npolys / (int)R.grid.z;
+    FusedSched f;
+    f.nlimbs = b.map.n;
+    f.LP = LP;
+    f.Ab = A.blocks;
+    f.lines_c = A.lines;
+    f.lines_r = B.lines;
+    f.lgc = R.lgc;
+    f.U = (b.npolys / LP) * b.map.n;
+    const int Tc = A.blocks * LP, Tr = (int)R.grid.x;
+    f.T1 = inv ? Tr : Tc;
+    f.T2 = inv ? Tc : Tr;
+    f.total = f.U * (f.T1 + f.T2);
+    const size_t smem = std::max(A.smem, B.smem);
+    auto kern = inv ? ntt_fused_r<LTC, LTR, true> : ntt_fused_r<LTC, LTR, false>;
+    static int nsm = 0;
+    static int occ[2] = {0, 0};
+    if (!nsm) CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c.device));
+    int& oc = occ[inv ? 1 : 0];
+    if (!oc) {
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&oc, kern, kThreads, smem));
+        if (oc < 1) oc = 1;
+    }
+    const int grid = std::min(f.total, nsm * oc);
+    // delay D: enough units that a unit's first phase has finished when its second phase is drawn, few enough that
+    // the intermediate words of the units in flight stay well inside L2 (48 MB)
+    const long unit_bytes = (long)LP * c.N * 8;
+    int D = (grid + f.T1 - 1) / f.T1 + 1;
+    D = (int)std::min<long>(D, std::max(1L, (48L << 20) / unit_bytes));
+    f.D = std::max(1, std::min(D, f.U));
+    Scratch sc(s);
+    int* buf = (int*)sc.get((size_t)(f.U + 2) / 2 + 1);
+    CUDA_TRY(cudaMemsetAsync(buf, 0, (size_t)(f.U + 1) * sizeof(int), s));
+    f.ticket = buf;
+    f.cnt = buf + 1;
+    launch_pdl(kern, dim3(grid), kThreads, smem, s, a, f);
+    return true;
+}
+
+bool ntt_fused(encf_ctx& c, const NttArgs& a, const PolyBatch& b, bool inv, cudaStream_t s) {
+    // default OFF: measured on the B200 the fused launch made the layer's NTT time 25.0 -> 29.4 ms (profiles/r02_summary.md)
+    static const bool on = [] { const char* e = std::getenv("ENCF_NTT_FUSED"); return e && std::atoi(e) != 0; }();
+    if (!on) return false;
+    switch (c.logN) {
+        case 12: return fused_launch<6, 6>(c, a, b, inv, s);
+        case 13: return fused_launch<6, 7>(c, a, b, inv, s);
+        case 14: return fused_launch<7, 7>(c, a, b, inv, s);
+        case 15: return fused_launch<7, 8>(c, a, b, inv, s);
+        case 16: return fused_launch<8, 8>(c, a, b, inv, s);
+        default: return false;
+    }
 }
 
 NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
@@ -603,8 +772,9 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
     // L2-sized chunks of polynomials: the rows phase of a chunk re-reads what the columns phase just wrote while it
     // is still in the 126 MB L2, instead of after a whole multi-hundred-MB batch has streamed through
-    const int cp = ntt_chunk_polys(c, b);
-    for (int p0 = 0; p0 < b.npolys; p0 += cp) {
+    const bool fused = ntt_fused(c, a, b, false, s);
+    const int cp = fused ? b.npolys : ntt_chunk_polys(c, b);
+    for (int p0 = 0; !fused && p0 < b.npolys; p0 += cp) {
         const int np = std::min(cp, b.npolys - p0);
         NttArgs ac = a;
         ac.base = a.base + (i64)p0 * a.poly_stride;
@@ -614,7 +784,7 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
         launch_rows<false>(c.s2, R.grid, B.threads, B.smem, s, ac, B.lines, R.lgc);
         c.st_launch += 2;
     }
-    c.st_launch -= 2;
+    c.st_launch -= fused ? 1 : 2;
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     {
@@ -637,8 +807,9 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
-    const int cp = ntt_chunk_polys(c, b);      // L2-sized chunks (see ntt_forward_epi)
-    for (int p0 = 0; p0 < b.npolys; p0 += cp) {
+    const bool fused = ntt_fused(c, a, b, true, s);
+    const int cp = fused ? b.npolys : ntt_chunk_polys(c, b);      // L2-sized chunks (see ntt_forward_epi)
+    for (int p0 = 0; !fused && p0 < b.npolys; p0 += cp) {
         const int np = std::min(cp, b.npolys - p0);
         NttArgs ac = a;
         ac.base = a.base + (i64)p0 * a.poly_stride;
@@ -648,7 +819,7 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
         launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, np), A.threads, A.smem, s, ac, A.lines);
         c.st_launch += 2;
     }
-    c.st_launch -= 2;
+    c.st_launch -= fused ? 1 : 2;
     c.prof_end(slot, s);
     c.st_ntt += (uint64_t)b.npolys * b.map.n;
     {

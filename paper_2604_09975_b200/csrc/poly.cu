@@ -7,6 +7,7 @@
 // Integer work runs on the IMAD pipe with 64x64->128 products; every kernel is HBM- or IMAD-bound
 // (no dense contraction here: DESIGN.md "Why no tensor cores").
 #include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "ctx.cuh"
@@ -448,16 +449,17 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
         ::"r"(smem_u32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
 }
 
-template <bool NARROW>
-__global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(const __grid_constant__ CUtensorMap tmw,
+template <bool NARROW, int ROWS, int MINB>
+__global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel(const __grid_constant__ CUtensorMap tmw,
                                                                              const u64* __restrict__ bank, int nbank,
                                                                              const u64* __restrict__ w, int units, i64 wus,
                                                                              u64* __restrict__ acc, i64 accs, int level, int N,
                                                                              const ModConst* __restrict__ mod, int limb0,
                                                                              int nstages) {
     extern __shared__ __align__(128) u64 dm_sm[];
+    constexpr int SW = MAC_LANES * ROWS * MAC_T;                 // words per stage
     u64* stg = dm_sm;                                            // [nstages][16 lanes][8 rows][32 coefficients]
-    u64* sb = stg + (size_t)nstages * DM_STAGE_WORDS;            // bank tile, layout of diag_mac_kernel
+    u64* sb = stg + (size_t)nstages * SW;            // bank tile, layout of diag_mac_kernel
     uint64_t* bars = (uint64_t*)(sb + (size_t)nbank * 2 * MAC_T);
     const int limb = limb0 + blockIdx.y;
     const int k0 = blockIdx.x * MAC_T;
@@ -484,15 +486,15 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(co
     }
     __syncthreads();
     const int ngroups = (units + MAC_LANES - 1) / MAC_LANES;
-    const int nch = (nbank + DM_ROWS - 1) / DM_ROWS;
+    const int nch = (nbank + ROWS - 1) / ROWS;
     const int mygroups = blockIdx.z < ngroups ? (ngroups - 1 - blockIdx.z) / gridDim.z + 1 : 0;
     const int total = mygroups * nch;
     auto issue = [&](int s) {
         if (tid != 0) return;
         const int g = blockIdx.z + (s / nch) * gridDim.z, c = s % nch;
         const int slot = s % nstages;
-        mbar_arrive_expect_tx(&bars[slot], (uint32_t)(DM_STAGE_WORDS * 8));      // the full box (OOB zero-filled)
-        tma_load_4d(stg + (size_t)slot * DM_STAGE_WORDS, &tmw, k0, limb, c * DM_ROWS, g * MAC_LANES, &bars[slot]);
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)(SW * 8));      // the full box (OOB zero-filled)
+        tma_load_4d(stg + (size_t)slot * SW, &tmw, k0, limb, c * ROWS, g * MAC_LANES, &bars[slot]);
     };
     (void)w; (void)pstride;
     for (int s = 0; s < nstages - 1 && s < total; s++) issue(s);
@@ -507,14 +509,14 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(co
         const int slot = s % nstages;
         mbar_wait(&bars[slot], (uint32_t)((s / nstages) & 1));
         const int g = blockIdx.z + (s / nch) * gridDim.z, c = s % nch;
-        const int rows = min(DM_ROWS, nbank - c * DM_ROWS);
+        const int rows = min(ROWS, nbank - c * ROWS);
         const int u = g * MAC_LANES + lane;
         if (u < units) {
-            const ulonglong2* xr = (const ulonglong2*)(stg + (size_t)slot * DM_STAGE_WORDS + (size_t)lane * DM_ROWS * MAC_T) + kp;
+            const ulonglong2* xr = (const ulonglong2*)(stg + (size_t)slot * SW + (size_t)lane * ROWS * MAC_T) + kp;
             if constexpr (NARROW) {
-                const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * DM_ROWS) * 2 * (MAC_T / 2);
+                const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * ROWS) * 2 * (MAC_T / 2);
 #pragma unroll
-                for (int t = 0; t < DM_ROWS; t++) {
+                for (int t = 0; t < ROWS; t++) {
                     if (t < rows) {
                         const ulonglong2 x = xr[t * (MAC_T / 2)];
                         const uint32_t ah = (uint32_t)(x.x >> 20), al = (uint32_t)(x.x & 0xFFFFF);
@@ -531,9 +533,9 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(co
             } else {
                 const ulonglong2* sbw = (const ulonglong2*)sb;
 #pragma unroll
-                for (int t = 0; t < DM_ROWS; t++) {
+                for (int t = 0; t < ROWS; t++) {
                     if (t < rows) {
-                        const int uq = c * DM_ROWS + t;
+                        const int uq = c * ROWS + t;
                         const ulonglong2 x = xr[t * (MAC_T / 2)];
                         const ulonglong2 b0 = sbw[uq * MAC_T + kp];
                         const ulonglong2 b1 = sbw[uq * MAC_T + MAC_T / 2 + kp];
@@ -543,7 +545,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, 1) diag_mac_tma_kernel(co
                         mac128(a11, b1.y, x.y);
                     }
                 }
-                if ((c & 3) == 3) {     // every 32 products (< 32 q^2 <= 2^127 for q < 2^61): fold below q
+                if ((((c + 1) * ROWS) & 31) == 0) {     // every 32 products (< 32 q^2 <= 2^127 for q < 2^61): fold below q
                     a00 = U128{barrett128(a00, mc.q, mc.rhi, mc.rlo), 0}; a01 = U128{barrett128(a01, mc.q, mc.rhi, mc.rlo), 0};
                     a10 = U128{barrett128(a10, mc.q, mc.rhi, mc.rlo), 0}; a11 = U128{barrett128(a11, mc.q, mc.rhi, mc.rlo), 0};
                 }
@@ -851,23 +853,42 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
                            (uint64_t)units * 2 * level * c.N * 8;
     int slot;
     c.prof_begin("diag_mac", s, bytes, slot);
-    // bulk-copy (TMA) pipeline when the bank tile leaves room for >= 2 stages of 32 KB (ENCF_MAC_LEGACY: register path)
-    static const bool legacy = std::getenv("ENCF_MAC_LEGACY") != nullptr;
-    constexpr size_t kMaxSmem = 227 * 1024;
+    // Path (ENCF_MAC_VARIANT): "tma2" (default) = tensor-map TMA ring of 32 KB stages at 2 CTAs/SM, "tma1" = 32 KB
+    // stages at 1 CTA/SM, "tma3" = 16 KB stages at 3 CTAs/SM, "reg" = register double buffer (diag_mac_kernel, 2 CTAs/SM).
+    // Measured on the B200 (BERT layer, profiles/r02_summary.md): tma2 10.3 ms, reg 11.0, tma3 13.2, tma1 14.7.
+    // All paths give the same words.
+    static const int variant = [] {
+        const char* e = std::getenv("ENCF_MAC_VARIANT");
+        if (!e) return 2;
+        if (!strcmp(e, "reg")) return 0;
+        if (!strcmp(e, "tma1")) return 1;
+        if (!strcmp(e, "tma2")) return 2;
+        if (!strcmp(e, "tma3")) return 3;
+        return 0;
+    }();
     const size_t bank_b = (size_t)nbank * 2 * MAC_T * 8;
-    const int nst = bank_b + 2 * DM_STAGE_WORDS * 8 + 64 <= kMaxSmem
-                        ? (int)std::min<size_t>(DM_MAX_STAGES, (kMaxSmem - bank_b - 64) / (DM_STAGE_WORDS * 8)) : 0;
-    if (!legacy && nst >= 2) {
+    const int rows = variant == 3 ? 4 : 8;
+    const size_t stage_b = (size_t)MAC_LANES * rows * MAC_T * 8;
+    const size_t cap = variant == 1 ? 227 * 1024 : variant == 2 ? 113 * 1024 : 75 * 1024;
+    const int nst = variant && bank_b + 2 * stage_b + 64 <= cap
+                        ? (int)std::min<size_t>(DM_MAX_STAGES, (cap - bank_b - 64) / stage_b) : 0;
+    if (nst >= 2) {
         static bool tma_attr = false;
         if (!tma_attr) {
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxSmem));
+            const int mx = 227 * 1024;
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             tma_attr = true;
         }
-        const size_t tsm = (size_t)nst * DM_STAGE_WORDS * 8 + bank_b + (size_t)nst * 8;
+        const size_t tsm = (size_t)nst * stage_b + bank_b + (size_t)nst * 8;
         const int groups = (units + MAC_LANES - 1) / MAC_LANES;
         int zs = 1;
-        while ((size_t)tiles * level * zs < 148 && zs < groups) zs *= 2;
+        const int per_sm = variant == 1 ? 1 : variant;
+        while ((size_t)tiles * level * zs < (size_t)148 * per_sm && zs < groups) zs *= 2;
         // the weight stream as a 4-D tensor [units][nbank][level][N] for the TMA engine
         static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
         if (!encode) {
@@ -878,17 +899,22 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         CUtensorMap tm;
         const cuuint64_t dims[4] = {(cuuint64_t)c.N, (cuuint64_t)level, (cuuint64_t)nbank, (cuuint64_t)units};
         const cuuint64_t strides[3] = {(cuuint64_t)c.N * 8, (cuuint64_t)level * c.N * 8, (cuuint64_t)wus * 8};
-        const cuuint32_t box[4] = {MAC_T, 1, DM_ROWS, MAC_LANES};
+        const cuuint32_t box[4] = {MAC_T, 1, (cuuint32_t)rows, MAC_LANES};
         const cuuint32_t estr[4] = {1, 1, 1, 1};
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, (void*)w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             throw EncfError(ENCF_ERR_CUDA, "diag_mac: cuTensorMapEncodeTiled failed");
-        if (nw > 0)
-            diag_mac_tma_kernel<false><<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs,
-                                                                                           level, c.N, c.d_mod, 0, nst);
-        if (nw < level)
-            diag_mac_tma_kernel<true><<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc,
-                                                                                                  accs, level, c.N, c.d_mod, nw, nst);
+        auto launch = [&](auto kw, auto kn) {
+            if (nw > 0)
+                kw<<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
+                                                                       c.d_mod, 0, nst);
+            if (nw < level)
+                kn<<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level,
+                                                                               c.N, c.d_mod, nw, nst);
+        };
+        if (variant == 1) launch(diag_mac_tma_kernel<false, 8, 1>, diag_mac_tma_kernel<true, 8, 1>);
+        else if (variant == 2) launch(diag_mac_tma_kernel<false, 8, 2>, diag_mac_tma_kernel<true, 8, 2>);
+        else launch(diag_mac_tma_kernel<false, 4, 3>, diag_mac_tma_kernel<true, 4, 3>);
     } else {
         if (nw > 0)
             diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
@@ -1070,6 +1096,83 @@ __global__ void __launch_bounds__(TB, KS_MINB) ks_inner_batch_kernel(KsInnerBatc
             *(ulonglong2*)(acc + ((size_t)nl + e) * N + kk[p]) =
                 make_ulonglong2(redc128(a1[p], mc.q, mc.qinv), redc128(b1[p], mc.q, mc.qinv));
         }
+    }
+}
+
+// The same inner product with the operands staged by the TMA engine (ENCF_KS_TMA, default on for N >= 1024): a CTA owns
+// an aligned tile of KT = 1024 coefficients of one (request, extended limb).  The Galois gather maps an aligned
+// 2^k-block of NTT-domain indices onto ONE aligned 2^k-block (brv keeps the block's low bits of 2 brv(i) + 1 fixed,
+// and multiplying by an odd g keeps them fixed), so per digit j three contiguous 8 KB bulk copies (cp.async.bulk,
+// SASS UBLKCP) bring the source ext block and the two key tiles into shared memory, all dnum digits issued up front on
+// one mbarrier each (up to 72 KB in flight per CTA); the threads then read their permuted pairs from shared memory.
+// Same arithmetic and output words as ks_inner_batch_kernel.
+constexpr int KT = 1024;
+__global__ void __launch_bounds__(TB, 3) ks_inner_tma_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
+                                                             LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
+    extern __shared__ __align__(128) u64 kt_sm[];      // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [dnum] mbarriers
+    uint64_t* bars = (uint64_t*)(kt_sm + (size_t)dnum * 3 * KT);
+    const int r = blockIdx.z, e = blockIdx.y;
+    const int kb = blockIdx.x * KT;
+    const u64* __restrict__ ext = B.ext[r];
+    const u64* __restrict__ key = B.key[r];
+    const uint32_t g = B.gather[r];
+    const uint32_t mask2n = 2 * N - 1;
+    auto src_of = [&](int k) -> int {
+        if (g == 1) return k;
+        const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+        return brv((int)((e2 - 1) >> 1), logN);
+    };
+    const int sb = src_of(kb) & ~(KT - 1);             // the aligned source block of this tile
+    const int kle = klm.kl[e];
+    if (threadIdx.x == 0) {
+        for (int j = 0; j < dnum; j++) mbar_init(&bars[j], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int j = 0; j < dnum; j++) {
+            u64* st = kt_sm + (size_t)j * 3 * KT;
+            const u64* kj = key + (size_t)j * 2 * key_nl * N;
+            mbar_arrive_expect_tx(&bars[j], 3 * KT * 8);
+            bulk_g2s(st, ext + ((size_t)j * nl + e) * N + sb, KT * 8, &bars[j]);
+            bulk_g2s(st + KT, kj + (size_t)kle * N + kb, KT * 8, &bars[j]);
+            bulk_g2s(st + 2 * KT, kj + ((size_t)key_nl + kle) * N + kb, KT * 8, &bars[j]);
+        }
+    }
+    __syncthreads();                                    // barrier initialisation visible to every waiting thread
+    const ModConst mc = mod[em.mod[e]];
+    constexpr int PP = KT / 2 / TB;                     // coefficient pairs per thread (2)
+    int kl[PP], sl[PP], sw[PP];
+#pragma unroll
+    for (int p = 0; p < PP; p++) {
+        kl[p] = 2 * (threadIdx.x + p * TB);             // local coefficient (even)
+        const int src = src_of(kb + kl[p]);
+        sl[p] = (src & ~1) - sb;
+        sw[p] = src & 1;
+    }
+    U128 a0[PP], a1[PP], b0[PP], b1[PP];
+#pragma unroll
+    for (int p = 0; p < PP; p++) a0[p] = a1[p] = b0[p] = b1[p] = U128{0, 0};
+    for (int j = 0; j < dnum; j++) {
+        mbar_wait(&bars[j], 0);
+        const u64* st = kt_sm + (size_t)j * 3 * KT;
+#pragma unroll
+        for (int p = 0; p < PP; p++) {
+            ulonglong2 x = *(const ulonglong2*)(st + sl[p]);
+            const ulonglong2 k0 = *(const ulonglong2*)(st + KT + kl[p]);
+            const ulonglong2 k1 = *(const ulonglong2*)(st + 2 * KT + kl[p]);
+            if (sw[p]) { u64 t = x.x; x.x = x.y; x.y = t; }
+            mac128(a0[p], x.x, k0.x);
+            mac128(b0[p], x.y, k0.y);
+            mac128(a1[p], x.x, k1.x);
+            mac128(b1[p], x.y, k1.y);
+        }
+    }
+    u64* __restrict__ acc = B.acc[r];
+#pragma unroll
+    for (int p = 0; p < PP; p++) {
+        *(ulonglong2*)(acc + (size_t)e * N + kb + kl[p]) =
+            make_ulonglong2(redc128(a0[p], mc.q, mc.qinv), redc128(b0[p], mc.q, mc.qinv));
+        *(ulonglong2*)(acc + ((size_t)nl + e) * N + kb + kl[p]) =
+            make_ulonglong2(redc128(a1[p], mc.q, mc.qinv), redc128(b1[p], mc.q, mc.qinv));
     }
 }
 
@@ -1376,6 +1479,142 @@ __global__ void __launch_bounds__(TB, 4) bconv_batch_kernel(const u64* __restric
     }
 }
 
+// ------------------------------------------------------------------------------------ tensor-core base conversion
+// The same conversion on the 5th-generation tensor cores (tcgen05.mma .kind::i8, u8 x u8 -> s32: exact integers).
+// With v_i = [x_i vfac_i]_{q_i} split into bytes v_i = sum_a v_i[a] 2^{8a} and the constant matrix
+// W'[i][a][t] = 2^{8a} wfac[i][t] mod q_t (wfac in Montgomery form) split into bytes W'[i][a][t][b] (ctx.cu
+// bconv_wbytes), one M = 128 coefficients x N = 8 nout x K = 64 bytes MMA pair gives
+//   D[k][(t, b)] = sum_{(i, a)} v_i[a](k) W'[i][a][t][b]       (< 64 * 255^2 < 2^22, no overflow)
+//   T[t][k] = sum_b D[k][(t, b)] 2^{8b} (+ r corr_t) = (sum_i v_i wfac[i][t] + r corr_t) mod q_t  (T < 2^79 < q_t 2^64)
+// and out = REDC(T): bit-identical to bconv_batch_kernel (the same REDC of a congruent 128-bit value < q_t 2^64).
+// Operands: A = the tile's v bytes [128 rows][64 B] and B = W' bytes [nb rows][64 B], both K-major in the canonical
+// no-swizzle layout ([16-byte K chunk][row][16 B]: SBO = 128 B between 8-row core matrices, LBO = rows x 16 B
+// between the two K chunks of one K32 step); D lives in TMEM (lane = coefficient, column = 8 t + b) and is read back
+// with tcgen05.ld 32x32b.x8 (one thread per coefficient row).  Inputs beyond NIN are zero rows of B.  Each CTA
+// (128 threads) loops over 128-coefficient tiles with the next tile's inputs in flight during the current MMA and
+// epilogue.  Microbench + decision: tools/micro/bconv_tc.cu, profiles/r02_summary.md.
+__device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);   // version 1, no swizzle
+}
+
+constexpr int BTC_TILE = 128;
+template <int NIN, bool CORR>
+__global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
+                                                           const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
+                                                           const uint8_t* __restrict__ wb, int nb, int tcols, LimbMap om,
+                                                           OutPos op, u64* __restrict__ out, i64 out_stride, int N,
+                                                           int npolys, const ModConst* __restrict__ mod,
+                                                           const u64* __restrict__ corr, const u64* __restrict__ cfix,
+                                                           const u64* __restrict__ csh) {
+    extern __shared__ __align__(1024) uint8_t btc_sm[];
+    uint8_t* sA = btc_sm;                                   // [4][128][16]
+    uint8_t* sB = btc_sm + BTC_TILE * 64;                   // [4][nb][16]
+    u64* sq = (u64*)(sB + (size_t)nb * 64);                 // [nout] q_t | qinv_t | corr_t | pos_t * N
+    u64* sqi = sq + 32;
+    u64* scr = sqi + 32;
+    u64* spos = scr + 32;
+    uint64_t* mbar = (uint64_t*)(spos + 32);
+    uint32_t* tmem_slot = (uint32_t*)(mbar + 1);
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int nout = om.n;
+    for (int i = tid; i < nb * 4; i += BTC_TILE) ((uint4*)sB)[i] = __ldg((const uint4*)wb + i);
+    for (int t = tid; t < nout; t += BTC_TILE) {
+        sq[t] = mod[om.mod[t]].q;
+        sqi[t] = mod[om.mod[t]].qinv;
+        scr[t] = CORR ? corr[t] : 0;
+        spos[t] = (u64)op.pos[t] * (u64)N;
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)), "r"(tcols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        mbar_init(mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tbase = *tmem_slot;
+    u64 qin[NIN], vf[NIN], vfs[NIN], cf[NIN];
+    int cs[NIN];
+#pragma unroll
+    for (int i = 0; i < NIN; i++) {
+        qin[i] = mod[im.mod[i]].q;
+        vf[i] = vfac[i];
+        vfs[i] = vfac_sh[i];
+        cf[i] = CORR ? cfix[i] : 0;
+        cs[i] = CORR ? (int)csh[i] : 0;
+    }
+    // instruction descriptor: D s32 (bits 4-5 = 2), A/B u8 (0), K-major, N = nb, M = 128
+    const uint32_t idesc = (2u << 4) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(BTC_TILE >> 4) << 24);
+    const int tpp = N / BTC_TILE, ntiles = tpp * npolys;
+    u64 nx[NIN];
+    auto load_tile = [&](int tile) {
+        if (tile >= ntiles) return;
+        const u64* ip = in + (size_t)(tile / tpp) * in_stride + (size_t)(tile % tpp) * BTC_TILE + tid;
+#pragma unroll
+        for (int i = 0; i < NIN; i++) nx[i] = __ldg(ip + (size_t)i * N);
+    };
+    load_tile(blockIdx.x);
+    uint32_t phase = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int p = tile / tpp, k0 = (tile % tpp) * BTC_TILE;
+        u64 r = 0;
+        {
+            u64 fsum = 0;
+#pragma unroll
+            for (int i = 0; i < NIN; i++) {
+                const u64 v = mul_shoup(nx[i], vf[i], vfs[i], qin[i]);
+                if (CORR) fsum += umulhi(v << cs[i], cf[i]);
+                *(u64*)(sA + (i >> 1) * (BTC_TILE * 16) + tid * 16 + (i & 1) * 8) = v;
+            }
+            if (CORR) r = (fsum + (1ull << 58)) >> 59;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic-proxy smem writes -> tensor core
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (tid == 0) {
+#pragma unroll
+            for (int st = 0; st < 2; st++) {   // K = 64 bytes: two K32 steps of two 16-byte chunks
+                const uint64_t da = umma_sdesc(smem_u32(sA) + st * 2 * BTC_TILE * 16, BTC_TILE * 16, 128);
+                const uint64_t db = umma_sdesc(smem_u32(sB) + st * 2 * nb * 16, nb * 16, 128);
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+                    ::"r"(tbase), "l"(da), "l"(db), "r"(idesc), "r"((uint32_t)st) : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+                         : "memory");
+        }
+        load_tile(tile + gridDim.x);   // next tile's inputs in flight during the MMA and the epilogue
+        mbar_wait(mbar, phase);
+        phase ^= 1;
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        u64* o = out + (size_t)p * out_stride + k0 + tid;
+        const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
+        for (int t = 0; t < nout; t++) {
+            uint32_t d[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+                         : "r"(tl + t * 8));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const u64 lo4 = (u64)d[0] + ((u64)d[1] << 8) + ((u64)d[2] << 16) + ((u64)d[3] << 24);
+            const u64 hi4 = (u64)d[4] + ((u64)d[5] << 8) + ((u64)d[6] << 16) + ((u64)d[7] << 24);
+            U128 T{lo4, 0};
+            add128(T, hi4 << 32);
+            T.hi += hi4 >> 32;
+            if (CORR) mac128(T, r, scr[t]);
+            o[spos[t]] = redc128(T, sq[t], sqi[t]);
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncthreads();               // TMEM and sA are free for the next tile
+    }
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(tcols));
+}
+
 // Gather-copy: dst + p*dst_stride <- src[p] (words each), optional Galois gather per item (NTT domain).
 __global__ void gather_copy_kernel(CopyBatch C, u64* dst, i64 dst_stride, size_t words, int N, int logN) {
     const int p = blockIdx.y;
@@ -1474,7 +1713,18 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
     const uint64_t bytes = (uint64_t)nreq * ((uint64_t)dnum * nl * c.N * 8 * 3 + (uint64_t)2 * nl * c.N * 8);
     int slot;
     c.prof_begin("ks_inner", s, bytes, slot);
-    ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+    static const bool tma = [] { const char* e = std::getenv("ENCF_KS_TMA"); return !e || std::atoi(e) != 0; }();
+    if (tma && c.N >= KT && dnum <= 4) {
+        const size_t sm = (size_t)dnum * 3 * KT * 8 + 64;
+        static bool attr = false;
+        if (!attr) {
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
+            attr = true;
+        }
+        ks_inner_tma_kernel<<<dim3(c.N / KT, nl, nreq), TB, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+    } else {
+        ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+    }
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
     CUDA_TRY(cudaGetLastError());
@@ -1589,7 +1839,7 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
-                   const u64* cfix, const u64* csh) {
+                   const u64* cfix, const u64* csh, const uint8_t* wb) {
     if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
     if (c.max_mod >= (1ull << 60) || im.n > 8) throw EncfError(ENCF_ERR_ARG, "bconv: the 30-bit split needs moduli < 2^60 and <= 8 inputs");
     {   // Montgomery bound of the lazy sum: sum_i q_i + (n_in + 1) <= 2^64 (then T < q_t 2^64)
@@ -1599,6 +1849,37 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
     }
     OutPos op;
     for (int t = 0; t < om.n; t++) op.pos[t] = pos[t];
+    static const bool tc = [] { const char* e = std::getenv("ENCF_BCONV_TC"); return !e || std::atoi(e) != 0; }();
+    if (tc && wb && om.n <= 32 && c.N % BTC_TILE == 0) {
+        const int nb = 8 * ((om.n + 1) & ~1);
+        const int tcols = nb <= 32 ? 32 : nb <= 64 ? 64 : nb <= 128 ? 128 : 256;
+        const int per_sm = std::min(4, 512 / tcols);   // TMEM: <= 512 columns per SM; smem request caps CTAs per SM
+        const size_t need = (size_t)BTC_TILE * 64 + (size_t)nb * 64 + 4 * 32 * 8 + 16;
+        const size_t smem_tc = std::max(need, (size_t)(220 * 1024) / per_sm);
+        static bool attr = false;
+        if (!attr) {
+#define A(NI) CUDA_TRY(cudaFuncSetAttribute(bconv_tc_kernel<NI, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024)); \
+              CUDA_TRY(cudaFuncSetAttribute(bconv_tc_kernel<NI, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            A(1) A(2) A(3) A(4) A(5) A(6) A(7) A(8)
+#undef A
+            attr = true;
+        }
+        const int ntiles = c.N / BTC_TILE * npolys;
+        const int grid = std::min(ntiles, 148 * per_sm);
+        { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
+        switch (im.n) {
+#define B(NI) case NI: if (corr) bconv_tc_kernel<NI, true><<<grid, BTC_TILE, smem_tc, s>>>(in, in_stride, im, vf, vfs, wb, nb, tcols, \
+                  om, op, out, out_stride, c.N, npolys, c.d_mod, corr, cfix, csh); \
+              else bconv_tc_kernel<NI, false><<<grid, BTC_TILE, smem_tc, s>>>(in, in_stride, im, vf, vfs, wb, nb, tcols, om, op, out, \
+                  out_stride, c.N, npolys, c.d_mod, corr, cfix, csh); break;
+            B(1) B(2) B(3) B(4) B(5) B(6) B(7) B(8)
+#undef B
+        }
+        c.prof_end(_slot, s); }
+        c.st_launch++; c.st_bytes += (uint64_t)npolys * (im.n + om.n) * c.N * 8;
+        CUDA_TRY(cudaGetLastError());
+        return;
+    }
     size_t smem = ((size_t)im.n * om.n + 4 * om.n + 5 * im.n) * sizeof(u64);
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
