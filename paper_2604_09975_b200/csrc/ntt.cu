@@ -165,7 +165,7 @@ struct Geo {
 
 __device__ __forceinline__ int pad(int x) { return x + (x >> 4); }
 #ifndef NTT_SMTW
-#define NTT_SMTW 1   // shared-memory twiddle tables (fill_tw_table); 0 = per-butterfly __ldg (A/B variant)
+#define NTT_SMTW 1   // shared-memory twiddle tables (tw_load / tw_store); 0 = per-butterfly __ldg (A/B variant)
 #endif
 // entry e of a shared twiddle table sits at e + e/8: round B reads entries j << r apart (r <= 3) across the threads j
 // of a line, which would otherwise all fall in one 16-byte bank group
@@ -250,16 +250,24 @@ __device__ __forceinline__ void sm_get_b(const T* line, int j, T (&y)[Geo<LT>::E
 // __ldg of its chunk's twiddles, profiles/r02_summary.md): entry i = 2^t + blk (t < LT, blk < 2^t) holds the twiddle of
 // local stage t, block blk of chunk c at global stage s0 + t, i.e. tw[2^(s0+t) + (c << t) + blk]; the rounds then index
 // it with s0 = 0, boff = 0.  Placed after the phase's data tile (lines x LSP words, rounded to 16 bytes).
+// Split in two so the table's load overlaps the phase's data loads: tw_load issues this thread's entry (one per thread,
+// 2^LT - 1 <= blockDim entries), tw_store writes it after the data loads are in flight; the caller's next
+// __syncthreads publishes the table.
 template <int LT, class TW>
-__device__ __forceinline__ TW* fill_tw_table(u64* sm_raw, int lines, const TW* __restrict__ tw2, int s0, int c) {
-    const int data_words = (lines * Geo<LT>::LSP + 1) & ~1;
-    TW* stw = reinterpret_cast<TW*>(sm_raw + data_words);
-    for (int i = threadIdx.x + 1; i < (1 << LT); i += blockDim.x) {
-        const int t = 31 - __clz(i), blk = i - (1 << t);
-        stw[tw_pad(i)] = __ldg(tw2 + (1 << (s0 + t)) + (c << t) + blk);
-    }
-    __syncthreads();
-    return stw;
+__device__ __forceinline__ TW tw_load(const TW* __restrict__ tw2, int s0, int c) {
+    const int i = threadIdx.x + 1;
+    if (i >= (1 << LT)) return TW{};
+    const int t = 31 - __clz(i), blk = i - (1 << t);
+    return __ldg(tw2 + (1 << (s0 + t)) + (c << t) + blk);
+}
+template <int LT, class TW>
+__device__ __forceinline__ TW* tw_table(u64* sm_raw, int lines) {
+    return reinterpret_cast<TW*>(sm_raw + ((lines * Geo<LT>::LSP + 1) & ~1));
+}
+template <int LT, class TW>
+__device__ __forceinline__ void tw_store(TW* stw, TW v) {
+    const int i = threadIdx.x + 1;
+    if (i < (1 << LT)) stw[tw_pad(i)] = v;
 }
 
 // global word <-> working value.  FIRST: the transform's first phase reads canonical u64 words; later
@@ -296,7 +304,8 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
     u64* gc = g + c0 + l + (i64)j * S;            // row j of column c0 + l
     using TWT = typename Ops::TW;
 #if NTT_SMTW
-    const TWT* stw = fill_tw_table<LT>(sm_raw, lines, tw2, 0, 0);
+    TWT* stw = tw_table<LT, TWT>(sm_raw, lines);
+    const TWT twv = tw_load<LT>(tw2, 0, 0);
 #else
     const TWT* stw = tw2;   // variant: per-butterfly __ldg twiddles (index formula with s0 = 0, boff = 0 is the same)
 #endif
@@ -307,6 +316,10 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
             u64 v[GG::E];
 #pragma unroll
             for (int k = 0; k < GG::E; k++) v[k] = __ldcg(gc + k * rs);
+#if NTT_SMTW
+            tw_store<LT>(stw, twv);
+            __syncthreads();
+#endif
 #pragma unroll
             for (int k = 0; k < GG::E; k++) x[k] = ld_val(v[k], ops, true);
         }
@@ -331,6 +344,9 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
                 const int e = threadIdx.x + it * blockDim.x;
                 v[it] = __ldcg(g + (i64)(e >> lgl) * S + c0 + (e & (lines - 1)));
             }
+#if NTT_SMTW
+            tw_store<LT>(stw, twv);
+#endif
 #pragma unroll
             for (int it = 0; it < GG::E; it++) {
                 const int e = threadIdx.x + it * blockDim.x;
@@ -407,7 +423,9 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
     T x[GG::E];
     // every line of the CTA is the same chunk (lgc = 0): its twiddles go through a shared-memory table
     using TWT = typename Ops::TW;
-    const TWT* stw = NTT_SMTW && lgc == 0 ? fill_tw_table<LT>(sm_raw, lines, tw2, a.s1, bx) : nullptr;
+    const bool use_tab = NTT_SMTW && lgc == 0;
+    TWT* stw = use_tab ? tw_table<LT, TWT>(sm_raw, lines) : nullptr;
+    const TWT twv = use_tab ? tw_load<LT>(tw2, a.s1, bx) : TWT{};
     auto rA = [&](auto inv_tag) {
         constexpr bool I = decltype(inv_tag)::value;
         if (stw) round_a<LT, I, Ops, true>(x, 0, 0, stw, ops); else round_a<LT, I>(x, a.s1, boff, tw2, ops);
@@ -419,6 +437,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
     if (!INV) {
 #pragma unroll
         for (int k = 0; k < GG::E; k++) x[k] = ld_val(__ldcg(gl + j + GG::TPL * k), ops, false);
+        if (use_tab) { tw_store<LT>(stw, twv); __syncthreads(); }
         rA(std::false_type{});
         sm_put_a<LT>(line, j, x);
         __syncthreads();
@@ -484,6 +503,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
             if (a.src_base) lp = a.src_base + (lp - a.base);
             v[it] = __ldcg(lp + (e & (GG::T - 1)));
         }
+        if (use_tab) tw_store<LT>(stw, twv);
 #pragma unroll
         for (int it = 0; it < GG::E; it++) {
             const int e = threadIdx.x + it * blockDim.x;

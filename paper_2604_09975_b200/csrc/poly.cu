@@ -2105,46 +2105,98 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         const u64 t40 = (1ull << 40) % mc.q;
         const uint2* ss = (const uint2*)sm_src;
         const uint2* sk = (const uint2*)sm_msk;
-        // register blocking: a thread computes TR = 4 consecutive t of one component, so each mask word
-        // (and its split sum) is loaded once per 4 products
-        constexpr int TR = 4;
+        // register blocking over TR = 8 consecutive t of one component with a SLIDING window: b_t needs src[t - u], so
+        // stepping u -> u + 1 shifts the thread's TR source words by one position -- one new shared-memory word (and
+        // one mask word) per TR products instead of TR + 1 (the window lives in a register ring indexed
+        // (j - u) mod TR, resolved at compile time by unrolling u by TR)
+        constexpr int TR = 8;
         const int ngrp = (A.nt + TR - 1) / TR;
         for (int o = w; o < ngrp * 2; o += nw) {
             const int t0 = (o >> 1) * TR, c = o & 1;
             u64 hh[TR], ll[TR], sum[TR];
 #pragma unroll
-            for (int j = 0; j < TR; j++) hh[j] = ll[j] = sum[j] = 0;
-            const uint2* sp = ss + (size_t)(t0 + A.dmax) * 2 * BC_T + c * BC_T + kk;
-            const int jmax = min(TR, A.nt - t0);
-#pragma unroll 4
-            for (int u = 0; u < A.nu; u++) {
-                const uint2 m = sk[u * BC_T + kk];
-                const uint32_t ms = m.x + m.y;
-                const uint2* su = sp - (i64)u * 2 * BC_T;
+            for (int jj = 0; jj < TR; jj++) hh[jj] = ll[jj] = sum[jj] = 0;
+            // src word of (t0 + jj, u) = ss[(t0 + jj + dmax - u) * 2 BC_T + c BC_T + kk]; indices past the window only
+            // occur for t >= nt (never stored) -- clamp them into it
+            const uint2* sp = ss + c * BC_T + kk;
+            const int dlast = A.nsrc - 1;
+            auto src_at = [&](int d) -> uint2 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
+            uint32_t wh[TR], wl[TR], ws[TR];
 #pragma unroll
-                for (int j = 0; j < TR; j++) {
-                    if (j < jmax) {
-                        const uint2 x = su[(i64)j * 2 * BC_T];
-                        hh[j] += (u64)x.x * m.x;
-                        ll[j] += (u64)x.y * m.y;
-                        sum[j] += (u64)(x.x + x.y) * ms;
+            for (int jj = 0; jj < TR; jj++) {
+                const uint2 x = src_at(t0 + jj + A.dmax);
+                wh[jj] = x.x; wl[jj] = x.y; ws[jj] = x.x + x.y;
+            }
+            for (int u0 = 0; u0 < A.nu; u0 += TR) {
+#pragma unroll
+                for (int du = 0; du < TR; du++) {
+                    const int u = u0 + du;
+                    if (u < A.nu) {
+                        if (u > 0) {   // position 0 of step u enters the slot that held position TR - 1 of step u - 1
+                            const uint2 x = src_at(t0 - u + A.dmax);
+                            const int sl = (TR - du) % TR;
+#pragma unroll
+                            for (int q = 0; q < TR; q++)
+                                if (q == sl) { wh[q] = x.x; wl[q] = x.y; ws[q] = x.x + x.y; }
+                        }
+                        const uint2 m = sk[u * BC_T + kk];
+                        const uint32_t ms = m.x + m.y;
+#pragma unroll
+                        for (int jj = 0; jj < TR; jj++) {
+                            const int q = (jj - du + TR) % TR;
+                            hh[jj] += (u64)wh[q] * m.x;
+                            ll[jj] += (u64)wl[q] * m.y;
+                            sum[jj] += (u64)ws[q] * ms;
+                        }
                     }
                 }
             }
+            const int jmax = min(TR, A.nt - t0);
 #pragma unroll
-            for (int j = 0; j < TR; j++)
-                if (j < jmax) A.out[t0 + j][c * cs + lo + kk] = kara_combine(hh[j], ll[j], sum[j], mc.q, mc.rhi, mc.rlo, t40);
+            for (int jj = 0; jj < TR; jj++)
+                if (jj < jmax) A.out[t0 + jj][c * cs + lo + kk] = kara_combine(hh[jj], ll[jj], sum[jj], mc.q, mc.rhi, mc.rlo, t40);
         }
         return;
     }
-    for (int o = w; o < A.nt * 2; o += nw) {
-        const int t = o >> 1, c = o & 1;
-        U128 acc{0, 0};
-        // src index of (t, u) = t + dmax - u  (window starts at delta = t0 - dmax)
-        const u64* sp = sm_src + (size_t)(t + A.dmax) * 2 * BC_T + c * BC_T + kk;
-#pragma unroll 8
-        for (int u = 0; u < A.nu; u++) mac128(acc, sp[-(i64)u * 2 * BC_T], sm_msk[u * BC_T + kk]);
-        A.out[t][c * cs + lo + kk] = barrett128(acc, mc.q, mc.rhi, mc.rlo);
+    // 128-bit path (q >= 2^41): the same sliding window over TR = 4 consecutive t; every 32 products the sums are
+    // folded below q (32 q^2 < 2^127 for q < 2^61)
+    constexpr int TW = 4;
+    const int ngw = (A.nt + TW - 1) / TW;
+    const int dlast = A.nsrc - 1;
+    for (int o = w; o < ngw * 2; o += nw) {
+        const int t0 = (o >> 1) * TW, c = o & 1;
+        U128 acc[TW];
+#pragma unroll
+        for (int jj = 0; jj < TW; jj++) acc[jj] = U128{0, 0};
+        const u64* sp = sm_src + c * BC_T + kk;
+        auto src_at = [&](int d) -> u64 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
+        u64 win[TW];
+#pragma unroll
+        for (int jj = 0; jj < TW; jj++) win[jj] = src_at(t0 + jj + A.dmax);
+        for (int u0 = 0; u0 < A.nu; u0 += TW) {
+#pragma unroll
+            for (int du = 0; du < TW; du++) {
+                const int u = u0 + du;
+                if (u < A.nu) {
+                    if (u > 0) {
+                        const u64 x = src_at(t0 - u + A.dmax);
+#pragma unroll
+                        for (int q = 0; q < TW; q++) if (q == (TW - du) % TW) win[q] = x;
+                    }
+                    const u64 m = sm_msk[u * BC_T + kk];
+#pragma unroll
+                    for (int jj = 0; jj < TW; jj++) mac128(acc[jj], win[(jj - du + TW) % TW], m);
+                }
+            }
+            if (((u0 + TW) & 31) == 0) {
+#pragma unroll
+                for (int jj = 0; jj < TW; jj++) acc[jj] = U128{barrett128(acc[jj], mc.q, mc.rhi, mc.rlo), 0};
+            }
+        }
+        const int jmax = min(TW, A.nt - t0);
+#pragma unroll
+        for (int jj = 0; jj < TW; jj++)
+            if (jj < jmax) A.out[t0 + jj][c * cs + lo + kk] = barrett128(acc[jj], mc.q, mc.rhi, mc.rlo);
     }
 }
 }  // namespace
