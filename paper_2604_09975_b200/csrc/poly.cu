@@ -8,6 +8,7 @@
 // (no dense contraction here: DESIGN.md "Why no tensor cores").
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "ctx.cuh"
@@ -449,19 +450,22 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
         ::"r"(smem_u32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
 }
 
-template <bool NARROW, int ROWS, int MINB>
+template <int ROWS, int MINB>
 __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel(const __grid_constant__ CUtensorMap tmw,
                                                                              const u64* __restrict__ bank, int nbank,
                                                                              const u64* __restrict__ w, int units, i64 wus,
                                                                              u64* __restrict__ acc, i64 accs, int level, int N,
-                                                                             const ModConst* __restrict__ mod, int limb0,
+                                                                             const ModConst* __restrict__ mod, int nw,
                                                                              int nstages) {
     extern __shared__ __align__(128) u64 dm_sm[];
     constexpr int SW = MAC_LANES * ROWS * MAC_T;                 // words per stage
     u64* stg = dm_sm;                                            // [nstages][16 lanes][8 rows][32 coefficients]
     u64* sb = stg + (size_t)nstages * SW;            // bank tile, layout of diag_mac_kernel
     uint64_t* bars = (uint64_t*)(sb + (size_t)nbank * 2 * MAC_T);
-    const int limb = limb0 + blockIdx.y;
+    // ONE launch covers every limb: limbs [0, nw) (q >= 2^41) take the 128-bit path, the others the 20-bit Karatsuba
+    // path, so the ALU-heavy 128-bit CTAs overlap the narrow CTAs' HBM stream instead of running as a second launch
+    const int limb = blockIdx.y;
+    const bool narrow = limb >= nw;
     const int k0 = blockIdx.x * MAC_T;
     const ModConst mc = mod[limb];
     const size_t cs = (size_t)level * N, bs = 2 * cs, pstride = (size_t)level * N;
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // bank tile (read once per CTA; L2-resident across the tiles of one launch)
-    if constexpr (NARROW) {
+    if (narrow) {
         uint2* sn = (uint2*)sb;
         for (int i = tid; i < nbank * 2 * MAC_T; i += blockDim.x) {
             const int uq = i / (2 * MAC_T), r = i % (2 * MAC_T), c = r / MAC_T, kk = r % MAC_T;
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
         const int u = g * MAC_LANES + lane;
         if (u < units) {
             const ulonglong2* xr = (const ulonglong2*)(stg + (size_t)slot * SW + (size_t)lane * ROWS * MAC_T) + kp;
-            if constexpr (NARROW) {
+            if (narrow) {
                 const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * ROWS) * 2 * (MAC_T / 2);
 #pragma unroll
                 for (int t = 0; t < ROWS; t++) {
@@ -552,7 +556,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
             }
             if (c == nch - 1) {
                 u64* o = acc + (size_t)u * accs + (size_t)limb * N + k0 + 2 * kp;
-                if constexpr (NARROW) {
+                if (narrow) {
                     *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
                                                       kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
                     *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
@@ -876,12 +880,9 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         static bool tma_attr = false;
         if (!tma_attr) {
             const int mx = 227 * 1024;
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             tma_attr = true;
         }
         const size_t tsm = (size_t)nst * stage_b + bank_b + (size_t)nst * 8;
@@ -904,17 +905,13 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, (void*)w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             throw EncfError(ENCF_ERR_CUDA, "diag_mac: cuTensorMapEncodeTiled failed");
-        auto launch = [&](auto kw, auto kn) {
-            if (nw > 0)
-                kw<<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
-                                                                       c.d_mod, 0, nst);
-            if (nw < level)
-                kn<<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level,
-                                                                               c.N, c.d_mod, nw, nst);
+        auto launch = [&](auto kern) {
+            kern<<<dim3(tiles, level, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
+                                                                       c.d_mod, nw, nst);
         };
-        if (variant == 1) launch(diag_mac_tma_kernel<false, 8, 1>, diag_mac_tma_kernel<true, 8, 1>);
-        else if (variant == 2) launch(diag_mac_tma_kernel<false, 8, 2>, diag_mac_tma_kernel<true, 8, 2>);
-        else launch(diag_mac_tma_kernel<false, 4, 3>, diag_mac_tma_kernel<true, 4, 3>);
+        if (variant == 1) launch(diag_mac_tma_kernel<8, 1>);
+        else if (variant == 2) launch(diag_mac_tma_kernel<8, 2>);
+        else launch(diag_mac_tma_kernel<4, 3>);
     } else {
         if (nw > 0)
             diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
@@ -924,7 +921,7 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
                                                                                                    accs, level, c.N, c.d_mod, nw);
     }
     c.prof_end(slot, s);
-    c.st_launch += (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // the 128-bit and the narrow launch
+    c.st_launch += nst >= 2 ? 1 : (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // TMA: one launch; register path: 128-bit + narrow
     c.st_bytes += bytes;
     c.st_ptmul += (uint64_t)units * nbank;
 }
@@ -1301,6 +1298,100 @@ __global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl
     u64* out = B.out[r];
     *(ulonglong2*)(out + (size_t)e * N + k) = make_ulonglong2(redc128(A0, q, mc.qinv), redc128(B0, q, mc.qinv));
     *(ulonglong2*)(out + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(A1, q, mc.qinv), redc128(B1, q, mc.qinv));
+}
+
+// ks_psi_kernel with its operands staged by the TMA engine (ENCF_KS_TMA, as ks_inner_tma_kernel): a CTA owns an aligned
+// tile of KT coefficients of one (request, extended limb); for each of the two terms i the Galois source block of ext
+// (every digit) and c0, the pre-masked key tiles and the P-mask tile arrive by cp.async.bulk on one mbarrier per term.
+// Same arithmetic and output words.
+__global__ void __launch_bounds__(TB, 1) ks_psi_tma_kernel(PsiBatch B, int dnum, int nl, int L, LimbMap em, int N, int logN,
+                                                          const ModConst* __restrict__ mod) {
+    extern __shared__ __align__(128) u64 kp_sm[];
+    const int r = blockIdx.x, e = blockIdx.z;
+    const int kb = blockIdx.y * KT;
+    const bool qlimb = e < L;
+    const int per = 3 * dnum + (qlimb ? 2 : 0);          // KT-word blocks per term: dnum x (ext, key0, key1) [+ c0, pm]
+    uint64_t* bars = (uint64_t*)(kp_sm + (size_t)2 * (3 * dnum + 2) * KT);
+    const uint32_t mask2n = 2 * N - 1;
+    auto src_of = [&](int k, uint32_t g) -> int {
+        const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+        return brv((int)((e2 - 1) >> 1), logN);
+    };
+    const u64* __restrict__ ext = B.ext[r];
+    int sb[2];
+#pragma unroll
+    for (int i = 0; i < 2; i++) sb[i] = src_of(kb, B.g[r][i]) & ~(KT - 1);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2; i++) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int i = 0; i < 2; i++) {
+            u64* st = kp_sm + (size_t)i * (3 * dnum + 2) * KT;
+            mbar_arrive_expect_tx(&bars[i], (uint32_t)per * KT * 8);
+            const u64* km = B.key[r][i];
+            for (int j = 0; j < dnum; j++) {
+                const u64* kj = km + (size_t)j * 2 * nl * N;
+                bulk_g2s(st + (3 * j) * KT, ext + ((size_t)j * nl + e) * N + sb[i], KT * 8, &bars[i]);
+                bulk_g2s(st + (3 * j + 1) * KT, kj + (size_t)e * N + kb, KT * 8, &bars[i]);
+                bulk_g2s(st + (3 * j + 2) * KT, kj + ((size_t)nl + e) * N + kb, KT * 8, &bars[i]);
+            }
+            if (qlimb) {
+                bulk_g2s(st + (3 * dnum) * KT, B.c0[r] + (size_t)e * N + sb[i], KT * 8, &bars[i]);
+                bulk_g2s(st + (3 * dnum + 1) * KT, B.mask[r][i] + (size_t)e * N + kb, KT * 8, &bars[i]);
+            }
+        }
+    }
+    __syncthreads();
+    const ModConst mc = mod[em.mod[e]];
+    const u64 q = mc.q;
+    constexpr int PP = KT / 2 / TB;
+    U128 A0[PP], B0[PP], A1[PP], B1[PP];
+#pragma unroll
+    for (int p = 0; p < PP; p++) A0[p] = B0[p] = A1[p] = B1[p] = U128{0, 0};
+#pragma unroll
+    for (int i = 0; i < 2; i++) {
+        const uint32_t g = B.g[r][i];
+        int kl[PP], sl[PP], sw[PP];
+#pragma unroll
+        for (int p = 0; p < PP; p++) {
+            kl[p] = 2 * (threadIdx.x + p * TB);
+            const int src = src_of(kb + kl[p], g);
+            sl[p] = (src & ~1) - sb[i];
+            sw[p] = src & 1;
+        }
+        mbar_wait(&bars[i], 0);
+        const u64* st = kp_sm + (size_t)i * (3 * dnum + 2) * KT;
+        for (int j = 0; j < dnum; j++) {
+#pragma unroll
+            for (int p = 0; p < PP; p++) {
+                ulonglong2 x = *(const ulonglong2*)(st + (3 * j) * KT + sl[p]);
+                if (sw[p]) { u64 t = x.x; x.x = x.y; x.y = t; }
+                const ulonglong2 k0 = *(const ulonglong2*)(st + (3 * j + 1) * KT + kl[p]);
+                const ulonglong2 k1 = *(const ulonglong2*)(st + (3 * j + 2) * KT + kl[p]);
+                mac128(A0[p], x.x, k0.x);
+                mac128(B0[p], x.y, k0.y);
+                mac128(A1[p], x.x, k1.x);
+                mac128(B1[p], x.y, k1.y);
+            }
+        }
+        if (qlimb) {
+#pragma unroll
+            for (int p = 0; p < PP; p++) {
+                ulonglong2 y = *(const ulonglong2*)(st + (3 * dnum) * KT + sl[p]);
+                if (sw[p]) { u64 t = y.x; y.x = y.y; y.y = t; }
+                const ulonglong2 pm = *(const ulonglong2*)(st + (3 * dnum + 1) * KT + kl[p]);
+                mac128(A0[p], y.x, pm.x);
+                mac128(B0[p], y.y, pm.y);
+            }
+        }
+    }
+    u64* out = B.out[r];
+#pragma unroll
+    for (int p = 0; p < PP; p++) {
+        const int k = kb + 2 * (threadIdx.x + p * TB);
+        *(ulonglong2*)(out + (size_t)e * N + k) = make_ulonglong2(redc128(A0[p], q, mc.qinv), redc128(B0[p], q, mc.qinv));
+        *(ulonglong2*)(out + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(A1[p], q, mc.qinv), redc128(B1[p], q, mc.qinv));
+    }
 }
 
 // km[j][c][e][k] = key[j][c][kl(e)][k] (.) mask[e][k] mod q_e (the key's Montgomery factor is kept);
@@ -1756,7 +1847,18 @@ void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key
     const uint64_t bytes = (uint64_t)nreq * (2 * dnum * nl + 2 * 2 * dnum * nl + 2 * L + 2 * L + 2 * nl) * c.N * 8;
     int slot;
     c.prof_begin("ks_psi", s, bytes, slot);
-    ks_psi_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
+    static const bool tma = [] { const char* e = std::getenv("ENCF_KS_TMA"); return !e || std::atoi(e) != 0; }();
+    const size_t sm = (size_t)2 * (3 * dnum + 2) * KT * 8 + 64;
+    if (tma && c.N >= KT && sm <= 227 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            CUDA_TRY(cudaFuncSetAttribute(ks_psi_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            attr = true;
+        }
+        ks_psi_tma_kernel<<<dim3(nreq, c.N / KT, nl), TB, sm, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
+    } else {
+        ks_psi_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
+    }
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
     c.st_ptmul += 2 * (uint64_t)nreq;
@@ -2080,6 +2182,81 @@ void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const*
 namespace {
 constexpr int BC_T = 32;
 
+// One (t group, component) item of the narrow path: b_t = sum_u src[t - u] (.) mask_u for t in [t0, t0 + BC_TR), with the
+// 20-bit Karatsuba split of diag_mac_kernel.  Sliding window: stepping u -> u + 1 shifts the TR source words by one
+// position, so each step loads one new source word and one mask word (register ring indexed (j - u) mod TR, resolved
+// at compile time by unrolling u by TR).  FP = true runs the same split products on the FP64 pipe: pieces < 2^21,
+// products < 2^42, sums of <= 64 products < 2^48 -- exact in doubles, so the words are identical.
+constexpr int BC_TR = 8;
+template <bool FP>
+__device__ __forceinline__ void bc_item(const BcastArgs& A, const uint2* ss, const uint2* sk, int kk, int t0, int c, size_t cs,
+                                        size_t lo, const ModConst& mc, u64 t40) {
+    constexpr int TR = BC_TR;
+    using V = typename std::conditional<FP, double, uint32_t>::type;
+    using Acc = typename std::conditional<FP, double, u64>::type;
+    auto cv = [](uint32_t x) -> V {
+        if constexpr (FP) return __dsub_rn(__hiloint2double(0x43300000, (int)x), 4503599627370496.0);
+        else return x;
+    };
+    Acc hh[TR], ll[TR], sum[TR];
+#pragma unroll
+    for (int jj = 0; jj < TR; jj++) hh[jj] = ll[jj] = sum[jj] = 0;
+    // src word of (t0 + jj, u) = ss[(t0 + jj + dmax - u) * 2 BC_T + c BC_T + kk]; indices past the window only occur for
+    // t >= nt (never stored) -- clamp them into it
+    const uint2* sp = ss + c * BC_T + kk;
+    const int dlast = A.nsrc - 1;
+    auto src_at = [&](int d) -> uint2 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
+    V wh[TR], wl[TR], ws[TR];
+#pragma unroll
+    for (int jj = 0; jj < TR; jj++) {
+        const uint2 x = src_at(t0 + jj + A.dmax);
+        wh[jj] = cv(x.x); wl[jj] = cv(x.y); ws[jj] = FP ? wh[jj] + wl[jj] : cv(x.x + x.y);
+    }
+    for (int u0 = 0; u0 < A.nu; u0 += TR) {
+#pragma unroll
+        for (int du = 0; du < TR; du++) {
+            const int u = u0 + du;
+            if (u < A.nu) {
+                if (u > 0) {   // position 0 of step u enters the slot that held position TR - 1 of step u - 1
+                    const uint2 x = src_at(t0 - u + A.dmax);
+                    const V h = cv(x.x), l = cv(x.y);
+                    const V sv = FP ? h + l : cv(x.x + x.y);
+                    const int sl = (TR - du) % TR;
+#pragma unroll
+                    for (int q = 0; q < TR; q++)
+                        if (q == sl) { wh[q] = h; wl[q] = l; ws[q] = sv; }
+                }
+                const uint2 m = sk[u * BC_T + kk];
+                const V mh = cv(m.x), ml = cv(m.y);
+                const V ms = FP ? mh + ml : cv(m.x + m.y);
+#pragma unroll
+                for (int jj = 0; jj < TR; jj++) {
+                    const int q = (jj - du + TR) % TR;
+                    if constexpr (FP) {
+                        hh[jj] = __fma_rn(wh[q], mh, hh[jj]);
+                        ll[jj] = __fma_rn(wl[q], ml, ll[jj]);
+                        sum[jj] = __fma_rn(ws[q], ms, sum[jj]);
+                    } else {
+                        hh[jj] += (u64)wh[q] * mh;
+                        ll[jj] += (u64)wl[q] * ml;
+                        sum[jj] += (u64)ws[q] * ms;
+                    }
+                }
+            }
+        }
+    }
+    const int jmax = min(TR, A.nt - t0);
+#pragma unroll
+    for (int jj = 0; jj < TR; jj++) {
+        if (jj < jmax) {
+            u64 h, l, sm;
+            if constexpr (FP) { h = (u64)__double2ull_rz(hh[jj]); l = (u64)__double2ull_rz(ll[jj]); sm = (u64)__double2ull_rz(sum[jj]); }
+            else { h = hh[jj]; l = ll[jj]; sm = sum[jj]; }
+            A.out[t0 + jj][c * cs + lo + kk] = kara_combine(h, l, sm, mc.q, mc.rhi, mc.rlo, t40);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, int N, const ModConst* __restrict__ mod) {
     extern __shared__ u64 sb[];                 // [nsrc][2][BC_T] then [nu][BC_T]  (narrow limbs: uint2 {h, l} per word)
     const int limb = blockIdx.y, k0 = blockIdx.x * BC_T;
@@ -2105,56 +2282,14 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         const u64 t40 = (1ull << 40) % mc.q;
         const uint2* ss = (const uint2*)sm_src;
         const uint2* sk = (const uint2*)sm_msk;
-        // register blocking over TR = 8 consecutive t of one component with a SLIDING window: b_t needs src[t - u], so
-        // stepping u -> u + 1 shifts the thread's TR source words by one position -- one new shared-memory word (and
-        // one mask word) per TR products instead of TR + 1 (the window lives in a register ring indexed
-        // (j - u) mod TR, resolved at compile time by unrolling u by TR)
-        constexpr int TR = 8;
-        const int ngrp = (A.nt + TR - 1) / TR;
+        // register blocking over TR = 8 consecutive t of one component with a SLIDING window (bc_item): warps 0-3 of
+        // the CTA run their items on the integer pipe, warps 4-7 on the FP64 pipe, so every SM sub-partition (warp % 4)
+        // keeps both pipes busy
+        const int ngrp = (A.nt + BC_TR - 1) / BC_TR;
+        const bool fpw = (w >> 2) & 1;
         for (int o = w; o < ngrp * 2; o += nw) {
-            const int t0 = (o >> 1) * TR, c = o & 1;
-            u64 hh[TR], ll[TR], sum[TR];
-#pragma unroll
-            for (int jj = 0; jj < TR; jj++) hh[jj] = ll[jj] = sum[jj] = 0;
-            // src word of (t0 + jj, u) = ss[(t0 + jj + dmax - u) * 2 BC_T + c BC_T + kk]; indices past the window only
-            // occur for t >= nt (never stored) -- clamp them into it
-            const uint2* sp = ss + c * BC_T + kk;
-            const int dlast = A.nsrc - 1;
-            auto src_at = [&](int d) -> uint2 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
-            uint32_t wh[TR], wl[TR], ws[TR];
-#pragma unroll
-            for (int jj = 0; jj < TR; jj++) {
-                const uint2 x = src_at(t0 + jj + A.dmax);
-                wh[jj] = x.x; wl[jj] = x.y; ws[jj] = x.x + x.y;
-            }
-            for (int u0 = 0; u0 < A.nu; u0 += TR) {
-#pragma unroll
-                for (int du = 0; du < TR; du++) {
-                    const int u = u0 + du;
-                    if (u < A.nu) {
-                        if (u > 0) {   // position 0 of step u enters the slot that held position TR - 1 of step u - 1
-                            const uint2 x = src_at(t0 - u + A.dmax);
-                            const int sl = (TR - du) % TR;
-#pragma unroll
-                            for (int q = 0; q < TR; q++)
-                                if (q == sl) { wh[q] = x.x; wl[q] = x.y; ws[q] = x.x + x.y; }
-                        }
-                        const uint2 m = sk[u * BC_T + kk];
-                        const uint32_t ms = m.x + m.y;
-#pragma unroll
-                        for (int jj = 0; jj < TR; jj++) {
-                            const int q = (jj - du + TR) % TR;
-                            hh[jj] += (u64)wh[q] * m.x;
-                            ll[jj] += (u64)wl[q] * m.y;
-                            sum[jj] += (u64)ws[q] * ms;
-                        }
-                    }
-                }
-            }
-            const int jmax = min(TR, A.nt - t0);
-#pragma unroll
-            for (int jj = 0; jj < TR; jj++)
-                if (jj < jmax) A.out[t0 + jj][c * cs + lo + kk] = kara_combine(hh[jj], ll[jj], sum[jj], mc.q, mc.rhi, mc.rlo, t40);
+            if (fpw) bc_item<true>(A, ss, sk, kk, (o >> 1) * BC_TR, o & 1, cs, lo, mc, t40);
+            else bc_item<false>(A, ss, sk, kk, (o >> 1) * BC_TR, o & 1, cs, lo, mc, t40);
         }
         return;
     }
