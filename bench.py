@@ -42,9 +42,10 @@ C_QK, BETA = 192, 16
 MODELS = {"layer": dict(name="bert-base-layer", d=768, H=12, dff=3072),
           "qkv": dict(name="bert-base-qkv", d=768, H=12, dff=3072),
           "bert-large-layer": dict(name="bert-large-layer", d=1024, H=16, dff=4096)}
-NTT_TRAFFIC = 1.94e6  # ncu dram__bytes (read + write) per limb transform (fwd cols+rows, 384-limb batch)
-NTT_TRAFFIC_SRC = "profiles/r01_ncu_ntt_fp64_vs_int.txt (ncu --set full, 384-limb forward batch)"
-DIAG_MAC_TRAFFIC_SRC = "profiles/r01_ncu_diag_mac_s4.txt (ncu --set full of the QKV launch)"
+NTT_TRAFFIC = 1.863e6  # ncu dram__bytes (read + write) per limb transform (fwd cols+rows, 384-limb batch)
+NTT_TRAFFIC_SRC = "profiles/r02_ncu_top_kernels.md (ncu --set full, 384-limb forward batch: (344.0 + 371.3) MB / 384)"
+DIAG_MAC_TRAFFIC_SRC = ("profiles/r02_ncu_top_kernels.md (ncu --set full of the QKV launches: narrow 21142.7 + 646.5 MB, "
+                        "128-bit 3020.9 + 93.2 MB)")
 
 
 def parse():
@@ -507,13 +508,13 @@ def run_ours(args):
                              "FP64-path limbs 8 butterflies/clk/SM (8 fp64-pipe ops each), integer-path limbs 2.77/clk/SM "
                              "(fmaheavy-bound), x 148 SMs x sm_max_mhz (DESIGN.md ALU roofline); hbm_floor_frac = the 4 limb-poly "
                              "passes per transform against the measured HBM peak; traffic = ncu dram bytes per limb transform "
-                             "(profiles/r01_summary.md)"},
+                             "(profiles/r02_ncu_top_kernels.md)"},
         "roofline_hbm": {"bound": "hbm", "kernel": "diag_mac", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 4), "traffic": 24.9e9 if args.workload in ("layer", "qkv") else None,
                          "traffic_source": DIAG_MAC_TRAFFIC_SRC,
                          "note": "the HBM-bound plaintext-diagonal MAC: algorithmic bytes per launch (plaintext stream + bank + "
                                  "accumulators) / CUDA-event duration; peak = MEASURED_PEAKS.json hbm_gbs (burst copy); traffic = "
-                                 "ncu dram read+write bytes of the QKV launch (24.8 GB algorithmic; profiles/r01_summary.md)"},
+                                 "ncu dram read+write bytes of the QKV launches (24.8 GB algorithmic; profiles/r02_ncu_top_kernels.md)"},
         "clocks": clk.summary(),
         "e2e": e2e,
         "setup_s": round(layer.setup_s, 1),

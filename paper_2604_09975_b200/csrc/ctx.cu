@@ -45,6 +45,24 @@ static uint8_t* bconv_wbytes(encf_ctx& c, const std::vector<u64>& wf, int na, in
     return d;
 }
 
+// Per-limb iNTT output factors f (u64 + Shoup quotient + FP64 {f, fl(f/q)}): ntt_inverse_scaled(.., NttPost) multiplies
+// its output by them, so the fast base conversion that follows reads [x (Q/q_i)^{-1} N^{-1}]_{q_i} directly.
+static NttPostTab make_post(encf_ctx& c, const std::vector<u64>& f, const std::vector<u64>& q) {
+    NttPostTab t;
+    std::vector<u64> fs(f.size());
+    std::vector<double> fd(2 * f.size());
+    for (size_t i = 0; i < f.size(); i++) {
+        fs[i] = shoup_pre(f[i], q[i]);
+        fd[2 * i] = (double)f[i];
+        fd[2 * i + 1] = (double)f[i] / (double)q[i];
+    }
+    t.f = upload(c, f);
+    t.fsh = upload(c, fs);
+    t.fd = (double*)c.dev_alloc(fd.size() * 8);
+    CUDA_TRY(cudaMemcpy(t.fd, fd.data(), fd.size() * 8, cudaMemcpyHostToDevice));
+    return t;
+}
+
 static int bitrev(int x, int bits) {
     int r = 0;
     for (int i = 0; i < bits; i++) { r = (r << 1) | (x & 1); x >>= 1; }
@@ -188,6 +206,7 @@ static void build(encf_ctx& c, const encf_params* p) {
     c.moddown.assign(c.L + 1, {});
     c.rescale.assign(c.L + 1, {});
     c.mdr.assign(c.L + 1, {});
+    c.modup_post.assign(c.L + 1, {});
     for (int lev = 1; lev <= c.L; lev++) {
         LimbMap ext = c.extmap(lev);
         for (int j = 0; j < c.dnum(lev); j++) {
@@ -223,6 +242,16 @@ static void build(encf_ctx& c, const encf_params* p) {
             }
             c.modup[lev].push_back(t);
         }
+        {   // every q-limb's ModUp input factor (its digit's vfac) for the ModUp iNTT epilogue
+            std::vector<u64> f(lev), q(lev);
+            for (int j = 0; j < c.dnum(lev); j++) {
+                const ModUpTab& t = c.modup[lev][j];
+                std::vector<u64> vf(t.hi - t.lo);
+                CUDA_TRY(cudaMemcpy(vf.data(), t.d_vfac, vf.size() * 8, cudaMemcpyDeviceToHost));
+                for (int a = t.lo; a < t.hi; a++) { f[a] = vf[a - t.lo]; q[a] = c.mods[a]; }
+            }
+            c.modup_post[lev] = make_post(c, f, q);
+        }
         // ModDown: y = fastBConv_{P->Q}([b]_P); out_i = (b_i - y_i) P^{-1} mod q_i, P = P_{K(lev)} (R-KL)
         const int Kl = c.Kof(lev);
         ModDownTab md;
@@ -248,6 +277,7 @@ static void build(encf_ctx& c, const encf_params* p) {
         }
         md.d_vfac = upload(c, vf); md.d_vfac_sh = upload(c, vfs); md.d_wfac = upload(c, wf);
         md.d_wb = bconv_wbytes(c, wf, Kl, lev, std::vector<u64>(c.mods.begin(), c.mods.begin() + lev));
+        md.post = make_post(c, vf, std::vector<u64>(c.mods.begin() + c.L, c.mods.begin() + c.L + Kl));
         md.d_pinv = upload(c, pinv); md.d_pinv_sh = upload(c, pinvs);
         std::vector<u64> pmod(lev);
         for (int i = 0; i < lev; i++) {
@@ -301,6 +331,7 @@ static void build(encf_ctx& c, const encf_params* p) {
             MDRTab mt;
             mt.d_vfac = upload(c, vf); mt.d_vfac_sh = upload(c, vfs); mt.d_wfac = upload(c, wf); mt.d_corr = upload(c, corr);
             mt.d_wb = bconv_wbytes(c, wf, nb, nt, std::vector<u64>(c.mods.begin(), c.mods.begin() + nt));
+            mt.post = make_post(c, vf, bp);
             mt.d_cfix = upload(c, cf); mt.d_csh = upload(c, cs); mt.d_inv = upload(c, inv); mt.d_inv_sh = upload(c, invs);
             c.mdr[lev] = mt;
         }

@@ -40,6 +40,8 @@ struct PolyBatch {
     LimbMap map;
 };
 
+struct NttPostTab { u64* f = nullptr; u64* fsh = nullptr; double* fd = nullptr; };   // per-limb iNTT output factors
+
 struct ModUpTab {         // fast BConv of digit j at level L: digit limbs [lo,hi) -> targets
     int lo, hi;
     LimbMap tgt;          // target modulus ids
@@ -62,11 +64,13 @@ struct ModDownTab {       // P -> Q_L
     u64* d_pl;            // [L]   P mod q_i and its Shoup quotient (extended-basis lift, R-LAZY)
     u64* d_pl_sh;
     uint8_t* d_wb = nullptr;    // d_wfac as the tensor-core byte matrix
+    NttPostTab post;            // vfac as iNTT output factors (the BConv input then arrives pre-scaled)
 };
 
 struct MDRTab {           // merged ModDown + rescale (R-LAZY): basis B' = {q_{L-1}, p_0..p_{K-1}} -> Q_{L-1}
     u64 *d_vfac, *d_vfac_sh, *d_wfac, *d_corr, *d_cfix, *d_csh, *d_inv, *d_inv_sh;
     uint8_t* d_wb = nullptr;    // d_wfac as the tensor-core byte matrix
+    NttPostTab post;            // vfac as iNTT output factors
 };
 
 struct RescaleTab {       // drop q_{L-1}
@@ -112,6 +116,7 @@ struct encf_ctx {
     u64 *d_ninv = nullptr, *d_ninv_sh = nullptr;    // [L+K]
     u64 *d_imag = nullptr, *d_imag_sh = nullptr;    // [L+K]  psi^{N/2} (a 4th root of unity)
     std::vector<std::vector<ModUpTab>> modup;       // [level][digit]
+    std::vector<NttPostTab> modup_post;             // [level]: every q-limb's ModUp vfac (its digit's) as iNTT output factors
     std::vector<ModDownTab> moddown;                // [level]
     std::vector<RescaleTab> rescale;                // [level]
     std::vector<MDRTab> mdr;                        // [level] (level >= 2)
@@ -245,7 +250,11 @@ void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s);
 // apply_ninv = false: returns N x (the coefficients); used only in front of the fast base conversions, whose
 // vfac constants (ModUp / ModDown / merged ModDown+rescale tables) carry the N^{-1}
 // src != nullptr: out-of-place (reads src with b's layout, writes b)
-void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src = nullptr);
+// post != nullptr (with apply_ninv = false): the output is x * post->f[limb] mod q instead of N x (limb = index in b.map)
+struct NttPost { const u64* f; const u64* fsh; const double* fd; };
+// src_stride: polynomial stride of src (default: b.poly_stride)
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src = nullptr,
+                        const NttPost* post = nullptr, i64 src_stride = -1);
 
 // ------------------------------------------------------------------------------------ launchers (poly.cu)
 void k_add(encf_ctx& c, const u64* a, const u64* b, u64* out, int npolys, const LimbMap& m, bool sub, cudaStream_t s);
@@ -307,7 +316,8 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s,
                    const u64* corr = nullptr, const u64* cfix = nullptr, const u64* csh = nullptr,
-                   const uint8_t* wb = nullptr);   // wb: byte matrix of wf for the tensor-core path (bconv_wbytes)
+                   const uint8_t* wb = nullptr,    // wb: byte matrix of wf for the tensor-core path (bconv_wbytes)
+                   bool prescaled = false);        // inputs already x vfac mod q_i (iNTT NttPost): skip the scaling
 void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_stride, size_t words, cudaStream_t s);
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s);
 void k_rescale_finish_batch(encf_ctx& c, const CopyBatch& In, const u64* corr, const CopyBatch& Out, int level, int npolys,

@@ -69,28 +69,40 @@ std::vector<DCt> Ev::alloc_many(int n, int L, int ncomp) {
 u64* Ev::modup_many(const std::vector<const u64*>& polys, const std::vector<uint32_t>& gathers, int L) {
     const int N = c.N, K = c.Kof(L), nl = L + K, dn = c.dnum(L), n = (int)polys.size();
     const size_t Lw = (size_t)L * N;
-    u64* dntt = sc.get(Lw * n);
-    for (int i0 = 0; i0 < n; i0 += CP_BATCH) {
-        int cnt = std::min(CP_BATCH, n - i0);
-        CopyBatch cb;
-        for (int i = 0; i < cnt; i++) { cb.src[i] = polys[i0 + i]; cb.g[i] = gathers.empty() ? 1u : gathers[i0 + i]; }
-        k_gather_copy(c, cb, cnt, dntt + Lw * i0, (i64)Lw, Lw, s);
-    }
-    u64* dco = sc.get(Lw * n);
-    ntt_inverse_scaled(c, PolyBatch{dco, (i64)Lw, n, c.qmap(L)}, false, s, dntt);   // out of place; N^{-1} in the ModUp vfac
     const size_t es = ext_stride(L);
     u64* ext = sc.get(es * n);
     LimbMap em = c.extmap(L);
+    // the inputs' digit limbs (NTT form, Galois-gathered) go straight to their place in ext; the iNTT reads them there
+    // (no staging copy of the whole input)
+    for (int j = 0; j < dn; j++) {
+        const ModUpTab& t = c.modup[L][j];
+        for (int i0 = 0; i0 < n; i0 += CP_BATCH) {
+            int cnt = std::min(CP_BATCH, n - i0);
+            CopyBatch cb;
+            for (int i = 0; i < cnt; i++) {
+                cb.src[i] = polys[i0 + i] + (size_t)t.lo * N;
+                cb.g[i] = gathers.empty() ? 1u : gathers[i0 + i];
+            }
+            k_gather_copy(c, cb, cnt, ext + es * i0 + (size_t)j * nl * N + (size_t)t.lo * N, (i64)es, (size_t)(t.hi - t.lo) * N, s);
+        }
+    }
+    u64* dco = sc.get(Lw * n);
+    for (int j = 0; j < dn; j++) {   // out of place, per digit; the output is x vfac (NttPost), the BConv input
+        const ModUpTab& t = c.modup[L][j];
+        LimbMap m; m.n = t.hi - t.lo;
+        for (int i = 0; i < m.n; i++) m.mod[i] = (unsigned char)(t.lo + i);
+        const NttPost post{c.modup_post[L].f + t.lo, c.modup_post[L].fsh + t.lo, c.modup_post[L].fd + 2 * t.lo};
+        ntt_inverse_scaled(c, PolyBatch{dco + (size_t)t.lo * N, (i64)Lw, n, m}, false, s,
+                           ext + (size_t)j * nl * N + (size_t)t.lo * N, &post, (i64)es);
+    }
     for (int j = 0; j < dn; j++) {
         const ModUpTab& t = c.modup[L][j];
         u64* ej = ext + (size_t)j * nl * N;
-        CUDA_TRY(cudaMemcpy2DAsync(ej + (size_t)t.lo * N, es * 8, dntt + (size_t)t.lo * N, Lw * 8, (size_t)(t.hi - t.lo) * N * 8,
-                                   n, cudaMemcpyDeviceToDevice, s));
         LimbMap im;
         im.n = t.hi - t.lo;
         for (int i = 0; i < im.n; i++) im.mod[i] = (unsigned char)(t.lo + i);
         k_bconv_batch(c, dco + (size_t)t.lo * N, (i64)Lw, im, t.d_vfac, t.d_vfac_sh, t.d_wfac, t.tgt, ej, (i64)es,
-                      t.tgt_pos.data(), n, s, nullptr, nullptr, nullptr, t.d_wb);
+                      t.tgt_pos.data(), n, s, nullptr, nullptr, nullptr, t.d_wb, true);
         if (t.lo > 0) {
             LimbMap m; m.n = t.lo;
             for (int i = 0; i < t.lo; i++) m.mod[i] = em.mod[i];
@@ -132,10 +144,13 @@ void Ev::ks_many(const std::vector<KsReq>& reqs, int L) {
             O.out[i][0] = q.out0; O.out[i][1] = q.out1; O.add[i][0] = q.add0; O.add[i][1] = q.add1;
         }
         k_ks_inner_batch(c, B, n, dn, nl, key_nl, klm, s);
-        ntt_inverse_scaled(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // [b]_P (x N; vfac has N^{-1})
+        {   // [b]_P x vfac (NttPost): the BConv input
+            const NttPost post{md.post.f, md.post.fsh, md.post.fd};
+            ntt_inverse_scaled(c, PolyBatch{acc + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s, nullptr, &post);
+        }
         u64* y = sc.get((size_t)n * 2 * L * N);
         k_bconv_batch(c, acc + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N,
-                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh, md.d_wb);              // rounded: y = centred [b]_P
+                      pos.data(), 2 * n, s, md.d_pmod, md.d_cfix, md.d_csh, md.d_wb, true);        // rounded: y = centred [b]_P
         std::vector<const u64*> esrc(2 * n), eadd(2 * n);
         std::vector<u64*> eout(2 * n);
         for (int i = 0; i < n; i++)
@@ -522,14 +537,17 @@ void Ev::moddown_rescale_many(const std::vector<DCt>& ins, std::vector<DCt>& out
     bm.n = K + 1;
     bm.mod[0] = (unsigned char)(L - 1);
     for (int k = 0; k < K; k++) bm.mod[1 + k] = (unsigned char)(c.L + k);
-    ntt_inverse_scaled(c, PolyBatch{x + (size_t)(L - 1) * N, (i64)nl * N, 2 * n, bm}, false, s);   // vfac has N^{-1}
+    {
+        const NttPost post{c.mdr[L].post.f, c.mdr[L].post.fsh, c.mdr[L].post.fd};   // x vfac: the BConv input
+        ntt_inverse_scaled(c, PolyBatch{x + (size_t)(L - 1) * N, (i64)nl * N, 2 * n, bm}, false, s, nullptr, &post);
+    }
     const MDRTab& t = c.mdr[L];
     LimbMap qm = c.qmap(L - 1);
     std::vector<int> pos(L - 1);
     for (int i = 0; i < L - 1; i++) pos[i] = i;
     u64* y = sc.get((size_t)n * 2 * (L - 1) * N);
     k_bconv_batch(c, x + (size_t)(L - 1) * N, (i64)nl * N, bm, t.d_vfac, t.d_vfac_sh, t.d_wfac, qm, y, (i64)(L - 1) * N,
-                  pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh, t.d_wb);
+                  pos.data(), 2 * n, s, t.d_corr, t.d_cfix, t.d_csh, t.d_wb, true);
     std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
     std::vector<u64*> eout(2 * n);
     for (int i = 0; i < n; i++) {
@@ -559,10 +577,13 @@ void Ev::moddown_many(const std::vector<DCt>& ins, std::vector<DCt>& outs) {
     std::vector<int> pos(L);
     for (int i = 0; i < L; i++) pos[i] = i;
     const ModDownTab& md = c.moddown[L];
-    ntt_inverse_scaled(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s);   // vfac has N^{-1}
+    {
+        const NttPost post{md.post.f, md.post.fsh, md.post.fd};   // x vfac: the BConv input
+        ntt_inverse_scaled(c, PolyBatch{x + (size_t)L * N, (i64)nl * N, 2 * n, pm}, false, s, nullptr, &post);
+    }
     u64* y = sc.get((size_t)n * 2 * L * N);
     k_bconv_batch(c, x + (size_t)L * N, (i64)nl * N, pm, md.d_vfac, md.d_vfac_sh, md.d_wfac, qm, y, (i64)L * N, pos.data(), 2 * n, s,
-                  md.d_pmod, md.d_cfix, md.d_csh, md.d_wb);
+                  md.d_pmod, md.d_cfix, md.d_csh, md.d_wb, true);
     std::vector<const u64*> esrc(2 * n), eadd(2 * n, nullptr);
     std::vector<u64*> eout(2 * n);
     for (int i = 0; i < n; i++) {

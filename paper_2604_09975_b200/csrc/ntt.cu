@@ -20,7 +20,8 @@ constexpr int kTileElems = 4096;   // 32 KB of shared memory per CTA
 struct NttArgs {
     u64* base;
     i64 poly_stride;
-    const u64* src_base;     // inverse only: the first phase reads from here (same layout) -> out-of-place transform
+    const u64* src_base;     // inverse only: the first phase reads from here -> out-of-place transform
+    i64 src_stride;          // polynomial stride of src_base (limb stride N, like base)
     LimbMap map;
     const ModConst* mod;
     const u64* tw;       // psi_brv (fwd) or ipsi_brv (inv): [mods][N]
@@ -39,6 +40,11 @@ struct NttArgs {
     const u64* ninv;
     const u64* ninv_sh;
     int apply_ninv;          // 0: inverse leaves the factor N (the consumer's base-conversion constants absorb N^{-1})
+    // optional inverse epilogue (apply_ninv = 0): out = x * post_f[limb] mod q (batch limb index), canonical -- the fast
+    // base conversion's per-limb input factor [(Q/q_i)^{-1} N^{-1}]_{q_i} applied where the transform writes its output
+    const u64* post_f;
+    const u64* post_fsh;
+    const double* post_fd;   // FP64 path: {f, fl(f / q)} per limb
     int N, logN, s1, s2;
 };
 
@@ -365,6 +371,10 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
                 const u64 ni = a.ninv[mi], nip = a.ninv_sh[mi];
 #pragma unroll
                 for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], ni, nip, ops.q);
+            } else if (a.post_f) {
+                const u64 f = a.post_f[limb], fs = a.post_fsh[limb];
+#pragma unroll
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = mul_shoup(x[k], f, fs, ops.q);
             } else {
 #pragma unroll
                 for (int k = 0; k < GG::E; k++) gc[k * rs] = canon8(x[k], ops.q);   // GS outputs in [0, 4q)
@@ -374,6 +384,10 @@ __device__ __forceinline__ void cols_body(const NttArgs& a, int lines, const Ops
                 const double ni = a.fpc[4 * mi + 2], niq = a.fpc[4 * mi + 3];
 #pragma unroll
                 for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_mulmod(x[k], ni, niq, ops.q), ops.q);
+            } else if (a.post_f) {
+                const double f = a.post_fd[2 * limb], fq = a.post_fd[2 * limb + 1];
+#pragma unroll
+                for (int k = 0; k < GG::E; k++) gc[k * rs] = fp_canon(fp_mulmod(x[k], f, fq, ops.q), ops.q);
             } else {
                 const double qinv = a.fpc[4 * mi + 1];
 #pragma unroll
@@ -411,10 +425,10 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
     const int limb = by;
     const int cmask = (1 << lgc) - 1;
     u64* g0 = a.base + (i64)limb * a.N;
-    auto line_ptr = [&](int ll) -> u64* {
-        return g0 + (i64)((bz << (31 - __clz(lines) - lgc)) + (ll >> lgc)) * a.poly_stride +
-               (i64)((bx << lgc) + (ll & cmask)) * GG::T;
+    auto line_off = [&](int ll, i64 pstride) -> i64 {
+        return (i64)((bz << (31 - __clz(lines) - lgc)) + (ll >> lgc)) * pstride + (i64)((bx << lgc) + (ll & cmask)) * GG::T;
     };
+    auto line_ptr = [&](int ll) -> u64* { return g0 + line_off(ll, a.poly_stride); };
     const int l = threadIdx.x / GG::TPL, j = threadIdx.x % GG::TPL;
     T* line = sm + l * GG::LSP;
     u64* gl = line_ptr(l);
@@ -499,8 +513,7 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
 #pragma unroll
         for (int it = 0; it < GG::E; it++) {
             const int e = threadIdx.x + it * blockDim.x;
-            const u64* lp = line_ptr(e >> LT);
-            if (a.src_base) lp = a.src_base + (lp - a.base);
+            const u64* lp = a.src_base ? a.src_base + (i64)limb * a.N + line_off(e >> LT, a.src_stride) : line_ptr(e >> LT);
             v[it] = __ldcg(lp + (e & (GG::T - 1)));
         }
         if (use_tab) tw_store<LT>(stw, twv);
@@ -765,7 +778,10 @@ NttArgs make_args(encf_ctx& c, const PolyBatch& b, bool inv) {
     a.ninv = c.d_ninv;
     a.ninv_sh = c.d_ninv_sh;
     a.apply_ninv = 1;
+    a.post_f = a.post_fsh = nullptr;
+    a.post_fd = nullptr;
     a.src_base = nullptr;
+    a.src_stride = b.poly_stride;
     a.epi_src = nullptr;
     a.epi_out = nullptr;
     a.epi_add = nullptr;
@@ -819,11 +835,14 @@ void ntt_forward_epi(encf_ctx& c, const PolyBatch& b, const NttEpilogue* epi, cu
 
 void ntt_inverse(encf_ctx& c, const PolyBatch& b, cudaStream_t s) { ntt_inverse_scaled(c, b, true, s); }
 
-void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src) {
+void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaStream_t s, const u64* src, const NttPost* post,
+                        i64 src_stride) {
     if (b.npolys <= 0 || b.map.n <= 0) return;
     NttArgs a = make_args(c, b, true);
     a.apply_ninv = apply_ninv ? 1 : 0;
+    if (post && !apply_ninv) { a.post_f = post->f; a.post_fsh = post->fsh; a.post_fd = post->fd; }
     a.src_base = src;
+    if (src_stride >= 0) a.src_stride = src_stride;
     PhaseCfg A = phase_cfg(c.s1, 1 << c.s2), B = phase_cfg(c.s2, 1 << c.s1);
     int slot;
     c.prof_begin("ntt", s, (uint64_t)b.npolys * b.map.n * c.N * 8 * 4, slot);
@@ -833,7 +852,7 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
         const int np = std::min(cp, b.npolys - p0);
         NttArgs ac = a;
         ac.base = a.base + (i64)p0 * a.poly_stride;
-        if (src) ac.src_base = a.src_base + (i64)p0 * a.poly_stride;
+        if (src) ac.src_base = a.src_base + (i64)p0 * a.src_stride;
         const RowsCfg R = rows_cfg(B, 1 << c.s1, np, b.map.n);
         launch_rows<true>(c.s2, R.grid, B.threads, B.smem, s, ac, B.lines, R.lgc);
         launch_cols<true>(c.s1, dim3(A.blocks, b.map.n, np), A.threads, A.smem, s, ac, A.lines);

@@ -450,22 +450,19 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
         ::"r"(smem_u32(dst)), "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar)) : "memory");
 }
 
-template <int ROWS, int MINB>
+template <bool NARROW, int ROWS, int MINB>
 __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel(const __grid_constant__ CUtensorMap tmw,
                                                                              const u64* __restrict__ bank, int nbank,
                                                                              const u64* __restrict__ w, int units, i64 wus,
                                                                              u64* __restrict__ acc, i64 accs, int level, int N,
-                                                                             const ModConst* __restrict__ mod, int nw,
+                                                                             const ModConst* __restrict__ mod, int limb0,
                                                                              int nstages) {
     extern __shared__ __align__(128) u64 dm_sm[];
     constexpr int SW = MAC_LANES * ROWS * MAC_T;                 // words per stage
     u64* stg = dm_sm;                                            // [nstages][16 lanes][8 rows][32 coefficients]
     u64* sb = stg + (size_t)nstages * SW;            // bank tile, layout of diag_mac_kernel
     uint64_t* bars = (uint64_t*)(sb + (size_t)nbank * 2 * MAC_T);
-    // ONE launch covers every limb: limbs [0, nw) (q >= 2^41) take the 128-bit path, the others the 20-bit Karatsuba
-    // path, so the ALU-heavy 128-bit CTAs overlap the narrow CTAs' HBM stream instead of running as a second launch
-    const int limb = blockIdx.y;
-    const bool narrow = limb >= nw;
+    const int limb = limb0 + blockIdx.y;
     const int k0 = blockIdx.x * MAC_T;
     const ModConst mc = mod[limb];
     const size_t cs = (size_t)level * N, bs = 2 * cs, pstride = (size_t)level * N;
@@ -475,7 +472,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     // bank tile (read once per CTA; L2-resident across the tiles of one launch)
-    if (narrow) {
+    if constexpr (NARROW) {
         uint2* sn = (uint2*)sb;
         for (int i = tid; i < nbank * 2 * MAC_T; i += blockDim.x) {
             const int uq = i / (2 * MAC_T), r = i % (2 * MAC_T), c = r / MAC_T, kk = r % MAC_T;
@@ -517,37 +514,43 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
         const int u = g * MAC_LANES + lane;
         if (u < units) {
             const ulonglong2* xr = (const ulonglong2*)(stg + (size_t)slot * SW + (size_t)lane * ROWS * MAC_T) + kp;
-            if (narrow) {
+            if constexpr (NARROW) {
                 const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * ROWS) * 2 * (MAC_T / 2);
+                auto row = [&](int t) {
+                    const ulonglong2 x = xr[t * (MAC_T / 2)];
+                    const uint32_t ah = (uint32_t)(x.x >> 20), al = (uint32_t)(x.x & 0xFFFFF);
+                    const uint32_t bh = (uint32_t)(x.y >> 20), bl = (uint32_t)(x.y & 0xFFFFF);
+                    const uint32_t as = ah + al, bsum = bh + bl;
+                    const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
+                    const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
+                    h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
+                    h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
+                    h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
+                    h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
+                };
+                if (rows == ROWS) {    // full chunk: no per-row guard in the unrolled body
 #pragma unroll
-                for (int t = 0; t < ROWS; t++) {
-                    if (t < rows) {
-                        const ulonglong2 x = xr[t * (MAC_T / 2)];
-                        const uint32_t ah = (uint32_t)(x.x >> 20), al = (uint32_t)(x.x & 0xFFFFF);
-                        const uint32_t bh = (uint32_t)(x.y >> 20), bl = (uint32_t)(x.y & 0xFFFFF);
-                        const uint32_t as = ah + al, bsum = bh + bl;
-                        const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
-                        const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
-                        h00 += (u64)pp.x * ah; l00 += (u64)pp.y * al; s00 += (u64)(pp.x + pp.y) * as;
-                        h01 += (u64)pp.z * bh; l01 += (u64)pp.w * bl; s01 += (u64)(pp.z + pp.w) * bsum;
-                        h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
-                        h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
-                    }
+                    for (int t = 0; t < ROWS; t++) row(t);
+                } else {
+                    for (int t = 0; t < rows; t++) row(t);
                 }
             } else {
                 const ulonglong2* sbw = (const ulonglong2*)sb;
+                auto row = [&](int t) {
+                    const int uq = c * ROWS + t;
+                    const ulonglong2 x = xr[t * (MAC_T / 2)];
+                    const ulonglong2 b0 = sbw[uq * MAC_T + kp];
+                    const ulonglong2 b1 = sbw[uq * MAC_T + MAC_T / 2 + kp];
+                    mac128(a00, b0.x, x.x);
+                    mac128(a01, b0.y, x.y);
+                    mac128(a10, b1.x, x.x);
+                    mac128(a11, b1.y, x.y);
+                };
+                if (rows == ROWS) {
 #pragma unroll
-                for (int t = 0; t < ROWS; t++) {
-                    if (t < rows) {
-                        const int uq = c * ROWS + t;
-                        const ulonglong2 x = xr[t * (MAC_T / 2)];
-                        const ulonglong2 b0 = sbw[uq * MAC_T + kp];
-                        const ulonglong2 b1 = sbw[uq * MAC_T + MAC_T / 2 + kp];
-                        mac128(a00, b0.x, x.x);
-                        mac128(a01, b0.y, x.y);
-                        mac128(a10, b1.x, x.x);
-                        mac128(a11, b1.y, x.y);
-                    }
+                    for (int t = 0; t < ROWS; t++) row(t);
+                } else {
+                    for (int t = 0; t < rows; t++) row(t);
                 }
                 if ((((c + 1) * ROWS) & 31) == 0) {     // every 32 products (< 32 q^2 <= 2^127 for q < 2^61): fold below q
                     a00 = U128{barrett128(a00, mc.q, mc.rhi, mc.rlo), 0}; a01 = U128{barrett128(a01, mc.q, mc.rhi, mc.rlo), 0};
@@ -556,7 +559,7 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
             }
             if (c == nch - 1) {
                 u64* o = acc + (size_t)u * accs + (size_t)limb * N + k0 + 2 * kp;
-                if (narrow) {
+                if constexpr (NARROW) {
                     *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
                                                       kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
                     *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
@@ -859,7 +862,8 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     c.prof_begin("diag_mac", s, bytes, slot);
     // Path (ENCF_MAC_VARIANT): "tma2" (default) = tensor-map TMA ring of 32 KB stages at 2 CTAs/SM, "tma1" = 32 KB
     // stages at 1 CTA/SM, "tma3" = 16 KB stages at 3 CTAs/SM, "reg" = register double buffer (diag_mac_kernel, 2 CTAs/SM).
-    // Measured on the B200 (BERT layer, profiles/r02_summary.md): tma2 10.3 ms, reg 11.0, tma3 13.2, tma1 14.7.
+    // Measured on the B200 (BERT layer, profiles/r02_summary.md): tma2 10.3 ms, reg 11.0, tma3 13.2, tma1 14.7; one launch
+    // covering the 128-bit and the narrow limbs together (runtime path per CTA, 112 registers) was slower: 12.1 ms.
     // All paths give the same words.
     static const int variant = [] {
         const char* e = std::getenv("ENCF_MAC_VARIANT");
@@ -880,9 +884,12 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         static bool tma_attr = false;
         if (!tma_attr) {
             const int mx = 227 * 1024;
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<false, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+            CUDA_TRY(cudaFuncSetAttribute(diag_mac_tma_kernel<true, 4, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
             tma_attr = true;
         }
         const size_t tsm = (size_t)nst * stage_b + bank_b + (size_t)nst * 8;
@@ -905,13 +912,17 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         if (encode(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT64, 4, (void*)w, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             throw EncfError(ENCF_ERR_CUDA, "diag_mac: cuTensorMapEncodeTiled failed");
-        auto launch = [&](auto kern) {
-            kern<<<dim3(tiles, level, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
-                                                                       c.d_mod, nw, nst);
+        auto launch = [&](auto kw, auto kn) {
+            if (nw > 0)
+                kw<<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
+                                                                       c.d_mod, 0, nst);
+            if (nw < level)
+                kn<<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level,
+                                                                               c.N, c.d_mod, nw, nst);
         };
-        if (variant == 1) launch(diag_mac_tma_kernel<8, 1>);
-        else if (variant == 2) launch(diag_mac_tma_kernel<8, 2>);
-        else launch(diag_mac_tma_kernel<4, 3>);
+        if (variant == 1) launch(diag_mac_tma_kernel<false, 8, 1>, diag_mac_tma_kernel<true, 8, 1>);
+        else if (variant == 2) launch(diag_mac_tma_kernel<false, 8, 2>, diag_mac_tma_kernel<true, 8, 2>);
+        else launch(diag_mac_tma_kernel<false, 4, 3>, diag_mac_tma_kernel<true, 4, 3>);
     } else {
         if (nw > 0)
             diag_mac_kernel<false><<<dim3(tiles, nw, zsplit), MAC_TPR * MAC_LANES, smem, s>>>(bank, nbank, w, units, wus, acc, accs,
@@ -921,7 +932,7 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
                                                                                                    accs, level, c.N, c.d_mod, nw);
     }
     c.prof_end(slot, s);
-    c.st_launch += nst >= 2 ? 1 : (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // TMA: one launch; register path: 128-bit + narrow
+    c.st_launch += (nw > 0 ? 1 : 0) + (nw < level ? 1 : 0);   // the 128-bit and the narrow launch
     c.st_bytes += bytes;
     c.st_ptmul += (uint64_t)units * nbank;
 }
@@ -1104,8 +1115,9 @@ __global__ void __launch_bounds__(TB, KS_MINB) ks_inner_batch_kernel(KsInnerBatc
 // one mbarrier each (up to 72 KB in flight per CTA); the threads then read their permuted pairs from shared memory.
 // Same arithmetic and output words as ks_inner_batch_kernel.
 constexpr int KT = 1024;
-__global__ void __launch_bounds__(TB, 3) ks_inner_tma_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
-                                                             LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
+                                                                    LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
     extern __shared__ __align__(128) u64 kt_sm[];      // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [dnum] mbarriers
     uint64_t* bars = (uint64_t*)(kt_sm + (size_t)dnum * 3 * KT);
     const int r = blockIdx.z, e = blockIdx.y;
@@ -1136,11 +1148,11 @@ __global__ void __launch_bounds__(TB, 3) ks_inner_tma_kernel(KsInnerBatch B, int
     }
     __syncthreads();                                    // barrier initialisation visible to every waiting thread
     const ModConst mc = mod[em.mod[e]];
-    constexpr int PP = KT / 2 / TB;                     // coefficient pairs per thread (2)
+    constexpr int PP = KT / 2 / NT;                     // coefficient pairs per thread
     int kl[PP], sl[PP], sw[PP];
 #pragma unroll
     for (int p = 0; p < PP; p++) {
-        kl[p] = 2 * (threadIdx.x + p * TB);             // local coefficient (even)
+        kl[p] = 2 * (threadIdx.x + p * NT);             // local coefficient (even)
         const int src = src_of(kb + kl[p]);
         sl[p] = (src & ~1) - sb;
         sw[p] = src & 1;
@@ -1304,8 +1316,10 @@ __global__ void __launch_bounds__(TB) ks_psi_kernel(PsiBatch B, int dnum, int nl
 // tile of KT coefficients of one (request, extended limb); for each of the two terms i the Galois source block of ext
 // (every digit) and c0, the pre-masked key tiles and the P-mask tile arrive by cp.async.bulk on one mbarrier per term.
 // Same arithmetic and output words.
-__global__ void __launch_bounds__(TB, 1) ks_psi_tma_kernel(PsiBatch B, int dnum, int nl, int L, LimbMap em, int N, int logN,
-                                                          const ModConst* __restrict__ mod) {
+template <int KTP, int NT>
+__global__ void __launch_bounds__(NT) ks_psi_tma_kernel(PsiBatch B, int dnum, int nl, int L, LimbMap em, int N, int logN,
+                                                       const ModConst* __restrict__ mod) {
+    constexpr int KT = KTP;
     extern __shared__ __align__(128) u64 kp_sm[];
     const int r = blockIdx.x, e = blockIdx.z;
     const int kb = blockIdx.y * KT;
@@ -1344,7 +1358,7 @@ __global__ void __launch_bounds__(TB, 1) ks_psi_tma_kernel(PsiBatch B, int dnum,
     __syncthreads();
     const ModConst mc = mod[em.mod[e]];
     const u64 q = mc.q;
-    constexpr int PP = KT / 2 / TB;
+    constexpr int PP = KT / 2 / NT;
     U128 A0[PP], B0[PP], A1[PP], B1[PP];
 #pragma unroll
     for (int p = 0; p < PP; p++) A0[p] = B0[p] = A1[p] = B1[p] = U128{0, 0};
@@ -1354,7 +1368,7 @@ __global__ void __launch_bounds__(TB, 1) ks_psi_tma_kernel(PsiBatch B, int dnum,
         int kl[PP], sl[PP], sw[PP];
 #pragma unroll
         for (int p = 0; p < PP; p++) {
-            kl[p] = 2 * (threadIdx.x + p * TB);
+            kl[p] = 2 * (threadIdx.x + p * NT);
             const int src = src_of(kb + kl[p], g);
             sl[p] = (src & ~1) - sb[i];
             sw[p] = src & 1;
@@ -1388,7 +1402,7 @@ __global__ void __launch_bounds__(TB, 1) ks_psi_tma_kernel(PsiBatch B, int dnum,
     u64* out = B.out[r];
 #pragma unroll
     for (int p = 0; p < PP; p++) {
-        const int k = kb + 2 * (threadIdx.x + p * TB);
+        const int k = kb + 2 * (threadIdx.x + p * NT);
         *(ulonglong2*)(out + (size_t)e * N + k) = make_ulonglong2(redc128(A0[p], q, mc.qinv), redc128(B0[p], q, mc.qinv));
         *(ulonglong2*)(out + ((size_t)nl + e) * N + k) = make_ulonglong2(redc128(A1[p], q, mc.qinv), redc128(B1[p], q, mc.qinv));
     }
@@ -1502,7 +1516,8 @@ __global__ void __launch_bounds__(TB, 4) bconv_batch_kernel(const u64* __restric
                                                             const u64* __restrict__ wfac, LimbMap om, OutPos op,
                                                             u64* __restrict__ out, i64 out_stride, int N,
                                                             const ModConst* __restrict__ mod, const u64* __restrict__ corr,
-                                                            const u64* __restrict__ cfix, const u64* __restrict__ csh) {
+                                                            const u64* __restrict__ cfix, const u64* __restrict__ csh,
+                                                            int pre) {
     // shared: [NIN][nout] wfac | [nout] corr | [nout] q_t | [nout] qinv_t | [NIN] q_i | vf | vfs | cfix | shift | [nout] pos
     // (uniform constants live in shared memory, not in registers: 4 CTAs/SM instead of 2)
     extern __shared__ u64 sw[];
@@ -1534,7 +1549,7 @@ __global__ void __launch_bounds__(TB, 4) bconv_batch_kernel(const u64* __restric
 #pragma unroll
         for (int i = 0; i < NIN; i++) v[i] = __ldg(in + (size_t)i * N + k);
 #pragma unroll
-        for (int i = 0; i < NIN; i++) v[i] = mul_shoup(v[i], s_in[NIN + i], s_in[2 * NIN + i], s_in[i]);
+        for (int i = 0; i < NIN; i++) v[i] = pre ? v[i] : mul_shoup(v[i], s_in[NIN + i], s_in[2 * NIN + i], s_in[i]);
         u64 r = 0;
         if (corr) {
             u64 fsum = 0;
@@ -1597,7 +1612,7 @@ __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restric
                                                            OutPos op, u64* __restrict__ out, i64 out_stride, int N,
                                                            int npolys, const ModConst* __restrict__ mod,
                                                            const u64* __restrict__ corr, const u64* __restrict__ cfix,
-                                                           const u64* __restrict__ csh) {
+                                                           const u64* __restrict__ csh, int pre) {
     extern __shared__ __align__(1024) uint8_t btc_sm[];
     uint8_t* sA = btc_sm;                                   // [4][128][16]
     uint8_t* sB = btc_sm + BTC_TILE * 64;                   // [4][nb][16]
@@ -1657,7 +1672,7 @@ __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restric
             u64 fsum = 0;
 #pragma unroll
             for (int i = 0; i < NIN; i++) {
-                const u64 v = mul_shoup(nx[i], vf[i], vfs[i], qin[i]);
+                const u64 v = pre ? nx[i] : mul_shoup(nx[i], vf[i], vfs[i], qin[i]);
                 if (CORR) fsum += umulhi(v << cs[i], cf[i]);
                 *(u64*)(sA + (i >> 1) * (BTC_TILE * 16) + tid * 16 + (i & 1) * 8) = v;
             }
@@ -1809,10 +1824,17 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
         const size_t sm = (size_t)dnum * 3 * KT * 8 + 64;
         static bool attr = false;
         if (!attr) {
-            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
             attr = true;
         }
-        ks_inner_tma_kernel<<<dim3(c.N / KT, nl, nreq), TB, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+        // ENCF_KS_TMA_T=128 (default): 4 coefficient pairs per thread, more CTAs (and bytes in flight) per SM
+        // measured (BERT layer): 128 threads x 4 pairs 3.79 ms, 256 threads x 2 pairs 4.61 ms (profiles/r02_summary.md)
+        static const int nt = [] { const char* e = std::getenv("ENCF_KS_TMA_T"); return e ? std::atoi(e) : 128; }();
+        if (nt == 128)
+            ks_inner_tma_kernel<128><<<dim3(c.N / KT, nl, nreq), 128, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+        else
+            ks_inner_tma_kernel<256><<<dim3(c.N / KT, nl, nreq), 256, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
     } else {
         ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
     }
@@ -1848,14 +1870,20 @@ void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key
     int slot;
     c.prof_begin("ks_psi", s, bytes, slot);
     static const bool tma = [] { const char* e = std::getenv("ENCF_KS_TMA"); return !e || std::atoi(e) != 0; }();
-    const size_t sm = (size_t)2 * (3 * dnum + 2) * KT * 8 + 64;
-    if (tma && c.N >= KT && sm <= 227 * 1024) {
+    // tile (ENCF_PSI_TILE): 512 coefficients x 128 threads (default) or 1024 x 256
+    static const int tile = [] { const char* e = std::getenv("ENCF_PSI_TILE"); return e ? std::atoi(e) : 512; }();
+    const size_t sm = (size_t)2 * (3 * dnum + 2) * tile * 8 + 64;
+    if (tma && c.N >= tile && sm <= 227 * 1024) {
         static bool attr = false;
         if (!attr) {
-            CUDA_TRY(cudaFuncSetAttribute(ks_psi_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(ks_psi_tma_kernel<1024, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+            CUDA_TRY(cudaFuncSetAttribute(ks_psi_tma_kernel<512, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
             attr = true;
         }
-        ks_psi_tma_kernel<<<dim3(nreq, c.N / KT, nl), TB, sm, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
+        if (tile == 1024)
+            ks_psi_tma_kernel<1024, 256><<<dim3(nreq, c.N / 1024, nl), 256, sm, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
+        else
+            ks_psi_tma_kernel<512, 128><<<dim3(nreq, c.N / 512, nl), 128, sm, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
     } else {
         ks_psi_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, L, em, c.N, c.logN, c.d_mod);
     }
@@ -1941,7 +1969,8 @@ void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const Out
 
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,
                    const LimbMap& om, u64* out, i64 out_stride, const int* pos, int npolys, cudaStream_t s, const u64* corr,
-                   const u64* cfix, const u64* csh, const uint8_t* wb) {
+                   const u64* cfix, const u64* csh, const uint8_t* wb, bool prescaled) {
+    const int pre = prescaled ? 1 : 0;
     if (im.n > 16 || im.n < 1) throw EncfError(ENCF_ERR_ARG, "bconv: 1..16 input limbs");
     if (c.max_mod >= (1ull << 60) || im.n > 8) throw EncfError(ENCF_ERR_ARG, "bconv: the 30-bit split needs moduli < 2^60 and <= 8 inputs");
     {   // Montgomery bound of the lazy sum: sum_i q_i + (n_in + 1) <= 2^64 (then T < q_t 2^64)
@@ -1971,9 +2000,9 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
         { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
         switch (im.n) {
 #define B(NI) case NI: if (corr) bconv_tc_kernel<NI, true><<<grid, BTC_TILE, smem_tc, s>>>(in, in_stride, im, vf, vfs, wb, nb, tcols, \
-                  om, op, out, out_stride, c.N, npolys, c.d_mod, corr, cfix, csh); \
+                  om, op, out, out_stride, c.N, npolys, c.d_mod, corr, cfix, csh, pre); \
               else bconv_tc_kernel<NI, false><<<grid, BTC_TILE, smem_tc, s>>>(in, in_stride, im, vf, vfs, wb, nb, tcols, om, op, out, \
-                  out_stride, c.N, npolys, c.d_mod, corr, cfix, csh); break;
+                  out_stride, c.N, npolys, c.d_mod, corr, cfix, csh, pre); break;
             B(1) B(2) B(3) B(4) B(5) B(6) B(7) B(8)
 #undef B
         }
@@ -1986,7 +2015,7 @@ void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im,
     dim3 grid((c.N + TB - 1) / TB, npolys);
     { int _slot; c.prof_begin("bconv_batch_kernel", s, 0, _slot);
     switch (im.n) {
-#define B(NI) case NI: bconv_batch_kernel<NI><<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix, csh); break;
+#define B(NI) case NI: bconv_batch_kernel<NI><<<grid, TB, smem, s>>>(in, in_stride, im, vf, vfs, wf, om, op, out, out_stride, c.N, c.d_mod, corr, cfix, csh, pre); break;
         B(1) B(2) B(3) B(4) B(5) B(6) B(7) B(8) B(9) B(10) B(11) B(12) B(13) B(14) B(15) B(16)
 #undef B
     }
