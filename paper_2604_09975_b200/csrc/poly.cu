@@ -1261,6 +1261,126 @@ __global__ void __launch_bounds__(TB) ks_rotsum_kernel(RotSumBatch B, int nterms
     *(ulonglong2*)(acc + ((size_t)nl + e) * N + k) = make_ulonglong2(s10, s11);
 }
 
+// ks_rotsum_kernel with its operands streamed by the TMA engine (ENCF_ROTSUM_TMA=1, off: measured slower): a CTA owns an aligned tile of RKT
+// coefficients of one (request, extended limb); stage (term i, digit j) = the Galois source block of ext (and, for j = 0
+// on q-limbs, of c0) plus the two key tiles, RS_NST stages in flight on an mbarrier ring.  Same arithmetic and words.
+constexpr int RKT = 512, RS_NT = 128, RS_NST = 4;
+__global__ void __launch_bounds__(RS_NT) ks_rotsum_tma_kernel(RotSumBatch B, int nterms, int dnum, int nl, int L, int key_nl,
+                                                              KeyLimb klm, LimbMap em, int N, int logN,
+                                                              const ModConst* __restrict__ mod, const u64* __restrict__ pl,
+                                                              const u64* __restrict__ pl_sh) {
+    extern __shared__ __align__(128) u64 rs_sm[];         // [RS_NST][4][RKT] | [RS_NST] mbarriers
+    uint64_t* bars = (uint64_t*)(rs_sm + (size_t)RS_NST * 4 * RKT);
+    const int r = blockIdx.x, e = blockIdx.z;
+    const int kb = blockIdx.y * RKT;
+    const bool qlimb = e < L;
+    const ModConst mc = mod[em.mod[e]];
+    const u64 q = mc.q;
+    const int kle = klm.kl[e];
+    const u64* __restrict__ ext = B.ext[r];
+    const u64* __restrict__ c0 = B.c0[r];
+    const uint32_t mask2n = 2 * N - 1;
+    auto src_of = [&](int k, uint32_t g) -> int {
+        const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+        return brv((int)((e2 - 1) >> 1), logN);
+    };
+    const int total = nterms * dnum;
+    auto issue = [&](int st) {
+        if (threadIdx.x != 0) return;
+        const int i = st / dnum, j = st % dnum, slot = st % RS_NST;
+        const int sb = src_of(kb, B.g[i]) & ~(RKT - 1);
+        u64* d = rs_sm + (size_t)slot * 4 * RKT;
+        const bool with_c0 = qlimb && j == 0;
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)(with_c0 ? 4 : 3) * RKT * 8);
+        const u64* kj = B.key[i] + (size_t)j * 2 * key_nl * N;
+        bulk_g2s(d, ext + ((size_t)j * nl + e) * N + sb, RKT * 8, &bars[slot]);
+        bulk_g2s(d + RKT, kj + (size_t)kle * N + kb, RKT * 8, &bars[slot]);
+        bulk_g2s(d + 2 * RKT, kj + ((size_t)key_nl + kle) * N + kb, RKT * 8, &bars[slot]);
+        if (with_c0) bulk_g2s(d + 3 * RKT, c0 + (size_t)e * N + sb, RKT * 8, &bars[slot]);
+    };
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RS_NST; i++) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int st = 0; st < RS_NST - 1 && st < total; st++) issue(st);
+    }
+    __syncthreads();
+    constexpr int PP = RKT / 2 / RS_NT;
+    int kl[PP];
+    u64 s00[PP], s01[PP], s10[PP], s11[PP], cs0[PP], cs1[PP];
+    U128 a0[PP], b0[PP], a1[PP], b1[PP];
+#pragma unroll
+    for (int p = 0; p < PP; p++) {
+        kl[p] = 2 * (threadIdx.x + p * RS_NT);
+        s00[p] = s01[p] = s10[p] = s11[p] = 0;
+        a0[p] = b0[p] = a1[p] = b1[p] = U128{0, 0};
+        cs0[p] = cs1[p] = 0;
+        if (qlimb) {
+            const ulonglong2 v = __ldg((const ulonglong2*)(c0 + (size_t)e * N + kb + kl[p]));
+            cs0[p] = v.x; cs1[p] = v.y;
+        }
+    }
+    int cnt = 0;
+    for (int st = 0; st < total; st++) {
+        if (st + RS_NST - 1 < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(st + RS_NST - 1);
+        }
+        const int i = st / dnum, j = st % dnum, slot = st % RS_NST;
+        const uint32_t g = B.g[i];
+        const int sb = src_of(kb, g) & ~(RKT - 1);
+        mbar_wait(&bars[slot], (uint32_t)((st / RS_NST) & 1));
+        const u64* d = rs_sm + (size_t)slot * 4 * RKT;
+        if (cnt + 1 > 8) {      // REDC every <= 8 products (8 q < 2^64)
+#pragma unroll
+            for (int p = 0; p < PP; p++) {
+                s00[p] = add_mod(s00[p], redc128(a0[p], q, mc.qinv), q); s01[p] = add_mod(s01[p], redc128(b0[p], q, mc.qinv), q);
+                s10[p] = add_mod(s10[p], redc128(a1[p], q, mc.qinv), q); s11[p] = add_mod(s11[p], redc128(b1[p], q, mc.qinv), q);
+                a0[p] = b0[p] = a1[p] = b1[p] = U128{0, 0};
+            }
+            cnt = 0;
+        }
+#pragma unroll
+        for (int p = 0; p < PP; p++) {
+            const int src = src_of(kb + kl[p], g);
+            const int sl = (src & ~1) - sb, sw = src & 1;
+            ulonglong2 x = *(const ulonglong2*)(d + sl);
+            if (sw) { u64 t = x.x; x.x = x.y; x.y = t; }
+            const ulonglong2 k0 = *(const ulonglong2*)(d + RKT + kl[p]);
+            const ulonglong2 k1 = *(const ulonglong2*)(d + 2 * RKT + kl[p]);
+            mac128(a0[p], x.x, k0.x);
+            mac128(b0[p], x.y, k0.y);
+            mac128(a1[p], x.x, k1.x);
+            mac128(b1[p], x.y, k1.y);
+            if (qlimb && j == 0) {
+                ulonglong2 y = *(const ulonglong2*)(d + 3 * RKT + sl);
+                if (sw) { u64 t = y.x; y.x = y.y; y.y = t; }
+                cs0[p] = add_mod(cs0[p], y.x, q);
+                cs1[p] = add_mod(cs1[p], y.y, q);
+            }
+        }
+        cnt++;
+        __syncthreads();            // every thread is done with this slot: it may be refilled
+    }
+    u64* accp = B.acc[r];
+#pragma unroll
+    for (int p = 0; p < PP; p++) {
+        u64 v00 = add_mod(s00[p], redc128(a0[p], q, mc.qinv), q), v01 = add_mod(s01[p], redc128(b0[p], q, mc.qinv), q);
+        u64 v10 = add_mod(s10[p], redc128(a1[p], q, mc.qinv), q), v11 = add_mod(s11[p], redc128(b1[p], q, mc.qinv), q);
+        const int k = kb + kl[p];
+        if (qlimb) {
+            const u64 pe = pl[e], pes = pl_sh[e];
+            const ulonglong2 v1 = __ldg((const ulonglong2*)(B.c1[r] + (size_t)e * N + k));
+            v00 = add_mod(v00, mul_shoup(cs0[p], pe, pes, q), q);
+            v01 = add_mod(v01, mul_shoup(cs1[p], pe, pes, q), q);
+            v10 = add_mod(v10, mul_shoup(v1.x, pe, pes, q), q);
+            v11 = add_mod(v11, mul_shoup(v1.y, pe, pes, q), q);
+        }
+        *(ulonglong2*)(accp + (size_t)e * N + k) = make_ulonglong2(v00, v01);
+        *(ulonglong2*)(accp + ((size_t)nl + e) * N + k) = make_ulonglong2(v10, v11);
+    }
+}
+
 // Masked shift Psi^t in the extended basis (DESIGN.md R-LAZY), fused: for request r = blockIdx.x, pair tile
 // blockIdx.y, extended limb e = blockIdx.z,
 //   out_c = sum_{i<2} mask_i (.) ( sum_j sigma_{g_i}(ext_j) key_i[j][c] + [c == 0] P sigma_{g_i}(c0) )
@@ -1853,8 +1973,22 @@ void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dn
     const uint64_t bytes = (uint64_t)nterms * dnum * 2 * nl * c.N * 8 + (uint64_t)nreq * (dnum * nl + 2 * L + 2 * nl) * c.N * 8;
     int slot;
     c.prof_begin("ks_rotsum", s, bytes, slot);
-    ks_rotsum_kernel<<<grid, TB, 0, s>>>(B, nterms, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod, c.moddown[L].d_pl,
-                                         c.moddown[L].d_pl_sh);
+    // ENCF_ROTSUM_TMA=1: the cp.async.bulk ring variant -- measured slower (BERT layer 1.93 -> 3.00 ms: one barrier round
+    // per (term, digit) stage of a 512-coefficient tile), so the register-load kernel is the default
+    static const bool tma = [] { const char* e = std::getenv("ENCF_ROTSUM_TMA"); return e && std::atoi(e) != 0; }();
+    if (tma && c.N >= RKT) {
+        const size_t sm = (size_t)RS_NST * 4 * RKT * 8 + RS_NST * 8;
+        static bool attr = false;
+        if (!attr) {
+            CUDA_TRY(cudaFuncSetAttribute(ks_rotsum_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            attr = true;
+        }
+        ks_rotsum_tma_kernel<<<dim3(nreq, c.N / RKT, nl), RS_NT, sm, s>>>(B, nterms, dnum, nl, L, key_nl, kl, em, c.N, c.logN,
+                                                                          c.d_mod, c.moddown[L].d_pl, c.moddown[L].d_pl_sh);
+    } else {
+        ks_rotsum_kernel<<<grid, TB, 0, s>>>(B, nterms, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod, c.moddown[L].d_pl,
+                                             c.moddown[L].d_pl_sh);
+    }
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
     CUDA_TRY(cudaGetLastError());
@@ -2311,13 +2445,15 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         const u64 t40 = (1ull << 40) % mc.q;
         const uint2* ss = (const uint2*)sm_src;
         const uint2* sk = (const uint2*)sm_msk;
-        // register blocking over TR = 8 consecutive t of one component with a SLIDING window (bc_item): warps 0-3 of
-        // the CTA run their items on the integer pipe, warps 4-7 on the FP64 pipe, so every SM sub-partition (warp % 4)
-        // keeps both pipes busy
+        // register blocking over TR = 8 consecutive t of one component with a SLIDING window (bc_item); every SM
+        // sub-partition (warp % 4) holds warps of both pipes
+        // An integer-pipe item costs ~1.6x an FP64-pipe item (3 half-rate IMAD.WIDE vs ~3.75 full-rate FP64 ops per
+        // product), so FP64 takes ~5/8 of the items: warps 4-7 always, warps 0-3 their second item in every other CTA.
         const int ngrp = (A.nt + BC_TR - 1) / BC_TR;
-        const bool fpw = (w >> 2) & 1;
+        const bool fpw = (w >> 2) & 1, odd_cta = (blockIdx.x + blockIdx.y) & 1;
         for (int o = w; o < ngrp * 2; o += nw) {
-            if (fpw) bc_item<true>(A, ss, sk, kk, (o >> 1) * BC_TR, o & 1, cs, lo, mc, t40);
+            const bool fp = fpw || (!odd_cta && o >= nw);
+            if (fp) bc_item<true>(A, ss, sk, kk, (o >> 1) * BC_TR, o & 1, cs, lo, mc, t40);
             else bc_item<false>(A, ss, sk, kk, (o >> 1) * BC_TR, o & 1, cs, lo, mc, t40);
         }
         return;
