@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="layer", choices=["layer", "qkv", "ks", "gpt2-linear", "bert-large-layer"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pipeline", action="store_true", help="e2e: copies serialised with each step (one graph)")
     ap.add_argument("--no-cpu-baseline", action="store_true", help="skip the oracle timing (A/B kernel experiments only)")
     ap.add_argument("--replicas", action="store_true",
                     help="N > 1: one independent layer per GPU (weak scaling) instead of ONE layer sharded over the N GPUs")
@@ -416,24 +417,37 @@ def run_ours(args):
     # graph's static inputs, the step, D2H of every exported (masked ciphertext, server share) to pinned memory
     e2e = None
     if not args.no_e2e:
-        outs_h = [(torch.empty(m.data.shape, dtype=m.data.dtype, pin_memory=True),
-                   torch.empty(sh.shape, dtype=sh.dtype, pin_memory=True) if sh is not None else None) for m, sh in gstep.outputs]
-        d2h = sum(a.numel() * 8 + (b.numel() * 8 if b is not None else 0) for a, b in outs_h)
+        # two graphs on two static input sets (PipelinedStep): step i+1's H2D and step i's D2H run on side streams
+        # under step i's device work; every copy of every step stays inside the timed region
+        from paper_2604_09975_b200.graphs import PipelinedStep
+        inputs_b = {k: [layer.E.Ciphertext(c.data.clone(), c.n_comp, c.n_limbs, c.scale, c.ntt) for c in v]
+                    for k, v in layer.dev_inputs.items()}
+        pipe = PipelinedStep(layer.step, gstep, inputs_b) if not args.no_pipeline else None
+        def pinned_outs(g):
+            return [(torch.empty(m.data.shape, dtype=m.data.dtype, pin_memory=True),
+                     torch.empty(sh.shape, dtype=sh.dtype, pin_memory=True) if sh is not None else None) for m, sh in g.outputs]
+        outs_h = [pinned_outs(gstep), pinned_outs(pipe.g[1]) if pipe else None]   # per input set
+        d2h = sum(a.numel() * 8 + (b.numel() * 8 if b is not None else 0) for a, b in outs_h[0])
+        host_in = {k: [h[0] for h in v] for k, v in layer.host_inputs.items()}
         torch.cuda.synchronize()
         barrier(ws)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            outs = gstep({k: [h[0] for h in v] for k, v in layer.host_inputs.items()})
-            for (m, sh), (hm, hs) in zip(outs, outs_h):
-                hm.copy_(m.data, non_blocking=True)
-                if sh is not None:
-                    hs.copy_(sh, non_blocking=True)
+        if pipe:
+            pipe.run(host_in, outs_h, args.steps)
+        else:
+            for _ in range(args.steps):
+                outs = gstep(host_in)
+                for (m, sh), (hm, hs) in zip(outs, outs_h[0]):
+                    hm.copy_(m.data, non_blocking=True)
+                    if sh is not None:
+                        hs.copy_(sh, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
         e2e = {"value": round(e_ms / ws, 3), "unit": "ms/layer", "h2d_bytes_per_step": layer.h2d_bytes, "d2h_bytes_per_step": d2h,
-               "path": "GraphedStep: H2D(pinned) -> graph replay -> D2H(pinned), per step"}
+               "path": ("PipelinedStep: two CUDA graphs on two input sets; H2D(pinned) of step i+1 and D2H(pinned) of step i "
+                        "on side streams under step i" if pipe else "GraphedStep: H2D(pinned) -> graph replay -> D2H(pinned), per step")}
     if rank != 0:
         return
     import json as _j

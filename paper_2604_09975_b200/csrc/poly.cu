@@ -480,9 +480,12 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
             sn[i] = make_uint2((uint32_t)(x >> 20), (uint32_t)(x & 0xFFFFF));
         }
     } else {
+        // 128-bit limbs (q < 2^60): bank words pre-split at 30 bits, {h, l} per word (see the consumer)
+        uint2* sn = (uint2*)sb;
         for (int i = tid; i < nbank * 2 * MAC_T; i += blockDim.x) {
             const int uq = i / (2 * MAC_T), r = i % (2 * MAC_T), c = r / MAC_T, kk = r % MAC_T;
-            sb[i] = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+            const u64 x = bank[(size_t)uq * bs + c * cs + (size_t)limb * N + k0 + kk];
+            sn[i] = make_uint2((uint32_t)(x >> 30), (uint32_t)(x & 0x3FFFFFFFu));
         }
     }
     __syncthreads();
@@ -535,16 +538,22 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                     for (int t = 0; t < rows; t++) row(t);
                 }
             } else {
-                const ulonglong2* sbw = (const ulonglong2*)sb;
+                // 30-bit split: x = xh 2^30 + xl, b = bh 2^30 + bl (q < 2^60), per product 4 IMAD.WIDE.U32 into 64-bit
+                // sums hh, md (= xh bl + xl bh), ll instead of a 64 x 64 -> 128 multiply-add; <= ROWS = 8 rows per
+                // chunk keep md < 16 (2^30 - 1)^2 < 2^64, and each chunk folds hh 2^60 + md 2^30 + ll into the 128-bit sum
+                const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * ROWS) * 2 * (MAC_T / 2);
+                u64 hh00 = 0, md00 = 0, ll00 = 0, hh01 = 0, md01 = 0, ll01 = 0, hh10 = 0, md10 = 0, ll10 = 0, hh11 = 0, md11 = 0,
+                    ll11 = 0;
                 auto row = [&](int t) {
-                    const int uq = c * ROWS + t;
                     const ulonglong2 x = xr[t * (MAC_T / 2)];
-                    const ulonglong2 b0 = sbw[uq * MAC_T + kp];
-                    const ulonglong2 b1 = sbw[uq * MAC_T + MAC_T / 2 + kp];
-                    mac128(a00, b0.x, x.x);
-                    mac128(a01, b0.y, x.y);
-                    mac128(a10, b1.x, x.x);
-                    mac128(a11, b1.y, x.y);
+                    const uint32_t ah = (uint32_t)(x.x >> 30), al = (uint32_t)(x.x & 0x3FFFFFFFu);
+                    const uint32_t bh = (uint32_t)(x.y >> 30), bl = (uint32_t)(x.y & 0x3FFFFFFFu);
+                    const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
+                    const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
+                    hh00 += (u64)pp.x * ah; md00 += (u64)pp.x * al + (u64)pp.y * ah; ll00 += (u64)pp.y * al;
+                    hh01 += (u64)pp.z * bh; md01 += (u64)pp.z * bl + (u64)pp.w * bh; ll01 += (u64)pp.w * bl;
+                    hh10 += (u64)rr.x * ah; md10 += (u64)rr.x * al + (u64)rr.y * ah; ll10 += (u64)rr.y * al;
+                    hh11 += (u64)rr.z * bh; md11 += (u64)rr.z * bl + (u64)rr.w * bh; ll11 += (u64)rr.w * bl;
                 };
                 if (rows == ROWS) {
 #pragma unroll
@@ -552,6 +561,15 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                 } else {
                     for (int t = 0; t < rows; t++) row(t);
                 }
+                auto fold = [](U128& a, u64 hh, u64 md, u64 ll) {
+                    add128(a, ll);
+                    add128(a, md << 30);
+                    a.hi += md >> 34;
+                    add128(a, hh << 60);
+                    a.hi += hh >> 4;
+                };
+                fold(a00, hh00, md00, ll00); fold(a01, hh01, md01, ll01);
+                fold(a10, hh10, md10, ll10); fold(a11, hh11, md11, ll11);
                 if ((((c + 1) * ROWS) & 31) == 0) {     // every 32 products (< 32 q^2 <= 2^127 for q < 2^61): fold below q
                     a00 = U128{barrett128(a00, mc.q, mc.rhi, mc.rlo), 0}; a01 = U128{barrett128(a01, mc.q, mc.rhi, mc.rlo), 0};
                     a10 = U128{barrett128(a10, mc.q, mc.rhi, mc.rlo), 0}; a11 = U128{barrett128(a11, mc.q, mc.rhi, mc.rlo), 0};
@@ -878,7 +896,8 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
     const int rows = variant == 3 ? 4 : 8;
     const size_t stage_b = (size_t)MAC_LANES * rows * MAC_T * 8;
     const size_t cap = variant == 1 ? 227 * 1024 : variant == 2 ? 113 * 1024 : 75 * 1024;
-    const int nst = variant && bank_b + 2 * stage_b + 64 <= cap
+    // the TMA kernel's 128-bit limbs use a 30-bit split (q < 2^60); larger moduli take the register path
+    const int nst = variant && c.max_mod < (1ull << 60) && bank_b + 2 * stage_b + 64 <= cap
                         ? (int)std::min<size_t>(DM_MAX_STAGES, (cap - bank_b - 64) / stage_b) : 0;
     if (nst >= 2) {
         static bool tma_attr = false;
@@ -2433,11 +2452,11 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         int d = i / (2 * BC_T), r = i % (2 * BC_T);
         int c = r / BC_T, kk = r % BC_T;
         const u64 x = A.src[d][c * cs + lo + kk];
-        sm_src[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : x;
+        sm_src[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : ((x >> 30) | ((x & 0x3FFFFFFFull) << 32));
     }
     for (int i = threadIdx.x; i < A.nu * BC_T; i += blockDim.x) {
         const u64 x = A.mask[i / BC_T][lo + i % BC_T];
-        sm_msk[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : x;
+        sm_msk[i] = narrow ? ((x >> 20) | ((x & 0xFFFFF) << 32)) : ((x >> 30) | ((x & 0x3FFFFFFFull) << 32));
     }
     __syncthreads();
     const int kk = threadIdx.x % BC_T, w = threadIdx.x / BC_T, nw = blockDim.x / BC_T;
@@ -2458,19 +2477,23 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
         }
         return;
     }
-    // 128-bit path (q >= 2^41): the same sliding window over TR = 4 consecutive t; every 32 products the sums are
-    // folded below q (32 q^2 < 2^127 for q < 2^61)
+    // 128-bit path (2^41 <= q < 2^60): the same sliding window over TW = 4 consecutive t, words split at 30 bits
+    // ({h, l} in shared memory): per product 4 IMAD.WIDE.U32 into 64-bit sums hh, md (= xh ml + xl mh), ll; every 8 u
+    // (md < 16 (2^30 - 1)^2 < 2^64) they fold into a 128-bit sum, reduced below q every 32 u (32 q^2 < 2^127)
     constexpr int TW = 4;
     const int ngw = (A.nt + TW - 1) / TW;
     const int dlast = A.nsrc - 1;
+    const uint2* ss = (const uint2*)sm_src;
+    const uint2* sk = (const uint2*)sm_msk;
     for (int o = w; o < ngw * 2; o += nw) {
         const int t0 = (o >> 1) * TW, c = o & 1;
         U128 acc[TW];
+        u64 hh[TW], md[TW], ll[TW];
 #pragma unroll
-        for (int jj = 0; jj < TW; jj++) acc[jj] = U128{0, 0};
-        const u64* sp = sm_src + c * BC_T + kk;
-        auto src_at = [&](int d) -> u64 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
-        u64 win[TW];
+        for (int jj = 0; jj < TW; jj++) { acc[jj] = U128{0, 0}; hh[jj] = md[jj] = ll[jj] = 0; }
+        const uint2* sp = ss + c * BC_T + kk;
+        auto src_at = [&](int d) -> uint2 { return sp[(size_t)min(d, dlast) * 2 * BC_T]; };
+        uint2 win[TW];
 #pragma unroll
         for (int jj = 0; jj < TW; jj++) win[jj] = src_at(t0 + jj + A.dmax);
         for (int u0 = 0; u0 < A.nu; u0 += TW) {
@@ -2479,13 +2502,29 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
                 const int u = u0 + du;
                 if (u < A.nu) {
                     if (u > 0) {
-                        const u64 x = src_at(t0 - u + A.dmax);
+                        const uint2 x = src_at(t0 - u + A.dmax);
 #pragma unroll
                         for (int q = 0; q < TW; q++) if (q == (TW - du) % TW) win[q] = x;
                     }
-                    const u64 m = sm_msk[u * BC_T + kk];
+                    const uint2 m = sk[u * BC_T + kk];
 #pragma unroll
-                    for (int jj = 0; jj < TW; jj++) mac128(acc[jj], win[(jj - du + TW) % TW], m);
+                    for (int jj = 0; jj < TW; jj++) {
+                        const uint2 x = win[(jj - du + TW) % TW];
+                        hh[jj] += (u64)x.x * m.x;
+                        md[jj] += (u64)x.x * m.y + (u64)x.y * m.x;
+                        ll[jj] += (u64)x.y * m.y;
+                    }
+                }
+            }
+            if (((u0 + TW) & 7) == 0 || u0 + TW >= A.nu) {
+#pragma unroll
+                for (int jj = 0; jj < TW; jj++) {
+                    add128(acc[jj], ll[jj]);
+                    add128(acc[jj], md[jj] << 30);
+                    acc[jj].hi += md[jj] >> 34;
+                    add128(acc[jj], hh[jj] << 60);
+                    acc[jj].hi += hh[jj] >> 4;
+                    hh[jj] = md[jj] = ll[jj] = 0;
                 }
             }
             if (((u0 + TW) & 31) == 0) {
@@ -2502,6 +2541,7 @@ __global__ void __launch_bounds__(256) bcast_mac_kernel(BcastArgs A, int level, 
 }  // namespace
 
 void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s) {
+    if (c.max_mod >= (1ull << 60)) throw EncfError(ENCF_ERR_ARG, "bcast_mac: the 30-bit split needs moduli < 2^60");
     const size_t smem = ((size_t)A.nsrc * 2 + A.nu) * BC_T * sizeof(u64);
     static bool attr = false;
     if (!attr) {

@@ -15,7 +15,7 @@ if not torch.cuda.is_available():
     pytest.skip("needs a CUDA device", allow_module_level=True)
 
 from paper_2604_09975_b200 import encf as E  # noqa: E402
-from paper_2604_09975_b200.graphs import GraphedStep  # noqa: E402
+from paper_2604_09975_b200.graphs import GraphedStep, PipelinedStep  # noqa: E402
 from tests.gpu_util import assert_ct_equal, dev_ct, weights_tensor  # noqa: E402
 
 P13 = O.Params("P13")
@@ -75,6 +75,19 @@ def test_graph_replay_projection_attention_export():
     for (a, b), (ea, eb) in zip(out1, eager1):
         assert torch.equal(a, ea)
         assert (b is None) or torch.equal(b, eb)
+    # the pipelined e2e path (bench.py): two graphs on two input sets, copies on side streams; after 4 steps both
+    # sets' host copies hold exactly the eager words
+    db = {k: [E.Ciphertext(c.data.clone(), c.n_comp, c.n_limbs, c.scale, c.ntt) for c in v] for k, v in d0.items()}
+    pipe = PipelinedStep(step, g, db)
+    pin = [[(torch.empty(a.shape, dtype=a.dtype, pin_memory=True),
+             torch.empty(b.shape, dtype=b.dtype, pin_memory=True) if b is not None else None) for a, b in gg.outputs]
+           for gg in pipe.g]
+    pipe.run(host, pin, 4)
+    torch.cuda.synchronize()
+    for hs in pin:
+        for (a, b), (ea, eb) in zip(hs, eager1):
+            assert torch.equal(a, ea.cpu())
+            assert (b is None) or torch.equal(b, eb.cpu())
 
 
 def test_graph_replays_draw_fresh_export_masks():
