@@ -451,19 +451,6 @@ __device__ __forceinline__ void rows_body(const NttArgs& a, int lines, int lgc, 
     if (!INV) {
 #pragma unroll
         for (int k = 0; k < GG::E; k++) x[k] = ld_val(__ldcg(gl + j + GG::TPL * k), ops, false);
-        if (a.epi_out) {
-            // fused ModDown / rescale finish: pull this CTA's epilogue operands (src, add) into L2 while the butterflies
-            // run, so the epilogue's loads hit L2 (one 128-byte line per thread per operand)
-            const int lgp = 31 - __clz(lines) - lgc;
-            for (int e = threadIdx.x * 16; e < tot; e += blockDim.x * 16) {
-                const int ll = e >> LT;
-                const int p = (bz << lgp) + (ll >> lgc);
-                const size_t off = (size_t)limb * a.N + (size_t)(((bx << lgc) + (ll & cmask)) * GG::T + (e & (GG::T - 1)));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(a.epi_src[p] + off));
-                const u64* ad = a.epi_add[p];
-                if (ad) asm volatile("prefetch.global.L2 [%0];" ::"l"(ad + off));
-            }
-        }
         if (use_tab) { tw_store<LT>(stw, twv); __syncthreads(); }
         rA(std::false_type{});
         sm_put_a<LT>(line, j, x);
