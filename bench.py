@@ -432,22 +432,24 @@ def run_ours(args):
         torch.cuda.synchronize()
         barrier(ws)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        if pipe:
-            pipe.run(host_in, outs_h, args.steps)
-        else:
-            for _ in range(args.steps):
-                outs = gstep(host_in)
-                for (m, sh), (hm, hs) in zip(outs, outs_h[0]):
-                    hm.copy_(m.data, non_blocking=True)
-                    if sh is not None:
-                        hs.copy_(sh, non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        with Clocks(local) as clk_e2e:
+            e0.record(stream)
+            if pipe:
+                pipe.run(host_in, outs_h, args.steps)
+            else:
+                for _ in range(args.steps):
+                    outs = gstep(host_in)
+                    for (m, sh), (hm, hs) in zip(outs, outs_h[0]):
+                        hm.copy_(m.data, non_blocking=True)
+                        if sh is not None:
+                            hs.copy_(sh, non_blocking=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
         e_ms = max_over_ranks(e0.elapsed_time(e1), ws) / args.steps
         e2e = {"value": round(e_ms / ws, 3), "unit": "ms/layer", "h2d_bytes_per_step": layer.h2d_bytes, "d2h_bytes_per_step": d2h,
                "path": ("PipelinedStep: two CUDA graphs on two input sets; H2D(pinned) of step i+1 and D2H(pinned) of step i "
-                        "on side streams under step i" if pipe else "GraphedStep: H2D(pinned) -> graph replay -> D2H(pinned), per step")}
+                        "on side streams under step i" if pipe else "GraphedStep: H2D(pinned) -> graph replay -> D2H(pinned), per step"),
+               "clocks": clk_e2e.summary()}
     if rank != 0:
         return
     import json as _j

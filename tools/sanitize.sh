@@ -14,4 +14,4 @@ echo "racecheck rc=$?" >> gpurun_out/sanitizer_racecheck.log
 timeout 900 $CS --tool synccheck --target-processes all --print-limit 50 --error-exitcode 9 \
     python -m pytest tests/test_gpu_parity.py -q -k "projection_config1 or score_and_export" > gpurun_out/sanitizer_synccheck.log 2>&1
 echo "synccheck rc=$?" >> gpurun_out/sanitizer_synccheck.log
-tail -3 gpurun_out/sanitizer_*.log
+for f in gpurun_out/sanitizer_*.log; do tail -n 3 "$f"; done
