@@ -478,6 +478,8 @@ encf_status encf_mask_clear(encf_ctx* c) {
     c->masks.clear();
     for (auto& kv : c->kmasks) cudaFree(kv.second);
     c->kmasks.clear();
+    for (auto& kv : c->bhat) cudaFree(kv.second);   // keyed by mask pointers: stale once the masks are gone
+    c->bhat.clear();
     return ENCF_OK;
 }
 

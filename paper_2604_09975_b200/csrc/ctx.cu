@@ -387,6 +387,7 @@ encf_status ctx_destroy_impl(encf_ctx* c) {
     cudaDeviceSynchronize();
     for (auto& kv : c->masks) cudaFree(kv.second);
     for (auto& kv : c->kmasks) cudaFree(kv.second);
+    for (auto& kv : c->bhat) cudaFree(kv.second);
     for (void* p : c->allocations) cudaFree(p);
     for (void* p : c->pinned) cudaFreeHost(p);
     delete c;

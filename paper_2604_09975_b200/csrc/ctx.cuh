@@ -124,6 +124,7 @@ struct encf_ctx {
     std::mutex mu;
     std::map<MaskKey, u64*> masks;      // NTT-form mask plaintexts [level][N]
     std::map<KMKey, u64*> kmasks;       // pre-masked keys (key (.) mask, Montgomery) + P (.) mask, per (keys, g, mask)
+    std::map<std::vector<const u64*>, u64*> bhat;   // value-kernel mask spectra (bcast_ntt_table): key = masks + level
     std::vector<int> rot_group;         // 5^j mod 2N (host, for encode)
     int* d_rot_group = nullptr;
     // live kernel timing (encf_profile_*): CUDA events recorded around selected launches
@@ -329,6 +330,10 @@ void k_lift_add(encf_ctx& c, const CopyBatch& dst, const CopyBatch& src, int n, 
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s);
 void k_bcast_mac(encf_ctx& c, const BcastArgs& A, int level, cudaStream_t s);
+// the same outputs through negacyclic 128-point transforms along the window (ntt.cu; needs nsrc <= 128): the masks'
+// spectrum table (cached per mask set and level) and the convolution launch
+const u64* bcast_ntt_table(encf_ctx& c, const u64* const* masks, int nu, int level, cudaStream_t s);
+void k_bcast_ntt(encf_ctx& c, const BcastArgs& A, const u64* bhat, int level, cudaStream_t s);
 void k_ring2field(encf_ctx& c, const u64* mp, u64* out, int L, const R2F& off, cudaStream_t s);
 void k_field2ring(encf_ctx& c, const u64* sh, u64* out, int ell, cudaStream_t s);
 void k_decode_limb0(encf_ctx& c, const u64* coeff_limb0, double scale, double* d_re, double* d_im, cudaStream_t s);

@@ -6,6 +6,7 @@
 // The schedules are exactly those of oracle/kernels.py (readings in DESIGN.md);
 // independent ciphertexts (blocks, t, bank offsets) are processed in lockstep so that every launch
 // covers all of them.  The parity tests compare every limb of every output.
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include "encformer.cuh"
@@ -564,6 +565,10 @@ void value_partial_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& 
     int ntot = 0;
     for (int i = 0; i < nb; i++) ntot += tb[i] - ta[i];
     std::vector<DCt> by = ev.alloc_many(ntot, Lp);
+    // the Toeplitz MAC as negacyclic 128-point convolutions along the window (k_bcast_ntt, same words);
+    // ENCF_BCAST_DIRECT=1 keeps the direct sliding-window MAC (bcast_mac_kernel) -- the variant parity tests run both
+    static const bool direct = std::getenv("ENCF_BCAST_DIRECT") != nullptr;
+    const u64* bhat = direct ? nullptr : bcast_ntt_table(ev.c, nmask.data(), a.d_h, Lp, ev.s);
     for (int i = 0, k0 = 0; i < nb; i++) {
         for (int t0 = ta[i]; t0 < tb[i]; t0 += 64) {
             BcastArgs A;
@@ -578,7 +583,8 @@ void value_partial_run(Ev& ev, const encf_attn_plan& a, const std::vector<DCt>& 
                 o.scale = ps[blocks[i]].scale * ev.mask_scale(Lp);
                 A.out[t] = o.d;
             }
-            k_bcast_mac(ev.c, A, Lp, ev.s);
+            if (bhat) k_bcast_ntt(ev.c, A, bhat, Lp, ev.s);
+            else k_bcast_mac(ev.c, A, Lp, ev.s);
         }
         k0 += tb[i] - ta[i];
     }

@@ -870,3 +870,182 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
     c.st_bytes += (uint64_t)b.npolys * b.map.n * c.N * 8 * 4;
     CUDA_TRY(cudaGetLastError());
 }
+
+// =============================================================================================
+// Value-kernel Toeplitz MAC (C8 step 4) as a negacyclic 128-point convolution along the window index.
+// For one coefficient k (limb, component) the broadcast MAC computes b_{t0+t} = sum_{u < nu} src[t + dmax - u] n_u
+// (t < nt, dmax = nu - 1): with A(X) = sum_{j < nsrc} src[j] X^j and B(X) = sum_{u < nu} n_u X^u this is the
+// coefficient of X^{t + dmax} in A B.  Modulo X^128 + 1 a term of degree r + 128 would alias onto r; the largest degree
+// is nsrc - 1 + nu - 1 < 128 + dmax whenever nsrc <= 128, so every wanted coefficient (r = t + dmax < 128) is EXACT in
+// the negacyclic product, which the ring's own transform computes: the first 128 entries of the N-point merged twiddle
+// tables ARE the 128-point ones (psi^{brv_16(i)} = (psi^{N/64})^{brv_7(i)} for i < 128).  Per coefficient: forward
+// NTT-128 of the window (CT, bit-reversed spectrum), x B^ (the masks' spectrum times 128^{-1}, precomputed once per mask
+// set: bcast_ntt_table), inverse NTT-128 (GS) -> 896 butterflies + 128 products instead of nu nt = 4096 MAC terms.
+// The result is the same residue as the direct sum, canonical, so the words are identical to bcast_mac_kernel's.
+// A CTA holds 32 coefficients (lines) x 128 window words; 8 threads per line (Geo<7>: E = 16 values per thread).
+namespace {
+
+constexpr int TZ_LINES = 32;
+#ifndef TZ_MINB
+#define TZ_MINB 3   // 4 CTAs/SM (64 registers) spills ~230 bytes
+#endif
+
+struct TzArgs {
+    const u64* src[128];       // window j (nullptr / j >= nsrc: zero)
+    u64* out[64];              // b_{t0 + t}
+    const u64* bhat;           // [level][128][N]: spectrum index e (bit-reversed order) of the masks, x 128^{-1}
+    u64* bhat_out;             // prep mode: written instead of out
+    u64 fac[MAX_LIMBS];        // prep mode: 128^{-1} (FP64-path limbs) or 128^{-1} 2^64 (integer limbs: Montgomery form)
+    i64 cs;                    // component stride of src / out (words)
+    int nsrc, nt, dmax;
+};
+
+template <bool PREP, class Ops>
+__device__ __forceinline__ void tz_body(const TzArgs& a, const Ops& ops, const typename Ops::TW* tw, const typename Ops::TW* itw,
+                                        const ModConst& mc, double qinv, int limb, int comp, int k0, int N) {
+    using GG = Geo<7>;
+    using T = typename Ops::T;
+    extern __shared__ u64 sm_raw[];
+    T* sm = reinterpret_cast<T*>(sm_raw);
+    const int l = threadIdx.x & (TZ_LINES - 1), j = threadIdx.x >> 5;
+    T* line = sm + l * GG::LSP;
+    const size_t off = (size_t)comp * a.cs + (size_t)limb * N + k0 + l;
+    T x[GG::E];
+    {
+        u64 v[GG::E];
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) {
+            const int e = j + GG::TPL * k;
+            v[k] = e < a.nsrc ? __ldcs(a.src[e] + off) : 0ull;
+        }
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) x[k] = ld_val(v[k], ops, true);
+    }
+    round_a<7, false, Ops>(x, 0, 0, tw, ops);
+    sm_put_a<7>(line, j, x);
+    __syncthreads();
+    sm_get_b<7>(line, j, x);
+    round_b<7, false, Ops>(x, j, 0, 0, tw, ops);
+    constexpr int EB = GG::EB, G = GG::G, KB = 1 << EB;
+    if constexpr (PREP) {
+        const u64 f = a.fac[limb];
+#pragma unroll
+        for (int g = 0; g < G; g++)
+#pragma unroll
+            for (int k = 0; k < KB; k++) {
+                const int e = ((j * G + g) << EB) + k;
+                u64 w;
+                if constexpr (std::is_same<T, u64>::value) w = canon8(x[g * KB + k], mc.q);
+                else w = fp_canon(fp_center(x[g * KB + k], ops.q, qinv), ops.q);
+                a.bhat_out[((size_t)limb * 128 + e) * N + k0 + l] = mulmod_barrett(w, f, mc.q, mc.rhi, mc.rlo);
+            }
+        return;
+    } else {
+        const u64* bh = a.bhat + ((size_t)limb * 128 + ((j * G) << EB)) * N + k0 + l;   // element e of this thread: (e - e0) N
+#pragma unroll
+        for (int i = 0; i < GG::E; i++) {
+            const u64 bvi = __ldg(bh + (size_t)((i / KB) << EB) * N + (size_t)(i % KB) * N);
+            if constexpr (std::is_same<T, u64>::value) {
+                // bhat in Montgomery form: REDC(x (b 2^64)) = x b mod q in [0, q); x < 8q keeps x b 2^64 < q 2^64
+                x[i] = redc128(U128{x[i] * bvi, umulhi(x[i], bvi)}, mc.q, mc.qinv);
+            } else {
+                const double b = fp_from_u64(bvi);
+                x[i] = fp_mulmod(x[i], b, __dmul_rn(b, qinv), ops.q);   // |x| < 8q < 2^44: exact, |result| < q
+            }
+        }
+        round_b<7, true, Ops>(x, j, 0, 0, itw, ops);   // same positions as sm_get_b: no hazard on the line
+        sm_put_b<7>(line, j, x);
+        __syncthreads();
+        sm_get_a<7>(line, j, x);
+        round_a<7, true, Ops>(x, 0, 0, itw, ops);
+#pragma unroll
+        for (int k = 0; k < GG::E; k++) {
+            const int t = j + GG::TPL * k - a.dmax;
+            if (t >= 0 && t < a.nt) {
+                u64 w;
+                if constexpr (std::is_same<T, u64>::value) w = canon8(x[k], mc.q);
+                else w = fp_canon(fp_center(x[k], ops.q, qinv), ops.q);
+                __stcs(a.out[t] + off, w);
+            }
+        }
+    }
+}
+
+// grid: x = 2 * (N / 32) (component fastest, so the two components of a tile read the same bhat words back to back
+// from L2), y = limb (modulus id = limb: the q-basis).  Prep: x = N / 32, component 0 only.
+template <bool PREP>
+__global__ void __launch_bounds__(256, TZ_MINB) bcast_ntt_kernel(TzArgs a, int N, const ModConst* __restrict__ mod,
+                                                           const ulonglong2* tw2, const ulonglong2* itw2, const double2* twf,
+                                                           const double2* itwf, const double* fpc, u64 fpmask) {
+    const int limb = blockIdx.y;
+    const int comp = PREP ? 0 : (blockIdx.x & 1);
+    const int k0 = (PREP ? blockIdx.x : blockIdx.x >> 1) * TZ_LINES;
+    const ModConst mc = mod[limb];
+    if ((fpmask >> limb) & 1ull) {
+        tz_body<PREP>(a, FpOps{fpc[4 * limb]}, twf + (size_t)limb * N, itwf + (size_t)limb * N, mc, fpc[4 * limb + 1], limb, comp,
+                      k0, N);
+    } else {
+        tz_body<PREP>(a, IntOps{mc.q, 4 * mc.q}, tw2 + (size_t)limb * N, itw2 + (size_t)limb * N, mc, 0.0, limb, comp, k0, N);
+    }
+}
+
+void tz_launch(encf_ctx& c, const TzArgs& a, int level, bool prep, cudaStream_t s) {
+    const size_t smem = (size_t)TZ_LINES * Geo<7>::LSP * 8;
+    dim3 grid((prep ? 1 : 2) * c.N / TZ_LINES, level);
+    if (prep)
+        bcast_ntt_kernel<true><<<grid, 256, smem, s>>>(a, c.N, c.d_mod, (const ulonglong2*)c.d_tw2, (const ulonglong2*)c.d_itw2,
+                                                       (const double2*)c.d_twf, (const double2*)c.d_itwf, c.d_fpc, c.fpmask);
+    else
+        bcast_ntt_kernel<false><<<grid, 256, smem, s>>>(a, c.N, c.d_mod, (const ulonglong2*)c.d_tw2, (const ulonglong2*)c.d_itw2,
+                                                        (const double2*)c.d_twf, (const double2*)c.d_itwf, c.d_fpc, c.fpmask);
+    CUDA_TRY(cudaGetLastError());
+}
+
+}  // namespace
+
+// The masks' spectra B^[limb][e][k] = NTT_128(n_0 .. n_{nu-1}, 0 ..)[e] 128^{-1} (Montgomery form on the integer limbs),
+// cached per (mask set, level) in the context (first use outside CUDA-graph capture, like the masks themselves).
+const u64* bcast_ntt_table(encf_ctx& c, const u64* const* masks, int nu, int level, cudaStream_t s) {
+    std::vector<const u64*> key(masks, masks + nu);
+    key.push_back(reinterpret_cast<const u64*>((uintptr_t)level));
+    {
+        std::lock_guard<std::mutex> lk(c.mu);
+        auto it = c.bhat.find(key);
+        if (it != c.bhat.end()) return it->second;
+    }
+    if (c.N % TZ_LINES || nu < 1 || nu > 64) throw EncfError(ENCF_ERR_PLAN_SHAPE, "bcast_ntt: unsupported shape");
+    u64* tab = nullptr;
+    CUDA_TRY(cudaMalloc(&tab, (size_t)level * 128 * c.N * 8));
+    TzArgs a{};
+    for (int u = 0; u < nu; u++) a.src[u] = masks[u];
+    a.nsrc = nu;
+    a.cs = 0;
+    a.bhat_out = tab;
+    for (int i = 0; i < level; i++) {
+        const u64 q = c.mods[i], inv = h_invmod(128, q);
+        a.fac[i] = ((c.fpmask >> i) & 1ull) ? inv : h_mulmod(inv, c.mont_R[i], q);
+    }
+    tz_launch(c, a, level, true, s);
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto it = c.bhat.find(key);
+    if (it != c.bhat.end()) { cudaFree(tab); return it->second; }
+    c.bhat[key] = tab;
+    return tab;
+}
+
+void k_bcast_ntt(encf_ctx& c, const BcastArgs& A, const u64* bhat, int level, cudaStream_t s) {
+    if (A.nsrc > 128 || A.nt > 64 || A.dmax != A.nu - 1) throw EncfError(ENCF_ERR_PLAN_SHAPE, "bcast_ntt: window longer than 128");
+    TzArgs a{};
+    for (int j = 0; j < A.nsrc; j++) a.src[j] = A.src[j];
+    for (int t = 0; t < A.nt; t++) a.out[t] = A.out[t];
+    a.bhat = bhat;
+    a.cs = (i64)level * c.N;
+    a.nsrc = A.nsrc; a.nt = A.nt; a.dmax = A.dmax;
+    // algorithmic bytes: the window and the outputs (both components) + the spectrum table once
+    const uint64_t bytes = ((uint64_t)A.nsrc * 2 + (uint64_t)A.nt * 2 + 128) * level * c.N * 8;
+    int slot;
+    c.prof_begin("bcast_mac", s, bytes, slot);
+    tz_launch(c, a, level, false, s);
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes; c.st_ptmul += (uint64_t)A.nt * A.nu;
+}

@@ -9,7 +9,9 @@ tests in a fresh interpreter with its environment:
   ENCF_ROTSUM_TMA=1    the cp.async.bulk ring routing sum
   ENCF_MAC_VARIANT=reg / tma1 / tma3   plaintext-MAC variants
   ENCF_NTT_FUSED=1     the fused persistent two-phase NTT
-  ENCF_NTT_INT_ONLY=1  every limb on the integer NTT path (no FP64 path)
+  ENCF_NTT_INT_ONLY=1  every limb on the integer NTT path (no FP64 path; includes the value kernel's 128-point
+                       window transforms)
+  ENCF_BCAST_DIRECT=1  the value kernel's direct sliding-window MAC instead of the 128-point window convolution
 """
 import os
 import subprocess
@@ -36,6 +38,7 @@ VARIANTS = [
     {"ENCF_MAC_VARIANT": "tma3"},
     {"ENCF_NTT_FUSED": "1"},
     {"ENCF_NTT_INT_ONLY": "1"},
+    {"ENCF_BCAST_DIRECT": "1"},
 ]
 
 
