@@ -102,6 +102,51 @@ struct IntOps {
     __device__ __forceinline__ void gs(u64& X, u64& Y, TW w) const { gs_bfly(X, Y, w.x, w.y, q, four_q); }
 };
 
+// q = 2^60 - c with c < 2^32 (every 60-bit prime of the parameter sets: NTT-friendly primes just below 2^60):
+// h q = (h << 60) - h c, so the Shoup remainder a w - h q = a w + h c - (h << 60) (mod 2^64, the same integer in
+// [0, 4q)) needs h c = one IMAD + one IMAD.WIDE.U32 instead of the three products of h q; h << 60 is one shift of
+// the low word.  Same words as mul_shoup_lazy4 by construction; NTT_CQ=0 builds without it (A/B).
+#ifndef NTT_CQ
+#define NTT_CQ 1
+#endif
+__device__ __forceinline__ u64 mul_shoup_lazy4_c(u64 a, u64 w, u64 wp, uint32_t c) {   // [0, 4q)
+    unsigned hl, hh;
+    asm("{\n\t.reg .u32 a0, a1, p0, p1, t0, t1, c;\n\t"
+        "mov.b64 {a0, a1}, %2;\n\t"
+        "mov.b64 {p0, p1}, %3;\n\t"
+        "mul.hi.u32 t0, a1, p0;\n\t"
+        "mad.hi.cc.u32 t1, a0, p1, t0;\n\t"
+        "addc.u32 c, 0, 0;\n\t"
+        "mad.lo.cc.u32 %0, a1, p1, t1;\n\t"
+        "madc.hi.u32 %1, a1, p1, c;\n\t}"
+        : "=r"(hl), "=r"(hh) : "l"(a), "l"(wp));
+    u64 hc;
+    asm("{\n\t.reg .u32 t, z;\n\t"
+        "mul.lo.u32 t, %1, %3;\n\t"
+        "mov.u32 z, 0;\n\t"
+        "mov.b64 %0, {z, t};\n\t"
+        "mad.wide.u32 %0, %2, %3, %0;\n\t}"
+        : "=l"(hc) : "r"(hh), "r"(hl), "r"(c));
+    return a * w + hc - ((u64)(hl << 28) << 32);
+}
+struct IntOpsC : IntOps {
+    uint32_t c;
+    __device__ __forceinline__ void ct(u64& X, u64& Y, TW w) const {
+        u64 x = X >= four_q ? X - four_q : X;
+        u64 t = mul_shoup_lazy4_c(Y, w.x, w.y, c);
+        X = x + t;
+        Y = x - t + four_q;
+    }
+    __device__ __forceinline__ void gs(u64& X, u64& Y, TW w) const {
+        u64 x = X + Y;
+        x = x >= four_q ? x - four_q : x;
+        u64 t = X - Y + four_q;
+        Y = mul_shoup_lazy4_c(t, w.x, w.y, c);
+        X = x;
+    }
+};
+__device__ __forceinline__ bool is_q60c(u64 q) { return NTT_CQ && q < (1ull << 60) && q > (1ull << 60) - (1ull << 32); }
+
 // ---------------------------------------------------------------------------------------------
 // FP64 path (q < 2^41; sm_100a runs DFMA/DMUL/DADD at 64 lanes/clk/SM on the fp64 pipe, while a 64-bit
 // Shoup product costs ~32 fmaheavy cycles per warp on the integer side -- tools/micro/pipes.cu).
@@ -405,7 +450,11 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_cols_r(NttArgs a, int 
         cols_body<LT, INV>(a, lines, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     } else {
         const u64 q = a.mod[mi].q;
-        cols_body<LT, INV>(a, lines, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
+        if (is_q60c(q))
+            cols_body<LT, INV>(a, lines, IntOpsC{{q, 4 * q}, (uint32_t)((1ull << 60) - q)}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x,
+                               blockIdx.y, blockIdx.z);
+        else
+            cols_body<LT, INV>(a, lines, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     }
 }
 
@@ -548,7 +597,11 @@ __global__ void __launch_bounds__(kThreads, NTT_MINB) ntt_rows_r(NttArgs a, int 
         rows_body<LT, INV>(a, lines, lgc, FpOps{a.fpc[4 * mi]}, a.twf + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     } else {
         const u64 q = a.mod[mi].q;
-        rows_body<LT, INV>(a, lines, lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
+        if (is_q60c(q))
+            rows_body<LT, INV>(a, lines, lgc, IntOpsC{{q, 4 * q}, (uint32_t)((1ull << 60) - q)}, a.tw2 + (size_t)mi * a.N, mi,
+                               blockIdx.x, blockIdx.y, blockIdx.z);
+        else
+            rows_body<LT, INV>(a, lines, lgc, IntOps{q, 4 * q}, a.tw2 + (size_t)mi * a.N, mi, blockIdx.x, blockIdx.y, blockIdx.z);
     }
 }
 
@@ -887,7 +940,7 @@ namespace {
 
 constexpr int TZ_LINES = 32;
 #ifndef TZ_MINB
-#define TZ_MINB 3   // 4 CTAs/SM (64 registers) spills ~230 bytes
+#define TZ_MINB 4   // 4 CTAs/SM (64 registers, ~230 bytes of spills): bcast 2.27 ms vs 2.64 at 3 CTAs/SM (80 registers)
 #endif
 
 struct TzArgs {
