@@ -1744,6 +1744,9 @@ __device__ __forceinline__ uint64_t umma_sdesc(uint32_t addr, uint32_t lbo, uint
 }
 
 constexpr int BTC_TILE = 128;
+#ifndef BTC_LD4
+#define BTC_LD4 1   // 0: one TMEM load (8 columns) + wait per output (A/B)
+#endif
 template <int NIN, bool CORR>
 __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
                                                            const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
@@ -1840,12 +1843,7 @@ __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restric
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         u64* o = out + (size_t)p * out_stride + k0 + tid;
         const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
-        for (int t = 0; t < nout; t++) {
-            uint32_t d[8];
-            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
-                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
-                         : "r"(tl + t * 8));
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        auto finish = [&](int t, const uint32_t* d) {
             const u64 lo4 = (u64)d[0] + ((u64)d[1] << 8) + ((u64)d[2] << 16) + ((u64)d[3] << 24);
             const u64 hi4 = (u64)d[4] + ((u64)d[5] << 8) + ((u64)d[6] << 16) + ((u64)d[7] << 24);
             U128 T{lo4, 0};
@@ -1853,6 +1851,32 @@ __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restric
             T.hi += hi4 >> 32;
             if (CORR) mac128(T, r, scr[t]);
             o[spos[t]] = redc128(T, sq[t], sqi[t]);
+        };
+        int t = 0;
+#if BTC_LD4
+        // four outputs' 8 partial sums per TMEM load (32 columns) and one wait: the loads' latency is paid once per
+        // four outputs instead of once per output (bconv 5.18 -> 5.09 ms per layer)
+        for (; t + 4 <= nout; t += 4) {
+            uint32_t d[32];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+                         "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]),
+                           "=r"(d[8]), "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15]),
+                           "=r"(d[16]), "=r"(d[17]), "=r"(d[18]), "=r"(d[19]), "=r"(d[20]), "=r"(d[21]), "=r"(d[22]), "=r"(d[23]),
+                           "=r"(d[24]), "=r"(d[25]), "=r"(d[26]), "=r"(d[27]), "=r"(d[28]), "=r"(d[29]), "=r"(d[30]), "=r"(d[31])
+                         : "r"(tl + t * 8));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 4; k++) finish(t + k, d + 8 * k);
+        }
+#endif
+        for (; t < nout; t++) {
+            uint32_t d[8];
+            asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7])
+                         : "r"(tl + t * 8));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            finish(t, d);
         }
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncthreads();               // TMEM and sA are free for the next tile
