@@ -1,0 +1,13 @@
+# A/B: 41-bit narrow products in the key-switch inner products (default) vs mac128 everywhere (KS_NARROW=0)
+set -u
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kl.py tests/test_gpu_shifts.py tests/test_gpu_fullsize.py -q -x > gpurun_out/ab26_tests.log 2>&1; tail -2 gpurun_out/ab26_tests.log
+for v in base kw; do
+  lib=""; [ "$v" != base ] && lib="ENCF_LIB_OVERRIDE=build_variants/lib_$v.so"
+  env $lib timeout 600 python bench.py --no-e2e --no-cpu-baseline 2>/dev/null | tail -1 > gpurun_out/ab26_bench_$v.json
+  python - gpurun_out/ab26_bench_$v.json "$v" <<'PY'
+import json,sys
+d=json.loads(open(sys.argv[1]).read().strip().splitlines()[-1]); k=d['kernel_time_ms_per_step']
+print(sys.argv[2], d["value"], {x: k.get(x) for x in ("ntt", "ks_inner", "ks_psi", "ks_rotsum", "bcast_mac")}, d["phase_ms"])
+PY
+done
