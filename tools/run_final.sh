@@ -12,6 +12,8 @@ for w in ks gpt2-linear bert-large-layer; do
 done
 timeout 900 python bench.py --ablation wo-scp --no-e2e --no-cpu-baseline > gpurun_out/${T}_bench_wo_scp.json 2> /dev/null; echo "wo-scp rc=$?"
 timeout 900 python tools/phase_breakdown.py > gpurun_out/${T}_phase_breakdown.json 2> /dev/null; echo "phases rc=$?"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${T}_launches_full.csv \
+ENCF_NCU_REGION=1 timeout 900 ncu --profile-from-start off --metrics gpu__time_duration.sum,launch__grid_size --clock-control none \
+    --csv --log-file gpurun_out/${T}_launches_full.csv \
     python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; echo "launches rc=$?"
-python tools/step_launches.py gpurun_out/${T}_launches_full.csv > gpurun_out/${T}_launches_step.md && rm -f gpurun_out/${T}_launches_full.csv
+python tools/step_launches.py gpurun_out/${T}_launches_full.csv > gpurun_out/${T}_launches_step.md
+python tools/launch_seq.py gpurun_out/${T}_launches_full.csv --all > gpurun_out/${T}_launches_seq.txt && rm -f gpurun_out/${T}_launches_full.csv

@@ -1,5 +1,6 @@
 """One timed step of an ncu --metrics gpu__time_duration.sum launch list (bench.py --steps 1 --warmup 3) as a
-markdown table: the launches between the last two QKV plaintext-MAC launch groups.
+markdown table: the whole file (a capture of the timed region) or, with --split, the launches between the last two QKV
+plaintext-MAC launch groups.
 Usage: python tools/step_launches.py launches.csv"""
 import collections
 import csv
@@ -14,7 +15,8 @@ def main(path):
            float(r[idx["Metric Value"]])) for r in rows[1:] if r[idx["Metric Name"]] == "gpu__time_duration.sum"]
     pos = [i for i, (k, _) in enumerate(ks) if "diag_mac" in k]
     starts = [p for i, p in enumerate(pos) if i == 0 or p - pos[i - 1] > 150]
-    step = ks[starts[-2]:starts[-1]]
+    # a capture of the timed region only (ENCF_NCU_REGION=1 + --profile-from-start off, one step) is the step itself
+    step = ks[starts[-2]:starts[-1]] if len(starts) >= 2 and "--split" in sys.argv else ks
     agg = collections.defaultdict(lambda: [0, 0.0])
     for k, t in step:
         agg[k][0] += 1
