@@ -169,7 +169,9 @@ encf_status encf_complexify(encf_ctx* ctx, const encf_ct* re, const encf_ct* im,
 /* Mask plaintexts (Alg A.2 H/U, App. A.3 e_s / n_u, export ranges): ones on rows [r0,r1) of segments
  * s0 + k*sstride (k < scount) of an m-row segment grid, encoded at scale q_{L-1} at level L.
  * The context caches them; encf_mask_put installs an externally encoded plaintext (host coefficient
- * form [L][N]) for a descriptor -- used by the parity tests to feed the oracle's encodings. */
+ * form [L][N]) for a descriptor -- used by the parity tests to feed the oracle's encodings.  Installing a mask drops
+ * the caches derived from it (pre-masked keys of that descriptor, the value kernel's mask spectra); encf_mask_clear
+ * drops every mask and every derived cache.  All of them are context-owned device memory. */
 typedef struct { int32_t m, r0, r1, s0, sstride, scount, level, ext; } encf_mask_desc;   /* ext = 1: [level + K][N], also reduced mod the special primes (lazy key switching, DESIGN R-LAZY) */
 encf_status encf_mask_put(encf_ctx* ctx, const encf_mask_desc* desc, const uint64_t* coeffs /*host [L][N]*/);
 encf_status encf_mask_clear(encf_ctx* ctx);
@@ -235,7 +237,9 @@ encf_status encf_ct_ct_attn_score(encf_ctx* ctx, const encf_keys* keys, const en
 encf_status encf_attn_export_stream(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
                                     const encf_ct* s_t, encf_ct* s_min, void* stream);
 /* Value kernel (C8): p_fd[B_V] (level Lp >= 3), v[B_V] (level Lv >= Lp + 1) -> o[B_V] at
- * level Lp - 2.  Errors: LEVEL_MISMATCH (level plan), MISSING_KEY. */
+ * level Lp - 2.  Step 4's Phi-broadcast b_t = sum_u Phi^{t-u}(p) (.) n_u runs as negacyclic 128-point convolutions
+ * along the window (exact); the first call per (mask set, level) caches the masks' spectra in the context
+ * (128 L N words, outside CUDA-graph capture like the masks).  Errors: LEVEL_MISMATCH (level plan), MISSING_KEY. */
 encf_status encf_ct_ct_attn_value(encf_ctx* ctx, const encf_keys* keys, const encf_attn_plan* plan,
                                   const encf_ct* p_fd, const encf_ct* v, encf_ct* o, void* stream);
 /* Sharded value kernel: units (l, t), flattened l (m/2) + t, in [unit_begin, unit_end).  For every

@@ -467,6 +467,14 @@ encf_status encf_mask_put(encf_ctx* c, const encf_mask_desc* d, const uint64_t* 
         auto it = c->masks.find(key);
         if (it != c->masks.end()) cudaFree(it->second);
         c->masks[key] = pt;
+        // caches derived from masks go stale: the pre-masked keys of this descriptor, and every value-kernel mask
+        // spectrum (keyed by mask addresses, which the allocator may hand out again)
+        for (auto k = c->kmasks.begin(); k != c->kmasks.end();) {
+            if (!(k->first.mk < key) && !(key < k->first.mk)) { cudaFree(k->second); k = c->kmasks.erase(k); }
+            else ++k;
+        }
+        for (auto& kv : c->bhat) cudaFree(kv.second);
+        c->bhat.clear();
     });
 }
 

@@ -931,7 +931,7 @@ void ntt_inverse_scaled(encf_ctx& c, const PolyBatch& b, bool apply_ninv, cudaSt
 // coefficient of X^{t + dmax} in A B.  Modulo X^128 + 1 a term of degree r + 128 would alias onto r; the largest degree
 // is nsrc - 1 + nu - 1 < 128 + dmax whenever nsrc <= 128, so every wanted coefficient (r = t + dmax < 128) is EXACT in
 // the negacyclic product, which the ring's own transform computes: the first 128 entries of the N-point merged twiddle
-// tables ARE the 128-point ones (psi^{brv_16(i)} = (psi^{N/64})^{brv_7(i)} for i < 128).  Per coefficient: forward
+// tables ARE the 128-point ones (psi^{brv_16(i)} = (psi^{N/128})^{brv_7(i)} for i < 128).  Per coefficient: forward
 // NTT-128 of the window (CT, bit-reversed spectrum), x B^ (the masks' spectrum times 128^{-1}, precomputed once per mask
 // set: bcast_ntt_table), inverse NTT-128 (GS) -> 896 butterflies + 128 products instead of nu nt = 4096 MAC terms.
 // The result is the same residue as the direct sum, canonical, so the words are identical to bcast_mac_kernel's.
