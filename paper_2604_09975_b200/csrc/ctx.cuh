@@ -206,6 +206,10 @@ struct KsInnerBatch {
     const u64* key[KS_BATCH];
     u64* acc[KS_BATCH];
     uint32_t gather[KS_BATCH];
+    // optional extended-basis lift (R-LAZY rotations kept in Q_L u P): acc_0 += P sigma_{g0}(c0) on the q-limbs, fused
+    // into the inner product (k_ks_inner_batch's pl / pl_sh); c0 = nullptr: none
+    const u64* c0[KS_BATCH] = {};
+    uint32_t g0[KS_BATCH] = {};
 };
 struct OutBatch {
     u64* out[KS_BATCH][2];
@@ -310,8 +314,9 @@ void k_ks_psi(encf_ctx& c, const PsiBatch& B, int nreq, int dnum, int L, int key
 void k_key_class(encf_ctx& c, const u64* full, int nl_full, u64* out, int nl_out, int ML, int dnum, const u64* sp, const u64* dr,
                  cudaStream_t s);
 void k_keymask(encf_ctx& c, const u64* key, int key_nl, const u64* mask, int dnum, int L, u64* out, cudaStream_t s);
+// pl / pl_sh: P mod q_i and its Shoup quotient for the requests' c0 lifts (required when any B.c0 is set)
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
-                      cudaStream_t s);
+                      cudaStream_t s, const u64* pl = nullptr, const u64* pl_sh = nullptr);
 void k_moddown_finish_batch(encf_ctx& c, const u64* acc, const u64* y, const OutBatch& O, int nreq, int level, int nl,
                             const ModDownTab& t, cudaStream_t s);
 void k_bconv_batch(encf_ctx& c, const u64* in, i64 in_stride, const LimbMap& im, const u64* vf, const u64* vfs, const u64* wf,

@@ -486,21 +486,16 @@ void Ev::hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<
     LimbMap klm;
     klm.n = nl;
     for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
-    u64* c0g = sc.get(Lw * m);
+    (void)Lw;
     for (int r0 = 0; r0 < m; r0 += KS_BATCH) {
         const int cnt = std::min(KS_BATCH, m - r0);
         KsInnerBatch B;
-        CopyBatch cb, dst, src;
         for (int i = 0; i < cnt; i++) {
             const R& q = rq[r0 + i];
             B.ext[i] = q.ext; B.key[i] = q.key; B.gather[i] = q.g; B.acc[i] = q.out;
-            cb.src[i] = q.c0; cb.g[i] = q.g;
-            dst.src[i] = q.out; dst.g[i] = 1u;
-            src.src[i] = c0g + Lw * (r0 + i); src.g[i] = 1u;
+            B.c0[i] = q.c0; B.g0[i] = q.g;   // + P sigma_g(c0) on the q-limbs, fused into the inner product
         }
-        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
-        k_gather_copy(c, cb, cnt, c0g + Lw * r0, (i64)Lw, Lw, s);
-        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);   // + P sigma_g(c0) on the q-limbs
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s, c.moddown[L].d_pl, c.moddown[L].d_pl_sh);
         c.st_ks += cnt;      // a key switch whose ModDown is deferred (merged into a later moddown_rescale)
     }
 }
@@ -615,22 +610,17 @@ void Ev::rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<u
     LimbMap klm;
     klm.n = nl;
     for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
-    u64* c0g = sc.get(Lw * n);
+    (void)Lw;
     for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
         const int cnt = std::min(KS_BATCH, n - r0);
         KsInnerBatch B;
-        CopyBatch cb, dst, src;
         for (int i = 0; i < cnt; i++) {
             DCt& o = outs[r0 + i];
             o.L = L; o.ncomp = 2; o.scale = ins[r0 + i]->scale; o.cstride = (i64)nl * N;
             B.ext[i] = ext + ext_stride(L) * (r0 + i); B.key[i] = key_for(gs[r0 + i], L); B.gather[i] = 1u; B.acc[i] = o.d;
-            cb.src[i] = ins[r0 + i]->comp(0, N); cb.g[i] = gs[r0 + i];
-            dst.src[i] = o.d; dst.g[i] = 1u;
-            src.src[i] = c0g + Lw * (r0 + i); src.g[i] = 1u;
+            B.c0[i] = ins[r0 + i]->comp(0, N); B.g0[i] = gs[r0 + i];   // + P sigma_g(c0), fused into the inner product
         }
-        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
-        k_gather_copy(c, cb, cnt, c0g + Lw * r0, (i64)Lw, Lw, s);
-        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s, c.moddown[L].d_pl, c.moddown[L].d_pl_sh);
         c.st_ks += cnt;
     }
 }

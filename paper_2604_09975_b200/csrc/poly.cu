@@ -1136,22 +1136,30 @@ __global__ void __launch_bounds__(TB, KS_MINB) ks_inner_batch_kernel(KsInnerBatc
 constexpr int KT = 1024;
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsInnerBatch B, int dnum, int nl, int key_nl, KeyLimb klm,
-                                                                    LimbMap em, int N, int logN, const ModConst* __restrict__ mod) {
-    extern __shared__ __align__(128) u64 kt_sm[];      // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [dnum] mbarriers
-    uint64_t* bars = (uint64_t*)(kt_sm + (size_t)dnum * 3 * KT);
+                                                                    LimbMap em, int N, int logN, const ModConst* __restrict__ mod,
+                                                                    int Lq, const u64* __restrict__ pl,
+                                                                    const u64* __restrict__ pl_sh, int lift_slot) {
+    // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [KT] the c0 block of a lift (lift_slot) | [dnum] mbarriers
+    extern __shared__ __align__(128) u64 kt_sm[];
+    u64* c0t = kt_sm + (size_t)dnum * 3 * KT;
+    uint64_t* bars = (uint64_t*)(c0t + (lift_slot ? KT : 0));
     const int r = blockIdx.z, e = blockIdx.y;
     const int kb = blockIdx.x * KT;
     const u64* __restrict__ ext = B.ext[r];
     const u64* __restrict__ key = B.key[r];
     const uint32_t g = B.gather[r];
+    const u64* __restrict__ c0 = e < Lq ? B.c0[r] : nullptr;    // lift P sigma_{g0}(c0) into component 0 (q-limbs)
+    const uint32_t g0 = B.g0[r];
     const uint32_t mask2n = 2 * N - 1;
-    auto src_of = [&](int k) -> int {
-        if (g == 1) return k;
+    auto src_of_g = [&](int k, uint32_t gg) -> int {
+        if (gg == 1) return k;
         const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
-        const uint32_t e2 = (uint32_t)(((uint64_t)ee * g) & mask2n);
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * gg) & mask2n);
         return brv((int)((e2 - 1) >> 1), logN);
     };
+    auto src_of = [&](int k) -> int { return src_of_g(k, g); };
     const int sb = src_of(kb) & ~(KT - 1);             // the aligned source block of this tile
+    const int sb0 = c0 ? src_of_g(kb, g0) & ~(KT - 1) : 0;
     const int kle = klm.kl[e];
     if (threadIdx.x == 0) {
         for (int j = 0; j < dnum; j++) mbar_init(&bars[j], 1);
@@ -1159,10 +1167,11 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsI
         for (int j = 0; j < dnum; j++) {
             u64* st = kt_sm + (size_t)j * 3 * KT;
             const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            mbar_arrive_expect_tx(&bars[j], 3 * KT * 8);
+            mbar_arrive_expect_tx(&bars[j], (3 + (j == 0 && c0 ? 1 : 0)) * KT * 8);
             bulk_g2s(st, ext + ((size_t)j * nl + e) * N + sb, KT * 8, &bars[j]);
             bulk_g2s(st + KT, kj + (size_t)kle * N + kb, KT * 8, &bars[j]);
             bulk_g2s(st + 2 * KT, kj + ((size_t)key_nl + kle) * N + kb, KT * 8, &bars[j]);
+            if (j == 0 && c0) bulk_g2s(c0t, c0 + (size_t)e * N + sb0, KT * 8, &bars[0]);
         }
     }
     __syncthreads();                                    // barrier initialisation visible to every waiting thread
@@ -1195,10 +1204,18 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsI
         }
     }
     u64* __restrict__ acc = B.acc[r];
+    const u64 f = c0 ? pl[e] : 0, fs = c0 ? pl_sh[e] : 0;
 #pragma unroll
     for (int p = 0; p < PP; p++) {
-        *(ulonglong2*)(acc + (size_t)e * N + kb + kl[p]) =
-            make_ulonglong2(redc128(a0[p], mc.q, mc.qinv), redc128(b0[p], mc.q, mc.qinv));
+        u64 o0 = redc128(a0[p], mc.q, mc.qinv), o1 = redc128(b0[p], mc.q, mc.qinv);
+        if (c0) {   // + P sigma_{g0}(c0): the words of k_lift_add over a gathered c0 (add_mod of the Shoup product)
+            const int src = src_of_g(kb + kl[p], g0);
+            ulonglong2 y = *(const ulonglong2*)(c0t + (src & ~1) - sb0);
+            if (src & 1) { const u64 t = y.x; y.x = y.y; y.y = t; }
+            o0 = add_mod(o0, mul_shoup(y.x, f, fs, mc.q), mc.q);
+            o1 = add_mod(o1, mul_shoup(y.y, f, fs, mc.q), mc.q);
+        }
+        *(ulonglong2*)(acc + (size_t)e * N + kb + kl[p]) = make_ulonglong2(o0, o1);
         *(ulonglong2*)(acc + ((size_t)nl + e) * N + kb + kl[p]) =
             make_ulonglong2(redc128(a1[p], mc.q, mc.qinv), redc128(b1[p], mc.q, mc.qinv));
     }
@@ -1967,7 +1984,10 @@ __global__ void rescale_finish_batch_kernel(CopyBatch In, const u64* corr, CopyB
 }  // namespace
 
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
-                      cudaStream_t s) {
+                      cudaStream_t s, const u64* pl, const u64* pl_sh) {
+    bool lift = false;
+    for (int i = 0; i < nreq; i++) lift |= B.c0[i] != nullptr;
+    if (lift && (!pl || !pl_sh)) throw EncfError(ENCF_ERR_ARG, "ks_inner: c0 lift without its P factors");
     if ((unsigned __int128)dnum * c.max_mod >= ((unsigned __int128)1 << 64))
         throw EncfError(ENCF_ERR_ARG, "ks_inner: dnum * q too large for one Montgomery reduction");
     KeyLimb kl;
@@ -1984,22 +2004,41 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
     c.prof_begin("ks_inner", s, bytes, slot);
     static const bool tma = [] { const char* e = std::getenv("ENCF_KS_TMA"); return !e || std::atoi(e) != 0; }();
     if (tma && c.N >= KT && dnum <= 4) {
-        const size_t sm = (size_t)dnum * 3 * KT * 8 + 64;
+        const size_t sm = (size_t)dnum * 3 * KT * 8 + (lift ? KT * 8 : 0) + 64;
         static bool attr = false;
         if (!attr) {
-            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
-            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 3 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * KT * 8 + 64));
             attr = true;
         }
         // ENCF_KS_TMA_T=128 (default): 4 coefficient pairs per thread, more CTAs (and bytes in flight) per SM
         // measured (BERT layer): 128 threads x 4 pairs 3.79 ms, 256 threads x 2 pairs 4.61 ms (profiles/r02_summary.md)
         static const int nt = [] { const char* e = std::getenv("ENCF_KS_TMA_T"); return e ? std::atoi(e) : 128; }();
         if (nt == 128)
-            ks_inner_tma_kernel<128><<<dim3(c.N / KT, nl, nreq), 128, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+            ks_inner_tma_kernel<128><<<dim3(c.N / KT, nl, nreq), 128, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod,
+                                                                              Lq, pl, pl_sh, lift ? 1 : 0);
         else
-            ks_inner_tma_kernel<256><<<dim3(c.N / KT, nl, nreq), 256, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+            ks_inner_tma_kernel<256><<<dim3(c.N / KT, nl, nreq), 256, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod,
+                                                                              Lq, pl, pl_sh, lift ? 1 : 0);
     } else {
         ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
+        if (lift) {   // register-load variant: the lift as the separate gather + lift_add passes (same words)
+            const size_t Lw = (size_t)Lq * c.N;
+            u64* c0g = nullptr;
+            CUDA_TRY(cudaMallocAsync((void**)&c0g, Lw * nreq * 8, s));
+            CopyBatch cb{}, dst{}, src{};
+            int n = 0;
+            for (int i = 0; i < nreq; i++) {
+                if (!B.c0[i]) continue;
+                cb.src[n] = B.c0[i]; cb.g[n] = B.g0[i];
+                dst.src[n] = B.acc[i]; dst.g[n] = 1u;
+                src.src[n] = c0g + Lw * n; src.g[n] = 1u;
+                n++;
+            }
+            k_gather_copy(c, cb, n, c0g, (i64)Lw, Lw, s);
+            k_lift_add(c, dst, src, n, Lq, pl, pl_sh, s);
+            CUDA_TRY(cudaFreeAsync(c0g, s));
+        }
     }
     c.prof_end(slot, s);
     c.st_launch++; c.st_bytes += bytes;
