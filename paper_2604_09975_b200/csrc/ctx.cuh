@@ -209,6 +209,7 @@ struct KsInnerBatch {
     // optional extended-basis lift (R-LAZY rotations kept in Q_L u P): acc_0 += P sigma_{g0}(c0) on the q-limbs, fused
     // into the inner product (k_ks_inner_batch's pl / pl_sh); c0 = nullptr: none
     const u64* c0[KS_BATCH] = {};
+    const u64* c1[KS_BATCH] = {};   // optional: acc_1 += P sigma_{g0}(c1) too (the relinearisation's P d1)
     uint32_t g0[KS_BATCH] = {};
 };
 struct OutBatch {
@@ -297,6 +298,20 @@ void k_encode_weights(encf_ctx& c, const double* dW, int d_in, int d_out, int C,
                       const double* dWim = nullptr, int real_input = 0);
 void k_ks_rotsum(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
 void k_ks_rma(encf_ctx& c, const RotSumBatch& B, int nreq, int nterms, int dnum, int L, int key_nl, cudaStream_t s);
+// Grouped extended-basis rotation sums (the projection's giant-step fold, R-LAZY): group g's output
+//   out_g = sum_{r in [start[g], start[g+1])} rot_ext(x_r, g_r) + P x0_g   over Q_L u P
+// with rot_ext(x_r, g_r) = (sum_j sigma(ext_r,j) key_r,j[0] + P sigma_{g_r}(c0_r), sum_j sigma(ext_r,j) key_r,j[1]) (ext_r the
+// ModUp of sigma_{g_r}(c1_r), so no digit gather) and x0_g an optional ciphertext lifted as is (both components, q-limbs)
+struct KsGroupBatch {
+    const u64* ext[KS_BATCH];
+    const u64* key[KS_BATCH];
+    const u64* c0[KS_BATCH];
+    uint32_t g[KS_BATCH];
+    int start[KS_BATCH + 1];
+    u64* out[KS_BATCH];            // [2][L+K][N] per group
+    const u64* x0[KS_BATCH];       // [2][L][N] or nullptr
+};
+void k_ks_group(encf_ctx& c, const KsGroupBatch& B, int ngrp, int dnum, int L, int key_nl, cudaStream_t s);
 constexpr int PSI_BATCH = 128;
 struct PsiBatch {                  // masked shift Psi^t without ModDown: h (.) rot_ext(x, g0) + u (.) rot_ext(x, g1)
     const u64* ext[PSI_BATCH];

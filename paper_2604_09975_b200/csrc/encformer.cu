@@ -112,6 +112,55 @@ void proj_phase1(Ev& ev, const encf_proj_plan& p, const std::vector<DCt>& x, con
         shift_sum_ext_many(ev, ptrs(cu), terms, accs);
         return;
     }
+    static const bool grouped = [] { const char* e = std::getenv("ENCF_PROJ_GROUP"); return !e || std::atoi(e) != 0; }();
+    if (grouped) {
+        // giant rotations and block sums in one grouped launch (k_ks_group): acc_b = P c~_{b,0} + sum_{p >= 1}
+        // rot_ext(c~_{b,p}, p N1 m) -- one ModUp of every sigma_g(c1) (gather fused), then per block the inner products,
+        // P sigma_g(c0) lifts and the P c~_{b,0} lift summed in registers (same words as rotate_many_ext + lift_many +
+        // sum_many_ext; ENCF_PROJ_GROUP=0 runs those)
+        std::vector<const u64*> c1s;
+        std::vector<uint32_t> g1s;
+        std::vector<int> ridx2(units, -1);
+        for (int un = u0; un < u1; un++) {
+            const int pp = un % p.N2;
+            if (!pp) continue;
+            ridx2[un - u0] = (int)c1s.size();
+            c1s.push_back(cu[un - u0].comp(1, N));
+            g1s.push_back(ev.galois_rot((long)pp * N1 * p.m));
+        }
+        const u64* ext = c1s.empty() ? nullptr : ev.modup_many(c1s, g1s, L);
+        const int nblk = b_last - b_first + 1;
+        accs = ev.alloc_many_ext(nblk, L);
+        const int K = ev.c.Kof(L), key_nl = ev.keys->max_level + K, dn = ev.c.dnum(L);
+        KsGroupBatch GB;
+        int ng = 0, nr = 0;
+        GB.start[0] = 0;
+        auto flush = [&]() {
+            if (ng) k_ks_group(ev.c, GB, ng, dn, L, key_nl, ev.s);
+            ng = 0; nr = 0; GB.start[0] = 0;
+        };
+        for (int b = b_first; b <= b_last; b++) {
+            int cnt = 0;
+            for (int un = std::max(u0, b * p.N2); un < std::min(u1, (b + 1) * p.N2); un++) cnt += ridx2[un - u0] >= 0;
+            if (ng == KS_BATCH || nr + cnt > KS_BATCH) flush();
+            DCt& a = accs[b - b_first];
+            a.scale = sc;
+            GB.out[ng] = a.d;
+            GB.x0[ng] = nullptr;
+            for (int un = std::max(u0, b * p.N2); un < std::min(u1, (b + 1) * p.N2); un++) {
+                const int ri = ridx2[un - u0];
+                if (ri < 0) { GB.x0[ng] = cu[un - u0].d; continue; }
+                GB.ext[nr] = ext + ev.ext_stride(L) * ri;
+                GB.key[nr] = ev.key_for(g1s[ri], L);
+                GB.c0[nr] = cu[un - u0].comp(0, N);
+                GB.g[nr] = g1s[ri];
+                nr++;
+            }
+            GB.start[++ng] = nr;
+        }
+        flush();
+        return;
+    }
     std::vector<const DCt*> rin, lin;
     std::vector<uint32_t> rg;
     std::vector<int> ridx, lidx;

@@ -681,19 +681,10 @@ void Ev::relin_rescale_many(const std::vector<const DCt*>& ins, std::vector<DCt>
         for (int i = 0; i < cnt; i++) {
             acc[r0 + i].scale = ins[r0 + i]->scale;
             B.ext[i] = ext + ext_stride(L) * (r0 + i); B.key[i] = key; B.gather[i] = 1u; B.acc[i] = acc[r0 + i].d;
+            B.c0[i] = ins[r0 + i]->comp(0, N); B.c1[i] = ins[r0 + i]->comp(1, N); B.g0[i] = 1u;   // + P d0, P d1 (fused)
         }
-        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s);
+        k_ks_inner_batch(c, B, cnt, dn, nl, key_nl, klm, s, c.moddown[L].d_pl, c.moddown[L].d_pl_sh);
         c.st_ks += cnt;
-    }
-    for (int r0 = 0; r0 < 2 * n; r0 += CP_BATCH) {       // + P d0, P d1 on the q-limbs
-        const int cnt = std::min(CP_BATCH, 2 * n - r0);
-        CopyBatch dst, src;
-        for (int i = 0; i < cnt; i++) {
-            const int idx = (r0 + i) / 2, comp = (r0 + i) % 2;
-            dst.src[i] = acc[idx].comp(comp, N); dst.g[i] = 1u;
-            src.src[i] = ins[idx]->comp(comp, N); src.g[i] = 1u;
-        }
-        k_lift_add(c, dst, src, cnt, L, c.moddown[L].d_pl, c.moddown[L].d_pl_sh, s);
     }
     moddown_rescale_many(acc, outs);
 }

@@ -1139,16 +1139,18 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsI
                                                                     LimbMap em, int N, int logN, const ModConst* __restrict__ mod,
                                                                     int Lq, const u64* __restrict__ pl,
                                                                     const u64* __restrict__ pl_sh, int lift_slot) {
-    // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [KT] the c0 block of a lift (lift_slot) | [dnum] mbarriers
+    // [dnum][3][KT]: ext block, key comp 0, key comp 1 | [lift_slot][KT] the c0 (c1) blocks of a lift | [dnum] mbarriers
     extern __shared__ __align__(128) u64 kt_sm[];
     u64* c0t = kt_sm + (size_t)dnum * 3 * KT;
-    uint64_t* bars = (uint64_t*)(c0t + (lift_slot ? KT : 0));
+    u64* c1t = c0t + KT;
+    uint64_t* bars = (uint64_t*)(c0t + (size_t)lift_slot * KT);
     const int r = blockIdx.z, e = blockIdx.y;
     const int kb = blockIdx.x * KT;
     const u64* __restrict__ ext = B.ext[r];
     const u64* __restrict__ key = B.key[r];
     const uint32_t g = B.gather[r];
     const u64* __restrict__ c0 = e < Lq ? B.c0[r] : nullptr;    // lift P sigma_{g0}(c0) into component 0 (q-limbs)
+    const u64* __restrict__ c1 = c0 ? B.c1[r] : nullptr;        // ... and P sigma_{g0}(c1) into component 1
     const uint32_t g0 = B.g0[r];
     const uint32_t mask2n = 2 * N - 1;
     auto src_of_g = [&](int k, uint32_t gg) -> int {
@@ -1167,11 +1169,12 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsI
         for (int j = 0; j < dnum; j++) {
             u64* st = kt_sm + (size_t)j * 3 * KT;
             const u64* kj = key + (size_t)j * 2 * key_nl * N;
-            mbar_arrive_expect_tx(&bars[j], (3 + (j == 0 && c0 ? 1 : 0)) * KT * 8);
+            mbar_arrive_expect_tx(&bars[j], (3 + (j == 0 && c0 ? 1 : 0) + (j == 0 && c1 ? 1 : 0)) * KT * 8);
             bulk_g2s(st, ext + ((size_t)j * nl + e) * N + sb, KT * 8, &bars[j]);
             bulk_g2s(st + KT, kj + (size_t)kle * N + kb, KT * 8, &bars[j]);
             bulk_g2s(st + 2 * KT, kj + ((size_t)key_nl + kle) * N + kb, KT * 8, &bars[j]);
             if (j == 0 && c0) bulk_g2s(c0t, c0 + (size_t)e * N + sb0, KT * 8, &bars[0]);
+            if (j == 0 && c1) bulk_g2s(c1t, c1 + (size_t)e * N + sb0, KT * 8, &bars[0]);
         }
     }
     __syncthreads();                                    // barrier initialisation visible to every waiting thread
@@ -1216,8 +1219,128 @@ __global__ void __launch_bounds__(NT, NT == 256 ? 3 : 4) ks_inner_tma_kernel(KsI
             o1 = add_mod(o1, mul_shoup(y.y, f, fs, mc.q), mc.q);
         }
         *(ulonglong2*)(acc + (size_t)e * N + kb + kl[p]) = make_ulonglong2(o0, o1);
-        *(ulonglong2*)(acc + ((size_t)nl + e) * N + kb + kl[p]) =
-            make_ulonglong2(redc128(a1[p], mc.q, mc.qinv), redc128(b1[p], mc.q, mc.qinv));
+        u64 o2 = redc128(a1[p], mc.q, mc.qinv), o3 = redc128(b1[p], mc.q, mc.qinv);
+        if (c1) {
+            const int src = src_of_g(kb + kl[p], g0);
+            ulonglong2 y = *(const ulonglong2*)(c1t + (src & ~1) - sb0);
+            if (src & 1) { const u64 t = y.x; y.x = y.y; y.y = t; }
+            o2 = add_mod(o2, mul_shoup(y.x, f, fs, mc.q), mc.q);
+            o3 = add_mod(o3, mul_shoup(y.y, f, fs, mc.q), mc.q);
+        }
+        *(ulonglong2*)(acc + ((size_t)nl + e) * N + kb + kl[p]) = make_ulonglong2(o2, o3);
+    }
+}
+
+// Grouped extended-basis rotation sums (KsGroupBatch): CTA = (tile of KT coefficients, extended limb e, group z); the
+// group's requests stream through a two-stage cp.async.bulk ring (per stage: every digit's ext block, both key tiles and,
+// on q-limbs, the Galois source block of c0), one request's products are reduced once (REDC) and summed mod q in
+// registers, and the group's P x0 lift is added at the end.  The same residues as ks_inner + lift + sum_many_ext.
+constexpr int KG_NT = 256, KG_PP = KT / 2 / KG_NT;
+__global__ void __launch_bounds__(KG_NT, 2) ks_group_tma_kernel(KsGroupBatch B, int dnum, int nl, int L, int key_nl, KeyLimb klm,
+                                                               LimbMap em, int N, int logN, const ModConst* __restrict__ mod,
+                                                               const u64* __restrict__ pl, const u64* __restrict__ pl_sh) {
+    extern __shared__ __align__(128) u64 kg_sm[];      // [2 stages][3 dnum + 1][KT] | [2] mbarriers
+    const int per = 3 * dnum + 1;
+    uint64_t* bars = (uint64_t*)(kg_sm + (size_t)2 * per * KT);
+    const int z = blockIdx.z, e = blockIdx.y;
+    const int kb = blockIdx.x * KT;
+    const int r0 = B.start[z], r1 = B.start[z + 1];
+    const bool qlimb = e < L;
+    const int kle = klm.kl[e];
+    const uint32_t mask2n = 2 * N - 1;
+    auto src_of_g = [&](int k, uint32_t gg) -> int {
+        if (gg == 1) return k;
+        const uint32_t ee = 2u * (uint32_t)brv(k, logN) + 1u;
+        const uint32_t e2 = (uint32_t)(((uint64_t)ee * gg) & mask2n);
+        return brv((int)((e2 - 1) >> 1), logN);
+    };
+    auto issue = [&](int r) {   // thread 0: request r into stage (r - r0) & 1
+        if (r >= r1) return;
+        const int slot = (r - r0) & 1;
+        u64* st = kg_sm + (size_t)slot * per * KT;
+        const u64* c0 = qlimb ? B.c0[r] : nullptr;
+        mbar_arrive_expect_tx(&bars[slot], (uint32_t)((3 * dnum + (c0 ? 1 : 0)) * KT * 8));
+        for (int j = 0; j < dnum; j++) {
+            const u64* kj = B.key[r] + (size_t)j * 2 * key_nl * N;
+            bulk_g2s(st + (3 * j) * KT, B.ext[r] + ((size_t)j * nl + e) * N + kb, KT * 8, &bars[slot]);
+            bulk_g2s(st + (3 * j + 1) * KT, kj + (size_t)kle * N + kb, KT * 8, &bars[slot]);
+            bulk_g2s(st + (3 * j + 2) * KT, kj + ((size_t)key_nl + kle) * N + kb, KT * 8, &bars[slot]);
+        }
+        if (c0) bulk_g2s(st + (3 * dnum) * KT, c0 + (size_t)e * N + (src_of_g(kb, B.g[r]) & ~(KT - 1)), KT * 8, &bars[slot]);
+    };
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        issue(r0);
+        issue(r0 + 1);
+    }
+    __syncthreads();
+    const ModConst mc = mod[em.mod[e]];
+    const u64 q = mc.q;
+    const u64 f = qlimb ? pl[e] : 0, fs = qlimb ? pl_sh[e] : 0;
+    u64 s0[KG_PP][2], s1[KG_PP][2];
+#pragma unroll
+    for (int p = 0; p < KG_PP; p++) s0[p][0] = s0[p][1] = s1[p][0] = s1[p][1] = 0;
+    for (int r = r0; r < r1; r++) {
+        const int it = r - r0, slot = it & 1;
+        mbar_wait(&bars[slot], (uint32_t)((it >> 1) & 1));
+        const u64* st = kg_sm + (size_t)slot * per * KT;
+        U128 a0[KG_PP], b0[KG_PP], a1[KG_PP], b1[KG_PP];
+#pragma unroll
+        for (int p = 0; p < KG_PP; p++) a0[p] = b0[p] = a1[p] = b1[p] = U128{0, 0};
+        for (int j = 0; j < dnum; j++) {
+#pragma unroll
+            for (int p = 0; p < KG_PP; p++) {
+                const int kl = 2 * (threadIdx.x + p * KG_NT);
+                const ulonglong2 x = *(const ulonglong2*)(st + (3 * j) * KT + kl);
+                const ulonglong2 k0 = *(const ulonglong2*)(st + (3 * j + 1) * KT + kl);
+                const ulonglong2 k1 = *(const ulonglong2*)(st + (3 * j + 2) * KT + kl);
+                mac128(a0[p], x.x, k0.x);
+                mac128(b0[p], x.y, k0.y);
+                mac128(a1[p], x.x, k1.x);
+                mac128(b1[p], x.y, k1.y);
+            }
+        }
+        const bool lift = qlimb && B.c0[r];
+        const uint32_t gr = B.g[r];
+        const int sb0 = lift ? src_of_g(kb, gr) & ~(KT - 1) : 0;
+#pragma unroll
+        for (int p = 0; p < KG_PP; p++) {
+            u64 o0 = redc128(a0[p], q, mc.qinv), o1 = redc128(b0[p], q, mc.qinv);
+            if (lift) {
+                const int src = src_of_g(kb + 2 * (threadIdx.x + p * KG_NT), gr);
+                ulonglong2 y = *(const ulonglong2*)(st + (3 * dnum) * KT + (src & ~1) - sb0);
+                if (src & 1) { const u64 t = y.x; y.x = y.y; y.y = t; }
+                o0 = add_mod(o0, mul_shoup(y.x, f, fs, q), q);
+                o1 = add_mod(o1, mul_shoup(y.y, f, fs, q), q);
+            }
+            s0[p][0] = add_mod(s0[p][0], o0, q);
+            s0[p][1] = add_mod(s0[p][1], o1, q);
+            s1[p][0] = add_mod(s1[p][0], redc128(a1[p], q, mc.qinv), q);
+            s1[p][1] = add_mod(s1[p][1], redc128(b1[p], q, mc.qinv), q);
+        }
+        __syncthreads();                                  // stage consumed by every thread
+        if (threadIdx.x == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(r + 2);
+        }
+    }
+    const u64* x0 = qlimb ? B.x0[z] : nullptr;
+    u64* out = B.out[z];
+#pragma unroll
+    for (int p = 0; p < KG_PP; p++) {
+        const int k = kb + 2 * (threadIdx.x + p * KG_NT);
+        if (x0) {   // + P x0 (both components; x0 is [2][L][N])
+            const ulonglong2 u = __ldg((const ulonglong2*)(x0 + (size_t)e * N + k));
+            const ulonglong2 v = __ldg((const ulonglong2*)(x0 + ((size_t)L + e) * N + k));
+            s0[p][0] = add_mod(s0[p][0], mul_shoup(u.x, f, fs, q), q);
+            s0[p][1] = add_mod(s0[p][1], mul_shoup(u.y, f, fs, q), q);
+            s1[p][0] = add_mod(s1[p][0], mul_shoup(v.x, f, fs, q), q);
+            s1[p][1] = add_mod(s1[p][1], mul_shoup(v.y, f, fs, q), q);
+        }
+        *(ulonglong2*)(out + (size_t)e * N + k) = make_ulonglong2(s0[p][0], s0[p][1]);
+        *(ulonglong2*)(out + ((size_t)nl + e) * N + k) = make_ulonglong2(s1[p][0], s1[p][1]);
     }
 }
 
@@ -1985,8 +2108,9 @@ __global__ void rescale_finish_batch_kernel(CopyBatch In, const u64* corr, CopyB
 
 void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, int nl, int key_nl, const LimbMap& key_limb_of,
                       cudaStream_t s, const u64* pl, const u64* pl_sh) {
-    bool lift = false;
-    for (int i = 0; i < nreq; i++) lift |= B.c0[i] != nullptr;
+    bool lift = false, lift1 = false;
+    for (int i = 0; i < nreq; i++) { lift |= B.c0[i] != nullptr; lift1 |= B.c1[i] != nullptr; }
+    const int lslots = lift ? (lift1 ? 2 : 1) : 0;
     if (lift && (!pl || !pl_sh)) throw EncfError(ENCF_ERR_ARG, "ks_inner: c0 lift without its P factors");
     if ((unsigned __int128)dnum * c.max_mod >= ((unsigned __int128)1 << 64))
         throw EncfError(ENCF_ERR_ARG, "ks_inner: dnum * q too large for one Montgomery reduction");
@@ -2004,11 +2128,11 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
     c.prof_begin("ks_inner", s, bytes, slot);
     static const bool tma = [] { const char* e = std::getenv("ENCF_KS_TMA"); return !e || std::atoi(e) != 0; }();
     if (tma && c.N >= KT && dnum <= 4) {
-        const size_t sm = (size_t)dnum * 3 * KT * 8 + (lift ? KT * 8 : 0) + 64;
+        const size_t sm = (size_t)dnum * 3 * KT * 8 + (size_t)lslots * KT * 8 + 64;
         static bool attr = false;
         if (!attr) {
-            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * KT * 8 + 64));
-            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 13 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 14 * KT * 8 + 64));
+            CUDA_TRY(cudaFuncSetAttribute(ks_inner_tma_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 14 * KT * 8 + 64));
             attr = true;
         }
         // ENCF_KS_TMA_T=128 (default): 4 coefficient pairs per thread, more CTAs (and bytes in flight) per SM
@@ -2016,24 +2140,28 @@ void k_ks_inner_batch(encf_ctx& c, const KsInnerBatch& B, int nreq, int dnum, in
         static const int nt = [] { const char* e = std::getenv("ENCF_KS_TMA_T"); return e ? std::atoi(e) : 128; }();
         if (nt == 128)
             ks_inner_tma_kernel<128><<<dim3(c.N / KT, nl, nreq), 128, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod,
-                                                                              Lq, pl, pl_sh, lift ? 1 : 0);
+                                                                              Lq, pl, pl_sh, lslots);
         else
             ks_inner_tma_kernel<256><<<dim3(c.N / KT, nl, nreq), 256, sm, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod,
-                                                                              Lq, pl, pl_sh, lift ? 1 : 0);
+                                                                              Lq, pl, pl_sh, lslots);
     } else {
         ks_inner_batch_kernel<<<grid, TB, 0, s>>>(B, dnum, nl, key_nl, kl, em, c.N, c.logN, c.d_mod);
         if (lift) {   // register-load variant: the lift as the separate gather + lift_add passes (same words)
             const size_t Lw = (size_t)Lq * c.N;
             u64* c0g = nullptr;
-            CUDA_TRY(cudaMallocAsync((void**)&c0g, Lw * nreq * 8, s));
+            CUDA_TRY(cudaMallocAsync((void**)&c0g, Lw * nreq * 2 * 8, s));
             CopyBatch cb{}, dst{}, src{};
             int n = 0;
             for (int i = 0; i < nreq; i++) {
                 if (!B.c0[i]) continue;
-                cb.src[n] = B.c0[i]; cb.g[n] = B.g0[i];
-                dst.src[n] = B.acc[i]; dst.g[n] = 1u;
-                src.src[n] = c0g + Lw * n; src.g[n] = 1u;
-                n++;
+                for (int cc = 0; cc < 2; cc++) {
+                    const u64* cp = cc ? B.c1[i] : B.c0[i];
+                    if (!cp) continue;
+                    cb.src[n] = cp; cb.g[n] = B.g0[i];
+                    dst.src[n] = B.acc[i] + (size_t)cc * nl * c.N; dst.g[n] = 1u;
+                    src.src[n] = c0g + Lw * n; src.g[n] = 1u;
+                    n++;
+                }
             }
             k_gather_copy(c, cb, n, c0g, (i64)Lw, Lw, s);
             k_lift_add(c, dst, src, n, Lq, pl, pl_sh, s);
@@ -2682,4 +2810,34 @@ void k_field2ring(encf_ctx& c, const u64* sh, u64* out, int ell, cudaStream_t s)
     field2ring_kernel<<<GRID((size_t)c.N), TB, 0, s>>>(sh, out, c.N, mask);
     c.prof_end(_slot, s); }
     c.st_launch++;
+}
+
+void k_ks_group(encf_ctx& c, const KsGroupBatch& B, int ngrp, int dnum, int L, int key_nl, cudaStream_t s) {
+    if (ngrp <= 0) return;
+    const int K = c.Kof(L), nl = L + K;
+    if ((unsigned __int128)dnum * c.max_mod >= ((unsigned __int128)1 << 64))
+        throw EncfError(ENCF_ERR_ARG, "ks_group: dnum * q too large for one Montgomery reduction");
+    const size_t sm = (size_t)2 * (3 * dnum + 1) * KT * 8 + 64;
+    if (c.N < KT || sm > 227 * 1024) throw EncfError(ENCF_ERR_PLAN_SHAPE, "ks_group: unsupported shape");
+    static bool attr = false;
+    if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(ks_group_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    KeyLimb kl;
+    LimbMap em;
+    em.n = nl;
+    for (int e = 0; e < nl; e++) {
+        kl.kl[e] = e < L ? e : (key_nl - K) + (e - L);
+        em.mod[e] = (unsigned char)(e < L ? e : c.L + (e - L));
+    }
+    const int nreq = B.start[ngrp];
+    const uint64_t bytes = (uint64_t)nreq * ((uint64_t)dnum * nl * 3 + L) * c.N * 8 + (uint64_t)ngrp * (2 * nl + 2 * L) * c.N * 8;
+    int slot;
+    c.prof_begin("ks_inner", s, bytes, slot);
+    ks_group_tma_kernel<<<dim3(c.N / KT, nl, ngrp), KG_NT, sm, s>>>(B, dnum, nl, L, key_nl, kl, em, c.N, c.logN, c.d_mod,
+                                                                     c.moddown[L].d_pl, c.moddown[L].d_pl_sh);
+    c.prof_end(slot, s);
+    c.st_launch++; c.st_bytes += bytes; c.st_ks += nreq;
+    CUDA_TRY(cudaGetLastError());
 }

@@ -12,6 +12,7 @@ tests in a fresh interpreter with its environment:
   ENCF_NTT_INT_ONLY=1  every limb on the integer NTT path (no FP64 path; includes the value kernel's 128-point
                        window transforms)
   ENCF_BCAST_DIRECT=1  the value kernel's direct sliding-window MAC instead of the 128-point window convolution
+  ENCF_PROJ_GROUP=0    projection giant steps as separate ext rotations + lifts + block sums (not one grouped launch)
 """
 import os
 import subprocess
@@ -38,7 +39,7 @@ VARIANTS = [
     {"ENCF_MAC_VARIANT": "tma3"},
     {"ENCF_NTT_FUSED": "1"},
     {"ENCF_NTT_INT_ONLY": "1"},
-    {"ENCF_BCAST_DIRECT": "1"},
+    {"ENCF_BCAST_DIRECT": "1", "ENCF_PROJ_GROUP": "0"},
 ]
 
 
