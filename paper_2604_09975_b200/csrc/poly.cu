@@ -2486,17 +2486,34 @@ __global__ void __launch_bounds__(TB) sum_csr2_kernel(const SumDev* __restrict__
 }
 
 // outs[o] = sum_{t in [off[o], off[o+1])} (a0 b0, a0 b1 + a1 b0, a1 b1)
+// Grid (output, coefficient block, limb) with the OUTPUT fastest: the CTAs running together cover one coefficient
+// block of every output, so operands shared between outputs (the score kernel's Q/K banks: B (beta + g/2) ciphertexts
+// feed all m/2 outputs) are read from HBM about once and re-read from L2.  Karatsuba per pair: a0 b1 + a1 b0 =
+// (a0 + a1)(b0 + b1) - a0 b0 - a1 b1, exact in 128 bits over chunks of 16 pairs ((2q)^2 16 < 2^128 for q < 2^61).
+// TENSOR_OLD=1 builds the previous kernel (limb-major grid, four products per pair) for A/B.
+#ifndef TENSOR_OLD
+#define TENSOR_OLD 0
+#endif
 __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restrict__ pairs, const int* __restrict__ off,
                                                         u64* const* __restrict__ outs, int level, int N,
                                                         const ModConst* __restrict__ mod) {
+#if TENSOR_OLD
     const int o = blockIdx.z, limb = blockIdx.y;
+#else
+    const int o = blockIdx.x, limb = blockIdx.z;
+#endif
     const ModConst mc = mod[limb];
     const size_t cs = (size_t)level * N;
     const int t0 = off[o], t1 = off[o + 1];
     u64* out = outs[o];
+#if TENSOR_OLD
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < N; k += gridDim.x * blockDim.x) {
+#else
+    for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < N; k += gridDim.y * blockDim.x) {
+#endif
         const size_t idx = (size_t)limb * N + k;
         u64 r0 = 0, r1 = 0, r2 = 0;
+#if TENSOR_OLD
         for (int ta = t0; ta < t1; ta += 64) {
             U128 d0{0, 0}, d1{0, 0}, d2{0, 0};
             const int tb = min(t1, ta + 64);
@@ -2509,6 +2526,29 @@ __global__ void __launch_bounds__(TB) tensor_csr_kernel(const PairDev* __restric
                 mac128(d1, a1, b0);
                 mac128(d2, a1, b1);
             }
+#else
+        for (int ta = t0; ta < t1; ta += 16) {
+            U128 d0{0, 0}, sm{0, 0}, d2{0, 0};
+            const int tb = min(t1, ta + 16);
+            for (int t = ta; t < tb; t++) {
+                const u64* a = pairs[t].a;
+                const u64* b = pairs[t].b;
+                u64 a0 = a[idx], a1 = a[pairs[t].as + idx], b0 = b[idx], b1 = b[pairs[t].bs + idx];
+                mac128(d0, a0, b0);
+                mac128(d2, a1, b1);
+                mac128(sm, a0 + a1, b0 + b1);
+            }
+            // d1 = sm - d0 - d2 >= 0 (exact)
+            U128 d1 = sm;
+            {
+                const u64 lo = d1.lo - d0.lo;
+                d1.hi = d1.hi - d0.hi - (d1.lo < d0.lo);
+                d1.lo = lo;
+                const u64 lo2 = d1.lo - d2.lo;
+                d1.hi = d1.hi - d2.hi - (d1.lo < d2.lo);
+                d1.lo = lo2;
+            }
+#endif
             r0 = add_mod(r0, barrett128(d0, mc.q, mc.rhi, mc.rlo), mc.q);
             r1 = add_mod(r1, barrett128(d1, mc.q, mc.rhi, mc.rlo), mc.q);
             r2 = add_mod(r2, barrett128(d2, mc.q, mc.rhi, mc.rlo), mc.q);
@@ -2539,7 +2579,12 @@ void k_sum_csr(encf_ctx& c, const SumDev* terms, const int* off, u64* const* out
 
 void k_tensor_csr(encf_ctx& c, const PairDev* pairs, const int* off, u64* const* outs, int nout, int nterms, int level,
                   cudaStream_t s) {
+#if TENSOR_OLD
     dim3 grid((c.N + TB - 1) / TB, level, nout);
+#else
+    if (nout > (1 << 30)) throw EncfError(ENCF_ERR_ARG, "tensor: too many outputs");
+    dim3 grid(nout, (c.N + TB - 1) / TB, level);
+#endif
     { int _slot; c.prof_begin("tensor_csr_kernel", s, 0, _slot);
     tensor_csr_kernel<<<grid, TB, 0, s>>>(pairs, off, outs, level, c.N, c.d_mod);
     c.prof_end(_slot, s); }
