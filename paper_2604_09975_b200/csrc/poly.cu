@@ -418,6 +418,9 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES) diag_mac_kernel(const u64
 constexpr int DM_ROWS = 8;
 constexpr int DM_STAGE_WORDS = MAC_LANES * DM_ROWS * MAC_T;   // 4096 words = 32 KB
 constexpr int DM_MAX_STAGES = 5;
+#ifndef MAC_KARA
+#define MAC_KARA 1   // wide-limb (30-bit split) plaintext MAC: Karatsuba, 3 products; 0: 4 products (A/B)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -538,9 +541,10 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                     for (int t = 0; t < rows; t++) row(t);
                 }
             } else {
-                // 30-bit split: x = xh 2^30 + xl, b = bh 2^30 + bl (q < 2^60), per product 4 IMAD.WIDE.U32 into 64-bit
-                // sums hh, md (= xh bl + xl bh), ll instead of a 64 x 64 -> 128 multiply-add; <= ROWS = 8 rows per
-                // chunk keep md < 16 (2^30 - 1)^2 < 2^64, and each chunk folds hh 2^60 + md 2^30 + ll into the 128-bit sum
+                // 30-bit split: x = xh 2^30 + xl, b = bh 2^30 + bl (q < 2^60); Karatsuba per product: 3 IMAD.WIDE.U32 into
+                // 64-bit sums hh, mm = sum (xh + xl)(bh + bl), ll (MAC_KARA=0: 4 products, md = xh bl + xl bh directly).
+                // mm wraps mod 2^64, but md = mm - hh - ll is exact there because md < 16 (2^30 - 1)^2 < 2^64 over the
+                // <= ROWS = 8 rows of a chunk; each chunk folds hh 2^60 + md 2^30 + ll into the 128-bit sum
                 const uint4* sb8 = (const uint4*)sb + kp + (size_t)(c * ROWS) * 2 * (MAC_T / 2);
                 u64 hh00 = 0, md00 = 0, ll00 = 0, hh01 = 0, md01 = 0, ll01 = 0, hh10 = 0, md10 = 0, ll10 = 0, hh11 = 0, md11 = 0,
                     ll11 = 0;
@@ -550,10 +554,18 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                     const uint32_t bh = (uint32_t)(x.y >> 30), bl = (uint32_t)(x.y & 0x3FFFFFFFu);
                     const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
                     const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
+#if MAC_KARA
+                    const uint32_t as = ah + al, bsum = bh + bl;
+                    hh00 += (u64)pp.x * ah; md00 += (u64)(pp.x + pp.y) * as; ll00 += (u64)pp.y * al;
+                    hh01 += (u64)pp.z * bh; md01 += (u64)(pp.z + pp.w) * bsum; ll01 += (u64)pp.w * bl;
+                    hh10 += (u64)rr.x * ah; md10 += (u64)(rr.x + rr.y) * as; ll10 += (u64)rr.y * al;
+                    hh11 += (u64)rr.z * bh; md11 += (u64)(rr.z + rr.w) * bsum; ll11 += (u64)rr.w * bl;
+#else
                     hh00 += (u64)pp.x * ah; md00 += (u64)pp.x * al + (u64)pp.y * ah; ll00 += (u64)pp.y * al;
                     hh01 += (u64)pp.z * bh; md01 += (u64)pp.z * bl + (u64)pp.w * bh; ll01 += (u64)pp.w * bl;
                     hh10 += (u64)rr.x * ah; md10 += (u64)rr.x * al + (u64)rr.y * ah; ll10 += (u64)rr.y * al;
                     hh11 += (u64)rr.z * bh; md11 += (u64)rr.z * bl + (u64)rr.w * bh; ll11 += (u64)rr.w * bl;
+#endif
                 };
                 if (rows == ROWS) {
 #pragma unroll
@@ -561,6 +573,9 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                 } else {
                     for (int t = 0; t < rows; t++) row(t);
                 }
+#if MAC_KARA
+                md00 -= hh00 + ll00; md01 -= hh01 + ll01; md10 -= hh10 + ll10; md11 -= hh11 + ll11;
+#endif
                 auto fold = [](U128& a, u64 hh, u64 md, u64 ll) {
                     add128(a, ll);
                     add128(a, md << 30);
