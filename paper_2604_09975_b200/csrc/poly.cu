@@ -1902,6 +1902,9 @@ constexpr int BTC_TILE = 128;
 #ifndef BTC_LD4
 #define BTC_LD4 1   // 0: one TMEM load (8 columns) + wait per output (A/B)
 #endif
+#ifndef BTC_COMB
+#define BTC_COMB 1  // 0: byte planes combined with 64-bit multiply-adds (A/B)
+#endif
 template <int NIN, bool CORR>
 __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restrict__ in, i64 in_stride, LimbMap im,
                                                            const u64* __restrict__ vfac, const u64* __restrict__ vfac_sh,
@@ -1999,12 +2002,31 @@ __global__ void __launch_bounds__(BTC_TILE) bconv_tc_kernel(const u64* __restric
         u64* o = out + (size_t)p * out_stride + k0 + tid;
         const uint32_t tl = tbase + ((uint32_t)(warp * 32) << 16);
         auto finish = [&](int t, const uint32_t* d) {
+#if BTC_COMB
+            // T = sum_b d_b 2^{8b} (d_b < 2^22, T < 2^79) in 32-bit words with shift-adds and carries (ALU pipe), not
+            // 64-bit multiply-adds by 2^{8b} (the compiler's IMAD.WIDE on the fmaheavy pipe that bounds this kernel)
+            uint32_t w0, w1, w2;
+            // byte shifts as PRMT (the shift-adds would be re-fused into IMAD by ptxas)
+            asm("{\n\t.reg .u32 A, B, C, D, t, lh, hl, hh;\n\t"
+                "prmt.b32 t, %4, 0, 0x2104;\n\tadd.u32 A, %3, t;\n\t"
+                "prmt.b32 t, %6, 0, 0x2104;\n\tadd.u32 B, %5, t;\n\t"
+                "prmt.b32 t, %8, 0, 0x2104;\n\tadd.u32 C, %7, t;\n\t"
+                "prmt.b32 t, %10, 0, 0x2104;\n\tadd.u32 D, %9, t;\n\t"
+                "prmt.b32 t, B, 0, 0x1044;\n\tadd.cc.u32 %0, A, t;\n\tprmt.b32 t, B, 0, 0x4432;\n\taddc.u32 lh, t, 0;\n\t"
+                "prmt.b32 t, D, 0, 0x1044;\n\tadd.cc.u32 hl, C, t;\n\tprmt.b32 t, D, 0, 0x4432;\n\taddc.u32 hh, t, 0;\n\t"
+                "add.cc.u32 %1, lh, hl;\n\taddc.u32 %2, hh, 0;\n\t}"
+                : "=r"(w0), "=r"(w1), "=r"(w2)
+                : "r"(d[0]), "r"(d[1]), "r"(d[2]), "r"(d[3]), "r"(d[4]), "r"(d[5]), "r"(d[6]), "r"(d[7]));
+            U128 T{((u64)w1 << 32) | w0, (u64)w2};
+            if (CORR) add128(T, r * scr[t]);   // r <= NIN <= 8 roundings, scr < 2^61: the product fits 64 bits
+#else
             const u64 lo4 = (u64)d[0] + ((u64)d[1] << 8) + ((u64)d[2] << 16) + ((u64)d[3] << 24);
             const u64 hi4 = (u64)d[4] + ((u64)d[5] << 8) + ((u64)d[6] << 16) + ((u64)d[7] << 24);
             U128 T{lo4, 0};
             add128(T, hi4 << 32);
             T.hi += hi4 >> 32;
             if (CORR) mac128(T, r, scr[t]);
+#endif
             o[spos[t]] = redc128(T, sq[t], sqi[t]);
         };
         int t = 0;
