@@ -459,8 +459,9 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                                                                              const u64* __restrict__ w, int units, i64 wus,
                                                                              u64* __restrict__ acc, i64 accs, int level, int N,
                                                                              const ModConst* __restrict__ mod, int limb0,
-                                                                             int nstages) {
+                                                                             int nstages, int fp_split) {
     extern __shared__ __align__(128) u64 dm_sm[];
+    const bool fpw = NARROW && fp_split && (threadIdx.x >> 5) >= 4;   // warp-uniform: FP64-pipe warps (narrow limbs)
     constexpr int SW = MAC_LANES * ROWS * MAC_T;                 // words per stage
     u64* stg = dm_sm;                                            // [nstages][16 lanes][8 rows][32 coefficients]
     u64* sb = stg + (size_t)nstages * SW;            // bank tile, layout of diag_mac_kernel
@@ -534,7 +535,38 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
                     h10 += (u64)rr.x * ah; l10 += (u64)rr.y * al; s10 += (u64)(rr.x + rr.y) * as;
                     h11 += (u64)rr.z * bh; l11 += (u64)rr.w * bl; s11 += (u64)(rr.z + rr.w) * bsum;
                 };
-                if (rows == ROWS) {    // full chunk: no per-row guard in the unrolled body
+                // FP64-pipe copy of the same split products (warps 4-7 when fp_split): pieces < 2^21 + 2^20, products
+                // < 2^44, sums of <= 512 products < 2^53 -- exact in doubles, kept in the bits of the same u64 accumulators
+                // and converted back before kara_combine, so the words are identical; each SM sub-partition runs one
+                // integer-pipe and one FP64-pipe warp of the CTA
+                auto row_fp = [&](int t) {
+                    auto cvd = [](uint32_t v) -> double {
+                        return __dsub_rn(__hiloint2double(0x43300000, (int)v), 4503599627370496.0);
+                    };
+                    auto acc = [](u64& a, double x, double y) {
+                        a = (u64)__double_as_longlong(__fma_rn(x, y, __longlong_as_double((long long)a)));
+                    };
+                    const ulonglong2 x = xr[t * (MAC_T / 2)];
+                    const double ah = cvd((uint32_t)(x.x >> 20)), al = cvd((uint32_t)(x.x & 0xFFFFF));
+                    const double bh = cvd((uint32_t)(x.y >> 20)), bl = cvd((uint32_t)(x.y & 0xFFFFF));
+                    const double as = __dadd_rn(ah, al), bsum = __dadd_rn(bh, bl);
+                    const uint4 pp = sb8[(t * 2 + 0) * (MAC_T / 2)];
+                    const uint4 rr = sb8[(t * 2 + 1) * (MAC_T / 2)];
+                    const double p0 = cvd(pp.x), p1 = cvd(pp.y), p2 = cvd(pp.z), p3 = cvd(pp.w);
+                    const double r0 = cvd(rr.x), r1 = cvd(rr.y), r2 = cvd(rr.z), r3 = cvd(rr.w);
+                    acc(h00, p0, ah); acc(l00, p1, al); acc(s00, __dadd_rn(p0, p1), as);
+                    acc(h01, p2, bh); acc(l01, p3, bl); acc(s01, __dadd_rn(p2, p3), bsum);
+                    acc(h10, r0, ah); acc(l10, r1, al); acc(s10, __dadd_rn(r0, r1), as);
+                    acc(h11, r2, bh); acc(l11, r3, bl); acc(s11, __dadd_rn(r2, r3), bsum);
+                };
+                if (fpw) {
+                    if (rows == ROWS) {
+#pragma unroll
+                        for (int t = 0; t < ROWS; t++) row_fp(t);
+                    } else {
+                        for (int t = 0; t < rows; t++) row_fp(t);
+                    }
+                } else if (rows == ROWS) {    // full chunk: no per-row guard in the unrolled body
 #pragma unroll
                     for (int t = 0; t < ROWS; t++) row(t);
                 } else {
@@ -593,6 +625,10 @@ __global__ void __launch_bounds__(MAC_TPR * MAC_LANES, MINB) diag_mac_tma_kernel
             if (c == nch - 1) {
                 u64* o = acc + (size_t)u * accs + (size_t)limb * N + k0 + 2 * kp;
                 if constexpr (NARROW) {
+                    if (fpw) {   // the FP64 warps' sums are exact integers < 2^53 held as double bits
+                        auto cv = [](u64& a) { a = (u64)__double2ull_rn(__longlong_as_double((long long)a)); };
+                        cv(h00); cv(l00); cv(s00); cv(h01); cv(l01); cv(s01); cv(h10); cv(l10); cv(s10); cv(h11); cv(l11); cv(s11);
+                    }
                     *(ulonglong2*)o = make_ulonglong2(kara_combine(h00, l00, s00, mc.q, mc.rhi, mc.rlo, t40),
                                                       kara_combine(h01, l01, s01, mc.q, mc.rhi, mc.rlo, t40));
                     *(ulonglong2*)(o + cs) = make_ulonglong2(kara_combine(h10, l10, s10, mc.q, mc.rhi, mc.rlo, t40),
@@ -949,10 +985,13 @@ void k_diag_mac(encf_ctx& c, const u64* bank, int nbank, const u64* w, int units
         auto launch = [&](auto kw, auto kn) {
             if (nw > 0)
                 kw<<<dim3(tiles, nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level, c.N,
-                                                                       c.d_mod, 0, nst);
+                                                                       c.d_mod, 0, nst, 0);
+            // narrow limbs: warps 4-7 on the FP64 pipe (exact while nbank <= 512; ENCF_MAC_FP=0: integer pipe only)
+            static const int fp_env = [] { const char* e = std::getenv("ENCF_MAC_FP"); return e ? std::atoi(e) : 1; }();
+            const int fp_split = fp_env && nbank <= 512 ? 1 : 0;
             if (nw < level)
                 kn<<<dim3(tiles, level - nw, zs), MAC_TPR * MAC_LANES, tsm, s>>>(tm, bank, nbank, w, units, wus, acc, accs, level,
-                                                                               c.N, c.d_mod, nw, nst);
+                                                                               c.N, c.d_mod, nw, nst, fp_split);
         };
         if (variant == 1) launch(diag_mac_tma_kernel<false, 8, 1>, diag_mac_tma_kernel<true, 8, 1>);
         else if (variant == 2) launch(diag_mac_tma_kernel<false, 8, 2>, diag_mac_tma_kernel<true, 8, 2>);

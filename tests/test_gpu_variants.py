@@ -13,6 +13,7 @@ tests in a fresh interpreter with its environment:
                        window transforms)
   ENCF_BCAST_DIRECT=1  the value kernel's direct sliding-window MAC instead of the 128-point window convolution
   ENCF_PROJ_GROUP=0    projection giant steps as separate ext rotations + lifts + block sums (not one grouped launch)
+  ENCF_MAC_FP=0        plaintext MAC on the integer pipe only (no FP64-pipe warps)
 """
 import os
 import subprocess
@@ -34,7 +35,7 @@ VARIANTS = [
     {"ENCF_BCONV_TC": "0"},
     {"ENCF_KS_TMA": "0"},
     {"ENCF_KS_TMA_T": "256", "ENCF_PSI_TILE": "1024", "ENCF_ROTSUM_TMA": "1"},
-    {"ENCF_MAC_VARIANT": "reg"},
+    {"ENCF_MAC_VARIANT": "reg", "ENCF_MAC_FP": "0"},
     {"ENCF_MAC_VARIANT": "tma1"},
     {"ENCF_MAC_VARIANT": "tma3"},
     {"ENCF_NTT_FUSED": "1"},
