@@ -35,8 +35,8 @@ VARIANTS = [
     {"ENCF_BCONV_TC": "0"},
     {"ENCF_KS_TMA": "0"},
     {"ENCF_KS_TMA_T": "256", "ENCF_PSI_TILE": "1024", "ENCF_ROTSUM_TMA": "1"},
-    {"ENCF_MAC_VARIANT": "reg", "ENCF_MAC_FP": "0"},
-    {"ENCF_MAC_VARIANT": "tma1"},
+    {"ENCF_MAC_VARIANT": "reg"},
+    {"ENCF_MAC_VARIANT": "tma1", "ENCF_MAC_FP": "0"},
     {"ENCF_MAC_VARIANT": "tma3"},
     {"ENCF_NTT_FUSED": "1"},
     {"ENCF_NTT_INT_ONLY": "1"},
