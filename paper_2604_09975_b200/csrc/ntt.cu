@@ -805,7 +805,9 @@ bool fused_launch(encf_ctx& c, const NttArgs& a, const PolyBatch& b, bool inv, c
 bool ntt_fused(encf_ctx& c, const NttArgs& a, const PolyBatch& b, bool inv, cudaStream_t s) {
     // default OFF: measured on the B200 the fused launch made the layer's NTT time 25.0 -> 29.4 ms (profiles/r02_summary.md)
     static const bool on = [] { const char* e = std::getenv("ENCF_NTT_FUSED"); return e && std::atoi(e) != 0; }();
-    if (!on) return false;
+    // small batches (under one wave: <= ENCF_NTT_FUSED_SMALL limb transforms): one launch instead of two (A/B knob)
+    static const int small = [] { const char* e = std::getenv("ENCF_NTT_FUSED_SMALL"); return e ? std::atoi(e) : 0; }();
+    if (!on && !(small > 0 && b.npolys * b.map.n <= small)) return false;
     switch (c.logN) {
         case 12: return fused_launch<6, 6>(c, a, b, inv, s);
         case 13: return fused_launch<6, 7>(c, a, b, inv, s);
