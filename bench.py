@@ -42,10 +42,10 @@ C_QK, BETA = 192, 16
 MODELS = {"layer": dict(name="bert-base-layer", d=768, H=12, dff=3072),
           "qkv": dict(name="bert-base-qkv", d=768, H=12, dff=3072),
           "bert-large-layer": dict(name="bert-large-layer", d=1024, H=16, dff=4096)}
-NTT_TRAFFIC = 1.863e6  # ncu dram__bytes (read + write) per limb transform (fwd cols+rows, 384-limb batch)
-NTT_TRAFFIC_SRC = "profiles/r02_ncu_top_kernels.md (ncu --set full, 384-limb forward batch: (344.0 + 371.3) MB / 384)"
-DIAG_MAC_TRAFFIC_SRC = ("profiles/r02_ncu_top_kernels.md (ncu --set full of the QKV launches: narrow 21142.7 + 646.5 MB, "
-                        "128-bit 3020.9 + 93.2 MB)")
+NTT_TRAFFIC = 1.873e6  # ncu dram__bytes (read + write) per limb transform (fwd cols+rows, 384-limb batch)
+NTT_TRAFFIC_SRC = "profiles/r02s4_ncu_top_kernels.md (ncu --set full, 384-limb forward batch: (348.4 + 371.0) MB / 384)"
+DIAG_MAC_TRAFFIC_SRC = ("profiles/r02s4_ncu_top_kernels.md (ncu --set full of the QKV launches: narrow 21142.9 + 647.0 MB) and "
+                        "profiles/r02_ncu_top_kernels.md (128-bit 3020.9 + 93.2 MB)")
 
 
 def parse():
