@@ -2148,20 +2148,23 @@ __global__ void gather_copy2_kernel(CopyBatch C, u64* dst, i64 dst_stride, size_
 }
 
 __global__ void rescale_prep_batch_kernel(const u64* last, u64* corr, int level, int N, const ModConst* mod, const u64* hmod) {
+    // corr[p][i][k] = ((last[p][k] + floor(q_{L-1}/2)) mod q_{L-1}) mod q_i - floor(q_{L-1}/2) mod q_i, i < L - 1.  A thread
+    // owns two coefficients of one polynomial and writes every target limb: the last limb is read once (was once per
+    // target limb), and l mod q_i is l itself when l < q_i (the 60-bit q_0) -- Barrett otherwise
     const int p = blockIdx.y;
     const int nl = level - 1;
     const u64* lp_in = last + (size_t)p * N;
     u64* cr = corr + (size_t)p * nl * N;
-    u64 qL = mod[level - 1].q, h = qL / 2;
-    const size_t pairs = (size_t)nl * N / 2;   // two coefficients per thread, 128-bit accesses
-    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < pairs; i += (size_t)gridDim.x * blockDim.x) {
-        const int limb = (int)(2 * i / N), k = (int)(2 * i % N);
-        const ModConst mc = mod[limb];
+    const u64 qL = mod[level - 1].q, h = qL / 2;
+    for (int k = 2 * (blockIdx.x * blockDim.x + threadIdx.x); k < N; k += 2 * gridDim.x * blockDim.x) {
         const ulonglong2 x = __ldg((const ulonglong2*)(lp_in + k));
         const u64 l0 = add_mod(x.x, h, qL), l1 = add_mod(x.y, h, qL);
-        // l mod q_i by Barrett (the 64-bit % was a software division per word)
-        const u64 r0 = barrett128(U128{l0, 0}, mc.q, mc.rhi, mc.rlo), r1 = barrett128(U128{l1, 0}, mc.q, mc.rhi, mc.rlo);
-        ((ulonglong2*)cr)[i] = make_ulonglong2(sub_mod(r0, hmod[limb], mc.q), sub_mod(r1, hmod[limb], mc.q));
+        for (int limb = 0; limb < nl; limb++) {
+            const ModConst mc = mod[limb];
+            const u64 r0 = l0 < mc.q ? l0 : barrett128(U128{l0, 0}, mc.q, mc.rhi, mc.rlo);
+            const u64 r1 = l1 < mc.q ? l1 : barrett128(U128{l1, 0}, mc.q, mc.rhi, mc.rlo);
+            *(ulonglong2*)(cr + (size_t)limb * N + k) = make_ulonglong2(sub_mod(r0, hmod[limb], mc.q), sub_mod(r1, hmod[limb], mc.q));
+        }
     }
 }
 
@@ -2460,7 +2463,7 @@ void k_gather_copy(encf_ctx& c, const CopyBatch& C, int n, u64* dst, i64 dst_str
 }
 
 void k_rescale_prep_batch(encf_ctx& c, const u64* last, u64* corr, int level, int npolys, cudaStream_t s) {
-    dim3 grid(nblocks((size_t)(level - 1) * c.N / 2, TB, 256), npolys);
+    dim3 grid(nblocks((size_t)c.N / 2, TB, 256), npolys);
     { int _slot; c.prof_begin("rescale_prep_batch_kernel", s, 0, _slot);
     rescale_prep_batch_kernel<<<grid, TB, 0, s>>>(last, corr, level, c.N, c.d_mod, c.rescale[level].d_hmod);
     c.prof_end(_slot, s); }
