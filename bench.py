@@ -282,7 +282,8 @@ class Layer:
             t[1:].add_(self.MASK_EPOCH)
 
     def _complex_pairs(self, ys):
-        out = [self.ctx.complexify(ys[2 * i], ys[2 * i + 1]) for i in range(len(ys) // 2)]
+        h = len(ys) // 2
+        out = self.ctx.complexify_many(ys[0:2 * h:2], ys[1:2 * h:2]) if h else []
         if len(ys) % 2:
             out.append(ys[-1])
         return out

@@ -165,6 +165,11 @@ encf_status encf_rescale(encf_ctx* ctx, const encf_ct* in, encf_ct* out, void* s
 encf_status encf_mod_drop(encf_ctx* ctx, const encf_ct* in, int32_t n_limbs, encf_ct* out, void* stream);
 /* Boundary wrapper: re + i im. */
 encf_status encf_complexify(encf_ctx* ctx, const encf_ct* re, const encf_ct* im, encf_ct* out, void* stream);
+/* Batched encf_complexify: out[i] = re[i] + i im[i] (X^{N/2} im[i]) for n pairs (host arrays of n), every input at one
+ * level and component count, in ceil(n / 32) launches; the same words as n encf_complexify calls.  Errors: ARG,
+ * LEVEL_MISMATCH, SCALE_MISMATCH. */
+encf_status encf_complexify_many(encf_ctx* ctx, const encf_ct* re /*host array of n*/, const encf_ct* im /*host array of n*/,
+                                 int32_t n, encf_ct* out /*host array of n*/, void* stream);
 
 /* Mask plaintexts (Alg A.2 H/U, App. A.3 e_s / n_u, export ranges): ones on rows [r0,r1) of segments
  * s0 + k*sstride (k < scount) of an m-row segment grid, encoded at scale q_{L-1} at level L.

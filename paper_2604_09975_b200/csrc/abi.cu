@@ -451,6 +451,25 @@ encf_status encf_complexify(encf_ctx* c, const encf_ct* re, const encf_ct* im, e
     });
 }
 
+encf_status encf_complexify_many(encf_ctx* c, const encf_ct* re, const encf_ct* im, int32_t n, encf_ct* out, void* stream) {
+    return guard([&] {
+        EV_BEGIN(nullptr);
+        need(re != nullptr && im != nullptr && out != nullptr && n >= 1, ENCF_ERR_ARG, "complexify_many: n >= 1 pairs");
+        std::vector<DCt> a, b, o;
+        for (int i = 0; i < n; i++) { a.push_back(view(c, &re[i])); b.push_back(view(c, &im[i])); }
+        std::vector<const DCt*> ap, bp;
+        for (int i = 0; i < n; i++) {
+            need(a[i].L == a[0].L && b[i].L == a[0].L && a[i].ncomp == a[0].ncomp && b[i].ncomp == a[0].ncomp,
+                 ENCF_ERR_LEVEL_MISMATCH, "complexify_many: every re/im at one level and component count");
+            ap.push_back(&a[i]);
+            bp.push_back(&b[i]);
+            o.push_back(outview(&out[i], a[i].L, a[i].ncomp));
+        }
+        ev.add_i_many(ap, bp, o);   // re + X^{N/2} im, batched (the words of encf_complexify)
+        for (int i = 0; i < n; i++) writeback(&out[i], o[i]);
+    });
+}
+
 encf_status encf_mask_put(encf_ctx* c, const encf_mask_desc* d, const uint64_t* coeffs) {
     return guard([&] {
         need(c && d && coeffs, ENCF_ERR_ARG, "mask_put: null argument");

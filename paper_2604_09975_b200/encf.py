@@ -73,6 +73,7 @@ _SIG = {
     "encf_rescale": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
     "encf_mod_drop": [_p, ctypes.POINTER(CT), _i32, ctypes.POINTER(CT), _p],
     "encf_complexify": [_p, ctypes.POINTER(CT), ctypes.POINTER(CT), ctypes.POINTER(CT), _p],
+    "encf_complexify_many": [_p, _p, _p, _i32, _p, _p],
     "encf_mask_put": [_p, ctypes.POINTER(MaskDesc), _p],
     "encf_mask_clear": [_p],
     "encf_proj_plan_create": [_p, _i32, _i32, _i32, _i32, _i32, _u32, ctypes.POINTER(_p)],
@@ -417,6 +418,17 @@ class Context:
         c = out._c()
         _chk(_lib.encf_complexify(self.h, ctypes.byref(re._c()), ctypes.byref(im._c()), ctypes.byref(c), _stream()), "complexify")
         return out._update(c)
+
+    def complexify_many(self, res, ims):
+        """[re + i im for (re, im) in zip(res, ims)] in batched launches (encf_complexify_many)."""
+        n = len(res)
+        a = (CT * n)(*[x._c() for x in res])
+        b = (CT * n)(*[x._c() for x in ims])
+        outs_py = [self.empty_ct(x.n_limbs, x.n_comp) for x in res]
+        outs = (CT * n)(*[o._c() for o in outs_py])
+        _chk(_lib.encf_complexify_many(self.h, ctypes.cast(a, _p), ctypes.cast(b, _p), n, ctypes.cast(outs, _p), _stream()),
+             "complexify_many")
+        return [o._update(outs[i]) for i, o in enumerate(outs_py)]
 
     def mask_put(self, desc, m, level, coeffs, ext=False):
         r0, r1, s0, ss, sc = desc

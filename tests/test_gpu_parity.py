@@ -169,6 +169,9 @@ def test_tensor_relin_rescale_bit_exact(c13, keys13):
     assert_ct_equal(c13, c13.add(da, db), O.add(P13, a, b), "add")
     assert_ct_equal(c13, c13.add(da, db, sub=True), O.sub(P13, a, b), "sub")
     assert_ct_equal(c13, c13.complexify(da, db), O.complexify(P13, a, b), "complexify")
+    many = c13.complexify_many([da, db, da], [db, da, da])      # batched (encf_complexify_many)
+    for got, (x, y) in zip(many, [(a, b), (b, a), (a, a)]):
+        assert_ct_equal(c13, got, O.complexify(P13, x, y), "complexify_many")
 
 
 def test_keyswitch_P16_top_level(c16):
