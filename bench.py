@@ -82,8 +82,14 @@ class Clocks:
                                           "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~1 s to start sampling: wait for its first row so that the (~1 s) timed region is sampled,
+            # and keep only the rows taken from here on
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10 and self.proc.poll() is None:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
+        self.start = len(self.rows)
         return self
 
     def _read(self):
@@ -92,6 +98,9 @@ class Clocks:
 
     def __exit__(self, *a):
         if self.proc:
+            t0 = time.time()
+            while len(self.rows) <= self.start and time.time() - t0 < 0.5:   # at least one row inside the region
+                time.sleep(0.01)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
@@ -99,8 +108,10 @@ class Clocks:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows[getattr(self, "start", 0):]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.rows = rows
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
