@@ -472,7 +472,6 @@ void Ev::hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<
         c1.push_back(ins[i]->comp(1, N));
     }
     u64* ext = modup_many(c1, {}, L);
-    const size_t Lw = (size_t)L * N;
     struct R { const u64* ext; const u64* key; uint32_t g; u64* out; const u64* c0; };
     std::vector<R> rq;
     for (int i = 0; i < n; i++)
@@ -486,7 +485,6 @@ void Ev::hoisted_many_ext(const std::vector<const DCt*>& ins, const std::vector<
     LimbMap klm;
     klm.n = nl;
     for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
-    (void)Lw;
     for (int r0 = 0; r0 < m; r0 += KS_BATCH) {
         const int cnt = std::min(KS_BATCH, m - r0);
         KsInnerBatch B;
@@ -605,12 +603,10 @@ void Ev::rotate_many_ext(const std::vector<const DCt*>& ins, const std::vector<u
         c1.push_back(ins[i]->comp(1, N));
     }
     u64* ext = modup_many(c1, gs, L);                 // ModUp of sigma_g(c1): the gather is fused into the copy
-    const size_t Lw = (size_t)L * N;
     const int ML = keys->max_level, key_nl = ML + K;
     LimbMap klm;
     klm.n = nl;
     for (int e2 = 0; e2 < nl; e2++) klm.mod[e2] = (unsigned char)(e2 < L ? e2 : ML + (e2 - L));
-    (void)Lw;
     for (int r0 = 0; r0 < n; r0 += KS_BATCH) {
         const int cnt = std::min(KS_BATCH, n - r0);
         KsInnerBatch B;
