@@ -67,14 +67,44 @@ def parse():
 
 # ------------------------------------------------------------------------------------ clocks
 class Clocks:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampling DURING the timed region (B200_PROFILING.md clocks line): NVML every 50 ms,
+    nvidia-smi -lms 200 when NVML is unavailable."""
 
     def __init__(self, index=0):
         self.index = index
         self.rows = []
         self.proc = None
+        self.nvml = False
+
+    def _nvml_loop(self):
+        import pynvml as nv
+        h = nv.nvmlDeviceGetHandleByIndex(self.index)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        while not self.stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append([str(self.index), str(sm), str(mx), "", hex(rs)] +
+                                 ["Active" if rs & b else "Not Active" for b in bits])
+            except Exception:
+                pass
+            time.sleep(0.05)
 
     def __enter__(self):
+        # NVML in a thread, every 50 ms (the nvidia-smi -lms loop takes ~1 s to start and may miss a ~1 s region)
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.stop = False
+            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self.t.start()
+            self.nvml = True
+            self.start = 0
+            return self
+        except Exception:
+            self.nvml = False
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
@@ -97,6 +127,10 @@ class Clocks:
             self.rows.append([x.strip() for x in line.split(",")])
 
     def __exit__(self, *a):
+        if getattr(self, "nvml", False):
+            self.stop = True
+            self.t.join(timeout=1)
+            return
         if self.proc:
             t0 = time.time()
             while len(self.rows) <= self.start and time.time() - t0 < 0.5:   # at least one row inside the region
